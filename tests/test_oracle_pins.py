@@ -1,0 +1,390 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix.
+
+Each test names the PAPER.md passage (P:L<n>) or the textbook fact it relies
+on.  None of them re-types the oracle's own formula: they use printed values
+(tests/golden/), closed forms, brute force on tiny inputs, special cases that
+reduce to a library routine, and invariants.
+"""
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import oracle as O
+from synth import gen_points, gen_problem
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# --------------------------------------------------------------------------- kernel
+def test_fig32_eigenvalue_count_pins_gaussian_convention():
+    """243 eigenvalues of (K + mu I) above 1.1 mu for n=1000, edge 10, l=5.
+
+    Pins exp(-r^2/l^2) (no factor 1/2) and the uniform-cube domain: the
+    exp(-r^2/(2 l^2)) convention gives far fewer."""
+    g = gold("fig32_eigcount.json")
+    lo, hi = g["band"]
+    counts, half = [], []
+    for s in g["seeds"]:
+        X, _ = gen_points(g["n"], 3, "cube", s, g["edge"])
+        K = O.kernel_block(X, X, g["l"])
+        ev = np.linalg.eigvalsh(K + g["mu"] * np.eye(g["n"]))
+        counts.append(int(np.count_nonzero(ev > g["factor"] * g["mu"])))
+        if s == 0:
+            Kh = O.kernel_block(X, X, g["l"] * math.sqrt(2.0))  # = exp(-r^2/(2 l^2))
+            evh = np.linalg.eigvalsh(Kh + g["mu"] * np.eye(g["n"]))
+            half.append(int(np.count_nonzero(evh > g["factor"] * g["mu"])))
+    assert all(lo <= c <= hi for c in counts), counts
+    assert abs(np.mean(counts) - g["paper_count"]) <= 6
+    assert half[0] < g["half_convention_must_be_below"]
+
+
+def test_kernel_closed_forms():
+    """K(x,x)=1, K=e^-1 at distance l; rescaling K(X;l)=K(X/l;1)."""
+    g = gold("gaussian_closed_forms.json")
+    for l in (0.3, 1.0, 7.0):
+        A = np.array([[0.0, 0.0, 0.0]])
+        B = np.array([[0.0, 0.0, 0.0], [l, 0.0, 0.0]])
+        K = O.kernel_block(A, B, l)
+        assert K[0, 0] == 1.0
+        assert abs(K[0, 1] - g["exp_minus_one"]) <= 2e-16
+    X, _ = gen_points(60, 3, "cube", 3)
+    for l in (0.5, 2.0, 4.0):
+        K1 = O.kernel_block(X, X, l)
+        K2 = O.kernel_block(X / l, X / l, 1.0)
+        assert np.max(np.abs(K1 - K2)) <= 1e-13
+    Kt = O.kernel_block(X, X, 1e-6)
+    assert np.array_equal(Kt, np.eye(60))
+    Kw = O.kernel_block(X, X, 1e6)
+    assert np.max(np.abs(Kw - 1.0)) <= 1e-9
+
+
+def test_kmv_lattice_poisson_sum():
+    """Interior row of K*1 on the 1-D integer lattice equals the theta sum
+    sum_m exp(-m^2/l^2) = l sqrt(pi)(1 + 2 sum exp(-pi^2 l^2 m^2))."""
+    g = gold("gaussian_closed_forms.json")
+    X = np.arange(401, dtype=np.float64)[:, None]
+    v = np.ones(401)
+    for ls, ref in g["lattice_row_sums"].items():
+        y = O.kmv(X, float(ls), 0.0, v)
+        assert abs(y[200] - ref) <= 4e-15 * ref, (ls, y[200], ref)
+
+
+def test_kmv_identities():
+    """(K + mu I)v: adjoint symmetry, v=0, l->0 gives (1+mu)v, l->inf gives sum(v)+mu v."""
+    X, _ = gen_points(300, 3, "cube", 1)
+    rng = np.random.default_rng(5)
+    u, v = rng.standard_normal(300), rng.standard_normal(300)
+    mu = 1e-3
+    Ku = O.kmv(X, 1.3, mu, u, block=64)
+    Kv = O.kmv(X, 1.3, mu, v, block=37)
+    assert abs(u @ Kv - Ku @ v) <= 1e-12 * np.linalg.norm(Ku) * np.linalg.norm(v)
+    assert np.array_equal(O.kmv(X, 1.3, mu, np.zeros(300)), np.zeros(300))
+    assert np.allclose(O.kmv(X, 1e-6, mu, v), (1 + mu) * v, rtol=0, atol=1e-15)
+    assert np.allclose(O.kmv(X, 1e7, mu, v), v.sum() + mu * v, rtol=1e-9, atol=1e-9)
+    # threaded row blocks give the same rows
+    assert np.array_equal(O.kmv(X, 1.3, mu, v, block=64, threads=4), O.kmv(X, 1.3, mu, v, block=64))
+    # single column e_j against the two-point closed form exp(-d^2/l^2) via math.exp
+    j = 17
+    e = np.zeros(300)
+    e[j] = 1.0
+    col = O.kmv(X, 1.3, 0.0, e)
+    for i in (0, 5, 299):
+        dd = sum((X[i, c] - X[j, c]) ** 2 for c in range(3))
+        assert abs(col[i] - math.exp(-dd / 1.69)) <= 4e-16
+
+
+# --------------------------------------------------------------------------- FPS
+def test_fps_golden_small():
+    for case in gold("fps_knn_small.json")["fps"]:
+        X = np.array(case["points_1d"])[:, None]
+        idx, _ = O.fps(X, case["k"], case["seed"])
+        assert idx.tolist() == case["expect_idx"], case["citation"]
+
+
+def test_fps_trace_and_nesting():
+    """fill_trace[i] = h_{X_{i+1}} computed independently; non-increasing;
+    nested selections X_{k-1} subset of X_k."""
+    X, _ = gen_points(400, 2, "cube", 7, 10.0)
+    idx, fill = O.fps(X, 40, 3)
+    assert idx[0] == 3 and len(set(idx.tolist())) == 40
+    for i in (0, 1, 5, 20, 39):
+        assert fill[i] == pytest.approx(O.fill_distance(X, idx[: i + 1]), rel=0, abs=1e-12)
+    assert np.all(np.diff(fill) <= 0)
+    idx2, _ = O.fps(X, 25, 3)
+    assert np.array_equal(idx2, idx[:25])
+    ia, fa = O.fps(X, 400, 3)
+    assert sorted(ia.tolist()) == list(range(400)) and fa[-1] == 0.0
+
+
+def test_fps_theorem_3_3_bruteforce():
+    """Thm 3.3: h <= q, q >= q*/2, h <= 2 h* against brute force optima."""
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        n = 9
+        X = rng.uniform(0, 1, size=(n, 2))
+        for k in (2, 3, 4):
+            idx, _ = O.fps(X, k, trial % n)
+            h = O.fill_distance(X, idx)
+            q = O.separation_distance(X, idx)
+            hstar = min(O.fill_distance(X, list(c)) for c in itertools.combinations(range(n), k))
+            qstar = max(O.separation_distance(X, list(c)) for c in itertools.combinations(range(n), k))
+            assert h <= q + 1e-12
+            assert q >= qstar / 2 - 1e-12
+            assert h <= 2 * hstar + 1e-12
+
+
+def test_fps_duplicates_never_repicked():
+    X = np.repeat(np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 3.0]]), 3, axis=0)
+    idx, fill = O.fps(X, 9, 0)
+    assert sorted(idx.tolist()) == list(range(9))
+    assert fill[2] == 0.0 and fill[-1] == 0.0
+
+
+# --------------------------------------------------------------------------- kNN
+def test_knn_golden_small():
+    for case in gold("fps_knn_small.json")["knn"]:
+        P = np.array(case["points_1d"])[:, None]
+        rp, col = O.knn_lower(P, case["w"])
+        rows = [col[rp[i]:rp[i + 1]].tolist() for i in range(len(P))]
+        assert rows == case["expect_rows"], case["citation"]
+
+
+def test_knn_sorted_line_closed_form():
+    """Increasing 1-D points: the w-1 nearest earlier points are the w-1 preceding."""
+    rng = np.random.default_rng(2)
+    P = np.cumsum(rng.uniform(0.1, 1.0, 120))[:, None]
+    for w in (1, 2, 7, 50):
+        rp, col = O.knn_lower(P, w)
+        for i in range(120):
+            assert col[rp[i]:rp[i + 1]].tolist() == list(range(max(0, i - w + 1), i + 1))
+
+
+def test_knn_validity_2d():
+    """Every kept neighbour precedes every dropped earlier point in (d2, position)."""
+    P, _ = gen_points(150, 2, "cube", 4)
+    rp, col = O.knn_lower(P, 10)
+    for i in range(150):
+        row = col[rp[i]:rp[i + 1]]
+        assert row[-1] == i and np.all(np.diff(row) > 0) and len(row) == min(10, i + 1)
+        kept = set(row[:-1].tolist())
+        key = lambda j: (float(np.sum((P[j] - P[i]) ** 2)), j)  # noqa: E731
+        if kept and len(kept) < i:
+            worst_kept = max(key(j) for j in kept)
+            best_dropped = min(key(j) for j in range(i) if j not in kept)
+            assert worst_kept < best_dropped
+
+
+# --------------------------------------------------------------------------- Alg. 1
+def test_splitmix64_reference_vector():
+    g = gold("splitmix64.json")
+    gold_c = int(g["golden"], 16)
+    t = np.array([0, gold_c, (2 * gold_c) % 2**64], dtype=np.uint64)
+    out = [int(v) for v in O.splitmix64(t)]
+    assert out == [int(s, 16) for s in g["state0_outputs"]]
+
+
+def test_subsample_ids_distinct_and_deterministic():
+    ids = O.subsample_ids(10000, 300, 0)
+    assert len(set(ids.tolist())) == 300 and ids.min() >= 0 and ids.max() < 10000
+    assert np.array_equal(ids, O.subsample_ids(10000, 300, 0))
+    assert not np.array_equal(ids, O.subsample_ids(10000, 300, 1))
+    assert np.array_equal(O.subsample_ids(10000, 100, 0), ids[:100])
+
+
+def test_alg1_special_cases():
+    """P:L661-678 limits: l->inf gives K_m = 11^T (r=1); l->0 gives K_m = I (r=m)."""
+    X, _ = gen_points(1000, 3, "cube", 0)
+    big = O.alg1(X, 1e6, m=100)
+    assert big["r"] == 1 and big["refined"] and big["khat"] == 1
+    tiny = O.alg1(X, 1e-6, m=100)
+    assert tiny["r"] == 100 and tiny["refined"] and tiny["khat"] == 100
+    X5, _ = gen_points(5000, 3, "cube", 0)
+    t5 = O.alg1(X5, 1e-6, m=100)
+    assert t5["r"] == 100 and not t5["refined"] and t5["khat"] == 5000
+    # coarse branch floor: r = 1 already gives n/m >= 2000
+    Xb, _ = gen_points(200000, 3, "cube", 0)
+    bb = O.alg1(Xb, 1e6, m=100)
+    assert bb["r"] == 1 and not bb["refined"] and bb["khat"] == 2000
+
+
+def test_alg1_schur_errors_match_explicit_nystrom():
+    """errs[r-1] = ||K22 - K21 K11^{-1} K12||_2 / ||K_m||_2 for the FPS-ordered
+    subsample; error curve non-increasing (nested landmarks)."""
+    X, _ = gen_points(3000, 3, "cube", 9)
+    res = O.alg1(X, 2.0, m=120, err_tol=-1.0)  # never stops early: full curve
+    errs = res["errs"]
+    assert np.all(np.diff(errs) <= 1e-12)
+    Xm = X[res["ids"]] * res["scale"]
+    Km = O.kernel_block(Xm, Xm, 2.0)
+    order, _ = O.fps(Xm, len(Xm), 0)
+    Kp = Km[np.ix_(order, order)]
+    nk = np.linalg.norm(Km, 2)
+    for r in (1, 2, 5, 10, 20):
+        S = Kp[r:, r:] - Kp[r:, :r] @ np.linalg.solve(Kp[:r, :r], Kp[:r, r:])
+        assert abs(np.linalg.norm(S, 2) / nk - errs[r - 1]) <= 1e-9
+
+
+# --------------------------------------------------------------------------- FSAI
+def _lower_full_pattern(N):
+    rp = np.zeros(N + 1, dtype=np.int64)
+    col = []
+    for i in range(N):
+        col.extend(range(i + 1))
+        rp[i + 1] = rp[i] + i + 1
+    return rp, np.array(col, dtype=np.int64)
+
+
+def test_fsai_special_cases():
+    """S=I -> G=I; S=diag(d) -> diag(1/sqrt d); w=1 -> 1/sqrt(S_ii) (Kolotilina-Yeremin)."""
+    N = 12
+    rp, col = _lower_full_pattern(N)
+    v = O.fsai_rows(lambda J: np.eye(len(J)), rp, col)
+    G = np.zeros((N, N))
+    for i in range(N):
+        G[i, col[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+    assert np.allclose(G, np.eye(N), atol=1e-15)
+    dvec = np.linspace(0.5, 4.0, N)
+    v = O.fsai_rows(lambda J: np.diag(dvec[J]), rp, col)
+    G[:] = 0
+    for i in range(N):
+        G[i, col[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+    assert np.allclose(G, np.diag(1 / np.sqrt(dvec)), atol=1e-15)
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((N, N))
+    S = A @ A.T + N * np.eye(N)
+    rp1 = np.arange(N + 1, dtype=np.int64)
+    c1 = np.arange(N, dtype=np.int64)
+    v1 = O.fsai_rows(lambda J: S[np.ix_(J, J)], rp1, c1)
+    assert np.allclose(v1, 1 / np.sqrt(np.diag(S)), rtol=1e-15)
+
+
+def test_fsai_full_pattern_is_exact_inverse_factor():
+    """Full lower pattern: G^T G = S^{-1} (G = inverse Cholesky factor), and the
+    defining row property (G S)_{iJ} = e_i / G_ii on the pattern."""
+    rng = np.random.default_rng(1)
+    N = 30
+    A = rng.standard_normal((N, N))
+    S = A @ A.T + 0.5 * np.eye(N)
+    rp, col = _lower_full_pattern(N)
+    v = O.fsai_rows(lambda J: S[np.ix_(J, J)], rp, col)
+    G = np.zeros((N, N))
+    for i in range(N):
+        G[i, col[rp[i]:rp[i + 1]]] = v[rp[i]:rp[i + 1]]
+    Sinv = np.linalg.inv(S)
+    assert np.linalg.norm(G.T @ G - Sinv) <= 1e-8 * np.linalg.norm(Sinv)
+    Lc = np.linalg.cholesky(S)
+    assert np.allclose(G, np.linalg.inv(Lc), rtol=0, atol=1e-9 * np.abs(np.linalg.inv(Lc)).max())
+    GS = G @ S
+    for i in range(N):
+        J = col[rp[i]:rp[i + 1]]
+        e = np.zeros(len(J))
+        e[-1] = 1.0 / G[i, i]
+        assert np.max(np.abs(GS[i, J] - e)) <= 1e-10 * np.abs(S).max() * np.abs(G[i]).max()
+
+
+# --------------------------------------------------------------------------- AFN
+@pytest.fixture(scope="module")
+def small_afn():
+    X, b = gen_points(260, 3, "cube", 2, 6.0)
+    return X, O.build_afn(X, 1.0, 1e-3, 40, 12)
+
+
+def test_afn_apply_equals_dense_BBt_inverse(small_afn):
+    """apply_afn = (B B^T)^{-1} r with B of eq:factorized-form."""
+    X, B = small_afn
+    Bd = O.dense_B(B)
+    M = Bd @ Bd.T
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        r = rng.standard_normal(B["n"])
+        z = O.apply_afn(B, r)
+        zd = np.linalg.solve(M, r)
+        assert np.linalg.norm(z - zd) <= 1e-10 * np.linalg.norm(zd)
+    u, v = rng.standard_normal(B["n"]), rng.standard_normal(B["n"])
+    assert abs(O.apply_afn(B, u) @ v - u @ O.apply_afn(B, v)) <= 1e-10 * np.linalg.norm(O.apply_afn(B, u)) * np.linalg.norm(v)
+
+
+def test_afn_realM_blocks(small_afn):
+    """eq:realM: M = [[K11+mu I, K12], [K12^T, (G^T G)^{-1} + K12^T (K11+mu I)^{-1} K12]]."""
+    X, B = small_afn
+    k, l, mu = B["k"], B["l"], B["mu"]
+    Xp = B["Xp"]
+    Bd = O.dense_B(B)
+    M = Bd @ Bd.T
+    K = O.kernel_block(Xp, Xp, l) + mu * np.eye(B["n"])
+    assert np.max(np.abs(M[:k, :k] - K[:k, :k])) <= 1e-13
+    assert np.max(np.abs(M[:k, k:] - K[:k, k:])) <= 1e-12
+    Gd = B["G"].toarray()
+    M22 = np.linalg.inv(Gd.T @ Gd) + K[k:, :k] @ np.linalg.solve(K[:k, :k], K[:k, k:])
+    assert np.max(np.abs(M[k:, k:] - M22)) <= 1e-8 * np.abs(M22).max()
+
+
+def test_afn_exact_when_fsai_pattern_full():
+    """G^T G = S^{-1} exactly gives M = K + mu I; PCG then takes 1 iteration."""
+    X, b = gen_points(150, 3, "cube", 5, 5.0)
+    b = np.random.default_rng(1).standard_normal(150)
+    B = O.build_afn(X, 1.0, 1e-3, 30, 200)
+    Bd = O.dense_B(B)
+    K = O.kernel_block(B["Xp"], B["Xp"], 1.0) + 1e-3 * np.eye(150)
+    assert np.linalg.norm(Bd @ Bd.T - K) <= 1e-9 * np.linalg.norm(K)
+    a, rep, _ = O.afn_pcg_solve(X, b, 1.0, 1e-3, 30, 200, tol=1e-10, B=B)
+    assert rep["iterations"] <= 2
+    ad = np.linalg.solve(O.kernel_block(X, X, 1.0) + 1e-3 * np.eye(150), b)
+    assert np.linalg.norm(a - ad) <= 1e-8 * np.linalg.norm(ad)
+
+
+def test_afn_k_equals_n_is_exact_inverse():
+    X, _ = gen_points(80, 3, "cube", 6, 4.0)
+    B = O.build_afn(X, 1.0, 1e-2, 80, 10)
+    assert B["G"].shape == (0, 0)
+    r = np.random.default_rng(2).standard_normal(80)
+    K = O.kernel_block(B["Xp"], B["Xp"], 1.0) + 1e-2 * np.eye(80)
+    assert np.linalg.norm(O.apply_afn(B, r) - np.linalg.solve(K, r)) <= 1e-10 * np.linalg.norm(np.linalg.solve(K, r))
+
+
+# --------------------------------------------------------------------------- PCG
+def test_pcg_textbook_cases():
+    """A=I: 1 iteration; diag(1..10), b=1: <= 10 iterations (finite termination);
+    the A-norm of the error is non-increasing; agrees with LAPACK at tight tol."""
+    b = np.ones(10)
+    x, rep = O.pcg(lambda v: v.copy(), lambda r: r.copy(), b, tol=1e-12)
+    assert rep["iterations"] == 1 and np.allclose(x, b)
+    D = np.arange(1.0, 11.0)
+    x, rep = O.pcg(lambda v: D * v, lambda r: r.copy(), b, tol=1e-12)
+    assert rep["iterations"] <= 10 and np.allclose(x, 1 / D, atol=1e-12)
+    X, _ = gen_points(200, 3, "cube", 1, 5.0)
+    A = O.kernel_block(X, X, 0.7) + 1e-2 * np.eye(200)
+    bb = np.random.default_rng(0).standard_normal(200)
+    xs = np.linalg.solve(A, bb)
+    errs = []
+    for it in range(1, 40):
+        xi, _ = O.pcg(lambda v: A @ v, lambda r: r.copy(), bb, tol=1e-30, maxit=it, fixed_iters=it)
+        e = xi - xs
+        errs.append(float(e @ A @ e))
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-10) for i in range(len(errs) - 1))
+    x, rep = O.pcg(lambda v: A @ v, lambda r: r.copy(), bb, tol=1e-13, maxit=2000)
+    assert rep["converged"] and np.linalg.norm(x - xs) <= 1e-9 * np.linalg.norm(xs)
+    x0, rep0 = O.pcg(lambda v: A @ v, lambda r: r, np.zeros(200))
+    assert rep0["iterations"] == 0 and not x0.any()
+
+
+def test_c1_afn_pcg_end_to_end():
+    """Config C1 (BASELINE.json configs[0]): converges, true residual <= tol, and far
+    fewer iterations than unpreconditioned CG (the paper's premise)."""
+    X, b = gen_problem("C1")
+    a, rep, B = O.afn_pcg_solve(X, b, 1.0, 1e-4, 100, 50)
+    assert rep["converged"] and rep["relres_true"] <= 1.5e-4
+    _, rcg = O.cg_solve(X, b, 1.0, 1e-4)
+    assert rep["iterations"] * 5 < rcg["iterations"]
+    Kd = O.kernel_block(X, X, 1.0) + 1e-4 * np.eye(1000)
+    assert np.linalg.norm(Kd @ a - b) / np.linalg.norm(b) == pytest.approx(rep["relres_true"], rel=1e-6)
