@@ -1,0 +1,184 @@
+/*
+ * afn.h -- C ABI of the B200-native AFN-preconditioned CG hot path
+ * (Adaptive Factorized Nystrom, arXiv 2304.05460).
+ *
+ * Problem (eq:Problem / eq:gaussianf):
+ *     (K + mu I) a = b,   K_ij = exp(-||x_i - x_j||^2 / l^2)     (no factor 1/2)
+ * for n points x_i in R^d.  K is never formed.
+ *
+ * Conventions for every entry point
+ *   - fp64 everywhere.  X is n x d row-major (x_i = X[i*d .. i*d+d-1]).
+ *   - Array pointers are DEVICE pointers on the current CUDA device unless the
+ *     argument is marked [host].  The caller owns every array it passes; the
+ *     library never frees caller memory.  `stream` is a cudaStream_t passed as
+ *     void* (NULL = legacy default stream).
+ *   - Entry points are stream-ordered unless marked [sync]; [sync] entry points
+ *     synchronise `stream` before returning because they return host values.
+ *   - Errors: every call returns an afn_status; nothing throws or exits across
+ *     the ABI.  afn_last_error() returns a thread-local description of the last
+ *     failure.  Arguments are validated first (sizes, ranges, and that array
+ *     pointers are device-accessible): violations return AFN_ERR_ARG and touch
+ *     nothing.
+ *   - Results are deterministic: no floating-point atomics; every reduction has
+ *     a fixed order that does not depend on timing.
+ *   - Integer outputs (landmark ids, kNN pattern, Alg. 1 rank) follow the
+ *     readings R3/R7-R15 of DESIGN.md: squared distances are sums over the
+ *     coordinates c = 0..d-1 in order of individually rounded (x_c - y_c)^2
+ *     (no FMA contraction), ties go to the lowest index.
+ */
+#ifndef AFN_H_
+#define AFN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AFN_ABI_VERSION 1
+
+typedef enum {
+  AFN_OK = 0,
+  AFN_ERR_ARG = 1,        /* invalid argument; nothing was modified            */
+  AFN_ERR_CUDA = 2,       /* CUDA runtime / launch failure                     */
+  AFN_ERR_NOMEM = 3,      /* device allocation failed                          */
+  AFN_ERR_NOT_SPD = 4,    /* Cholesky breakdown of K11+mu I or an FSAI block  */
+  AFN_ERR_BREAKDOWN = 5,  /* PCG breakdown (p.q <= 0 or non-finite)            */
+  AFN_ERR_STATE = 7       /* handle used in a state that does not allow it     */
+} afn_status;
+
+/* Opaque built preconditioner (immutable after afn_build). */
+typedef struct afn_handle_s* afn_handle;
+
+/* Build parameters.  Cite: l, mu; k_cap "limit ... such as 2000"
+ * (P:L209-210); w "the w-1 nearest neighbors" (w counts the
+ * diagonal, reading R15); m, rng_seed, k_threshold: Algorithm 1 (P:L661-678,
+ * readings R6-R13); fps_seed: "an arbitrary point" (reading R2). */
+typedef struct {
+  double l;             /* length-scale, > 0                                   */
+  double mu;            /* regularisation, > 0                                 */
+  int64_t k_cap;        /* landmark cap, >= 1                                  */
+  int32_t k_adaptive;   /* 1: k = min(k_cap, max(1, Alg.1 khat)); 0: k = k_cap */
+  int32_t w;            /* FSAI nonzeros per row incl. diagonal, 1..128        */
+  int32_t m;            /* Alg. 1 subsample size; 0 = min(500,max(100,n/100))  */
+  int32_t k_threshold;  /* Alg. 1 branch threshold (paper: 2000)               */
+  int64_t fps_seed;     /* first FPS point, 0 <= fps_seed < n                  */
+  uint64_t rng_seed;    /* Alg. 1 subsample seed (splitmix64 counter, R7)      */
+} afn_params;
+
+/* Information about a built handle (host struct). */
+typedef struct {
+  int64_t n, k, khat, nnz;      /* points, landmarks used, Alg.1 estimate, nnz(G) */
+  int32_t d, r, m, refined;     /* dims; Alg.1 rank r on the subsample, m, branch  */
+  double scale;                 /* Alg.1 coordinate scale (m/n)^(1/d)              */
+  double ms_alg1, ms_fps, ms_chol, ms_trsm, ms_knn, ms_fsai, ms_total; /* phase times */
+  double ms_fsai_rows;          /* the FSAI row kernel alone (inside ms_fsai)      */
+} afn_info;
+
+/* PCG report (host struct).  history: optional host array of >= maxit+1
+ * doubles receiving ||r_i||/||b|| (entry 0 = 1). */
+typedef struct {
+  int32_t iterations;   /* number of (K+mu I)p products in the loop            */
+  int32_t converged;    /* 1 if ||r||/||b|| <= tol was reached                 */
+  int32_t breakdown;    /* 1 if p.q <= 0 or a non-finite scalar stopped it     */
+  int32_t applies;      /* number of M^{-1} applications                       */
+  double relres;        /* recurrence residual at exit                         */
+  double relres_true;   /* ||b - (K+mu I)a|| / ||b|| (one extra matvec)        */
+  double solve_ms;      /* device time of the solve loop (CUDA events)         */
+  double matvec_ms;     /* device time of the loop's kernel matvecs            */
+  double apply_ms;      /* device time of the loop's AFN applications          */
+  double* history;      /* [host, optional] len maxit+1                        */
+} afn_solve_report;
+
+/* ------------------------------------------------------------------------ */
+/* Kernel matvec  y = (K + mu I) v   */
+/* X: n x d device, v,y: n device (y must not alias v or X).  Stream-ordered. */
+/* Rows are evaluated with a fixed column-chunk order, so the output is       */
+/* bit-identical run to run.  n >= 1, 1 <= d <= 16, l > 0, mu >= 0.           */
+afn_status kernel_matvec(const double* X, int64_t n, int32_t d, double l, double mu,
+                         const double* v, double* y, void* stream);
+
+/* Rows [row0, row0+nrows) of y = (K + mu I) v against all n columns (the row
+ * shard a rank owns in the multi-GPU layout).  y has nrows entries. */
+afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, double l, double mu,
+                              const double* v, int64_t row0, int64_t nrows, double* y,
+                              void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Farthest point sampling (eq.(3.3); brute force) [sync] */
+/* idx: k int64 device (original ids, selection order); fill: k doubles      */
+/* device (fill[i] = fill distance after i+1 selections) or NULL.     */
+afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t seed,
+                   int64_t* idx, double* fill, void* stream);
+
+/* kNN lower pattern.  For each position i of the N points P:   */
+/* row i = {i} plus the min(w-1, i) nearest positions j < i; columns        */
+/* ascending (diagonal last).  row_ptr: N+1 int64 device (closed form        */
+/* row_ptr[i] = sum_{t<i} min(w, t+1)), col: row_ptr[N] int32 device.        */
+/* 1 <= w <= 128.  Stream-ordered.                                           */
+afn_status afn_knn_pattern(const double* P, int64_t N, int32_t d, int32_t w,
+                           int64_t* row_ptr, int32_t* col, void* stream);
+
+/* Algorithm 1 on device.  [sync]  Outputs (host): khat, r, and */
+/* refined (1 if the eigenvalue-count branch was taken).  m = 0 -> default.  */
+afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, double l, int32_t m,
+                             uint64_t rng_seed, int32_t k_threshold, int64_t* khat,
+                             int32_t* r, int32_t* refined, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Build the AFN preconditioner M = B B^T of eq:factorized-form:*/
+/*   landmarks X_k by FPS, perm = [landmarks; rest ascending],   */
+/*   L L^T = K11 + mu I, W = K21 L^{-T} (= (L^{-1}K12)^T),      */
+/*   kNN pattern and FSAI G of S = K22 + mu I - K21 (K11+mu I)^{-1} K12      */
+/*   (P:L211-212, L248-263).  X is copied; the caller may free it after.     */
+/*   [sync].  On error *out is NULL.                                          */
+afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* params /*host*/,
+                     void* stream, afn_handle* out /*host*/);
+
+/* z = M^{-1} r with the two-step algorithm in V-form:         */
+/*   t = L^{-1} r1; u = r2 - W t; s2 = G^T (G u); s1 = L^{-T} (t - W^T s2).   */
+/* r, z: n device, ORIGINAL point order (the handle permutes).  Stream-ordered */
+/* on `stream`; must not alias.                                              */
+afn_status afn_apply(afn_handle h, const double* r, double* z, void* stream);
+
+/* PCG on (K+mu I) a = b with M = AFN: x0 = 0, stop when      */
+/* ||r||/||b|| <= tol (recurrence residual), at most maxit iterations;        */
+/* fixed_iters > 0 runs exactly that many.  b, a: n device, original order.   */
+/* Non-convergence is AFN_OK with converged = 0.  [sync]                      */
+afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, int32_t maxit,
+                         int32_t fixed_iters, afn_solve_report* rep /*host*/, void* stream);
+
+/* End-to-end convenience with HOST buffers: copies X, b in, builds, solves, */
+/* copies a out (all inside the call).  X: n x d host, b, a: n host. [sync]   */
+afn_status afn_solve_host(const double* X, const double* b, double* a, int64_t n, int32_t d,
+                          const afn_params* params, double tol, int32_t maxit,
+                          afn_info* info /*host, optional*/, afn_solve_report* rep /*host, optional*/,
+                          void* stream);
+
+afn_status afn_get_info(afn_handle h, afn_info* info /*host*/);
+
+/* Copy internal arrays to HOST memory (tests / diagnostics). bytes must equal */
+/* the array size: PERM int64[n]; FILL double[k]; L double[k*k] (row-major,   */
+/* lower); ROWPTR int64[n-k+1]; COL int32[nnz]; GVAL double[nnz];             */
+/* W_ROWS double[(n-k)*k] (row-major W = K21 L^{-T}).                        */
+enum { AFN_OUT_PERM = 0, AFN_OUT_FILL = 1, AFN_OUT_L = 2, AFN_OUT_ROWPTR = 3,
+       AFN_OUT_COL = 4, AFN_OUT_GVAL = 5, AFN_OUT_W = 6 };
+afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes);
+
+void afn_destroy(afn_handle h);
+
+/* ------------------------------------------------------------------------ */
+/* Measurement helpers (bench.py): FP64 FMA peak probe.  Runs `iters` DFMA   */
+/* chains on every SM and returns achieved FP64 TFLOP/s (FMA = 2). [sync]    */
+afn_status afn_probe_dfma(int64_t iters, double* tflops /*host*/, void* stream);
+
+/* Number of kernels this library launched since load (its own kernels only). */
+int64_t afn_launch_count(void);
+const char* afn_last_error(void);
+int32_t afn_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AFN_H_ */

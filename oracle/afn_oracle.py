@@ -23,7 +23,7 @@ import scipy.sparse as sp
 
 __all__ = [
     "sqdist_to", "sqdist_block", "kernel_block", "kmv", "kmv_rows",
-    "fps", "fill_distance", "separation_distance", "knn_lower",
+    "fps", "fill_distance", "separation_distance", "knn_lower", "knn_row",
     "splitmix64", "subsample_ids", "default_m", "alg1",
     "fsai_rows", "build_afn", "apply_afn", "dense_B", "pcg", "afn_pcg_solve",
     "cg_solve",
@@ -154,6 +154,17 @@ def separation_distance(X, sel) -> float:
 # ----------------------------------------------------------------------------
 # FSAI sparsity pattern
 # ----------------------------------------------------------------------------
+def knn_row(P: np.ndarray, i: int, w: int) -> np.ndarray:
+    """Pattern of row i: the min(w-1, i) nearest positions j < i by
+    the total order (d2, j) (R3), ascending, then i itself (R15)."""
+    if i == 0 or w == 1:
+        nb = np.empty(0, dtype=np.int64)
+    else:
+        d2 = sqdist_to(P[:i], P[i])
+        nb = np.argsort(d2, kind="stable")[: w - 1]
+    return np.concatenate([np.sort(nb), [i]]).astype(np.int64)
+
+
 def knn_lower(P: np.ndarray, w: int):
     """Row i = {i} plus its min(w-1, i) nearest neighbours among positions < i.
 
@@ -167,12 +178,7 @@ def knn_lower(P: np.ndarray, w: int):
     row_ptr = np.zeros(N + 1, dtype=np.int64)
     cols = []
     for i in range(N):
-        if i == 0 or w == 1:
-            nb = np.empty(0, dtype=np.int64)
-        else:
-            d2 = sqdist_to(P[:i], P[i])
-            nb = np.argsort(d2, kind="stable")[: w - 1]
-        row = np.concatenate([np.sort(nb), [i]]).astype(np.int64)
+        row = knn_row(P, i, w)
         cols.append(row)
         row_ptr[i + 1] = row_ptr[i] + len(row)
     col = np.concatenate(cols) if cols else np.empty(0, dtype=np.int64)

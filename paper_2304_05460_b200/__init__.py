@@ -1,0 +1,294 @@
+"""paper_2304_05460_b200 -- B200-native AFN-preconditioned CG (arXiv 2304.05460).
+
+Thin ctypes binding over the C ABI in ``include/afn.h`` (``libafn.so``, built
+for sm_100a by ``paper_2304_05460_b200.build``).  This module only marshals
+arguments: every step of the hot path runs in the library's CUDA kernels.
+There is no CPU fallback -- importing fails loudly if the library is missing.
+
+Device arrays are ``torch.Tensor`` objects (float64, contiguous, on a CUDA
+device); PyTorch supplies memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libafn.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build it with `python -m paper_2304_05460_b200.build` "
+        "(no CPU fallback exists)")
+
+_lib = C.CDLL(LIB_PATH)
+
+AFN_OK = 0
+STATUS = {0: "AFN_OK", 1: "AFN_ERR_ARG", 2: "AFN_ERR_CUDA", 3: "AFN_ERR_NOMEM",
+          4: "AFN_ERR_NOT_SPD", 5: "AFN_ERR_BREAKDOWN", 7: "AFN_ERR_STATE"}
+OUT_PERM, OUT_FILL, OUT_L, OUT_ROWPTR, OUT_COL, OUT_GVAL, OUT_W = range(7)
+
+
+class AfnError(RuntimeError):
+    def __init__(self, status, where):
+        msg = _lib.afn_last_error().decode(errors="replace")
+        super().__init__(f"{where}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Params(C.Structure):
+    _fields_ = [("l", C.c_double), ("mu", C.c_double), ("k_cap", C.c_int64),
+                ("k_adaptive", C.c_int32), ("w", C.c_int32), ("m", C.c_int32),
+                ("k_threshold", C.c_int32), ("fps_seed", C.c_int64), ("rng_seed", C.c_uint64)]
+
+
+class Info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("k", C.c_int64), ("khat", C.c_int64), ("nnz", C.c_int64),
+                ("d", C.c_int32), ("r", C.c_int32), ("m", C.c_int32), ("refined", C.c_int32),
+                ("scale", C.c_double), ("ms_alg1", C.c_double), ("ms_fps", C.c_double),
+                ("ms_chol", C.c_double), ("ms_trsm", C.c_double), ("ms_knn", C.c_double),
+                ("ms_fsai", C.c_double), ("ms_total", C.c_double), ("ms_fsai_rows", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class Report(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("breakdown", C.c_int32),
+                ("applies", C.c_int32), ("relres", C.c_double), ("relres_true", C.c_double),
+                ("solve_ms", C.c_double), ("matvec_ms", C.c_double), ("apply_ms", C.c_double),
+                ("history", C.POINTER(C.c_double))]
+
+    def as_dict(self):
+        return dict(iterations=self.iterations, converged=bool(self.converged),
+                    breakdown=bool(self.breakdown), applies=self.applies, relres=self.relres,
+                    relres_true=self.relres_true, solve_ms=self.solve_ms,
+                    matvec_ms=self.matvec_ms, apply_ms=self.apply_ms)
+
+
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+_sig = {
+    "kernel_matvec": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P, _P, _P]),
+    "kernel_matvec_rows": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P,
+                                     C.c_int64, C.c_int64, _P, _P]),
+    "afn_fps": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, _P, _P, _P]),
+    "afn_knn_pattern": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
+    "afn_estimate_rank": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_int32, C.c_uint64,
+                                    C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                    C.POINTER(C.c_int32), _P]),
+    "afn_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.POINTER(Params), _P, C.POINTER(_P)]),
+    "afn_apply": (C.c_int, [_P, _P, _P, _P]),
+    "afn_pcg_solve": (C.c_int, [_P, _P, _P, C.c_double, C.c_int32, C.c_int32, C.POINTER(Report), _P]),
+    "afn_solve_host": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.POINTER(Params), C.c_double,
+                                 C.c_int32, C.POINTER(Info), C.POINTER(Report), _P]),
+    "afn_get_info": (C.c_int, [_P, C.POINTER(Info)]),
+    "afn_copy_out": (C.c_int, [_P, C.c_int32, _P, C.c_size_t]),
+    "afn_destroy": (None, [_P]),
+    "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
+    "afn_launch_count": (C.c_int64, []),
+    "afn_last_error": (C.c_char_p, []),
+    "afn_abi_version": (C.c_int32, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_sig)
+
+
+def _check(status, where):
+    if status != AFN_OK:
+        raise AfnError(status, where)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev(t, name, dtype=None):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def launch_count() -> int:
+    return int(_lib.afn_launch_count())
+
+
+def abi_version() -> int:
+    return int(_lib.afn_abi_version())
+
+
+# ---------------------------------------------------------------------------
+def kernel_matvec(X, l, mu, v, y=None, stream=None):
+    """y = (K + mu I) v on the device (include/afn.h kernel_matvec)."""
+    torch = _torch()
+    n, d = X.shape
+    if y is None:
+        y = torch.empty_like(v)
+    _check(_lib.kernel_matvec(_dev(X, "X", torch.float64), n, d, float(l), float(mu),
+                              _dev(v, "v", torch.float64), _dev(y, "y", torch.float64),
+                              _stream(stream)), "kernel_matvec")
+    return y
+
+
+def kernel_matvec_rows(X, l, mu, v, row0, nrows, y=None, stream=None):
+    torch = _torch()
+    n, d = X.shape
+    if y is None:
+        y = torch.empty(nrows, dtype=torch.float64, device=v.device)
+    _check(_lib.kernel_matvec_rows(_dev(X, "X", torch.float64), n, d, float(l), float(mu),
+                                   _dev(v, "v", torch.float64), int(row0), int(nrows),
+                                   _dev(y, "y", torch.float64), _stream(stream)),
+           "kernel_matvec_rows")
+    return y
+
+
+def afn_fps(X, k, seed=0, stream=None):
+    """Farthest point sampling -> (idx int64[k], fill float64[k]) device tensors."""
+    torch = _torch()
+    n, d = X.shape
+    idx = torch.empty(k, dtype=torch.int64, device=X.device)
+    fill = torch.empty(k, dtype=torch.float64, device=X.device)
+    _check(_lib.afn_fps(_dev(X, "X", torch.float64), n, d, int(k), int(seed), _dev(idx, "idx"),
+                        _dev(fill, "fill"), _stream(stream)), "afn_fps")
+    return idx, fill
+
+
+def knn_nnz(N, w):
+    return N * (N + 1) // 2 if N < w else w * (w + 1) // 2 + (N - w) * w
+
+
+def afn_knn_pattern(P, w, stream=None):
+    """kNN lower pattern -> (row_ptr int64[N+1], col int32[nnz]) device tensors."""
+    torch = _torch()
+    N, d = P.shape
+    rp = torch.empty(N + 1, dtype=torch.int64, device=P.device)
+    col = torch.empty(max(1, knn_nnz(N, w)), dtype=torch.int32, device=P.device)
+    _check(_lib.afn_knn_pattern(_dev(P, "P", torch.float64), N, d, int(w), _dev(rp, "row_ptr"),
+                                _dev(col, "col"), _stream(stream)), "afn_knn_pattern")
+    return rp, col[:knn_nnz(N, w)]
+
+
+def afn_estimate_rank(X, l, m=0, rng_seed=0, k_threshold=2000, stream=None):
+    torch = _torch()
+    n, d = X.shape
+    kh, r, ref = C.c_int64(), C.c_int32(), C.c_int32()
+    _check(_lib.afn_estimate_rank(_dev(X, "X", torch.float64), n, d, float(l), int(m),
+                                  int(rng_seed), int(k_threshold), C.byref(kh), C.byref(r),
+                                  C.byref(ref), _stream(stream)), "afn_estimate_rank")
+    return dict(khat=kh.value, r=r.value, refined=bool(ref.value))
+
+
+def make_params(l, mu, k_cap, w, k_adaptive=False, m=0, k_threshold=2000, fps_seed=0, rng_seed=0):
+    return Params(float(l), float(mu), int(k_cap), int(bool(k_adaptive)), int(w), int(m),
+                  int(k_threshold), int(fps_seed), int(rng_seed))
+
+
+class Handle:
+    """A built AFN preconditioner (include/afn.h afn_handle)."""
+
+    def __init__(self, X, params: Params, stream=None):
+        torch = _torch()
+        self.n, self.d = X.shape
+        self.device = X.device
+        h = C.c_void_p()
+        _check(_lib.afn_build(_dev(X, "X", torch.float64), self.n, self.d, C.byref(params),
+                              _stream(stream), C.byref(h)), "afn_build")
+        self._h = h
+        self.params = params
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _lib.afn_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        inf = Info()
+        _check(_lib.afn_get_info(self._h, C.byref(inf)), "afn_get_info")
+        return inf.as_dict()
+
+    def apply(self, r, z=None, stream=None):
+        torch = _torch()
+        if z is None:
+            z = torch.empty_like(r)
+        _check(_lib.afn_apply(self._h, _dev(r, "r", torch.float64), _dev(z, "z", torch.float64),
+                              _stream(stream)), "afn_apply")
+        return z
+
+    def pcg_solve(self, b, a=None, tol=1e-4, maxit=500, fixed_iters=0, history=False, stream=None):
+        torch = _torch()
+        import numpy as np
+        if a is None:
+            a = torch.empty_like(b)
+        rep = Report()
+        hist = None
+        if history:
+            hist = np.zeros(maxit + 1)
+            rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))
+        _check(_lib.afn_pcg_solve(self._h, _dev(b, "b", torch.float64), _dev(a, "a", torch.float64),
+                                  float(tol), int(maxit), int(fixed_iters), C.byref(rep),
+                                  _stream(stream)), "afn_pcg_solve")
+        out = rep.as_dict()
+        if hist is not None:
+            out["history"] = hist[: rep.iterations + 1].copy()
+        return a, out
+
+    def copy_out(self, what):
+        import numpy as np
+        inf = self.info()
+        n, k, nnz = inf["n"], inf["k"], inf["nnz"]
+        shapes = {OUT_PERM: (np.int64, (n,)), OUT_FILL: (np.float64, (k,)),
+                  OUT_L: (np.float64, (k, k)), OUT_ROWPTR: (np.int64, (n - k + 1,)),
+                  OUT_COL: (np.int32, (nnz,)), OUT_GVAL: (np.float64, (nnz,)),
+                  OUT_W: (np.float64, (n - k, k))}
+        dt, shp = shapes[what]
+        arr = np.empty(shp, dtype=dt)
+        _check(_lib.afn_copy_out(self._h, int(what), arr.ctypes.data_as(C.c_void_p), arr.nbytes),
+               "afn_copy_out")
+        return arr
+
+
+def afn_build(X, params: Params, stream=None) -> Handle:
+    return Handle(X, params, stream)
+
+
+def afn_solve_host(X, b, params: Params, tol=1e-4, maxit=500, stream=None):
+    """End-to-end solve with HOST numpy arrays (copies inside the C call)."""
+    import numpy as np
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    n, d = X.shape
+    a = np.empty(n)
+    inf, rep = Info(), Report()
+    _check(_lib.afn_solve_host(X.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+                               a.ctypes.data_as(C.c_void_p), n, d, C.byref(params), float(tol),
+                               int(maxit), C.byref(inf), C.byref(rep), _stream(stream)),
+           "afn_solve_host")
+    return a, inf.as_dict(), rep.as_dict()
+
+
+def probe_dfma(iters=1 << 16, stream=None) -> float:
+    out = C.c_double()
+    _check(_lib.afn_probe_dfma(int(iters), C.byref(out), _stream(stream)), "afn_probe_dfma")
+    return out.value

@@ -1,0 +1,144 @@
+// afn_common.cuh -- shared device helpers of the sm_100a AFN path.
+// (Product code.  Shares nothing with oracle/.)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/afn.h"
+
+namespace afn {
+
+// ---------------------------------------------------------------------------
+// Launch accounting (bench.py reports how many of our kernels ran).
+void note_launch(int count = 1);
+
+// ---------------------------------------------------------------------------
+// Bit-exact squared distance (readings R3): c = 0..d-1 in order, each
+// subtract / multiply / add individually rounded -- no FMA contraction.
+template <int D>
+__device__ __forceinline__ double d2_exact(const double* a, const double* b) {
+  double s = __dmul_rn(__dsub_rn(a[0], b[0]), __dsub_rn(a[0], b[0]));
+#pragma unroll
+  for (int c = 1; c < D; ++c) {
+    double t = __dsub_rn(a[c], b[c]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return s;
+}
+
+__device__ __forceinline__ double d2_exact_rt(const double* a, const double* b, int d) {
+  double t0 = __dsub_rn(a[0], b[0]);
+  double s = __dmul_rn(t0, t0);
+  for (int c = 1; c < d; ++c) {
+    double t = __dsub_rn(a[c], b[c]);
+    s = __dadd_rn(s, __dmul_rn(t, t));
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// 2^y for y <= 0 (the Gaussian kernel exp(-d^2/l^2) = 2^(-d^2 log2(e)/l^2)).
+// Reduction y = n + j/16 + f, |f| <= 1/32; 2^(j/16) from a 16-entry table;
+// 2^f = e^(f ln2) by its degree-6 Taylor polynomial (truncation < 5e-16
+// relative).  2^n is applied by an integer add to the exponent field.
+// y < -1020 (values < 2^-1020 ~ 9e-308) returns +0.
+// FP64 pipe cost: 1 DFMA (scale+round) + 1 DADD + 1 DFMA (f) + 6 DFMA (poly)
+// + 1 DMUL (table) = 10.
+// ---------------------------------------------------------------------------
+
+#define AFN_EXP2_TAB_INIT                                                          \
+  {0x1.0000000000000p+0, 0x1.0b5586cf9890fp+0, 0x1.172b83c7d517bp+0,              \
+   0x1.2387a6e756238p+0, 0x1.306fe0a31b715p+0, 0x1.3dea64c123422p+0,              \
+   0x1.4bfdad5362a27p+0, 0x1.5ab07dd485429p+0, 0x1.6a09e667f3bcdp+0,              \
+   0x1.7a11473eb0187p+0, 0x1.8ace5422aa0dbp+0, 0x1.9c49182a3f090p+0,              \
+   0x1.ae89f995ad3adp+0, 0x1.c199bdd85529cp+0, 0x1.d5818dcfba487p+0,              \
+   0x1.ea4afa2a490dap+0}
+
+static __device__ __constant__ double c_exp2_tab[16] = AFN_EXP2_TAB_INIT;
+
+// copy the table into shared memory (call by all threads, then __syncthreads)
+__device__ __forceinline__ void load_exp2_tab(double* s_tab) {
+  if (threadIdx.x < 16) s_tab[threadIdx.x] = c_exp2_tab[threadIdx.x];
+}
+
+// ln(2)^k / k!, k = 0..6
+#define AFN_E2C0 0x1.0000000000000p+0
+#define AFN_E2C1 0x1.62e42fefa39efp-1
+#define AFN_E2C2 0x1.ebfbdff82c58fp-3
+#define AFN_E2C3 0x1.c6b08d704a0c0p-5
+#define AFN_E2C4 0x1.3b2ab6fba4e77p-7
+#define AFN_E2C5 0x1.5d87fe78a6731p-10
+#define AFN_E2C6 0x1.430912f86c787p-13
+#define AFN_LOG2E 0x1.71547652b82fep+0
+#define AFN_SQRT_LOG2E 0x1.337cc2183b050p+0
+
+// s = -y >= 0 (pass the positive exponent). tab: 16-entry table (smem or const).
+__device__ __forceinline__ double exp2_neg(double s, const double* tab) {
+  const double magic = 0x1.8p52;
+  double t = fma(s, -16.0, magic);          // rint(-16 s) in the low word
+  double nf = t - magic;                    // = rint(-16 s) as a double
+  double f = fma(nf, -0.0625, -s);          // -s - nf/16, exact, |f| <= 1/32
+  int n16 = __double2loint(t);
+  double p = AFN_E2C6;
+  p = fma(p, f, AFN_E2C5);
+  p = fma(p, f, AFN_E2C4);
+  p = fma(p, f, AFN_E2C3);
+  p = fma(p, f, AFN_E2C2);
+  p = fma(p, f, AFN_E2C1);
+  p = fma(p, f, AFN_E2C0);
+  p = p * tab[n16 & 15];
+  int hi = __double2hiint(p) + ((n16 >> 4) << 20);
+  double r = __hiloint2double(hi, __double2loint(p));
+  // s >= 1020 (hi word of 1020.0 is 0x408FE000) -> +0; also covers huge s / inf
+  return (__double2hiint(s) >= 0x408FE000) ? 0.0 : r;
+}
+
+// Gaussian entry from a squared distance: exp(-d2/l^2) with c = log2(e)/l^2.
+__device__ __forceinline__ double gauss_from_d2(double d2, double c, const double* tab) {
+  return exp2_neg(d2 * c, tab);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic block reductions.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double* sh /*>= NT/32*/) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = (lane < NT / 32) ? sh[lane] : 0.0;
+    r = warp_sum(r);
+  }
+  return r;  // valid in warp 0
+}
+
+}  // namespace afn
+
+// ---------------------------------------------------------------------------
+// Host-side error plumbing shared by the .cu files.
+namespace afn {
+void set_error(const char* fmt, ...);
+afn_status cuda_status(cudaError_t e, const char* what);
+}  // namespace afn
+
+#define AFN_CUDA(call)                                                       \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess) return afn::cuda_status(e_, #call);               \
+  } while (0)
+
+#define AFN_LAUNCH_CHECK(what)                                               \
+  do {                                                                       \
+    cudaError_t e_ = cudaGetLastError();                                     \
+    if (e_ != cudaSuccess) return afn::cuda_status(e_, what);                \
+    afn::note_launch();                                                      \
+  } while (0)

@@ -1,0 +1,103 @@
+// afn_internal.h -- host-side internal interfaces between the .cu modules and
+// the C ABI (abi.cu).  Not part of the public boundary (include/afn.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/afn.h"
+
+namespace afn {
+
+int num_sms();  // SM count of the current device (cached per device)
+
+// Stream-ordered device allocation helpers (cudaMallocAsync pool).
+afn_status dalloc(void** p, size_t bytes, cudaStream_t st);
+void dfree(void* p, cudaStream_t st);
+
+// ---- kernel matvec (kmv.cu) ----------------------------------------------
+struct KmvPlan {
+  int64_t row_tiles = 0, chunks = 1, chunk_cols = 0;
+};
+KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms);
+// Xs = X * sqrt(log2 e)/l   (n x d)
+afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs, cudaStream_t st);
+// y[0..nrows) = rows [row0,row0+nrows) of (K + mu I) v; partial: chunks*nrows doubles
+afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, int64_t row0,
+                      int64_t nrows, double* y, double* partial, const KmvPlan& p, cudaStream_t st);
+
+// ---- FPS (fps.cu) ---------------------------------------------------------
+afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
+                   double* fill, cudaStream_t st);
+
+// ---- kNN pattern (knn.cu) -------------------------------------------------
+int64_t knn_nnz(int64_t N, int w);
+afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, int32_t* col,
+                   cudaStream_t st);
+
+// ---- dense build (dense.cu) -----------------------------------------------
+// gather rows: Y[i] = X[perm[i]] (n x d)
+afn_status gather_rows(const double* X, int64_t n, int d, const int64_t* perm, double* Y,
+                       cudaStream_t st);
+// A = K(X1, X1) + mu I, full k x k row-major
+afn_status gen_k11(const double* X1, int64_t k, int d, double l, double mu, double* A,
+                   cudaStream_t st);
+// in-place lower Cholesky of the k x k row-major A (upper triangle zeroed);
+// *d_info = 0 on success, else 1 + the failing row.
+afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st);
+// W (N x k row-major) = K(Xr, X1) L^{-T}  (i.e. L W^T = K12), K tiles on the fly
+afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
+                  double l, double* W, cudaStream_t st);
+// LinvT (k x k row-major) = L^{-T} (upper triangular)
+afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st);
+
+// ---- FSAI (fsai.cu) -------------------------------------------------------
+// G values on the pattern of the Schur complement S = K22 + mu I - W W^T
+afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
+                    int64_t k, const int64_t* row_ptr, const int32_t* col, double* gval,
+                    int* d_info, cudaStream_t st);
+// CSR transpose (N x N, columns sorted within each output row)
+afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* val, int64_t N,
+                         int64_t nnz, int64_t* trp, int32_t* tcol, double* tval, cudaStream_t st);
+
+// ---- BLAS-2 / SpMV / vectors (blas.cu) ------------------------------------
+// y = ybase + alpha * A x, A: R x C row-major (lda = C).  ybase may be null (0)
+afn_status gemv_n(const double* A, int64_t R, int64_t C, const double* x, const double* ybase,
+                  double alpha, double* y, cudaStream_t st);
+// y = ybase + alpha * A^T x; ws >= gemv_t_ws(R, C) doubles
+int64_t gemv_t_ws(int64_t R, int64_t C);
+afn_status gemv_t(const double* A, int64_t R, int64_t C, const double* x, const double* ybase,
+                  double alpha, double* y, double* ws, cudaStream_t st);
+afn_status spmv_csr(const int64_t* rp, const int32_t* col, const double* val, int64_t N,
+                    const double* x, double* y, cudaStream_t st);
+afn_status gather_vec(const double* x, const int64_t* perm, int64_t n, double* y, cudaStream_t st);
+afn_status scatter_vec(const double* x, const int64_t* perm, int64_t n, double* y, cudaStream_t st);
+
+// deterministic dot: *out = a . b  (ws >= dot_ws() doubles, cnt: 1 zeroed uint)
+int64_t dot_ws();
+afn_status dot(const double* a, const double* b, int64_t n, double* out, double* ws,
+               unsigned* cnt, cudaStream_t st);
+// PCG scalar slots (device doubles): rz alternates between slots 0 and 1
+enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_N = 8 };
+// x += a p; r -= a q with a = sc[rz_slot]/sc[PQ] (0 if PQ <= 0); sc[RR] = r.r
+afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, int64_t n,
+                         double* sc, int rz_slot, double* ws, unsigned* cnt, cudaStream_t st);
+// p = z + beta p, beta = sc[rz_new_slot]/sc[rz_old_slot]
+afn_status pcg_update_p(double* p, const double* z, int64_t n, const double* sc, int rz_new_slot,
+                        int rz_old_slot, cudaStream_t st);
+afn_status vec_copy(double* y, const double* x, int64_t n, cudaStream_t st);
+afn_status vec_axpby(double* y, double a, const double* x, double b, int64_t n, cudaStream_t st);
+
+// ---- Alg. 1 (alg1.cu) ------------------------------------------------------
+struct Alg1Result {
+  int64_t khat = 0;
+  int32_t r = 0, m = 0, refined = 0;
+  double scale = 0.0;
+};
+int alg1_default_m(int64_t n);
+afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t rng_seed,
+                    int k_threshold, Alg1Result* res, cudaStream_t st);
+
+// ---- probes (probe.cu) -----------------------------------------------------
+afn_status probe_dfma(int64_t iters, double* tflops, cudaStream_t st);
+
+}  // namespace afn

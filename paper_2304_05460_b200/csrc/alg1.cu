@@ -1,0 +1,398 @@
+// alg1.cu -- Algorithm 1, Nystrom rank estimation,
+// on the device.
+//
+//  1. "randomly subsample a subset X_m of m points" (L666): counter-based
+//     splitmix64 keys h_i = splitmix64(seed ^ i*golden) (reading R7); the m
+//     smallest keys in ascending order.  A grid kernel collects every key
+//     below a threshold, one CTA bitonic-sorts them.
+//  2. scale the coordinates by s = (m/n)^(1/d) (L666, R8; s from the host),
+//     form K_m (L667), FPS on X_m from subsample position 0 (fps.cu).
+//  3. "the Nystrom rank r such that the relative Nystrom approximation error
+//     falls below 0.1" (L668): with S^(r) the Schur complement of K_m after r
+//     elimination steps in FPS order (K_m - K_nys,r = [0 0; 0 S^(r)], P:L559;
+//     pivots <= m eps ||K_m|| are skipped, R10), the test
+//     ||S^(r)||_2 < 0.1 ||K_m||_2 is decided as "0.1||K_m|| I - S^(r) is
+//     positive definite" by a Cholesky attempt (S^(r) is PSD).  The error
+//     curve is non-increasing in r (nested landmarks), so the smallest
+//     passing r is found by bisection.
+//  4. k = r n / m rounded half up (R11); if k < 2000 the count of eigenvalues
+//     of K_m on the unscaled points above 0.1 (L673-674) by Sturm counts on a
+//     Householder tridiagonalisation.  ||K_m||_2 = lambda_max also comes from
+//     the tridiagonal form (bisection).
+// All dense work is small (m <= 1024) and runs in single-CTA kernels on
+// L2-resident global memory.
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <vector>
+
+#include "afn_common.cuh"
+#include "afn_internal.h"
+
+namespace afn {
+namespace {
+
+constexpr int AT = 1024;         // threads of the single-CTA kernels
+constexpr int CAND_CAP = 4096;   // candidate keys sorted in one CTA
+
+__device__ __forceinline__ uint64_t splitmix64_dev(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+__global__ void cand_kernel(int64_t n, uint64_t seed, uint64_t thr, unsigned long long* keys,
+                            long long* ids, unsigned* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = splitmix64_dev(seed ^ ((uint64_t)i * 0x9E3779B97F4A7C15ULL));
+  if (h < thr) {
+    const unsigned p = atomicAdd(cnt, 1u);
+    if (p < CAND_CAP) {
+      keys[p] = h;
+      ids[p] = i;
+    }
+  }
+}
+
+// sort the candidates by key (unique), write the first m ids
+__global__ void __launch_bounds__(AT) cand_sort_kernel(const unsigned long long* keys, const long long* ids,
+                                                       const unsigned* cnt, int m, int64_t* out) {
+  extern __shared__ unsigned long long dsm_keys[];
+  unsigned long long* sk = dsm_keys;
+  long long* si = reinterpret_cast<long long*>(dsm_keys + CAND_CAP);
+  const unsigned c = min(*cnt, (unsigned)CAND_CAP);
+  for (int t = threadIdx.x; t < CAND_CAP; t += AT) {
+    sk[t] = t < (int)c ? keys[t] : ~0ULL;
+    si[t] = t < (int)c ? ids[t] : -1;
+  }
+  __syncthreads();
+  for (int k = 2; k <= CAND_CAP; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = threadIdx.x; t < CAND_CAP; t += AT) {
+        const int p = t ^ j;
+        if (p > t) {
+          const bool up = (t & k) == 0;
+          const unsigned long long a = sk[t], b = sk[p];
+          if ((a > b) == up) {
+            sk[t] = b; sk[p] = a;
+            const long long x = si[t]; si[t] = si[p]; si[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int t = threadIdx.x; t < m; t += AT) out[t] = si[t];
+}
+
+__global__ void gather_scale_kernel(const double* __restrict__ X, int d, const int64_t* __restrict__ ids,
+                                    int m, double s, double* __restrict__ Xm, double* __restrict__ Xu) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * d) return;
+  const int i = e / d, c = e - i * d;
+  const double x = X[ids[i] * d + c];
+  Xu[e] = x;
+  Xm[e] = x * s;
+}
+
+__global__ void permute_sym_kernel(const double* __restrict__ A, int m, const int64_t* __restrict__ ord,
+                                   double* __restrict__ B) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m * m) return;
+  const int i = e / m, j = e - i * m;
+  B[e] = A[ord[i] * m + ord[j]];
+}
+
+__device__ double block_sum_1024(double v, double* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = sh[lane];
+  r = warp_sum(r);
+  return r;  // every thread gets the total (blockDim = 1024 -> 32 warps)
+}
+
+// Householder tridiagonalisation of the symmetric m x m A (destroyed);
+// diag -> dgl[0..m), offdiag -> off[0..m-1)
+__global__ void __launch_bounds__(AT) tridiag_kernel(double* A, int m, double* dgl, double* off) {
+  __shared__ double v[1024];
+  __shared__ double p[1024];
+  __shared__ double sh[32];
+  __shared__ double s_beta, s_alpha;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int j = 0; j + 2 < m; ++j) {
+    const int L = m - j - 1;  // length of the column below the diagonal
+    double loc = 0.0;
+    for (int t = tid; t < L; t += AT) {
+      const double x = A[(int64_t)(j + 1 + t) * m + j];
+      v[t] = x;
+      loc += x * x;
+    }
+    const double nrm2 = block_sum_1024(loc, sh);
+    if (tid == 0) {
+      const double x0 = v[0];
+      const double nrm = sqrt(nrm2);
+      double alpha = (x0 > 0.0) ? -nrm : nrm;
+      const double v0 = x0 - alpha;
+      const double vv = nrm2 - x0 * x0 + v0 * v0;
+      if (nrm2 == 0.0 || vv == 0.0) {
+        s_beta = 0.0;
+        alpha = x0;
+      } else {
+        s_beta = 2.0 / vv;
+      }
+      v[0] = v0;
+      s_alpha = alpha;
+      dgl[j] = A[(int64_t)j * m + j];
+      off[j] = alpha;
+    }
+    __syncthreads();
+    const double beta = s_beta;
+    if (beta == 0.0) continue;
+    // p = beta * A22 v   (warp per row, lanes over columns)
+    for (int i = wid; i < L; i += AT / 32) {
+      const double* row = A + (int64_t)(j + 1 + i) * m + (j + 1);
+      double s = 0.0;
+      for (int t = lane; t < L; t += 32) s = fma(row[t], v[t], s);
+      s = warp_sum(s);
+      if (lane == 0) p[i] = beta * s;
+    }
+    __syncthreads();
+    double loc2 = 0.0;
+    for (int t = tid; t < L; t += AT) loc2 += p[t] * v[t];
+    const double pv = block_sum_1024(loc2, sh);
+    const double K = 0.5 * beta * pv;
+    for (int t = tid; t < L; t += AT) p[t] = p[t] - K * v[t];  // w
+    __syncthreads();
+    for (int64_t e = tid; e < (int64_t)L * L; e += AT) {
+      const int i = (int)(e / L), t = (int)(e - (int64_t)i * L);
+      double* a = A + (int64_t)(j + 1 + i) * m + (j + 1 + t);
+      *a = *a - v[i] * p[t] - p[i] * v[t];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (m >= 2) {
+      dgl[m - 2] = A[(int64_t)(m - 2) * m + (m - 2)];
+      dgl[m - 1] = A[(int64_t)(m - 1) * m + (m - 1)];
+      off[m - 2] = A[(int64_t)(m - 1) * m + (m - 2)];
+    } else {
+      dgl[0] = A[0];
+    }
+  }
+}
+
+// number of eigenvalues of the tridiagonal (dgl, off) strictly below x (Sturm)
+__device__ int sturm_count(const double* dgl, const double* off, int m, double x) {
+  int c = 0;
+  double q = dgl[0] - x;
+  if (q < 0.0) ++c;
+  for (int i = 1; i < m; ++i) {
+    double qq = (q != 0.0) ? q : DBL_MIN * 4.0;
+    q = dgl[i] - x - off[i - 1] * off[i - 1] / qq;
+    if (q < 0.0) ++c;
+  }
+  return c;
+}
+
+// out[0] = lambda_max (bisection), out[1] = #{lambda > x_count}
+__global__ void eig_summary_kernel(const double* dgl, const double* off, int m, double x_count,
+                                   double* out) {
+  if (threadIdx.x != 0) return;
+  double lo = DBL_MAX, hi = -DBL_MAX;
+  for (int i = 0; i < m; ++i) {
+    const double r = (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < m ? fabs(off[i]) : 0.0);
+    lo = fmin(lo, dgl[i] - r);
+    hi = fmax(hi, dgl[i] + r);
+  }
+  for (int it = 0; it < 200 && hi > lo; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_count(dgl, off, m, mid) == m) hi = mid; else lo = mid;
+  }
+  out[0] = hi;
+  out[1] = (double)(m - sturm_count(dgl, off, m, x_count));
+}
+
+// pass = [ tau I - S^(r) is positive definite ], S^(r) the Schur complement of
+// Kp after r threshold-pivoted elimination steps.  W: m x m scratch.
+__global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict__ Kp, int m, int r,
+                                                        double thr, double tau, double* W, int* pass) {
+  __shared__ double s_piv;
+  __shared__ int s_ok;
+  const int tid = threadIdx.x;
+  for (int64_t e = tid; e < (int64_t)m * m; e += AT) W[e] = Kp[e];
+  if (tid == 0) s_ok = 1;
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    const double pj = W[(int64_t)j * m + j];
+    if (!(pj > thr)) continue;  // exhausted column (uniform across the CTA)
+    const int L = m - j - 1;
+    for (int64_t e = tid; e < (int64_t)L * L; e += AT) {
+      const int i = j + 1 + (int)(e / L), t = j + 1 + (int)(e % L);
+      W[(int64_t)i * m + t] -= (W[(int64_t)i * m + j] * W[(int64_t)j * m + t]) / pj;
+    }
+    __syncthreads();
+  }
+  // Cholesky of tau I - W[r:, r:]
+  for (int j = r; j < m; ++j) {
+    if (tid == 0) {
+      const double c = tau - W[(int64_t)j * m + j];
+      if (!(c > 0.0)) s_ok = 0;
+      s_piv = c > 0.0 ? sqrt(c) : 1.0;
+    }
+    __syncthreads();
+    if (!s_ok) break;
+    const double piv = s_piv;
+    // column j below the diagonal of C = tau I - W: C[i][j] = -W[i][j]
+    for (int i = j + 1 + tid; i < m; i += AT) W[(int64_t)i * m + j] = -W[(int64_t)i * m + j] / piv;
+    __syncthreads();
+    const int L = m - j - 1;
+    // trailing C[i][t] -= l_i l_t  <=>  W[i][t] += l_i l_t (lower part)
+    for (int64_t e = tid; e < (int64_t)L * L; e += AT) {
+      const int i = j + 1 + (int)(e / L), t = j + 1 + (int)(e % L);
+      if (t <= i) W[(int64_t)i * m + t] += W[(int64_t)i * m + j] * W[(int64_t)t * m + j];
+    }
+    __syncthreads();
+    // keep the diagonal as W (C = tau - W): handled by the lower update (t == i)
+  }
+  if (tid == 0) *pass = s_ok;
+}
+
+}  // namespace
+
+int alg1_default_m(int64_t n) {
+  int64_t m = std::min<int64_t>(500, std::max<int64_t>(100, n / 100));
+  return (int)std::min<int64_t>(m, n);
+}
+
+afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t rng_seed,
+                    int k_threshold, Alg1Result* res, cudaStream_t st) {
+  if (m < 2 || m > 1024 || m > n) {
+    set_error("alg1: need 2 <= m <= min(n, 1024) (m=%d)", m);
+    return AFN_ERR_ARG;
+  }
+  std::vector<void*> tmp;
+  auto get = [&](void** p, size_t bytes) {
+    afn_status s = dalloc(p, bytes, st);
+    if (s == AFN_OK) tmp.push_back(*p);
+    return s;
+  };
+  struct Free {
+    std::vector<void*>* t;
+    cudaStream_t st;
+    ~Free() {
+      for (void* p : *t) dfree(p, st);
+    }
+  } fr{&tmp, st};
+  afn_status s;
+  unsigned long long* keys;
+  long long* cids;
+  unsigned* cnt;
+  int64_t* ids;
+  if ((s = get((void**)&keys, sizeof(unsigned long long) * CAND_CAP)) != AFN_OK) return s;
+  if ((s = get((void**)&cids, sizeof(long long) * CAND_CAP)) != AFN_OK) return s;
+  if ((s = get((void**)&cnt, sizeof(unsigned) * 4)) != AFN_OK) return s;
+  if ((s = get((void**)&ids, sizeof(int64_t) * m)) != AFN_OK) return s;
+
+  // ---- 1. subsample: keys below thr contain the m smallest iff count >= m
+  {
+    long double frac = (long double)std::min<int64_t>(n, 2LL * m + 64) / (long double)n;
+    for (int attempt = 0; attempt < 64; ++attempt) {
+      const long double tl = frac * 18446744073709551616.0L;
+      const uint64_t thr = (frac >= 1.0L || tl >= 18446744073709551615.0L) ? ~0ULL : (uint64_t)tl;
+      AFN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), st));
+      cand_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, rng_seed, thr, keys, cids, cnt);
+      AFN_LAUNCH_CHECK("cand_kernel");
+      unsigned hc = 0;
+      AFN_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      AFN_CUDA(cudaStreamSynchronize(st));
+      if (thr == ~0ULL && hc < (unsigned)m) { set_error("alg1: subsample failed"); return AFN_ERR_CUDA; }
+      if (hc < (unsigned)m) { frac *= 2; continue; }
+      if (hc > (unsigned)CAND_CAP) { frac *= 0.5L; continue; }
+      break;
+    }
+    const int sbytes = (int)(16 * CAND_CAP);
+    AFN_CUDA(cudaFuncSetAttribute(cand_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sbytes));
+    cand_sort_kernel<<<1, AT, sbytes, st>>>(keys, cids, cnt, m, ids);
+    AFN_LAUNCH_CHECK("cand_sort_kernel");
+  }
+  // ---- 2. scaled / unscaled subsample, K_m, FPS order
+  const double scale = std::pow((double)m / (double)n, 1.0 / (double)d);
+  double *Xm, *Xu, *Km, *Kp, *Wk, *dgl, *off, *summ;
+  int64_t* ord;
+  double* fill;
+  int* pass;
+  const size_t mm = (size_t)m * m;
+  if ((s = get((void**)&Xm, sizeof(double) * m * d)) != AFN_OK) return s;
+  if ((s = get((void**)&Xu, sizeof(double) * m * d)) != AFN_OK) return s;
+  if ((s = get((void**)&Km, sizeof(double) * mm)) != AFN_OK) return s;
+  if ((s = get((void**)&Kp, sizeof(double) * mm)) != AFN_OK) return s;
+  if ((s = get((void**)&Wk, sizeof(double) * mm)) != AFN_OK) return s;
+  if ((s = get((void**)&dgl, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&off, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&summ, sizeof(double) * 4)) != AFN_OK) return s;
+  if ((s = get((void**)&ord, sizeof(int64_t) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&fill, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&pass, sizeof(int) * 2)) != AFN_OK) return s;
+  gather_scale_kernel<<<(m * d + 255) / 256, 256, 0, st>>>(X, d, ids, m, scale, Xm, Xu);
+  AFN_LAUNCH_CHECK("gather_scale_kernel");
+  if ((s = gen_k11(Xm, m, d, l, 0.0, Km, st)) != AFN_OK) return s;
+  if ((s = fps_run(Xm, m, d, m, 0, ord, fill, st)) != AFN_OK) return s;
+  permute_sym_kernel<<<(unsigned)((mm + 255) / 256), 256, 0, st>>>(Km, m, ord, Kp);
+  AFN_LAUNCH_CHECK("permute_sym_kernel");
+  // ||K_m||_2 = lambda_max (tridiagonal + bisection)
+  AFN_CUDA(cudaMemcpyAsync(Wk, Km, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
+  tridiag_kernel<<<1, AT, 0, st>>>(Wk, m, dgl, off);
+  AFN_LAUNCH_CHECK("tridiag_kernel");
+  eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
+  AFN_LAUNCH_CHECK("eig_summary_kernel");
+  double hs[2];
+  AFN_CUDA(cudaMemcpyAsync(hs, summ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaStreamSynchronize(st));
+  const double normK = hs[0];
+  const double thr = (double)m * DBL_EPSILON * normK;
+  const double tau = 0.1 * normK;
+
+  // ---- 3. smallest r in [1, m] with ||S^(r)|| < 0.1 ||K_m|| (pass(m) = true)
+  auto test = [&](int r, int* out) -> afn_status {
+    schur_test_kernel<<<1, AT, 0, st>>>(Kp, m, r, thr, tau, Wk, pass);
+    AFN_LAUNCH_CHECK("schur_test_kernel");
+    AFN_CUDA(cudaMemcpyAsync(out, pass, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    return AFN_OK;
+  };
+  int lo = 0, hi = m;  // pass(hi) true, pass(lo) false (lo = 0: no landmarks)
+  while (hi - lo > 1) {
+    const int mid = lo + (hi - lo) / 2;
+    int ok = 0;
+    if ((s = test(mid, &ok)) != AFN_OK) return s;
+    if (ok) hi = mid; else lo = mid;
+  }
+  const int r = hi;
+  int64_t khat = (2LL * r * n + m) / (2LL * m);
+  int refined = 0;
+  // ---- 4. refined branch: #{eig(K_m on unscaled points) > 0.1}
+  if (khat < k_threshold) {
+    if ((s = gen_k11(Xu, m, d, l, 0.0, Wk, st)) != AFN_OK) return s;
+    tridiag_kernel<<<1, AT, 0, st>>>(Wk, m, dgl, off);
+    AFN_LAUNCH_CHECK("tridiag_kernel");
+    eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
+    AFN_LAUNCH_CHECK("eig_summary_kernel");
+    AFN_CUDA(cudaMemcpyAsync(hs, summ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    khat = (int64_t)hs[1];
+    refined = 1;
+  }
+  res->khat = khat;
+  res->r = r;
+  res->m = m;
+  res->refined = refined;
+  res->scale = scale;
+  return AFN_OK;
+}
+
+}  // namespace afn

@@ -1,0 +1,268 @@
+// blas.cu -- bandwidth-bound pieces of the AFN apply and
+// the PCG vector updates (L788): GEMV with W = K21 L^{-T} and L^{-T}, CSR SpMV
+// with G and G^T, deterministic dot products.  All reductions have a fixed
+// order (warp butterflies, per-block partials summed in block order) so a
+// solve is bit-reproducible.
+#include <algorithm>
+#include <cmath>
+
+#include "afn_common.cuh"
+#include "afn_internal.h"
+
+namespace afn {
+namespace {
+
+constexpr int VT = 256;
+constexpr int DOT_BLOCKS = 296;  // fixed -> deterministic partial layout
+
+// y[r] = ybase[r] + alpha * A[r,:] x   (one warp per row)
+__global__ void __launch_bounds__(VT) gemv_n_kernel(const double* __restrict__ A, int64_t R, int64_t C,
+                                                   const double* __restrict__ x,
+                                                   const double* __restrict__ ybase, double alpha,
+                                                   double* __restrict__ y) {
+  const int64_t r = (int64_t)blockIdx.x * (VT / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= R) return;
+  const double* a = A + r * C;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int64_t c = lane;
+  for (; c + 96 < C; c += 128) {
+    s0 = fma(__ldcs(&a[c]), __ldg(&x[c]), s0);
+    s1 = fma(__ldcs(&a[c + 32]), __ldg(&x[c + 32]), s1);
+    s2 = fma(__ldcs(&a[c + 64]), __ldg(&x[c + 64]), s2);
+    s3 = fma(__ldcs(&a[c + 96]), __ldg(&x[c + 96]), s3);
+  }
+  for (; c < C; c += 32) s0 = fma(__ldcs(&a[c]), __ldg(&x[c]), s0);
+  double s = warp_sum((s0 + s1) + (s2 + s3));
+  if (lane == 0) y[r] = (ybase ? ybase[r] : 0.0) + alpha * s;
+}
+
+// partial[b, c] = sum_{r in block b} A[r, c] x[r]
+__global__ void __launch_bounds__(VT) gemv_t_partial_kernel(const double* __restrict__ A, int64_t R,
+                                                           int64_t C, int64_t rows_per_block,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ part) {
+  extern __shared__ double sx[];
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r1 = min(R, r0 + rows_per_block);
+  const int nr = (int)(r1 - r0);
+  for (int t = threadIdx.x; t < nr; t += VT) sx[t] = x[r0 + t];
+  __syncthreads();
+  for (int64_t c = threadIdx.x; c < C; c += VT) {
+    const double* a = A + r0 * C + c;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int t = 0;
+    for (; t + 3 < nr; t += 4) {
+      s0 = fma(__ldcs(&a[(int64_t)t * C]), sx[t], s0);
+      s1 = fma(__ldcs(&a[(int64_t)(t + 1) * C]), sx[t + 1], s1);
+      s2 = fma(__ldcs(&a[(int64_t)(t + 2) * C]), sx[t + 2], s2);
+      s3 = fma(__ldcs(&a[(int64_t)(t + 3) * C]), sx[t + 3], s3);
+    }
+    for (; t < nr; ++t) s0 = fma(__ldcs(&a[(int64_t)t * C]), sx[t], s0);
+    part[(int64_t)blockIdx.x * C + c] = (s0 + s1) + (s2 + s3);
+  }
+}
+
+__global__ void gemv_t_reduce_kernel(const double* __restrict__ part, int nb, int64_t C,
+                                     const double* __restrict__ ybase, double alpha,
+                                     double* __restrict__ y) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * C + c];
+  y[c] = (ybase ? ybase[c] : 0.0) + alpha * s;
+}
+
+__global__ void __launch_bounds__(VT) spmv_kernel(const int64_t* __restrict__ rp,
+                                                 const int32_t* __restrict__ col,
+                                                 const double* __restrict__ val, int64_t N,
+                                                 const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t r = (int64_t)blockIdx.x * (VT / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= N) return;
+  double s = 0.0;
+  for (int64_t e = rp[r] + lane; e < rp[r + 1]; e += 32) s = fma(val[e], __ldg(&x[col[e]]), s);
+  s = warp_sum(s);
+  if (lane == 0) y[r] = s;
+}
+
+__global__ void gather_vec_kernel(const double* __restrict__ x, const int64_t* __restrict__ perm,
+                                  int64_t n, double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = x[perm[i]];
+}
+__global__ void scatter_vec_kernel(const double* __restrict__ x, const int64_t* __restrict__ perm,
+                                   int64_t n, double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[perm[i]] = x[i];
+}
+
+// last-block-done deterministic finish: partials in block order
+__device__ void finish_sum(double partial, double* ws, unsigned* cnt, double* out) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    ws[blockIdx.x] = partial;
+    __threadfence();
+    const unsigned t = atomicAdd(cnt, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += __ldcg(&ws[b]);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *cnt = 0u;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(VT) dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                                int64_t n, double* out, double* ws, unsigned* cnt) {
+  __shared__ double sh[VT / 32];
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VT)
+    s = fma(a[i], b[i], s);
+  s = block_sum<VT>(s, sh);
+  finish_sum(s, ws, cnt, out);
+}
+
+__global__ void __launch_bounds__(VT) update_xr_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                      const double* __restrict__ p,
+                                                      const double* __restrict__ q, int64_t n,
+                                                      double* sc, int rz_slot, double* ws,
+                                                      unsigned* cnt) {
+  __shared__ double sh[VT / 32];
+  const double pq = sc[SC_PQ];
+  const double alpha = (pq > 0.0 && isfinite(pq)) ? sc[rz_slot] / pq : 0.0;
+  double s = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VT) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum<VT>(s, sh);
+  finish_sum(s, ws, cnt, &sc[SC_RR]);
+}
+
+__global__ void update_p_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                                const double* sc, int rz_new_slot, int rz_old_slot) {
+  const double beta = sc[rz_new_slot] / sc[rz_old_slot];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = fma(beta, p[i], z[i]);
+}
+
+__global__ void copy_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i];
+}
+__global__ void axpby_kernel(double* __restrict__ y, double a, const double* __restrict__ x, double b,
+                             int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = fma(a, x[i], b * y[i]);
+}
+
+unsigned grid_for(int64_t n, int nt, int cap) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(cap, (n + nt - 1) / nt));
+}
+
+int64_t gemv_t_rows_per_block(int64_t R) {
+  const int64_t target = 4 * (int64_t)num_sms();
+  return std::max<int64_t>(16, (R + target - 1) / target);
+}
+
+}  // namespace
+
+afn_status gemv_n(const double* A, int64_t R, int64_t C, const double* x, const double* ybase,
+                  double alpha, double* y, cudaStream_t st) {
+  if (R <= 0) return AFN_OK;
+  gemv_n_kernel<<<(unsigned)((R + 7) / 8), VT, 0, st>>>(A, R, C, x, ybase, alpha, y);
+  AFN_LAUNCH_CHECK("gemv_n_kernel");
+  return AFN_OK;
+}
+
+int64_t gemv_t_ws(int64_t R, int64_t C) {
+  const int64_t rpb = gemv_t_rows_per_block(R);
+  return ((R + rpb - 1) / rpb) * C + 1;
+}
+
+afn_status gemv_t(const double* A, int64_t R, int64_t C, const double* x, const double* ybase,
+                  double alpha, double* y, double* ws, cudaStream_t st) {
+  if (C <= 0) return AFN_OK;
+  const int64_t rpb = gemv_t_rows_per_block(R);
+  const int nb = (int)((R + rpb - 1) / rpb);
+  if (nb > 0) {
+    gemv_t_partial_kernel<<<nb, VT, sizeof(double) * rpb, st>>>(A, R, C, rpb, x, ws);
+    AFN_LAUNCH_CHECK("gemv_t_partial_kernel");
+  }
+  gemv_t_reduce_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(ws, nb, C, ybase, alpha, y);
+  AFN_LAUNCH_CHECK("gemv_t_reduce_kernel");
+  return AFN_OK;
+}
+
+afn_status spmv_csr(const int64_t* rp, const int32_t* col, const double* val, int64_t N,
+                    const double* x, double* y, cudaStream_t st) {
+  if (N <= 0) return AFN_OK;
+  spmv_kernel<<<(unsigned)((N + 7) / 8), VT, 0, st>>>(rp, col, val, N, x, y);
+  AFN_LAUNCH_CHECK("spmv_kernel");
+  return AFN_OK;
+}
+
+afn_status gather_vec(const double* x, const int64_t* perm, int64_t n, double* y, cudaStream_t st) {
+  if (n <= 0) return AFN_OK;
+  gather_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, perm, n, y);
+  AFN_LAUNCH_CHECK("gather_vec_kernel");
+  return AFN_OK;
+}
+
+afn_status scatter_vec(const double* x, const int64_t* perm, int64_t n, double* y, cudaStream_t st) {
+  if (n <= 0) return AFN_OK;
+  scatter_vec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, perm, n, y);
+  AFN_LAUNCH_CHECK("scatter_vec_kernel");
+  return AFN_OK;
+}
+
+int64_t dot_ws() { return DOT_BLOCKS; }
+
+afn_status dot(const double* a, const double* b, int64_t n, double* out, double* ws, unsigned* cnt,
+               cudaStream_t st) {
+  dot_kernel<<<DOT_BLOCKS, VT, 0, st>>>(a, b, n, out, ws, cnt);
+  AFN_LAUNCH_CHECK("dot_kernel");
+  return AFN_OK;
+}
+
+afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, int64_t n,
+                         double* sc, int rz_slot, double* ws, unsigned* cnt, cudaStream_t st) {
+  update_xr_kernel<<<DOT_BLOCKS, VT, 0, st>>>(x, r, p, q, n, sc, rz_slot, ws, cnt);
+  AFN_LAUNCH_CHECK("update_xr_kernel");
+  return AFN_OK;
+}
+
+afn_status pcg_update_p(double* p, const double* z, int64_t n, const double* sc, int rz_new_slot,
+                        int rz_old_slot, cudaStream_t st) {
+  update_p_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(p, z, n, sc, rz_new_slot, rz_old_slot);
+  AFN_LAUNCH_CHECK("update_p_kernel");
+  return AFN_OK;
+}
+
+afn_status vec_copy(double* y, const double* x, int64_t n, cudaStream_t st) {
+  if (n <= 0) return AFN_OK;
+  copy_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(y, x, n);
+  AFN_LAUNCH_CHECK("copy_kernel");
+  return AFN_OK;
+}
+
+afn_status vec_axpby(double* y, double a, const double* x, double b, int64_t n, cudaStream_t st) {
+  if (n <= 0) return AFN_OK;
+  axpby_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(y, a, x, b, n);
+  AFN_LAUNCH_CHECK("axpby_kernel");
+  return AFN_OK;
+}
+
+}  // namespace afn

@@ -1,0 +1,308 @@
+// fps.cu -- farthest point sampling (eq. (3.3)), the
+// paper's brute-force parallel form (L800: "an O(n) distance update in
+// parallel at each step").
+//
+// One persistent cooperative kernel runs all k dependent steps.  Each thread
+// keeps P points and their running min squared distance `mind` in registers
+// (or, for very large n, streams them from global/L2).  A step is: update mind
+// with the newest landmark, argmax over (mind desc, index asc) by warp
+// shuffles, a shared-memory block reduce, one grid barrier, and a redundant
+// (identical in every CTA) reduce of the G per-CTA winners, whose coordinates
+// travel with them so no dependent load follows the barrier.
+// Bit-exact with the readings R3: squared distances are sums in coordinate
+// order of individually rounded (x_c - y_c)^2; selected points carry mind = -1
+// and are never re-picked; ties go to the lowest index.
+#include <algorithm>
+#include <cmath>
+
+#include "afn_common.cuh"
+#include "afn_internal.h"
+
+namespace afn {
+namespace {
+
+constexpr int FPS_NT = 512;
+
+__device__ __forceinline__ bool better(double d1, long long i1, double d2, long long i2) {
+  return d1 > d2 || (d1 == d2 && i1 < i2);
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// slot layout: [0] = d2, [1] = idx (bits), [2..2+DP) = coordinates
+template <int DP>
+struct Slot {
+  static constexpr int S = DP + 2;
+};
+
+// P > 0: points in registers; P == 0: points streamed from global (mind in gmem).
+template <int DP, int P>
+__global__ void __launch_bounds__(FPS_NT, 1)
+fps_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
+           int64_t* __restrict__ idx_out, double* __restrict__ fill_out, double* slots,
+           unsigned* bar, double* __restrict__ gmind, int pglob) {
+  constexpr int S = Slot<DP>::S;
+  constexpr int NW = FPS_NT / 32;
+  constexpr int PR = P > 0 ? P : 1;
+  __shared__ double s_w[NW][S];
+  __shared__ double s_new[S];
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int G = gridDim.x;
+  const int64_t stride = (int64_t)G * FPS_NT;
+  const int64_t gtid = (int64_t)blockIdx.x * FPS_NT + tid;
+  const int np = P > 0 ? P : pglob;
+
+  double pts[PR][DP];
+  double mind[PR];
+
+  // seed coordinates
+  double y[DP];
+#pragma unroll
+  for (int c = 0; c < DP; ++c) y[c] = c < d ? X[seed * d + c] : 0.0;
+
+  auto load_pt = [&](int64_t i, double* q) {
+#pragma unroll
+    for (int c = 0; c < DP; ++c) q[c] = (c < d) ? X[i * d + c] : 0.0;
+  };
+
+  if (P > 0) {
+#pragma unroll
+    for (int s = 0; s < PR; ++s) {
+      const int64_t i = gtid + s * stride;
+      if (i < n) {
+        load_pt(i, pts[s]);
+        mind[s] = (i == seed) ? -1.0 : d2_exact<DP>(pts[s], y);
+      } else {
+#pragma unroll
+        for (int c = 0; c < DP; ++c) pts[s][c] = 0.0;
+        mind[s] = -2.0;
+      }
+    }
+  } else {
+    for (int s = 0; s < np; ++s) {
+      const int64_t i = gtid + s * stride;
+      if (i < n) {
+        double q[DP];
+        load_pt(i, q);
+        gmind[i] = (i == seed) ? -1.0 : d2_exact<DP>(q, y);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) idx_out[0] = seed;
+
+  for (int64_t step = 1; step <= k; ++step) {
+    // ---- local argmax (indices ascend with s, strict > keeps the lowest)
+    double bd = -3.0;
+    long long bi = 0x7fffffffffffffffLL;
+    double bc[DP];
+#pragma unroll
+    for (int c = 0; c < DP; ++c) bc[c] = 0.0;
+    if (P > 0) {
+#pragma unroll
+      for (int s = 0; s < PR; ++s) {
+        const int64_t i = gtid + s * stride;
+        if (mind[s] > bd) {
+          bd = mind[s];
+          bi = i;
+#pragma unroll
+          for (int c = 0; c < DP; ++c) bc[c] = pts[s][c];
+        }
+      }
+    } else {
+      for (int s = 0; s < np; ++s) {
+        const int64_t i = gtid + s * stride;
+        if (i < n) {
+          const double m = __ldcg(&gmind[i]);
+          if (m > bd) { bd = m; bi = i; }
+        }
+      }
+      if (bi < n) load_pt(bi, bc);
+    }
+    // ---- warp argmax (butterfly: every lane ends with the same winner)
+    double wd = bd;
+    long long wi = bi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, wd, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, wi, o);
+      if (better(od, oi, wd, wi)) { wd = od; wi = oi; }
+    }
+    if (bi == wi && bd == wd) {  // the owning lane (unique: indices are unique)
+      s_w[wid][0] = wd;
+      s_w[wid][1] = __longlong_as_double(wi);
+#pragma unroll
+      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = bc[c];
+    }
+    __syncthreads();
+    double* myslot = slots + ((step & 1) * (int64_t)G + blockIdx.x) * S;
+    if (wid == 0) {
+      double vd = lane < NW ? s_w[lane][0] : -3.0;
+      long long vi = lane < NW ? __double_as_longlong(s_w[lane][1]) : 0x7fffffffffffffffLL;
+      int src = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, vd, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, vi, o);
+        const int os = __shfl_xor_sync(0xffffffffu, src, o);
+        if (better(od, oi, vd, vi)) { vd = od; vi = oi; src = os; }
+      }
+      if (G == 1) {
+        if (lane < S) s_new[lane] = s_w[src][lane];
+      } else {
+        if (lane < S) {
+          myslot[lane] = s_w[src][lane];
+          __threadfence();
+        }
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(bar, 1u);
+          const unsigned target = (unsigned)(G * step);
+          while (ld_acquire(bar) < target) {
+          }
+        }
+        __syncwarp();
+        // reduce the G CTA winners (same order in every CTA -> same result)
+        const double* base = slots + ((step & 1) * (int64_t)G) * S;
+        double gd = -3.0;
+        long long gi = 0x7fffffffffffffffLL;
+        int gsrc = -1;
+        for (int b = lane; b < G; b += 32) {
+          const double od = __ldcg(&base[(int64_t)b * S]);
+          const long long oi = __double_as_longlong(__ldcg(&base[(int64_t)b * S + 1]));
+          if (better(od, oi, gd, gi)) { gd = od; gi = oi; gsrc = b; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double od = __shfl_xor_sync(0xffffffffu, gd, o);
+          const long long oi = __shfl_xor_sync(0xffffffffu, gi, o);
+          const int os = __shfl_xor_sync(0xffffffffu, gsrc, o);
+          if (better(od, oi, gd, gi)) { gd = od; gi = oi; gsrc = os; }
+        }
+        if (lane < S) s_new[lane] = __ldcg(&base[(int64_t)gsrc * S + lane]);
+      }
+    }
+    __syncthreads();
+    const double nd = s_new[0];
+    const long long ni = __double_as_longlong(s_new[1]);
+    if (blockIdx.x == 0 && tid == 0) {
+      fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
+      if (step < k) idx_out[step] = ni;
+    }
+    if (step == k) break;
+#pragma unroll
+    for (int c = 0; c < DP; ++c) y[c] = s_new[2 + c];
+    if (P > 0) {
+#pragma unroll
+      for (int s = 0; s < PR; ++s) {
+        const int64_t i = gtid + s * stride;
+        if (i < n) {
+          const double dd = d2_exact<DP>(pts[s], y);
+          mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
+        }
+      }
+    } else {
+      for (int s = 0; s < np; ++s) {
+        const int64_t i = gtid + s * stride;
+        if (i < n) {
+          double q[DP];
+          load_pt(i, q);
+          const double dd = d2_exact<DP>(q, y);
+          const double m = __ldcg(&gmind[i]);
+          __stcg(&gmind[i], (i == ni) ? -1.0 : fmin(m, dd));
+        }
+      }
+    }
+  }
+}
+
+template <int DP, int P>
+afn_status launch_fps(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
+                      double* fill, int G, double* slots, unsigned* bar, double* gmind, int pglob,
+                      cudaStream_t st) {
+  auto kern = fps_kernel<DP, P>;
+  int occ = 0;
+  AFN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, FPS_NT, 0));
+  if (G > 1 && occ * num_sms() < G) {
+    set_error("fps: grid %d exceeds co-resident capacity %d", G, occ * num_sms());
+    return AFN_ERR_CUDA;
+  }
+  void* args[] = {(void*)&X, (void*)&n, (void*)&d, (void*)&k, (void*)&seed, (void*)&idx,
+                  (void*)&fill, (void*)&slots, (void*)&bar, (void*)&gmind, (void*)&pglob};
+  if (G > 1) {
+    AFN_CUDA(cudaLaunchCooperativeKernel((const void*)kern, dim3(G), dim3(FPS_NT), args, 0, st));
+  } else {
+    kern<<<1, FPS_NT, 0, st>>>(X, n, d, k, seed, idx, fill, slots, bar, gmind, pglob);
+  }
+  AFN_LAUNCH_CHECK("fps_kernel");
+  return AFN_OK;
+}
+
+template <int DP>
+afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
+                          double* fill, cudaStream_t st) {
+  const int sms = num_sms();
+  // choose points per thread P and grid G (G = 1 needs no grid barrier)
+  int P = 0, G = 0, pglob = 0;
+  const int64_t per1 = FPS_NT;
+  if (n <= per1 * 8) {
+    G = 1;
+    P = 1;
+    while ((int64_t)P * per1 < n) P *= 2;
+  } else {
+    const int64_t cap_reg = (int64_t)sms * per1 * 8;
+    if (n <= cap_reg) {
+      P = 1;
+      while ((int64_t)sms * per1 * P < n) P *= 2;
+      G = (int)((n + per1 * P - 1) / (per1 * P));
+    } else {
+      P = 0;
+      G = sms;
+      pglob = (int)((n + (int64_t)G * per1 - 1) / ((int64_t)G * per1));
+    }
+  }
+  double* slots = nullptr;
+  unsigned* bar = nullptr;
+  double* gmind = nullptr;
+  const size_t slot_bytes = sizeof(double) * 2 * (size_t)G * (DP + 2);
+  afn_status s = dalloc((void**)&slots, slot_bytes + 256, st);
+  if (s != AFN_OK) return s;
+  bar = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(slots) + slot_bytes);
+  AFN_CUDA(cudaMemsetAsync(bar, 0, 256, st));
+  if (P == 0) {
+    s = dalloc((void**)&gmind, sizeof(double) * n, st);
+    if (s != AFN_OK) { dfree(slots, st); return s; }
+  }
+  switch (P) {
+    case 0: s = launch_fps<DP, 0>(X, n, d, k, seed, idx, fill, G, slots, bar, gmind, pglob, st); break;
+    case 1: s = launch_fps<DP, 1>(X, n, d, k, seed, idx, fill, G, slots, bar, gmind, pglob, st); break;
+    case 2: s = launch_fps<DP, 2>(X, n, d, k, seed, idx, fill, G, slots, bar, gmind, pglob, st); break;
+    case 4: s = launch_fps<DP, 4>(X, n, d, k, seed, idx, fill, G, slots, bar, gmind, pglob, st); break;
+    default: s = launch_fps<DP, 8>(X, n, d, k, seed, idx, fill, G, slots, bar, gmind, pglob, st); break;
+  }
+  dfree(slots, st);
+  if (gmind) dfree(gmind, st);
+  return s;
+}
+
+}  // namespace
+
+afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
+                   double* fill, cudaStream_t st) {
+  // coordinates are zero-padded to DP: adding +0.0 terms leaves d2 bit-identical
+  if (d <= 1) return fps_dispatch_p<1>(X, n, d, k, seed, idx, fill, st);
+  if (d <= 2) return fps_dispatch_p<2>(X, n, d, k, seed, idx, fill, st);
+  if (d <= 3) return fps_dispatch_p<3>(X, n, d, k, seed, idx, fill, st);
+  if (d <= 4) return fps_dispatch_p<4>(X, n, d, k, seed, idx, fill, st);
+  if (d <= 8) return fps_dispatch_p<8>(X, n, d, k, seed, idx, fill, st);
+  if (d <= 16) return fps_dispatch_p<16>(X, n, d, k, seed, idx, fill, st);
+  set_error("fps: d=%d unsupported (1..16)", d);
+  return AFN_ERR_ARG;
+}
+
+}  // namespace afn

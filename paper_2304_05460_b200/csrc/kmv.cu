@@ -1,0 +1,195 @@
+// kmv.cu -- matrix-free Gaussian kernel matvec y = (K + mu I) v  (PAPER.md
+// L33, L38; the paper's "explicit" dense matvec, L957).  FP64 SIMT, ALU-bound.
+//
+// Layout: the points are pre-scaled once, Xs = X * sqrt(log2 e)/l, so that
+// ||xs_i - xs_j||^2 = log2(e) ||x_i - x_j||^2 / l^2 and K_ij = 2^(-||xs_i-xs_j||^2).
+// Grid (row tiles x column chunks): each thread owns RB rows (registers), a CTA
+// owns NT*RB rows and one column chunk, streamed through shared memory in
+// tiles of TC columns (x_j and v_j interleaved).  Each thread sums its rows
+// over the chunk in column order; a second kernel adds the chunk partials in
+// chunk order plus mu v_i -> bit-identical results run to run and independent
+// of how rows are sharded across GPUs.
+// Per pair (d=3): 3 DADD + 1 DMUL + 2 DFMA (distance) + 10 (exp2) + 1 DFMA = 17
+// FP64-pipe instructions, 28 flops counting an FMA as 2.
+#include <algorithm>
+#include <cmath>
+
+#include "afn_common.cuh"
+#include "afn_internal.h"
+
+namespace afn {
+
+namespace {
+
+constexpr int KMV_NT = 256;
+
+template <int D>
+struct KmvTraits {
+  static constexpr int CS = ((D + 1) + 1) & ~1;   // coords + v, padded to even
+  static constexpr int TC = D <= 8 ? 512 : 256;   // columns per smem tile (<= 40 KB)
+  static constexpr int RB = D <= 4 ? 4 : (D <= 8 ? 2 : 1);  // rows per thread
+};
+
+template <int D, int RB>
+__global__ void __launch_bounds__(KMV_NT, 2)
+kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int64_t n,
+                   int64_t row0, int64_t nrows, int64_t chunk_cols,
+                   double* __restrict__ partial) {
+  constexpr int CS = KmvTraits<D>::CS;
+  constexpr int KMV_TC = KmvTraits<D>::TC;
+  __shared__ double s_tab[16];
+  __shared__ __align__(16) double s_col[KMV_TC * CS];
+  load_exp2_tab(s_tab);
+
+  const int64_t rbase = row0 + (int64_t)blockIdx.x * (KMV_NT * RB) + threadIdx.x;
+  const int64_t rend = row0 + nrows;
+  double xi[RB][D];
+  double acc[RB];
+#pragma unroll
+  for (int t = 0; t < RB; ++t) {
+    int64_t r = rbase + (int64_t)t * KMV_NT;
+    r = r < rend ? r : row0;  // clamp (masked at the write)
+#pragma unroll
+    for (int c = 0; c < D; ++c) xi[t][c] = Xs[r * D + c];
+    acc[t] = 0.0;
+  }
+
+  const int64_t c0 = (int64_t)blockIdx.y * chunk_cols;
+  const int64_t c1 = min(n, c0 + chunk_cols);
+  for (int64_t tb = c0; tb < c1; tb += KMV_TC) {
+    const int tcn = (int)min((int64_t)KMV_TC, c1 - tb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < KMV_TC * CS; e += KMV_NT) {
+      const int j = e / CS, c = e - j * CS;
+      double val = 0.0;
+      if (j < tcn) {
+        if (c < D) val = Xs[(tb + j) * D + c];
+        else if (c == D) val = v[tb + j];
+      }
+      s_col[e] = val;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int j = 0; j < tcn; ++j) {
+      double xj[CS];
+#pragma unroll
+      for (int c = 0; c < CS; c += 2) {
+        const double2 q = *reinterpret_cast<const double2*>(&s_col[j * CS + c]);
+        xj[c] = q.x;
+        xj[c + 1] = q.y;
+      }
+      const double vj = xj[D];
+#pragma unroll
+      for (int t = 0; t < RB; ++t) {
+        double dd = xi[t][0] - xj[0];
+        double s = dd * dd;
+#pragma unroll
+        for (int c = 1; c < D; ++c) {
+          dd = xi[t][c] - xj[c];
+          s = fma(dd, dd, s);
+        }
+        acc[t] = fma(exp2_neg(s, s_tab), vj, acc[t]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < RB; ++t) {
+    const int64_t r = rbase + (int64_t)t * KMV_NT;
+    if (r < rend) partial[(int64_t)blockIdx.y * nrows + (r - row0)] = acc[t];
+  }
+}
+
+__global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, int64_t nrows,
+                                  const double* __restrict__ v, int64_t row0, double mu,
+                                  double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += partial[(int64_t)c * nrows + i];
+  y[i] = fma(mu, v[row0 + i], s);
+}
+
+__global__ void prescale_kernel(const double* __restrict__ X, int64_t n, int d, double f,
+                                double* __restrict__ Xs) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n * d) Xs[e] = X[e] * f;
+}
+
+template <int D>
+void launch_partial(int64_t row_tiles_unused, const KmvPlan& p, cudaStream_t st, const double* Xs,
+                    const double* v, int64_t n, int64_t row0, int64_t nrows, double* partial) {
+  (void)row_tiles_unused;
+  constexpr int RB = KmvTraits<D>::RB;
+  const int64_t rows_per_cta = (int64_t)KMV_NT * RB;
+  dim3 grid((unsigned)((nrows + rows_per_cta - 1) / rows_per_cta), (unsigned)p.chunks);
+  kmv_partial_kernel<D, RB><<<grid, KMV_NT, 0, st>>>(Xs, v, n, row0, nrows, p.chunk_cols, partial);
+}
+
+int rows_per_thread(int d) { return d <= 4 ? 4 : (d <= 8 ? 2 : 1); }
+
+}  // namespace
+
+KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
+  KmvPlan p;
+  const int64_t rows_per_cta = (int64_t)KMV_NT * rows_per_thread(d);
+  p.row_tiles = (nrows + rows_per_cta - 1) / rows_per_cta;
+  const int64_t slots = (int64_t)num_sms * 2;  // 2 CTAs/SM (launch bounds)
+  // enough CTAs for >= 4 waves, chunk >= 256 columns, minimal wave quantisation
+  int64_t best_chunks = 1;
+  double best_cost = 1e300;
+  const int64_t cmax = std::max<int64_t>(1, (n + 255) / 256);
+  const int64_t cmin = std::min<int64_t>(cmax, std::max<int64_t>(1, (4 * slots + p.row_tiles - 1) / p.row_tiles));
+  for (int64_t ch = cmin; ch <= std::min(cmax, cmin + 64); ++ch) {
+    const int64_t cc = (n + ch - 1) / ch;
+    const int64_t nch = (n + cc - 1) / cc;
+    const int64_t ctas = p.row_tiles * nch;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    // cost ~ waves * work per CTA (columns), plus a small per-chunk reduce cost
+    const double cost = (double)waves * (double)cc + 0.02 * (double)nch * (double)rows_per_cta;
+    if (cost < best_cost) { best_cost = cost; best_chunks = nch; }
+  }
+  p.chunk_cols = (n + best_chunks - 1) / best_chunks;
+  p.chunks = (n + p.chunk_cols - 1) / p.chunk_cols;
+  return p;
+}
+
+afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs, cudaStream_t st) {
+  const double f = AFN_SQRT_LOG2E / l;
+  const int64_t total = n * (int64_t)d;
+  const int nt = 256;
+  prescale_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(X, n, d, f, Xs);
+  AFN_LAUNCH_CHECK("prescale_kernel");
+  return AFN_OK;
+}
+
+afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, int64_t row0,
+                      int64_t nrows, double* y, double* partial, const KmvPlan& p, cudaStream_t st) {
+  if (nrows <= 0) return AFN_OK;
+  switch (d) {
+    case 1: launch_partial<1>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 2: launch_partial<2>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 3: launch_partial<3>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 4: launch_partial<4>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 5: launch_partial<5>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 6: launch_partial<6>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 7: launch_partial<7>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 8: launch_partial<8>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 9: launch_partial<9>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 10: launch_partial<10>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 11: launch_partial<11>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 12: launch_partial<12>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 13: launch_partial<13>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 14: launch_partial<14>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 15: launch_partial<15>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 16: launch_partial<16>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    default: set_error("kernel_matvec: d=%d unsupported (1..16)", d); return AFN_ERR_ARG;
+  }
+  AFN_LAUNCH_CHECK("kmv_partial_kernel");
+  const int nt = 256;
+  kmv_reduce_kernel<<<(unsigned)((nrows + nt - 1) / nt), nt, 0, st>>>(partial, (int)p.chunks, nrows,
+                                                                     v, row0, mu, y);
+  AFN_LAUNCH_CHECK("kmv_reduce_kernel");
+  return AFN_OK;
+}
+
+}  // namespace afn
