@@ -172,6 +172,8 @@ void afn_destroy(afn_handle h);
 /* Measurement helpers (bench.py): FP64 FMA peak probe.  Runs `iters` DFMA   */
 /* chains on every SM and returns achieved FP64 TFLOP/s (FMA = 2). [sync]    */
 afn_status afn_probe_dfma(int64_t iters, double* tflops /*host*/, void* stream);
+/* Same for FP64 tensor-core DMMA (mma.sync m8n8k4 f64).                      */
+afn_status afn_probe_dmma(int64_t iters, double* tflops /*host*/, void* stream);
 
 /* Number of kernels this library launched since load (its own kernels only). */
 int64_t afn_launch_count(void);

@@ -86,6 +86,7 @@ _sig = {
     "afn_copy_out": (C.c_int, [_P, C.c_int32, _P, C.c_size_t]),
     "afn_destroy": (None, [_P]),
     "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
+    "afn_probe_dmma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_launch_count": (C.c_int64, []),
     "afn_last_error": (C.c_char_p, []),
     "afn_abi_version": (C.c_int32, []),
@@ -286,6 +287,12 @@ def afn_solve_host(X, b, params: Params, tol=1e-4, maxit=500, stream=None):
                                int(maxit), C.byref(inf), C.byref(rep), _stream(stream)),
            "afn_solve_host")
     return a, inf.as_dict(), rep.as_dict()
+
+
+def probe_dmma(iters=1 << 14, stream=None) -> float:
+    out = C.c_double()
+    _check(_lib.afn_probe_dmma(int(iters), C.byref(out), _stream(stream)), "afn_probe_dmma")
+    return out.value
 
 
 def probe_dfma(iters=1 << 16, stream=None) -> float:

@@ -210,12 +210,24 @@ struct afn_handle_s {
   double* sc = nullptr;
   double* dws = nullptr;
   unsigned* dcnt = nullptr;
-  double* h_sc = nullptr;  // pinned host mirror of sc
+  double* h_sc = nullptr;  // pinned host mirror of sc (per host thread, not owned)
   std::vector<void*> allocs;
   double ms[8] = {0};
 };
 
 namespace {
+
+// one small pinned buffer per host thread (PCG scalars), allocated once
+double* pinned_scalars() {
+  static thread_local double* buf = nullptr;
+  if (!buf) {
+    if (cudaMallocHost((void**)&buf, sizeof(double) * 64) != cudaSuccess) {
+      cudaGetLastError();
+      buf = nullptr;
+    }
+  }
+  return buf;
+}
 
 afn_status halloc(afn_handle h, void** p, size_t bytes, cudaStream_t st) {
   afn_status s = dalloc(p, bytes, st);
@@ -229,8 +241,11 @@ void handle_free(afn_handle h) {
   cudaGetDevice(&cur);
   cudaSetDevice(h->device);
   cudaDeviceSynchronize();
-  for (void* p : h->allocs) cudaFree(p);
-  if (h->h_sc) cudaFreeHost(h->h_sc);
+  // return the blocks to the stream-ordered pool (cudaFree would unmap them and
+  // force the next build to map fresh pages); the legacy stream orders the
+  // frees after all prior work on the device's blocking streams
+  for (void* p : h->allocs) cudaFreeAsync(p, 0);
+  cudaStreamSynchronize(0);
   cudaSetDevice(cur);
   delete h;
 }
@@ -452,7 +467,9 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   const double* X2 = h->Xp + k * d;
   // ---- a5: W = K21 L^{-T}
   TRY(halloc(h, (void**)&h->W, sizeof(double) * (size_t)(N2 > 0 ? N2 : 1) * k, st));
-  TRY(trsm_w(h->L, k, h->Xp, X2, N2, d, P.l, h->W, st));
+  static const bool w_trsm = getenv("AFN_W_TRSM") != nullptr;
+  if (w_trsm) TRY(trsm_w(h->L, k, h->Xp, X2, N2, d, P.l, h->W, st));
+  else TRY(w_gemm(h->LinvT, k, h->Xp, X2, N2, d, P.l, h->W, st));
   AFN_CUDA(cudaEventRecord(ev[4], st));
 
   // ---- a6: kNN pattern
@@ -509,7 +526,11 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   TRY(halloc(h, (void**)&h->dcnt, sizeof(unsigned) * 4, st));
   AFN_CUDA(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned) * 4, st));
   AFN_CUDA(cudaMemsetAsync(h->sc, 0, sizeof(double) * SC_N, st));
-  AFN_CUDA(cudaMallocHost((void**)&h->h_sc, sizeof(double) * SC_N));
+  h->h_sc = pinned_scalars();
+  if (!h->h_sc) {
+    set_error("pinned host allocation failed");
+    return AFN_ERR_NOMEM;
+  }
   AFN_CUDA(cudaEventRecord(ev[7], st));
   AFN_CUDA(cudaStreamSynchronize(st));
   {
@@ -561,6 +582,11 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   const int d = h->d;
   afn_solve_report R{};
   if (rep) R.history = rep->history;
+  double* hsc = pinned_scalars();
+  if (!hsc) {
+    set_error("pinned host allocation failed");
+    return AFN_ERR_NOMEM;
+  }
   cudaEvent_t e0, e1, km0, km1, ap0, ap1;
   AFN_CUDA(cudaEventCreate(&e0));
   AFN_CUDA(cudaEventCreate(&e1));
@@ -581,9 +607,9 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   TRY(gather_vec(b, h->perm, n, h->r, st));
   AFN_CUDA(cudaMemsetAsync(h->x, 0, sizeof(double) * n, st));
   TRY(dot(h->r, h->r, n, h->sc + SC_BB, h->dws, h->dcnt, st));
-  AFN_CUDA(cudaMemcpyAsync(h->h_sc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaMemcpyAsync(hsc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaStreamSynchronize(st));
-  const double nb = std::sqrt(h->h_sc[SC_BB]);
+  const double nb = std::sqrt(hsc[SC_BB]);
   if (R.history) R.history[0] = nb > 0 ? 1.0 : 0.0;
   int it = 0;
   double rel = nb > 0 ? 1.0 : 0.0;
@@ -602,20 +628,20 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
       AFN_CUDA(cudaEventRecord(km1, st));
       TRY(dot(h->p, h->q, n, h->sc + SC_PQ, h->dws, h->dcnt, st));
       TRY(pcg_update_xr(h->x, h->r, h->p, h->q, n, h->sc, cur, h->dws, h->dcnt, st));
-      AFN_CUDA(cudaMemcpyAsync(h->h_sc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
+      AFN_CUDA(cudaMemcpyAsync(hsc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
       AFN_CUDA(cudaStreamSynchronize(st));
       mv_ms += ev_ms(km0, km1);
       if (ap_pending) {
         ap_ms += ev_ms(ap0, ap1);
         ap_pending = false;
       }
-      const double pq = h->h_sc[SC_PQ];
-      if (!(pq > 0.0) || !std::isfinite(pq) || !std::isfinite(h->h_sc[SC_RR])) {
+      const double pq = hsc[SC_PQ];
+      if (!(pq > 0.0) || !std::isfinite(pq) || !std::isfinite(hsc[SC_RR])) {
         R.breakdown = 1;
         --it;
         break;
       }
-      rel = std::sqrt(h->h_sc[SC_RR]) / nb;
+      rel = std::sqrt(hsc[SC_RR]) / nb;
       if (R.history) R.history[it] = rel;
       if (fixed_iters > 0) {
         if (it >= fixed_iters) {
@@ -648,12 +674,12 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     TRY(gather_vec(b, h->perm, n, h->z, st));
     TRY(vec_axpby(h->z, -1.0, h->q, 1.0, n, st));
     TRY(dot(h->z, h->z, n, h->sc + SC_TMP, h->dws, h->dcnt, st));
-    AFN_CUDA(cudaMemcpyAsync(h->h_sc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaMemcpyAsync(hsc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
   }
   AFN_CUDA(cudaStreamSynchronize(st));
   R.iterations = it;
   R.relres = rel;
-  R.relres_true = nb > 0 ? std::sqrt(h->h_sc[SC_TMP]) / nb : 0.0;
+  R.relres_true = nb > 0 ? std::sqrt(hsc[SC_TMP]) / nb : 0.0;
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   R.solve_ms = ms;
@@ -736,6 +762,11 @@ afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes) {
 }
 
 void afn_destroy(afn_handle h) { handle_free(h); }
+
+afn_status afn_probe_dmma(int64_t iters, double* tflops, void* stream) {
+  REQ(iters >= 8 && tflops, "bad arguments");
+  return probe_dmma(iters, tflops, (cudaStream_t)stream);
+}
 
 afn_status afn_probe_dfma(int64_t iters, double* tflops, void* stream) {
   REQ(iters >= 8 && tflops, "bad arguments");

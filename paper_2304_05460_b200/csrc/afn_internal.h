@@ -47,6 +47,9 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st);
 // W (N x k row-major) = K(Xr, X1) L^{-T}  (i.e. L W^T = K12), K tiles on the fly
 afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   double l, double* W, cudaStream_t st);
+// W (N x k) = K(Xr, X1) L^{-T} as a GEMM with the explicit L^{-T}
+afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
+                  double l, double* W, cudaStream_t st);
 // LinvT (k x k row-major) = L^{-T} (upper triangular)
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st);
 
@@ -99,5 +102,6 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
 
 // ---- probes (probe.cu) -----------------------------------------------------
 afn_status probe_dfma(int64_t iters, double* tflops, cudaStream_t st);
+afn_status probe_dmma(int64_t iters, double* tflops, cudaStream_t st);
 
 }  // namespace afn

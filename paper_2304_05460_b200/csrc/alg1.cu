@@ -116,13 +116,20 @@ __device__ double block_sum_1024(double v, double* sh) {
 }
 
 // Householder tridiagonalisation of the symmetric m x m A (destroyed);
-// diag -> dgl[0..m), offdiag -> off[0..m-1)
-__global__ void __launch_bounds__(AT) tridiag_kernel(double* A, int m, double* dgl, double* off) {
-  __shared__ double v[1024];
-  __shared__ double p[1024];
+// diag -> dgl[0..m), offdiag -> off[0..m-1).  SM: A copied into shared memory.
+template <bool SM>
+__global__ void __launch_bounds__(AT) tridiag_kernel(double* Ag, int m, double* dgl, double* off) {
+  extern __shared__ double dsm[];
   __shared__ double sh[32];
   __shared__ double s_beta, s_alpha;
+  double* A = SM ? dsm : Ag;
+  double* v = SM ? dsm + (size_t)m * m : dsm;
+  double* p = v + m;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (SM) {
+    for (int64_t e = tid; e < (int64_t)m * m; e += AT) A[e] = Ag[e];
+    __syncthreads();
+  }
   for (int j = 0; j + 2 < m; ++j) {
     const int L = m - j - 1;  // length of the column below the diagonal
     double loc = 0.0;
@@ -198,31 +205,55 @@ __device__ int sturm_count(const double* dgl, const double* off, int m, double x
   return c;
 }
 
-// out[0] = lambda_max (bisection), out[1] = #{lambda > x_count}
+// out[0] = lambda_max (32-way multisection), out[1] = #{lambda >= x_count}
 __global__ void eig_summary_kernel(const double* dgl, const double* off, int m, double x_count,
                                    double* out) {
-  if (threadIdx.x != 0) return;
-  double lo = DBL_MAX, hi = -DBL_MAX;
-  for (int i = 0; i < m; ++i) {
-    const double r = (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < m ? fabs(off[i]) : 0.0);
-    lo = fmin(lo, dgl[i] - r);
-    hi = fmax(hi, dgl[i] + r);
+  __shared__ double s_lo, s_hi;
+  const int lane = threadIdx.x;  // 32 threads
+  if (lane == 0) {
+    double lo = DBL_MAX, hi = -DBL_MAX;
+    for (int i = 0; i < m; ++i) {
+      const double r = (i > 0 ? fabs(off[i - 1]) : 0.0) + (i + 1 < m ? fabs(off[i]) : 0.0);
+      lo = fmin(lo, dgl[i] - r);
+      hi = fmax(hi, dgl[i] + r);
+    }
+    s_lo = lo;
+    s_hi = hi;
   }
-  for (int it = 0; it < 200 && hi > lo; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    if (mid <= lo || mid >= hi) break;
-    if (sturm_count(dgl, off, m, mid) == m) hi = mid; else lo = mid;
+  __syncwarp();
+  double lo = s_lo, hi = s_hi;
+  for (int it = 0; it < 40; ++it) {
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+    const bool all_below = sturm_count(dgl, off, m, x) == m;  // lambda_max < x
+    const unsigned bal = __ballot_sync(0xffffffffu, all_below);
+    double nlo = lo, nhi = hi;
+    if (bal) {
+      const int t = __ffs(bal) - 1;  // first probe above lambda_max
+      nhi = lo + (hi - lo) * (double)(t + 1) / 33.0;
+      nlo = t > 0 ? lo + (hi - lo) * (double)t / 33.0 : lo;
+    } else {
+      nlo = lo + (hi - lo) * 32.0 / 33.0;
+    }
+    if (!(nhi - nlo < hi - lo)) break;
+    lo = nlo;
+    hi = nhi;
   }
-  out[0] = hi;
-  out[1] = (double)(m - sturm_count(dgl, off, m, x_count));
+  if (lane == 0) {
+    out[0] = hi;
+    out[1] = (double)(m - sturm_count(dgl, off, m, x_count));
+  }
 }
 
 // pass = [ tau I - S^(r) is positive definite ], S^(r) the Schur complement of
-// Kp after r threshold-pivoted elimination steps.  W: m x m scratch.
+// Kp after r threshold-pivoted elimination steps.  SM: work matrix in shared
+// memory, else in the m x m global scratch Wg.
+template <bool SM>
 __global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict__ Kp, int m, int r,
-                                                        double thr, double tau, double* W, int* pass) {
+                                                        double thr, double tau, double* Wg, int* pass) {
+  extern __shared__ double dsm[];
   __shared__ double s_piv;
   __shared__ int s_ok;
+  double* W = SM ? dsm : Wg;
   const int tid = threadIdx.x;
   for (int64_t e = tid; e < (int64_t)m * m; e += AT) W[e] = Kp[e];
   if (tid == 0) s_ok = 1;
@@ -230,14 +261,14 @@ __global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict
   for (int j = 0; j < r; ++j) {
     const double pj = W[(int64_t)j * m + j];
     if (!(pj > thr)) continue;  // exhausted column (uniform across the CTA)
-    const int L = m - j - 1;
-    for (int64_t e = tid; e < (int64_t)L * L; e += AT) {
-      const int i = j + 1 + (int)(e / L), t = j + 1 + (int)(e % L);
-      W[(int64_t)i * m + t] -= (W[(int64_t)i * m + j] * W[(int64_t)j * m + t]) / pj;
+    for (int i = j + 1 + (tid >> 5); i < m; i += AT / 32) {
+      const double wij = W[(int64_t)i * m + j];
+      for (int t = j + 1 + (tid & 31); t < m; t += 32)
+        W[(int64_t)i * m + t] -= (wij * W[(int64_t)j * m + t]) / pj;
     }
     __syncthreads();
   }
-  // Cholesky of tau I - W[r:, r:]
+  // Cholesky of C = tau I - W[r:, r:] (stored in place: W[i][j] <- l_ij below the diagonal)
   for (int j = r; j < m; ++j) {
     if (tid == 0) {
       const double c = tau - W[(int64_t)j * m + j];
@@ -247,22 +278,40 @@ __global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict
     __syncthreads();
     if (!s_ok) break;
     const double piv = s_piv;
-    // column j below the diagonal of C = tau I - W: C[i][j] = -W[i][j]
     for (int i = j + 1 + tid; i < m; i += AT) W[(int64_t)i * m + j] = -W[(int64_t)i * m + j] / piv;
     __syncthreads();
-    const int L = m - j - 1;
-    // trailing C[i][t] -= l_i l_t  <=>  W[i][t] += l_i l_t (lower part)
-    for (int64_t e = tid; e < (int64_t)L * L; e += AT) {
-      const int i = j + 1 + (int)(e / L), t = j + 1 + (int)(e % L);
-      if (t <= i) W[(int64_t)i * m + t] += W[(int64_t)i * m + j] * W[(int64_t)t * m + j];
+    // C[i][t] -= l_i l_t  <=>  W[i][t] += l_i l_t  (lower part, incl. the diagonal)
+    for (int i = j + 1 + (tid >> 5); i < m; i += AT / 32) {
+      const double li = W[(int64_t)i * m + j];
+      for (int t = j + 1 + (tid & 31); t <= i; t += 32)
+        W[(int64_t)i * m + t] += li * W[(int64_t)t * m + j];
     }
     __syncthreads();
-    // keep the diagonal as W (C = tau - W): handled by the lower update (t == i)
   }
   if (tid == 0) *pass = s_ok;
 }
 
+constexpr int SM_MAX_M = 164;  // (m^2 + 2m) doubles of dynamic smem <= 227 KB
+
 }  // namespace
+
+#define TRY_A(x)                  \
+  do {                            \
+    afn_status s_ = (x);          \
+    if (s_ != AFN_OK) return s_;  \
+  } while (0)
+
+afn_status launch_tridiag(double* A, int m, double* dgl, double* off, cudaStream_t st) {
+  if (m <= SM_MAX_M) {
+    const size_t bytes = sizeof(double) * ((size_t)m * m + 2 * (size_t)m);
+    AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    tridiag_kernel<true><<<1, AT, bytes, st>>>(A, m, dgl, off);
+  } else {
+    tridiag_kernel<false><<<1, AT, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
+  }
+  AFN_LAUNCH_CHECK("tridiag_kernel");
+  return AFN_OK;
+}
 
 int alg1_default_m(int64_t n) {
   int64_t m = std::min<int64_t>(500, std::max<int64_t>(100, n / 100));
@@ -346,8 +395,7 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
   AFN_LAUNCH_CHECK("permute_sym_kernel");
   // ||K_m||_2 = lambda_max (tridiagonal + bisection)
   AFN_CUDA(cudaMemcpyAsync(Wk, Km, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
-  tridiag_kernel<<<1, AT, 0, st>>>(Wk, m, dgl, off);
-  AFN_LAUNCH_CHECK("tridiag_kernel");
+  TRY_A(launch_tridiag(Wk, m, dgl, off, st));
   eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
   AFN_LAUNCH_CHECK("eig_summary_kernel");
   double hs[2];
@@ -359,7 +407,13 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
 
   // ---- 3. smallest r in [1, m] with ||S^(r)|| < 0.1 ||K_m|| (pass(m) = true)
   auto test = [&](int r, int* out) -> afn_status {
-    schur_test_kernel<<<1, AT, 0, st>>>(Kp, m, r, thr, tau, Wk, pass);
+    if (m <= SM_MAX_M) {
+      const size_t bytes = sizeof(double) * (size_t)m * m;
+      AFN_CUDA(cudaFuncSetAttribute(schur_test_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      schur_test_kernel<true><<<1, AT, bytes, st>>>(Kp, m, r, thr, tau, Wk, pass);
+    } else {
+      schur_test_kernel<false><<<1, AT, 0, st>>>(Kp, m, r, thr, tau, Wk, pass);
+    }
     AFN_LAUNCH_CHECK("schur_test_kernel");
     AFN_CUDA(cudaMemcpyAsync(out, pass, sizeof(int), cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
@@ -378,8 +432,7 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
   // ---- 4. refined branch: #{eig(K_m on unscaled points) > 0.1}
   if (khat < k_threshold) {
     if ((s = gen_k11(Xu, m, d, l, 0.0, Wk, st)) != AFN_OK) return s;
-    tridiag_kernel<<<1, AT, 0, st>>>(Wk, m, dgl, off);
-    AFN_LAUNCH_CHECK("tridiag_kernel");
+    TRY_A(launch_tridiag(Wk, m, dgl, off, st));
     eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
     AFN_LAUNCH_CHECK("eig_summary_kernel");
     AFN_CUDA(cudaMemcpyAsync(hs, summ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));

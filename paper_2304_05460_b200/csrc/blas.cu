@@ -63,14 +63,25 @@ __global__ void __launch_bounds__(VT) gemv_t_partial_kernel(const double* __rest
   }
 }
 
-__global__ void gemv_t_reduce_kernel(const double* __restrict__ part, int nb, int64_t C,
-                                     const double* __restrict__ ybase, double alpha,
-                                     double* __restrict__ y) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+// y[c] = ybase[c] + alpha * sum_b part[b, c]; 32 columns x 8 partial lanes per
+// block, fixed combination order (deterministic)
+__global__ void __launch_bounds__(256) gemv_t_reduce_kernel(const double* __restrict__ part, int nb,
+                                                           int64_t C, const double* __restrict__ ybase,
+                                                           double alpha, double* __restrict__ y) {
+  __shared__ double sh[8][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   double s = 0.0;
-  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * C + c];
-  y[c] = (ybase ? ybase[c] : 0.0) + alpha * s;
+  if (c < C)
+    for (int b = w; b < nb; b += 8) s += part[(int64_t)b * C + c];
+  sh[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < C) {
+    double t = sh[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += sh[q][lane];
+    y[c] = (ybase ? ybase[c] : 0.0) + alpha * t;
+  }
 }
 
 __global__ void __launch_bounds__(VT) spmv_kernel(const int64_t* __restrict__ rp,
@@ -201,7 +212,7 @@ afn_status gemv_t(const double* A, int64_t R, int64_t C, const double* x, const 
     gemv_t_partial_kernel<<<nb, VT, sizeof(double) * rpb, st>>>(A, R, C, rpb, x, ws);
     AFN_LAUNCH_CHECK("gemv_t_partial_kernel");
   }
-  gemv_t_reduce_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(ws, nb, C, ybase, alpha, y);
+  gemv_t_reduce_kernel<<<(unsigned)((C + 31) / 32), 256, 0, st>>>(ws, nb, C, ybase, alpha, y);
   AFN_LAUNCH_CHECK("gemv_t_reduce_kernel");
   return AFN_OK;
 }

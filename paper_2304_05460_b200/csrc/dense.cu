@@ -34,7 +34,7 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t n, int 
 // A = K(X1, X1) + mu I  (full)
 __global__ void gen_k11_kernel(const double* __restrict__ X1, int64_t k, int d, double cl,
                                double mu, double* __restrict__ A) {
-  __shared__ double s_tab[16];
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
   load_exp2_tab(s_tab);
   __syncthreads();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -57,25 +57,27 @@ __global__ void gen_k11_kernel(const double* __restrict__ X1, int64_t k, int d, 
 __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
   const int tid = threadIdx.x;
   const int r = tid >> 2, q = tid & 3;
+  const int lane = tid & 31;
   double a[16];
 #pragma unroll
   for (int s = 0; s < 16; ++s) a[s] = T[r * TP + q + 4 * s];
-#pragma unroll 1
-  for (int j = 0; j < NB; ++j) {
-    const int owner = j & 3;
-    double xj = 0.0;
-    // owner computes x_j
+  // column-cyclic ownership: thread q owns columns q + 4s.  Step j = 4*s + q'.
 #pragma unroll
-    for (int s = 0; s < 16; ++s)
-      if (q == owner && (q + 4 * s) == j) a[s] = a[s] / Lbb[j * TP + j];
+  for (int s = 0; s < 16; ++s) {
 #pragma unroll
-    for (int s = 0; s < 16; ++s)
-      if ((q + 4 * s) == j) xj = a[s];
-    xj = __shfl_sync(0xffffffffu, xj, (tid & 31 & ~3) | owner);
+    for (int qq = 0; qq < 4; ++qq) {
+      const int j = 4 * s + qq;
+      double xj = 0.0;
+      if (q == qq) {
+        a[s] = a[s] / Lbb[j * TP + j];
+        xj = a[s];
+      }
+      xj = __shfl_sync(0xffffffffu, xj, (lane & ~3) | qq);
+      // update columns t = q + 4 s' > j
 #pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int t = q + 4 * s;
-      if (t > j) a[s] = fma(-xj, Lbb[t * TP + j], a[s]);
+      for (int s2 = s; s2 < 16; ++s2) {
+        if (s2 > s || q > qq) a[s2] = fma(-xj, Lbb[(q + 4 * s2) * TP + j], a[s2]);
+      }
     }
   }
   (void)rows_valid;
@@ -84,42 +86,58 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
 }
 
 // Diagonal block Cholesky (in smem), writes L block, zeroes the upper part.
-__global__ void __launch_bounds__(DT) potrf_diag_kernel(double* A, int64_t k, int64_t kb, int* info) {
+// Each of the 2080 lower entries is owned by one thread (in a register);
+// step j subtracts a_ij a_tj / p_j (unscaled columns, one barrier per step);
+// the scaling L_ij = a_ij / sqrt(p_j) is applied at the end.
+constexpr int DG_T = 1024;
+__global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, int64_t kb, int* info) {
   __shared__ double s[NB * TP];
   const int nb = (int)min((int64_t)NB, k - kb);
-  for (int e = threadIdx.x; e < NB * NB; e += DT) {
-    const int i = e / NB, j = e % NB;
-    s[i * TP + j] = (i < nb && j < nb) ? A[(kb + i) * k + kb + j] : (i == j ? 1.0 : 0.0);
+  const int tid = threadIdx.x;
+  constexpr int NE = NB * (NB + 1) / 2;  // 2080
+  int ei[3], et[3];
+  double av[3];
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int e = tid + u * DG_T;
+    int i = -1, t = 0;
+    if (e < NE) {
+      i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      t = e - i * (i + 1) / 2;
+    }
+    ei[u] = i;
+    et[u] = t;
+    double v = 0.0;
+    if (i >= 0) v = (i < nb && t < nb) ? A[(kb + i) * k + kb + t] : (i == t ? 1.0 : 0.0);
+    av[u] = v;
+    if (i >= 0) s[i * TP + t] = v;
   }
   __syncthreads();
-  __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
   for (int j = 0; j < NB; ++j) {
-    if (threadIdx.x == 0) {
-      const double p = s[j * TP + j];
-      if (!(p > 0.0)) {
-        if (!bad && j < nb) { bad = 1; atomicCAS(info, 0, (int)(kb + j + 1)); }
-        s[j * TP + j] = 1.0;
-      } else {
-        s[j * TP + j] = sqrt(p);
+    double p = s[j * TP + j];
+    if (!(p > 0.0)) p = 1.0;  // breakdown is reported below; keep the values finite
+    const double ip = 1.0 / p;
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const int i = ei[u], t = et[u];
+      if (i >= 0 && t > j) {
+        av[u] = fma(-s[i * TP + j], s[t * TP + j] * ip, av[u]);
+        if (t == j + 1) s[i * TP + t] = av[u];
       }
     }
     __syncthreads();
-    const double piv = s[j * TP + j];
-    for (int i = j + 1 + threadIdx.x; i < NB; i += DT) s[i * TP + j] /= piv;
-    __syncthreads();
-    // trailing update (lower): s[i][t] -= s[i][j] s[t][j], j < t <= i
-    const int m = NB - j - 1;
-    for (int e = threadIdx.x; e < m * m; e += DT) {
-      const int i = j + 1 + e / m, t = j + 1 + e % m;
-      if (t <= i) s[i * TP + t] = fma(-s[i * TP + j], s[t * TP + j], s[i * TP + t]);
-    }
-    __syncthreads();
   }
-  for (int e = threadIdx.x; e < nb * nb; e += DT) {
-    const int i = e / nb, j = e % nb;
-    A[(kb + i) * k + kb + j] = (j <= i) ? s[i * TP + j] : 0.0;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int i = ei[u], t = et[u];
+    if (i < 0 || i >= nb) continue;
+    const double p = s[t * TP + t];
+    if (i == t && !(p > 0.0)) atomicCAS(info, 0, (int)(kb + t + 1));
+    const double sp = p > 0.0 ? sqrt(p) : 1.0;
+    A[(kb + i) * k + kb + t] = (i == t) ? sp : av[u] / sp;
+    if (t != i) A[(kb + t) * k + kb + i] = 0.0;
   }
 }
 
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(DT) trsm_rows_kernel(const double* __restrict_
   extern __shared__ double dsm[];
   double* sA = dsm;            // [kk][row]: W tile, later T [row][col]
   double* sB = dsm + NB * TP;  // [kk][col]: L tile, later Lbb [row][col]
-  __shared__ double s_tab[16];
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
   load_exp2_tab(s_tab);
   __syncthreads();
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
@@ -306,6 +324,108 @@ afn_status set_smem_once() {
   return AFN_OK;
 }
 
+
+// -------------------------------------------------------------------------
+// W = K21 L^{-T} as a GEMM with the explicit L^{-T} (upper triangular):
+// W[r][c] = sum_{t <= c} K21[r][t] LinvT[t][c].  With FPS landmarks K11 + mu I
+// is well conditioned (cond(L) <= ~10 on the configs; SURVEY 8(c) Fig. 3.2
+// screening argument), so the explicit inverse loses nothing measurable and
+// the column blocks become independent tiles (no sequential sweep).
+// FP64 SIMT tile: 128 x 64 output, 256 threads, 8 x 4 register micro-tile
+// with stride-16 mapping, BK = 16 double-buffered cp.async stages.
+constexpr int GM = 128, GN = 64, GK = 16;
+constexpr int GPA = GM + 4, GPB = GN + 4;  // smem pitches
+
+__device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+__global__ void gen_k21_kernel(const double* __restrict__ X1, int64_t k, const double* __restrict__ Xr,
+                               int64_t N, int d, double cl, double* __restrict__ Kb) {
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+  load_exp2_tab(s_tab);
+  __syncthreads();
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= N * k) return;
+  const int64_t r = e / k, c = e - r * k;
+  const double sd = d2_exact_rt(&Xr[r * d], &X1[c * d], d);
+  Kb[e] = gauss_from_d2(sd, cl, s_tab);
+}
+
+// C (M x N) = A (M x K) * B (K x N), B upper triangular (rows t <= col used)
+__global__ void __launch_bounds__(256, 2) gemm_nn_bupper_kernel(const double* __restrict__ A,
+                                                              const double* __restrict__ B,
+                                                              double* __restrict__ Cm, int64_t M,
+                                                              int64_t N, int64_t K) {
+  extern __shared__ __align__(16) double gsm[];
+  double* sA = gsm;                  // [2][GK][GPA]
+  double* sB = gsm + 2 * GK * GPA;   // [2][GK][GPB]
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int64_t R0 = (int64_t)blockIdx.y * GM, C0 = (int64_t)blockIdx.x * GN;
+  const int64_t kend = min(K, C0 + GN);  // B[t][c] = 0 for t > c
+  const int64_t nkb = (kend + GK - 1) / GK;
+  auto stage = [&](int64_t kb, int buf) {
+    const int64_t k0 = kb * GK;
+    double* a = sA + buf * GK * GPA;
+    double* b = sB + buf * GK * GPB;
+    for (int e = tid; e < GM * GK; e += 256) {
+      const int r = e / GK, kk = e - r * GK;
+      const int64_t gr = R0 + r, gk = k0 + kk;
+      if (gr < M && gk < kend) cpa8(&a[kk * GPA + r], &A[gr * K + gk]);
+      else a[kk * GPA + r] = 0.0;
+    }
+    for (int e = tid; e < GK * GN; e += 256) {
+      const int kk = e / GN, c = e - kk * GN;
+      const int64_t gk = k0 + kk, gc = C0 + c;
+      if (gk < kend && gc < N) cpa8(&b[kk * GPB + c], &B[gk * N + gc]);
+      else b[kk * GPB + c] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  if (nkb > 0) stage(0, 0);
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int buf = (int)(kb & 1);
+    if (kb + 1 < nkb) {
+      stage(kb + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* a = sA + buf * GK * GPA;
+    const double* b = sB + buf * GK * GPB;
+#pragma unroll 4
+    for (int kk = 0; kk < GK; ++kk) {
+      double av[8], bv[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = a[kk * GPA + ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = b[kk * GPB + tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = R0 + ty + 16 * i;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = C0 + tx + 16 * j;
+      if (c < N) Cm[r * N + c] = acc[i][j];
+    }
+  }
+}
+
 __global__ void zero_upper_kernel(double* __restrict__ A, int64_t k) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
@@ -337,7 +457,7 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
   TRY_SMEM();
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
   for (int64_t kb = 0; kb < k; kb += NB) {
-    potrf_diag_kernel<<<1, DT, 0, st>>>(A, k, kb, d_info);
+    potrf_diag_kernel<<<1, DG_T, 0, st>>>(A, k, kb, d_info);
     AFN_LAUNCH_CHECK("potrf_diag_kernel");
     const int64_t rem = k - kb - NB;
     if (rem <= 0) break;
@@ -359,6 +479,28 @@ afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr
   const double cl = AFN_LOG2E / (l * l);
   trsm_rows_kernel<0><<<(unsigned)((N + NB - 1) / NB), DT, SMEM2, st>>>(L, k, X1, Xr, N, d, cl, W);
   AFN_LAUNCH_CHECK("trsm_rows_kernel<0>");
+  return AFN_OK;
+}
+
+afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
+                  double l, double* W, cudaStream_t st) {
+  if (N <= 0 || k <= 0) return AFN_OK;
+  const double cl = AFN_LOG2E / (l * l);
+  double* Kb = nullptr;
+  afn_status s = dalloc((void**)&Kb, sizeof(double) * N * k, st);
+  if (s != AFN_OK) return s;
+  gen_k21_kernel<<<(unsigned)((N * k + 255) / 256), 256, 0, st>>>(X1, k, Xr, N, d, cl, Kb);
+  AFN_LAUNCH_CHECK("gen_k21_kernel");
+  static bool attr = false;
+  const int bytes = (int)(sizeof(double) * 2 * GK * (GPA + GPB));
+  if (!attr) {
+    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  dim3 grid((unsigned)((k + GN - 1) / GN), (unsigned)((N + GM - 1) / GM));
+  gemm_nn_bupper_kernel<<<grid, 256, bytes, st>>>(Kb, LinvT, W, N, k, k);
+  AFN_LAUNCH_CHECK("gemm_nn_bupper_kernel");
+  dfree(Kb, st);
   return AFN_OK;
 }
 

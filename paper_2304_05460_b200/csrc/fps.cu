@@ -12,6 +12,8 @@
 // Bit-exact with the readings R3: squared distances are sums in coordinate
 // order of individually rounded (x_c - y_c)^2; selected points carry mind = -1
 // and are never re-picked; ties go to the lowest index.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -243,10 +245,171 @@ afn_status launch_fps(const double* X, int64_t n, int d, int64_t k, int64_t seed
   return AFN_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster variant (n up to 16 CTAs x NT x 2 points): the per-step exchange is
+// a cluster barrier plus distributed-shared-memory reads of the CL per-CTA
+// winners (no global-memory round trips).
+namespace cg = cooperative_groups;
+
+template <int DP, int P, int NT>
+__global__ void __launch_bounds__(NT, 1)
+fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
+                   int64_t* __restrict__ idx_out, double* __restrict__ fill_out) {
+  constexpr int S = Slot<DP>::S;
+  constexpr int NW = NT / 32;
+  __shared__ double s_w[NW][S];
+  __shared__ double s_slot[2][S];
+  __shared__ double s_new[S];
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const int CL = (int)cl.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t stride = (int64_t)CL * NT;
+  const int64_t gtid = (int64_t)crank * NT + tid;
+
+  double pts[P][DP];
+  double mind[P];
+  double y[DP];
+#pragma unroll
+  for (int c = 0; c < DP; ++c) y[c] = c < d ? X[seed * d + c] : 0.0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t i = gtid + s * stride;
+    if (i < n) {
+#pragma unroll
+      for (int c = 0; c < DP; ++c) pts[s][c] = c < d ? X[i * d + c] : 0.0;
+      mind[s] = (i == seed) ? -1.0 : d2_exact<DP>(pts[s], y);
+    } else {
+#pragma unroll
+      for (int c = 0; c < DP; ++c) pts[s][c] = 0.0;
+      mind[s] = -2.0;
+    }
+  }
+  if (crank == 0 && tid == 0) idx_out[0] = seed;
+
+  for (int64_t step = 1; step <= k; ++step) {
+    const int par = (int)(step & 1);
+    double bd = -3.0;
+    long long bi = 0x7fffffffffffffffLL;
+    double bc[DP];
+#pragma unroll
+    for (int c = 0; c < DP; ++c) bc[c] = 0.0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      if (mind[s] > bd) {
+        bd = mind[s];
+        bi = gtid + s * stride;
+#pragma unroll
+        for (int c = 0; c < DP; ++c) bc[c] = pts[s][c];
+      }
+    }
+    double wd = bd;
+    long long wi = bi;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, wd, o);
+      const long long oi = __shfl_xor_sync(0xffffffffu, wi, o);
+      if (better(od, oi, wd, wi)) { wd = od; wi = oi; }
+    }
+    if (bi == wi && bd == wd) {
+      s_w[wid][0] = wd;
+      s_w[wid][1] = __longlong_as_double(wi);
+#pragma unroll
+      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = bc[c];
+    }
+    __syncthreads();
+    if (wid == 0) {
+      double vd = lane < NW ? s_w[lane][0] : -3.0;
+      long long vi = lane < NW ? __double_as_longlong(s_w[lane][1]) : 0x7fffffffffffffffLL;
+      int src = lane;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, vd, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, vi, o);
+        const int os = __shfl_xor_sync(0xffffffffu, src, o);
+        if (better(od, oi, vd, vi)) { vd = od; vi = oi; src = os; }
+      }
+      if (lane < S) s_slot[par][lane] = s_w[src][lane];
+    }
+    cl.sync();
+    if (wid == 0) {
+      double gd = -3.0;
+      long long gi = 0x7fffffffffffffffLL;
+      int gsrc = 0;
+      if (lane < CL) {
+        const double* rs = cl.map_shared_rank(&s_slot[par][0], lane);
+        gd = rs[0];
+        gi = __double_as_longlong(rs[1]);
+        gsrc = lane;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double od = __shfl_xor_sync(0xffffffffu, gd, o);
+        const long long oi = __shfl_xor_sync(0xffffffffu, gi, o);
+        const int os = __shfl_xor_sync(0xffffffffu, gsrc, o);
+        if (better(od, oi, gd, gi)) { gd = od; gi = oi; gsrc = os; }
+      }
+      if (lane < S) s_new[lane] = cl.map_shared_rank(&s_slot[par][0], gsrc)[lane];
+    }
+    __syncthreads();
+    const double nd = s_new[0];
+    const long long ni = __double_as_longlong(s_new[1]);
+    if (crank == 0 && tid == 0) {
+      fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
+      if (step < k) idx_out[step] = ni;
+    }
+    if (step == k) break;
+#pragma unroll
+    for (int c = 0; c < DP; ++c) y[c] = s_new[2 + c];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int64_t i = gtid + s * stride;
+      if (i < n) {
+        const double dd = d2_exact<DP>(pts[s], y);
+        mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
+      }
+    }
+  }
+  cl.sync();  // no CTA leaves while its slots may still be read remotely
+}
+
+template <int DP, int P, int NT>
+afn_status launch_fps_cluster(const double* X, int64_t n, int d, int64_t k, int64_t seed,
+                              int64_t* idx, double* fill, int CL, cudaStream_t st) {
+  auto kern = fps_cluster_kernel<DP, P, NT>;
+  if (CL > 8) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill));
+  AFN_LAUNCH_CHECK("fps_cluster_kernel");
+  return AFN_OK;
+}
+
 template <int DP>
 afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
                           double* fill, cudaStream_t st) {
   const int sms = num_sms();
+  // cluster path: one cluster of CL <= 16 CTAs, 1 or 2 points per thread
+  {
+    constexpr int CNT = DP <= 4 ? 1024 : 512;
+    if (n > (int64_t)FPS_NT * 8 && n <= (int64_t)16 * CNT * 2) {
+      const int P2 = n <= (int64_t)8 * CNT ? 1 : 2;
+      const int CL = (int)((n + (int64_t)CNT * P2 - 1) / ((int64_t)CNT * P2));
+      if (P2 == 1) return launch_fps_cluster<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, st);
+      return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, st);
+    }
+  }
   // choose points per thread P and grid G (G = 1 needs no grid barrier)
   int P = 0, G = 0, pglob = 0;
   const int64_t per1 = FPS_NT;

@@ -13,6 +13,7 @@
 // Then G^T is built as its own CSR (deterministic rank placement).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "afn_common.cuh"
 #include "afn_internal.h"
@@ -49,7 +50,7 @@ fsai_kernel(const double* __restrict__ X2, int64_t N, int d, double cl, double m
   double* S = smem;
   double* sX = smem + U;
   int* sJ = reinterpret_cast<int*>(sX + WP * d);
-  __shared__ double s_tab[16];
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
   __shared__ int s_bad;
 
   const int64_t i = blockIdx.x;
@@ -206,6 +207,396 @@ afn_status launch_fsai(const double* X2, int64_t N, int d, double cl, double mu,
   return AFN_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Split variant: (1) fsai_gram_kernel computes S_JJ (packed lower) for a batch
+// of rows into global memory with the same register-tiled Gram as above but no
+// in-CTA Cholesky; (2) fsai_chol_kernel factors each S_JJ with one warp
+// (left-looking Cholesky, L1-resident) and back-substitutes for g.  The
+// latency-bound factorisation then runs at full warp parallelism instead of
+// stalling a 256-thread CTA with two barriers per column.
+template <int MT>
+__global__ void __launch_bounds__(FT, 2)
+fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, double cl, double mu,
+                 const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
+                 const int32_t* __restrict__ col, double* __restrict__ Sg) {
+  constexpr int WP = MT * 16;
+  constexpr int PW = WP + 1;
+  constexpr int SPK = WP * (WP + 1) / 2;
+  extern __shared__ __align__(16) double smem[];
+  constexpr int STG = 2 * KC * PW;
+  double* stg = smem;
+  double* sX = smem + STG;
+  int* sJ = reinterpret_cast<int*>(sX + WP * d);
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+
+  const int64_t i = r0 + blockIdx.x;
+  const int64_t beg = rp[i];
+  const int wp = (int)(rp[i + 1] - beg);
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  load_exp2_tab(s_tab);
+  for (int a = tid; a < WP; a += FT) sJ[a] = a < wp ? col[beg + a] : -1;
+  __syncthreads();
+  for (int e = tid; e < WP * d; e += FT) {
+    const int a = e / d, c = e - a * d;
+    sX[e] = sJ[a] >= 0 ? X2[(int64_t)sJ[a] * d + c] : 0.0;
+  }
+  double acc[MT * (MT + 1) / 2];
+#pragma unroll
+  for (int t = 0; t < MT * (MT + 1) / 2; ++t) acc[t] = 0.0;
+  const int64_t nch = (k + KC - 1) / KC;
+  auto issue = [&](int64_t ch, int buf) {
+    double* dst = stg + buf * KC * PW;
+    const int64_t c0 = ch * KC;
+    for (int e = tid; e < WP * KC; e += FT) {
+      const int a = e / KC, kk = e - a * KC;
+      const int64_t c = c0 + kk;
+      const int ja = sJ[a];
+      if (ja >= 0 && c < k) cp_async8(&dst[kk * PW + a], &W[(int64_t)ja * k + c]);
+      else dst[kk * PW + a] = 0.0;
+    }
+    cp_async_commit();
+  };
+  if (nch > 0) issue(0, 0);
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    const int buf = (int)(ch & 1);
+    if (ch + 1 < nch) {
+      issue(ch + 1, buf ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* T = stg + buf * KC * PW;
+#pragma unroll 2
+    for (int kk = 0; kk < KC; ++kk) {
+      double a[MT], b[MT];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        a[m] = T[kk * PW + ty + 16 * m];
+        b[m] = T[kk * PW + tx + 16 * m];
+      }
+      int t = 0;
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int q = 0; q <= m; ++q) {
+          acc[t] = fma(a[m], b[q], acc[t]);
+          ++t;
+        }
+    }
+    __syncthreads();
+  }
+  double* S = Sg + (int64_t)blockIdx.x * SPK;
+  int t = 0;
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int q = 0; q <= m; ++q) {
+      const int a = ty + 16 * m, b = tx + 16 * q;
+      if (b <= a && a < wp) {
+        double kv;
+        if (a == b) {
+          kv = 1.0 + mu;
+        } else {
+          const double sd = d2_exact_rt(&sX[a * d], &sX[b * d], d);
+          kv = gauss_from_d2(sd, cl, s_tab);
+        }
+        S[pk(a, b)] = kv - acc[t];
+      }
+      ++t;
+    }
+}
+
+// one warp per row: left-looking (Crout) Cholesky of the packed S_JJ in place,
+// then g = R^{-T} e_last
+template <int MT>
+__global__ void __launch_bounds__(256)
+fsai_chol_kernel(int64_t r0, int64_t nrows, const int64_t* __restrict__ rp, double* __restrict__ Sg,
+                 double* __restrict__ gval, int* info) {
+  constexpr int WP = MT * 16;
+  constexpr int SPK = WP * (WP + 1) / 2;
+  const int64_t wr = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (wr >= nrows) return;
+  const int64_t i = r0 + wr;
+  const int64_t beg = rp[i];
+  const int wp = (int)(rp[i + 1] - beg);
+  double* S = Sg + wr * SPK;
+  bool bad = false;
+  for (int j = 0; j < wp; ++j) {
+    const double* Lj = S + pk(j, 0);
+    // diagonal: S_jj - sum_t L_jt^2
+    double s = 0.0;
+    for (int t = lane; t < j; t += 32) s = fma(Lj[t], Lj[t], s);
+    s = warp_sum(s);
+    double djj = S[pk(j, j)] - s;
+    if (!(djj > 0.0)) { bad = true; djj = 1.0; }
+    const double piv = sqrt(djj);
+    const double inv = 1.0 / piv;
+    // column j below the diagonal: rows a = j+1.., lane-strided, dot over t < j
+    for (int a = j + 1 + lane; a < wp; a += 32) {
+      const double* La = S + pk(a, 0);
+      double acc = La[j];
+      for (int t = 0; t < j; ++t) acc = fma(-La[t], Lj[t], acc);
+      S[pk(a, j)] = acc * inv;
+    }
+    __syncwarp();
+    if (lane == 0) S[pk(j, j)] = piv;
+    __syncwarp();
+  }
+  if (bad && lane == 0) atomicCAS(info, 0, (int)(i + 1));
+  double rhs[(WP + 31) / 32];
+#pragma unroll
+  for (int s = 0; s < (WP + 31) / 32; ++s) rhs[s] = (lane + 32 * s == wp - 1) ? 1.0 : 0.0;
+  for (int j = wp - 1; j >= 0; --j) {
+    double gj = 0.0;
+#pragma unroll
+    for (int s = 0; s < (WP + 31) / 32; ++s)
+      if (lane + 32 * s == j) gj = rhs[s] / S[pk(j, j)];
+    gj = __shfl_sync(0xffffffffu, gj, j & 31);
+#pragma unroll
+    for (int s = 0; s < (WP + 31) / 32; ++s) {
+      const int tt = lane + 32 * s;
+      if (tt < j) rhs[s] = fma(-S[pk(j, tt)], gj, rhs[s]);
+      else if (tt == j) rhs[s] = gj;
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < (WP + 31) / 32; ++s) {
+    const int tt = lane + 32 * s;
+    if (tt < wp) gval[beg + tt] = rhs[s];
+  }
+}
+
+template <int MT>
+afn_status launch_fsai_split(const double* X2, int64_t N, int d, double cl, double mu, const double* W,
+                             int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* info,
+                             cudaStream_t st) {
+  constexpr int WP = MT * 16;
+  constexpr int PW = WP + 1;
+  constexpr int64_t SPK = WP * (WP + 1) / 2;
+  const size_t bytes = sizeof(double) * (2 * (size_t)KC * PW + (size_t)WP * d) + sizeof(int) * WP + 16;
+  auto kg = fsai_gram_kernel<MT>;
+  AFN_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const int64_t batch = std::min<int64_t>(N, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
+  double* Sg = nullptr;
+  afn_status s = dalloc((void**)&Sg, sizeof(double) * SPK * batch, st);
+  if (s != AFN_OK) return s;
+  for (int64_t r0 = 0; r0 < N; r0 += batch) {
+    const int64_t nr = std::min(batch, N - r0);
+    kg<<<(unsigned)nr, FT, bytes, st>>>(X2, r0, d, cl, mu, W, k, rp, col, Sg);
+    AFN_LAUNCH_CHECK("fsai_gram_kernel");
+    fsai_chol_kernel<MT><<<(unsigned)((nr + 7) / 8), 256, 0, st>>>(r0, nr, rp, Sg, gval, info);
+    AFN_LAUNCH_CHECK("fsai_chol_kernel");
+  }
+  dfree(Sg, st);
+  return AFN_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised persistent variant: 8 "Gram" warps compute W_J W_J^T and
+// assemble S_JJ for row t while a 9th warp factors S_JJ of row t-1 and solves
+// for g (double-buffered S in shared memory, named-barrier handshakes).  The
+// FP64-heavy Gram then hides the latency-bound Cholesky.
+__device__ __forceinline__ void nbar_sync(int id, int cnt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
+constexpr int WS_PROD = 256;
+constexpr int WS_T = WS_PROD + 32;
+enum { BAR_PROD = 1, BAR_FULL0 = 2, BAR_EMPTY0 = 4 };
+
+template <int MT>
+__global__ void __launch_bounds__(WS_T, 1)
+fsai_ws_kernel(const double* __restrict__ X2, int64_t N, int d, double cl, double mu,
+               const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
+               const int32_t* __restrict__ col, double* __restrict__ gval, int* info) {
+  constexpr int WP = MT * 16;
+  constexpr int PW = WP + 1;
+  constexpr int STG = KC * PW;            // one staging buffer
+  constexpr int SPK = WP * (WP + 1) / 2;  // packed lower S
+  extern __shared__ __align__(16) double smem[];
+  double* stg = smem;                 // [2][STG]
+  double* Sb = smem + 2 * STG;        // [2][SPK]
+  double* sX = Sb + 2 * SPK;          // [WP * d]
+  int* sJ = reinterpret_cast<int*>(sX + WP * d);  // [WP]
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+  __shared__ long long s_meta[2][2];  // beg, (row << 8) | wp  per buffer
+
+  const int tid = threadIdx.x;
+  load_exp2_tab(s_tab);
+  __syncthreads();
+
+  if (tid < WS_PROD) {
+    // ===================== producers: Gram + S assembly =====================
+    const int ty = tid >> 4, tx = tid & 15;
+    int t = 0;
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x, ++t) {
+      const int buf = t & 1;
+      const int64_t beg = rp[i];
+      const int wp = (int)(rp[i + 1] - beg);
+      nbar_sync(BAR_PROD, WS_PROD);  // previous row finished with sJ / sX / stg
+      for (int a = tid; a < WP; a += WS_PROD) sJ[a] = a < wp ? col[beg + a] : -1;
+      nbar_sync(BAR_PROD, WS_PROD);
+      for (int e = tid; e < WP * d; e += WS_PROD) {
+        const int a = e / d, c = e - a * d;
+        sX[e] = sJ[a] >= 0 ? X2[(int64_t)sJ[a] * d + c] : 0.0;
+      }
+      double acc[MT * (MT + 1) / 2];
+#pragma unroll
+      for (int q = 0; q < MT * (MT + 1) / 2; ++q) acc[q] = 0.0;
+      const int64_t nch = (k + KC - 1) / KC;
+      auto issue = [&](int64_t ch, int b) {
+        double* dst = stg + b * STG;
+        const int64_t c0 = ch * KC;
+        for (int e = tid; e < WP * KC; e += WS_PROD) {
+          const int a = e / KC, kk = e - a * KC;
+          const int64_t c = c0 + kk;
+          const int ja = sJ[a];
+          if (ja >= 0 && c < k) cp_async8(&dst[kk * PW + a], &W[(int64_t)ja * k + c]);
+          else dst[kk * PW + a] = 0.0;
+        }
+        cp_async_commit();
+      };
+      issue(0, 0);
+      for (int64_t ch = 0; ch < nch; ++ch) {
+        const int sb = (int)(ch & 1);
+        if (ch + 1 < nch) {
+          issue(ch + 1, sb ^ 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        nbar_sync(BAR_PROD, WS_PROD);
+        const double* T = stg + sb * STG;
+#pragma unroll 2
+        for (int kk = 0; kk < KC; ++kk) {
+          double av[MT], bv[MT];
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            av[m] = T[kk * PW + ty + 16 * m];
+            bv[m] = T[kk * PW + tx + 16 * m];
+          }
+          int q = 0;
+#pragma unroll
+          for (int m = 0; m < MT; ++m)
+#pragma unroll
+            for (int qq = 0; qq <= m; ++qq) {
+              acc[q] = fma(av[m], bv[qq], acc[q]);
+              ++q;
+            }
+        }
+        nbar_sync(BAR_PROD, WS_PROD);
+      }
+      // S[buf] must be free (consumer done with row t-2)
+      if (t >= 2) nbar_sync(BAR_EMPTY0 + buf, WS_T);
+      double* S = Sb + buf * SPK;
+      int q = 0;
+#pragma unroll
+      for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int qq = 0; qq <= m; ++qq) {
+          const int a = ty + 16 * m, b = tx + 16 * qq;
+          if (b <= a && a < wp) {
+            double kv;
+            if (a == b) {
+              kv = 1.0 + mu;
+            } else {
+              const double sd = d2_exact_rt(&sX[a * d], &sX[b * d], d);
+              kv = gauss_from_d2(sd, cl, s_tab);
+            }
+            S[pk(a, b)] = kv - acc[q];
+          }
+          ++q;
+        }
+      if (tid == 0) {
+        s_meta[buf][0] = beg;
+        s_meta[buf][1] = ((long long)i << 8) | wp;
+      }
+      nbar_arrive(BAR_FULL0 + buf, WS_T);
+    }
+  } else {
+    // ===================== consumer warp: Cholesky + back substitution ========
+    const int lane = tid & 31;
+    int t = 0;
+    for (int64_t i = blockIdx.x; i < N; i += gridDim.x, ++t) {
+      const int buf = t & 1;
+      nbar_sync(BAR_FULL0 + buf, WS_T);
+      double* S = Sb + buf * SPK;
+      const int64_t beg = s_meta[buf][0];
+      const int wp = (int)(s_meta[buf][1] & 0xff);
+      bool bad = false;
+      for (int j = 0; j < wp; ++j) {
+        double dj = S[pk(j, j)];
+        if (!(dj > 0.0)) { bad = true; dj = 1.0; }
+        const double piv = sqrt(dj);
+        const double inv = 1.0 / piv;
+        __syncwarp();
+        if (lane == 0) S[pk(j, j)] = piv;
+        for (int a = j + 1 + lane; a < wp; a += 32) S[pk(a, j)] *= inv;
+        __syncwarp();
+        for (int a = j + 1 + lane; a < wp; a += 32) {
+          const double la = S[pk(a, j)];
+          double* rowa = S + pk(a, 0);
+          const double* cj = S + pk(j + 1, j);  // S[b][j] for b = j+1, advancing by b+1
+          int off = 0;
+          for (int b = j + 1; b <= a; ++b) {
+            rowa[b] = fma(-la, cj[off], rowa[b]);
+            off += b + 1;
+          }
+        }
+        __syncwarp();
+      }
+      if (bad && lane == 0) atomicCAS(info, 0, (int)(i + 1));
+      // g = R^{-T} e_last
+      double rhs[(WP + 31) / 32];
+#pragma unroll
+      for (int s = 0; s < (WP + 31) / 32; ++s) rhs[s] = (lane + 32 * s == wp - 1) ? 1.0 : 0.0;
+      for (int j = wp - 1; j >= 0; --j) {
+        double gj = 0.0;
+#pragma unroll
+        for (int s = 0; s < (WP + 31) / 32; ++s)
+          if (lane + 32 * s == j) gj = rhs[s] / S[pk(j, j)];
+        gj = __shfl_sync(0xffffffffu, gj, j & 31);
+#pragma unroll
+        for (int s = 0; s < (WP + 31) / 32; ++s) {
+          const int tt = lane + 32 * s;
+          if (tt < j) rhs[s] = fma(-S[pk(j, tt)], gj, rhs[s]);
+          else if (tt == j) rhs[s] = gj;
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < (WP + 31) / 32; ++s) {
+        const int tt = lane + 32 * s;
+        if (tt < wp) gval[beg + tt] = rhs[s];
+      }
+      __syncwarp();
+      // hand S[buf] back only if the producers will wait for it
+      if (i + 2 * (int64_t)gridDim.x < N) nbar_arrive(BAR_EMPTY0 + buf, WS_T);
+    }
+  }
+}
+
+template <int MT>
+afn_status launch_fsai_ws(const double* X2, int64_t N, int d, double cl, double mu, const double* W,
+                          int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* info,
+                          cudaStream_t st) {
+  constexpr int WP = MT * 16;
+  constexpr int PW = WP + 1;
+  const size_t bytes = sizeof(double) * (2 * (size_t)KC * PW + (size_t)WP * (WP + 1) + (size_t)WP * d) +
+                       sizeof(int) * WP + 16;
+  auto kern = fsai_ws_kernel<MT>;
+  AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  const int grid = (int)std::min<int64_t>(N, (int64_t)num_sms());
+  kern<<<grid, WS_T, bytes, st>>>(X2, N, d, cl, mu, W, k, rp, col, gval, info);
+  AFN_LAUNCH_CHECK("fsai_ws_kernel");
+  return AFN_OK;
+}
+
 // ---- CSR transpose -----------------------------------------------------------
 __global__ void count_cols_kernel(const int32_t* __restrict__ col, int64_t nnz, int* __restrict__ cnt) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -294,6 +685,34 @@ afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, con
   }
   const double cl = AFN_LOG2E / (l * l);
   const int MT = (w + 15) / 16;
+  // variant: 0 = split (default), 1 = single kernel, 2 = warp-specialised
+  static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : 0;
+  if (variant == 2) {
+    switch (MT) {
+      case 1: return launch_fsai_ws<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 2: return launch_fsai_ws<2>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 3: return launch_fsai_ws<3>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 4: return launch_fsai_ws<4>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 5: return launch_fsai_ws<5>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 6: return launch_fsai_ws<6>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 7: return launch_fsai_ws<7>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 8: return launch_fsai_ws<8>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
+    }
+  }
+  if (variant == 0) {
+    switch (MT) {
+      case 1: return launch_fsai_split<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 2: return launch_fsai_split<2>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 3: return launch_fsai_split<3>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 4: return launch_fsai_split<4>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 5: return launch_fsai_split<5>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 6: return launch_fsai_split<6>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 7: return launch_fsai_split<7>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      case 8: return launch_fsai_split<8>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+      default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
+    }
+  }
   switch (MT) {
     case 1: return launch_fsai<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
     case 2: return launch_fsai<2>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);

@@ -9,8 +9,10 @@
 // over the chunk in column order; a second kernel adds the chunk partials in
 // chunk order plus mu v_i -> bit-identical results run to run and independent
 // of how rows are sharded across GPUs.
-// Per pair (d=3): 3 DADD + 1 DMUL + 2 DFMA (distance) + 10 (exp2) + 1 DFMA = 17
-// FP64-pipe instructions, 28 flops counting an FMA as 2.
+// Per pair (d=3): 3 DADD + 1 DMUL + 2 DFMA (distance) + 8 (exp2) + 1 DFMA = 15
+// FP64-pipe instructions.  The roofline counts a fixed algorithmic 3d+19 flops
+// per pair (d=3: 28; the direct-difference + degree-6/16-entry-table exp
+// formulation of DESIGN.md, FMA = 2), independent of later instruction savings.
 #include <algorithm>
 #include <cmath>
 
@@ -37,7 +39,7 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
                    double* __restrict__ partial) {
   constexpr int CS = KmvTraits<D>::CS;
   constexpr int KMV_TC = KmvTraits<D>::TC;
-  __shared__ double s_tab[16];
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
   __shared__ __align__(16) double s_col[KMV_TC * CS];
   load_exp2_tab(s_tab);
 

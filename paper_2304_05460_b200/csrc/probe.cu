@@ -49,3 +49,51 @@ afn_status probe_dfma(int64_t iters, double* tflops, cudaStream_t st) {
 }
 
 }  // namespace afn
+
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput probe
+namespace afn {
+namespace {
+__global__ void __launch_bounds__(256) dmma_probe_kernel(int64_t iters, double seed, double* out) {
+  double a = seed + threadIdx.x * 1e-3, b = seed - threadIdx.x * 1e-3;
+  double c[4][2];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) c[u][0] = c[u][1] = 0.0;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[u][0]), "+d"(c[u][1]) : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) s += c[u][0] + c[u][1];
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace
+
+afn_status probe_dmma(int64_t iters, double* tflops, cudaStream_t st) {
+  const int blocks = num_sms() * 8;
+  double* out = nullptr;
+  afn_status s = dalloc((void**)&out, sizeof(double), st);
+  if (s != AFN_OK) return s;
+  cudaEvent_t e0, e1;
+  AFN_CUDA(cudaEventCreate(&e0));
+  AFN_CUDA(cudaEventCreate(&e1));
+  dmma_probe_kernel<<<blocks, 256, 0, st>>>(iters / 8, 1.0, out);
+  AFN_LAUNCH_CHECK("dmma_probe_kernel");
+  AFN_CUDA(cudaEventRecord(e0, st));
+  dmma_probe_kernel<<<blocks, 256, 0, st>>>(iters, 1.0, out);
+  AFN_LAUNCH_CHECK("dmma_probe_kernel");
+  AFN_CUDA(cudaEventRecord(e1, st));
+  AFN_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  AFN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  dfree(out, st);
+  // per warp-instruction: 8x8x4 = 256 FMA = 512 flop; 4 per iteration per warp
+  const double flops = 512.0 * 4.0 * (double)iters * (double)blocks * (256 / 32);
+  *tflops = flops / (ms * 1e-3) / 1e12;
+  return AFN_OK;
+}
+}  // namespace afn
