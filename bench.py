@@ -34,6 +34,16 @@ METRIC = "AFN-PCG solve sec & kernel-matvec Gpairs/s (fp64) vs FP64 roofline"
 # FP64 peak derived from the guide's unit counts:
 # 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def _hbm_peak():
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+HBM_PEAK_GBS = _hbm_peak()
 # kernel matvec: algorithmic flops per pair for d = 3: 3d + 19
 KMV_FLOPS_PER_PAIR = lambda d: 3 * d + 19  # noqa: E731
 
@@ -227,8 +237,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
-    from paper_2304_05460_b200 import build as _b
-    _b.build()
+    import __graft_entry__ as ge
+    ge._build_module().build()
     import paper_2304_05460_b200 as afn
     from synth import CONFIGS, gen_problem
 
@@ -263,6 +273,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     l0 = afn.launch_count()
+    afn.kernel_timers(reset=True, enable=True)
     with sampler:
         for s in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the event pair)
@@ -271,6 +282,7 @@ def main():
             evs[s][1].record(stream)
         torch.cuda.synchronize()
     launches = afn.launch_count() - l0
+    kt = afn.kernel_timers(enable=False)
     if dist:
         dist.barrier()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
@@ -282,50 +294,59 @@ def main():
     n_solves = len(cfg.ls)
     value_s = job_ms / 1e3 / (args.steps * n_solves)
 
-    # ---- per-kernel accounting (from events inside the library, timed region)
+    # ---- per-kernel accounting (CUDA events inside the library, timed region)
     n = cfg.n
     kmv_ms = sum(r["matvec_ms"] for _, _, r in records)
     kmv_calls = sum(r["iterations"] for _, _, r in records)
-    fsai_ms = sum(i["ms_fsai_rows"] for _, i, _ in records)
-    fsai_fl = sum(fsai_flops(i["n"] - i["k"], i["k"], cfg.w) for _, i, _ in records)
-    kmv_fl = KMV_FLOPS_PER_PAIR(cfg.d) * float(n) * n * kmv_calls
     per_l = {}
     for l, inf, rep in records[: len(my_ls)]:
         per_l[str(l)] = {"khat": inf["khat"], "k": inf["k"], "iters": rep["iterations"],
                          "setup_ms": inf["ms_total"], "pcg_ms": rep["solve_ms"],
                          "relres_true": rep["relres_true"]}
     kmv_gpairs = (float(n) * n * kmv_calls) / (kmv_ms * 1e-3) / 1e9 if kmv_ms > 0 else None
-    shares = {"fsai_kernel": fsai_ms, "kmv_kernel": kmv_ms,
+    shares = {"fsai_phase": sum(i["ms_fsai_rows"] for _, i, _ in records), "kmv_kernel": kmv_ms,
               "fps": sum(i["ms_fps"] for _, i, _ in records),
-              "trsm_W": sum(i["ms_trsm"] for _, i, _ in records),
+              "W": sum(i["ms_trsm"] for _, i, _ in records),
               "chol_Linv": sum(i["ms_chol"] for _, i, _ in records),
               "alg1": sum(i["ms_alg1"] for _, i, _ in records),
               "knn": sum(i["ms_knn"] for _, i, _ in records),
               "apply": sum(r["apply_ms"] for _, _, r in records)}
-    dom = "fsai_kernel" if fsai_ms >= kmv_ms else "kmv_kernel"
+    single = {k: v for k, v in kt.items() if k not in ("potrf", "alg1") and v["count"] > 0}
+    dom = max(single, key=lambda k: single[k]["ms"]) if single else None
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and dom:
         try:
             traffic = json.load(open(tr_path)).get(dom)
         except Exception:
             traffic = None
 
-    def roof(fl, ms, calls, name):
-        if ms <= 0 or calls <= 0:
+    def roof(name):
+        v = kt.get(name)
+        if not v or v["count"] <= 0 or v["ms"] <= 0:
             return None
-        ach = fl / (ms * 1e-3) / 1e12
-        return {"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": ach / FP64_PEAK_TFLOPS, "traffic": None, "kernel": name,
-                "launches": calls, "ms_per_launch": ms / calls, "flops_per_launch": fl / calls,
-                "peak_source": "guide unit counts: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"}
+        per_ms = v["ms"] / v["count"]
+        out = {"kernel": name, "launches": v["count"], "ms_per_launch": per_ms,
+               "share_of_step": v["ms"] / total_ms if total_ms > 0 else None, "traffic": None}
+        if name == "apply":
+            ach = v["work"] / (v["ms"] * 1e-3) / 1e9
+            out.update({"bound": "hbm", "achieved": ach, "peak": HBM_PEAK_GBS, "unit": "GB/s",
+                        "frac": ach / HBM_PEAK_GBS, "bytes_per_launch": v["work"] / v["count"],
+                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
+        elif v["work"] > 0:
+            ach = v["work"] / (v["ms"] * 1e-3) / 1e12
+            out.update({"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": ach / FP64_PEAK_TFLOPS, "flops_per_launch": v["work"] / v["count"],
+                        "peak_source": "guide unit counts: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"})
+        else:
+            out.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None})
+        return out
 
-    r_fsai = roof(fsai_fl, fsai_ms, len(records), "fsai_kernel")
-    r_kmv = roof(kmv_fl, kmv_ms, kmv_calls, "kmv_partial_kernel")
-    roofline = r_fsai if dom == "fsai_kernel" else r_kmv
+    roofline = roof(dom) if dom else None
     if roofline is not None:
         roofline["traffic"] = traffic
-        roofline["share_of_step"] = shares[dom] / (total_ms) if total_ms > 0 else None
+    r_kmv = roof("kmv_partial_kernel")
+    kernel_ms = {k: round(v["ms"], 3) for k, v in kt.items() if v["count"] > 0}
 
     # ---- e2e: host buffers through the C ABI (copies inside the timed region)
     e2e = None
@@ -375,7 +396,7 @@ def main():
                 "kmv_gpairs_per_s": kmv_gpairs,
                 "gpu_launches": launches,
                 "roofline": roofline, "roofline_kmv": r_kmv,
-                "time_share_ms": shares,
+                "time_share_ms": shares, "kernel_ms": kernel_ms,
                 "clocks": sampler.summary(),
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

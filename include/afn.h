@@ -175,6 +175,16 @@ afn_status afn_probe_dfma(int64_t iters, double* tflops /*host*/, void* stream);
 /* Same for FP64 tensor-core DMMA (mma.sync m8n8k4 f64).                      */
 afn_status afn_probe_dmma(int64_t iters, double* tflops /*host*/, void* stream);
 
+/* Per-kernel CUDA-event timers (off by default).  When enabled the library
+ * records an event pair around each timed kernel class on the launching
+ * stream and accumulates device ms, algorithmic work (flops) and counts.
+ * Classes: 0 kmv, 1 FSAI pair GEMM, 2 FSAI assembly, 3 FSAI Cholesky,
+ * 4 FSAI per-row Gram (fallback), 5 FPS, 6 W GEMM, 7 L^-T, 8 potrf, 9 kNN,
+ * 10 apply, 11 Alg. 1.  afn_kt_read returns the number of classes.          */
+void afn_kt_enable(int32_t on);
+void afn_kt_reset(void);
+int32_t afn_kt_read(double* ms /*host*/, double* work /*host*/, int64_t* count /*host*/, int32_t n);
+
 /* Number of kernels this library launched since load (its own kernels only). */
 int64_t afn_launch_count(void);
 const char* afn_last_error(void);

@@ -88,6 +88,9 @@ _sig = {
     "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_probe_dmma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_launch_count": (C.c_int64, []),
+    "afn_kt_enable": (None, [C.c_int32]),
+    "afn_kt_reset": (None, []),
+    "afn_kt_read": (C.c_int32, [_D, _D, C.POINTER(C.c_int64), C.c_int32]),
     "afn_last_error": (C.c_char_p, []),
     "afn_abi_version": (C.c_int32, []),
 }
@@ -124,6 +127,25 @@ def _stream(stream=None):
     torch = _torch()
     s = stream if stream is not None else torch.cuda.current_stream()
     return C.c_void_p(s.cuda_stream)
+
+
+KT_NAMES = ("kmv_partial_kernel", "group_gemm_kernel", "fsai_assemble_kernel", "fsai_chol_kernel",
+            "fsai_gram_kernel", "fps_kernel", "gemm_nn_bupper_kernel", "trsm_rows_kernel<1>",
+            "potrf", "knn_kernel", "apply", "alg1")
+
+
+def kernel_timers(enable=None, reset=False):
+    """Per-kernel-class device ms / algorithmic work / launch counts (include/afn.h)."""
+    if reset:
+        _lib.afn_kt_reset()
+    if enable is not None:
+        _lib.afn_kt_enable(1 if enable else 0)
+    n = 16
+    ms = (C.c_double * n)()
+    wk = (C.c_double * n)()
+    ct = (C.c_int64 * n)()
+    m = _lib.afn_kt_read(ms, wk, ct, n)
+    return {KT_NAMES[i]: dict(ms=ms[i], work=wk[i], count=ct[i]) for i in range(min(m, len(KT_NAMES)))}
 
 
 def launch_count() -> int:

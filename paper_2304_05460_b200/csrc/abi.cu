@@ -74,6 +74,58 @@ void dfree(void* p, cudaStream_t st) {
   if (p) cudaFreeAsync(p, st);
 }
 
+// ---- per-kernel timers
+namespace {
+struct KtPending {
+  int id;
+  cudaEvent_t e0, e1;
+  double work;
+};
+std::atomic<bool> g_kt_on{false};
+std::vector<KtPending> g_kt_pending;
+std::vector<cudaEvent_t> g_kt_pool;
+double g_kt_ms[KT_N] = {0};
+double g_kt_work[KT_N] = {0};
+int64_t g_kt_cnt[KT_N] = {0};
+cudaEvent_t g_kt_open[KT_N];
+cudaEvent_t kt_event() {
+  if (!g_kt_pool.empty()) {
+    cudaEvent_t e = g_kt_pool.back();
+    g_kt_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+bool kt_enabled() { return g_kt_on.load(); }
+void kt_begin(int id, cudaStream_t st) {
+  if (!kt_enabled()) return;
+  g_kt_open[id] = kt_event();
+  cudaEventRecord(g_kt_open[id], st);
+}
+void kt_end(int id, cudaStream_t st, double work) {
+  if (!kt_enabled()) return;
+  cudaEvent_t e1 = kt_event();
+  cudaEventRecord(e1, st);
+  g_kt_pending.push_back({id, g_kt_open[id], e1, work});
+}
+void kt_collect() {
+  for (auto& p : g_kt_pending) {
+    cudaEventSynchronize(p.e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.e0, p.e1);
+    g_kt_ms[p.id] += ms;
+    g_kt_work[p.id] += p.work;
+    g_kt_cnt[p.id] += 1;
+    g_kt_pool.push_back(p.e0);
+    g_kt_pool.push_back(p.e1);
+  }
+  g_kt_pending.clear();
+}
+
 namespace {
 
 bool is_dev(const void* p) {
@@ -250,6 +302,13 @@ void handle_free(afn_handle h) {
   delete h;
 }
 
+// algorithmic HBM bytes of one apply: W read twice, L^{-T} twice (upper half),
+// G and G^T (values + 4-byte columns) once each, plus the vectors
+double apply_bytes(afn_handle h) {
+  const double k = (double)h->k, N2 = (double)h->N2, nnz = (double)h->nnz;
+  return 8.0 * (2.0 * N2 * k + k * (k + 1.0)) + 2.0 * 12.0 * nnz + 8.0 * (6.0 * N2 + 6.0 * k);
+}
+
 // z = M^{-1} r in the permuted order (V-form)
 afn_status apply_perm(afn_handle h, const double* r, double* z, cudaStream_t st) {
   const int64_t k = h->k, N2 = h->N2;
@@ -290,6 +349,25 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 extern "C" {
 
 int32_t afn_abi_version(void) { return AFN_ABI_VERSION; }
+
+void afn_kt_enable(int32_t on) {
+  kt_collect();
+  g_kt_on.store(on != 0);
+}
+void afn_kt_reset(void) {
+  kt_collect();
+  for (int i = 0; i < KT_N; ++i) g_kt_ms[i] = g_kt_work[i] = 0.0, g_kt_cnt[i] = 0;
+}
+int32_t afn_kt_read(double* ms, double* work, int64_t* count, int32_t n) {
+  kt_collect();
+  const int m = n < KT_N ? n : KT_N;
+  for (int i = 0; i < m; ++i) {
+    if (ms) ms[i] = g_kt_ms[i];
+    if (work) work[i] = g_kt_work[i];
+    if (count) count[i] = g_kt_cnt[i];
+  }
+  return KT_N;
+}
 const char* afn_last_error(void) { return g_err; }
 int64_t afn_launch_count(void) { return g_launches.load(); }
 
@@ -417,7 +495,9 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   int64_t* idx;
   TRY(halloc(h, (void**)&idx, sizeof(int64_t) * k, st));
   TRY(halloc(h, (void**)&h->fill, sizeof(double) * k, st));
+  kt_begin(KT_FPS, st);
   TRY(fps_run(X, n, d, k, P.fps_seed, idx, h->fill, st));
+  kt_end(KT_FPS, st, 0.0);
   AFN_CUDA(cudaEventRecord(ev[2], st));
 
   // ---- a1: permutation, permuted + prescaled points
@@ -449,9 +529,13 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   int* dinfo;
   TRY(halloc(h, (void**)&dinfo, sizeof(int) * 2, st));
   AFN_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * 2, st));
+  kt_begin(KT_POTRF, st);
   TRY(potrf_lower(h->L, k, dinfo, st));
+  kt_end(KT_POTRF, st, (double)k * k * k / 3.0);
   TRY(halloc(h, (void**)&h->LinvT, sizeof(double) * k * k, st));
+  kt_begin(KT_LINV, st);
   TRY(trsm_linvt(h->L, k, h->LinvT, st));
+  kt_end(KT_LINV, st, (double)k * k * k / 3.0);
   AFN_CUDA(cudaEventRecord(ev[3], st));
   {
     int info = 0;
@@ -469,7 +553,11 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   TRY(halloc(h, (void**)&h->W, sizeof(double) * (size_t)(N2 > 0 ? N2 : 1) * k, st));
   static const bool w_trsm = getenv("AFN_W_TRSM") != nullptr;
   if (w_trsm) TRY(trsm_w(h->L, k, h->Xp, X2, N2, d, P.l, h->W, st));
-  else TRY(w_gemm(h->LinvT, k, h->Xp, X2, N2, d, P.l, h->W, st));
+  else {
+    kt_begin(KT_W_GEMM, st);
+    TRY(w_gemm(h->LinvT, k, h->Xp, X2, N2, d, P.l, h->W, st));
+    kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k);  // N2 k^2/2 FMA
+  }
   AFN_CUDA(cudaEventRecord(ev[4], st));
 
   // ---- a6: kNN pattern
@@ -477,7 +565,9 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   TRY(halloc(h, (void**)&h->rp, sizeof(int64_t) * (N2 + 1), st));
   TRY(halloc(h, (void**)&h->col, sizeof(int32_t) * (h->nnz > 0 ? h->nnz : 1), st));
   if (N2 > 0) {
+    kt_begin(KT_KNN, st);
     TRY(knn_run(X2, N2, d, P.w, h->rp, h->col, st));
+    kt_end(KT_KNN, st, 0.0);
     check_pattern_kernel<<<(unsigned)((N2 + 255) / 256), 256, 0, st>>>(h->rp, h->col, N2, derr);
     AFN_LAUNCH_CHECK("check_pattern_kernel");
   } else {
@@ -500,10 +590,25 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   AFN_CUDA(cudaEventRecord(ef0, st));
   AFN_CUDA(cudaEventRecord(ef1, st));
   if (N2 > 0) {
+    int64_t* tmap = nullptr;
+    TRY(halloc(h, (void**)&tmap, sizeof(int64_t) * (h->nnz > 0 ? h->nnz : 1), st));
+    // transposed pattern first (the pair-union FSAI needs "rows containing a")
+    TRY(csr_transpose(h->rp, h->col, nullptr, N2, h->nnz, h->trp, h->tcol, nullptr, st, tmap));
     AFN_CUDA(cudaEventRecord(ef0, st));
-    TRY(fsai_run(X2, N2, d, P.l, P.mu, h->W, k, h->rp, h->col, h->gval, dinfo + 1, st));
+    static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : -1;
+    afn_status fs = AFN_ERR_STATE;
+    if (variant < 0) {
+      fs = fsai_sddmm_run(X2, N2, d, P.l, P.mu, h->W, k, h->rp, h->col, h->trp, h->tcol, h->gval,
+                          dinfo + 1, st);
+      if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
+    }
+    if (fs != AFN_OK) {
+      kt_begin(KT_FSAI_GRAM, st);
+      TRY(fsai_run(X2, N2, d, P.l, P.mu, h->W, k, h->rp, h->col, h->gval, dinfo + 1, st));
+      kt_end(KT_FSAI_GRAM, st, 0.0);
+    }
     AFN_CUDA(cudaEventRecord(ef1, st));
-    TRY(csr_transpose(h->rp, h->col, h->gval, N2, h->nnz, h->trp, h->tcol, h->tval, st));
+    TRY(gather_map(h->gval, tmap, h->nnz, h->tval, st));
   } else {
     AFN_CUDA(cudaMemsetAsync(h->trp, 0, sizeof(int64_t), st));
   }
@@ -555,6 +660,7 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
   h->ms[5] = ev_ms(ev[5], ev[6]);  // fsai + G^T
   h->ms[6] = ev_ms(ev[0], ev[7]);  // total
   h->ms[7] = ev_ms(ef0, ef1);      // fsai row kernel
+  kt_collect();
   *out = h;
   h = nullptr;  // release the guard
   return AFN_OK;
@@ -624,7 +730,9 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     TRY(vec_copy(h->p, h->z, n, st));
     for (it = 1; it <= maxit; ++it) {
       AFN_CUDA(cudaEventRecord(km0, st));
+      kt_begin(KT_KMV, st);
       TRY(kmv_launch(h->Xs, n, d, h->p, h->mu, 0, n, h->q, h->kmv_part, h->plan, st));
+      kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0));
       AFN_CUDA(cudaEventRecord(km1, st));
       TRY(dot(h->p, h->q, n, h->sc + SC_PQ, h->dws, h->dcnt, st));
       TRY(pcg_update_xr(h->x, h->r, h->p, h->q, n, h->sc, cur, h->dws, h->dcnt, st));
@@ -653,7 +761,9 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
         break;
       }
       AFN_CUDA(cudaEventRecord(ap0, st));
+      kt_begin(KT_APPLY, st);
       TRY(apply_perm(h, h->r, h->z, st));
+      kt_end(KT_APPLY, st, apply_bytes(h));
       AFN_CUDA(cudaEventRecord(ap1, st));
       ap_pending = true;
       ++napply;
@@ -686,6 +796,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   if (ap_pending) ap_ms += ev_ms(ap0, ap1);
   R.matvec_ms = mv_ms;
   R.apply_ms = ap_ms;
+  kt_collect();
   R.applies = napply;
   if (rep) *rep = R;
   return AFN_OK;

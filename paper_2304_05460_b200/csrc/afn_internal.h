@@ -10,6 +10,14 @@ namespace afn {
 
 int num_sms();  // SM count of the current device (cached per device)
 
+// ---- optional per-kernel CUDA-event timers (bench.py roofline) -------------
+enum KtId { KT_KMV = 0, KT_FSAI_GEMM, KT_FSAI_ASM, KT_FSAI_CHOL, KT_FSAI_GRAM, KT_FPS, KT_W_GEMM,
+            KT_LINV, KT_POTRF, KT_KNN, KT_APPLY, KT_ALG1, KT_N };
+bool kt_enabled();
+void kt_begin(int id, cudaStream_t st);
+void kt_end(int id, cudaStream_t st, double work);  // work: algorithmic flops (or bytes)
+void kt_collect();                                  // after a stream sync
+
 // Stream-ordered device allocation helpers (cudaMallocAsync pool).
 afn_status dalloc(void** p, size_t bytes, cudaStream_t st);
 void dfree(void* p, cudaStream_t st);
@@ -58,9 +66,17 @@ afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st
 afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
                     int64_t k, const int64_t* row_ptr, const int32_t* col, double* gval,
                     int* d_info, cudaStream_t st);
-// CSR transpose (N x N, columns sorted within each output row)
+// CSR transpose (N x N, columns sorted within each output row).  val/tval may
+// be null (pattern only); tmap (optional) receives the source nnz index.
 afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* val, int64_t N,
-                         int64_t nnz, int64_t* trp, int32_t* tcol, double* tval, cudaStream_t st);
+                         int64_t nnz, int64_t* trp, int32_t* tcol, double* tval, cudaStream_t st,
+                         int64_t* tmap = nullptr);
+afn_status gather_map(const double* v, const int64_t* map, int64_t nnz, double* out, cudaStream_t st);
+// FSAI through the union of needed Schur-complement pairs (fsai_sddmm.cu).
+// Returns AFN_ERR_STATE (nothing written) if a group's pair union overflows.
+afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
+                          int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
+                          const int32_t* tcol, double* gval, int* d_info, cudaStream_t st);
 
 // ---- BLAS-2 / SpMV / vectors (blas.cu) ------------------------------------
 // y = ybase + alpha * A x, A: R x C row-major (lda = C).  ybase may be null (0)

@@ -248,12 +248,15 @@ __global__ void eig_summary_kernel(const double* dgl, const double* off, int m, 
 // Kp after r threshold-pivoted elimination steps.  SM: work matrix in shared
 // memory, else in the m x m global scratch Wg.
 template <bool SM>
-__global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict__ Kp, int m, int r,
-                                                        double thr, double tau, double* Wg, int* pass) {
+__global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict__ Kp, int m,
+                                                        const int* __restrict__ rlist, double thr,
+                                                        double tau, double* Wg, int* pass) {
   extern __shared__ double dsm[];
   __shared__ double s_piv;
   __shared__ int s_ok;
-  double* W = SM ? dsm : Wg;
+  const int r = rlist[blockIdx.x];
+  double* W = SM ? dsm : Wg + (int64_t)blockIdx.x * m * m;
+  pass += blockIdx.x;
   const int tid = threadIdx.x;
   for (int64_t e = tid; e < (int64_t)m * m; e += AT) W[e] = Kp[e];
   if (tid == 0) s_ok = 1;
@@ -405,26 +408,40 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
   const double thr = (double)m * DBL_EPSILON * normK;
   const double tau = 0.1 * normK;
 
-  // ---- 3. smallest r in [1, m] with ||S^(r)|| < 0.1 ||K_m|| (pass(m) = true)
-  auto test = [&](int r, int* out) -> afn_status {
-    if (m <= SM_MAX_M) {
-      const size_t bytes = sizeof(double) * (size_t)m * m;
-      AFN_CUDA(cudaFuncSetAttribute(schur_test_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      schur_test_kernel<true><<<1, AT, bytes, st>>>(Kp, m, r, thr, tau, Wk, pass);
-    } else {
-      schur_test_kernel<false><<<1, AT, 0, st>>>(Kp, m, r, thr, tau, Wk, pass);
-    }
-    AFN_LAUNCH_CHECK("schur_test_kernel");
-    AFN_CUDA(cudaMemcpyAsync(out, pass, sizeof(int), cudaMemcpyDeviceToHost, st));
-    AFN_CUDA(cudaStreamSynchronize(st));
-    return AFN_OK;
-  };
+  // ---- 3. smallest r in [1, m] with ||S^(r)|| < 0.1 ||K_m|| (pass(m) = true).
+  // Multisection: up to 32 probes per round run as independent CTAs.
+  constexpr int NPROBE = 32;
+  int* rdev;
+  int* pdev;
+  double* Wp = nullptr;
+  if ((s = get((void**)&rdev, sizeof(int) * NPROBE)) != AFN_OK) return s;
+  if ((s = get((void**)&pdev, sizeof(int) * NPROBE)) != AFN_OK) return s;
+  if (m > SM_MAX_M && (s = get((void**)&Wp, sizeof(double) * mm * NPROBE)) != AFN_OK) return s;
+  const size_t smb = sizeof(double) * mm;
+  if (m <= SM_MAX_M)
+    AFN_CUDA(cudaFuncSetAttribute(schur_test_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
   int lo = 0, hi = m;  // pass(hi) true, pass(lo) false (lo = 0: no landmarks)
   while (hi - lo > 1) {
-    const int mid = lo + (hi - lo) / 2;
-    int ok = 0;
-    if ((s = test(mid, &ok)) != AFN_OK) return s;
-    if (ok) hi = mid; else lo = mid;
+    int rs[NPROBE];
+    int np = 0;
+    const int span = hi - lo;
+    const int want = std::min(NPROBE, span - 1);
+    for (int j = 1; j <= want; ++j) {
+      const int r = lo + (int)(((int64_t)j * span) / (want + 1));
+      if (r > lo && r < hi && (np == 0 || r != rs[np - 1])) rs[np++] = r;
+    }
+    AFN_CUDA(cudaMemcpyAsync(rdev, rs, sizeof(int) * np, cudaMemcpyHostToDevice, st));
+    if (m <= SM_MAX_M) schur_test_kernel<true><<<np, AT, smb, st>>>(Kp, m, rdev, thr, tau, Wk, pdev);
+    else schur_test_kernel<false><<<np, AT, 0, st>>>(Kp, m, rdev, thr, tau, Wp, pdev);
+    AFN_LAUNCH_CHECK("schur_test_kernel");
+    int ok[NPROBE];
+    AFN_CUDA(cudaMemcpyAsync(ok, pdev, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    int first = np;
+    for (int j = 0; j < np; ++j)
+      if (ok[j]) { first = j; break; }
+    if (first < np) hi = rs[first];
+    if (first > 0) lo = rs[first - 1];
   }
   const int r = hi;
   int64_t khat = (2LL * r * n + m) / (2LL * m);

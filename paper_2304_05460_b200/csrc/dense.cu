@@ -7,6 +7,7 @@
 // stride-16 mapping (conflict-free shared-memory broadcasts).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "afn_common.cuh"
 #include "afn_internal.h"
@@ -311,6 +312,8 @@ __global__ void __launch_bounds__(DT) trsm_rows_kernel(const double* __restrict_
 
 constexpr size_t SMEM2 = sizeof(double) * 2 * NB * TP;
 
+__global__ void diag_inv_kernel(const double* __restrict__ Lp, int64_t kp, double* __restrict__ X);
+
 afn_status set_smem_once() {
   static bool done[64] = {false};
   int dev = 0;
@@ -320,6 +323,7 @@ afn_status set_smem_once() {
   AFN_CUDA(cudaFuncSetAttribute(potrf_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
   AFN_CUDA(cudaFuncSetAttribute(trsm_rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
   AFN_CUDA(cudaFuncSetAttribute(trsm_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
+  AFN_CUDA(cudaFuncSetAttribute(diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
   if (dev >= 0 && dev < 64) done[dev] = true;
   return AFN_OK;
 }
@@ -426,6 +430,138 @@ __global__ void __launch_bounds__(256, 2) gemm_nn_bupper_kernel(const double* __
   }
 }
 
+
+// -------------------------------------------------------------------------
+// L^{-1} by recursive 2x2 block inversion on a power-of-two padding kp:
+//   inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 B A^-1, C^-1]]
+// 64x64 diagonal blocks first (in-smem triangular solves), then one batched
+// pair of GEMMs per level (all independent tiles) -> log2(kp/64) levels.
+// Mode 1: A lower (K range <= row end); mode 2: B lower (K range >= col start).
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) gemm_nn_batched_kernel(const double* __restrict__ A,
+                                                                const double* __restrict__ B,
+                                                                double* __restrict__ Cm, int64_t n,
+                                                                int64_t ld, int64_t sA, int64_t sB,
+                                                                int64_t sC, double alpha) {
+  extern __shared__ __align__(16) double gsm[];
+  double* sAs = gsm;
+  double* sBs = gsm + 2 * GK * GPA;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int64_t z = blockIdx.z;
+  A += z * sA;
+  B += z * sB;
+  Cm += z * sC;
+  const int64_t R0 = (int64_t)blockIdx.y * GM, C0 = (int64_t)blockIdx.x * GN;
+  int64_t kbeg = 0, kend = n;
+  if (MODE == 1) kend = min(n, R0 + GM);
+  if (MODE == 2) kbeg = C0;
+  const int64_t kb0 = kbeg / GK;
+  const int64_t nkb = (kend + GK - 1) / GK - kb0;
+  auto stage = [&](int64_t kb, int buf) {
+    const int64_t k0 = (kb0 + kb) * GK;
+    double* a = sAs + buf * GK * GPA;
+    double* b = sBs + buf * GK * GPB;
+    for (int e = tid; e < GM * GK; e += 256) {
+      const int r = e / GK, kk = e - r * GK;
+      const int64_t gr = R0 + r, gk = k0 + kk;
+      if (gr < n && gk < kend) cpa8(&a[kk * GPA + r], &A[gr * ld + gk]);
+      else a[kk * GPA + r] = 0.0;
+    }
+    for (int e = tid; e < GK * GN; e += 256) {
+      const int kk = e / GN, c = e - kk * GN;
+      const int64_t gk = k0 + kk, gc = C0 + c;
+      if (gk < kend && gc < n) cpa8(&b[kk * GPB + c], &B[gk * ld + gc]);
+      else b[kk * GPB + c] = 0.0;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+  if (nkb > 0) stage(0, 0);
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int buf = (int)(kb & 1);
+    if (kb + 1 < nkb) {
+      stage(kb + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* a = sAs + buf * GK * GPA;
+    const double* b = sBs + buf * GK * GPB;
+#pragma unroll 4
+    for (int kk = 0; kk < GK; ++kk) {
+      double av[8], bv[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) av[i] = a[kk * GPA + ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = b[kk * GPB + tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = R0 + ty + 16 * i;
+    if (r >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = C0 + tx + 16 * j;
+      if (c < n) Cm[r * ld + c] = alpha * acc[i][j];
+    }
+  }
+}
+
+// pad L (k x k) into Lp (kp x kp): identity beyond k, zero elsewhere
+__global__ void pad_l_kernel(const double* __restrict__ L, int64_t k, double* __restrict__ Lp, int64_t kp) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kp * kp) return;
+  const int64_t i = e / kp, j = e - i * kp;
+  Lp[e] = (i < k && j < k) ? (j <= i ? L[i * k + j] : 0.0) : (i == j ? 1.0 : 0.0);
+}
+
+// X_bb = inverse of the 64x64 diagonal block b of Lp (lower), written into X
+__global__ void __launch_bounds__(DT) diag_inv_kernel(const double* __restrict__ Lp, int64_t kp,
+                                                      double* __restrict__ X) {  // (declared above)
+  extern __shared__ double dsm[];
+  double* sT = dsm;
+  double* sL = dsm + NB * TP;
+  const int64_t b0 = (int64_t)blockIdx.x * NB;
+  for (int e = threadIdx.x; e < NB * NB; e += DT) {
+    const int r = e / NB, c = e % NB;
+    sL[r * TP + c] = Lp[(b0 + r) * kp + b0 + c];
+    sT[r * TP + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  rows_trsm_64(sT, sL, NB);  // sT = I * Lbb^{-T} = Lbb^{-T}
+  __syncthreads();
+  for (int e = threadIdx.x; e < NB * NB; e += DT) {
+    const int r = e / NB, c = e % NB;  // X[r][c] = (Lbb^{-T})[c][r]
+    X[(b0 + r) * kp + b0 + c] = sT[c * TP + r];
+  }
+}
+
+// LinvT[i][j] = X[j][i] for i, j < k (32x32 smem transpose tiles)
+__global__ void transpose_k_kernel(const double* __restrict__ X, int64_t kp, int64_t k, double* __restrict__ LinvT) {
+  __shared__ double t[32][33];
+  const int64_t bi = (int64_t)blockIdx.y * 32, bj = (int64_t)blockIdx.x * 32;
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = bi + r, j = bj + threadIdx.x;
+    t[r][threadIdx.x] = (i < k && j < k) ? X[i * kp + j] : 0.0;
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int64_t i = bj + r, j = bi + threadIdx.x;
+    if (i < k && j < k) LinvT[i * k + j] = t[threadIdx.x][r];
+  }
+}
+
 __global__ void zero_upper_kernel(double* __restrict__ A, int64_t k) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
@@ -504,7 +640,51 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
   return AFN_OK;
 }
 
+afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_t st) {
+  int64_t kp = NB;
+  while (kp < k) kp <<= 1;
+  double *Lp = nullptr, *X = nullptr, *Tt = nullptr;
+  afn_status s;
+  if ((s = dalloc((void**)&Lp, sizeof(double) * kp * kp, st)) != AFN_OK) return s;
+  if ((s = dalloc((void**)&X, sizeof(double) * kp * kp, st)) != AFN_OK) { dfree(Lp, st); return s; }
+  if ((s = dalloc((void**)&Tt, sizeof(double) * kp * kp, st)) != AFN_OK) { dfree(Lp, st); dfree(X, st); return s; }
+  struct F { double *a, *b, *c; cudaStream_t st; ~F() { dfree(a, st); dfree(b, st); dfree(c, st); } } fr{Lp, X, Tt, st};
+  AFN_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kp * kp, st));
+  pad_l_kernel<<<(unsigned)((kp * kp + 255) / 256), 256, 0, st>>>(L, k, Lp, kp);
+  AFN_LAUNCH_CHECK("pad_l_kernel");
+  diag_inv_kernel<<<(unsigned)(kp / NB), DT, SMEM2, st>>>(Lp, kp, X);
+  AFN_LAUNCH_CHECK("diag_inv_kernel");
+  static bool attr = false;
+  const int bytes = (int)(sizeof(double) * 2 * GK * (GPA + GPB));
+  if (!attr) {
+    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_batched_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_batched_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  for (int64_t h = NB; h < kp; h <<= 1) {
+    const int64_t pairs = kp / (2 * h);
+    const int64_t stride = 2 * h * kp + 2 * h;  // next diagonal pair
+    dim3 grid((unsigned)((h + GN - 1) / GN), (unsigned)((h + GM - 1) / GM), (unsigned)pairs);
+    // T = B * A^{-1}   (B = Lp[h.., 0..h), A^{-1} = X[0..h, 0..h) lower -> K >= col start)
+    gemm_nn_batched_kernel<2><<<grid, 256, bytes, st>>>(Lp + h * kp, X, Tt, h, kp, stride, stride, stride, 1.0);
+    AFN_LAUNCH_CHECK("gemm_nn_batched_kernel<2>");
+    // X21 = -C^{-1} * T   (C^{-1} = X[h.., h..) lower -> K <= row end)
+    gemm_nn_batched_kernel<1><<<grid, 256, bytes, st>>>(X + h * kp + h, Tt, X + h * kp, h, kp, stride, stride,
+                                                        stride, -1.0);
+    AFN_LAUNCH_CHECK("gemm_nn_batched_kernel<1>");
+  }
+  dim3 tg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
+  transpose_k_kernel<<<tg, dim3(32, 8), 0, st>>>(X, kp, k, LinvT);
+  AFN_LAUNCH_CHECK("transpose_k_kernel");
+  return AFN_OK;
+}
+
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st) {
+  static const bool legacy = getenv("AFN_LINV_TRSM") != nullptr;
+  if (!legacy) {
+    TRY_SMEM();
+    return linv_recursive(L, k, LinvT, st);
+  }
   TRY_SMEM();
   trsm_rows_kernel<1><<<(unsigned)((k + NB - 1) / NB), DT, SMEM2, st>>>(L, k, nullptr, nullptr, k, 1,
                                                                    0.0, LinvT);

@@ -246,6 +246,21 @@ afn_status launch_fps(const double* X, int64_t n, int d, int64_t k, int64_t seed
 }
 
 
+
+// (d2 desc, index asc) argmax across a warp with three redux.sync reductions.
+// key = bits(d2) + 1 for d2 >= 0 (monotone), 0 for selected (-1) / padding.
+__device__ __forceinline__ unsigned long long fps_key(double d) {
+  return d >= 0.0 ? (unsigned long long)__double_as_longlong(d) + 1ULL : 0ULL;
+}
+__device__ __forceinline__ void warp_argmax_key(unsigned long long key, unsigned idx,
+                                                unsigned long long& wkey, unsigned& widx) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  wkey = ((unsigned long long)mhi << 32) | mlo;
+  widx = __reduce_min_sync(0xffffffffu, key == wkey ? idx : 0xffffffffu);
+}
+
 // ---------------------------------------------------------------------------
 // Cluster variant (n up to 16 CTAs x NT x 2 points): the per-step exchange is
 // a cluster barrier plus distributed-shared-memory reads of the CL per-CTA
@@ -290,67 +305,46 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
 
   for (int64_t step = 1; step <= k; ++step) {
     const int par = (int)(step & 1);
+    // thread-local best (indices ascend with s: strict > keeps the lowest)
     double bd = -3.0;
-    long long bi = 0x7fffffffffffffffLL;
-    double bc[DP];
+    unsigned bi = 0xffffffffu;
+    int bs = 0;
 #pragma unroll
-    for (int c = 0; c < DP; ++c) bc[c] = 0.0;
+    for (int s = 0; s < P; ++s)
+      if (mind[s] > bd) { bd = mind[s]; bi = (unsigned)(gtid + s * stride); bs = s; }
+    unsigned long long wkey;
+    unsigned widx;
+    warp_argmax_key(fps_key(bd), bi, wkey, widx);
+    if (bi == widx) {
+      s_w[wid][0] = bd;
+      s_w[wid][1] = __longlong_as_double((long long)widx);
 #pragma unroll
-    for (int s = 0; s < P; ++s) {
-      if (mind[s] > bd) {
-        bd = mind[s];
-        bi = gtid + s * stride;
-#pragma unroll
-        for (int c = 0; c < DP; ++c) bc[c] = pts[s][c];
-      }
-    }
-    double wd = bd;
-    long long wi = bi;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double od = __shfl_xor_sync(0xffffffffu, wd, o);
-      const long long oi = __shfl_xor_sync(0xffffffffu, wi, o);
-      if (better(od, oi, wd, wi)) { wd = od; wi = oi; }
-    }
-    if (bi == wi && bd == wd) {
-      s_w[wid][0] = wd;
-      s_w[wid][1] = __longlong_as_double(wi);
-#pragma unroll
-      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = bc[c];
+      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pts[bs][c];
     }
     __syncthreads();
     if (wid == 0) {
-      double vd = lane < NW ? s_w[lane][0] : -3.0;
-      long long vi = lane < NW ? __double_as_longlong(s_w[lane][1]) : 0x7fffffffffffffffLL;
-      int src = lane;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double od = __shfl_xor_sync(0xffffffffu, vd, o);
-        const long long oi = __shfl_xor_sync(0xffffffffu, vi, o);
-        const int os = __shfl_xor_sync(0xffffffffu, src, o);
-        if (better(od, oi, vd, vi)) { vd = od; vi = oi; src = os; }
-      }
+      const double vd = lane < NW ? s_w[lane][0] : -3.0;
+      const unsigned vi = lane < NW ? (unsigned)__double_as_longlong(s_w[lane][1]) : 0xffffffffu;
+      unsigned long long k2;
+      unsigned i2;
+      warp_argmax_key(fps_key(vd), vi, k2, i2);
+      const int src = __ffs(__ballot_sync(0xffffffffu, lane < NW && vi == i2)) - 1;
       if (lane < S) s_slot[par][lane] = s_w[src][lane];
     }
     cl.sync();
     if (wid == 0) {
       double gd = -3.0;
-      long long gi = 0x7fffffffffffffffLL;
-      int gsrc = 0;
+      unsigned gi = 0xffffffffu;
       if (lane < CL) {
         const double* rs = cl.map_shared_rank(&s_slot[par][0], lane);
         gd = rs[0];
-        gi = __double_as_longlong(rs[1]);
-        gsrc = lane;
+        gi = (unsigned)__double_as_longlong(rs[1]);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double od = __shfl_xor_sync(0xffffffffu, gd, o);
-        const long long oi = __shfl_xor_sync(0xffffffffu, gi, o);
-        const int os = __shfl_xor_sync(0xffffffffu, gsrc, o);
-        if (better(od, oi, gd, gi)) { gd = od; gi = oi; gsrc = os; }
-      }
-      if (lane < S) s_new[lane] = cl.map_shared_rank(&s_slot[par][0], gsrc)[lane];
+      unsigned long long k3;
+      unsigned i3;
+      warp_argmax_key(fps_key(gd), gi, k3, i3);
+      const int src = __ffs(__ballot_sync(0xffffffffu, lane < CL && gi == i3)) - 1;
+      if (lane < S) s_new[lane] = cl.map_shared_rank(&s_slot[par][0], src)[lane];
     }
     __syncthreads();
     const double nd = s_new[0];

@@ -19,10 +19,13 @@
 #include "afn_internal.h"
 
 namespace afn {
+afn_status fsai_chol_batch(int64_t r0, int64_t nrows, int MT, const int64_t* rp, double* Sg,
+                           double* gval, int* info, cudaStream_t st);
 namespace {
 
 constexpr int FT = 256;  // threads
 constexpr int KC = 32;   // W columns per chunk
+constexpr int GSTAGES = 3;  // cp.async pipeline depth of the split Gram kernel
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -33,6 +36,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ int pk(int a, int b) { return a * (a + 1) / 2 + b; }  // packed lower, b <= a
+// column-major packed lower of a wp x wp matrix: entry (a, t), a >= t
+__device__ __forceinline__ int cmo(int a, int t, int wp) { return t * wp - (t * (t - 1)) / 2 + (a - t); }
 
 template <int MT>
 __global__ void __launch_bounds__(FT, 2)
@@ -221,10 +226,11 @@ fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, double cl, do
                  const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
                  const int32_t* __restrict__ col, double* __restrict__ Sg) {
   constexpr int WP = MT * 16;
-  constexpr int PW = WP + 1;
+  constexpr int PW2 = 2 * WP + 2;          // pitch of one kk-pair row (double2 per a)
   constexpr int SPK = WP * (WP + 1) / 2;
   extern __shared__ __align__(16) double smem[];
-  constexpr int STG = 2 * KC * PW;
+  constexpr int STG1 = (KC / 2) * PW2;      // one staging buffer
+  constexpr int STG = GSTAGES * STG1;
   double* stg = smem;
   double* sX = smem + STG;
   int* sJ = reinterpret_cast<int*>(sX + WP * d);
@@ -246,47 +252,52 @@ fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, double cl, do
   for (int t = 0; t < MT * (MT + 1) / 2; ++t) acc[t] = 0.0;
   const int64_t nch = (k + KC - 1) / KC;
   auto issue = [&](int64_t ch, int buf) {
-    double* dst = stg + buf * KC * PW;
+    double* dst = stg + buf * STG1;
     const int64_t c0 = ch * KC;
     for (int e = tid; e < WP * KC; e += FT) {
       const int a = e / KC, kk = e - a * KC;
       const int64_t c = c0 + kk;
       const int ja = sJ[a];
-      if (ja >= 0 && c < k) cp_async8(&dst[kk * PW + a], &W[(int64_t)ja * k + c]);
-      else dst[kk * PW + a] = 0.0;
+      double* q = &dst[(kk >> 1) * PW2 + 2 * a + (kk & 1)];
+      if (ja >= 0 && c < k) cp_async8(q, &W[(int64_t)ja * k + c]);
+      else *q = 0.0;
     }
     cp_async_commit();
   };
-  if (nch > 0) issue(0, 0);
+  // GSTAGES-deep cp.async pipeline over the k chunks
+#pragma unroll
+  for (int st0 = 0; st0 < GSTAGES - 1; ++st0) {
+    if (st0 < nch) issue(st0, st0);
+    else cp_async_commit();
+  }
   for (int64_t ch = 0; ch < nch; ++ch) {
-    const int buf = (int)(ch & 1);
-    if (ch + 1 < nch) {
-      issue(ch + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<GSTAGES - 2>();
     __syncthreads();
-    const double* T = stg + buf * KC * PW;
-#pragma unroll 2
-    for (int kk = 0; kk < KC; ++kk) {
-      double a[MT], b[MT];
+    const int64_t nx = ch + GSTAGES - 1;
+    if (nx < nch) issue(nx, (int)(nx % GSTAGES));
+    else cp_async_commit();
+    const double* T = stg + (int)(ch % GSTAGES) * STG1;
+#pragma unroll 1
+    for (int k2 = 0; k2 < KC / 2; ++k2) {
+      double2 a[MT], b[MT];
 #pragma unroll
       for (int m = 0; m < MT; ++m) {
-        a[m] = T[kk * PW + ty + 16 * m];
-        b[m] = T[kk * PW + tx + 16 * m];
+        a[m] = *reinterpret_cast<const double2*>(&T[k2 * PW2 + 2 * (ty + 16 * m)]);
+        b[m] = *reinterpret_cast<const double2*>(&T[k2 * PW2 + 2 * (tx + 16 * m)]);
       }
       int t = 0;
 #pragma unroll
       for (int m = 0; m < MT; ++m)
 #pragma unroll
         for (int q = 0; q <= m; ++q) {
-          acc[t] = fma(a[m], b[q], acc[t]);
+          acc[t] = fma(a[m].x, b[q].x, acc[t]);
+          acc[t] = fma(a[m].y, b[q].y, acc[t]);
           ++t;
         }
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
+  __syncthreads();
   double* S = Sg + (int64_t)blockIdx.x * SPK;
   int t = 0;
 #pragma unroll
@@ -302,71 +313,100 @@ fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, double cl, do
           const double sd = d2_exact_rt(&sX[a * d], &sX[b * d], d);
           kv = gauss_from_d2(sd, cl, s_tab);
         }
-        S[pk(a, b)] = kv - acc[t];
+        S[cmo(a, b, wp)] = kv - acc[t];
       }
       ++t;
     }
 }
 
-// one warp per row: left-looking (Crout) Cholesky of the packed S_JJ in place,
-// then g = R^{-T} e_last
+// one warp per row: blocked left-looking (Crout) Cholesky of S_JJ in shared
+// memory, then g = R^{-T} e_last.  S arrives column-major packed lower (entry
+// (a, t), a >= t, at cmo(a, t, wp)), so the lanes' row-parallel updates read
+// consecutive addresses.  Columns are factored in panels of 4: each loaded
+// L[a][t] feeds 4 FMAs (one per panel column) before the in-panel solve.
+// Shared memory per warp: wmax(wmax+1)/2 + wmax doubles; blockDim = 32 * CW.
 template <int MT>
 __global__ void __launch_bounds__(256)
-fsai_chol_kernel(int64_t r0, int64_t nrows, const int64_t* __restrict__ rp, double* __restrict__ Sg,
-                 double* __restrict__ gval, int* info) {
+fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict__ rp,
+                 double* __restrict__ Sg, double* __restrict__ gval, int* info) {
   constexpr int WP = MT * 16;
   constexpr int SPK = WP * (WP + 1) / 2;
-  const int64_t wr = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
+  extern __shared__ __align__(16) double csm[];
+  const int CW = blockDim.x >> 5;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t wr = (int64_t)blockIdx.x * CW + wid;
   if (wr >= nrows) return;
+  const int per = wmax * (wmax + 1) / 2 + wmax;
+  double* L = csm + (int64_t)wid * per;
+  double* gs = L + wmax * (wmax + 1) / 2;
   const int64_t i = r0 + wr;
   const int64_t beg = rp[i];
   const int wp = (int)(rp[i + 1] - beg);
-  double* S = Sg + wr * SPK;
+  const int ne = wp * (wp + 1) / 2;
+  const double* src = Sg + wr * SPK;
+  for (int e = lane; e < ne; e += 32) L[e] = src[e];
+  __syncwarp();
   bool bad = false;
-  for (int j = 0; j < wp; ++j) {
-    const double* Lj = S + pk(j, 0);
-    // diagonal: S_jj - sum_t L_jt^2
-    double s = 0.0;
-    for (int t = lane; t < j; t += 32) s = fma(Lj[t], Lj[t], s);
-    s = warp_sum(s);
-    double djj = S[pk(j, j)] - s;
-    if (!(djj > 0.0)) { bad = true; djj = 1.0; }
-    const double piv = sqrt(djj);
-    const double inv = 1.0 / piv;
-    // column j below the diagonal: rows a = j+1.., lane-strided, dot over t < j
-    for (int a = j + 1 + lane; a < wp; a += 32) {
-      const double* La = S + pk(a, 0);
-      double acc = La[j];
-      for (int t = 0; t < j; ++t) acc = fma(-La[t], Lj[t], acc);
-      S[pk(a, j)] = acc * inv;
+  for (int j0 = 0; j0 < wp; j0 += 4) {
+    const int nc = min(4, wp - j0);
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int a = j0 + lane + 32 * r;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = (c < nc && a < wp && a >= j0 + c) ? L[cmo(a, j0 + c, wp)] : 0.0;
     }
-    __syncwarp();
-    if (lane == 0) S[pk(j, j)] = piv;
+    int cb = 0;  // column base of column t: t*wp - t(t-1)/2
+    for (int t = 0; t < j0; ++t) {
+      double lj[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) lj[c] = c < nc ? L[cb + j0 + c - t] : 0.0;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int a = j0 + lane + 32 * r;
+        const double la = a < wp ? L[cb + a - t] : 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(-la, lj[c], acc[r][c]);
+      }
+      cb += wp - t;
+    }
+    // in-panel factorisation (row j0 + c is lane c, r = 0)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c >= nc) break;
+      const int j = j0 + c;
+      double dj = __shfl_sync(0xffffffffu, acc[0][c], c);
+      if (!(dj > 0.0)) { bad = true; dj = 1.0; }
+      const double piv = sqrt(dj);
+      const double inv = 1.0 / piv;
+      double lv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int a = j0 + lane + 32 * r;
+        lv[r] = (a > j && a < wp) ? acc[r][c] * inv : 0.0;
+        if (a > j && a < wp) L[cmo(a, j, wp)] = lv[r];
+      }
+      if (lane == c) L[cmo(j, j, wp)] = piv;
+#pragma unroll
+      for (int c2 = c + 1; c2 < 4; ++c2) {
+        const double l2 = __shfl_sync(0xffffffffu, lv[0], c2);  // L[j0 + c2][j]
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[r][c2] = fma(-lv[r], l2, acc[r][c2]);
+      }
+    }
     __syncwarp();
   }
   if (bad && lane == 0) atomicCAS(info, 0, (int)(i + 1));
-  double rhs[(WP + 31) / 32];
-#pragma unroll
-  for (int s = 0; s < (WP + 31) / 32; ++s) rhs[s] = (lane + 32 * s == wp - 1) ? 1.0 : 0.0;
+  // g_j = (e_j - sum_{t>j} R[t][j] g_t) / R[j][j], j = wp-1 .. 0 (column j contiguous)
   for (int j = wp - 1; j >= 0; --j) {
-    double gj = 0.0;
-#pragma unroll
-    for (int s = 0; s < (WP + 31) / 32; ++s)
-      if (lane + 32 * s == j) gj = rhs[s] / S[pk(j, j)];
-    gj = __shfl_sync(0xffffffffu, gj, j & 31);
-#pragma unroll
-    for (int s = 0; s < (WP + 31) / 32; ++s) {
-      const int tt = lane + 32 * s;
-      if (tt < j) rhs[s] = fma(-S[pk(j, tt)], gj, rhs[s]);
-      else if (tt == j) rhs[s] = gj;
-    }
+    double s = 0.0;
+    const int cbj = cmo(j, j, wp);
+    for (int t = j + 1 + lane; t < wp; t += 32) s = fma(L[cbj + t - j], gs[t], s);
+    s = warp_sum(s);
+    if (lane == 0) gs[j] = ((j == wp - 1 ? 1.0 : 0.0) - s) / L[cbj];
+    __syncwarp();
   }
-#pragma unroll
-  for (int s = 0; s < (WP + 31) / 32; ++s) {
-    const int tt = lane + 32 * s;
-    if (tt < wp) gval[beg + tt] = rhs[s];
-  }
+  for (int t = lane; t < wp; t += 32) gval[beg + t] = gs[t];
 }
 
 template <int MT>
@@ -376,7 +416,9 @@ afn_status launch_fsai_split(const double* X2, int64_t N, int d, double cl, doub
   constexpr int WP = MT * 16;
   constexpr int PW = WP + 1;
   constexpr int64_t SPK = WP * (WP + 1) / 2;
-  const size_t bytes = sizeof(double) * (2 * (size_t)KC * PW + (size_t)WP * d) + sizeof(int) * WP + 16;
+  (void)PW;
+  const size_t bytes = sizeof(double) * (GSTAGES * (size_t)(KC / 2) * (2 * WP + 2) + (size_t)WP * d) +
+                       sizeof(int) * WP + 16;
   auto kg = fsai_gram_kernel<MT>;
   AFN_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   const int64_t batch = std::min<int64_t>(N, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
@@ -387,8 +429,8 @@ afn_status launch_fsai_split(const double* X2, int64_t N, int d, double cl, doub
     const int64_t nr = std::min(batch, N - r0);
     kg<<<(unsigned)nr, FT, bytes, st>>>(X2, r0, d, cl, mu, W, k, rp, col, Sg);
     AFN_LAUNCH_CHECK("fsai_gram_kernel");
-    fsai_chol_kernel<MT><<<(unsigned)((nr + 7) / 8), 256, 0, st>>>(r0, nr, rp, Sg, gval, info);
-    AFN_LAUNCH_CHECK("fsai_chol_kernel");
+    afn_status cs = fsai_chol_batch(r0, nr, MT, rp, Sg, gval, info, st);
+    if (cs != AFN_OK) { dfree(Sg, st); return cs; }
   }
   dfree(Sg, st);
   return AFN_OK;
@@ -645,7 +687,8 @@ __global__ void fill_cols_kernel(const int64_t* __restrict__ rp, const int32_t* 
 __global__ void rank_cols_kernel(const int64_t* __restrict__ trp, const int32_t* __restrict__ trow_tmp,
                                  int64_t N, const int64_t* __restrict__ rp,
                                  const int32_t* __restrict__ col, const double* __restrict__ val,
-                                 int32_t* __restrict__ tcol, double* __restrict__ tval) {
+                                 int32_t* __restrict__ tcol, double* __restrict__ tval,
+                                 int64_t* __restrict__ tmap) {
   const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (c >= N) return;
@@ -661,11 +704,46 @@ __global__ void rank_cols_kernel(const int64_t* __restrict__ trp, const int32_t*
       if (col[mid] < c) lo = mid + 1; else hi = mid;
     }
     tcol[b + rank] = r;
-    tval[b + rank] = val[lo];
+    if (tval) tval[b + rank] = val[lo];
+    if (tmap) tmap[b + rank] = lo;
   }
 }
 
 }  // namespace
+
+template <int MT>
+afn_status launch_chol(int64_t r0, int64_t nrows, const int64_t* rp, double* Sg, double* gval, int* info,
+                       cudaStream_t st) {
+  constexpr int WP = MT * 16;
+  // widest row of the batch (rows grow to w and stay there)
+  int64_t h2[2];
+  const int64_t last = r0 + nrows - 1;
+  AFN_CUDA(cudaMemcpyAsync(h2, rp + last, sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaStreamSynchronize(st));
+  const int wmax = std::max(1, std::min(WP, (int)(h2[1] - h2[0])));
+  const size_t per = sizeof(double) * ((size_t)wmax * (wmax + 1) / 2 + wmax);
+  const int CW = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(220 * 1024) / per));
+  const size_t bytes = per * CW;
+  auto kern = fsai_chol_kernel<MT>;
+  AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  kern<<<(unsigned)((nrows + CW - 1) / CW), CW * 32, bytes, st>>>(r0, nrows, wmax, rp, Sg, gval, info);
+  AFN_LAUNCH_CHECK("fsai_chol_kernel");
+  return AFN_OK;
+}
+
+afn_status fsai_chol_batch(int64_t r0, int64_t nrows, int MT, const int64_t* rp, double* Sg,
+                           double* gval, int* info, cudaStream_t st) {
+  switch (MT) {
+    case 1: return launch_chol<1>(r0, nrows, rp, Sg, gval, info, st);
+    case 2: return launch_chol<2>(r0, nrows, rp, Sg, gval, info, st);
+    case 3: return launch_chol<3>(r0, nrows, rp, Sg, gval, info, st);
+    case 4: return launch_chol<4>(r0, nrows, rp, Sg, gval, info, st);
+    case 5: return launch_chol<5>(r0, nrows, rp, Sg, gval, info, st);
+    case 6: return launch_chol<6>(r0, nrows, rp, Sg, gval, info, st);
+    case 7: return launch_chol<7>(r0, nrows, rp, Sg, gval, info, st);
+    default: return launch_chol<8>(r0, nrows, rp, Sg, gval, info, st);
+  }
+}
 
 afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
                     int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* d_info,
@@ -686,7 +764,7 @@ afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, con
   const double cl = AFN_LOG2E / (l * l);
   const int MT = (w + 15) / 16;
   // variant: 0 = split (default), 1 = single kernel, 2 = warp-specialised
-  static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : 0;
+  static const int variant = getenv("AFN_FSAI_VARIANT") ? std::max(0, atoi(getenv("AFN_FSAI_VARIANT"))) : 0;
   if (variant == 2) {
     switch (MT) {
       case 1: return launch_fsai_ws<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
@@ -726,8 +804,22 @@ afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, con
   }
 }
 
+__global__ void gather_map_kernel(const double* __restrict__ v, const int64_t* __restrict__ map,
+                                  int64_t nnz, double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < nnz) out[e] = v[map[e]];
+}
+
+afn_status gather_map(const double* v, const int64_t* map, int64_t nnz, double* out, cudaStream_t st) {
+  if (nnz <= 0) return AFN_OK;
+  gather_map_kernel<<<(unsigned)((nnz + 255) / 256), 256, 0, st>>>(v, map, nnz, out);
+  AFN_LAUNCH_CHECK("gather_map_kernel");
+  return AFN_OK;
+}
+
 afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* val, int64_t N,
-                         int64_t nnz, int64_t* trp, int32_t* tcol, double* tval, cudaStream_t st) {
+                         int64_t nnz, int64_t* trp, int32_t* tcol, double* tval, cudaStream_t st,
+                         int64_t* tmap) {
   if (N <= 0) return AFN_OK;
   int* cnt = nullptr;
   int32_t* tmp = nullptr;
@@ -743,7 +835,7 @@ afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* va
   AFN_LAUNCH_CHECK("scan_kernel");
   fill_cols_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(rp, col, N, trp, cur, tmp);
   AFN_LAUNCH_CHECK("fill_cols_kernel");
-  rank_cols_kernel<<<(unsigned)((N + 7) / 8), 256, 0, st>>>(trp, tmp, N, rp, col, val, tcol, tval);
+  rank_cols_kernel<<<(unsigned)((N + 7) / 8), 256, 0, st>>>(trp, tmp, N, rp, col, val, tcol, tval, tmap);
   AFN_LAUNCH_CHECK("rank_cols_kernel");
   dfree(tmp, st);
   dfree(cnt, st);
