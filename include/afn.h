@@ -166,6 +166,15 @@ enum { AFN_OUT_PERM = 0, AFN_OUT_FILL = 1, AFN_OUT_L = 2, AFN_OUT_ROWPTR = 3,
        AFN_OUT_COL = 4, AFN_OUT_GVAL = 5, AFN_OUT_W = 6 };
 afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes);
 
+/* Copy selected ROWS of a dense internal array to HOST memory (sampled parity
+ * checks at sizes where the whole array does not fit the host, e.g. W at
+ * n = 2^20, k = 8000 is 66.6 GB).  what: AFN_OUT_W (row t = non-landmark
+ * position t, 0 <= t < n-k, k doubles each) or AFN_OUT_L (row t of L, k
+ * doubles each).  rows: nrows host int64; host receives nrows*k doubles;
+ * bytes must equal 8*nrows*k.  Out-of-range rows -> AFN_ERR_ARG.  [sync] */
+afn_status afn_copy_out_rows(afn_handle h, int32_t what, const int64_t* rows /*host*/,
+                             int64_t nrows, void* host, size_t bytes);
+
 void afn_destroy(afn_handle h);
 
 /* ------------------------------------------------------------------------ */

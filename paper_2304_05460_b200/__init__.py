@@ -84,6 +84,7 @@ _sig = {
                                  C.c_int32, C.POINTER(Info), C.POINTER(Report), _P]),
     "afn_get_info": (C.c_int, [_P, C.POINTER(Info)]),
     "afn_copy_out": (C.c_int, [_P, C.c_int32, _P, C.c_size_t]),
+    "afn_copy_out_rows": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, C.c_size_t]),
     "afn_destroy": (None, [_P]),
     "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_probe_dmma": (C.c_int, [C.c_int64, _D, _P]),
@@ -289,6 +290,17 @@ class Handle:
         arr = np.empty(shp, dtype=dt)
         _check(_lib.afn_copy_out(self._h, int(what), arr.ctypes.data_as(C.c_void_p), arr.nbytes),
                "afn_copy_out")
+        return arr
+
+    def copy_out_rows(self, what, rows):
+        """Rows of W (non-landmark positions) or L as a (len(rows), k) host array."""
+        import numpy as np
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        k = self.info()["k"]
+        arr = np.empty((len(rows), k))
+        _check(_lib.afn_copy_out_rows(self._h, int(what), rows.ctypes.data_as(C.c_void_p),
+                                      len(rows), arr.ctypes.data_as(C.c_void_p), arr.nbytes),
+               "afn_copy_out_rows")
         return arr
 
 

@@ -872,6 +872,26 @@ afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes) {
   return AFN_OK;
 }
 
+afn_status afn_copy_out_rows(afn_handle h, int32_t what, const int64_t* rows, int64_t nrows,
+                             void* host, size_t bytes) {
+  REQ(h && host && (rows || nrows == 0) && nrows >= 0, "null argument");
+  const double* src = nullptr;
+  int64_t R = 0;
+  if (what == AFN_OUT_W) src = h->W, R = h->N2;
+  else if (what == AFN_OUT_L) src = h->L, R = h->k;
+  else REQ(false, "copy_out_rows: selector %d unsupported (W or L only)", what);
+  const size_t rowb = sizeof(double) * (size_t)h->k;
+  REQ(bytes == rowb * (size_t)nrows, "copy_out_rows: bytes=%zu, need %zu", bytes,
+      rowb * (size_t)nrows);
+  for (int64_t t = 0; t < nrows; ++t)
+    REQ(rows[t] >= 0 && rows[t] < R, "copy_out_rows: row %lld out of range [0, %lld)",
+        (long long)rows[t], (long long)R);
+  for (int64_t t = 0; t < nrows; ++t)
+    AFN_CUDA(cudaMemcpy(static_cast<char*>(host) + rowb * t, src + (size_t)rows[t] * h->k, rowb,
+                        cudaMemcpyDeviceToHost));
+  return AFN_OK;
+}
+
 void afn_destroy(afn_handle h) { handle_free(h); }
 
 afn_status afn_probe_dmma(int64_t iters, double* tflops, void* stream) {

@@ -136,18 +136,19 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
   const int64_t rows_per_cta = (int64_t)KMV_NT * rows_per_thread(d);
   p.row_tiles = (nrows + rows_per_cta - 1) / rows_per_cta;
   const int64_t slots = (int64_t)num_sms * 2;  // 2 CTAs/SM (launch bounds)
-  // enough CTAs for >= 4 waves, chunk >= 256 columns, minimal wave quantisation
+  // Choose the column-chunk count minimising (waves x columns per CTA): whole
+  // waves of `slots` CTAs (a partial last wave idles SMs), chunks >= 64
+  // columns, plus a small per-chunk cost for the partial sums and the reduce.
   int64_t best_chunks = 1;
   double best_cost = 1e300;
-  const int64_t cmax = std::max<int64_t>(1, (n + 255) / 256);
-  const int64_t cmin = std::min<int64_t>(cmax, std::max<int64_t>(1, (4 * slots + p.row_tiles - 1) / p.row_tiles));
-  for (int64_t ch = cmin; ch <= std::min(cmax, cmin + 64); ++ch) {
+  const int64_t cmax = std::max<int64_t>(1, std::min<int64_t>((n + 63) / 64, 4096));
+  for (int64_t ch = 1; ch <= cmax; ++ch) {
     const int64_t cc = (n + ch - 1) / ch;
     const int64_t nch = (n + cc - 1) / cc;
+    if (nch != ch) continue;
     const int64_t ctas = p.row_tiles * nch;
     const int64_t waves = (ctas + slots - 1) / slots;
-    // cost ~ waves * work per CTA (columns), plus a small per-chunk reduce cost
-    const double cost = (double)waves * (double)cc + 0.02 * (double)nch * (double)rows_per_cta;
+    const double cost = (double)waves * (double)cc + 0.002 * (double)nch * (double)rows_per_cta;
     if (cost < best_cost) { best_cost = cost; best_chunks = nch; }
   }
   p.chunk_cols = (n + best_chunks - 1) / best_chunks;

@@ -1,0 +1,137 @@
+"""GPU parity at BASELINE.json's full sizes C3 (n = 2^17), C4 (n = 2^18, d = 8)
+and C5 (n = 2^20), where the oracle cannot run the whole solve (one oracle
+matvec at C5 is 1.1e12 kernel evaluations).  Parity is therefore checked by
+component:
+
+  * Alg. 1 (k-hat, r, branch) and ALL k FPS landmarks + fill trace: bit-exact
+    against the oracle run in full;
+  * permutation: landmarks first, then the rest ascending (R14);
+  * kNN pattern rows, W = (L^{-1} K12)^T rows and FSAI rows on a sample of
+    non-landmark positions (always including the first and the last rows),
+    with the oracle's own L, landmarks and pattern;
+  * kernel matvec on sampled rows (<= 1e-12 relative);
+  * PCG: converged with the GPU's true relative residual <= tol, the GPU
+    matvec that computes it being checked on sampled rows of the solution.
+
+The C5 case needs ~70 GB of device memory (W is 66.6 GB) and a few minutes of
+oracle time; it is marked slow as well as gpu."""
+import math
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import oracle as O
+from synth import CONFIGS, gen_problem
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2304_05460_b200 as afn  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def sample_rows(N, count, seed):
+    rng = np.random.default_rng(seed)
+    s = set(rng.choice(N, min(N, count), replace=False).tolist())
+    s.update({0, min(1, N - 1), N - 1, N // 2})
+    return np.array(sorted(s), dtype=np.int64)
+
+
+CASES = [pytest.param("C3", 1.0, id="C3-l1"),
+         pytest.param("C4", 1.0, id="C4-l1"),
+         pytest.param("C4", 3.0, id="C4-l3"),
+         pytest.param("C5", 1.0, id="C5-l1", marks=pytest.mark.slow)]
+
+
+@pytest.mark.parametrize("name,l", CASES)
+def test_full_size_component_parity(name, l):
+    cfg = CONFIGS[name]
+    X, b = gen_problem(cfg)
+    n = cfg.n
+    Xd, bd = T(X), T(b)
+    h = afn.afn_build(Xd, afn.make_params(l, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True))
+    inf = h.info()
+
+    # ---- Alg. 1: bit-exact decisions
+    ro = O.alg1(X, l)
+    if min(ro["err_margin"], ro["ev_margin"]) >= 1e-9:
+        assert (inf["khat"], inf["r"], bool(inf["refined"])) == (ro["khat"], ro["r"], ro["refined"])
+    k = min(cfg.k_cap, max(1, ro["khat"]), n)
+    assert inf["k"] == k
+
+    # ---- FPS, all k landmarks and the fill trace: bit-exact
+    idx, fill = O.fps(X, k, 0)
+    perm = h.copy_out(afn.OUT_PERM)
+    assert np.array_equal(perm[:k], idx)
+    assert np.array_equal(h.copy_out(afn.OUT_FILL), fill)
+    rest = perm[k:]
+    mask = np.ones(n, bool)
+    mask[idx] = False
+    perm_o = np.concatenate([idx, np.nonzero(mask)[0]])
+    assert np.array_equal(rest, perm_o[k:])  # ascending original ids (R14)
+
+    # ---- oracle factors on its own landmarks
+    Xp = X[perm_o]
+    X1, X2 = Xp[:k], Xp[k:]
+    N2 = n - k
+    L = np.linalg.cholesky(O.kernel_block(X1, X1, l) + cfg.mu * np.eye(k))
+    lrows = sample_rows(k, 24, 5)
+    Lg = h.copy_out_rows(afn.OUT_L, lrows)
+    assert np.abs(Lg - L[lrows]).max() <= 1e-12 * np.abs(L).max()
+
+    def V_cols(J):  # V = L^{-1} K12 on the columns J
+        return sla.solve_triangular(L, O.kernel_block(X1, X2[J], l), lower=True)
+
+    rows = sample_rows(N2, 40, 7)
+    Wg = h.copy_out_rows(afn.OUT_W, rows)
+    Vo = V_cols(rows)
+    assert np.abs(Wg - Vo.T).max() <= 1e-11 * max(1.0, np.abs(Vo).max())
+
+    # ---- kNN rows: bit-exact; FSAI rows: 1e-10 per row
+    rp = h.copy_out(afn.OUT_ROWPTR)
+    col = h.copy_out(afn.OUT_COL)
+    gv = h.copy_out(afn.OUT_GVAL)
+    worst = 0.0
+    for i in rows:
+        J = O.knn_row(X2, int(i), cfg.w)
+        a, e = rp[i], rp[i + 1]
+        assert np.array_equal(col[a:e].astype(np.int64), J), f"pattern row {i}"
+        VJ = V_cols(J)
+        SJ = O.kernel_block(X2[J], X2[J], l) + cfg.mu * np.eye(len(J)) - VJ.T @ VJ
+        go = O.fsai_rows(lambda _J: SJ, np.array([0, len(J)]), J)
+        worst = max(worst, rel(gv[a:e], go))
+    assert worst <= 1e-10, worst
+
+    # ---- kernel matvec on sampled rows, original order
+    v = np.random.default_rng(3).standard_normal(n)
+    y = afn.kernel_matvec(Xd, l, cfg.mu, T(v)).cpu().numpy()
+    mrows = sample_rows(n, 64, 9)
+    assert rel(y[mrows], O.kmv_rows(X, l, cfg.mu, v, mrows)) <= 1e-12
+
+    # ---- PCG
+    a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit)
+    assert rep["converged"] and not rep["breakdown"]
+    assert rep["relres_true"] <= cfg.tol
+    an = a.cpu().numpy()
+    ya = afn.kernel_matvec(Xd, l, cfg.mu, a).cpu().numpy()
+    assert rel(ya[mrows], O.kmv_rows(X, l, cfg.mu, an, mrows)) <= 1e-12
+    res = b - ya
+    assert math.isclose(np.linalg.norm(res) / np.linalg.norm(b), rep["relres_true"],
+                        rel_tol=1e-6, abs_tol=1e-12)
+    print(f"{name} l={l}: k={k} khat={inf['khat']} iters={rep['iterations']} "
+          f"relres_true={rep['relres_true']:.3e} setup_ms={inf['ms_total']:.1f} "
+          f"solve_ms={rep['solve_ms']:.1f}")
+    h.close()
