@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define AFN_ABI_VERSION 1
+#define AFN_ABI_VERSION 2
 
 typedef enum {
   AFN_OK = 0,
@@ -45,11 +45,14 @@ typedef enum {
   AFN_ERR_NOMEM = 3,      /* device allocation failed                          */
   AFN_ERR_NOT_SPD = 4,    /* Cholesky breakdown of K11+mu I or an FSAI block  */
   AFN_ERR_BREAKDOWN = 5,  /* PCG breakdown (p.q <= 0 or non-finite)            */
+  AFN_ERR_NCCL = 6,       /* NCCL unavailable or a collective failed           */
   AFN_ERR_STATE = 7       /* handle used in a state that does not allow it     */
 } afn_status;
 
 /* Opaque built preconditioner (immutable after afn_build). */
 typedef struct afn_handle_s* afn_handle;
+/* Opaque communicator of the row-sharded multi-GPU path (afn_comm_*). */
+typedef struct afn_comm_s* afn_comm;
 
 /* Build parameters.  Cite: l, mu; k_cap "limit ... such as 2000"
  * (P:L209-210); w "the w-1 nearest neighbors" (w counts the
@@ -74,6 +77,8 @@ typedef struct {
   double scale;                 /* Alg.1 coordinate scale (m/n)^(1/d)              */
   double ms_alg1, ms_fps, ms_chol, ms_trsm, ms_knn, ms_fsai, ms_total; /* phase times */
   double ms_fsai_rows;          /* the FSAI row kernel alone (inside ms_fsai)      */
+  int32_t nranks, rank;         /* communicator size, this (first local) rank      */
+  int64_t row_a0, row_na, row_b0, row_nb; /* rows of the permuted order it owns   */
 } afn_info;
 
 /* PCG report (host struct).  history: optional host array of >= maxit+1
@@ -88,6 +93,7 @@ typedef struct {
   double solve_ms;      /* device time of the solve loop (CUDA events)         */
   double matvec_ms;     /* device time of the loop's kernel matvecs            */
   double apply_ms;      /* device time of the loop's AFN applications          */
+  double comm_ms;       /* device time of the loop's exchanges (multi-rank)    */
   double* history;      /* [host, optional] len maxit+1                        */
 } afn_solve_report;
 
@@ -175,7 +181,48 @@ afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes);
 afn_status afn_copy_out_rows(afn_handle h, int32_t what, const int64_t* rows /*host*/,
                              int64_t nrows, void* host, size_t bytes);
 
+/* Same as afn_copy_out for local rank `local_rank` of a multi-rank handle
+ * (emulated communicators drive several ranks in one process).  W holds only
+ * the rank's own non-landmark rows (row_nb x k) when nranks > 1. */
+afn_status afn_copy_out_local(afn_handle h, int32_t local_rank, int32_t what, void* host, size_t bytes);
+
 void afn_destroy(afn_handle h);
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU: one process per GPU, rows sharded, points replicated            */
+/* (BASELINE north star (3)).  Rank s owns the rows          */
+/*   [a0, a0+na) = [k s/R, k (s+1)/R)  of the landmark block and             */
+/*   [b0, b0+nb) = [k + N2 s/R, k + N2 (s+1)/R)  of the rest (N2 = n-k)      */
+/* of the permuted order (afn_shard_rows).  Alg. 1, FPS, K11 + mu I and its  */
+/* Cholesky factor are computed redundantly on every rank (identical,        */
+/* deterministic); W rows, kNN rows, FSAI rows, kernel-matvec rows and the   */
+/* vector updates are sharded; the exchanges are all-gathers (NCCL broadcasts */
+/* of each owner's rows): W, pattern and G rows once after the build, and    */
+/* per PCG iteration the CG vector p, the apply's u and G u, the k-vector    */
+/* partials of W^T s2 and the dot-product partials, all summed in rank order  */
+/* (deterministic, identical on every rank).                                 */
+#define AFN_COMM_ID_BYTES 128
+/* NCCL unique id (rank 0 creates it and broadcasts the 128 bytes, e.g. with */
+/* torch.distributed).  nccl_path: libnccl.so.2 to dlopen, NULL = default.  */
+afn_status afn_comm_unique_id(void* id /*host, 128 B*/, const char* nccl_path);
+/* Join a communicator of nranks processes, one GPU each (the current        */
+/* device).  Collective over the nranks processes.  nranks = 1 needs no NCCL. */
+afn_status afn_comm_init(const void* id /*host*/, int32_t nranks, int32_t rank,
+                         const char* nccl_path, afn_comm* out /*host*/);
+/* Test communicator: nranks logical ranks driven by this one process on the */
+/* current device, each with its own buffers; the exchanges are device      */
+/* copies between them.  Results match a real nranks-GPU run bit for bit.   */
+afn_status afn_comm_init_emulated(int32_t nranks, afn_comm* out /*host*/);
+void afn_comm_destroy(afn_comm c);
+/* rows[4] = {a0, na, b0, nb} owned by `rank` (host arithmetic only). */
+afn_status afn_shard_rows(int64_t n, int64_t k, int32_t nranks, int32_t rank, int64_t* rows /*host*/);
+/* afn_build over a communicator (comm = NULL: single GPU, same as afn_build).*/
+/* Every process passes the same X and params.  The handle keeps the comm   */
+/* pointer (destroy the handle first).  afn_apply / afn_pcg_solve on such a   */
+/* handle are collective: r / b are the full vectors (replicated), z / a     */
+/* receive the full result on every process.  [sync]                        */
+afn_status afn_build_dist(afn_comm comm, const double* X, int64_t n, int32_t d,
+                          const afn_params* params /*host*/, void* stream, afn_handle* out /*host*/);
 
 /* ------------------------------------------------------------------------ */
 /* Measurement helpers (bench.py): FP64 FMA peak probe.  Runs `iters` DFMA   */

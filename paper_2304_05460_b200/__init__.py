@@ -25,7 +25,8 @@ _lib = C.CDLL(LIB_PATH)
 
 AFN_OK = 0
 STATUS = {0: "AFN_OK", 1: "AFN_ERR_ARG", 2: "AFN_ERR_CUDA", 3: "AFN_ERR_NOMEM",
-          4: "AFN_ERR_NOT_SPD", 5: "AFN_ERR_BREAKDOWN", 7: "AFN_ERR_STATE"}
+          4: "AFN_ERR_NOT_SPD", 5: "AFN_ERR_BREAKDOWN", 6: "AFN_ERR_NCCL", 7: "AFN_ERR_STATE"}
+COMM_ID_BYTES = 128
 OUT_PERM, OUT_FILL, OUT_L, OUT_ROWPTR, OUT_COL, OUT_GVAL, OUT_W = range(7)
 
 
@@ -47,7 +48,9 @@ class Info(C.Structure):
                 ("d", C.c_int32), ("r", C.c_int32), ("m", C.c_int32), ("refined", C.c_int32),
                 ("scale", C.c_double), ("ms_alg1", C.c_double), ("ms_fps", C.c_double),
                 ("ms_chol", C.c_double), ("ms_trsm", C.c_double), ("ms_knn", C.c_double),
-                ("ms_fsai", C.c_double), ("ms_total", C.c_double), ("ms_fsai_rows", C.c_double)]
+                ("ms_fsai", C.c_double), ("ms_total", C.c_double), ("ms_fsai_rows", C.c_double),
+                ("nranks", C.c_int32), ("rank", C.c_int32), ("row_a0", C.c_int64),
+                ("row_na", C.c_int64), ("row_b0", C.c_int64), ("row_nb", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -57,13 +60,13 @@ class Report(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("breakdown", C.c_int32),
                 ("applies", C.c_int32), ("relres", C.c_double), ("relres_true", C.c_double),
                 ("solve_ms", C.c_double), ("matvec_ms", C.c_double), ("apply_ms", C.c_double),
-                ("history", C.POINTER(C.c_double))]
+                ("comm_ms", C.c_double), ("history", C.POINTER(C.c_double))]
 
     def as_dict(self):
         return dict(iterations=self.iterations, converged=bool(self.converged),
                     breakdown=bool(self.breakdown), applies=self.applies, relres=self.relres,
                     relres_true=self.relres_true, solve_ms=self.solve_ms,
-                    matvec_ms=self.matvec_ms, apply_ms=self.apply_ms)
+                    matvec_ms=self.matvec_ms, apply_ms=self.apply_ms, comm_ms=self.comm_ms)
 
 
 _P = C.c_void_p
@@ -85,6 +88,13 @@ _sig = {
     "afn_get_info": (C.c_int, [_P, C.POINTER(Info)]),
     "afn_copy_out": (C.c_int, [_P, C.c_int32, _P, C.c_size_t]),
     "afn_copy_out_rows": (C.c_int, [_P, C.c_int32, _P, C.c_int64, _P, C.c_size_t]),
+    "afn_copy_out_local": (C.c_int, [_P, C.c_int32, C.c_int32, _P, C.c_size_t]),
+    "afn_comm_unique_id": (C.c_int, [_P, C.c_char_p]),
+    "afn_comm_init": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_char_p, C.POINTER(_P)]),
+    "afn_comm_init_emulated": (C.c_int, [C.c_int32, C.POINTER(_P)]),
+    "afn_comm_destroy": (None, [_P]),
+    "afn_shard_rows": (C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64)]),
+    "afn_build_dist": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(Params), _P, C.POINTER(_P)]),
     "afn_destroy": (None, [_P]),
     "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_probe_dmma": (C.c_int, [C.c_int64, _D, _P]),
@@ -223,16 +233,99 @@ def make_params(l, mu, k_cap, w, k_adaptive=False, m=0, k_threshold=2000, fps_se
                   int(k_threshold), int(fps_seed), int(rng_seed))
 
 
-class Handle:
-    """A built AFN preconditioner (include/afn.h afn_handle)."""
+def nccl_library_path():
+    """libnccl.so.2 of the nvidia-nccl wheel (the copy PyTorch loads), or None."""
+    try:
+        import nvidia.nccl
+        for base in nvidia.nccl.__path__:
+            p = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except ImportError:
+        pass
+    return None
 
-    def __init__(self, X, params: Params, stream=None):
+
+def shard_rows(n, k, nranks, rank):
+    """Rows (a0, na, b0, nb) of the permuted order owned by `rank` (include/afn.h)."""
+    out = (C.c_int64 * 4)()
+    _check(_lib.afn_shard_rows(int(n), int(k), int(nranks), int(rank), out), "afn_shard_rows")
+    return tuple(out)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    path = nccl_library_path()
+    _check(_lib.afn_comm_unique_id(buf, path.encode() if path else None), "afn_comm_unique_id")
+    return buf.raw
+
+
+def bootstrap_unique_id(dist=None) -> bytes:
+    """Rank 0's NCCL unique id, broadcast over an initialised torch.distributed group."""
+    if dist is None:
+        import torch.distributed as dist
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+class Comm:
+    """Communicator of the row-sharded path (include/afn.h afn_comm)."""
+
+    def __init__(self, ptr, nranks, rank, nlocal):
+        self._c = ptr
+        self.nranks, self.rank, self.nlocal = nranks, rank, nlocal
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, nranks: int, rank: int):
+        """One process per GPU; every rank passes rank 0's nccl_unique_id()."""
+        c = C.c_void_p()
+        path = nccl_library_path()
+        _check(_lib.afn_comm_init(C.c_char_p(unique_id), int(nranks), int(rank),
+                                  path.encode() if path else None, C.byref(c)), "afn_comm_init")
+        return cls(c, nranks, rank, 1)
+
+    @classmethod
+    def from_process_group(cls, dist=None):
+        """Bootstrap from an initialised torch.distributed group (rank 0's id is broadcast)."""
+        if dist is None:
+            import torch.distributed as dist
+        uid = bootstrap_unique_id(dist)
+        return cls.nccl(uid, dist.get_world_size(), dist.get_rank())
+
+    @classmethod
+    def emulated(cls, nranks: int):
+        """nranks logical ranks driven by this process on the current device (tests)."""
+        c = C.c_void_p()
+        _check(_lib.afn_comm_init_emulated(int(nranks), C.byref(c)), "afn_comm_init_emulated")
+        return cls(c, nranks, 0, nranks)
+
+    def close(self):
+        if getattr(self, "_c", None) is not None and self._c.value:
+            _lib.afn_comm_destroy(self._c)
+            self._c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Handle:
+    """A built AFN preconditioner (include/afn.h afn_handle); `comm` shards it."""
+
+    def __init__(self, X, params: Params, stream=None, comm: Comm = None):
         torch = _torch()
         self.n, self.d = X.shape
         self.device = X.device
+        self.comm = comm  # keeps the communicator alive while the handle is
         h = C.c_void_p()
-        _check(_lib.afn_build(_dev(X, "X", torch.float64), self.n, self.d, C.byref(params),
-                              _stream(stream), C.byref(h)), "afn_build")
+        _check(_lib.afn_build_dist(comm._c if comm is not None else None,
+                                   _dev(X, "X", torch.float64), self.n, self.d, C.byref(params),
+                                   _stream(stream), C.byref(h)), "afn_build_dist")
         self._h = h
         self.params = params
 
@@ -278,18 +371,22 @@ class Handle:
             out["history"] = hist[: rep.iterations + 1].copy()
         return a, out
 
-    def copy_out(self, what):
+    def copy_out(self, what, local_rank=0):
         import numpy as np
         inf = self.info()
         n, k, nnz = inf["n"], inf["k"], inf["nnz"]
+        nw = n - k
+        if inf["nranks"] > 1:
+            nw = shard_rows(n, k, inf["nranks"], inf["rank"] + local_rank)[3]
         shapes = {OUT_PERM: (np.int64, (n,)), OUT_FILL: (np.float64, (k,)),
                   OUT_L: (np.float64, (k, k)), OUT_ROWPTR: (np.int64, (n - k + 1,)),
                   OUT_COL: (np.int32, (nnz,)), OUT_GVAL: (np.float64, (nnz,)),
-                  OUT_W: (np.float64, (n - k, k))}
+                  OUT_W: (np.float64, (nw, k))}
         dt, shp = shapes[what]
         arr = np.empty(shp, dtype=dt)
-        _check(_lib.afn_copy_out(self._h, int(what), arr.ctypes.data_as(C.c_void_p), arr.nbytes),
-               "afn_copy_out")
+        _check(_lib.afn_copy_out_local(self._h, int(local_rank), int(what),
+                                       arr.ctypes.data_as(C.c_void_p), arr.nbytes),
+               "afn_copy_out_local")
         return arr
 
     def copy_out_rows(self, what, rows):
@@ -304,8 +401,8 @@ class Handle:
         return arr
 
 
-def afn_build(X, params: Params, stream=None) -> Handle:
-    return Handle(X, params, stream)
+def afn_build(X, params: Params, stream=None, comm: Comm = None) -> Handle:
+    return Handle(X, params, stream, comm)
 
 
 def afn_solve_host(X, b, params: Params, tol=1e-4, maxit=500, stream=None):

@@ -24,6 +24,22 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xcompiler", "-Wall", "-diag-suppress", "177"]
 
 
+def _nccl_include():
+    """nccl.h (types only: libnccl.so.2 is dlopen'ed at run time, comm.cu)."""
+    try:
+        import nvidia.nccl
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    for inc in ("/usr/include", "/usr/local/cuda/include"):
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel or system NCCL)")
+
+
 def sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
@@ -43,7 +59,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
 
     def compile_one(src):
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, "-I", _nccl_include(), *extra, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -57,7 +73,7 @@ def build(verbose: bool = False, force: bool = False, ptxas_v: bool = False) -> 
                 print(f"== {os.path.basename(obj)}\n{err}", file=sys.stderr)
     objs = [o for o, _ in results]
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

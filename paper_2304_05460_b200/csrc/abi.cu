@@ -222,6 +222,49 @@ __global__ void perm_kernel(const unsigned char* __restrict__ flag, const int64_
 using namespace afn;
 
 // ---------------------------------------------------------------------------
+// The built handle.  One RankSt per logical rank this process drives (one on
+// a single GPU or with NCCL; R with an emulated communicator).  Replicated
+// pieces (permuted points, L, L^{-T}, the pattern, G, G^T) are held by every
+// rank; W holds the rank's own non-landmark rows; the PCG vectors are full
+// length with only the rank's own rows (RankSt::own) computed locally.
+struct RankSt {
+  int rank = 0;
+  Seg2 own{};
+  int64_t lo = 0, hi = 0;  // own non-landmark rows, numbered 0..N2
+  int64_t* perm = nullptr;
+  double* fill = nullptr;
+  double* Xp = nullptr;     // permuted points n x d
+  double* Xs = nullptr;     // prescaled permuted points (kmv)
+  double* L = nullptr;      // k x k lower (row-major)
+  double* LinvT = nullptr;  // k x k, L^{-T}
+  double* W = nullptr;      // own rows (hi - lo) x k of W = K21 L^{-T}
+  int64_t* rp = nullptr;
+  int32_t* col = nullptr;
+  double* gval = nullptr;
+  int64_t* trp = nullptr;
+  int32_t* tcol = nullptr;
+  double* tval = nullptr;
+  int* derr = nullptr;
+  int* dinfo = nullptr;
+  // workspaces
+  KmvPlan plan{};
+  double* kmv_part = nullptr;
+  double* gws = nullptr;    // gemv_t partials
+  double* tvec = nullptr;   // k
+  double* vvec = nullptr;   // k
+  double* kpart = nullptr;  // R x k partials of W^T s2
+  double* uvec = nullptr;   // N2
+  double* yvec = nullptr;   // N2
+  double* rbuf = nullptr;   // n (public apply)
+  double* zbuf = nullptr;   // n
+  double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;  // n
+  double* sc = nullptr;      // SC_N combined scalars
+  double* scpart = nullptr;  // R x SC_N per-rank partials
+  double* dws = nullptr;
+  unsigned* dcnt = nullptr;
+  std::vector<void*> allocs;
+};
+
 struct afn_handle_s {
   int device = 0;
   int64_t n = 0, k = 0, N2 = 0, nnz = 0;
@@ -229,41 +272,9 @@ struct afn_handle_s {
   double l = 0, mu = 0;
   afn_params params{};
   Alg1Result a1{};
-  // device arrays
-  int64_t* perm = nullptr;
-  double* fill = nullptr;
-  double* Xp = nullptr;     // permuted points n x d
-  double* Xs = nullptr;     // prescaled permuted points (kmv)
-  double* L = nullptr;      // k x k lower (row-major)
-  double* LinvT = nullptr;  // k x k, L^{-T}
-  double* W = nullptr;      // N2 x k
-  int64_t* rp = nullptr;
-  int32_t* col = nullptr;
-  double* gval = nullptr;
-  int64_t* trp = nullptr;
-  int32_t* tcol = nullptr;
-  double* tval = nullptr;
-  // workspaces
-  KmvPlan plan{};
-  double* kmv_part = nullptr;
-  double* gws = nullptr;  // gemv_t partials
-  double* tvec = nullptr;  // k
-  double* vvec = nullptr;  // k
-  double* uvec = nullptr;  // N2
-  double* yvec = nullptr;  // N2
-  double* rbuf = nullptr;  // n (public apply)
-  double* zbuf = nullptr;  // n
-  // pcg
-  double* x = nullptr;
-  double* r = nullptr;
-  double* z = nullptr;
-  double* p = nullptr;
-  double* q = nullptr;
-  double* sc = nullptr;
-  double* dws = nullptr;
-  unsigned* dcnt = nullptr;
-  double* h_sc = nullptr;  // pinned host mirror of sc (per host thread, not owned)
-  std::vector<void*> allocs;
+  const Comm* comm = nullptr;  // not owned; null = single GPU
+  int R = 1;
+  std::vector<RankSt> rk;
   double ms[8] = {0};
 };
 
@@ -281,10 +292,24 @@ double* pinned_scalars() {
   return buf;
 }
 
-afn_status halloc(afn_handle h, void** p, size_t bytes, cudaStream_t st) {
-  afn_status s = dalloc(p, bytes, st);
-  if (s == AFN_OK) h->allocs.push_back(*p);
-  return s;
+template <class T>
+afn_status ralloc(RankSt& s, T** p, size_t count, cudaStream_t st) {
+  void* v = nullptr;
+  afn_status e = dalloc(&v, sizeof(T) * (count > 0 ? count : 1), st);
+  if (e == AFN_OK) {
+    s.allocs.push_back(v);
+    *p = static_cast<T*>(v);
+  }
+  return e;
+}
+
+void rfree(RankSt& s, void* p, cudaStream_t st) {
+  for (auto it = s.allocs.begin(); it != s.allocs.end(); ++it)
+    if (*it == p) {
+      s.allocs.erase(it);
+      break;
+    }
+  dfree(p, st);
 }
 
 void handle_free(afn_handle h) {
@@ -296,10 +321,65 @@ void handle_free(afn_handle h) {
   // return the blocks to the stream-ordered pool (cudaFree would unmap them and
   // force the next build to map fresh pages); the legacy stream orders the
   // frees after all prior work on the device's blocking streams
-  for (void* p : h->allocs) cudaFreeAsync(p, 0);
+  for (auto& s : h->rk)
+    for (void* p : s.allocs) cudaFreeAsync(p, 0);
   cudaStreamSynchronize(0);
   cudaSetDevice(cur);
   delete h;
+}
+
+// closed-form kNN row pointer (knn.cu): sum_{t<i} min(w, t+1)
+int64_t rowptr_at(int64_t i, int w) {
+  const int64_t wl = w;
+  return (i < wl) ? i * (i + 1) / 2 : wl * (wl + 1) / 2 + (i - wl) * wl;
+}
+
+// ---- exchanges (all-gather of each rank's owned byte ranges) -------------
+template <class F, class G>
+afn_status exchange(afn_handle h, F buf_of, G ranges_of, cudaStream_t st) {
+  if (h->R <= 1) return AFN_OK;
+  std::vector<char*> bufs;
+  for (auto& s : h->rk) bufs.push_back(reinterpret_cast<char*>(buf_of(s)));
+  std::vector<RankRanges> owned(h->R);
+  for (int s = 0; s < h->R; ++s) owned[s] = ranges_of(s);
+  return comm_allgatherv(h->comm, bufs.data(), owned, st);
+}
+
+// a full-length (n) double vector: each rank's own rows
+RankRanges vec_ranges(afn_handle h, int s) {
+  const Seg2 g = shard_rows(h->n, h->k, h->R, s);
+  return {{8 * (size_t)g.a0, 8 * (size_t)g.na}, {8 * (size_t)g.b0, 8 * (size_t)g.nb}};
+}
+// the landmark block [0, k) of a full-length vector
+RankRanges landmark_ranges(afn_handle h, int s) {
+  const Seg2 g = shard_rows(h->n, h->k, h->R, s);
+  return {{8 * (size_t)g.a0, 8 * (size_t)g.na}};
+}
+// an N2-vector (non-landmark numbering), `width` bytes per row
+RankRanges rows2_ranges(afn_handle h, int s, size_t width) {
+  const Seg2 g = shard_rows(h->n, h->k, h->R, s);
+  const size_t lo = (size_t)(g.b0 - h->k);
+  return {{width * lo, width * (size_t)g.nb}};
+}
+// pattern-aligned arrays (col / gval) of the rank's rows, `width` bytes per nonzero
+RankRanges nnz_ranges(afn_handle h, int s, size_t width) {
+  const Seg2 g = shard_rows(h->n, h->k, h->R, s);
+  const int64_t lo = g.b0 - h->k, hi = lo + g.nb;
+  const int64_t e0 = rowptr_at(lo, h->params.w), e1 = rowptr_at(hi, h->params.w);
+  return {{width * (size_t)e0, width * (size_t)(e1 - e0)}};
+}
+
+// destination of a rank's partial of scalar `slot`
+double* part_dst(afn_handle h, RankSt& s, int slot) {
+  return h->R == 1 ? s.sc + slot : s.scpart + (size_t)s.rank * SC_N + slot;
+}
+// sum the partials of the slots in `mask` over the ranks (rank order)
+afn_status reduce_slots(afn_handle h, unsigned mask, cudaStream_t st) {
+  if (h->R == 1) return AFN_OK;
+  TRY(exchange(h, [](RankSt& s) { return s.scpart; },
+               [&](int s) { return RankRanges{{8 * (size_t)s * SC_N, 8 * (size_t)SC_N}}; }, st));
+  for (auto& s : h->rk) TRY(combine_slots(s.scpart, h->R, SC_N, mask, s.sc, st));
+  return AFN_OK;
 }
 
 // algorithmic HBM bytes of one apply: W read twice, L^{-T} twice (upper half),
@@ -309,23 +389,47 @@ double apply_bytes(afn_handle h) {
   return 8.0 * (2.0 * N2 * k + k * (k + 1.0)) + 2.0 * 12.0 * nnz + 8.0 * (6.0 * N2 + 6.0 * k);
 }
 
-// z = M^{-1} r in the permuted order (V-form)
-afn_status apply_perm(afn_handle h, const double* r, double* z, cudaStream_t st) {
+// z = M^{-1} r in the permuted order (V-form):
+//   t = L^{-1} r1;  u = r2 - W t;  y = G u;  s2 = G^T y;  s1 = L^{-T} (t - W^T s2).
+// r: the rank's own rows valid (landmark rows are all-gathered here); z: the
+// rank's own rows are written (s1 in full).
+template <class RF, class ZF>
+afn_status apply_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   const int64_t k = h->k, N2 = h->N2;
-  // t = L^{-1} r1 = (L^{-T})^T r1
-  TRY(gemv_t(h->LinvT, k, k, r, nullptr, 1.0, h->tvec, h->gws, st));
+  const int R = h->R;
+  // t = L^{-1} r1 needs all of r1
+  TRY(exchange(h, r_of, [&](int s) { return landmark_ranges(h, s); }, st));
+  for (auto& s : h->rk) {
+    const double* r = r_of(s);
+    TRY(gemv_t(s.LinvT, k, k, r, nullptr, 1.0, s.tvec, s.gws, st));
+    // u = r2 - W t (own rows)
+    if (s.hi > s.lo) TRY(gemv_n(s.W, s.hi - s.lo, k, s.tvec, r + k + s.lo, -1.0, s.uvec + s.lo, st));
+  }
   if (N2 > 0) {
-    // u = r2 - W t
-    TRY(gemv_n(h->W, N2, k, h->tvec, r + k, -1.0, h->uvec, st));
-    // y = G u ; s2 = G^T y
-    TRY(spmv_csr(h->rp, h->col, h->gval, N2, h->uvec, h->yvec, st));
-    TRY(spmv_csr(h->trp, h->tcol, h->tval, N2, h->yvec, z + k, st));
-    // v = t - W^T s2
-    TRY(gemv_t(h->W, N2, k, z + k, h->tvec, -1.0, h->vvec, h->gws, st));
-    // s1 = L^{-T} v
-    TRY(gemv_n(h->LinvT, k, k, h->vvec, nullptr, 1.0, z, st));
+    TRY(exchange(h, [](RankSt& s) { return s.uvec; }, [&](int s) { return rows2_ranges(h, s, 8); }, st));
+    for (auto& s : h->rk)  // y = G u (own rows)
+      TRY(spmv_csr(s.rp + s.lo, s.col, s.gval, s.hi - s.lo, s.uvec, s.yvec + s.lo, st));
+    TRY(exchange(h, [](RankSt& s) { return s.yvec; }, [&](int s) { return rows2_ranges(h, s, 8); }, st));
+    for (auto& s : h->rk) {
+      double* z = z_of(s);
+      // s2 = G^T y (own rows of G^T)
+      TRY(spmv_csr(s.trp + s.lo, s.tcol, s.tval, s.hi - s.lo, s.yvec, z + k + s.lo, st));
+      if (R == 1) {  // v = t - W^T s2
+        TRY(gemv_t(s.W, N2, k, z + k, s.tvec, -1.0, s.vvec, s.gws, st));
+      } else {       // rank partial of W^T s2
+        double* kp = s.kpart + (size_t)s.rank * k;
+        if (s.hi > s.lo) TRY(gemv_t(s.W, s.hi - s.lo, k, z + k + s.lo, nullptr, 1.0, kp, s.gws, st));
+        else AFN_CUDA(cudaMemsetAsync(kp, 0, sizeof(double) * k, st));
+      }
+    }
+    if (R > 1) {
+      TRY(exchange(h, [](RankSt& s) { return s.kpart; },
+                   [&](int s) { return RankRanges{{8 * (size_t)s * k, 8 * (size_t)k}}; }, st));
+      for (auto& s : h->rk) TRY(combine_sub(s.kpart, R, k, s.tvec, s.vvec, st));
+    }
+    for (auto& s : h->rk) TRY(gemv_n(s.LinvT, k, k, s.vvec, nullptr, 1.0, z_of(s), st));  // s1
   } else {
-    TRY(gemv_n(h->LinvT, k, k, h->tvec, nullptr, 1.0, z, st));
+    for (auto& s : h->rk) TRY(gemv_n(s.LinvT, k, k, s.tvec, nullptr, 1.0, z_of(s), st));
   }
   return AFN_OK;
 }
@@ -341,6 +445,315 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, a, b);
   return ms;
+}
+
+// reusable event pairs for per-phase timing inside a solve
+struct EvPairs {
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  ~EvPairs() {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+  cudaEvent_t next() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  double total_ms() {  // pairs (0,1), (2,3), ...
+    double t = 0;
+    for (size_t i = 0; i + 1 < used; i += 2) t += ev_ms(pool[i], pool[i + 1]);
+    return t;
+  }
+};
+
+afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, const afn_params* prm,
+                      void* stream, afn_handle* out) {
+  REQ(out != nullptr, "out must be non-null");
+  *out = nullptr;
+  TRY(validate_X(X, n, d));
+  REQ(prm != nullptr, "params must be non-null");
+  const afn_params P = *prm;
+  REQ(P.l > 0 && std::isfinite(P.l), "l must be > 0");
+  REQ(P.mu > 0 && std::isfinite(P.mu), "mu must be > 0");
+  REQ(P.k_cap >= 1, "k_cap must be >= 1");
+  REQ(P.w >= 1 && P.w <= 128, "w must be in 1..128");
+  REQ(P.fps_seed >= 0 && P.fps_seed < n, "need 0 <= fps_seed < n");
+  REQ(n <= 0x7fffffffLL, "n must fit int32 indices");
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0;
+  AFN_CUDA(cudaGetDevice(&dev));
+
+  cudaEvent_t ev[10];
+  for (auto& e : ev) AFN_CUDA(cudaEventCreate(&e));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 10; ++i) cudaEventDestroy(e[i]);
+    }
+  } evg{ev};
+
+  afn_handle h = new afn_handle_s();
+  h->device = dev;
+  h->n = n;
+  h->d = d;
+  h->l = P.l;
+  h->mu = P.mu;
+  h->params = P;
+  h->comm = (comm && comm->R > 1) ? comm : nullptr;
+  h->R = h->comm ? comm->R : 1;
+  const int nlocal = h->comm ? comm->nlocal : 1;
+  const int rank0 = h->comm ? comm->rank0 : 0;
+  h->rk.resize(nlocal);
+  for (int q = 0; q < nlocal; ++q) h->rk[q].rank = rank0 + q;
+  struct HGuard {
+    afn_handle* hp;
+    ~HGuard() {
+      if (*hp) handle_free(*hp);
+    }
+  } hg{&h};
+
+  AFN_CUDA(cudaEventRecord(ev[0], st));
+  // ---- a2: adaptive k (Alg. 1) -- replicated: every rank computes the same k
+  int64_t k = std::min<int64_t>(P.k_cap, n);
+  if (P.k_adaptive) {
+    int m = P.m > 0 ? P.m : alg1_default_m(n);
+    REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
+    kt_begin(KT_ALG1, st);
+    TRY(alg1_run(X, n, d, P.l, m, P.rng_seed, P.k_threshold > 0 ? P.k_threshold : 2000, &h->a1, st));
+    kt_end(KT_ALG1, st, 0.0);
+    k = std::min<int64_t>(P.k_cap, std::max<int64_t>(1, h->a1.khat));
+    k = std::min<int64_t>(k, n);
+  }
+  h->k = k;
+  const int64_t N2 = n - k;
+  h->N2 = N2;
+  h->nnz = knn_nnz(N2, P.w);
+  for (auto& s : h->rk) {
+    s.own = shard_rows(n, k, h->R, s.rank);
+    s.lo = s.own.b0 - k;
+    s.hi = s.lo + s.own.nb;
+  }
+  AFN_CUDA(cudaEventRecord(ev[1], st));
+
+  // ---- a3: FPS (replicated)
+  std::vector<int64_t*> idx(nlocal);
+  kt_begin(KT_FPS, st);
+  for (int q = 0; q < nlocal; ++q) {
+    RankSt& s = h->rk[q];
+    TRY(ralloc(s, &idx[q], (size_t)k, st));
+    TRY(ralloc(s, &s.fill, (size_t)k, st));
+    TRY(fps_run(X, n, d, k, P.fps_seed, idx[q], s.fill, st));
+  }
+  kt_end(KT_FPS, st, 0.0);
+  AFN_CUDA(cudaEventRecord(ev[2], st));
+
+  // ---- a1: permutation, permuted + prescaled points; a4: L L^T = K11 + mu I, L^{-T}
+  for (int q = 0; q < nlocal; ++q) {
+    RankSt& s = h->rk[q];
+    TRY(ralloc(s, &s.derr, 4, st));
+    AFN_CUDA(cudaMemsetAsync(s.derr, 0, sizeof(int) * 4, st));
+    unsigned char* flag;
+    unsigned* flag32;
+    TRY(ralloc(s, &flag, (size_t)n, st));
+    TRY(ralloc(s, &flag32, (size_t)n, st));
+    AFN_CUDA(cudaMemsetAsync(flag32, 0, sizeof(unsigned) * (size_t)n, st));
+    mark_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(idx[q], k, n, flag32, s.derr);
+    AFN_LAUNCH_CHECK("mark_kernel");
+    flag8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flag32, n, flag);
+    AFN_LAUNCH_CHECK("flag8_kernel");
+    TRY(ralloc(s, &s.perm, (size_t)n, st));
+    perm_kernel<<<1, 1024, 0, st>>>(flag, idx[q], n, k, s.perm);
+    AFN_LAUNCH_CHECK("perm_kernel");
+    rfree(s, flag, st);
+    rfree(s, flag32, st);
+    TRY(ralloc(s, &s.Xp, (size_t)n * d, st));
+    TRY(gather_rows(X, n, d, s.perm, s.Xp, st));
+    TRY(ralloc(s, &s.Xs, (size_t)n * d, st));
+    TRY(kmv_prescale(s.Xp, n, d, P.l, s.Xs, st));
+    TRY(ralloc(s, &s.L, (size_t)k * k, st));
+    TRY(gen_k11(s.Xp, k, d, P.l, P.mu, s.L, st));
+    TRY(ralloc(s, &s.dinfo, 2, st));
+    AFN_CUDA(cudaMemsetAsync(s.dinfo, 0, sizeof(int) * 2, st));
+    kt_begin(KT_POTRF, st);
+    TRY(potrf_lower(s.L, k, s.dinfo, st));
+    kt_end(KT_POTRF, st, (double)k * k * k / 3.0);
+    TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
+    kt_begin(KT_LINV, st);
+    TRY(trsm_linvt(s.L, k, s.LinvT, st));
+    kt_end(KT_LINV, st, (double)k * k * k / 3.0);
+  }
+  AFN_CUDA(cudaEventRecord(ev[3], st));
+  for (auto& s : h->rk) {
+    int info = 0;
+    AFN_CUDA(cudaMemcpyAsync(&info, s.dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    if (info) {
+      set_error("Cholesky of K11 + mu I broke down at row %d", info - 1);
+      return AFN_ERR_NOT_SPD;
+    }
+  }
+
+  // ---- a5: W = K21 L^{-T}, own rows (into a full-height buffer when sharded:
+  // the FSAI rows of a rank need the W rows of all their pattern neighbours)
+  std::vector<double*> Wf(nlocal);
+  static const bool w_trsm = getenv("AFN_W_TRSM") != nullptr;
+  kt_begin(KT_W_GEMM, st);
+  for (int q = 0; q < nlocal; ++q) {
+    RankSt& s = h->rk[q];
+    TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
+    const double* X2 = s.Xp + k * d;
+    if (s.hi > s.lo) {
+      if (w_trsm) TRY(trsm_w(s.L, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, P.l, Wf[q] + s.lo * k, st));
+      else TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, P.l, Wf[q] + s.lo * k, st));
+    }
+  }
+  kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k / h->R);  // (N2/R) k^2/2 FMA per rank
+  AFN_CUDA(cudaEventRecord(ev[4], st));
+
+  // ---- a6: kNN pattern (own rows; row_ptr in closed form)
+  kt_begin(KT_KNN, st);
+  for (auto& s : h->rk) {
+    TRY(ralloc(s, &s.rp, (size_t)N2 + 1, st));
+    TRY(ralloc(s, &s.col, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
+    if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, st, s.lo, s.hi));
+    else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), st));
+  }
+  kt_end(KT_KNN, st, 0.0);
+  AFN_CUDA(cudaEventRecord(ev[5], st));
+  if (N2 > 0) {
+    // exchange W rows and pattern rows
+    {
+      int q = 0;
+      TRY(exchange(h, [&](RankSt&) { return Wf[q++]; },
+                   [&](int s) { return rows2_ranges(h, s, 8 * (size_t)k); }, st));
+    }
+    TRY(exchange(h, [](RankSt& s) { return s.col; }, [&](int s) { return nnz_ranges(h, s, 4); }, st));
+    for (auto& s : h->rk) {
+      check_pattern_kernel<<<(unsigned)((N2 + 255) / 256), 256, 0, st>>>(s.rp, s.col, N2, s.derr);
+      AFN_LAUNCH_CHECK("check_pattern_kernel");
+    }
+  }
+  AFN_CUDA(cudaEventRecord(ev[6], st));
+
+  // ---- a7: FSAI rows (own), then G^T
+  std::vector<int64_t*> tmap(nlocal, nullptr);
+  for (int q = 0; q < nlocal; ++q) {
+    RankSt& s = h->rk[q];
+    TRY(ralloc(s, &s.gval, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
+    TRY(ralloc(s, &s.trp, (size_t)N2 + 1, st));
+    TRY(ralloc(s, &s.tcol, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
+    TRY(ralloc(s, &s.tval, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
+    if (N2 > 0) {
+      TRY(ralloc(s, &tmap[q], (size_t)(h->nnz > 0 ? h->nnz : 1), st));
+      // transposed pattern first (the pair-union FSAI needs "rows containing a")
+      TRY(csr_transpose(s.rp, s.col, nullptr, N2, h->nnz, s.trp, s.tcol, nullptr, st, tmap[q]));
+    } else {
+      AFN_CUDA(cudaMemsetAsync(s.trp, 0, sizeof(int64_t), st));
+    }
+  }
+  AFN_CUDA(cudaEventRecord(ev[7], st));
+  if (N2 > 0) {
+    static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : -1;
+    for (int q = 0; q < nlocal; ++q) {
+      RankSt& s = h->rk[q];
+      const double* X2 = s.Xp + k * d;
+      afn_status fs = AFN_ERR_STATE;
+      if (variant < 0) {
+        fs = fsai_sddmm_run(X2, N2, d, P.l, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo, s.hi,
+                            s.gval, s.dinfo + 1, st);
+        if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
+      }
+      if (fs != AFN_OK) {
+        kt_begin(KT_FSAI_GRAM, st);
+        TRY(fsai_run(X2, N2, d, P.l, P.mu, Wf[q], k, s.rp, s.col, s.lo, s.hi, s.gval, s.dinfo + 1, st));
+        kt_end(KT_FSAI_GRAM, st, 0.0);
+      }
+    }
+  }
+  AFN_CUDA(cudaEventRecord(ev[8], st));
+  if (N2 > 0) {
+    TRY(exchange(h, [](RankSt& s) { return s.gval; }, [&](int s) { return nnz_ranges(h, s, 8); }, st));
+    for (int q = 0; q < nlocal; ++q) {
+      RankSt& s = h->rk[q];
+      TRY(gather_map(s.gval, tmap[q], h->nnz, s.tval, st));
+      rfree(s, tmap[q], st);
+    }
+  }
+  // W: keep the rank's own rows only
+  for (int q = 0; q < nlocal; ++q) {
+    RankSt& s = h->rk[q];
+    if (h->R == 1) {
+      s.W = Wf[q];
+    } else {
+      TRY(ralloc(s, &s.W, (size_t)std::max<int64_t>(1, s.hi - s.lo) * k, st));
+      if (s.hi > s.lo)
+        AFN_CUDA(cudaMemcpyAsync(s.W, Wf[q] + s.lo * k, sizeof(double) * (s.hi - s.lo) * k,
+                                 cudaMemcpyDeviceToDevice, st));
+      rfree(s, Wf[q], st);
+    }
+  }
+
+  // ---- workspaces for apply / PCG
+  for (auto& s : h->rk) {
+    const int64_t nl = s.own.size();
+    s.plan = kmv_plan(n, nl, d, num_sms());
+    TRY(ralloc(s, &s.kmv_part, (size_t)s.plan.chunks * std::max<int64_t>(1, nl), st));
+    const int64_t gw = std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k));
+    TRY(ralloc(s, &s.gws, (size_t)gw, st));
+    TRY(ralloc(s, &s.tvec, (size_t)k, st));
+    TRY(ralloc(s, &s.vvec, (size_t)k, st));
+    TRY(ralloc(s, &s.kpart, (size_t)h->R * k, st));
+    TRY(ralloc(s, &s.uvec, (size_t)(N2 > 0 ? N2 : 1), st));
+    TRY(ralloc(s, &s.yvec, (size_t)(N2 > 0 ? N2 : 1), st));
+    TRY(ralloc(s, &s.rbuf, (size_t)n, st));
+    TRY(ralloc(s, &s.zbuf, (size_t)n, st));
+    for (double** v : {&s.x, &s.r, &s.z, &s.p, &s.q}) {
+      TRY(ralloc(s, v, (size_t)n, st));
+      AFN_CUDA(cudaMemsetAsync(*v, 0, sizeof(double) * n, st));
+    }
+    TRY(ralloc(s, &s.sc, SC_N, st));
+    TRY(ralloc(s, &s.scpart, (size_t)h->R * SC_N, st));
+    TRY(ralloc(s, &s.dws, (size_t)dot_ws(), st));
+    TRY(ralloc(s, &s.dcnt, 4, st));
+    AFN_CUDA(cudaMemsetAsync(s.dcnt, 0, sizeof(unsigned) * 4, st));
+    AFN_CUDA(cudaMemsetAsync(s.sc, 0, sizeof(double) * SC_N, st));
+    AFN_CUDA(cudaMemsetAsync(s.scpart, 0, sizeof(double) * h->R * SC_N, st));
+  }
+  if (!pinned_scalars()) {
+    set_error("pinned host allocation failed");
+    return AFN_ERR_NOMEM;
+  }
+  AFN_CUDA(cudaEventRecord(ev[9], st));
+  AFN_CUDA(cudaStreamSynchronize(st));
+  for (auto& s : h->rk) {
+    int e = 0;
+    AFN_CUDA(cudaMemcpy(&e, s.derr, sizeof(int), cudaMemcpyDeviceToHost));
+    if (e) {
+      set_error("internal consistency check failed (code %d: 1/2 landmark ids, 4/8 pattern)", e);
+      return AFN_ERR_CUDA;
+    }
+    int info = 0;
+    AFN_CUDA(cudaMemcpy(&info, s.dinfo + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    if (info && !getenv("AFN_DEBUG_ALLOW_NOT_SPD")) {
+      set_error("FSAI block Cholesky broke down in row %d", info - 1);
+      return AFN_ERR_NOT_SPD;
+    }
+  }
+  h->ms[0] = ev_ms(ev[0], ev[1]);  // alg1
+  h->ms[1] = ev_ms(ev[1], ev[2]);  // fps
+  h->ms[2] = ev_ms(ev[2], ev[3]);  // perm + chol + L^{-T}
+  h->ms[3] = ev_ms(ev[3], ev[4]);  // W
+  h->ms[4] = ev_ms(ev[4], ev[5]);  // knn
+  h->ms[5] = ev_ms(ev[5], ev[9]);  // exchanges + transpose + fsai + G^T + workspaces
+  h->ms[6] = ev_ms(ev[0], ev[9]);  // total
+  h->ms[7] = ev_ms(ev[7], ev[8]);  // fsai rows
+  kt_collect();
+  *out = h;
+  h = nullptr;  // release the guard
+  return AFN_OK;
 }
 
 }  // namespace
@@ -387,7 +800,7 @@ afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, double l, d
   KmvPlan plan = kmv_plan(n, nrows, d, num_sms());
   double* part;
   TRY(t.get(&part, (size_t)plan.chunks * (nrows > 0 ? nrows : 1)));
-  TRY(kmv_launch(Xs, n, d, v, mu, row0, nrows, y, part, plan, st));
+  TRY(kmv_launch(Xs, n, d, v, mu, seg_range(row0, nrows), y, false, part, plan, st));
   return AFN_OK;
 }
 
@@ -439,240 +852,22 @@ afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, double l, in
 
 afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* prm, void* stream,
                      afn_handle* out) {
-  REQ(out != nullptr, "out must be non-null");
-  *out = nullptr;
-  TRY(validate_X(X, n, d));
-  REQ(prm != nullptr, "params must be non-null");
-  const afn_params P = *prm;
-  REQ(P.l > 0 && std::isfinite(P.l), "l must be > 0");
-  REQ(P.mu > 0 && std::isfinite(P.mu), "mu must be > 0");
-  REQ(P.k_cap >= 1, "k_cap must be >= 1");
-  REQ(P.w >= 1 && P.w <= 128, "w must be in 1..128");
-  REQ(P.fps_seed >= 0 && P.fps_seed < n, "need 0 <= fps_seed < n");
-  REQ(n <= 0x7fffffffLL, "n must fit int32 indices");
-  cudaStream_t st = (cudaStream_t)stream;
-  int dev = 0;
-  AFN_CUDA(cudaGetDevice(&dev));
+  return build_impl(nullptr, X, n, d, prm, stream, out);
+}
 
-  cudaEvent_t ev[8];
-  for (auto& e : ev) AFN_CUDA(cudaEventCreate(&e));
-  struct EvGuard {
-    cudaEvent_t* e;
-    ~EvGuard() {
-      for (int i = 0; i < 8; ++i) cudaEventDestroy(e[i]);
-    }
-  } evg{ev};
-
-  afn_handle h = new afn_handle_s();
-  h->device = dev;
-  h->n = n;
-  h->d = d;
-  h->l = P.l;
-  h->mu = P.mu;
-  h->params = P;
-  struct HGuard {
-    afn_handle* hp;
-    ~HGuard() {
-      if (*hp) handle_free(*hp);
-    }
-  } hg{&h};
-
-  AFN_CUDA(cudaEventRecord(ev[0], st));
-  // ---- a2: adaptive k (Alg. 1)
-  int64_t k = std::min<int64_t>(P.k_cap, n);
-  if (P.k_adaptive) {
-    int m = P.m > 0 ? P.m : alg1_default_m(n);
-    REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
-    TRY(alg1_run(X, n, d, P.l, m, P.rng_seed, P.k_threshold > 0 ? P.k_threshold : 2000, &h->a1, st));
-    k = std::min<int64_t>(P.k_cap, std::max<int64_t>(1, h->a1.khat));
-    k = std::min<int64_t>(k, n);
-  }
-  h->k = k;
-  h->N2 = n - k;
-  AFN_CUDA(cudaEventRecord(ev[1], st));
-
-  // ---- a3: FPS
-  int64_t* idx;
-  TRY(halloc(h, (void**)&idx, sizeof(int64_t) * k, st));
-  TRY(halloc(h, (void**)&h->fill, sizeof(double) * k, st));
-  kt_begin(KT_FPS, st);
-  TRY(fps_run(X, n, d, k, P.fps_seed, idx, h->fill, st));
-  kt_end(KT_FPS, st, 0.0);
-  AFN_CUDA(cudaEventRecord(ev[2], st));
-
-  // ---- a1: permutation, permuted + prescaled points
-  int* derr;
-  TRY(halloc(h, (void**)&derr, sizeof(int) * 4, st));
-  AFN_CUDA(cudaMemsetAsync(derr, 0, sizeof(int) * 4, st));
-  {
-    unsigned char* flag;
-    unsigned* flag32;
-    TRY(halloc(h, (void**)&flag, (size_t)n, st));
-    TRY(halloc(h, (void**)&flag32, sizeof(unsigned) * (size_t)n, st));
-    AFN_CUDA(cudaMemsetAsync(flag32, 0, sizeof(unsigned) * (size_t)n, st));
-    mark_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(idx, k, n, flag32, derr);
-    AFN_LAUNCH_CHECK("mark_kernel");
-    flag8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flag32, n, flag);
-    AFN_LAUNCH_CHECK("flag8_kernel");
-    TRY(halloc(h, (void**)&h->perm, sizeof(int64_t) * n, st));
-    perm_kernel<<<1, 1024, 0, st>>>(flag, idx, n, k, h->perm);
-    AFN_LAUNCH_CHECK("perm_kernel");
-  }
-  TRY(halloc(h, (void**)&h->Xp, sizeof(double) * n * d, st));
-  TRY(gather_rows(X, n, d, h->perm, h->Xp, st));
-  TRY(halloc(h, (void**)&h->Xs, sizeof(double) * n * d, st));
-  TRY(kmv_prescale(h->Xp, n, d, P.l, h->Xs, st));
-
-  // ---- a4: L L^T = K11 + mu I ; L^{-T}
-  TRY(halloc(h, (void**)&h->L, sizeof(double) * k * k, st));
-  TRY(gen_k11(h->Xp, k, d, P.l, P.mu, h->L, st));
-  int* dinfo;
-  TRY(halloc(h, (void**)&dinfo, sizeof(int) * 2, st));
-  AFN_CUDA(cudaMemsetAsync(dinfo, 0, sizeof(int) * 2, st));
-  kt_begin(KT_POTRF, st);
-  TRY(potrf_lower(h->L, k, dinfo, st));
-  kt_end(KT_POTRF, st, (double)k * k * k / 3.0);
-  TRY(halloc(h, (void**)&h->LinvT, sizeof(double) * k * k, st));
-  kt_begin(KT_LINV, st);
-  TRY(trsm_linvt(h->L, k, h->LinvT, st));
-  kt_end(KT_LINV, st, (double)k * k * k / 3.0);
-  AFN_CUDA(cudaEventRecord(ev[3], st));
-  {
-    int info = 0;
-    AFN_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
-    AFN_CUDA(cudaStreamSynchronize(st));
-    if (info) {
-      set_error("Cholesky of K11 + mu I broke down at row %d", info - 1);
-      return AFN_ERR_NOT_SPD;
-    }
-  }
-
-  const int64_t N2 = h->N2;
-  const double* X2 = h->Xp + k * d;
-  // ---- a5: W = K21 L^{-T}
-  TRY(halloc(h, (void**)&h->W, sizeof(double) * (size_t)(N2 > 0 ? N2 : 1) * k, st));
-  static const bool w_trsm = getenv("AFN_W_TRSM") != nullptr;
-  if (w_trsm) TRY(trsm_w(h->L, k, h->Xp, X2, N2, d, P.l, h->W, st));
-  else {
-    kt_begin(KT_W_GEMM, st);
-    TRY(w_gemm(h->LinvT, k, h->Xp, X2, N2, d, P.l, h->W, st));
-    kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k);  // N2 k^2/2 FMA
-  }
-  AFN_CUDA(cudaEventRecord(ev[4], st));
-
-  // ---- a6: kNN pattern
-  h->nnz = knn_nnz(N2, P.w);
-  TRY(halloc(h, (void**)&h->rp, sizeof(int64_t) * (N2 + 1), st));
-  TRY(halloc(h, (void**)&h->col, sizeof(int32_t) * (h->nnz > 0 ? h->nnz : 1), st));
-  if (N2 > 0) {
-    kt_begin(KT_KNN, st);
-    TRY(knn_run(X2, N2, d, P.w, h->rp, h->col, st));
-    kt_end(KT_KNN, st, 0.0);
-    check_pattern_kernel<<<(unsigned)((N2 + 255) / 256), 256, 0, st>>>(h->rp, h->col, N2, derr);
-    AFN_LAUNCH_CHECK("check_pattern_kernel");
-  } else {
-    AFN_CUDA(cudaMemsetAsync(h->rp, 0, sizeof(int64_t), st));
-  }
-  AFN_CUDA(cudaEventRecord(ev[5], st));
-
-  // ---- a7: FSAI rows, then G^T
-  TRY(halloc(h, (void**)&h->gval, sizeof(double) * (h->nnz > 0 ? h->nnz : 1), st));
-  TRY(halloc(h, (void**)&h->trp, sizeof(int64_t) * (N2 + 1), st));
-  TRY(halloc(h, (void**)&h->tcol, sizeof(int32_t) * (h->nnz > 0 ? h->nnz : 1), st));
-  TRY(halloc(h, (void**)&h->tval, sizeof(double) * (h->nnz > 0 ? h->nnz : 1), st));
-  cudaEvent_t ef0, ef1;
-  AFN_CUDA(cudaEventCreate(&ef0));
-  AFN_CUDA(cudaEventCreate(&ef1));
-  struct EvGuard2 {
-    cudaEvent_t a, b;
-    ~EvGuard2() { cudaEventDestroy(a); cudaEventDestroy(b); }
-  } evg2{ef0, ef1};
-  AFN_CUDA(cudaEventRecord(ef0, st));
-  AFN_CUDA(cudaEventRecord(ef1, st));
-  if (N2 > 0) {
-    int64_t* tmap = nullptr;
-    TRY(halloc(h, (void**)&tmap, sizeof(int64_t) * (h->nnz > 0 ? h->nnz : 1), st));
-    // transposed pattern first (the pair-union FSAI needs "rows containing a")
-    TRY(csr_transpose(h->rp, h->col, nullptr, N2, h->nnz, h->trp, h->tcol, nullptr, st, tmap));
-    AFN_CUDA(cudaEventRecord(ef0, st));
-    static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : -1;
-    afn_status fs = AFN_ERR_STATE;
-    if (variant < 0) {
-      fs = fsai_sddmm_run(X2, N2, d, P.l, P.mu, h->W, k, h->rp, h->col, h->trp, h->tcol, h->gval,
-                          dinfo + 1, st);
-      if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
-    }
-    if (fs != AFN_OK) {
-      kt_begin(KT_FSAI_GRAM, st);
-      TRY(fsai_run(X2, N2, d, P.l, P.mu, h->W, k, h->rp, h->col, h->gval, dinfo + 1, st));
-      kt_end(KT_FSAI_GRAM, st, 0.0);
-    }
-    AFN_CUDA(cudaEventRecord(ef1, st));
-    TRY(gather_map(h->gval, tmap, h->nnz, h->tval, st));
-  } else {
-    AFN_CUDA(cudaMemsetAsync(h->trp, 0, sizeof(int64_t), st));
-  }
-  AFN_CUDA(cudaEventRecord(ev[6], st));
-
-  // ---- workspaces for apply / PCG
-  h->plan = kmv_plan(n, n, d, num_sms());
-  TRY(halloc(h, (void**)&h->kmv_part, sizeof(double) * h->plan.chunks * n, st));
-  const int64_t gw = std::max(gemv_t_ws(k, k), gemv_t_ws(N2, k));
-  TRY(halloc(h, (void**)&h->gws, sizeof(double) * gw, st));
-  TRY(halloc(h, (void**)&h->tvec, sizeof(double) * k, st));
-  TRY(halloc(h, (void**)&h->vvec, sizeof(double) * k, st));
-  TRY(halloc(h, (void**)&h->uvec, sizeof(double) * (N2 > 0 ? N2 : 1), st));
-  TRY(halloc(h, (void**)&h->yvec, sizeof(double) * (N2 > 0 ? N2 : 1), st));
-  TRY(halloc(h, (void**)&h->rbuf, sizeof(double) * n, st));
-  TRY(halloc(h, (void**)&h->zbuf, sizeof(double) * n, st));
-  for (double** v : {&h->x, &h->r, &h->z, &h->p, &h->q}) TRY(halloc(h, (void**)v, sizeof(double) * n, st));
-  TRY(halloc(h, (void**)&h->sc, sizeof(double) * SC_N, st));
-  TRY(halloc(h, (void**)&h->dws, sizeof(double) * dot_ws(), st));
-  TRY(halloc(h, (void**)&h->dcnt, sizeof(unsigned) * 4, st));
-  AFN_CUDA(cudaMemsetAsync(h->dcnt, 0, sizeof(unsigned) * 4, st));
-  AFN_CUDA(cudaMemsetAsync(h->sc, 0, sizeof(double) * SC_N, st));
-  h->h_sc = pinned_scalars();
-  if (!h->h_sc) {
-    set_error("pinned host allocation failed");
-    return AFN_ERR_NOMEM;
-  }
-  AFN_CUDA(cudaEventRecord(ev[7], st));
-  AFN_CUDA(cudaStreamSynchronize(st));
-  {
-    int e = 0;
-    AFN_CUDA(cudaMemcpy(&e, derr, sizeof(int), cudaMemcpyDeviceToHost));
-    if (e) {
-      set_error("internal consistency check failed (code %d: 1/2 landmark ids, 4/8 pattern)", e);
-      return AFN_ERR_CUDA;
-    }
-    int info = 0;
-    AFN_CUDA(cudaMemcpy(&info, dinfo + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (info && !getenv("AFN_DEBUG_ALLOW_NOT_SPD")) {
-      set_error("FSAI block Cholesky broke down in row %d", info - 1);
-      return AFN_ERR_NOT_SPD;
-    }
-  }
-  h->ms[0] = ev_ms(ev[0], ev[1]);  // alg1
-  h->ms[1] = ev_ms(ev[1], ev[2]);  // fps
-  h->ms[2] = ev_ms(ev[2], ev[3]);  // perm + chol + L^{-T}
-  h->ms[3] = ev_ms(ev[3], ev[4]);  // trsm W
-  h->ms[4] = ev_ms(ev[4], ev[5]);  // knn
-  h->ms[5] = ev_ms(ev[5], ev[6]);  // fsai + G^T
-  h->ms[6] = ev_ms(ev[0], ev[7]);  // total
-  h->ms[7] = ev_ms(ef0, ef1);      // fsai row kernel
-  kt_collect();
-  *out = h;
-  h = nullptr;  // release the guard
-  return AFN_OK;
+afn_status afn_build_dist(afn_comm comm, const double* X, int64_t n, int32_t d, const afn_params* prm,
+                          void* stream, afn_handle* out) {
+  return build_impl(comm, X, n, d, prm, stream, out);
 }
 
 afn_status afn_apply(afn_handle h, const double* r, double* z, void* stream) {
   REQ(h != nullptr, "null handle");
   REQ(is_dev(r) && is_dev(z) && r != z, "r, z must be distinct device pointers");
   cudaStream_t st = (cudaStream_t)stream;
-  TRY(gather_vec(r, h->perm, h->n, h->rbuf, st));
-  TRY(apply_perm(h, h->rbuf, h->zbuf, st));
-  TRY(scatter_vec(h->zbuf, h->perm, h->n, z, st));
+  for (auto& s : h->rk) TRY(gather_vec(r, s.perm, h->n, s.rbuf, st));
+  TRY(apply_perm(h, [](RankSt& s) { return s.rbuf; }, [](RankSt& s) { return s.zbuf; }, st));
+  TRY(exchange(h, [](RankSt& s) { return s.zbuf; }, [&](int s) { return vec_ranges(h, s); }, st));
+  TRY(scatter_vec(h->rk[0].zbuf, h->rk[0].perm, h->n, z, st));
   return AFN_OK;
 }
 
@@ -704,40 +899,60 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     cudaEvent_t e[6];
     ~EvG() { for (auto x : e) cudaEventDestroy(x); }
   } evg{{e0, e1, km0, km1, ap0, ap1}};
+  EvPairs cm;  // the per-iteration all-gathers of p (multi-rank)
   double mv_ms = 0.0, ap_ms = 0.0;
   int napply = 0;
   bool ap_pending = false;
+  auto sc_to_host = [&]() -> afn_status {
+    AFN_CUDA(cudaMemcpyAsync(hsc, h->rk[0].sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    return AFN_OK;
+  };
+  auto apply = [&]() -> afn_status {
+    return apply_perm(h, [](RankSt& s) { return s.r; }, [](RankSt& s) { return s.z; }, st);
+  };
   AFN_CUDA(cudaEventRecord(e0, st));
 
   // r = b (permuted), x = 0
-  TRY(gather_vec(b, h->perm, n, h->r, st));
-  AFN_CUDA(cudaMemsetAsync(h->x, 0, sizeof(double) * n, st));
-  TRY(dot(h->r, h->r, n, h->sc + SC_BB, h->dws, h->dcnt, st));
-  AFN_CUDA(cudaMemcpyAsync(hsc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
-  AFN_CUDA(cudaStreamSynchronize(st));
+  for (auto& s : h->rk) {
+    TRY(gather_vec(b, s.perm, n, s.r, st));
+    AFN_CUDA(cudaMemsetAsync(s.x, 0, sizeof(double) * n, st));
+    TRY(dot(s.r, s.r, s.own, part_dst(h, s, SC_BB), s.dws, s.dcnt, st));
+  }
+  TRY(reduce_slots(h, 1u << SC_BB, st));
+  TRY(sc_to_host());
   const double nb = std::sqrt(hsc[SC_BB]);
   if (R.history) R.history[0] = nb > 0 ? 1.0 : 0.0;
   int it = 0;
   double rel = nb > 0 ? 1.0 : 0.0;
   if (nb > 0) {
     AFN_CUDA(cudaEventRecord(ap0, st));
-    TRY(apply_perm(h, h->r, h->z, st));
+    TRY(apply());
     AFN_CUDA(cudaEventRecord(ap1, st));
     ap_pending = true;
     ++napply;
     int cur = SC_RZ0;
-    TRY(dot(h->r, h->z, n, h->sc + cur, h->dws, h->dcnt, st));
-    TRY(vec_copy(h->p, h->z, n, st));
+    for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, cur), s.dws, s.dcnt, st));
+    TRY(reduce_slots(h, 1u << cur, st));
+    for (auto& s : h->rk) TRY(vec_copy(s.p, s.z, s.own, st));
     for (it = 1; it <= maxit; ++it) {
       AFN_CUDA(cudaEventRecord(km0, st));
+      if (h->R > 1) {  // p: every rank's rows (the north star's per-iteration all-gather)
+        AFN_CUDA(cudaEventRecord(cm.next(), st));
+        TRY(exchange(h, [](RankSt& s) { return s.p; }, [&](int s) { return vec_ranges(h, s); }, st));
+        AFN_CUDA(cudaEventRecord(cm.next(), st));
+      }
       kt_begin(KT_KMV, st);
-      TRY(kmv_launch(h->Xs, n, d, h->p, h->mu, 0, n, h->q, h->kmv_part, h->plan, st));
-      kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0));
+      for (auto& s : h->rk)
+        TRY(kmv_launch(s.Xs, n, d, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+      kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0) / h->R);
       AFN_CUDA(cudaEventRecord(km1, st));
-      TRY(dot(h->p, h->q, n, h->sc + SC_PQ, h->dws, h->dcnt, st));
-      TRY(pcg_update_xr(h->x, h->r, h->p, h->q, n, h->sc, cur, h->dws, h->dcnt, st));
-      AFN_CUDA(cudaMemcpyAsync(hsc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
-      AFN_CUDA(cudaStreamSynchronize(st));
+      for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
+      TRY(reduce_slots(h, 1u << SC_PQ, st));
+      for (auto& s : h->rk)
+        TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
+      TRY(reduce_slots(h, 1u << SC_RR, st));
+      TRY(sc_to_host());
       mv_ms += ev_ms(km0, km1);
       if (ap_pending) {
         ap_ms += ev_ms(ap0, ap1);
@@ -762,40 +977,43 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
       }
       AFN_CUDA(cudaEventRecord(ap0, st));
       kt_begin(KT_APPLY, st);
-      TRY(apply_perm(h, h->r, h->z, st));
-      kt_end(KT_APPLY, st, apply_bytes(h));
+      TRY(apply());
+      kt_end(KT_APPLY, st, apply_bytes(h) / h->R);
       AFN_CUDA(cudaEventRecord(ap1, st));
       ap_pending = true;
       ++napply;
       const int nxt = cur ^ 1;
-      TRY(dot(h->r, h->z, n, h->sc + nxt, h->dws, h->dcnt, st));
-      TRY(pcg_update_p(h->p, h->z, n, h->sc, nxt, cur, st));
+      for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, nxt), s.dws, s.dcnt, st));
+      TRY(reduce_slots(h, 1u << nxt, st));
+      for (auto& s : h->rk) TRY(pcg_update_p(s.p, s.z, s.own, s.sc, nxt, cur, st));
       cur = nxt;
     }
     if (it > maxit) it = maxit;
   } else {
     R.converged = 1;
   }
-  // a = x (un-permuted); true residual ||b - (K + mu I) x|| / ||b||
-  TRY(scatter_vec(h->x, h->perm, n, a, st));
+  // a = x (all ranks' rows, un-permuted); true residual ||b - (K + mu I) x|| / ||b||
+  TRY(exchange(h, [](RankSt& s) { return s.x; }, [&](int s) { return vec_ranges(h, s); }, st));
+  TRY(scatter_vec(h->rk[0].x, h->rk[0].perm, n, a, st));
   AFN_CUDA(cudaEventRecord(e1, st));
   if (nb > 0) {
-    TRY(kmv_launch(h->Xs, n, d, h->x, h->mu, 0, n, h->q, h->kmv_part, h->plan, st));
-    TRY(gather_vec(b, h->perm, n, h->z, st));
-    TRY(vec_axpby(h->z, -1.0, h->q, 1.0, n, st));
-    TRY(dot(h->z, h->z, n, h->sc + SC_TMP, h->dws, h->dcnt, st));
-    AFN_CUDA(cudaMemcpyAsync(hsc, h->sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
+    for (auto& s : h->rk) {
+      TRY(kmv_launch(s.Xs, n, d, s.x, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+      TRY(gather_vec(b, s.perm, n, s.z, st));
+      TRY(vec_axpby(s.z, -1.0, s.q, 1.0, s.own, st));
+      TRY(dot(s.z, s.z, s.own, part_dst(h, s, SC_TMP), s.dws, s.dcnt, st));
+    }
+    TRY(reduce_slots(h, 1u << SC_TMP, st));
   }
-  AFN_CUDA(cudaStreamSynchronize(st));
+  TRY(sc_to_host());
   R.iterations = it;
   R.relres = rel;
   R.relres_true = nb > 0 ? std::sqrt(hsc[SC_TMP]) / nb : 0.0;
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  R.solve_ms = ms;
+  R.solve_ms = ev_ms(e0, e1);
   if (ap_pending) ap_ms += ev_ms(ap0, ap1);
   R.matvec_ms = mv_ms;
   R.apply_ms = ap_ms;
+  R.comm_ms = cm.total_ms();
   kt_collect();
   R.applies = napply;
   if (rep) *rep = R;
@@ -848,22 +1066,30 @@ afn_status afn_get_info(afn_handle h, afn_info* info) {
   I.ms_fsai = h->ms[5];
   I.ms_total = h->ms[6];
   I.ms_fsai_rows = h->ms[7];
+  I.nranks = h->R;
+  I.rank = h->rk[0].rank;
+  I.row_a0 = h->rk[0].own.a0;
+  I.row_na = h->rk[0].own.na;
+  I.row_b0 = h->rk[0].own.b0;
+  I.row_nb = h->rk[0].own.nb;
   *info = I;
   return AFN_OK;
 }
 
-afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes) {
+afn_status afn_copy_out_local(afn_handle h, int32_t local_rank, int32_t what, void* host, size_t bytes) {
   REQ(h && host, "null argument");
+  REQ(local_rank >= 0 && local_rank < (int)h->rk.size(), "local rank %d out of range", local_rank);
+  const RankSt& s = h->rk[local_rank];
   const void* src = nullptr;
   size_t need = 0;
   switch (what) {
-    case AFN_OUT_PERM: src = h->perm; need = sizeof(int64_t) * h->n; break;
-    case AFN_OUT_FILL: src = h->fill; need = sizeof(double) * h->k; break;
-    case AFN_OUT_L: src = h->L; need = sizeof(double) * h->k * h->k; break;
-    case AFN_OUT_ROWPTR: src = h->rp; need = sizeof(int64_t) * (h->N2 + 1); break;
-    case AFN_OUT_COL: src = h->col; need = sizeof(int32_t) * h->nnz; break;
-    case AFN_OUT_GVAL: src = h->gval; need = sizeof(double) * h->nnz; break;
-    case AFN_OUT_W: src = h->W; need = sizeof(double) * h->N2 * h->k; break;
+    case AFN_OUT_PERM: src = s.perm; need = sizeof(int64_t) * h->n; break;
+    case AFN_OUT_FILL: src = s.fill; need = sizeof(double) * h->k; break;
+    case AFN_OUT_L: src = s.L; need = sizeof(double) * h->k * h->k; break;
+    case AFN_OUT_ROWPTR: src = s.rp; need = sizeof(int64_t) * (h->N2 + 1); break;
+    case AFN_OUT_COL: src = s.col; need = sizeof(int32_t) * h->nnz; break;
+    case AFN_OUT_GVAL: src = s.gval; need = sizeof(double) * h->nnz; break;
+    case AFN_OUT_W: src = s.W; need = sizeof(double) * (s.hi - s.lo) * h->k; break;
     default: set_error("unknown copy_out selector %d", what); return AFN_ERR_ARG;
   }
   REQ(bytes == need, "copy_out: bytes=%zu, need %zu", bytes, need);
@@ -872,22 +1098,27 @@ afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes) {
   return AFN_OK;
 }
 
+afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes) {
+  return afn_copy_out_local(h, 0, what, host, bytes);
+}
+
 afn_status afn_copy_out_rows(afn_handle h, int32_t what, const int64_t* rows, int64_t nrows,
                              void* host, size_t bytes) {
   REQ(h && host && (rows || nrows == 0) && nrows >= 0, "null argument");
+  const RankSt& s = h->rk[0];
   const double* src = nullptr;
-  int64_t R = 0;
-  if (what == AFN_OUT_W) src = h->W, R = h->N2;
-  else if (what == AFN_OUT_L) src = h->L, R = h->k;
+  int64_t lo = 0, hi = 0;
+  if (what == AFN_OUT_W) src = s.W, lo = s.lo, hi = s.hi;
+  else if (what == AFN_OUT_L) src = s.L, lo = 0, hi = h->k;
   else REQ(false, "copy_out_rows: selector %d unsupported (W or L only)", what);
   const size_t rowb = sizeof(double) * (size_t)h->k;
   REQ(bytes == rowb * (size_t)nrows, "copy_out_rows: bytes=%zu, need %zu", bytes,
       rowb * (size_t)nrows);
   for (int64_t t = 0; t < nrows; ++t)
-    REQ(rows[t] >= 0 && rows[t] < R, "copy_out_rows: row %lld out of range [0, %lld)",
-        (long long)rows[t], (long long)R);
+    REQ(rows[t] >= lo && rows[t] < hi, "copy_out_rows: row %lld out of range [%lld, %lld)",
+        (long long)rows[t], (long long)lo, (long long)hi);
   for (int64_t t = 0; t < nrows; ++t)
-    AFN_CUDA(cudaMemcpy(static_cast<char*>(host) + rowb * t, src + (size_t)rows[t] * h->k, rowb,
+    AFN_CUDA(cudaMemcpy(static_cast<char*>(host) + rowb * t, src + (size_t)(rows[t] - lo) * h->k, rowb,
                         cudaMemcpyDeviceToHost));
   return AFN_OK;
 }

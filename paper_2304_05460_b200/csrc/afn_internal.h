@@ -4,9 +4,50 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+#include <vector>
+
 #include "../../include/afn.h"
 
+// Communicator (comm.cu): R logical ranks; this process drives ranks
+// [rank0, rank0 + nlocal) -- one with NCCL, all R when emulated (tests).
+struct afn_comm_s {
+  int R = 1;
+  int nlocal = 1;
+  int rank0 = 0;
+  bool emulated = false;
+  void* nccl = nullptr;  // ncclComm_t
+};
+
 namespace afn {
+
+using Comm = afn_comm_s;
+
+// Rows of the permuted order owned by one rank: a block of
+// the landmark rows [a0, a0+na) and a block of the non-landmark rows
+// [b0, b0+nb).  Row t of the rank's local numbering is phys(t).  With one
+// rank the two blocks are adjacent ({0, k, k, n-k}) and phys(t) = t.
+struct Seg2 {
+  int64_t a0 = 0, na = 0, b0 = 0, nb = 0;
+  __host__ __device__ int64_t size() const { return na + nb; }
+  __host__ __device__ int64_t phys(int64_t t) const { return t < na ? a0 + t : b0 + (t - na); }
+};
+inline Seg2 shard_rows(int64_t n, int64_t k, int R, int s) {
+  const int64_t N2 = n - k;
+  Seg2 g;
+  g.a0 = k * s / R;
+  g.na = k * (s + 1) / R - g.a0;
+  g.b0 = k + N2 * s / R;
+  g.nb = k + N2 * (s + 1) / R - g.b0;
+  return g;
+}
+inline Seg2 seg_range(int64_t row0, int64_t nrows) { return Seg2{row0, nrows, row0 + nrows, 0}; }
+
+// byte ranges [offset, offset+len) a rank owns in an exchanged buffer
+using RankRanges = std::vector<std::pair<size_t, size_t>>;
+// every local rank's buffer bufs[q] receives all ranks' owned ranges
+afn_status comm_allgatherv(const Comm* c, char* const* bufs, const std::vector<RankRanges>& owned,
+                           cudaStream_t st);
 
 int num_sms();  // SM count of the current device (cached per device)
 
@@ -29,9 +70,10 @@ struct KmvPlan {
 KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms);
 // Xs = X * sqrt(log2 e)/l   (n x d)
 afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs, cudaStream_t st);
-// y[0..nrows) = rows [row0,row0+nrows) of (K + mu I) v; partial: chunks*nrows doubles
-afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, int64_t row0,
-                      int64_t nrows, double* y, double* partial, const KmvPlan& p, cudaStream_t st);
+// rows `rows` of (K + mu I) v (v: all n entries); partial: chunks*rows.size() doubles.
+// y_phys: y[rows.phys(t)] (true) or y[t] (false) receives row t.
+afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, Seg2 rows,
+                      double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st);
 
 // ---- FPS (fps.cu) ---------------------------------------------------------
 afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
@@ -39,8 +81,9 @@ afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, i
 
 // ---- kNN pattern (knn.cu) -------------------------------------------------
 int64_t knn_nnz(int64_t N, int w);
+// row_ptr for all N rows (closed form); col for rows [row_lo, row_hi) (default: all)
 afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, int32_t* col,
-                   cudaStream_t st);
+                   cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = -1);
 
 // ---- dense build (dense.cu) -----------------------------------------------
 // gather rows: Y[i] = X[perm[i]] (n x d)
@@ -62,10 +105,11 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st);
 
 // ---- FSAI (fsai.cu) -------------------------------------------------------
-// G values on the pattern of the Schur complement S = K22 + mu I - W W^T
+// G values of rows [row_lo, row_hi) on the pattern of the Schur complement
+// S = K22 + mu I - W W^T (W: all N rows)
 afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
-                    int64_t k, const int64_t* row_ptr, const int32_t* col, double* gval,
-                    int* d_info, cudaStream_t st);
+                    int64_t k, const int64_t* row_ptr, const int32_t* col, int64_t row_lo,
+                    int64_t row_hi, double* gval, int* d_info, cudaStream_t st);
 // CSR transpose (N x N, columns sorted within each output row).  val/tval may
 // be null (pattern only); tmap (optional) receives the source nnz index.
 afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* val, int64_t N,
@@ -76,7 +120,8 @@ afn_status gather_map(const double* v, const int64_t* map, int64_t nnz, double* 
 // Returns AFN_ERR_STATE (nothing written) if a group's pair union overflows.
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
-                          const int32_t* tcol, double* gval, int* d_info, cudaStream_t st);
+                          const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval,
+                          int* d_info, cudaStream_t st);
 
 // ---- BLAS-2 / SpMV / vectors (blas.cu) ------------------------------------
 // y = ybase + alpha * A x, A: R x C row-major (lda = C).  ybase may be null (0)
@@ -91,20 +136,28 @@ afn_status spmv_csr(const int64_t* rp, const int32_t* col, const double* val, in
 afn_status gather_vec(const double* x, const int64_t* perm, int64_t n, double* y, cudaStream_t st);
 afn_status scatter_vec(const double* x, const int64_t* perm, int64_t n, double* y, cudaStream_t st);
 
-// deterministic dot: *out = a . b  (ws >= dot_ws() doubles, cnt: 1 zeroed uint)
+// Vector operations over the rows `g` of full-length (n) vectors.
+// deterministic dot: *out = a . b over g  (ws >= dot_ws() doubles, cnt: 1 zeroed uint)
 int64_t dot_ws();
-afn_status dot(const double* a, const double* b, int64_t n, double* out, double* ws,
-               unsigned* cnt, cudaStream_t st);
+afn_status dot(const double* a, const double* b, Seg2 g, double* out, double* ws, unsigned* cnt,
+               cudaStream_t st);
 // PCG scalar slots (device doubles): rz alternates between slots 0 and 1
 enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_N = 8 };
-// x += a p; r -= a q with a = sc[rz_slot]/sc[PQ] (0 if PQ <= 0); sc[RR] = r.r
-afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, int64_t n,
-                         double* sc, int rz_slot, double* ws, unsigned* cnt, cudaStream_t st);
-// p = z + beta p, beta = sc[rz_new_slot]/sc[rz_old_slot]
-afn_status pcg_update_p(double* p, const double* z, int64_t n, const double* sc, int rz_new_slot,
+// x += a p; r -= a q over g with a = sc[rz_slot]/sc[PQ] (0 if PQ <= 0); *rr = r.r over g
+afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, Seg2 g,
+                         const double* sc, int rz_slot, double* rr, double* ws, unsigned* cnt,
+                         cudaStream_t st);
+// p = z + beta p over g, beta = sc[rz_new_slot]/sc[rz_old_slot]
+afn_status pcg_update_p(double* p, const double* z, Seg2 g, const double* sc, int rz_new_slot,
                         int rz_old_slot, cudaStream_t st);
-afn_status vec_copy(double* y, const double* x, int64_t n, cudaStream_t st);
-afn_status vec_axpby(double* y, double a, const double* x, double b, int64_t n, cudaStream_t st);
+afn_status vec_copy(double* y, const double* x, Seg2 g, cudaStream_t st);
+afn_status vec_axpby(double* y, double a, const double* x, double b, Seg2 g, cudaStream_t st);
+// sc[slot] = sum_{s < R} part[s * stride + slot] (rank order) for each slot in mask
+afn_status combine_slots(const double* part, int R, int stride, unsigned mask, double* sc,
+                         cudaStream_t st);
+// y[c] = base[c] - sum_{s < R} part[s * C + c] (rank order), c < C
+afn_status combine_sub(const double* part, int R, int64_t C, const double* base, double* y,
+                       cudaStream_t st);
 
 // ---- Alg. 1 (alg1.cu) ------------------------------------------------------
 struct Alg1Result {

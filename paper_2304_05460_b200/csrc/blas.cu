@@ -131,52 +131,84 @@ __device__ void finish_sum(double partial, double* ws, unsigned* cnt, double* ou
 }
 
 __global__ void __launch_bounds__(VT) dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
-                                                int64_t n, double* out, double* ws, unsigned* cnt) {
+                                                Seg2 g, double* out, double* ws, unsigned* cnt) {
   __shared__ double sh[VT / 32];
   double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VT)
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * VT + threadIdx.x; t < n; t += (int64_t)gridDim.x * VT) {
+    const int64_t i = g.phys(t);
     s = fma(a[i], b[i], s);
+  }
   s = block_sum<VT>(s, sh);
   finish_sum(s, ws, cnt, out);
 }
 
 __global__ void __launch_bounds__(VT) update_xr_kernel(double* __restrict__ x, double* __restrict__ r,
                                                       const double* __restrict__ p,
-                                                      const double* __restrict__ q, int64_t n,
-                                                      double* sc, int rz_slot, double* ws,
-                                                      unsigned* cnt) {
+                                                      const double* __restrict__ q, Seg2 g,
+                                                      const double* sc, int rz_slot, double* rr,
+                                                      double* ws, unsigned* cnt) {
   __shared__ double sh[VT / 32];
   const double pq = sc[SC_PQ];
   const double alpha = (pq > 0.0 && isfinite(pq)) ? sc[rz_slot] / pq : 0.0;
   double s = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * VT + threadIdx.x; i < n; i += (int64_t)gridDim.x * VT) {
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * VT + threadIdx.x; t < n; t += (int64_t)gridDim.x * VT) {
+    const int64_t i = g.phys(t);
     x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     r[i] = ri;
     s = fma(ri, ri, s);
   }
   s = block_sum<VT>(s, sh);
-  finish_sum(s, ws, cnt, &sc[SC_RR]);
+  finish_sum(s, ws, cnt, rr);
 }
 
-__global__ void update_p_kernel(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+__global__ void update_p_kernel(double* __restrict__ p, const double* __restrict__ z, Seg2 g,
                                 const double* sc, int rz_new_slot, int rz_old_slot) {
   const double beta = sc[rz_new_slot] / sc[rz_old_slot];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = g.phys(t);
     p[i] = fma(beta, p[i], z[i]);
+  }
 }
 
-__global__ void copy_kernel(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
+__global__ void copy_kernel(double* __restrict__ y, const double* __restrict__ x, Seg2 g) {
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = g.phys(t);
     y[i] = x[i];
+  }
 }
 __global__ void axpby_kernel(double* __restrict__ y, double a, const double* __restrict__ x, double b,
-                             int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
+                             Seg2 g) {
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = g.phys(t);
     y[i] = fma(a, x[i], b * y[i]);
+  }
+}
+
+// rank-ordered sums of per-rank partials (deterministic, identical on every rank)
+__global__ void combine_slots_kernel(const double* __restrict__ part, int R, int stride, unsigned mask,
+                                     double* __restrict__ sc) {
+  const int slot = threadIdx.x;
+  if (slot >= stride || !((mask >> slot) & 1u)) return;
+  double s = 0.0;
+  for (int q = 0; q < R; ++q) s += part[(int64_t)q * stride + slot];
+  sc[slot] = s;
+}
+__global__ void combine_sub_kernel(const double* __restrict__ part, int R, int64_t C,
+                                   const double* __restrict__ base, double* __restrict__ y) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0;
+  for (int q = 0; q < R; ++q) s += part[(int64_t)q * C + c];
+  y[c] = base[c] - s;
 }
 
 unsigned grid_for(int64_t n, int nt, int cap) {
@@ -241,38 +273,55 @@ afn_status scatter_vec(const double* x, const int64_t* perm, int64_t n, double* 
 
 int64_t dot_ws() { return DOT_BLOCKS; }
 
-afn_status dot(const double* a, const double* b, int64_t n, double* out, double* ws, unsigned* cnt,
+afn_status dot(const double* a, const double* b, Seg2 g, double* out, double* ws, unsigned* cnt,
                cudaStream_t st) {
-  dot_kernel<<<DOT_BLOCKS, VT, 0, st>>>(a, b, n, out, ws, cnt);
+  dot_kernel<<<DOT_BLOCKS, VT, 0, st>>>(a, b, g, out, ws, cnt);
   AFN_LAUNCH_CHECK("dot_kernel");
   return AFN_OK;
 }
 
-afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, int64_t n,
-                         double* sc, int rz_slot, double* ws, unsigned* cnt, cudaStream_t st) {
-  update_xr_kernel<<<DOT_BLOCKS, VT, 0, st>>>(x, r, p, q, n, sc, rz_slot, ws, cnt);
+afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, Seg2 g,
+                         const double* sc, int rz_slot, double* rr, double* ws, unsigned* cnt,
+                         cudaStream_t st) {
+  update_xr_kernel<<<DOT_BLOCKS, VT, 0, st>>>(x, r, p, q, g, sc, rz_slot, rr, ws, cnt);
   AFN_LAUNCH_CHECK("update_xr_kernel");
   return AFN_OK;
 }
 
-afn_status pcg_update_p(double* p, const double* z, int64_t n, const double* sc, int rz_new_slot,
+afn_status pcg_update_p(double* p, const double* z, Seg2 g, const double* sc, int rz_new_slot,
                         int rz_old_slot, cudaStream_t st) {
-  update_p_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(p, z, n, sc, rz_new_slot, rz_old_slot);
+  if (g.size() <= 0) return AFN_OK;
+  update_p_kernel<<<grid_for(g.size(), 256, 1184), 256, 0, st>>>(p, z, g, sc, rz_new_slot, rz_old_slot);
   AFN_LAUNCH_CHECK("update_p_kernel");
   return AFN_OK;
 }
 
-afn_status vec_copy(double* y, const double* x, int64_t n, cudaStream_t st) {
-  if (n <= 0) return AFN_OK;
-  copy_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(y, x, n);
+afn_status vec_copy(double* y, const double* x, Seg2 g, cudaStream_t st) {
+  if (g.size() <= 0) return AFN_OK;
+  copy_kernel<<<grid_for(g.size(), 256, 1184), 256, 0, st>>>(y, x, g);
   AFN_LAUNCH_CHECK("copy_kernel");
   return AFN_OK;
 }
 
-afn_status vec_axpby(double* y, double a, const double* x, double b, int64_t n, cudaStream_t st) {
-  if (n <= 0) return AFN_OK;
-  axpby_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(y, a, x, b, n);
+afn_status vec_axpby(double* y, double a, const double* x, double b, Seg2 g, cudaStream_t st) {
+  if (g.size() <= 0) return AFN_OK;
+  axpby_kernel<<<grid_for(g.size(), 256, 1184), 256, 0, st>>>(y, a, x, b, g);
   AFN_LAUNCH_CHECK("axpby_kernel");
+  return AFN_OK;
+}
+
+afn_status combine_slots(const double* part, int R, int stride, unsigned mask, double* sc,
+                         cudaStream_t st) {
+  combine_slots_kernel<<<1, 32, 0, st>>>(part, R, stride, mask, sc);
+  AFN_LAUNCH_CHECK("combine_slots_kernel");
+  return AFN_OK;
+}
+
+afn_status combine_sub(const double* part, int R, int64_t C, const double* base, double* y,
+                       cudaStream_t st) {
+  if (C <= 0) return AFN_OK;
+  combine_sub_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(part, R, C, base, y);
+  AFN_LAUNCH_CHECK("combine_sub_kernel");
   return AFN_OK;
 }
 

@@ -1,8 +1,10 @@
 // fsai.cu -- FSAI factor G of the regularised Schur complement
 //   S = K22 + mu I - K21 (K11 + mu I)^{-1} K12 = K22 + mu I - W W^T
 // on the kNN pattern (Kolotilina-Yeremin).
-// "The computation of each row of G is independent" (L260-261): one CTA per
-// row i with pattern J (ascending, i last, |J| <= 128):
+// "The computation of each row of G is independent" (L260-261).  This file
+// holds the per-row fallback used when the pair-union path (fsai_sddmm.cu)
+// does not apply: one CTA per row i with pattern J (ascending, i last,
+// |J| <= 128):
 //   1. Gram  W_J W_J^T  (lower triangle only): W rows gathered in 32-column
 //      chunks through double-buffered shared memory (cp.async), 16x16 threads
 //      with stride-16 register micro-tiles;
@@ -38,180 +40,6 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 __device__ __forceinline__ int pk(int a, int b) { return a * (a + 1) / 2 + b; }  // packed lower, b <= a
 // column-major packed lower of a wp x wp matrix: entry (a, t), a >= t
 __device__ __forceinline__ int cmo(int a, int t, int wp) { return t * wp - (t * (t - 1)) / 2 + (a - t); }
-
-template <int MT>
-__global__ void __launch_bounds__(FT, 2)
-fsai_kernel(const double* __restrict__ X2, int64_t N, int d, double cl, double mu,
-            const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
-            const int32_t* __restrict__ col, double* __restrict__ gval, int* info) {
-  constexpr int WP = MT * 16;
-  constexpr int PW = WP + 1;  // staging pitch
-  extern __shared__ __align__(16) double smem[];
-  // layout: [ union{ staging 2*KC*PW , S packed WP*(WP+1)/2 } | X_J WP*d | J ]
-  constexpr int STG = 2 * KC * PW;
-  constexpr int SPK = WP * (WP + 1) / 2;
-  constexpr int U = STG > SPK ? STG : SPK;
-  double* stg = smem;
-  double* S = smem;
-  double* sX = smem + U;
-  int* sJ = reinterpret_cast<int*>(sX + WP * d);
-  __shared__ double s_tab[AFN_EXP2_TAB_N];
-  __shared__ int s_bad;
-
-  const int64_t i = blockIdx.x;
-  const int64_t beg = rp[i];
-  const int wp = (int)(rp[i + 1] - beg);
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  load_exp2_tab(s_tab);
-  if (tid == 0) s_bad = 0;
-  for (int a = tid; a < WP; a += FT) sJ[a] = a < wp ? col[beg + a] : -1;
-  __syncthreads();
-  for (int e = tid; e < WP * d; e += FT) {
-    const int a = e / d, c = e - a * d;
-    sX[e] = sJ[a] >= 0 ? X2[(int64_t)sJ[a] * d + c] : 0.0;
-  }
-
-  // ---------------- 1. Gram (lower blocks j <= i of the stride-16 tiling)
-  double acc[MT * (MT + 1) / 2];
-#pragma unroll
-  for (int t = 0; t < MT * (MT + 1) / 2; ++t) acc[t] = 0.0;
-
-  const int64_t nch = (k + KC - 1) / KC;
-  auto issue = [&](int64_t ch, int buf) {
-    double* dst = stg + buf * KC * PW;
-    const int64_t c0 = ch * KC;
-    for (int e = tid; e < WP * KC; e += FT) {
-      const int a = e / KC, kk = e - a * KC;
-      const int64_t c = c0 + kk;
-      const int ja = sJ[a];
-      if (ja >= 0 && c < k) cp_async8(&dst[kk * PW + a], &W[(int64_t)ja * k + c]);
-      else dst[kk * PW + a] = 0.0;
-    }
-    cp_async_commit();
-  };
-  if (nch > 0) issue(0, 0);
-  for (int64_t ch = 0; ch < nch; ++ch) {
-    const int buf = (int)(ch & 1);
-    if (ch + 1 < nch) {
-      issue(ch + 1, buf ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* T = stg + buf * KC * PW;
-#pragma unroll 2
-    for (int kk = 0; kk < KC; ++kk) {
-      double a[MT], b[MT];
-#pragma unroll
-      for (int m = 0; m < MT; ++m) {
-        a[m] = T[kk * PW + ty + 16 * m];
-        b[m] = T[kk * PW + tx + 16 * m];
-      }
-      int t = 0;
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int q = 0; q <= m; ++q) {
-          acc[t] = fma(a[m], b[q], acc[t]);
-          ++t;
-        }
-    }
-    __syncthreads();  // buffer `buf` is refilled by the next-next issue
-  }
-
-  // ---------------- 2. S_JJ = K_JJ + mu I - Gram  (packed lower)
-  {
-    int t = 0;
-#pragma unroll
-    for (int m = 0; m < MT; ++m)
-#pragma unroll
-      for (int q = 0; q <= m; ++q) {
-        const int a = ty + 16 * m, b = tx + 16 * q;
-        if (b <= a && a < wp) {
-          double kv;
-          if (a == b) {
-            kv = 1.0 + mu;
-          } else {
-            const double s = d2_exact_rt(&sX[a * d], &sX[b * d], d);
-            kv = gauss_from_d2(s, cl, s_tab);
-          }
-          S[pk(a, b)] = kv - acc[t];
-        }
-        ++t;
-      }
-  }
-  __syncthreads();
-
-  // ---------------- 3. Cholesky (right-looking, packed lower)
-  for (int j = 0; j < wp; ++j) {
-    if (tid == 0) {
-      const double p = S[pk(j, j)];
-      if (!(p > 0.0)) {
-        if (!s_bad) { s_bad = 1; atomicCAS(info, 0, (int)(i + 1)); }
-        S[pk(j, j)] = 1.0;
-      } else {
-        S[pk(j, j)] = sqrt(p);
-      }
-    }
-    __syncthreads();
-    const double piv = S[pk(j, j)];
-    for (int a = j + 1 + tid; a < wp; a += FT) S[pk(a, j)] /= piv;
-    __syncthreads();
-    for (int a = j + 1 + ty; a < wp; a += 16) {
-      const double sa = S[pk(a, j)];
-      for (int b = j + 1 + tx; b <= a; b += 16) S[pk(a, b)] = fma(-sa, S[pk(b, j)], S[pk(a, b)]);
-    }
-    __syncthreads();
-  }
-
-  // ---------------- 4. g = R^{-T} e_last  (one warp, back substitution)
-  if (tid < 32) {
-    const int lane = tid;
-    double rhs[WP / 32 > 0 ? (WP + 31) / 32 : 1];
-#pragma unroll
-    for (int s = 0; s < (WP + 31) / 32; ++s) {
-      const int t = lane + 32 * s;
-      rhs[s] = (t == wp - 1) ? 1.0 : 0.0;
-    }
-    for (int j = wp - 1; j >= 0; --j) {
-      double gj = 0.0;
-#pragma unroll
-      for (int s = 0; s < (WP + 31) / 32; ++s)
-        if (lane + 32 * s == j) gj = rhs[s] / S[pk(j, j)];
-      gj = __shfl_sync(0xffffffffu, gj, j & 31);
-#pragma unroll
-      for (int s = 0; s < (WP + 31) / 32; ++s) {
-        const int t = lane + 32 * s;
-        if (t < j) rhs[s] = fma(-S[pk(j, t)], gj, rhs[s]);
-        else if (t == j) rhs[s] = gj;
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < (WP + 31) / 32; ++s) {
-      const int t = lane + 32 * s;
-      if (t < wp) gval[beg + t] = rhs[s];
-    }
-  }
-}
-
-template <int MT>
-afn_status launch_fsai(const double* X2, int64_t N, int d, double cl, double mu, const double* W,
-                       int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* info,
-                       cudaStream_t st) {
-  constexpr int WP = MT * 16;
-  constexpr int PW = WP + 1;
-  constexpr int STG = 2 * KC * PW;
-  constexpr int SPK = WP * (WP + 1) / 2;
-  constexpr int U = STG > SPK ? STG : SPK;
-  const size_t bytes = sizeof(double) * (U + (size_t)WP * d) + sizeof(int) * WP + 16;
-  auto kern = fsai_kernel<MT>;
-  AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  kern<<<(unsigned)N, FT, bytes, st>>>(X2, N, d, cl, mu, W, k, rp, col, gval, info);
-  AFN_LAUNCH_CHECK("fsai_kernel");
-  return AFN_OK;
-}
-
 
 // ---------------------------------------------------------------------------
 // Split variant: (1) fsai_gram_kernel computes S_JJ (packed lower) for a batch
@@ -410,9 +238,9 @@ fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict_
 }
 
 template <int MT>
-afn_status launch_fsai_split(const double* X2, int64_t N, int d, double cl, double mu, const double* W,
-                             int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* info,
-                             cudaStream_t st) {
+afn_status launch_fsai_split(const double* X2, int64_t row_lo, int64_t row_hi, int d, double cl, double mu,
+                             const double* W, int64_t k, const int64_t* rp, const int32_t* col,
+                             double* gval, int* info, cudaStream_t st) {
   constexpr int WP = MT * 16;
   constexpr int PW = WP + 1;
   constexpr int64_t SPK = WP * (WP + 1) / 2;
@@ -421,221 +249,19 @@ afn_status launch_fsai_split(const double* X2, int64_t N, int d, double cl, doub
                        sizeof(int) * WP + 16;
   auto kg = fsai_gram_kernel<MT>;
   AFN_CUDA(cudaFuncSetAttribute(kg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  const int64_t batch = std::min<int64_t>(N, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
+  const int64_t NR = row_hi - row_lo;
+  const int64_t batch = std::min<int64_t>(NR, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
   double* Sg = nullptr;
   afn_status s = dalloc((void**)&Sg, sizeof(double) * SPK * batch, st);
   if (s != AFN_OK) return s;
-  for (int64_t r0 = 0; r0 < N; r0 += batch) {
-    const int64_t nr = std::min(batch, N - r0);
+  for (int64_t r0 = row_lo; r0 < row_hi; r0 += batch) {
+    const int64_t nr = std::min(batch, row_hi - r0);
     kg<<<(unsigned)nr, FT, bytes, st>>>(X2, r0, d, cl, mu, W, k, rp, col, Sg);
     AFN_LAUNCH_CHECK("fsai_gram_kernel");
     afn_status cs = fsai_chol_batch(r0, nr, MT, rp, Sg, gval, info, st);
     if (cs != AFN_OK) { dfree(Sg, st); return cs; }
   }
   dfree(Sg, st);
-  return AFN_OK;
-}
-
-// ---------------------------------------------------------------------------
-// Warp-specialised persistent variant: 8 "Gram" warps compute W_J W_J^T and
-// assemble S_JJ for row t while a 9th warp factors S_JJ of row t-1 and solves
-// for g (double-buffered S in shared memory, named-barrier handshakes).  The
-// FP64-heavy Gram then hides the latency-bound Cholesky.
-__device__ __forceinline__ void nbar_sync(int id, int cnt) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int cnt) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(cnt) : "memory");
-}
-
-constexpr int WS_PROD = 256;
-constexpr int WS_T = WS_PROD + 32;
-enum { BAR_PROD = 1, BAR_FULL0 = 2, BAR_EMPTY0 = 4 };
-
-template <int MT>
-__global__ void __launch_bounds__(WS_T, 1)
-fsai_ws_kernel(const double* __restrict__ X2, int64_t N, int d, double cl, double mu,
-               const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
-               const int32_t* __restrict__ col, double* __restrict__ gval, int* info) {
-  constexpr int WP = MT * 16;
-  constexpr int PW = WP + 1;
-  constexpr int STG = KC * PW;            // one staging buffer
-  constexpr int SPK = WP * (WP + 1) / 2;  // packed lower S
-  extern __shared__ __align__(16) double smem[];
-  double* stg = smem;                 // [2][STG]
-  double* Sb = smem + 2 * STG;        // [2][SPK]
-  double* sX = Sb + 2 * SPK;          // [WP * d]
-  int* sJ = reinterpret_cast<int*>(sX + WP * d);  // [WP]
-  __shared__ double s_tab[AFN_EXP2_TAB_N];
-  __shared__ long long s_meta[2][2];  // beg, (row << 8) | wp  per buffer
-
-  const int tid = threadIdx.x;
-  load_exp2_tab(s_tab);
-  __syncthreads();
-
-  if (tid < WS_PROD) {
-    // ===================== producers: Gram + S assembly =====================
-    const int ty = tid >> 4, tx = tid & 15;
-    int t = 0;
-    for (int64_t i = blockIdx.x; i < N; i += gridDim.x, ++t) {
-      const int buf = t & 1;
-      const int64_t beg = rp[i];
-      const int wp = (int)(rp[i + 1] - beg);
-      nbar_sync(BAR_PROD, WS_PROD);  // previous row finished with sJ / sX / stg
-      for (int a = tid; a < WP; a += WS_PROD) sJ[a] = a < wp ? col[beg + a] : -1;
-      nbar_sync(BAR_PROD, WS_PROD);
-      for (int e = tid; e < WP * d; e += WS_PROD) {
-        const int a = e / d, c = e - a * d;
-        sX[e] = sJ[a] >= 0 ? X2[(int64_t)sJ[a] * d + c] : 0.0;
-      }
-      double acc[MT * (MT + 1) / 2];
-#pragma unroll
-      for (int q = 0; q < MT * (MT + 1) / 2; ++q) acc[q] = 0.0;
-      const int64_t nch = (k + KC - 1) / KC;
-      auto issue = [&](int64_t ch, int b) {
-        double* dst = stg + b * STG;
-        const int64_t c0 = ch * KC;
-        for (int e = tid; e < WP * KC; e += WS_PROD) {
-          const int a = e / KC, kk = e - a * KC;
-          const int64_t c = c0 + kk;
-          const int ja = sJ[a];
-          if (ja >= 0 && c < k) cp_async8(&dst[kk * PW + a], &W[(int64_t)ja * k + c]);
-          else dst[kk * PW + a] = 0.0;
-        }
-        cp_async_commit();
-      };
-      issue(0, 0);
-      for (int64_t ch = 0; ch < nch; ++ch) {
-        const int sb = (int)(ch & 1);
-        if (ch + 1 < nch) {
-          issue(ch + 1, sb ^ 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
-        nbar_sync(BAR_PROD, WS_PROD);
-        const double* T = stg + sb * STG;
-#pragma unroll 2
-        for (int kk = 0; kk < KC; ++kk) {
-          double av[MT], bv[MT];
-#pragma unroll
-          for (int m = 0; m < MT; ++m) {
-            av[m] = T[kk * PW + ty + 16 * m];
-            bv[m] = T[kk * PW + tx + 16 * m];
-          }
-          int q = 0;
-#pragma unroll
-          for (int m = 0; m < MT; ++m)
-#pragma unroll
-            for (int qq = 0; qq <= m; ++qq) {
-              acc[q] = fma(av[m], bv[qq], acc[q]);
-              ++q;
-            }
-        }
-        nbar_sync(BAR_PROD, WS_PROD);
-      }
-      // S[buf] must be free (consumer done with row t-2)
-      if (t >= 2) nbar_sync(BAR_EMPTY0 + buf, WS_T);
-      double* S = Sb + buf * SPK;
-      int q = 0;
-#pragma unroll
-      for (int m = 0; m < MT; ++m)
-#pragma unroll
-        for (int qq = 0; qq <= m; ++qq) {
-          const int a = ty + 16 * m, b = tx + 16 * qq;
-          if (b <= a && a < wp) {
-            double kv;
-            if (a == b) {
-              kv = 1.0 + mu;
-            } else {
-              const double sd = d2_exact_rt(&sX[a * d], &sX[b * d], d);
-              kv = gauss_from_d2(sd, cl, s_tab);
-            }
-            S[pk(a, b)] = kv - acc[q];
-          }
-          ++q;
-        }
-      if (tid == 0) {
-        s_meta[buf][0] = beg;
-        s_meta[buf][1] = ((long long)i << 8) | wp;
-      }
-      nbar_arrive(BAR_FULL0 + buf, WS_T);
-    }
-  } else {
-    // ===================== consumer warp: Cholesky + back substitution ========
-    const int lane = tid & 31;
-    int t = 0;
-    for (int64_t i = blockIdx.x; i < N; i += gridDim.x, ++t) {
-      const int buf = t & 1;
-      nbar_sync(BAR_FULL0 + buf, WS_T);
-      double* S = Sb + buf * SPK;
-      const int64_t beg = s_meta[buf][0];
-      const int wp = (int)(s_meta[buf][1] & 0xff);
-      bool bad = false;
-      for (int j = 0; j < wp; ++j) {
-        double dj = S[pk(j, j)];
-        if (!(dj > 0.0)) { bad = true; dj = 1.0; }
-        const double piv = sqrt(dj);
-        const double inv = 1.0 / piv;
-        __syncwarp();
-        if (lane == 0) S[pk(j, j)] = piv;
-        for (int a = j + 1 + lane; a < wp; a += 32) S[pk(a, j)] *= inv;
-        __syncwarp();
-        for (int a = j + 1 + lane; a < wp; a += 32) {
-          const double la = S[pk(a, j)];
-          double* rowa = S + pk(a, 0);
-          const double* cj = S + pk(j + 1, j);  // S[b][j] for b = j+1, advancing by b+1
-          int off = 0;
-          for (int b = j + 1; b <= a; ++b) {
-            rowa[b] = fma(-la, cj[off], rowa[b]);
-            off += b + 1;
-          }
-        }
-        __syncwarp();
-      }
-      if (bad && lane == 0) atomicCAS(info, 0, (int)(i + 1));
-      // g = R^{-T} e_last
-      double rhs[(WP + 31) / 32];
-#pragma unroll
-      for (int s = 0; s < (WP + 31) / 32; ++s) rhs[s] = (lane + 32 * s == wp - 1) ? 1.0 : 0.0;
-      for (int j = wp - 1; j >= 0; --j) {
-        double gj = 0.0;
-#pragma unroll
-        for (int s = 0; s < (WP + 31) / 32; ++s)
-          if (lane + 32 * s == j) gj = rhs[s] / S[pk(j, j)];
-        gj = __shfl_sync(0xffffffffu, gj, j & 31);
-#pragma unroll
-        for (int s = 0; s < (WP + 31) / 32; ++s) {
-          const int tt = lane + 32 * s;
-          if (tt < j) rhs[s] = fma(-S[pk(j, tt)], gj, rhs[s]);
-          else if (tt == j) rhs[s] = gj;
-        }
-      }
-#pragma unroll
-      for (int s = 0; s < (WP + 31) / 32; ++s) {
-        const int tt = lane + 32 * s;
-        if (tt < wp) gval[beg + tt] = rhs[s];
-      }
-      __syncwarp();
-      // hand S[buf] back only if the producers will wait for it
-      if (i + 2 * (int64_t)gridDim.x < N) nbar_arrive(BAR_EMPTY0 + buf, WS_T);
-    }
-  }
-}
-
-template <int MT>
-afn_status launch_fsai_ws(const double* X2, int64_t N, int d, double cl, double mu, const double* W,
-                          int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* info,
-                          cudaStream_t st) {
-  constexpr int WP = MT * 16;
-  constexpr int PW = WP + 1;
-  const size_t bytes = sizeof(double) * (2 * (size_t)KC * PW + (size_t)WP * (WP + 1) + (size_t)WP * d) +
-                       sizeof(int) * WP + 16;
-  auto kern = fsai_ws_kernel<MT>;
-  AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  const int grid = (int)std::min<int64_t>(N, (int64_t)num_sms());
-  kern<<<grid, WS_T, bytes, st>>>(X2, N, d, cl, mu, W, k, rp, col, gval, info);
-  AFN_LAUNCH_CHECK("fsai_ws_kernel");
   return AFN_OK;
 }
 
@@ -746,60 +372,32 @@ afn_status fsai_chol_batch(int64_t r0, int64_t nrows, int MT, const int64_t* rp,
 }
 
 afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
-                    int64_t k, const int64_t* rp, const int32_t* col, double* gval, int* d_info,
-                    cudaStream_t st) {
+                    int64_t k, const int64_t* rp, const int32_t* col, int64_t row_lo, int64_t row_hi,
+                    double* gval, int* d_info, cudaStream_t st) {
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
-  if (N <= 0) return AFN_OK;
-  // pattern width: all rows have <= w entries; the caller guarantees w <= 128
+  if (N <= 0 || row_hi <= row_lo) return AFN_OK;
+  // pattern width: all rows have <= w entries (the widest row is the last
+  // one: rows grow then stay at w); the caller guarantees w <= 128
   int w = 0;
   {
     int64_t h[2];
     AFN_CUDA(cudaMemcpyAsync(h, rp + (N > 1 ? N - 1 : 0), sizeof(int64_t) * (N > 1 ? 2 : 1),
                              cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
-    // the widest row is the last one (rows grow then stay at w)
     w = (int)(N > 1 ? (h[1] - h[0]) : h[0]);
     if (N == 1) w = 1;
   }
   const double cl = AFN_LOG2E / (l * l);
   const int MT = (w + 15) / 16;
-  // variant: 0 = split (default), 1 = single kernel, 2 = warp-specialised
-  static const int variant = getenv("AFN_FSAI_VARIANT") ? std::max(0, atoi(getenv("AFN_FSAI_VARIANT"))) : 0;
-  if (variant == 2) {
-    switch (MT) {
-      case 1: return launch_fsai_ws<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 2: return launch_fsai_ws<2>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 3: return launch_fsai_ws<3>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 4: return launch_fsai_ws<4>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 5: return launch_fsai_ws<5>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 6: return launch_fsai_ws<6>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 7: return launch_fsai_ws<7>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 8: return launch_fsai_ws<8>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
-    }
-  }
-  if (variant == 0) {
-    switch (MT) {
-      case 1: return launch_fsai_split<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 2: return launch_fsai_split<2>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 3: return launch_fsai_split<3>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 4: return launch_fsai_split<4>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 5: return launch_fsai_split<5>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 6: return launch_fsai_split<6>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 7: return launch_fsai_split<7>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      case 8: return launch_fsai_split<8>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-      default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
-    }
-  }
   switch (MT) {
-    case 1: return launch_fsai<1>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 2: return launch_fsai<2>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 3: return launch_fsai<3>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 4: return launch_fsai<4>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 5: return launch_fsai<5>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 6: return launch_fsai<6>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 7: return launch_fsai<7>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 8: return launch_fsai<8>(X2, N, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 1: return launch_fsai_split<1>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 2: return launch_fsai_split<2>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 3: return launch_fsai_split<3>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 4: return launch_fsai_split<4>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 5: return launch_fsai_split<5>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 6: return launch_fsai_split<6>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 7: return launch_fsai_split<7>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 8: return launch_fsai_split<8>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
     default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
   }
 }

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
                                                           const int32_t* __restrict__ col,
                                                           const int64_t* __restrict__ trp,
                                                           const int32_t* __restrict__ tcol,
+                                                          int64_t row_lo, int64_t row_hi,
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
                                                           int* overflow) {
   extern __shared__ int hs[];  // HC
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     const int a = sorder[m0 + j];
     for (int64_t e = trp[a] + tid; e < trp[a + 1]; e += 256) {
       const int i = tcol[e];
+      if (i < row_lo || i >= row_hi) continue;  // rows this rank factors
       for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
         const int b = col[q];
         if (b > a) break;
@@ -408,8 +410,9 @@ void launch_assemble(unsigned grid, cudaStream_t st, int64_t r0, const double* X
 
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
-                          const int32_t* tcol, double* gval, int* d_info, cudaStream_t st) {
-  if (N <= 0) return AFN_OK;
+                          const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval, int* d_info,
+                          cudaStream_t st) {
+  if (N <= 0 || row_hi <= row_lo) return AFN_OK;
   if (d > 16) {
     set_error("fsai_sddmm: d > 16");
     return AFN_ERR_STATE;
@@ -500,7 +503,8 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double m
       AFN_CUDA(cudaFuncSetAttribute(group_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       uattr = true;
     }
-    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, col, trp, tcol, Ucount, Ulist, ovf);
+    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, col, trp, tcol, row_lo, row_hi,
+                                                         Ucount, Ulist, ovf);
     AFN_LAUNCH_CHECK("group_union_kernel");
   }
   int hov = 0;
@@ -533,12 +537,13 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double m
   // ---- 4. per-row assembly + warp Cholesky, in batches
   const int64_t WP = (int64_t)MT * 16;
   const int64_t SPK = WP * (WP + 1) / 2;
-  const int64_t batch = std::min<int64_t>(N, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
+  const int64_t NR = row_hi - row_lo;
+  const int64_t batch = std::min<int64_t>(NR, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
   double* Sg;
   if ((s = get((void**)&Sg, sizeof(double) * SPK * batch)) != AFN_OK) return s;
   const double cl = AFN_LOG2E / (l * l);
-  for (int64_t r0 = 0; r0 < N; r0 += batch) {
-    const int64_t nr = std::min(batch, N - r0);
+  for (int64_t r0 = row_lo; r0 < row_hi; r0 += batch) {
+    const int64_t nr = std::min(batch, row_hi - r0);
     const unsigned grid = (unsigned)nr;
     kt_begin(KT_FSAI_ASM, st);
     switch (MT) {

@@ -35,22 +35,22 @@ struct KmvTraits {
 template <int D, int RB>
 __global__ void __launch_bounds__(KMV_NT, 2)
 kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int64_t n,
-                   int64_t row0, int64_t nrows, int64_t chunk_cols,
-                   double* __restrict__ partial) {
+                   Seg2 rows, int64_t chunk_cols, double* __restrict__ partial) {
   constexpr int CS = KmvTraits<D>::CS;
   constexpr int KMV_TC = KmvTraits<D>::TC;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   __shared__ __align__(16) double s_col[KMV_TC * CS];
   load_exp2_tab(s_tab);
 
-  const int64_t rbase = row0 + (int64_t)blockIdx.x * (KMV_NT * RB) + threadIdx.x;
-  const int64_t rend = row0 + nrows;
+  // local row t -> physical row rows.phys(t) (two blocks when row-sharded)
+  const int64_t nrows = rows.size();
+  const int64_t rbase = (int64_t)blockIdx.x * (KMV_NT * RB) + threadIdx.x;
   double xi[RB][D];
   double acc[RB];
 #pragma unroll
   for (int t = 0; t < RB; ++t) {
-    int64_t r = rbase + (int64_t)t * KMV_NT;
-    r = r < rend ? r : row0;  // clamp (masked at the write)
+    const int64_t lr = rbase + (int64_t)t * KMV_NT;
+    const int64_t r = rows.phys(lr < nrows ? lr : 0);  // clamp (masked at the write)
 #pragma unroll
     for (int c = 0; c < D; ++c) xi[t][c] = Xs[r * D + c];
     acc[t] = 0.0;
@@ -96,19 +96,21 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
   }
 #pragma unroll
   for (int t = 0; t < RB; ++t) {
-    const int64_t r = rbase + (int64_t)t * KMV_NT;
-    if (r < rend) partial[(int64_t)blockIdx.y * nrows + (r - row0)] = acc[t];
+    const int64_t lr = rbase + (int64_t)t * KMV_NT;
+    if (lr < nrows) partial[(int64_t)blockIdx.y * nrows + lr] = acc[t];
   }
 }
 
-__global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, int64_t nrows,
-                                  const double* __restrict__ v, int64_t row0, double mu,
+__global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, Seg2 rows,
+                                  const double* __restrict__ v, double mu, bool y_phys,
                                   double* __restrict__ y) {
+  const int64_t nrows = rows.size();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
   double s = 0.0;
   for (int c = 0; c < nchunks; ++c) s += partial[(int64_t)c * nrows + i];
-  y[i] = fma(mu, v[row0 + i], s);
+  const int64_t r = rows.phys(i);
+  y[y_phys ? r : i] = fma(mu, v[r], s);
 }
 
 __global__ void prescale_kernel(const double* __restrict__ X, int64_t n, int d, double f,
@@ -118,20 +120,20 @@ __global__ void prescale_kernel(const double* __restrict__ X, int64_t n, int d, 
 }
 
 template <int D>
-void launch_partial(int64_t row_tiles_unused, const KmvPlan& p, cudaStream_t st, const double* Xs,
-                    const double* v, int64_t n, int64_t row0, int64_t nrows, double* partial) {
-  (void)row_tiles_unused;
+void launch_partial(const KmvPlan& p, cudaStream_t st, const double* Xs, const double* v, int64_t n,
+                    Seg2 rows, double* partial) {
   constexpr int RB = KmvTraits<D>::RB;
   const int64_t rows_per_cta = (int64_t)KMV_NT * RB;
-  dim3 grid((unsigned)((nrows + rows_per_cta - 1) / rows_per_cta), (unsigned)p.chunks);
-  kmv_partial_kernel<D, RB><<<grid, KMV_NT, 0, st>>>(Xs, v, n, row0, nrows, p.chunk_cols, partial);
+  dim3 grid((unsigned)((rows.size() + rows_per_cta - 1) / rows_per_cta), (unsigned)p.chunks);
+  kmv_partial_kernel<D, RB><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial);
 }
 
 int rows_per_thread(int d) { return d <= 4 ? 4 : (d <= 8 ? 2 : 1); }
 
 }  // namespace
 
-KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
+namespace {
+KmvPlan plan_for(int64_t n, int64_t nrows, int d, int num_sms) {
   KmvPlan p;
   const int64_t rows_per_cta = (int64_t)KMV_NT * rows_per_thread(d);
   p.row_tiles = (nrows + rows_per_cta - 1) / rows_per_cta;
@@ -155,6 +157,21 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
   p.chunks = (n + p.chunk_cols - 1) / p.chunk_cols;
   return p;
 }
+}  // namespace
+
+// The column chunking fixes each row's summation order.  A row shard keeps
+// the chunking of the full n-row plan (so sharded rows are bit-identical to
+// the single-GPU matvec) unless that would leave it under two waves of CTAs,
+// in which case the shard gets its own plan.
+KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
+  const KmvPlan full = plan_for(n, n, d, num_sms);
+  if (nrows == n) return full;
+  KmvPlan p = full;
+  const int64_t rows_per_cta = (int64_t)KMV_NT * rows_per_thread(d);
+  p.row_tiles = (nrows + rows_per_cta - 1) / rows_per_cta;
+  if (p.row_tiles * p.chunks >= 2 * 2 * (int64_t)num_sms) return p;
+  return plan_for(n, nrows, d, num_sms);
+}
 
 afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs, cudaStream_t st) {
   const double f = AFN_SQRT_LOG2E / l;
@@ -165,32 +182,33 @@ afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs,
   return AFN_OK;
 }
 
-afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, int64_t row0,
-                      int64_t nrows, double* y, double* partial, const KmvPlan& p, cudaStream_t st) {
+afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, Seg2 rows,
+                      double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st) {
+  const int64_t nrows = rows.size();
   if (nrows <= 0) return AFN_OK;
   switch (d) {
-    case 1: launch_partial<1>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 2: launch_partial<2>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 3: launch_partial<3>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 4: launch_partial<4>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 5: launch_partial<5>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 6: launch_partial<6>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 7: launch_partial<7>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 8: launch_partial<8>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 9: launch_partial<9>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 10: launch_partial<10>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 11: launch_partial<11>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 12: launch_partial<12>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 13: launch_partial<13>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 14: launch_partial<14>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 15: launch_partial<15>(0, p, st, Xs, v, n, row0, nrows, partial); break;
-    case 16: launch_partial<16>(0, p, st, Xs, v, n, row0, nrows, partial); break;
+    case 1: launch_partial<1>(p, st, Xs, v, n, rows, partial); break;
+    case 2: launch_partial<2>(p, st, Xs, v, n, rows, partial); break;
+    case 3: launch_partial<3>(p, st, Xs, v, n, rows, partial); break;
+    case 4: launch_partial<4>(p, st, Xs, v, n, rows, partial); break;
+    case 5: launch_partial<5>(p, st, Xs, v, n, rows, partial); break;
+    case 6: launch_partial<6>(p, st, Xs, v, n, rows, partial); break;
+    case 7: launch_partial<7>(p, st, Xs, v, n, rows, partial); break;
+    case 8: launch_partial<8>(p, st, Xs, v, n, rows, partial); break;
+    case 9: launch_partial<9>(p, st, Xs, v, n, rows, partial); break;
+    case 10: launch_partial<10>(p, st, Xs, v, n, rows, partial); break;
+    case 11: launch_partial<11>(p, st, Xs, v, n, rows, partial); break;
+    case 12: launch_partial<12>(p, st, Xs, v, n, rows, partial); break;
+    case 13: launch_partial<13>(p, st, Xs, v, n, rows, partial); break;
+    case 14: launch_partial<14>(p, st, Xs, v, n, rows, partial); break;
+    case 15: launch_partial<15>(p, st, Xs, v, n, rows, partial); break;
+    case 16: launch_partial<16>(p, st, Xs, v, n, rows, partial); break;
     default: set_error("kernel_matvec: d=%d unsupported (1..16)", d); return AFN_ERR_ARG;
   }
   AFN_LAUNCH_CHECK("kmv_partial_kernel");
   const int nt = 256;
-  kmv_reduce_kernel<<<(unsigned)((nrows + nt - 1) / nt), nt, 0, st>>>(partial, (int)p.chunks, nrows,
-                                                                     v, row0, mu, y);
+  kmv_reduce_kernel<<<(unsigned)((nrows + nt - 1) / nt), nt, 0, st>>>(partial, (int)p.chunks, rows, v,
+                                                                     mu, y_phys, y);
   AFN_LAUNCH_CHECK("kmv_reduce_kernel");
   return AFN_OK;
 }

@@ -66,7 +66,8 @@ __device__ void warp_bitonic_int(int* v) {
 
 template <int DP>
 __global__ void __launch_bounds__(KNN_NW * 32)
-knn_kernel(const double* __restrict__ P, int64_t N, int d, int w, int32_t* __restrict__ col) {
+knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, int w,
+           int32_t* __restrict__ col) {
   constexpr int TILE = DP <= 4 ? 512 : (DP <= 8 ? 256 : 128);
   __shared__ double s_pts[TILE * DP];
   __shared__ double s_key[KNN_NW][KNN_CAP];
@@ -75,9 +76,9 @@ knn_kernel(const double* __restrict__ P, int64_t N, int d, int w, int32_t* __res
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // heaviest rows first (row i scans i candidates)
   const int64_t blk = (int64_t)gridDim.x - 1 - blockIdx.x;
-  const int64_t i0 = blk * KNN_NW;
+  const int64_t i0 = row_lo + blk * KNN_NW;
   const int64_t i = i0 + wid;
-  const bool active = i < N;
+  const bool active = i < row_hi;
   const int W1 = active ? (int)min((int64_t)w - 1, i) : 0;
 
   double q[DP];
@@ -99,7 +100,7 @@ knn_kernel(const double* __restrict__ P, int64_t N, int d, int w, int32_t* __res
     __syncwarp();
   };
 
-  const int64_t jmax = min(N, i0 + KNN_NW) - 1;  // largest candidate needed in this CTA
+  const int64_t jmax = min(row_hi, i0 + KNN_NW) - 1;  // largest candidate needed in this CTA
   for (int64_t tb = 0; tb < jmax; tb += TILE) {
     const int tn = (int)min((int64_t)TILE, jmax - tb);
     __syncthreads();
@@ -158,9 +159,9 @@ __global__ void knn_rowptr_kernel(int64_t N, int w, int64_t* __restrict__ rp) {
 }
 
 template <int DP>
-void launch_knn(const double* P, int64_t N, int d, int w, int32_t* col, cudaStream_t st) {
-  const int64_t blocks = (N + KNN_NW - 1) / KNN_NW;
-  knn_kernel<DP><<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(P, N, d, w, col);
+void launch_knn(const double* P, int64_t lo, int64_t hi, int d, int w, int32_t* col, cudaStream_t st) {
+  const int64_t blocks = (hi - lo + KNN_NW - 1) / KNN_NW;
+  knn_kernel<DP><<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(P, lo, hi, d, w, col);
 }
 
 }  // namespace
@@ -171,7 +172,8 @@ int64_t knn_nnz(int64_t N, int w) {
 }
 
 afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, int32_t* col,
-                   cudaStream_t st) {
+                   cudaStream_t st, int64_t row_lo, int64_t row_hi) {
+  if (row_hi < 0) row_hi = N;
   if (w < 1 || w > 128) {
     set_error("knn: w=%d unsupported (1..128)", w);
     return AFN_ERR_ARG;
@@ -179,12 +181,14 @@ afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, i
   if (N <= 0) return AFN_OK;
   knn_rowptr_kernel<<<(unsigned)((N + 1 + 255) / 256), 256, 0, st>>>(N, w, row_ptr);
   AFN_LAUNCH_CHECK("knn_rowptr_kernel");
-  if (d <= 1) launch_knn<1>(P, N, d, w, col, st);
-  else if (d <= 2) launch_knn<2>(P, N, d, w, col, st);
-  else if (d <= 3) launch_knn<3>(P, N, d, w, col, st);
-  else if (d <= 4) launch_knn<4>(P, N, d, w, col, st);
-  else if (d <= 8) launch_knn<8>(P, N, d, w, col, st);
-  else if (d <= 16) launch_knn<16>(P, N, d, w, col, st);
+  if (row_hi <= row_lo) return AFN_OK;
+  const int64_t lo = row_lo, hi = row_hi;
+  if (d <= 1) launch_knn<1>(P, lo, hi, d, w, col, st);
+  else if (d <= 2) launch_knn<2>(P, lo, hi, d, w, col, st);
+  else if (d <= 3) launch_knn<3>(P, lo, hi, d, w, col, st);
+  else if (d <= 4) launch_knn<4>(P, lo, hi, d, w, col, st);
+  else if (d <= 8) launch_knn<8>(P, lo, hi, d, w, col, st);
+  else if (d <= 16) launch_knn<16>(P, lo, hi, d, w, col, st);
   else {
     set_error("knn: d=%d unsupported (1..16)", d);
     return AFN_ERR_ARG;

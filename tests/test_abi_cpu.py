@@ -49,11 +49,11 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_struct_layout(lib):
     import ctypes as C
-    assert lib.abi_version() == 1
+    assert lib.abi_version() == 2
     # afn_params: 2 doubles, int64, 4 int32, int64, uint64 = 56 bytes
     assert C.sizeof(lib.Params) == 56
-    assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9
-    assert C.sizeof(lib.Report) == 4 * 4 + 8 * 5 + 8
+    assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4
+    assert C.sizeof(lib.Report) == 4 * 4 + 8 * 6 + 8
 
 
 def test_host_pointers_are_rejected_without_compute(lib):

@@ -1,0 +1,77 @@
+"""Row-sharded multi-rank path on ONE GPU through the emulated communicator
+(include/afn.h afn_comm_init_emulated): R logical ranks, each with its own
+buffers, exchanging their rows by device copies -- the same build / apply /
+PCG code that runs with NCCL across GPUs.  No kernel waits
+on another rank.  Checks against the single-GPU handle (itself checked
+against the oracle in test_gpu_parity.py) and against the oracle:
+
+  * replicated pieces (permutation, L, pattern, G) bit-identical on every rank;
+  * each rank's W rows bit-identical to the same rows of the single-GPU W;
+  * apply and PCG: same iteration count, solution and apply within rounding
+    of the single-GPU path, true residual <= tol; oracle iteration count +-2."""
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import gen_problem, gen_small
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2304_05460_b200 as afn  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+CASES = [(2, 1000, 1.0, 1e-4, 100, 50, False), (3, 1000, 1.0, 1e-4, 100, 50, False),
+         (8, 2000, 2.0, 1e-4, 150, 60, False), (4, 777, 0.5, 1e-3, 777, 20, False),
+         (2, 16384, 1.0, 1e-4, 2000, 100, True), (8, 16384, 2.0, 1e-4, 2000, 100, True)]
+
+
+@pytest.mark.parametrize("R,n,l,mu,k,w,adaptive", CASES)
+def test_emulated_ranks_match_single_gpu(R, n, l, mu, k, w, adaptive):
+    if n == 16384:
+        X, b = gen_problem("C2")
+    else:
+        X, b = gen_small(n, 3, seed=21)
+    Xd, bd = T(X), T(b)
+    prm = afn.make_params(l, mu, k, w, k_adaptive=adaptive)
+    h1 = afn.afn_build(Xd, prm)
+    comm = afn.Comm.emulated(R)
+    hR = afn.afn_build(Xd, prm, comm=comm)
+    i1, iR = h1.info(), hR.info()
+    assert iR["nranks"] == R and iR["k"] == i1["k"] and iR["nnz"] == i1["nnz"]
+    kk = i1["k"]
+    W1 = h1.copy_out(afn.OUT_W)
+    for q in range(R):
+        for what in (afn.OUT_PERM, afn.OUT_FILL, afn.OUT_L, afn.OUT_ROWPTR, afn.OUT_COL, afn.OUT_GVAL):
+            assert np.array_equal(hR.copy_out(what, q), h1.copy_out(what)), (q, what)
+        a0, na, b0, nb = afn.shard_rows(n, kk, R, q)
+        assert np.array_equal(hR.copy_out(afn.OUT_W, q), W1[b0 - kk:b0 - kk + nb])
+    # apply
+    r = T(np.random.default_rng(3).standard_normal(n))
+    z1 = h1.apply(r).cpu().numpy()
+    zR = hR.apply(r).cpu().numpy()
+    assert rel(zR, z1) <= 1e-12
+    # PCG
+    a1, rep1 = h1.pcg_solve(bd, tol=1e-4)
+    aR, repR = hR.pcg_solve(bd, tol=1e-4)
+    assert repR["converged"] and repR["iterations"] == rep1["iterations"]
+    assert repR["relres_true"] <= 1e-4
+    assert rel(aR.cpu().numpy(), a1.cpu().numpy()) <= 1e-9
+    if n <= 2000:
+        ao, ro, _ = O.afn_pcg_solve(X, b, l, mu, kk, w)
+        assert abs(repR["iterations"] - ro["iterations"]) <= 2
+    hR.close()
+    comm.close()

@@ -122,7 +122,9 @@ def test_full_size_component_parity(name, l):
     assert rel(y[mrows], O.kmv_rows(X, l, cfg.mu, v, mrows)) <= 1e-12
 
     # ---- PCG
-    a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit)
+    a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit, history=True)
+    hist = rep.pop("history")
+    print(name, l, inf, rep, hist[:: max(1, len(hist) // 20)])
     assert rep["converged"] and not rep["breakdown"]
     assert rep["relres_true"] <= cfg.tol
     an = a.cpu().numpy()
