@@ -9,15 +9,18 @@
 //   1. spatial order: non-landmark points sorted by grid cell (tiled cell
 //      order), consecutive GA = 16 points form a group g;
 //   2. U_g = union over a in g of B_a = { b <= a : a, b in J_i for some row i }
-//      (rows containing a come from the transposed pattern), sorted;
+//      (rows containing a come from the transposed pattern), numbered in the
+//      slot order of a hash set whose global copy maps b -> position in U_g;
 //   3. D_g = W_g W_{U_g}^T (GA x |U_g|, k-long FP64 dots; register-tiled,
 //      cp.async-staged through shared memory) -- ~4x fewer flops than the
 //      per-row Gram on the C2 pattern;
-//   4. per row: S_JJ assembled by look-up (binary search of b in U_{g(a)}),
-//      then the warp-per-row Cholesky of fsai.cu.
+//   4. per row (one CTA): S_JJ assembled by hash look-up of b in U_{g(a)},
+//      blocked Cholesky in shared memory, g = L^{-T} e_last.
 // Values are independent of the grouping (each dot has a fixed summation
 // order), so the result is deterministic even though the cell sort uses atomics.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -25,10 +28,6 @@
 #include "afn_internal.h"
 
 namespace afn {
-
-// shared with fsai.cu (defined there)
-afn_status fsai_chol_batch(int64_t r0, int64_t nrows, int MT, const int64_t* rp, double* Sg,
-                           double* gval, int* info, cudaStream_t st);
 
 namespace {
 
@@ -151,6 +150,11 @@ __global__ void cell_scatter_kernel(const int* __restrict__ key, int64_t N, cons
   sorder[off[k] + p] = (int)i;
 }
 
+__global__ void pass_count_kernel(const int* __restrict__ Ucount, int64_t G, int* __restrict__ pc) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < G) pc[g] = (Ucount[g] + UT - 1) / UT;
+}
+
 __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int* __restrict__ grp,
                                   int* __restrict__ loc) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -161,6 +165,12 @@ __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int
 }
 
 // ---------------------------------------------------------------- group unions
+// One CTA per group g: insert every needed b (b <= a, a in g, a and b in the
+// pattern of a row this rank factors) into a shared-memory hash set (linear
+// probing), then number the keys in slot order: U_g[u] (the GEMM's column
+// list) and the global copy of the table H_g[slot] = (b, u) that the factor
+// kernel uses to find W_a . W_b in D_g (one or two probes).  A warp walks
+// one pattern row at a time, lanes over its entries.
 __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict__ sorder, int64_t N,
                                                           const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ col,
@@ -168,10 +178,11 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
                                                           const int32_t* __restrict__ tcol,
                                                           int64_t row_lo, int64_t row_hi,
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
-                                                          int* overflow) {
-  extern __shared__ int hs[];  // HC
+                                                          int2* __restrict__ Htab, int* overflow) {
+  extern __shared__ int hs[];  // HC keys
   __shared__ int s_n;
-  const int tid = threadIdx.x;
+  __shared__ int s_scan[256];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t g = blockIdx.x;
   for (int t = tid; t < HC; t += 256) hs[t] = -1;
   if (tid == 0) s_n = 0;
@@ -180,12 +191,12 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
   const int cnt = (int)min((int64_t)GA, N - m0);
   for (int j = 0; j < cnt; ++j) {
     const int a = sorder[m0 + j];
-    for (int64_t e = trp[a] + tid; e < trp[a + 1]; e += 256) {
+    for (int64_t e = trp[a] + wid; e < trp[a + 1]; e += 8) {
       const int i = tcol[e];
       if (i < row_lo || i >= row_hi) continue;  // rows this rank factors
-      for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+      for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
         const int b = col[q];
-        if (b > a) break;
+        if (b > a) break;  // columns ascending
         unsigned h = ((unsigned)b * 2654435761u) & (HC - 1);
         while (true) {
           const int old = atomicCAS(&hs[h], -1, b);
@@ -196,8 +207,8 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
           if (old == b) break;
           h = (h + 1) & (HC - 1);
         }
-        if (s_n > (HC * 3) / 4) break;  // overflow guard (checked below)
       }
+      if (s_n > (HC * 3) / 4) break;  // overflow guard (checked below)
     }
   }
   __syncthreads();
@@ -206,37 +217,31 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     if (tid == 0) atomicExch(overflow, 1);
     return;
   }
-  // compact the occupied slots to the front (order irrelevant), then sort
-  // the first next_pow2(nu) entries ascending
-  __shared__ int s_c;
-  if (tid == 0) s_c = 0;
+  // number the occupied slots in slot order (block scan over 32-slot strips)
+  constexpr int PER = HC / 256;
+  int c = 0;
+  for (int t = 0; t < PER; ++t) c += hs[tid * PER + t] >= 0;
+  s_scan[tid] = c;
   __syncthreads();
-  int* tmpk = hs + HC;  // second buffer (HC ints)
-  for (int t = tid; t < HC; t += 256) {
-    const int v = hs[t];
-    if (v >= 0) tmpk[atomicAdd(&s_c, 1)] = v;
+  for (int o = 1; o < 256; o <<= 1) {
+    const int v = tid >= o ? s_scan[tid - o] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
   }
-  __syncthreads();
-  int P2 = 1;
-  while (P2 < nu) P2 <<= 1;
-  for (int t = tid; t < P2; t += 256) hs[t] = t < nu ? tmpk[t] : 0x7fffffff;
-  __syncthreads();
-  for (int kk = 2; kk <= P2; kk <<= 1)
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int t = tid; t < P2; t += 256) {
-        const int p = t ^ j;
-        if (p > t) {
-          const bool up = (t & kk) == 0;
-          const int x = hs[t], y = hs[p];
-          if ((x > y) == up) {
-            hs[t] = y;
-            hs[p] = x;
-          }
-        }
-      }
-      __syncthreads();
+  int u = s_scan[tid] - c;
+  int2* H = Htab + g * HC;
+  for (int t = 0; t < PER; ++t) {
+    const int slot = tid * PER + t;
+    const int b = hs[slot];
+    if (b >= 0) {
+      Ulist[g * UCAP + u] = b;
+      H[slot] = make_int2(b, u);
+      ++u;
+    } else {
+      H[slot] = make_int2(-1, -1);
     }
-  for (int t = tid; t < nu; t += 256) Ulist[g * UCAP + t] = hs[t];
+  }
   if (tid == 0) Ucount[g] = nu;
 }
 
@@ -254,6 +259,7 @@ __global__ void __launch_bounds__(256, 2) group_gemm_kernel(const int* __restric
                                                             const int* __restrict__ Ucount,
                                                             const int* __restrict__ Ulist,
                                                             const int64_t* __restrict__ Doff,
+                                                            const int64_t* __restrict__ Poff, int64_t G,
                                                             double* __restrict__ D) {
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                    // [NST][KC2/2][GA][2]
@@ -261,7 +267,15 @@ __global__ void __launch_bounds__(256, 2) group_gemm_kernel(const int* __restric
   __shared__ int s_a[GA];
   __shared__ int s_u[UT];
   const int tid = threadIdx.x;
-  const int64_t g = blockIdx.x;
+  // work item = (group g, pass of UT columns of U_g): Poff = scan of passes
+  const int64_t item = blockIdx.x;
+  int64_t glo = 0, ghi = G;  // largest g with Poff[g] <= item
+  while (ghi - glo > 1) {
+    const int64_t mid = (glo + ghi) >> 1;
+    if (Poff[mid] <= item) glo = mid; else ghi = mid;
+  }
+  const int64_t g = glo;
+  const int pass = (int)(item - Poff[g]);
   const int64_t m0 = g * GA;
   const int cnt = (int)min((int64_t)GA, N - m0);
   const int nu = Ucount[g];
@@ -269,7 +283,8 @@ __global__ void __launch_bounds__(256, 2) group_gemm_kernel(const int* __restric
   if (tid < GA) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
   const int64_t nch = (k + KC2 - 1) / KC2;
   const bool even = (k & 1) == 0;  // 16-byte aligned rows -> 16-byte copies
-  for (int u0 = 0; u0 < nu; u0 += UT) {
+  {
+    const int u0 = pass * UT;
     const int un = min(UT, nu - u0);
     __syncthreads();
     for (int t = tid; t < UT; t += 256) s_u[t] = t < un ? Ulist[g * UCAP + u0 + t] : -1;
@@ -344,66 +359,279 @@ __global__ void __launch_bounds__(256, 2) group_gemm_kernel(const int* __restric
   }
 }
 
-// ---------------------------------------------------------------- assembly
+// ---------------------------------------------------------------- factor
+// One CTA (FT2 threads) per FSAI row i with pattern J (|J| = wp <= 16 MT,
+// ascending, i last).  CTAs take the rows in the spatial (cell) order of the
+// union step, so CTAs running together touch the same groups' D blocks (L2).
+//   1. S_JJ = K(X_J, X_J) + mu I - D (Gram entries found through the groups'
+//      hash tables), lower triangle into shared memory, rows padded to even
+//      length (16-byte aligned panel reads), padded to WP rows with identity;
+//   2. right-looking blocked Cholesky diag(S_JJ, I) = L L^T with 16-column
+//      panels: every warp factors the 16x16 diagonal block redundantly with
+//      shuffles (warp-uniform code: no divergence fallback, no spills; warp 0
+//      stores it), one row per thread for the panel solve, 4x4 register tiles
+//      (LDS.128 operand pairs) for the trailing update;
+//   3. g = L^{-T} e_last by column-oriented back substitution over the
+//      contiguous rows of L (every warp, warp 0 stores) -- the
+//      Kolotilina-Yeremin row with diag(G S G^T) = 1 (reading R16).
+constexpr int FT2 = 128;
+
+// Unblocked Cholesky of a 16x16 block held one row per lane (row lr =
+// lane & 15 in dr[0..lr]; lanes 16..31 mirror 0..15).  myinv = 1 / L_{lr,lr}.
+// Returns true on a non-positive pivot (replaced by 1 so the warp stays in step).
+__device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, int lr) {
+  bool bad = false;
+#pragma unroll 16
+  for (int c = 0; c < 16; ++c) {
+    double piv = __shfl_sync(0xffffffffu, dr[c], c);
+    if (!(piv > 0.0)) { bad = true; piv = 1.0; }
+    const double inv = rsqrt(piv);
+    if (lr == c) myinv = inv;
+    dr[c] = (lr == c) ? piv * inv : (lr > c ? dr[c] * inv : dr[c]);
+#pragma unroll 16
+    for (int c2 = 1; c2 < 16; ++c2) {  // fixed trip count (c2 > c active) keeps dr[] in registers
+      if (c2 > c) {
+        const double v = __shfl_sync(0xffffffffu, dr[c], c2);
+        dr[c2] = (lr >= c2) ? fma(-dr[c], v, dr[c2]) : dr[c2];
+      }
+    }
+  }
+  return bad;
+}
+
 template <int MT>
-__global__ void __launch_bounds__(256) fsai_assemble_kernel(int64_t r0, const double* __restrict__ X2, int d,
-                                                            double cl, double mu, const int64_t* __restrict__ rp,
-                                                            const int32_t* __restrict__ col,
-                                                            const int* __restrict__ grp, const int* __restrict__ loc,
-                                                            const int* __restrict__ Ucount,
-                                                            const int* __restrict__ Ulist,
-                                                            const int64_t* __restrict__ Doff,
-                                                            const double* __restrict__ D, double* __restrict__ Sg) {
+__global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
+                                                         int64_t row_hi, const double* __restrict__ X2, int d,
+                                                         double cl, double mu, const int64_t* __restrict__ rp,
+                                                         const int32_t* __restrict__ col,
+                                                         const int* __restrict__ grp, const int* __restrict__ loc,
+                                                         const int* __restrict__ Ucount,
+                                                         const int2* __restrict__ Htab,
+                                                         const int64_t* __restrict__ Doff,
+                                                         const double* __restrict__ D, double* __restrict__ gval,
+                                                         int* info) {
   constexpr int WP = MT * 16;
-  constexpr int SPK = WP * (WP + 1) / 2;
+  constexpr int LSZ = WP * (WP + 1) / 2 + WP;  // packed lower, rows padded to even length
+  extern __shared__ __align__(16) double fsm[];
+  double* Lm = fsm;            // [LSZ]
+  double* sX = fsm + LSZ;      // [WP * d]
   __shared__ double s_tab[AFN_EXP2_TAB_N];
+  __shared__ double s_inv[WP];
   __shared__ int sJ[WP];
-  __shared__ double sX[WP * 16];
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const int64_t i = r0 + blockIdx.x;
+  __shared__ int s_off[WP + 1];
+  __shared__ int s_g[WP];
+  __shared__ int64_t s_db[WP];
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, lr = lane & 15;
+  const int64_t i = rorder[blockIdx.x];
+  if (i < row_lo || i >= row_hi) return;  // another rank's row
   const int64_t beg = rp[i];
   const int wp = (int)(rp[i + 1] - beg);
   load_exp2_tab(s_tab);
-  for (int a = tid; a < wp; a += 256) sJ[a] = col[beg + a];
+  if (tid == 0) {
+    s_bad = 0;
+    int o = 0;
+    for (int a = 0; a < WP; ++a) {
+      s_off[a] = o;
+      o += (a + 2) & ~1;  // row a holds a+1 entries, padded to even
+    }
+    s_off[WP] = o;
+  }
+  for (int a = tid; a < wp; a += FT2) sJ[a] = col[beg + a];
   __syncthreads();
-  for (int e = tid; e < wp * d; e += 256) {
+  for (int e = tid; e < wp * d; e += FT2) {
     const int a = e / d, c = e - a * d;
     sX[e] = X2[(int64_t)sJ[a] * d + c];
   }
-  __syncthreads();
-  double* S = Sg + (int64_t)blockIdx.x * SPK;
-  for (int p = ty; p < wp; p += 16) {
+  // ---- 1. assemble S_JJ (lower).  Per row p (point a = J_p): the group
+  // g(a) and the offset of a's row in D_g; then 8 entries per thread at a
+  // time (8 independent hash probes, then 8 independent D loads).
+  for (int p = tid; p < wp; p += FT2) {
     const int a = sJ[p];
     const int g = grp[a];
-    const int nu = Ucount[g];
-    const int* U = Ulist + (int64_t)g * UCAP;
-    const double* Drow = D + Doff[g] + (int64_t)loc[a] * nu;
-    for (int q = tx; q <= p; q += 16) {
-      const int b = sJ[q];  // b <= a (columns ascending)
-      int lo = 0, hi = nu - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (U[mid] < b) lo = mid + 1; else hi = mid;
+    s_g[p] = g;
+    s_db[p] = Doff[g] + (int64_t)loc[a] * Ucount[g];
+  }
+  __syncthreads();
+  {
+    constexpr int B = 8;
+    const int ne = wp * (wp + 1) / 2;
+    for (int e0 = tid * B; e0 < ne; e0 += FT2 * B) {
+      int pp[B], qq[B];
+      unsigned hh[B];
+      int2 hv[B];
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const int e = min(e0 + t, ne - 1);
+        int p = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+        while (p * (p + 1) / 2 > e) --p;
+        while ((p + 1) * (p + 2) / 2 <= e) ++p;
+        pp[t] = p;
+        qq[t] = e - p * (p + 1) / 2;
+        hh[t] = ((unsigned)sJ[qq[t]] * 2654435761u) & (HC - 1);
+        hv[t] = __ldg(&Htab[(int64_t)s_g[p] * HC + hh[t]]);
       }
-      const double gram = Drow[lo];
-      double kv;
-      if (p == q) {
-        kv = 1.0 + mu;
-      } else {
-        const double sd = d2_exact_rt(&sX[p * d], &sX[q * d], d);
-        kv = gauss_from_d2(sd, cl, s_tab);
+      double gram[B];
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        const int b = sJ[qq[t]];
+        const int2* H = Htab + (int64_t)s_g[pp[t]] * HC;
+        while (hv[t].x != b) {  // b is in U_g by construction
+          hh[t] = (hh[t] + 1) & (HC - 1);
+          hv[t] = __ldg(&H[hh[t]]);
+        }
+        gram[t] = D[s_db[pp[t]] + hv[t].y];
       }
-      S[cml(p, q, wp)] = kv - gram;
+#pragma unroll
+      for (int t = 0; t < B; ++t) {
+        if (e0 + t >= ne) break;
+        const int p = pp[t], q = qq[t];
+        double kv;
+        if (p == q) {
+          kv = 1.0 + mu;
+        } else {
+          const double sd = d2_exact_rt(&sX[p * d], &sX[q * d], d);
+          kv = gauss_from_d2(sd, cl, s_tab);
+        }
+        Lm[s_off[p] + q] = kv - gram[t];
+      }
+    }
+  }
+  for (int p = wp + tid; p < WP; p += FT2)
+    for (int q = 0; q <= p; ++q) Lm[s_off[p] + q] = (p == q) ? 1.0 : 0.0;
+  __syncthreads();
+  // ---- 2. blocked right-looking Cholesky of diag(S_JJ, I) (WP x WP)
+#pragma unroll 1
+  for (int kb = 0; kb < WP; kb += 16) {
+    {  // diagonal block, every warp (warp 0 stores)
+      double dr[16], myinv = 1.0;
+      const double* row = Lm + s_off[kb + lr] + kb;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) dr[c] = (c <= lr) ? row[c] : 0.0;
+      const bool bad = factor_diag16(dr, myinv, lr);
+      __syncthreads();  // every warp has read the block before warp 0 overwrites it
+      if (tid < 16) {
+        double* wrow = Lm + s_off[kb + tid] + kb;
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c <= tid) wrow[c] = dr[c];
+        s_inv[kb + tid] = myinv;
+        if (bad) s_bad = 1;
+      }
+    }
+    __syncthreads();
+    const int r0 = kb + 16;
+    const int m = WP - r0;
+    if (m <= 0) break;
+    // panel: rows a >= r0, columns kb..kb+15: x L_diag^T = A
+    for (int a = r0 + tid; a < WP; a += FT2) {
+      double x[16];
+      double* row = Lm + s_off[a] + kb;
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(row + c);
+        x[c] = v.x;
+        x[c + 1] = v.y;
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        double sacc = x[c];
+        const double* lrow = Lm + s_off[kb + c] + kb;
+#pragma unroll
+        for (int c2 = 0; c2 < c; ++c2) sacc = fma(-x[c2], lrow[c2], sacc);
+        x[c] = sacc * s_inv[kb + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(x[c], x[c + 1]);
+    }
+    __syncthreads();
+    // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], a >= b >= r0, 4x4 tiles
+    const int mt = m >> 2;
+    const int ntile = mt * (mt + 1) / 2;
+    for (int t = tid; t < ntile; t += FT2) {
+      int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      while (I * (I + 1) / 2 > t) --I;
+      while ((I + 1) * (I + 2) / 2 <= t) ++I;
+      const int J = t - I * (I + 1) / 2;
+      const int a0 = r0 + 4 * I, b0 = r0 + 4 * J;
+      const double* pa[4];
+      const double* pb[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        pa[r] = Lm + s_off[a0 + r] + kb;
+        pb[r] = Lm + s_off[b0 + r] + kb;
+      }
+      double acc[4][4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 2) {
+        double2 va[4], vb[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          va[r] = *reinterpret_cast<const double2*>(pa[r] + kk);
+          vb[r] = *reinterpret_cast<const double2*>(pb[r] + kk);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc[r][c] = fma(va[r].x, vb[c].x, acc[r][c]);
+            acc[r][c] = fma(va[r].y, vb[c].y, acc[r][c]);
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (b0 + c <= a0 + r) Lm[s_off[a0 + r] + b0 + c] -= acc[r][c];
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) atomicCAS(info, 0, (int)(i + 1));
+    return;
+  }
+  // ---- 3. g = L^{-T} e_last: rhs_j -= L[t][j] g_t over the rows t, every
+  // warp redundantly (shuffles in warp-uniform code), warp 0 stores
+  double rhs[WP / 32 + 1];
+#pragma unroll
+  for (int r = 0; r <= WP / 32; ++r) rhs[r] = (lane + 32 * r == wp - 1) ? 1.0 : 0.0;
+  for (int t = wp - 1; t >= 0; --t) {
+    const int rt = t >> 5;
+    double v = 0.0;
+#pragma unroll
+    for (int r = 0; r <= WP / 32; ++r)
+      if (r == rt) v = rhs[r];
+    const double gt = __shfl_sync(0xffffffffu, v, t & 31) * s_inv[t];
+    if (tid == 0) gval[beg + t] = gt;
+    const double* lrw = Lm + s_off[t];
+#pragma unroll
+    for (int r = 0; r <= WP / 32; ++r) {
+      const int j = lane + 32 * r;
+      if (j < t) rhs[r] = fma(-lrw[j], gt, rhs[r]);
     }
   }
 }
 
 template <int MT>
-void launch_assemble(unsigned grid, cudaStream_t st, int64_t r0, const double* X2, int d, double cl,
-                     double mu, const int64_t* rp, const int32_t* col, const int* grp, const int* loc,
-                     const int* Ucount, const int* Ulist, const int64_t* Doff, const double* D, double* Sg) {
-  fsai_assemble_kernel<MT><<<grid, 256, 0, st>>>(r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist,
-                                                 Doff, D, Sg);
+afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t row_hi, cudaStream_t st,
+                         const double* X2, int d, double cl, double mu, const int64_t* rp, const int32_t* col,
+                         const int* grp, const int* loc, const int* Ucount, const int2* Htab,
+                         const int64_t* Doff, const double* D, double* gval, int* info) {
+  constexpr int WP = MT * 16;
+  const size_t bytes = sizeof(double) * ((size_t)WP * (WP + 1) / 2 + WP + (size_t)WP * d);
+  auto kern = fsai_factor_kernel<MT>;
+  AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  for (int64_t r0 = 0; r0 < N; r0 += 1 << 30) {
+    const int64_t nr = std::min<int64_t>(N - r0, 1 << 30);
+    kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, cl, mu, rp, col, grp, loc,
+                                          Ucount, Htab, Doff, D, gval, info);
+    AFN_LAUNCH_CHECK("fsai_factor_kernel");
+  }
+  return AFN_OK;
 }
 
 }  // namespace
@@ -493,18 +721,20 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double m
   int64_t* Doff;
   if ((s = get((void**)&Ucount, sizeof(int) * G)) != AFN_OK) return s;
   if ((s = get((void**)&Ulist, sizeof(int) * G * UCAP)) != AFN_OK) return s;
+  int2* Htab;
+  if ((s = get((void**)&Htab, sizeof(int2) * G * HC)) != AFN_OK) return s;
   if ((s = get((void**)&ovf, sizeof(int) * 2)) != AFN_OK) return s;
   if ((s = get((void**)&Doff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
   AFN_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int) * 2, st));
   {
-    const int bytes = (int)(sizeof(int) * 2 * HC);
+    const int bytes = (int)(sizeof(int) * HC);
     static bool uattr = false;
     if (!uattr) {
       AFN_CUDA(cudaFuncSetAttribute(group_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       uattr = true;
     }
     group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, col, trp, tcol, row_lo, row_hi,
-                                                         Ucount, Ulist, ovf);
+                                                         Ucount, Ulist, Htab, ovf);
     AFN_LAUNCH_CHECK("group_union_kernel");
   }
   int hov = 0;
@@ -516,7 +746,16 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double m
   }
   scan_i64_kernel<<<1, 1024, 0, st>>>(Ucount, G, GA, Doff);
   AFN_LAUNCH_CHECK("scan_i64_kernel");
-  int64_t totD = 0;
+  int* pc;
+  int64_t* Poff;
+  if ((s = get((void**)&pc, sizeof(int) * G)) != AFN_OK) return s;
+  if ((s = get((void**)&Poff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
+  pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, pc);
+  AFN_LAUNCH_CHECK("pass_count_kernel");
+  scan_i64_kernel<<<1, 1024, 0, st>>>(pc, G, 1, Poff);
+  AFN_LAUNCH_CHECK("scan_i64_kernel");
+  int64_t totD = 0, items = 0;
+  AFN_CUDA(cudaMemcpyAsync(&items, Poff + G, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaMemcpyAsync(&totD, Doff + G, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaStreamSynchronize(st));
   // ---- 3. dense group products
@@ -530,38 +769,26 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double m
       attr = true;
     }
     kt_begin(KT_FSAI_GEMM, st);
-    group_gemm_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, D);
-    AFN_LAUNCH_CHECK("group_gemm_kernel");
+    if (items > 0) {
+      group_gemm_kernel<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D);
+      AFN_LAUNCH_CHECK("group_gemm_kernel");
+    }
     kt_end(KT_FSAI_GEMM, st, 2.0 * (double)k * (double)totD);
   }
-  // ---- 4. per-row assembly + warp Cholesky, in batches
-  const int64_t WP = (int64_t)MT * 16;
-  const int64_t SPK = WP * (WP + 1) / 2;
-  const int64_t NR = row_hi - row_lo;
-  const int64_t batch = std::min<int64_t>(NR, std::max<int64_t>(4096, (int64_t)(1LL << 30) / (SPK * 8)));
-  double* Sg;
-  if ((s = get((void**)&Sg, sizeof(double) * SPK * batch)) != AFN_OK) return s;
+  // ---- 4. per-row assembly + Cholesky + g (one CTA per row, rows in the
+  // spatial order sorder; CTAs of other ranks' rows exit at once)
   const double cl = AFN_LOG2E / (l * l);
-  for (int64_t r0 = row_lo; r0 < row_hi; r0 += batch) {
-    const int64_t nr = std::min(batch, row_hi - r0);
-    const unsigned grid = (unsigned)nr;
-    kt_begin(KT_FSAI_ASM, st);
-    switch (MT) {
-      case 1: launch_assemble<1>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      case 2: launch_assemble<2>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      case 3: launch_assemble<3>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      case 4: launch_assemble<4>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      case 5: launch_assemble<5>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      case 6: launch_assemble<6>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      case 7: launch_assemble<7>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-      default: launch_assemble<8>(grid, st, r0, X2, d, cl, mu, rp, col, grp, loc, Ucount, Ulist, Doff, D, Sg); break;
-    }
-    AFN_LAUNCH_CHECK("fsai_assemble_kernel");
-    kt_end(KT_FSAI_ASM, st, 0.0);
-    kt_begin(KT_FSAI_CHOL, st);
-    if ((s = fsai_chol_batch(r0, nr, MT, rp, Sg, gval, d_info, st)) != AFN_OK) return s;
-    kt_end(KT_FSAI_CHOL, st, (double)nr * ((double)w * w * w / 3.0 + (double)w * w));
+  const int64_t NR = row_hi - row_lo;
+  kt_begin(KT_FSAI_CHOL, st);
+  switch (MT) {
+#define AFN_FACTOR(M) \
+    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, st, X2, d, cl, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    AFN_FACTOR(1) AFN_FACTOR(2) AFN_FACTOR(3) AFN_FACTOR(4) AFN_FACTOR(5) AFN_FACTOR(6) AFN_FACTOR(7)
+    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, st, X2, d, cl, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+#undef AFN_FACTOR
   }
+  if (s != AFN_OK) return s;
+  kt_end(KT_FSAI_CHOL, st, (double)NR * ((double)w * w * w / 3.0 + (double)w * w));
   return AFN_OK;
 }
 
