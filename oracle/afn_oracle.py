@@ -26,8 +26,13 @@ __all__ = [
     "fps", "fill_distance", "separation_distance", "knn_lower", "knn_row",
     "splitmix64", "subsample_ids", "default_m", "alg1",
     "fsai_rows", "build_afn", "apply_afn", "dense_B", "pcg", "afn_pcg_solve",
-    "cg_solve",
+    "cg_solve", "kernel_from_d2", "uniform_landmarks", "build_nystrom", "apply_nystrom",
+    "choose_method", "build_precond", "apply_precond", "KERNELS", "NYS_NU", "UNIFORM_SEED_XOR",
 ]
+
+KERNELS = ("gaussian", "matern32")
+NYS_NU = 1e-10          # K11 shift of the Nystrom preconditioner (reading R30)
+UNIFORM_SEED_XOR = 0x6A09E667F3BCC909  # landmark key stream (reading R29)
 
 EPS = np.finfo(np.float64).eps
 
@@ -56,24 +61,36 @@ def sqdist_block(A: np.ndarray, B: np.ndarray) -> np.ndarray:
     return d2
 
 
-def kernel_block(A: np.ndarray, B: np.ndarray, l: float) -> np.ndarray:
-    """K_AB with K(x,y) = exp(-||x-y||^2 / l^2), no factor 1/2 (R1)."""
-    return np.exp(-sqdist_block(A, B) / (l * l))
+def kernel_from_d2(d2, l: float, kernel: str = "gaussian"):
+    """Kernel value from the squared distance:
+    gaussian  exp(-d2 / l^2)  (no factor 1/2, P:L38, R1);
+    matern32  (1 + sqrt(3) r / l) exp(-sqrt(3) r / l), r = sqrt(d2)."""
+    if kernel == "gaussian":
+        return np.exp(-d2 / (l * l))
+    if kernel == "matern32":
+        t = math.sqrt(3.0) * np.sqrt(d2) / l
+        return (1.0 + t) * np.exp(-t)
+    raise ValueError(f"unknown kernel {kernel!r}")
+
+
+def kernel_block(A: np.ndarray, B: np.ndarray, l: float, kernel: str = "gaussian") -> np.ndarray:
+    """K_AB (P:L38, P:L767-769)."""
+    return kernel_from_d2(sqdist_block(A, B), l, kernel)
 
 
 def kmv_rows(X: np.ndarray, l: float, mu: float, v: np.ndarray, rows: np.ndarray,
-             block: int = 256) -> np.ndarray:
+             block: int = 256, kernel: str = "gaussian") -> np.ndarray:
     """y_i = sum_j K(x_i, x_j) v_j + mu v_i for the listed rows i."""
     rows = np.asarray(rows)
     out = np.empty(len(rows))
     for s in range(0, len(rows), block):
         r = rows[s:s + block]
-        out[s:s + block] = kernel_block(X[r], X, l) @ v + mu * v[r]
+        out[s:s + block] = kernel_block(X[r], X, l, kernel) @ v + mu * v[r]
     return out
 
 
 def kmv(X: np.ndarray, l: float, mu: float, v: np.ndarray, block: int = 256,
-        threads: int | None = None) -> np.ndarray:
+        threads: int | None = None, kernel: str = "gaussian") -> np.ndarray:
     """(K + mu I) v with K never stored whole (explicit matvec).
 
     Row blocks; with ``threads`` > 1 the blocks go to a thread pool (NumPy
@@ -86,7 +103,7 @@ def kmv(X: np.ndarray, l: float, mu: float, v: np.ndarray, block: int = 256,
 
     def work(s):
         e = min(n, s + block)
-        y[s:e] = kernel_block(X[s:e], X, l) @ v + mu * v[s:e]
+        y[s:e] = kernel_block(X[s:e], X, l, kernel) @ v + mu * v[s:e]
 
     starts = range(0, n, block)
     if threads and threads > 1:
@@ -217,7 +234,8 @@ def default_m(n: int) -> int:
 
 
 def alg1(X: np.ndarray, l: float, m: int | None = None, rng_seed: int = 0,
-         k_threshold: int = 2000, err_tol: float = 0.1, ev_tol: float = 0.1):
+         k_threshold: int = 2000, err_tol: float = 0.1, ev_tol: float = 0.1,
+         kernel: str = "gaussian"):
     """Algorithm 1 step by step.
 
     1. subsample m points, scale coordinates by s = (m/n)^(1/d)       (L666, R8)
@@ -237,7 +255,7 @@ def alg1(X: np.ndarray, l: float, m: int | None = None, rng_seed: int = 0,
     ids = subsample_ids(n, m, rng_seed)
     s = (m / n) ** (1.0 / d)
     Xm = X[ids] * s
-    Km = kernel_block(Xm, Xm, l)
+    Km = kernel_block(Xm, Xm, l, kernel)
     order, _ = fps(Xm, m, 0)
     S = Km[np.ix_(order, order)].copy()
     normK = float(np.max(np.abs(np.linalg.eigvalsh(Km))))
@@ -264,7 +282,7 @@ def alg1(X: np.ndarray, l: float, m: int | None = None, rng_seed: int = 0,
     ev_margin = float("inf")
     if khat < k_threshold:
         Xu = X[ids]
-        ev = np.linalg.eigvalsh(kernel_block(Xu, Xu, l))
+        ev = np.linalg.eigvalsh(kernel_block(Xu, Xu, l, kernel))
         khat = int(np.count_nonzero(ev > ev_tol))
         ev_margin = float(np.min(np.abs(ev - ev_tol)))
         refined = True
@@ -302,7 +320,26 @@ def fsai_rows(S_sub, row_ptr, col):
 # ----------------------------------------------------------------------------
 # AFN build
 # ----------------------------------------------------------------------------
-def build_afn(X: np.ndarray, l: float, mu: float, k: int, w: int, fps_seed: int = 0):
+def uniform_landmarks(n: int, k: int, rng_seed: int = 0) -> np.ndarray:
+    """Uniformly random landmarks, the paper's choice for its high-dimensional
+    datasets, read as R29: the k smallest splitmix64 keys of the
+    stream rng_seed ^ 0x6A09E667F3BCC909 (the generator of subsample_ids)."""
+    return subsample_ids(n, k, int(rng_seed) ^ UNIFORM_SEED_XOR)
+
+
+def _landmarks(X, k, landmarks, fps_seed, rng_seed):
+    n = len(X)
+    if k == 0:
+        return np.empty(0, dtype=np.int64), np.empty(0)
+    if landmarks == "fps":
+        return fps(X, k, fps_seed)
+    if landmarks == "uniform":
+        return uniform_landmarks(n, k, rng_seed), np.zeros(k)
+    raise ValueError(f"unknown landmarks {landmarks!r}")
+
+
+def build_afn(X: np.ndarray, l: float, mu: float, k: int, w: int, fps_seed: int = 0,
+              kernel: str = "gaussian", landmarks: str = "fps", rng_seed: int = 0):
     """Build the AFN factors, paper-literal.
 
     * X_k by FPS; landmarks indexed first, the rest
@@ -315,24 +352,24 @@ def build_afn(X: np.ndarray, l: float, mu: float, k: int, w: int, fps_seed: int 
     """
     X = np.asarray(X, dtype=np.float64)
     n = X.shape[0]
-    k = int(min(k, n))
-    idx, fill = fps(X, k, fps_seed)
+    k = int(min(k, n))  # k = 0: plain FSAI of K + mu I
+    idx, fill = _landmarks(X, k, landmarks, fps_seed, rng_seed)
     mask = np.ones(n, bool)
     mask[idx] = False
     rest = np.nonzero(mask)[0].astype(np.int64)
-    perm = np.concatenate([idx, rest])
+    perm = np.concatenate([idx, rest]).astype(np.int64)
     Xp = X[perm]
     X1, X2 = Xp[:k], Xp[k:]
-    A11 = kernel_block(X1, X1, l) + mu * np.eye(k)
-    L = np.linalg.cholesky(A11)
-    K12 = kernel_block(X1, X2, l)
-    V = sla.solve_triangular(L, K12, lower=True)
+    A11 = kernel_block(X1, X1, l, kernel) + mu * np.eye(k)
+    L = np.linalg.cholesky(A11) if k > 0 else np.zeros((0, 0))
+    K12 = kernel_block(X1, X2, l, kernel)
+    V = sla.solve_triangular(L, K12, lower=True) if k > 0 else np.zeros((0, n))
     N2 = n - k
     if N2 > 0:
         row_ptr, col = knn_lower(X2, w)
 
         def S_sub(J):
-            return kernel_block(X2[J], X2[J], l) + mu * np.eye(len(J)) - V[:, J].T @ V[:, J]
+            return kernel_block(X2[J], X2[J], l, kernel) + mu * np.eye(len(J)) - V[:, J].T @ V[:, J]
 
         gv = fsai_rows(S_sub, row_ptr, col)
         G = sp.csr_matrix((gv, col, row_ptr), shape=(N2, N2))
@@ -340,8 +377,9 @@ def build_afn(X: np.ndarray, l: float, mu: float, k: int, w: int, fps_seed: int 
         row_ptr = np.zeros(1, dtype=np.int64)
         col = np.empty(0, dtype=np.int64)
         G = sp.csr_matrix((0, 0))
-    return dict(n=n, k=k, w=w, l=l, mu=mu, idx=idx, fill=fill, perm=perm, Xp=Xp,
-                L=L, K12=K12, V=V, row_ptr=row_ptr, col=col, G=G)
+    return dict(method="afn" if k > 0 else "fsai", n=n, k=k, w=w, l=l, mu=mu, kernel=kernel,
+                idx=idx, fill=fill, perm=perm, Xp=Xp, L=L, K12=K12, V=V, row_ptr=row_ptr,
+                col=col, G=G)
 
 
 def apply_afn(B: dict, r: np.ndarray) -> np.ndarray:
@@ -354,8 +392,12 @@ def apply_afn(B: dict, r: np.ndarray) -> np.ndarray:
     r1, r2 = r[:k], r[k:]
 
     def LLt_solve(v):
+        if k == 0:
+            return np.empty(0)
         return sla.solve_triangular(L.T, sla.solve_triangular(L, v, lower=True), lower=False)
 
+    if k == 0:  # plain FSAI: M^{-1} = G^T G
+        return G.T @ (G @ r2)
     if len(r2):
         s2 = G.T @ (G @ (r2 - K12.T @ LLt_solve(r1)))
         s1 = LLt_solve(r1 - K12 @ s2)
@@ -363,6 +405,60 @@ def apply_afn(B: dict, r: np.ndarray) -> np.ndarray:
         s2 = np.empty(0)
         s1 = LLt_solve(r1)
     return np.concatenate([s1, s2])
+
+
+def build_nystrom(X: np.ndarray, l: float, mu: float, k: int, fps_seed: int = 0,
+                  kernel: str = "gaussian", landmarks: str = "fps", rng_seed: int = 0,
+                  nu: float = NYS_NU):
+    """Nystrom preconditioner K_nys + mu I on k landmarks indexed
+    first, K_nys = K_{X,Xk} (K11 + nu I)^{-1} K_{Xk,X} (R30: the
+    paper cites stabilised implementations; nu = 1e-10)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    k = int(min(max(k, 1), n))
+    idx, fill = _landmarks(X, k, landmarks, fps_seed, rng_seed)
+    mask = np.ones(n, bool)
+    mask[idx] = False
+    perm = np.concatenate([idx, np.nonzero(mask)[0]]).astype(np.int64)
+    Xp = X[perm]
+    X1 = Xp[:k]
+    K11 = kernel_block(X1, X1, l, kernel)
+    K12 = kernel_block(X1, Xp[k:], l, kernel)
+    return dict(method="nystrom", n=n, k=k, l=l, mu=mu, nu=nu, kernel=kernel, idx=idx,
+                fill=fill, perm=perm, Xp=Xp, K11=K11, K12=K12)
+
+
+def apply_nystrom(N: dict, r: np.ndarray) -> np.ndarray:
+    """(K_nys + mu I)^{-1} r by the SMW formula eq:smw, with
+    K11 -> K11 + nu I in the inner matrix (R30):
+      r/mu - (1/mu^2) [K11 K12]^T (K11 + nu I + (K11^2 + K12 K12^T)/mu)^{-1} [K11 K12] r.
+    r in the permuted (landmarks-first) order."""
+    K11, K12, mu, nu, k = N["K11"], N["K12"], N["mu"], N["nu"], N["k"]
+    r = np.asarray(r, dtype=np.float64)
+    A = np.hstack([K11, K12])
+    inner = K11 + nu * np.eye(k) + (K11 @ K11 + K12 @ K12.T) / mu
+    return r / mu - (A.T @ np.linalg.solve(inner, A @ r)) / (mu * mu)
+
+
+def choose_method(khat: int, k_threshold: int = 2000) -> str:
+    """Algorithm 2: AFN if the estimated rank is >= 2000, else Nystrom."""
+    return "afn" if khat >= k_threshold else "nystrom"
+
+
+def build_precond(X, l, mu, k, w, method="afn", kernel="gaussian", landmarks="fps",
+                  fps_seed=0, rng_seed=0):
+    """AFN (eq:factorized-form), Nystrom or plain FSAI (k = 0)."""
+    if method == "nystrom":
+        return build_nystrom(X, l, mu, k, fps_seed, kernel, landmarks, rng_seed)
+    if method == "fsai":
+        return build_afn(X, l, mu, 0, w, fps_seed, kernel, landmarks, rng_seed)
+    return build_afn(X, l, mu, k, w, fps_seed, kernel, landmarks, rng_seed)
+
+
+def apply_precond(B: dict, r: np.ndarray) -> np.ndarray:
+    if B.get("method") == "nystrom":
+        return apply_nystrom(B, r)
+    return apply_afn(B, r)
 
 
 def dense_B(B: dict) -> np.ndarray:
@@ -429,21 +525,23 @@ def pcg(Amv, Minv, b, tol: float = 1e-4, maxit: int = 500, fixed_iters: int = 0,
 
 
 def afn_pcg_solve(X, b, l, mu, k, w, tol=1e-4, maxit=500, fixed_iters=0, fps_seed=0,
-                  B=None, threads=None):
-    """Full path: build AFN (unless ``B`` given), PCG on the permuted system,
-    un-permute.  Returns (a, report, B)."""
+                  B=None, threads=None, method="afn", kernel="gaussian", landmarks="fps",
+                  rng_seed=0):
+    """Full path: build the preconditioner (unless ``B`` given), PCG on the
+    permuted system, un-permute.  Returns (a, report, B)."""
     X = np.asarray(X, dtype=np.float64)
     if B is None:
-        B = build_afn(X, l, mu, k, w, fps_seed)
+        B = build_precond(X, l, mu, k, w, method, kernel, landmarks, fps_seed, rng_seed)
+    kernel = B.get("kernel", kernel)
     perm = B["perm"]
     Xp = B["Xp"]
     bp = np.asarray(b, dtype=np.float64)[perm]
-    x, rep = pcg(lambda v: kmv(Xp, l, mu, v, threads=threads), lambda r: apply_afn(B, r),
-                 bp, tol, maxit, fixed_iters)
+    x, rep = pcg(lambda v: kmv(Xp, l, mu, v, threads=threads, kernel=kernel),
+                 lambda r: apply_precond(B, r), bp, tol, maxit, fixed_iters)
     a = np.empty_like(x)
     a[perm] = x
     nb = float(np.linalg.norm(b))
-    res = b - kmv(X, l, mu, a, threads=threads)
+    res = b - kmv(X, l, mu, a, threads=threads, kernel=kernel)
     rep["relres_true"] = float(np.linalg.norm(res)) / nb if nb > 0 else 0.0
     return a, rep, B
 

@@ -388,3 +388,89 @@ def test_c1_afn_pcg_end_to_end():
     assert rep["iterations"] * 5 < rcg["iterations"]
     Kd = O.kernel_block(X, X, 1.0) + 1e-4 * np.eye(1000)
     assert np.linalg.norm(Kd @ a - b) / np.linalg.norm(b) == pytest.approx(rep["relres_true"], rel=1e-6)
+
+
+# --------------------------------------------------------------------------- next rows
+def test_matern32_is_the_nu_three_halves_matern():
+    """(1 + sqrt3 r/l) exp(-sqrt3 r/l) is the Matern kernel with nu = 3/2,
+    2^(1-nu)/Gamma(nu) z^nu K_nu(z), z = sqrt(2 nu) r / l (scipy's Bessel K)."""
+    from scipy.special import gamma, kv
+    X, _ = gen_points(40, 3, "cube", 2)
+    for l in (0.5, 2.0, 10.0):
+        d2 = O.sqdist_block(X, X)
+        K = O.kernel_block(X, X, l, "matern32")
+        r = np.sqrt(d2)
+        nu = 1.5
+        z = np.sqrt(2 * nu) * r / l
+        with np.errstate(invalid="ignore"):
+            ref = 2 ** (1 - nu) / gamma(nu) * z ** nu * kv(nu, z)
+        ref[r == 0] = 1.0
+        assert np.allclose(K, ref, rtol=1e-12, atol=1e-300)
+        assert np.all(np.linalg.eigvalsh(K) > 0)  # positive definite on distinct points
+
+
+def test_alg1_special_cases_hold_for_matern():
+    """Alg. 1 limits do not depend on the kernel: l -> inf gives a
+    rank-one K_m (r = 1), l -> 0 gives K_m = I (refined count = m)."""
+    X, _ = gen_points(1000, 3, "cube", 0)
+    big = O.alg1(X, 1e9, m=100, kernel="matern32")
+    assert big["r"] == 1
+    tiny = O.alg1(X, 1e-9, m=100, kernel="matern32")
+    assert tiny["refined"] and tiny["khat"] == 100
+
+
+def test_uniform_landmarks_are_the_smallest_keys():
+    """R29: k distinct indices, in key order, every unselected key larger."""
+    n, k, seed = 5000, 300, 7
+    idx = O.uniform_landmarks(n, k, seed)
+    keys = O.splitmix64(np.uint64(seed ^ O.UNIFORM_SEED_XOR) ^
+                        (np.arange(n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)))
+    assert len(set(idx.tolist())) == k
+    assert np.all(np.diff(keys[idx].astype(np.float64)) > 0)
+    rest = np.setdiff1d(np.arange(n), idx)
+    assert keys[rest].min() > keys[idx].max()
+
+
+def test_nystrom_apply_equals_dense_solve():
+    """eq:smw against an explicit K_nys + mu I and a
+    dense LAPACK solve, at a size where the latter is cheap."""
+    X, b = gen_problem("C1")
+    for kernel, l in (("gaussian", 2.0), ("matern32", 3.0)):
+        N = O.build_nystrom(X, l, 1e-3, 80, kernel=kernel)
+        Xp = N["Xp"]
+        C = O.kernel_block(Xp, Xp[:80], l, kernel)
+        Knys = C @ np.linalg.solve(N["K11"] + N["nu"] * np.eye(80), C.T)
+        r = np.random.default_rng(1).standard_normal(len(X))
+        z = O.apply_nystrom(N, r)
+        zd = np.linalg.solve(Knys + 1e-3 * np.eye(len(X)), r)
+        assert np.linalg.norm(z - zd) <= 1e-8 * np.linalg.norm(zd)
+
+
+def test_nystrom_with_all_landmarks_is_exact():
+    """k = n: K_nys = K (P:L185 with K22 - K21 K11^-1 K12 = 0), so PCG with the
+    Nystrom preconditioner converges at once."""
+    X, b = gen_points(150, 3, "cube", 5, edge=4.0)
+    b = np.random.default_rng(2).standard_normal(150)
+    a, rep, _ = O.afn_pcg_solve(X, b, 1.0, 1e-2, 150, 10, method="nystrom", tol=1e-8)
+    assert rep["iterations"] <= 2
+    ad = np.linalg.solve(O.kernel_block(X, X, 1.0) + 1e-2 * np.eye(150), b)
+    assert np.linalg.norm(a - ad) <= 1e-6 * np.linalg.norm(ad)
+
+
+def test_plain_fsai_full_pattern_is_exact():
+    """k = 0 (plain FSAI of K + mu I) with the full pattern:
+    G^T G = (K + mu I)^{-1} (Kolotilina-Yeremin), PCG in one step."""
+    X, _ = gen_points(120, 3, "cube", 3, edge=4.0)
+    b = np.random.default_rng(3).standard_normal(120)
+    B = O.build_precond(X, 1.0, 1e-3, 0, 128, method="fsai")
+    A = O.kernel_block(X, X, 1.0) + 1e-3 * np.eye(120)
+    G = B["G"].toarray()
+    assert np.allclose(G.T @ G, np.linalg.inv(A), rtol=1e-6, atol=1e-8 * np.abs(np.linalg.inv(A)).max())
+    a, rep, _ = O.afn_pcg_solve(X, b, 1.0, 1e-3, 0, 128, method="fsai", tol=1e-10, B=B)
+    assert rep["iterations"] <= 2
+
+
+def test_algorithm2_threshold():
+    """Alg. 2: AFN when k >= 2000, Nystrom below."""
+    assert O.choose_method(2000) == "afn" and O.choose_method(1999) == "nystrom"
+    assert O.choose_method(10, k_threshold=10) == "afn"
