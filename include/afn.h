@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define AFN_ABI_VERSION 2
+#define AFN_ABI_VERSION 3
 
 typedef enum {
   AFN_OK = 0,
@@ -54,6 +54,26 @@ typedef struct afn_handle_s* afn_handle;
 /* Opaque communicator of the row-sharded multi-GPU path (afn_comm_*). */
 typedef struct afn_comm_s* afn_comm;
 
+/* Kernel functions, r = ||x - y||:
+ *   AFN_KERNEL_GAUSSIAN  exp(-r^2 / l^2)          (eq:gaussianf)
+ *   AFN_KERNEL_MATERN32  (1 + sqrt(3) r / l) exp(-sqrt(3) r / l)            */
+enum { AFN_KERNEL_GAUSSIAN = 0, AFN_KERNEL_MATERN32 = 1 };
+/* Landmark selection: farthest point sampling or uniform
+ * random sampling, the paper's choice for its high-dimensional datasets
+ * (P:L957): the k points with the smallest splitmix64 keys of
+ * (rng_seed ^ 0x6A09E667F3BCC909) ^ i*golden, in key order (reading R29). */
+enum { AFN_LANDMARKS_FPS = 0, AFN_LANDMARKS_UNIFORM = 1 };
+/* Preconditioner (Algorithm 2):
+ *   AFN_METHOD_AFN      AFN (eq:factorized-form) with k landmarks
+ *   AFN_METHOD_ALG2     Algorithm 2: AFN if Alg. 1's khat >= k_threshold,
+ *                       else the Nystrom preconditioner with khat landmarks
+ *                       (needs k_adaptive = 1)
+ *   AFN_METHOD_NYSTROM  Nystrom preconditioner K_nys + mu I
+ *                       applied exactly through an equivalent stable SMW form
+ *   AFN_METHOD_FSAI     plain FSAI of K + mu I on the kNN pattern of all
+ *                       points in the original order (k = 0)    */
+enum { AFN_METHOD_AFN = 0, AFN_METHOD_ALG2 = 1, AFN_METHOD_NYSTROM = 2, AFN_METHOD_FSAI = 3 };
+
 /* Build parameters.  Cite: l, mu; k_cap "limit ... such as 2000"
  * (P:L209-210); w "the w-1 nearest neighbors" (w counts the
  * diagonal, reading R15); m, rng_seed, k_threshold: Algorithm 1 (P:L661-678,
@@ -68,6 +88,10 @@ typedef struct {
   int32_t k_threshold;  /* Alg. 1 branch threshold (paper: 2000)               */
   int64_t fps_seed;     /* first FPS point, 0 <= fps_seed < n                  */
   uint64_t rng_seed;    /* Alg. 1 subsample seed (splitmix64 counter, R7)      */
+  int32_t kernel;       /* AFN_KERNEL_*                                        */
+  int32_t landmarks;    /* AFN_LANDMARKS_*                                     */
+  int32_t method;       /* AFN_METHOD_*                                        */
+  int32_t reserved;     /* 0                                                   */
 } afn_params;
 
 /* Information about a built handle (host struct). */
@@ -79,6 +103,8 @@ typedef struct {
   double ms_fsai_rows;          /* the FSAI row kernel alone (inside ms_fsai)      */
   int32_t nranks, rank;         /* communicator size, this (first local) rank      */
   int64_t row_a0, row_na, row_b0, row_nb; /* rows of the permuted order it owns   */
+  int32_t kernel, method;       /* kernel, preconditioner built (AFN_METHOD_AFN,   */
+                                /* _NYSTROM or _FSAI)                              */
 } afn_info;
 
 /* PCG report (host struct).  history: optional host array of >= maxit+1
@@ -102,12 +128,12 @@ typedef struct {
 /* X: n x d device, v,y: n device (y must not alias v or X).  Stream-ordered. */
 /* Rows are evaluated with a fixed column-chunk order, so the output is       */
 /* bit-identical run to run.  n >= 1, 1 <= d <= 16, l > 0, mu >= 0.           */
-afn_status kernel_matvec(const double* X, int64_t n, int32_t d, double l, double mu,
+afn_status kernel_matvec(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
                          const double* v, double* y, void* stream);
 
 /* Rows [row0, row0+nrows) of y = (K + mu I) v against all n columns (the row
  * shard a rank owns in the multi-GPU layout).  y has nrows entries. */
-afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, double l, double mu,
+afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
                               const double* v, int64_t row0, int64_t nrows, double* y,
                               void* stream);
 
@@ -128,7 +154,7 @@ afn_status afn_knn_pattern(const double* P, int64_t N, int32_t d, int32_t w,
 
 /* Algorithm 1 on device.  [sync]  Outputs (host): khat, r, and */
 /* refined (1 if the eigenvalue-count branch was taken).  m = 0 -> default.  */
-afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, double l, int32_t m,
+afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, int32_t kernel, double l, int32_t m,
                              uint64_t rng_seed, int32_t k_threshold, int64_t* khat,
                              int32_t* r, int32_t* refined, void* stream);
 

@@ -27,6 +27,14 @@ AFN_OK = 0
 STATUS = {0: "AFN_OK", 1: "AFN_ERR_ARG", 2: "AFN_ERR_CUDA", 3: "AFN_ERR_NOMEM",
           4: "AFN_ERR_NOT_SPD", 5: "AFN_ERR_BREAKDOWN", 6: "AFN_ERR_NCCL", 7: "AFN_ERR_STATE"}
 COMM_ID_BYTES = 128
+KERNEL_GAUSSIAN, KERNEL_MATERN32 = 0, 1
+LANDMARKS_FPS, LANDMARKS_UNIFORM = 0, 1
+METHOD_AFN, METHOD_ALG2, METHOD_NYSTROM, METHOD_FSAI = 0, 1, 2, 3
+_KERNELS = {"gaussian": KERNEL_GAUSSIAN, "matern32": KERNEL_MATERN32}
+
+
+def _kernel_id(kernel):
+    return _KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
 OUT_PERM, OUT_FILL, OUT_L, OUT_ROWPTR, OUT_COL, OUT_GVAL, OUT_W = range(7)
 
 
@@ -40,7 +48,9 @@ class AfnError(RuntimeError):
 class Params(C.Structure):
     _fields_ = [("l", C.c_double), ("mu", C.c_double), ("k_cap", C.c_int64),
                 ("k_adaptive", C.c_int32), ("w", C.c_int32), ("m", C.c_int32),
-                ("k_threshold", C.c_int32), ("fps_seed", C.c_int64), ("rng_seed", C.c_uint64)]
+                ("k_threshold", C.c_int32), ("fps_seed", C.c_int64), ("rng_seed", C.c_uint64),
+                ("kernel", C.c_int32), ("landmarks", C.c_int32), ("method", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -50,7 +60,8 @@ class Info(C.Structure):
                 ("ms_chol", C.c_double), ("ms_trsm", C.c_double), ("ms_knn", C.c_double),
                 ("ms_fsai", C.c_double), ("ms_total", C.c_double), ("ms_fsai_rows", C.c_double),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("row_a0", C.c_int64),
-                ("row_na", C.c_int64), ("row_b0", C.c_int64), ("row_nb", C.c_int64)]
+                ("row_na", C.c_int64), ("row_b0", C.c_int64), ("row_nb", C.c_int64),
+                ("kernel", C.c_int32), ("method", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -72,12 +83,14 @@ class Report(C.Structure):
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _sig = {
-    "kernel_matvec": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P, _P, _P]),
-    "kernel_matvec_rows": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, _P,
+    "kernel_matvec": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_double, _P, _P,
+                                _P]),
+    "kernel_matvec_rows": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_double, _P,
                                      C.c_int64, C.c_int64, _P, _P]),
     "afn_fps": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, _P, _P, _P]),
     "afn_knn_pattern": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
-    "afn_estimate_rank": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_int32, C.c_uint64,
+    "afn_estimate_rank": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                                    C.c_uint64,
                                     C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32), _P]),
     "afn_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.POINTER(Params), _P, C.POINTER(_P)]),
@@ -168,24 +181,25 @@ def abi_version() -> int:
 
 
 # ---------------------------------------------------------------------------
-def kernel_matvec(X, l, mu, v, y=None, stream=None):
+def kernel_matvec(X, l, mu, v, y=None, stream=None, kernel="gaussian"):
     """y = (K + mu I) v on the device (include/afn.h kernel_matvec)."""
     torch = _torch()
     n, d = X.shape
     if y is None:
         y = torch.empty_like(v)
-    _check(_lib.kernel_matvec(_dev(X, "X", torch.float64), n, d, float(l), float(mu),
+    _check(_lib.kernel_matvec(_dev(X, "X", torch.float64), n, d, _kernel_id(kernel), float(l), float(mu),
                               _dev(v, "v", torch.float64), _dev(y, "y", torch.float64),
                               _stream(stream)), "kernel_matvec")
     return y
 
 
-def kernel_matvec_rows(X, l, mu, v, row0, nrows, y=None, stream=None):
+def kernel_matvec_rows(X, l, mu, v, row0, nrows, y=None, stream=None, kernel="gaussian"):
     torch = _torch()
     n, d = X.shape
     if y is None:
         y = torch.empty(nrows, dtype=torch.float64, device=v.device)
-    _check(_lib.kernel_matvec_rows(_dev(X, "X", torch.float64), n, d, float(l), float(mu),
+    _check(_lib.kernel_matvec_rows(_dev(X, "X", torch.float64), n, d, _kernel_id(kernel), float(l),
+                                   float(mu),
                                    _dev(v, "v", torch.float64), int(row0), int(nrows),
                                    _dev(y, "y", torch.float64), _stream(stream)),
            "kernel_matvec_rows")
@@ -218,19 +232,21 @@ def afn_knn_pattern(P, w, stream=None):
     return rp, col[:knn_nnz(N, w)]
 
 
-def afn_estimate_rank(X, l, m=0, rng_seed=0, k_threshold=2000, stream=None):
+def afn_estimate_rank(X, l, m=0, rng_seed=0, k_threshold=2000, stream=None, kernel="gaussian"):
     torch = _torch()
     n, d = X.shape
     kh, r, ref = C.c_int64(), C.c_int32(), C.c_int32()
-    _check(_lib.afn_estimate_rank(_dev(X, "X", torch.float64), n, d, float(l), int(m),
+    _check(_lib.afn_estimate_rank(_dev(X, "X", torch.float64), n, d, _kernel_id(kernel), float(l), int(m),
                                   int(rng_seed), int(k_threshold), C.byref(kh), C.byref(r),
                                   C.byref(ref), _stream(stream)), "afn_estimate_rank")
     return dict(khat=kh.value, r=r.value, refined=bool(ref.value))
 
 
-def make_params(l, mu, k_cap, w, k_adaptive=False, m=0, k_threshold=2000, fps_seed=0, rng_seed=0):
+def make_params(l, mu, k_cap, w, k_adaptive=False, m=0, k_threshold=2000, fps_seed=0, rng_seed=0,
+                kernel="gaussian", landmarks=LANDMARKS_FPS, method=METHOD_AFN):
     return Params(float(l), float(mu), int(k_cap), int(bool(k_adaptive)), int(w), int(m),
-                  int(k_threshold), int(fps_seed), int(rng_seed))
+                  int(k_threshold), int(fps_seed), int(rng_seed), _kernel_id(kernel), int(landmarks),
+                  int(method), 0)
 
 
 def nccl_library_path():

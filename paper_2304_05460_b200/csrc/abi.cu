@@ -227,6 +227,8 @@ using namespace afn;
 // pieces (permuted points, L, L^{-T}, the pattern, G, G^T) are held by every
 // rank; W holds the rank's own non-landmark rows; the PCG vectors are full
 // length with only the rank's own rows (RankSt::own) computed locally.
+#define AFN_NYS_NU 1e-10  // K11 shift of the Nystrom branch (reading R30)
+
 struct RankSt {
   int rank = 0;
   Seg2 own{};
@@ -262,6 +264,10 @@ struct RankSt {
   double* scpart = nullptr;  // R x SC_N per-rank partials
   double* dws = nullptr;
   unsigned* dcnt = nullptr;
+  // Nystrom branch (AFN_METHOD_NYSTROM): F = K(X_own, X_k) L0^{-T} (own rows,
+  // local order), RinvT = R^{-T} with R R^T = mu I + F^T F
+  double* F = nullptr;
+  double* RinvT = nullptr;
   std::vector<void*> allocs;
 };
 
@@ -270,6 +276,8 @@ struct afn_handle_s {
   int64_t n = 0, k = 0, N2 = 0, nnz = 0;
   int d = 0;
   double l = 0, mu = 0;
+  Kern kn{};
+  int method = AFN_METHOD_AFN;  // the preconditioner built (AFN, NYSTROM or FSAI)
   afn_params params{};
   Alg1Result a1{};
   const Comm* comm = nullptr;  // not owned; null = single GPU
@@ -394,7 +402,7 @@ double apply_bytes(afn_handle h) {
 // r: the rank's own rows valid (landmark rows are all-gathered here); z: the
 // rank's own rows are written (s1 in full).
 template <class RF, class ZF>
-afn_status apply_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
+afn_status apply_afn_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   const int64_t k = h->k, N2 = h->N2;
   const int R = h->R;
   // t = L^{-1} r1 needs all of r1
@@ -434,6 +442,54 @@ afn_status apply_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   return AFN_OK;
 }
 
+// z = (K_nys + mu I)^{-1} r with K_nys = F F^T, F = K_{X,X_k} L0^{-T}:
+//   SMW  (F F^T + mu I)^{-1} = (I - F (mu I + F^T F)^{-1} F^T) / mu,
+//   t = F^T r (rank partials), u = R^{-1} t, v = R^{-T} u, z = (r - F v) / mu.
+template <class RF, class ZF>
+afn_status apply_nystrom_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
+  const int64_t k = h->k;
+  const int R = h->R;
+  for (auto& s : h->rk) {
+    const double* r = r_of(s);
+    double* tdst = R == 1 ? s.tvec : s.kpart + (size_t)s.rank * k;
+    const Seg2 g = s.own;
+    if (g.na + g.nb == 0) {
+      AFN_CUDA(cudaMemsetAsync(tdst, 0, sizeof(double) * k, st));
+    } else if (g.a0 + g.na == g.b0 || g.nb == 0) {  // contiguous rows
+      TRY(gemv_t(s.F, g.na + g.nb, k, r + g.a0, nullptr, 1.0, tdst, s.gws, st));
+    } else if (g.na == 0) {
+      TRY(gemv_t(s.F, g.nb, k, r + g.b0, nullptr, 1.0, tdst, s.gws, st));
+    } else {
+      TRY(gemv_t(s.F, g.na, k, r + g.a0, nullptr, 1.0, s.vvec, s.gws, st));
+      TRY(gemv_t(s.F + (size_t)g.na * k, g.nb, k, r + g.b0, s.vvec, 1.0, tdst, s.gws, st));
+    }
+  }
+  if (R > 1) {
+    TRY(exchange(h, [](RankSt& s) { return s.kpart; },
+                 [&](int s) { return RankRanges{{8 * (size_t)s * k, 8 * (size_t)k}}; }, st));
+    for (auto& s : h->rk) TRY(combine_sub(s.kpart, R, k, nullptr, s.tvec, st));  // t = sum (negated below)
+  }
+  const double alpha_t = R > 1 ? -1.0 : 1.0;  // combine_sub stores -sum
+  for (auto& s : h->rk) {
+    const double* r = r_of(s);
+    double* z = z_of(s);
+    TRY(gemv_t(s.RinvT, k, k, s.tvec, nullptr, alpha_t, s.uvec, s.gws, st));  // u = R^{-1} t
+    TRY(gemv_n(s.RinvT, k, k, s.uvec, nullptr, -1.0 / h->mu, s.vvec, st));   // v = -R^{-T} u / mu
+    const Seg2 g = s.own;
+    // z = r / mu - F (R^{-T} u) / mu  (own rows)
+    if (g.na > 0) TRY(gemv_n(s.F, g.na, k, s.vvec, nullptr, 1.0, z + g.a0, st));
+    if (g.nb > 0) TRY(gemv_n(s.F + (size_t)g.na * k, g.nb, k, s.vvec, nullptr, 1.0, z + g.b0, st));
+    TRY(vec_axpby(z, 1.0 / h->mu, r, 1.0, g, st));
+  }
+  return AFN_OK;
+}
+
+template <class RF, class ZF>
+afn_status apply_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
+  if (h->method == AFN_METHOD_NYSTROM) return apply_nystrom_perm(h, r_of, z_of, st);
+  return apply_afn_perm(h, r_of, z_of, st);
+}
+
 afn_status validate_X(const double* X, int64_t n, int32_t d) {
   REQ(n >= 1, "n must be >= 1 (got %lld)", (long long)n);
   REQ(d >= 1 && d <= 16, "d must be in 1..16 (got %d)", d);
@@ -469,6 +525,47 @@ struct EvPairs {
   }
 };
 
+// Nystrom branch: F = K(X_own, X_k) L0^{-T} with L0 L0^T = K11 +
+// nu I (already in s.L / s.LinvT), Gram F^T F summed over the ranks, then
+// R R^T = mu I + F^T F and R^{-T}.
+afn_status build_nystrom(afn_handle h, cudaStream_t st) {
+  const int64_t k = h->k;
+  const int d = h->d;
+  const int R = h->R;
+  std::vector<double*> Gm(h->rk.size()), Gp(h->rk.size());
+  for (size_t q = 0; q < h->rk.size(); ++q) {
+    RankSt& s = h->rk[q];
+    const Seg2 g = s.own;
+    TRY(ralloc(s, &s.F, (size_t)std::max<int64_t>(1, g.size()) * k, st));
+    if (g.na > 0) TRY(w_gemm(s.LinvT, k, s.Xp, s.Xp + g.a0 * d, g.na, d, h->kn, s.F, st));
+    if (g.nb > 0) TRY(w_gemm(s.LinvT, k, s.Xp, s.Xp + g.b0 * d, g.nb, d, h->kn, s.F + (size_t)g.na * k, st));
+    TRY(ralloc(s, &Gm[q], (size_t)k * k, st));
+    TRY(ralloc(s, &Gp[q], (size_t)R * k * k, st));
+    double* dst = R == 1 ? Gm[q] : Gp[q] + (size_t)s.rank * k * k;
+    if (g.size() > 0) TRY(syrk_ata(s.F, g.size(), k, dst, st));
+    else AFN_CUDA(cudaMemsetAsync(dst, 0, sizeof(double) * k * k, st));
+  }
+  if (R > 1) {
+    size_t q = 0;
+    TRY(exchange(h, [&](RankSt&) { return Gp[q++]; },
+                 [&](int s) { return RankRanges{{8 * (size_t)s * k * k, 8 * (size_t)k * k}}; }, st));
+    for (size_t q2 = 0; q2 < h->rk.size(); ++q2) {
+      TRY(combine_sub(Gp[q2], R, k * k, nullptr, Gm[q2], st));  // -sum, rank order
+      TRY(vec_scale(Gm[q2], -1.0, Gm[q2], seg_range(0, k * k), st));
+    }
+  }
+  for (size_t q = 0; q < h->rk.size(); ++q) {
+    RankSt& s = h->rk[q];
+    TRY(add_diag(Gm[q], k, h->mu, st));
+    TRY(potrf_lower(Gm[q], k, s.dinfo + 1, st));
+    TRY(ralloc(s, &s.RinvT, (size_t)k * k, st));
+    TRY(trsm_linvt(Gm[q], k, s.RinvT, st));
+    rfree(s, Gm[q], st);
+    rfree(s, Gp[q], st);
+  }
+  return AFN_OK;
+}
+
 afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, const afn_params* prm,
                       void* stream, afn_handle* out) {
   REQ(out != nullptr, "out must be non-null");
@@ -478,10 +575,16 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   const afn_params P = *prm;
   REQ(P.l > 0 && std::isfinite(P.l), "l must be > 0");
   REQ(P.mu > 0 && std::isfinite(P.mu), "mu must be > 0");
-  REQ(P.k_cap >= 1, "k_cap must be >= 1");
+  REQ(P.method >= AFN_METHOD_AFN && P.method <= AFN_METHOD_FSAI, "unknown method %d", P.method);
+  REQ(P.k_cap >= 1 || P.method == AFN_METHOD_FSAI, "k_cap must be >= 1");
   REQ(P.w >= 1 && P.w <= 128, "w must be in 1..128");
   REQ(P.fps_seed >= 0 && P.fps_seed < n, "need 0 <= fps_seed < n");
   REQ(n <= 0x7fffffffLL, "n must fit int32 indices");
+  REQ(P.kernel == AFN_KERNEL_GAUSSIAN || P.kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", P.kernel);
+  REQ(P.landmarks == AFN_LANDMARKS_FPS || P.landmarks == AFN_LANDMARKS_UNIFORM, "unknown landmarks %d",
+      P.landmarks);
+  REQ(P.method != AFN_METHOD_ALG2 || P.k_adaptive, "AFN_METHOD_ALG2 needs k_adaptive = 1");
+  REQ(P.reserved == 0, "reserved must be 0");
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0;
   AFN_CUDA(cudaGetDevice(&dev));
@@ -501,6 +604,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   h->d = d;
   h->l = P.l;
   h->mu = P.mu;
+  h->kn = Kern{P.kernel, P.l};
   h->params = P;
   h->comm = (comm && comm->R > 1) ? comm : nullptr;
   h->R = h->comm ? comm->R : 1;
@@ -517,35 +621,50 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
 
   AFN_CUDA(cudaEventRecord(ev[0], st));
   // ---- a2: adaptive k (Alg. 1) -- replicated: every rank computes the same k
+  const Kern kn = h->kn;
   int64_t k = std::min<int64_t>(P.k_cap, n);
-  if (P.k_adaptive) {
+  const int kthr = P.k_threshold > 0 ? P.k_threshold : 2000;
+  h->method = P.method == AFN_METHOD_NYSTROM ? AFN_METHOD_NYSTROM
+              : P.method == AFN_METHOD_FSAI  ? AFN_METHOD_FSAI
+                                             : AFN_METHOD_AFN;
+  if (P.k_adaptive && P.method != AFN_METHOD_FSAI) {
     int m = P.m > 0 ? P.m : alg1_default_m(n);
     REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
     kt_begin(KT_ALG1, st);
-    TRY(alg1_run(X, n, d, P.l, m, P.rng_seed, P.k_threshold > 0 ? P.k_threshold : 2000, &h->a1, st));
+    TRY(alg1_run(X, n, d, kn, m, P.rng_seed, kthr, &h->a1, st));
     kt_end(KT_ALG1, st, 0.0);
     k = std::min<int64_t>(P.k_cap, std::max<int64_t>(1, h->a1.khat));
     k = std::min<int64_t>(k, n);
+    // Algorithm 2: AFN if khat >= 2000, else Nystrom with khat landmarks
+    if (P.method == AFN_METHOD_ALG2) h->method = h->a1.khat >= kthr ? AFN_METHOD_AFN : AFN_METHOD_NYSTROM;
   }
+  if (h->method == AFN_METHOD_FSAI) k = 0;  // plain FSAI of K + mu I
+  const bool nys = h->method == AFN_METHOD_NYSTROM;
   h->k = k;
-  const int64_t N2 = n - k;
+  const int64_t N2 = nys ? 0 : n - k;  // the Nystrom branch has no Schur complement
   h->N2 = N2;
   h->nnz = knn_nnz(N2, P.w);
   for (auto& s : h->rk) {
     s.own = shard_rows(n, k, h->R, s.rank);
-    s.lo = s.own.b0 - k;
-    s.hi = s.lo + s.own.nb;
+    s.lo = nys ? 0 : s.own.b0 - k;  // own non-landmark rows (W, pattern, G)
+    s.hi = nys ? 0 : s.lo + s.own.nb;
   }
   AFN_CUDA(cudaEventRecord(ev[1], st));
 
-  // ---- a3: FPS (replicated)
+  // ---- a3: landmarks (replicated): FPS or uniform (R29)
   std::vector<int64_t*> idx(nlocal);
   kt_begin(KT_FPS, st);
   for (int q = 0; q < nlocal; ++q) {
     RankSt& s = h->rk[q];
     TRY(ralloc(s, &idx[q], (size_t)k, st));
     TRY(ralloc(s, &s.fill, (size_t)k, st));
-    TRY(fps_run(X, n, d, k, P.fps_seed, idx[q], s.fill, st));
+    if (k == 0) continue;
+    if (P.landmarks == AFN_LANDMARKS_UNIFORM) {
+      TRY(uniform_landmarks(n, k, P.rng_seed ^ 0x6A09E667F3BCC909ULL, idx[q], st));
+      AFN_CUDA(cudaMemsetAsync(s.fill, 0, sizeof(double) * k, st));  // no fill trace
+    } else {
+      TRY(fps_run(X, n, d, k, P.fps_seed, idx[q], s.fill, st));
+    }
   }
   kt_end(KT_FPS, st, 0.0);
   AFN_CUDA(cudaEventRecord(ev[2], st));
@@ -560,8 +679,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(ralloc(s, &flag, (size_t)n, st));
     TRY(ralloc(s, &flag32, (size_t)n, st));
     AFN_CUDA(cudaMemsetAsync(flag32, 0, sizeof(unsigned) * (size_t)n, st));
-    mark_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(idx[q], k, n, flag32, s.derr);
-    AFN_LAUNCH_CHECK("mark_kernel");
+    if (k > 0) {
+      mark_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(idx[q], k, n, flag32, s.derr);
+      AFN_LAUNCH_CHECK("mark_kernel");
+    }
     flag8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flag32, n, flag);
     AFN_LAUNCH_CHECK("flag8_kernel");
     TRY(ralloc(s, &s.perm, (size_t)n, st));
@@ -572,15 +693,17 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(ralloc(s, &s.Xp, (size_t)n * d, st));
     TRY(gather_rows(X, n, d, s.perm, s.Xp, st));
     TRY(ralloc(s, &s.Xs, (size_t)n * d, st));
-    TRY(kmv_prescale(s.Xp, n, d, P.l, s.Xs, st));
-    TRY(ralloc(s, &s.L, (size_t)k * k, st));
-    TRY(gen_k11(s.Xp, k, d, P.l, P.mu, s.L, st));
+    TRY(kmv_prescale(s.Xp, n, d, kn, s.Xs, st));
     TRY(ralloc(s, &s.dinfo, 2, st));
     AFN_CUDA(cudaMemsetAsync(s.dinfo, 0, sizeof(int) * 2, st));
+    TRY(ralloc(s, &s.L, (size_t)k * k, st));
+    TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
+    if (k == 0) continue;
+    // AFN: K11 + mu I.  Nystrom: K11 + nu I, nu = 1e-10 (reading R30)
+    TRY(gen_k11(s.Xp, k, d, kn, nys ? AFN_NYS_NU : P.mu, s.L, st));
     kt_begin(KT_POTRF, st);
     TRY(potrf_lower(s.L, k, s.dinfo, st));
     kt_end(KT_POTRF, st, (double)k * k * k / 3.0);
-    TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
     kt_begin(KT_LINV, st);
     TRY(trsm_linvt(s.L, k, s.LinvT, st));
     kt_end(KT_LINV, st, (double)k * k * k / 3.0);
@@ -591,10 +714,18 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     AFN_CUDA(cudaMemcpyAsync(&info, s.dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
     if (info) {
-      set_error("Cholesky of K11 + mu I broke down at row %d", info - 1);
+      set_error("Cholesky of K11 + %s I broke down at row %d", nys ? "nu" : "mu", info - 1);
       return AFN_ERR_NOT_SPD;
     }
   }
+  if (nys) {
+    TRY(build_nystrom(h, st));
+    AFN_CUDA(cudaEventRecord(ev[4], st));
+    AFN_CUDA(cudaEventRecord(ev[5], st));
+    AFN_CUDA(cudaEventRecord(ev[6], st));
+    AFN_CUDA(cudaEventRecord(ev[7], st));
+    AFN_CUDA(cudaEventRecord(ev[8], st));
+  } else {
 
   // ---- a5: W = K21 L^{-T}, own rows (into a full-height buffer when sharded:
   // the FSAI rows of a rank need the W rows of all their pattern neighbours)
@@ -606,8 +737,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
     const double* X2 = s.Xp + k * d;
     if (s.hi > s.lo) {
-      if (w_trsm) TRY(trsm_w(s.L, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, P.l, Wf[q] + s.lo * k, st));
-      else TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, P.l, Wf[q] + s.lo * k, st));
+      if (w_trsm) TRY(trsm_w(s.L, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
+      else TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
     }
   }
   kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k / h->R);  // (N2/R) k^2/2 FMA per rank
@@ -662,13 +793,13 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       const double* X2 = s.Xp + k * d;
       afn_status fs = AFN_ERR_STATE;
       if (variant < 0) {
-        fs = fsai_sddmm_run(X2, N2, d, P.l, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo, s.hi,
+        fs = fsai_sddmm_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo, s.hi,
                             s.gval, s.dinfo + 1, st);
         if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
       }
       if (fs != AFN_OK) {
         kt_begin(KT_FSAI_GRAM, st);
-        TRY(fsai_run(X2, N2, d, P.l, P.mu, Wf[q], k, s.rp, s.col, s.lo, s.hi, s.gval, s.dinfo + 1, st));
+        TRY(fsai_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.lo, s.hi, s.gval, s.dinfo + 1, st));
         kt_end(KT_FSAI_GRAM, st, 0.0);
       }
     }
@@ -696,17 +827,20 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
   }
 
+  }  // AFN / FSAI
+
   // ---- workspaces for apply / PCG
   for (auto& s : h->rk) {
     const int64_t nl = s.own.size();
     s.plan = kmv_plan(n, nl, d, num_sms());
     TRY(ralloc(s, &s.kmv_part, (size_t)s.plan.chunks * std::max<int64_t>(1, nl), st));
-    const int64_t gw = std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k));
+    const int64_t gw = std::max(std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k)),
+                                nys ? gemv_t_ws(nl, k) : (int64_t)1);
     TRY(ralloc(s, &s.gws, (size_t)gw, st));
     TRY(ralloc(s, &s.tvec, (size_t)k, st));
     TRY(ralloc(s, &s.vvec, (size_t)k, st));
     TRY(ralloc(s, &s.kpart, (size_t)h->R * k, st));
-    TRY(ralloc(s, &s.uvec, (size_t)(N2 > 0 ? N2 : 1), st));
+    TRY(ralloc(s, &s.uvec, (size_t)std::max<int64_t>(std::max<int64_t>(N2, k), 1), st));
     TRY(ralloc(s, &s.yvec, (size_t)(N2 > 0 ? N2 : 1), st));
     TRY(ralloc(s, &s.rbuf, (size_t)n, st));
     TRY(ralloc(s, &s.zbuf, (size_t)n, st));
@@ -784,9 +918,10 @@ int32_t afn_kt_read(double* ms, double* work, int64_t* count, int32_t n) {
 const char* afn_last_error(void) { return g_err; }
 int64_t afn_launch_count(void) { return g_launches.load(); }
 
-afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, double l, double mu,
+afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
                               const double* v, int64_t row0, int64_t nrows, double* y, void* stream) {
   TRY(validate_X(X, n, d));
+  REQ(kernel == AFN_KERNEL_GAUSSIAN || kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", kernel);
   REQ(l > 0 && std::isfinite(l), "l must be > 0");
   REQ(mu >= 0 && std::isfinite(mu), "mu must be >= 0");
   REQ(row0 >= 0 && nrows >= 0 && row0 + nrows <= n, "row range out of bounds");
@@ -796,17 +931,17 @@ afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, double l, d
   Temps t(st);
   double* Xs;
   TRY(t.get(&Xs, (size_t)n * d));
-  TRY(kmv_prescale(X, n, d, l, Xs, st));
+  TRY(kmv_prescale(X, n, d, Kern{kernel, l}, Xs, st));
   KmvPlan plan = kmv_plan(n, nrows, d, num_sms());
   double* part;
   TRY(t.get(&part, (size_t)plan.chunks * (nrows > 0 ? nrows : 1)));
-  TRY(kmv_launch(Xs, n, d, v, mu, seg_range(row0, nrows), y, false, part, plan, st));
+  TRY(kmv_launch(Xs, n, d, kernel, v, mu, seg_range(row0, nrows), y, false, part, plan, st));
   return AFN_OK;
 }
 
-afn_status kernel_matvec(const double* X, int64_t n, int32_t d, double l, double mu, const double* v,
-                         double* y, void* stream) {
-  return kernel_matvec_rows(X, n, d, l, mu, v, 0, n, y, stream);
+afn_status kernel_matvec(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
+                         const double* v, double* y, void* stream) {
+  return kernel_matvec_rows(X, n, d, kernel, l, mu, v, 0, n, y, stream);
 }
 
 afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t seed, int64_t* idx,
@@ -833,17 +968,18 @@ afn_status afn_knn_pattern(const double* P, int64_t N, int32_t d, int32_t w, int
   return knn_run(P, N, d, w, row_ptr, col, (cudaStream_t)stream);
 }
 
-afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, double l, int32_t m,
+afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, int32_t kernel, double l, int32_t m,
                              uint64_t rng_seed, int32_t k_threshold, int64_t* khat, int32_t* r,
                              int32_t* refined, void* stream) {
   TRY(validate_X(X, n, d));
   REQ(l > 0 && std::isfinite(l), "l must be > 0");
+  REQ(kernel == AFN_KERNEL_GAUSSIAN || kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", kernel);
   if (m == 0) m = alg1_default_m(n);
   REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
   REQ(k_threshold >= 1, "k_threshold must be >= 1");
   REQ(khat && r && refined, "outputs must be non-null host pointers");
   Alg1Result res;
-  TRY(alg1_run(X, n, d, l, m, rng_seed, k_threshold, &res, (cudaStream_t)stream));
+  TRY(alg1_run(X, n, d, Kern{kernel, l}, m, rng_seed, k_threshold, &res, (cudaStream_t)stream));
   *khat = res.khat;
   *r = res.r;
   *refined = res.refined;
@@ -944,7 +1080,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
       }
       kt_begin(KT_KMV, st);
       for (auto& s : h->rk)
-        TRY(kmv_launch(s.Xs, n, d, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+        TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
       kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0) / h->R);
       AFN_CUDA(cudaEventRecord(km1, st));
       for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
@@ -998,7 +1134,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   AFN_CUDA(cudaEventRecord(e1, st));
   if (nb > 0) {
     for (auto& s : h->rk) {
-      TRY(kmv_launch(s.Xs, n, d, s.x, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+      TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.x, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
       TRY(gather_vec(b, s.perm, n, s.z, st));
       TRY(vec_axpby(s.z, -1.0, s.q, 1.0, s.own, st));
       TRY(dot(s.z, s.z, s.own, part_dst(h, s, SC_TMP), s.dws, s.dcnt, st));
@@ -1072,6 +1208,8 @@ afn_status afn_get_info(afn_handle h, afn_info* info) {
   I.row_na = h->rk[0].own.na;
   I.row_b0 = h->rk[0].own.b0;
   I.row_nb = h->rk[0].own.nb;
+  I.kernel = h->kn.kind;
+  I.method = h->method;
   *info = I;
   return AFN_OK;
 }

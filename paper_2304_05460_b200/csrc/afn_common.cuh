@@ -92,9 +92,24 @@ __device__ __forceinline__ double exp2_neg(double s, const double* tab) {
   return (__double2hiint(s) >= 0x408FE000) ? 0.0 : r;
 }
 
-// Gaussian entry from a squared distance: exp(-d2/l^2) with c = log2(e)/l^2.
-__device__ __forceinline__ double gauss_from_d2(double d2, double c, const double* tab) {
-  return exp2_neg(d2 * c, tab);
+#define AFN_SQRT3 0x1.bb67ae8584caap+0
+
+// Kernel entry from a squared distance d2 = ||x - y||^2:
+//   kind 0, Gaussian      exp(-d2 / l^2)                     c = log2(e) / l^2
+//   kind 1, Matern-3/2    (1 + t) exp(-t),  t = sqrt(3 d2)/l  c = sqrt(3) / l
+struct KernelFn {
+  int kind;
+  double c;
+};
+__host__ __device__ inline KernelFn kernel_fn(int kind, double l) {
+  return kind == 1 ? KernelFn{1, AFN_SQRT3 / l} : KernelFn{0, AFN_LOG2E / (l * l)};
+}
+__device__ __forceinline__ double kern_from_d2(KernelFn f, double d2, const double* tab) {
+  if (f.kind == 1) {
+    const double t = sqrt(d2) * f.c;
+    return (1.0 + t) * exp2_neg(t * AFN_LOG2E, tab);
+  }
+  return exp2_neg(d2 * f.c, tab);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,12 @@ namespace afn {
 
 using Comm = afn_comm_s;
 
+// kernel function and length-scale l; kind = AFN_KERNEL_*
+struct Kern {
+  int kind = 0;
+  double l = 1.0;
+};
+
 // Rows of the permuted order owned by one rank: a block of
 // the landmark rows [a0, a0+na) and a block of the non-landmark rows
 // [b0, b0+nb).  Row t of the rank's local numbering is phys(t).  With one
@@ -69,10 +75,10 @@ struct KmvPlan {
 };
 KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms);
 // Xs = X * sqrt(log2 e)/l   (n x d)
-afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs, cudaStream_t st);
+afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st);
 // rows `rows` of (K + mu I) v (v: all n entries); partial: chunks*rows.size() doubles.
 // y_phys: y[rows.phys(t)] (true) or y[t] (false) receives row t.
-afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, Seg2 rows,
+afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double* v, double mu, Seg2 rows,
                       double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st);
 
 // ---- FPS (fps.cu) ---------------------------------------------------------
@@ -90,24 +96,26 @@ afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, i
 afn_status gather_rows(const double* X, int64_t n, int d, const int64_t* perm, double* Y,
                        cudaStream_t st);
 // A = K(X1, X1) + mu I, full k x k row-major
-afn_status gen_k11(const double* X1, int64_t k, int d, double l, double mu, double* A,
+afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, double* A,
                    cudaStream_t st);
 // in-place lower Cholesky of the k x k row-major A (upper triangle zeroed);
 // *d_info = 0 on success, else 1 + the failing row.
 afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st);
 // W (N x k row-major) = K(Xr, X1) L^{-T}  (i.e. L W^T = K12), K tiles on the fly
 afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
-                  double l, double* W, cudaStream_t st);
+                  Kern kn, double* W, cudaStream_t st);
 // W (N x k) = K(Xr, X1) L^{-T} as a GEMM with the explicit L^{-T}
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
-                  double l, double* W, cudaStream_t st);
+                  Kern kn, double* W, cudaStream_t st);
+// G = F^T F (C x C, full) for F: R x C row-major; deterministic
+afn_status syrk_ata(const double* F, int64_t R, int64_t C, double* G, cudaStream_t st);
 // LinvT (k x k row-major) = L^{-T} (upper triangular)
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st);
 
 // ---- FSAI (fsai.cu) -------------------------------------------------------
 // G values of rows [row_lo, row_hi) on the pattern of the Schur complement
 // S = K22 + mu I - W W^T (W: all N rows)
-afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
+afn_status fsai_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                     int64_t k, const int64_t* row_ptr, const int32_t* col, int64_t row_lo,
                     int64_t row_hi, double* gval, int* d_info, cudaStream_t st);
 // CSR transpose (N x N, columns sorted within each output row).  val/tval may
@@ -118,7 +126,7 @@ afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* va
 afn_status gather_map(const double* v, const int64_t* map, int64_t nnz, double* out, cudaStream_t st);
 // FSAI through the union of needed Schur-complement pairs (fsai_sddmm.cu).
 // Returns AFN_ERR_STATE (nothing written) if a group's pair union overflows.
-afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
+afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval,
                           int* d_info, cudaStream_t st);
@@ -152,10 +160,14 @@ afn_status pcg_update_p(double* p, const double* z, Seg2 g, const double* sc, in
                         int rz_old_slot, cudaStream_t st);
 afn_status vec_copy(double* y, const double* x, Seg2 g, cudaStream_t st);
 afn_status vec_axpby(double* y, double a, const double* x, double b, Seg2 g, cudaStream_t st);
+// y = a x over g
+afn_status vec_scale(double* y, double a, const double* x, Seg2 g, cudaStream_t st);
+// A[i][i] += v (k x k row-major)
+afn_status add_diag(double* A, int64_t k, double v, cudaStream_t st);
 // sc[slot] = sum_{s < R} part[s * stride + slot] (rank order) for each slot in mask
 afn_status combine_slots(const double* part, int R, int stride, unsigned mask, double* sc,
                          cudaStream_t st);
-// y[c] = base[c] - sum_{s < R} part[s * C + c] (rank order), c < C
+// y[c] = base[c] - sum_{s < R} part[s * C + c] (rank order), c < C; base may be null (0)
 afn_status combine_sub(const double* part, int R, int64_t C, const double* base, double* y,
                        cudaStream_t st);
 
@@ -166,7 +178,9 @@ struct Alg1Result {
   double scale = 0.0;
 };
 int alg1_default_m(int64_t n);
-afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t rng_seed,
+// k uniform random landmarks (reading R29), key order
+afn_status uniform_landmarks(int64_t n, int64_t k, uint64_t seed, int64_t* idx, cudaStream_t st);
+afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t rng_seed,
                     int k_threshold, Alg1Result* res, cudaStream_t st);
 
 // ---- probes (probe.cu) -----------------------------------------------------

@@ -56,6 +56,50 @@ __global__ void cand_kernel(int64_t n, uint64_t seed, uint64_t thr, unsigned lon
   }
 }
 
+// candidates below thr into (keys, ids) up to cap (uniform landmark selection)
+__global__ void cand_cap_kernel(int64_t n, uint64_t seed, uint64_t thr, int64_t cap,
+                                unsigned long long* keys, long long* ids, unsigned long long* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h = splitmix64_dev(seed ^ ((uint64_t)i * 0x9E3779B97F4A7C15ULL));
+  if (h < thr) {
+    const unsigned long long p = atomicAdd(cnt, 1ULL);
+    if ((int64_t)p < cap) {
+      keys[p] = h;
+      ids[p] = i;
+    }
+  }
+}
+
+// one-CTA bitonic sort of P (power of two) (key, id) pairs in global memory,
+// padding beyond the count with ~0; writes the first k ids
+__global__ void __launch_bounds__(AT) bitonic_global_kernel(unsigned long long* keys, long long* ids,
+                                                            const unsigned long long* cnt, int64_t P,
+                                                            int64_t k, int64_t* out) {
+  const int64_t c = (int64_t)min(*cnt, (unsigned long long)P);
+  for (int64_t t = c + threadIdx.x; t < P; t += AT) {
+    keys[t] = ~0ULL;
+    ids[t] = -1;
+  }
+  __syncthreads();
+  for (int64_t kk = 2; kk <= P; kk <<= 1)
+    for (int64_t j = kk >> 1; j > 0; j >>= 1) {
+      for (int64_t t = threadIdx.x; t < P; t += AT) {
+        const int64_t p = t ^ j;
+        if (p > t) {
+          const bool up = (t & kk) == 0;
+          const unsigned long long a = keys[t], b = keys[p];
+          if ((a > b) == up) {
+            keys[t] = b; keys[p] = a;
+            const long long x = ids[t]; ids[t] = ids[p]; ids[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (int64_t t = threadIdx.x; t < k; t += AT) out[t] = ids[t];
+}
+
 // sort the candidates by key (unique), write the first m ids
 __global__ void __launch_bounds__(AT) cand_sort_kernel(const unsigned long long* keys, const long long* ids,
                                                        const unsigned* cnt, int m, int64_t* out) {
@@ -316,12 +360,55 @@ afn_status launch_tridiag(double* A, int m, double* dgl, double* off, cudaStream
   return AFN_OK;
 }
 
+// Uniform random landmarks (reading R29): the k indices with the
+// smallest splitmix64 keys h_i = splitmix64(seed ^ i*golden), in key order.
+afn_status uniform_landmarks(int64_t n, int64_t k, uint64_t seed, int64_t* idx, cudaStream_t st) {
+  if (k < 1 || k > n || k > (1LL << 22)) {
+    set_error("uniform landmarks: need 1 <= k <= min(n, 2^22)");
+    return AFN_ERR_ARG;
+  }
+  int64_t P = 1024;
+  while (P < k + 8 * (int64_t)std::sqrt((double)k) + 64) P <<= 1;
+  P = std::min<int64_t>(P << 1, 1LL << 23);  // slack for the threshold search
+  unsigned long long *keys = nullptr, *cnt = nullptr;
+  long long* ids = nullptr;
+  afn_status s = dalloc((void**)&keys, sizeof(unsigned long long) * P, st);
+  if (s == AFN_OK) s = dalloc((void**)&ids, sizeof(long long) * P, st);
+  if (s == AFN_OK) s = dalloc((void**)&cnt, sizeof(unsigned long long), st);
+  struct Free {
+    void* p[3];
+    cudaStream_t st;
+    ~Free() { for (void* q : p) dfree(q, st); }
+  } fr{{keys, ids, cnt}, st};
+  if (s != AFN_OK) return s;
+  long double frac = std::min<long double>(1.0L, ((long double)k + 4.0L * std::sqrt((long double)k) + 32.0L) / n);
+  for (int attempt = 0;; ++attempt) {
+    const long double tl = frac * 18446744073709551616.0L;
+    const uint64_t thr = (frac >= 1.0L || tl >= 18446744073709551615.0L) ? ~0ULL : (uint64_t)tl;
+    AFN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), st));
+    cand_cap_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, seed, thr, P, keys, ids, cnt);
+    AFN_LAUNCH_CHECK("cand_cap_kernel");
+    unsigned long long hc = 0;
+    AFN_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    if ((int64_t)hc >= k && (int64_t)hc <= P) break;
+    if (attempt > 200 || (thr == ~0ULL && (int64_t)hc < k)) {
+      set_error("uniform landmarks: selection failed");
+      return AFN_ERR_CUDA;
+    }
+    frac = (int64_t)hc < k ? std::min<long double>(1.0L, frac * 1.25L) : frac * 0.8L;
+  }
+  bitonic_global_kernel<<<1, AT, 0, st>>>(keys, ids, cnt, P, k, idx);
+  AFN_LAUNCH_CHECK("bitonic_global_kernel");
+  return AFN_OK;
+}
+
 int alg1_default_m(int64_t n) {
   int64_t m = std::min<int64_t>(500, std::max<int64_t>(100, n / 100));
   return (int)std::min<int64_t>(m, n);
 }
 
-afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t rng_seed,
+afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t rng_seed,
                     int k_threshold, Alg1Result* res, cudaStream_t st) {
   if (m < 2 || m > 1024 || m > n) {
     set_error("alg1: need 2 <= m <= min(n, 1024) (m=%d)", m);
@@ -392,7 +479,7 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
   if ((s = get((void**)&pass, sizeof(int) * 2)) != AFN_OK) return s;
   gather_scale_kernel<<<(m * d + 255) / 256, 256, 0, st>>>(X, d, ids, m, scale, Xm, Xu);
   AFN_LAUNCH_CHECK("gather_scale_kernel");
-  if ((s = gen_k11(Xm, m, d, l, 0.0, Km, st)) != AFN_OK) return s;
+  if ((s = gen_k11(Xm, m, d, kn, 0.0, Km, st)) != AFN_OK) return s;
   if ((s = fps_run(Xm, m, d, m, 0, ord, fill, st)) != AFN_OK) return s;
   permute_sym_kernel<<<(unsigned)((mm + 255) / 256), 256, 0, st>>>(Km, m, ord, Kp);
   AFN_LAUNCH_CHECK("permute_sym_kernel");
@@ -448,7 +535,7 @@ afn_status alg1_run(const double* X, int64_t n, int d, double l, int m, uint64_t
   int refined = 0;
   // ---- 4. refined branch: #{eig(K_m on unscaled points) > 0.1}
   if (khat < k_threshold) {
-    if ((s = gen_k11(Xu, m, d, l, 0.0, Wk, st)) != AFN_OK) return s;
+    if ((s = gen_k11(Xu, m, d, kn, 0.0, Wk, st)) != AFN_OK) return s;
     TRY_A(launch_tridiag(Wk, m, dgl, off, st));
     eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
     AFN_LAUNCH_CHECK("eig_summary_kernel");

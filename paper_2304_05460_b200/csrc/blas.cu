@@ -208,7 +208,21 @@ __global__ void combine_sub_kernel(const double* __restrict__ part, int R, int64
   if (c >= C) return;
   double s = 0.0;
   for (int q = 0; q < R; ++q) s += part[(int64_t)q * C + c];
-  y[c] = base[c] - s;
+  y[c] = (base ? base[c] : 0.0) - s;
+}
+
+__global__ void scale_kernel(double* __restrict__ y, double a, const double* __restrict__ x, Seg2 g) {
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = g.phys(t);
+    y[i] = a * x[i];
+  }
+}
+
+__global__ void add_diag_kernel(double* __restrict__ A, int64_t k, double v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < k) A[i * k + i] += v;
 }
 
 unsigned grid_for(int64_t n, int nt, int cap) {
@@ -307,6 +321,20 @@ afn_status vec_axpby(double* y, double a, const double* x, double b, Seg2 g, cud
   if (g.size() <= 0) return AFN_OK;
   axpby_kernel<<<grid_for(g.size(), 256, 1184), 256, 0, st>>>(y, a, x, b, g);
   AFN_LAUNCH_CHECK("axpby_kernel");
+  return AFN_OK;
+}
+
+afn_status vec_scale(double* y, double a, const double* x, Seg2 g, cudaStream_t st) {
+  if (g.size() <= 0) return AFN_OK;
+  scale_kernel<<<grid_for(g.size(), 256, 1184), 256, 0, st>>>(y, a, x, g);
+  AFN_LAUNCH_CHECK("scale_kernel");
+  return AFN_OK;
+}
+
+afn_status add_diag(double* A, int64_t k, double v, cudaStream_t st) {
+  if (k <= 0) return AFN_OK;
+  add_diag_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(A, k, v);
+  AFN_LAUNCH_CHECK("add_diag_kernel");
   return AFN_OK;
 }
 

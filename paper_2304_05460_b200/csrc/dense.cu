@@ -33,7 +33,7 @@ __global__ void gather_rows_kernel(const double* __restrict__ X, int64_t n, int 
 }
 
 // A = K(X1, X1) + mu I  (full)
-__global__ void gen_k11_kernel(const double* __restrict__ X1, int64_t k, int d, double cl,
+__global__ void gen_k11_kernel(const double* __restrict__ X1, int64_t k, int d, KernelFn kf,
                                double mu, double* __restrict__ A) {
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   load_exp2_tab(s_tab);
@@ -46,7 +46,7 @@ __global__ void gen_k11_kernel(const double* __restrict__ X1, int64_t k, int d, 
     v = 1.0 + mu;
   } else {
     const double s = d2_exact_rt(&X1[i * d], &X1[j * d], d);
-    v = gauss_from_d2(s, cl, s_tab);
+    v = kern_from_d2(kf, s, s_tab);
   }
   A[e] = v;
 }
@@ -220,7 +220,7 @@ template <int MODE>
 __global__ void __launch_bounds__(DT) trsm_rows_kernel(const double* __restrict__ L, int64_t k,
                                                        const double* __restrict__ X1,
                                                        const double* __restrict__ Xr, int64_t N,
-                                                       int d, double cl, double* __restrict__ W) {
+                                                       int d, KernelFn kf, double* __restrict__ W) {
   extern __shared__ double dsm[];
   double* sA = dsm;            // [kk][row]: W tile, later T [row][col]
   double* sB = dsm + NB * TP;  // [kk][col]: L tile, later Lbb [row][col]
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(DT) trsm_rows_kernel(const double* __restrict_
         if (r < N && c < k) {
           if (MODE == 0) {
             const double s = d2_exact_rt(&Xr[r * d], &X1[c * d], d);
-            v = gauss_from_d2(s, cl, s_tab);
+            v = kern_from_d2(kf, s, s_tab);
           } else {
             v = (r == c) ? 1.0 : 0.0;
           }
@@ -346,7 +346,7 @@ __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
 }
 
 __global__ void gen_k21_kernel(const double* __restrict__ X1, int64_t k, const double* __restrict__ Xr,
-                               int64_t N, int d, double cl, double* __restrict__ Kb) {
+                               int64_t N, int d, KernelFn kf, double* __restrict__ Kb) {
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   load_exp2_tab(s_tab);
   __syncthreads();
@@ -354,7 +354,7 @@ __global__ void gen_k21_kernel(const double* __restrict__ X1, int64_t k, const d
   if (e >= N * k) return;
   const int64_t r = e / k, c = e - r * k;
   const double sd = d2_exact_rt(&Xr[r * d], &X1[c * d], d);
-  Kb[e] = gauss_from_d2(sd, cl, s_tab);
+  Kb[e] = kern_from_d2(kf, sd, s_tab);
 }
 
 // C (M x N) = A (M x K) * B (K x N), B upper triangular (rows t <= col used)
@@ -569,7 +569,89 @@ __global__ void zero_upper_kernel(double* __restrict__ A, int64_t k) {
   if (j > i) A[e] = 0.0;
 }
 
+// ---- G = F^T F (Nystrom branch Gram, SYRK): 32x32 lower tiles of G, row
+// chunks of F in parallel, partials summed in chunk order (deterministic)
+constexpr int ST = 32;
+__global__ void __launch_bounds__(256) syrk_partial_kernel(const double* __restrict__ F, int64_t R, int64_t C,
+                                                           int64_t rows_per_chunk, double* __restrict__ part) {
+  __shared__ double sa[ST][ST + 1], sb[ST][ST + 1];
+  const int64_t tile = blockIdx.x, chunk = blockIdx.y;
+  int I = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+  while ((int64_t)I * (I + 1) / 2 > tile) --I;
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
+  const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t r0 = chunk * rows_per_chunk, r1 = min(R, r0 + rows_per_chunk);
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int64_t rb = r0; rb < r1; rb += ST) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < ST * ST; e += 256) {
+      const int rr = e / ST, c = e - rr * ST;
+      const int64_t r = rb + rr;
+      const int64_t ci = (int64_t)I * ST + c, cj = (int64_t)J * ST + c;
+      sa[rr][c] = (r < r1 && ci < C) ? F[r * C + ci] : 0.0;
+      sb[rr][c] = (r < r1 && cj < C) ? F[r * C + cj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < ST; ++rr) {
+      const double a0 = sa[rr][ty], a1 = sa[rr][ty + 16];
+      const double b0 = sb[rr][tx], b1 = sb[rr][tx + 16];
+      acc[0][0] = fma(a0, b0, acc[0][0]);
+      acc[0][1] = fma(a0, b1, acc[0][1]);
+      acc[1][0] = fma(a1, b0, acc[1][0]);
+      acc[1][1] = fma(a1, b1, acc[1][1]);
+    }
+  }
+  double* P = part + (chunk * gridDim.x + tile) * (ST * ST);
+  P[ty * ST + tx] = acc[0][0];
+  P[ty * ST + tx + 16] = acc[0][1];
+  P[(ty + 16) * ST + tx] = acc[1][0];
+  P[(ty + 16) * ST + tx + 16] = acc[1][1];
+}
+
+__global__ void syrk_reduce_kernel(const double* __restrict__ part, int64_t ntile, int64_t nchunk, int64_t C,
+                                   double* __restrict__ G) {
+  const int64_t tile = blockIdx.x;
+  int I = (int)((sqrt(8.0 * (double)tile + 1.0) - 1.0) * 0.5);
+  while ((int64_t)I * (I + 1) / 2 > tile) --I;
+  while ((int64_t)(I + 1) * (I + 2) / 2 <= tile) ++I;
+  const int J = (int)(tile - (int64_t)I * (I + 1) / 2);
+  for (int e = threadIdx.x; e < ST * ST; e += blockDim.x) {
+    const int a = e / ST, b = e - a * ST;
+    const int64_t i = (int64_t)I * ST + a, j = (int64_t)J * ST + b;
+    if (i >= C || j >= C) continue;
+    double s = 0.0;
+    for (int64_t c = 0; c < nchunk; ++c) s += part[(c * ntile + tile) * (ST * ST) + e];
+    G[i * C + j] = s;
+    G[j * C + i] = s;
+  }
+}
+
 }  // namespace
+
+afn_status syrk_ata(const double* F, int64_t R, int64_t C, double* G, cudaStream_t st) {
+  if (C <= 0) return AFN_OK;
+  const int64_t T = (C + ST - 1) / ST;
+  const int64_t ntile = T * (T + 1) / 2;
+  int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>((R + 2047) / 2048, std::max<int64_t>(1, 32768 / ntile)));
+  const int64_t rpc = (R + nchunk - 1) / nchunk;
+  nchunk = std::max<int64_t>(1, (R + rpc - 1) / rpc);
+  double* part = nullptr;
+  afn_status s = dalloc((void**)&part, sizeof(double) * nchunk * ntile * ST * ST, st);
+  if (s != AFN_OK) return s;
+  syrk_partial_kernel<<<dim3((unsigned)ntile, (unsigned)nchunk), 256, 0, st>>>(F, R, C, rpc, part);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    note_launch();
+    syrk_reduce_kernel<<<(unsigned)ntile, 256, 0, st>>>(part, ntile, nchunk, C, G);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) note_launch();
+  }
+  dfree(part, st);
+  if (e != cudaSuccess) return cuda_status(e, "syrk kernels");
+  return AFN_OK;
+}
 
 afn_status gather_rows(const double* X, int64_t n, int d, const int64_t* perm, double* Y,
                        cudaStream_t st) {
@@ -580,11 +662,11 @@ afn_status gather_rows(const double* X, int64_t n, int d, const int64_t* perm, d
   return AFN_OK;
 }
 
-afn_status gen_k11(const double* X1, int64_t k, int d, double l, double mu, double* A,
+afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, double* A,
                    cudaStream_t st) {
   const int64_t tot = k * k;
-  const double cl = AFN_LOG2E / (l * l);
-  gen_k11_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(X1, k, d, cl, mu, A);
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
+  gen_k11_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(X1, k, d, kf, mu, A);
   AFN_LAUNCH_CHECK("gen_k11_kernel");
   return AFN_OK;
 }
@@ -609,23 +691,23 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
 }
 
 afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
-                  double l, double* W, cudaStream_t st) {
+                  Kern kn, double* W, cudaStream_t st) {
   if (N <= 0 || k <= 0) return AFN_OK;
   TRY_SMEM();
-  const double cl = AFN_LOG2E / (l * l);
-  trsm_rows_kernel<0><<<(unsigned)((N + NB - 1) / NB), DT, SMEM2, st>>>(L, k, X1, Xr, N, d, cl, W);
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
+  trsm_rows_kernel<0><<<(unsigned)((N + NB - 1) / NB), DT, SMEM2, st>>>(L, k, X1, Xr, N, d, kf, W);
   AFN_LAUNCH_CHECK("trsm_rows_kernel<0>");
   return AFN_OK;
 }
 
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
-                  double l, double* W, cudaStream_t st) {
+                  Kern kn, double* W, cudaStream_t st) {
   if (N <= 0 || k <= 0) return AFN_OK;
-  const double cl = AFN_LOG2E / (l * l);
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
   double* Kb = nullptr;
   afn_status s = dalloc((void**)&Kb, sizeof(double) * N * k, st);
   if (s != AFN_OK) return s;
-  gen_k21_kernel<<<(unsigned)((N * k + 255) / 256), 256, 0, st>>>(X1, k, Xr, N, d, cl, Kb);
+  gen_k21_kernel<<<(unsigned)((N * k + 255) / 256), 256, 0, st>>>(X1, k, Xr, N, d, kf, Kb);
   AFN_LAUNCH_CHECK("gen_k21_kernel");
   static bool attr = false;
   const int bytes = (int)(sizeof(double) * 2 * GK * (GPA + GPB));
@@ -687,7 +769,7 @@ afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st
   }
   TRY_SMEM();
   trsm_rows_kernel<1><<<(unsigned)((k + NB - 1) / NB), DT, SMEM2, st>>>(L, k, nullptr, nullptr, k, 1,
-                                                                   0.0, LinvT);
+                                                                   KernelFn{0, 0.0}, LinvT);
   AFN_LAUNCH_CHECK("trsm_rows_kernel<1>");
   return AFN_OK;
 }

@@ -50,7 +50,7 @@ __device__ __forceinline__ int cmo(int a, int t, int wp) { return t * wp - (t * 
 // stalling a 256-thread CTA with two barriers per column.
 template <int MT>
 __global__ void __launch_bounds__(FT, 2)
-fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, double cl, double mu,
+fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, KernelFn kf, double mu,
                  const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
                  const int32_t* __restrict__ col, double* __restrict__ Sg) {
   constexpr int WP = MT * 16;
@@ -139,7 +139,7 @@ fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, double cl, do
           kv = 1.0 + mu;
         } else {
           const double sd = d2_exact_rt(&sX[a * d], &sX[b * d], d);
-          kv = gauss_from_d2(sd, cl, s_tab);
+          kv = kern_from_d2(kf, sd, s_tab);
         }
         S[cmo(a, b, wp)] = kv - acc[t];
       }
@@ -238,7 +238,7 @@ fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict_
 }
 
 template <int MT>
-afn_status launch_fsai_split(const double* X2, int64_t row_lo, int64_t row_hi, int d, double cl, double mu,
+afn_status launch_fsai_split(const double* X2, int64_t row_lo, int64_t row_hi, int d, KernelFn kf, double mu,
                              const double* W, int64_t k, const int64_t* rp, const int32_t* col,
                              double* gval, int* info, cudaStream_t st) {
   constexpr int WP = MT * 16;
@@ -256,7 +256,7 @@ afn_status launch_fsai_split(const double* X2, int64_t row_lo, int64_t row_hi, i
   if (s != AFN_OK) return s;
   for (int64_t r0 = row_lo; r0 < row_hi; r0 += batch) {
     const int64_t nr = std::min(batch, row_hi - r0);
-    kg<<<(unsigned)nr, FT, bytes, st>>>(X2, r0, d, cl, mu, W, k, rp, col, Sg);
+    kg<<<(unsigned)nr, FT, bytes, st>>>(X2, r0, d, kf, mu, W, k, rp, col, Sg);
     AFN_LAUNCH_CHECK("fsai_gram_kernel");
     afn_status cs = fsai_chol_batch(r0, nr, MT, rp, Sg, gval, info, st);
     if (cs != AFN_OK) { dfree(Sg, st); return cs; }
@@ -371,7 +371,7 @@ afn_status fsai_chol_batch(int64_t r0, int64_t nrows, int MT, const int64_t* rp,
   }
 }
 
-afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
+afn_status fsai_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                     int64_t k, const int64_t* rp, const int32_t* col, int64_t row_lo, int64_t row_hi,
                     double* gval, int* d_info, cudaStream_t st) {
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
@@ -387,17 +387,17 @@ afn_status fsai_run(const double* X2, int64_t N, int d, double l, double mu, con
     w = (int)(N > 1 ? (h[1] - h[0]) : h[0]);
     if (N == 1) w = 1;
   }
-  const double cl = AFN_LOG2E / (l * l);
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
   const int MT = (w + 15) / 16;
   switch (MT) {
-    case 1: return launch_fsai_split<1>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 2: return launch_fsai_split<2>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 3: return launch_fsai_split<3>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 4: return launch_fsai_split<4>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 5: return launch_fsai_split<5>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 6: return launch_fsai_split<6>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 7: return launch_fsai_split<7>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
-    case 8: return launch_fsai_split<8>(X2, row_lo, row_hi, d, cl, mu, W, k, rp, col, gval, d_info, st);
+    case 1: return launch_fsai_split<1>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 2: return launch_fsai_split<2>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 3: return launch_fsai_split<3>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 4: return launch_fsai_split<4>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 5: return launch_fsai_split<5>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 6: return launch_fsai_split<6>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 7: return launch_fsai_split<7>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
+    case 8: return launch_fsai_split<8>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
     default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
   }
 }

@@ -402,7 +402,7 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
 template <int MT>
 __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
                                                          int64_t row_hi, const double* __restrict__ X2, int d,
-                                                         double cl, double mu, const int64_t* __restrict__ rp,
+                                                         KernelFn kf, double mu, const int64_t* __restrict__ rp,
                                                          const int32_t* __restrict__ col,
                                                          const int* __restrict__ grp, const int* __restrict__ loc,
                                                          const int* __restrict__ Ucount,
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
           kv = 1.0 + mu;
         } else {
           const double sd = d2_exact_rt(&sX[p * d], &sX[q * d], d);
-          kv = gauss_from_d2(sd, cl, s_tab);
+          kv = kern_from_d2(kf, sd, s_tab);
         }
         Lm[s_off[p] + q] = kv - gram[t];
       }
@@ -618,7 +618,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
 
 template <int MT>
 afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t row_hi, cudaStream_t st,
-                         const double* X2, int d, double cl, double mu, const int64_t* rp, const int32_t* col,
+                         const double* X2, int d, KernelFn kf, double mu, const int64_t* rp, const int32_t* col,
                          const int* grp, const int* loc, const int* Ucount, const int2* Htab,
                          const int64_t* Doff, const double* D, double* gval, int* info) {
   constexpr int WP = MT * 16;
@@ -627,7 +627,7 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
   AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   for (int64_t r0 = 0; r0 < N; r0 += 1 << 30) {
     const int64_t nr = std::min<int64_t>(N - r0, 1 << 30);
-    kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, cl, mu, rp, col, grp, loc,
+    kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, kf, mu, rp, col, grp, loc,
                                           Ucount, Htab, Doff, D, gval, info);
     AFN_LAUNCH_CHECK("fsai_factor_kernel");
   }
@@ -636,7 +636,7 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
 
 }  // namespace
 
-afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double mu, const double* W,
+afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval, int* d_info,
                           cudaStream_t st) {
@@ -777,14 +777,14 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, double l, double m
   }
   // ---- 4. per-row assembly + Cholesky + g (one CTA per row, rows in the
   // spatial order sorder; CTAs of other ranks' rows exit at once)
-  const double cl = AFN_LOG2E / (l * l);
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
   const int64_t NR = row_hi - row_lo;
   kt_begin(KT_FSAI_CHOL, st);
   switch (MT) {
 #define AFN_FACTOR(M) \
-    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, st, X2, d, cl, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
     AFN_FACTOR(1) AFN_FACTOR(2) AFN_FACTOR(3) AFN_FACTOR(4) AFN_FACTOR(5) AFN_FACTOR(6) AFN_FACTOR(7)
-    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, st, X2, d, cl, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
 #undef AFN_FACTOR
   }
   if (s != AFN_OK) return s;

@@ -32,7 +32,10 @@ struct KmvTraits {
   static constexpr int RB = D <= 4 ? 4 : (D <= 8 ? 2 : 1);  // rows per thread
 };
 
-template <int D, int RB>
+// KER 0 (Gaussian): Xs = X sqrt(log2 e)/l, K = 2^(-|xs_i - xs_j|^2).
+// KER 1 (Matern-3/2): Xs = X sqrt(3)/l, t = |xs_i - xs_j|,
+//        K = (1 + t) 2^(-t log2 e).
+template <int D, int RB, int KER>
 __global__ void __launch_bounds__(KMV_NT, 2)
 kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int64_t n,
                    Seg2 rows, int64_t chunk_cols, double* __restrict__ partial) {
@@ -90,7 +93,12 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
           dd = xi[t][c] - xj[c];
           s = fma(dd, dd, s);
         }
-        acc[t] = fma(exp2_neg(s, s_tab), vj, acc[t]);
+        if (KER == 1) {
+          const double tt = sqrt(s);
+          acc[t] = fma((1.0 + tt) * exp2_neg(tt * AFN_LOG2E, s_tab), vj, acc[t]);
+        } else {
+          acc[t] = fma(exp2_neg(s, s_tab), vj, acc[t]);
+        }
       }
     }
   }
@@ -121,11 +129,12 @@ __global__ void prescale_kernel(const double* __restrict__ X, int64_t n, int d, 
 
 template <int D>
 void launch_partial(const KmvPlan& p, cudaStream_t st, const double* Xs, const double* v, int64_t n,
-                    Seg2 rows, double* partial) {
+                    Seg2 rows, double* partial, int kind) {
   constexpr int RB = KmvTraits<D>::RB;
   const int64_t rows_per_cta = (int64_t)KMV_NT * RB;
   dim3 grid((unsigned)((rows.size() + rows_per_cta - 1) / rows_per_cta), (unsigned)p.chunks);
-  kmv_partial_kernel<D, RB><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial);
+  if (kind == 1) kmv_partial_kernel<D, RB, 1><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial);
+  else kmv_partial_kernel<D, RB, 0><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial);
 }
 
 int rows_per_thread(int d) { return d <= 4 ? 4 : (d <= 8 ? 2 : 1); }
@@ -173,8 +182,8 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
   return plan_for(n, nrows, d, num_sms);
 }
 
-afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs, cudaStream_t st) {
-  const double f = AFN_SQRT_LOG2E / l;
+afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st) {
+  const double f = kn.kind == 1 ? AFN_SQRT3 / kn.l : AFN_SQRT_LOG2E / kn.l;
   const int64_t total = n * (int64_t)d;
   const int nt = 256;
   prescale_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(X, n, d, f, Xs);
@@ -182,27 +191,27 @@ afn_status kmv_prescale(const double* X, int64_t n, int d, double l, double* Xs,
   return AFN_OK;
 }
 
-afn_status kmv_launch(const double* Xs, int64_t n, int d, const double* v, double mu, Seg2 rows,
+afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double* v, double mu, Seg2 rows,
                       double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st) {
   const int64_t nrows = rows.size();
   if (nrows <= 0) return AFN_OK;
   switch (d) {
-    case 1: launch_partial<1>(p, st, Xs, v, n, rows, partial); break;
-    case 2: launch_partial<2>(p, st, Xs, v, n, rows, partial); break;
-    case 3: launch_partial<3>(p, st, Xs, v, n, rows, partial); break;
-    case 4: launch_partial<4>(p, st, Xs, v, n, rows, partial); break;
-    case 5: launch_partial<5>(p, st, Xs, v, n, rows, partial); break;
-    case 6: launch_partial<6>(p, st, Xs, v, n, rows, partial); break;
-    case 7: launch_partial<7>(p, st, Xs, v, n, rows, partial); break;
-    case 8: launch_partial<8>(p, st, Xs, v, n, rows, partial); break;
-    case 9: launch_partial<9>(p, st, Xs, v, n, rows, partial); break;
-    case 10: launch_partial<10>(p, st, Xs, v, n, rows, partial); break;
-    case 11: launch_partial<11>(p, st, Xs, v, n, rows, partial); break;
-    case 12: launch_partial<12>(p, st, Xs, v, n, rows, partial); break;
-    case 13: launch_partial<13>(p, st, Xs, v, n, rows, partial); break;
-    case 14: launch_partial<14>(p, st, Xs, v, n, rows, partial); break;
-    case 15: launch_partial<15>(p, st, Xs, v, n, rows, partial); break;
-    case 16: launch_partial<16>(p, st, Xs, v, n, rows, partial); break;
+    case 1: launch_partial<1>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 2: launch_partial<2>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 3: launch_partial<3>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 4: launch_partial<4>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 5: launch_partial<5>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 6: launch_partial<6>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 7: launch_partial<7>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 8: launch_partial<8>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 9: launch_partial<9>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 10: launch_partial<10>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 11: launch_partial<11>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 12: launch_partial<12>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 13: launch_partial<13>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 14: launch_partial<14>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 15: launch_partial<15>(p, st, Xs, v, n, rows, partial, kind); break;
+    case 16: launch_partial<16>(p, st, Xs, v, n, rows, partial, kind); break;
     default: set_error("kernel_matvec: d=%d unsupported (1..16)", d); return AFN_ERR_ARG;
   }
   AFN_LAUNCH_CHECK("kmv_partial_kernel");

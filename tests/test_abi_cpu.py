@@ -49,10 +49,10 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_struct_layout(lib):
     import ctypes as C
-    assert lib.abi_version() == 2
-    # afn_params: 2 doubles, int64, 4 int32, int64, uint64 = 56 bytes
-    assert C.sizeof(lib.Params) == 56
-    assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4
+    assert lib.abi_version() == 3
+    # afn_params: 2 doubles, int64, 4 int32, int64, uint64, 4 int32 = 72 bytes
+    assert C.sizeof(lib.Params) == 72
+    assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4 + 4 * 2
     assert C.sizeof(lib.Report) == 4 * 4 + 8 * 6 + 8
 
 
@@ -62,12 +62,12 @@ def test_host_pointers_are_rejected_without_compute(lib):
     X = np.zeros((4, 3))
     v = np.zeros(4)
     y = np.zeros(4)
-    st = lib._lib.kernel_matvec(X.ctypes.data_as(C.c_void_p), 4, 3, 1.0, 1e-4,
+    st = lib._lib.kernel_matvec(X.ctypes.data_as(C.c_void_p), 4, 3, 0, 1.0, 1e-4,
                                 v.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), None)
     assert st == 1  # AFN_ERR_ARG
     assert b"device pointer" in lib._lib.afn_last_error()
     # bad sizes are rejected first
-    st = lib._lib.kernel_matvec(None, 0, 3, 1.0, 1e-4, None, None, None)
+    st = lib._lib.kernel_matvec(None, 0, 3, 0, 1.0, 1e-4, None, None, None)
     assert st == 1
     h = C.c_void_p()
     p = lib.make_params(1.0, 1e-4, 10, 500)  # w > 128
