@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mode", default="sweep", choices=["sweep", "dist"],
+                    help="sweep: the C2 l-sweep, problems split over ranks (default); "
+                         "dist: every rank solves the same problem row-sharded (SURVEY 8(e))")
     return ap.parse_args()
 
 
@@ -220,10 +223,97 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def run_dist(args):
+    """--mode dist: one AFN-PCG problem per step, rows sharded over all ranks
+    (one GPU each, NCCL all-gathers; include/afn.h "Multi-GPU").  Strong
+    scaling: the total work is fixed as N grows."""
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import __graft_entry__ as ge
+    ge._build_module().build()
+    import paper_2304_05460_b200 as afn
+    from synth import CONFIGS, gen_problem
+    cfg = CONFIGS[args.config]
+    X, b = gen_problem(cfg)
+    Xd, bd = torch.from_numpy(X).to(dev), torch.from_numpy(b).to(dev)
+    comm = afn.Comm.from_process_group(dist) if dist else None
+    recs = []
+
+    def step(record=False):
+        for l in cfg.ls:
+            h = afn.afn_build(Xd, afn.make_params(l, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True),
+                              comm=comm)
+            a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit)
+            if record:
+                recs.append((l, h.info(), rep))
+            h.close()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = afn.launch_count()
+    with sampler:
+        for s in range(args.steps):
+            evs[s][0].record(stream)
+            step(record=True)
+            evs[s][1].record(stream)
+        torch.cuda.synchronize()
+    launches = afn.launch_count() - l0
+    if dist:
+        dist.barrier()
+    t = torch.tensor([sum(a.elapsed_time(c) for a, c in evs)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    job_ms = float(t.item())
+    nsolve = args.steps * len(cfg.ls)
+    mv_ms = sum(r["matvec_ms"] for _, _, r in recs)
+    its = sum(r["iterations"] for _, _, r in recs)
+    if rank == 0:
+        inf, rep = recs[0][1], recs[0][2]
+        line = {"metric": METRIC, "value": job_ms / 1e3 / nsolve, "unit": "s/solve", "n_gpus": world,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": job_ms / args.steps,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, BASELINE configs)",
+                "config": {"workload": args.config, "n": cfg.n, "d": cfg.d, "ls": list(cfg.ls),
+                           "mu": cfg.mu, "k_cap": cfg.k_cap, "w": cfg.w, "tol": cfg.tol,
+                           "parallelism": f"rows sharded over {world} rank(s), points replicated",
+                           "l2": "inputs and working set (W) larger than L2"},
+                "kmv_gpairs_per_s": float(cfg.n) ** 2 * its / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None,
+                "per_solve": {"k": inf["k"], "khat": inf["khat"], "iters": rep["iterations"],
+                              "setup_ms": inf["ms_total"], "pcg_ms": rep["solve_ms"],
+                              "matvec_ms": rep["matvec_ms"], "apply_ms": rep["apply_ms"],
+                              "comm_ms": rep["comm_ms"], "relres_true": rep["relres_true"]},
+                "gpu_launches": launches, "clocks": sampler.summary()}
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "dist":
+        if args.config == "C2":
+            args.config = "C3"
+        return run_dist(args)
 
     import numpy as np
     import torch

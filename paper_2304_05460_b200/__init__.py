@@ -154,7 +154,7 @@ def _stream(stream=None):
 
 
 KT_NAMES = ("kmv_partial_kernel", "group_gemm_kernel", "fsai_assemble_kernel", "fsai_chol_kernel",
-            "fsai_gram_kernel", "fps_kernel", "gemm_nn_bupper_kernel", "trsm_rows_kernel<1>",
+            "fsai_gram_kernel", "fps_kernel", "gemm128_bupper_kernel", "trsm_rows_kernel<1>",
             "potrf", "knn_kernel", "apply", "alg1")
 
 

@@ -432,6 +432,130 @@ __global__ void __launch_bounds__(256, 2) gemm_nn_bupper_kernel(const double* __
 
 
 // -------------------------------------------------------------------------
+// C = A B with B upper triangular (B[t][c] = 0 for t > c): the W = K21 L^{-T}
+// product.  128 x 128 tiles, 256 threads with 8 x 8 register tiles
+// (rows ty*4 + {0..3, 64..67}, columns tx*4 + {0..3, 64..67}: every operand
+// read is an LDS.128 of two adjacent doubles pairs, A broadcast within the
+// warp, B conflict-free), BK = 16 double-buffered through cp.async (A
+// transposed into [kk][row] while staging).  FP64 SIMT: 64 DFMA per 8 LDS.128.
+constexpr int HM = 128, HN = 128, HK = 16, HPA = HM + 4, HPB = HN + 4;
+
+__global__ void __launch_bounds__(256, 1) gemm128_bupper_kernel(const double* __restrict__ A,
+                                                               const double* __restrict__ B,
+                                                               double* __restrict__ Cm, int64_t M,
+                                                               int64_t N, int64_t K) {
+  extern __shared__ __align__(16) double hsm[];
+  double* sA = hsm;                  // [2][HK][HPA]
+  double* sB = hsm + 2 * HK * HPA;   // [2][HK][HPB]
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const int64_t R0 = (int64_t)blockIdx.y * HM, C0 = (int64_t)blockIdx.x * HN;
+  const int64_t kend = min(K, C0 + HN);  // B[t][c] = 0 for t > c
+  const int64_t nkb = (kend + HK - 1) / HK;
+  auto stage = [&](int64_t kb, int buf) {
+    const int64_t k0 = kb * HK;
+    double* a = sA + buf * HK * HPA;
+    double* b = sB + buf * HK * HPB;
+#pragma unroll
+    for (int u = 0; u < (HM * HK) / 256; ++u) {  // A: 8 B copies, row r, k k0+kk
+      const int e = tid + 256 * u;
+      const int r = e / HK, kk = e - r * HK;
+      const int64_t gr = R0 + r, gk = k0 + kk;
+      if (gr < M && gk < kend) cpa8(&a[kk * HPA + r], &A[gr * K + gk]);
+      else a[kk * HPA + r] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < (HK * HN) / (2 * 256); ++u) {  // B: 16 B copies
+      const int e = tid + 256 * u;
+      const int kk = e / (HN / 2), c = 2 * (e - kk * (HN / 2));
+      const int64_t gk = k0 + kk, gc = C0 + c;
+      double* dst = &b[kk * HPB + c];
+      if (gk < kend && gc + 1 < N && (N & 1) == 0) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(&B[gk * N + gc]) : "memory");
+      } else {
+        dst[0] = (gk < kend && gc < N) ? B[gk * N + gc] : 0.0;
+        dst[1] = (gk < kend && gc + 1 < N) ? B[gk * N + gc + 1] : 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  if (nkb > 0) stage(0, 0);
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    const int buf = (int)(kb & 1);
+    if (kb + 1 < nkb) {
+      stage(kb + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* a = sA + buf * HK * HPA + ty * 4;
+    const double* b = sB + buf * HK * HPB + tx * 4;
+    // operands of step kk+1 are loaded while step kk's 64 DFMA run (the
+    // two CTA warps per scheduler cannot hide the LDS latency otherwise)
+    double2 ca[4], cb[4];
+    ca[0] = *reinterpret_cast<const double2*>(a);
+    ca[1] = *reinterpret_cast<const double2*>(a + 2);
+    ca[2] = *reinterpret_cast<const double2*>(a + 64);
+    ca[3] = *reinterpret_cast<const double2*>(a + 66);
+    cb[0] = *reinterpret_cast<const double2*>(b);
+    cb[1] = *reinterpret_cast<const double2*>(b + 2);
+    cb[2] = *reinterpret_cast<const double2*>(b + 64);
+    cb[3] = *reinterpret_cast<const double2*>(b + 66);
+#pragma unroll
+    for (int kk = 0; kk < HK; ++kk) {
+      double2 na[4], nb[4];
+      if (kk + 1 < HK) {
+        const double* an = a + (kk + 1) * HPA;
+        const double* bn = b + (kk + 1) * HPB;
+        na[0] = *reinterpret_cast<const double2*>(an);
+        na[1] = *reinterpret_cast<const double2*>(an + 2);
+        na[2] = *reinterpret_cast<const double2*>(an + 64);
+        na[3] = *reinterpret_cast<const double2*>(an + 66);
+        nb[0] = *reinterpret_cast<const double2*>(bn);
+        nb[1] = *reinterpret_cast<const double2*>(bn + 2);
+        nb[2] = *reinterpret_cast<const double2*>(bn + 64);
+        nb[3] = *reinterpret_cast<const double2*>(bn + 66);
+      }
+      const double av[8] = {ca[0].x, ca[0].y, ca[1].x, ca[1].y, ca[2].x, ca[2].y, ca[3].x, ca[3].y};
+      const double bv[8] = {cb[0].x, cb[0].y, cb[1].x, cb[1].y, cb[2].x, cb[2].y, cb[3].x, cb[3].y};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      if (kk + 1 < HK) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ca[q] = na[q];
+          cb[q] = nb[q];
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t r = R0 + ty * 4 + (i & 3) + (i >> 2) * 64;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      const int64_t c = C0 + tx * 4 + (j & 3) + (j >> 2) * 64;
+      if (c + 1 < N && (N & 1) == 0) {
+        *reinterpret_cast<double2*>(&Cm[r * N + c]) = make_double2(acc[i][j], acc[i][j + 1]);
+      } else {
+        if (c < N) Cm[r * N + c] = acc[i][j];
+        if (c + 1 < N) Cm[r * N + c + 1] = acc[i][j + 1];
+      }
+    }
+  }
+}
+
+// -------------------------------------------------------------------------
 // L^{-1} by recursive 2x2 block inversion on a power-of-two padding kp:
 //   inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 B A^-1, C^-1]]
 // 64x64 diagonal blocks first (in-smem triangular solves), then one batched
@@ -704,20 +828,37 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
                   Kern kn, double* W, cudaStream_t st) {
   if (N <= 0 || k <= 0) return AFN_OK;
   const KernelFn kf = kernel_fn(kn.kind, kn.l);
+  // K21 is generated in row blocks of <= ~1 GiB (not all N x k at once: at
+  // n = 2^20, k = 8000 that alone would be 66.6 GB)
+  const int64_t rb = std::max<int64_t>(HM, std::min<int64_t>(N, ((1LL << 27) / k) / HM * HM));
   double* Kb = nullptr;
-  afn_status s = dalloc((void**)&Kb, sizeof(double) * N * k, st);
+  afn_status s = dalloc((void**)&Kb, sizeof(double) * rb * k, st);
   if (s != AFN_OK) return s;
-  gen_k21_kernel<<<(unsigned)((N * k + 255) / 256), 256, 0, st>>>(X1, k, Xr, N, d, kf, Kb);
-  AFN_LAUNCH_CHECK("gen_k21_kernel");
+  static const bool legacy = getenv("AFN_W_GEMM64") != nullptr;
   static bool attr = false;
-  const int bytes = (int)(sizeof(double) * 2 * GK * (GPA + GPB));
   if (!attr) {
-    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 2 * GK * (GPA + GPB))));
+    AFN_CUDA(cudaFuncSetAttribute(gemm128_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 2 * HK * (HPA + HPB))));
     attr = true;
   }
-  dim3 grid((unsigned)((k + GN - 1) / GN), (unsigned)((N + GM - 1) / GM));
-  gemm_nn_bupper_kernel<<<grid, 256, bytes, st>>>(Kb, LinvT, W, N, k, k);
-  AFN_LAUNCH_CHECK("gemm_nn_bupper_kernel");
+  for (int64_t r0 = 0; r0 < N; r0 += rb) {
+    const int64_t nr = std::min(rb, N - r0);
+    gen_k21_kernel<<<(unsigned)((nr * k + 255) / 256), 256, 0, st>>>(X1, k, Xr + r0 * d, nr, d, kf, Kb);
+    AFN_LAUNCH_CHECK("gen_k21_kernel");
+    if (legacy) {
+      dim3 grid((unsigned)((k + GN - 1) / GN), (unsigned)((nr + GM - 1) / GM));
+      gemm_nn_bupper_kernel<<<grid, 256, (int)(sizeof(double) * 2 * GK * (GPA + GPB)), st>>>(
+          Kb, LinvT, W + r0 * k, nr, k, k);
+      AFN_LAUNCH_CHECK("gemm_nn_bupper_kernel");
+    } else {
+      dim3 grid((unsigned)((k + HN - 1) / HN), (unsigned)((nr + HM - 1) / HM));
+      gemm128_bupper_kernel<<<grid, 256, (int)(sizeof(double) * 2 * HK * (HPA + HPB)), st>>>(
+          Kb, LinvT, W + r0 * k, nr, k, k);
+      AFN_LAUNCH_CHECK("gemm128_bupper_kernel");
+    }
+  }
   dfree(Kb, st);
   return AFN_OK;
 }
