@@ -288,6 +288,17 @@ struct afn_handle_s {
 
 namespace {
 
+// non-blocking side stream per device and host thread (Alg. 1 runs on it
+// concurrently with FPS)
+cudaStream_t side_stream() {
+  static thread_local cudaStream_t ss[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!ss[dev]) cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
+  return ss[dev];
+}
+
 // one small pinned buffer per host thread (PCG scalars), allocated once
 double* pinned_scalars() {
   static thread_local double* buf = nullptr;
@@ -627,12 +638,52 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   h->method = P.method == AFN_METHOD_NYSTROM ? AFN_METHOD_NYSTROM
               : P.method == AFN_METHOD_FSAI  ? AFN_METHOD_FSAI
                                              : AFN_METHOD_AFN;
-  if (P.k_adaptive && P.method != AFN_METHOD_FSAI) {
+  const bool adaptive = P.k_adaptive && P.method != AFN_METHOD_FSAI;
+  // FPS landmarks are nested (X_{k-1} in X_k): with an adaptive k the
+  // FPS for min(k_cap, n) points runs on the build stream WHILE Alg. 1 runs on
+  // a side stream; the first k of them are exactly FPS(k).
+  const int64_t kfps = (adaptive && P.landmarks == AFN_LANDMARKS_FPS) ? std::min<int64_t>(P.k_cap, n) : 0;
+  std::vector<int64_t*> idx(nlocal, nullptr);
+  cudaEvent_t efps0, efps1;
+  AFN_CUDA(cudaEventCreate(&efps0));
+  AFN_CUDA(cudaEventCreate(&efps1));
+  struct EvG3 {
+    cudaEvent_t a, b;
+    ~EvG3() { cudaEventDestroy(a); cudaEventDestroy(b); }
+  } eg3{efps0, efps1};
+  AFN_CUDA(cudaEventRecord(efps0, st));
+  if (kfps > 0) {
+    kt_begin(KT_FPS, st);
+    for (int q = 0; q < nlocal; ++q) {
+      RankSt& s = h->rk[q];
+      TRY(ralloc(s, &idx[q], (size_t)kfps, st));
+      TRY(ralloc(s, &s.fill, (size_t)kfps, st));
+      TRY(fps_run(X, n, d, kfps, P.fps_seed, idx[q], s.fill, st));
+    }
+    kt_end(KT_FPS, st, 0.0);
+    AFN_CUDA(cudaEventRecord(efps1, st));
+  }
+  float alg1_ms = 0.f;
+  if (adaptive) {
     int m = P.m > 0 ? P.m : alg1_default_m(n);
     REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
-    kt_begin(KT_ALG1, st);
-    TRY(alg1_run(X, n, d, kn, m, P.rng_seed, kthr, &h->a1, st));
-    kt_end(KT_ALG1, st, 0.0);
+    cudaStream_t s2 = side_stream();
+    cudaEvent_t a0, a1;
+    AFN_CUDA(cudaEventCreate(&a0));
+    AFN_CUDA(cudaEventCreate(&a1));
+    struct EvG2 {
+      cudaEvent_t a, b;
+      ~EvG2() { cudaEventDestroy(a); cudaEventDestroy(b); }
+    } eg2{a0, a1};
+    AFN_CUDA(cudaStreamWaitEvent(s2, ev[0], 0));
+    AFN_CUDA(cudaEventRecord(a0, s2));
+    kt_begin(KT_ALG1, s2);
+    TRY(alg1_run(X, n, d, kn, m, P.rng_seed, kthr, &h->a1, s2));
+    kt_end(KT_ALG1, s2, 0.0);
+    AFN_CUDA(cudaEventRecord(a1, s2));
+    AFN_CUDA(cudaStreamWaitEvent(st, a1, 0));
+    AFN_CUDA(cudaEventSynchronize(a1));
+    alg1_ms = ev_ms(a0, a1);
     k = std::min<int64_t>(P.k_cap, std::max<int64_t>(1, h->a1.khat));
     k = std::min<int64_t>(k, n);
     // Algorithm 2: AFN if khat >= 2000, else Nystrom with khat landmarks
@@ -649,24 +700,26 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     s.lo = nys ? 0 : s.own.b0 - k;  // own non-landmark rows (W, pattern, G)
     s.hi = nys ? 0 : s.lo + s.own.nb;
   }
-  AFN_CUDA(cudaEventRecord(ev[1], st));
 
   // ---- a3: landmarks (replicated): FPS or uniform (R29)
-  std::vector<int64_t*> idx(nlocal);
-  kt_begin(KT_FPS, st);
-  for (int q = 0; q < nlocal; ++q) {
-    RankSt& s = h->rk[q];
-    TRY(ralloc(s, &idx[q], (size_t)k, st));
-    TRY(ralloc(s, &s.fill, (size_t)k, st));
-    if (k == 0) continue;
-    if (P.landmarks == AFN_LANDMARKS_UNIFORM) {
-      TRY(uniform_landmarks(n, k, P.rng_seed ^ 0x6A09E667F3BCC909ULL, idx[q], st));
-      AFN_CUDA(cudaMemsetAsync(s.fill, 0, sizeof(double) * k, st));  // no fill trace
-    } else {
-      TRY(fps_run(X, n, d, k, P.fps_seed, idx[q], s.fill, st));
+  if (kfps == 0) {
+    AFN_CUDA(cudaEventRecord(efps0, st));
+    kt_begin(KT_FPS, st);
+    for (int q = 0; q < nlocal; ++q) {
+      RankSt& s = h->rk[q];
+      TRY(ralloc(s, &idx[q], (size_t)k, st));
+      TRY(ralloc(s, &s.fill, (size_t)k, st));
+      if (k == 0) continue;
+      if (P.landmarks == AFN_LANDMARKS_UNIFORM) {
+        TRY(uniform_landmarks(n, k, P.rng_seed ^ 0x6A09E667F3BCC909ULL, idx[q], st));
+        AFN_CUDA(cudaMemsetAsync(s.fill, 0, sizeof(double) * k, st));  // no fill trace
+      } else {
+        TRY(fps_run(X, n, d, k, P.fps_seed, idx[q], s.fill, st));
+      }
     }
+    kt_end(KT_FPS, st, 0.0);
+    AFN_CUDA(cudaEventRecord(efps1, st));
   }
-  kt_end(KT_FPS, st, 0.0);
   AFN_CUDA(cudaEventRecord(ev[2], st));
 
   // ---- a1: permutation, permuted + prescaled points; a4: L L^T = K11 + mu I, L^{-T}
@@ -876,8 +929,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       return AFN_ERR_NOT_SPD;
     }
   }
-  h->ms[0] = ev_ms(ev[0], ev[1]);  // alg1
-  h->ms[1] = ev_ms(ev[1], ev[2]);  // fps
+  h->ms[0] = alg1_ms;                                       // alg1 (side stream)
+  h->ms[1] = ev_ms(efps0, efps1);  // fps (overlapping alg1 when k is adaptive)
   h->ms[2] = ev_ms(ev[2], ev[3]);  // perm + chol + L^{-T}
   h->ms[3] = ev_ms(ev[3], ev[4]);  // W
   h->ms[4] = ev_ms(ev[4], ev[5]);  // knn
