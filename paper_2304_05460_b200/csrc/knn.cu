@@ -9,6 +9,8 @@
 // bit-exact and independent of scan order (readings R3, R15).
 #include <algorithm>
 #include <cfloat>
+#include <cmath>
+#include <cstdlib>
 
 #include "afn_common.cuh"
 #include "afn_internal.h"
@@ -151,6 +153,255 @@ knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, 
   if (lane == 0) col[start + W1] = (int32_t)i;
 }
 
+// ---------------------------------------------------------------------------
+// Grid path (d = 3, large N).  Row i only needs the w-1 nearest among the
+// EARLIER points j < i, so its search radius grows like (N/i)^(1/3): a warp
+// scans the cells of a uniform grid that cover the cube [x - r - h, x + r + h]
+// (h = cell edge), keeps the candidates j < i with the same threshold buffer as
+// the brute-force kernel, and accepts when w-1 candidates were found with
+// d2 < r^2 (1 - 1e-12): every point with a smaller key lies inside the scanned
+// cells, so the kept set is the exact (d2, j) selection.  Otherwise r grows by
+// 1.6x.  Rows whose cube would hold more points than i (small i) scan j < i
+// directly.  Bit-identical to the brute-force kernel.
+struct KnnGrid {
+  double lo[3], inv_h, h;
+  int g;  // cells per axis
+};
+
+__global__ void knn_cell_count_kernel(const double* __restrict__ P, int64_t N, KnnGrid G,
+                                      int* __restrict__ cell, int* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int c3[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    int v = (int)((P[i * 3 + c] - G.lo[c]) * G.inv_h);
+    c3[c] = v < 0 ? 0 : (v >= G.g ? G.g - 1 : v);
+  }
+  const int cid = (c3[2] * G.g + c3[1]) * G.g + c3[0];
+  cell[i] = cid;
+  atomicAdd(&cnt[cid], 1);
+}
+
+__global__ void knn_cell_scan_kernel(const int* __restrict__ cnt, int64_t M, int* __restrict__ start) {
+  __shared__ int part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (M + 1023) / 1024;
+  const int64_t b = tid * per, e = min(M, b + per);
+  int s = 0;
+  for (int64_t t = b; t < e; ++t) s += cnt[t];
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int run = tid > 0 ? part[tid - 1] : 0;
+  for (int64_t t = b; t < e; ++t) {
+    start[t] = run;
+    run += cnt[t];
+  }
+  if (tid == 1023) start[M] = part[1023];
+}
+
+// cell-sorted points (coordinates + original position), positions within a
+// cell in ascending order is not required (the selection is order-free)
+__global__ void knn_cell_fill_kernel(const double* __restrict__ P, int64_t N, const int* __restrict__ cell,
+                                     const int* __restrict__ start, int* __restrict__ cur,
+                                     double4* __restrict__ cp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  const int c = cell[i];
+  const int pos = start[c] + atomicAdd(&cur[c], 1);
+  cp[pos] = make_double4(P[i * 3], P[i * 3 + 1], P[i * 3 + 2], __longlong_as_double((long long)i));
+}
+
+__global__ void __launch_bounds__(KNN_NW * 32)
+knn_grid_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int64_t N, int w, KnnGrid G,
+                const int* __restrict__ start, const double4* __restrict__ cp, int32_t* __restrict__ col) {
+  __shared__ double s_key[KNN_NW][KNN_CAP];
+  __shared__ int s_idx[KNN_NW][KNN_CAP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = row_lo + (int64_t)blockIdx.x * KNN_NW + wid;
+  if (i >= row_hi) return;
+  const int W1 = (int)min((int64_t)w - 1, i);
+  double* key = s_key[wid];
+  int* idx = s_idx[wid];
+  const double q[3] = {P[i * 3], P[i * 3 + 1], P[i * 3 + 2]};
+  int cnt = 0;
+  double tau_d = DBL_MAX;
+  int tau_j = 0x7fffffff;
+  auto compact = [&]() {
+    for (int t = cnt + lane; t < KNN_CAP; t += 32) { key[t] = DBL_MAX; idx[t] = 0x7fffffff; }
+    __syncwarp();
+    warp_bitonic(key, idx);
+    cnt = min(cnt, W1);
+    if (cnt == W1 && W1 > 0) { tau_d = key[W1 - 1]; tau_j = idx[W1 - 1]; }
+    __syncwarp();
+  };
+  auto offer = [&](bool valid, double dd, int j) {
+    if (cnt > KNN_CAP - 32) compact();
+    const bool take = valid && key_less(dd, j, tau_d, tau_j);
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+      key[pos] = dd;
+      idx[pos] = j;
+    }
+    cnt += __popc(m);
+    __syncwarp();
+  };
+  if (W1 > 0) {
+    // radius for ~2 w earlier points at the average density of the earlier points
+    const double V = (double)G.g * G.g * G.g * G.h * G.h * G.h;
+    double r = cbrt(2.0 * (double)w * V / (4.18879020478639 * (double)i));
+    bool done = false;
+    while (!done) {
+      const int span = (int)ceil(r * G.inv_h) + 1;
+      int lo3[3], hi3[3];
+      int64_t ncell = 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        int cc = (int)((q[c] - G.lo[c]) * G.inv_h);
+        cc = cc < 0 ? 0 : (cc >= G.g ? G.g - 1 : cc);
+        lo3[c] = max(0, cc - span);
+        hi3[c] = min(G.g - 1, cc + span);
+        ncell *= (int64_t)(hi3[c] - lo3[c] + 1);
+      }
+      const int64_t est = (int64_t)((double)ncell * (double)N / ((double)G.g * G.g * G.g));
+      cnt = 0;
+      tau_d = DBL_MAX;
+      tau_j = 0x7fffffff;
+      if (est >= i || (lo3[0] == 0 && lo3[1] == 0 && lo3[2] == 0 && hi3[0] == G.g - 1 &&
+                       hi3[1] == G.g - 1 && hi3[2] == G.g - 1)) {
+        // brute force over j < i (small i, or the cube covers the grid)
+        for (int64_t b = 0; b < i; b += 32) {
+          const int64_t j = b + lane;
+          double dd = 0.0;
+          if (j < i) dd = d2_exact<3>(&P[j * 3], q);
+          offer(j < i, dd, (int)j);
+        }
+        done = true;
+      } else {
+        for (int z = lo3[2]; z <= hi3[2]; ++z)
+          for (int y = lo3[1]; y <= hi3[1]; ++y) {
+            const int c0 = (z * G.g + y) * G.g;
+            const int b = start[c0 + lo3[0]], e = start[c0 + hi3[0] + 1];
+            for (int t = b; t < e; t += 32) {
+              bool valid = false;
+              double dd = 0.0;
+              int j = 0;
+              if (t + lane < e) {
+                const double4 pt = cp[t + lane];
+                j = (int)__double_as_longlong(pt.w);
+                if (j < i) {
+                  const double pp[3] = {pt.x, pt.y, pt.z};
+                  dd = d2_exact<3>(pp, q);
+                  valid = true;
+                }
+              }
+              offer(valid, dd, j);
+            }
+          }
+        compact();
+        if (cnt == W1 && tau_d < r * r * (1.0 - 1e-12)) done = true;
+        else r *= 1.6;
+      }
+    }
+    compact();
+    for (int t = lane; t < KNN_CAP; t += 32) {
+      const int v = t < W1 ? idx[t] : 0x7fffffff;
+      __syncwarp();
+      idx[t] = v;
+    }
+    __syncwarp();
+    warp_bitonic_int(idx);
+  }
+  const int64_t wl = w;
+  const int64_t start_i = (i < wl) ? i * (i + 1) / 2 : wl * (wl + 1) / 2 + (i - wl) * wl;
+  for (int t = lane; t < W1; t += 32) col[start_i + t] = idx[t];
+  if (lane == 0) col[start_i + W1] = (int32_t)i;
+}
+
+__global__ void knn_bbox_kernel(const double* __restrict__ P, int64_t N, double* __restrict__ box) {
+  // one block: min / max per coordinate (exact: min/max are order-free)
+  __shared__ double smin[3][256], smax[3][256];
+  double mn[3] = {DBL_MAX, DBL_MAX, DBL_MAX}, mx[3] = {-DBL_MAX, -DBL_MAX, -DBL_MAX};
+  for (int64_t i = threadIdx.x; i < N; i += 256)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double v = P[i * 3 + c];
+      mn[c] = fmin(mn[c], v);
+      mx[c] = fmax(mx[c], v);
+    }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) { smin[c][threadIdx.x] = mn[c]; smax[c][threadIdx.x] = mx[c]; }
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        smin[c][threadIdx.x] = fmin(smin[c][threadIdx.x], smin[c][threadIdx.x + o]);
+        smax[c][threadIdx.x] = fmax(smax[c][threadIdx.x], smax[c][threadIdx.x + o]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int c = 0; c < 3; ++c) { box[c] = smin[c][0]; box[3 + c] = smax[c][0]; }
+}
+
+afn_status knn_grid_run(const double* P, int64_t N, int w, int32_t* col, int64_t lo, int64_t hi,
+                        cudaStream_t st) {
+  double* box = nullptr;
+  afn_status s = dalloc((void**)&box, sizeof(double) * 6, st);
+  if (s != AFN_OK) return s;
+  knn_bbox_kernel<<<1, 256, 0, st>>>(P, N, box);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { dfree(box, st); return cuda_status(e, "knn_bbox_kernel"); }
+  note_launch();
+  double hb[6];
+  e = cudaMemcpyAsync(hb, box, sizeof(hb), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  dfree(box, st);
+  if (e != cudaSuccess) return cuda_status(e, "knn bbox copy");
+  KnnGrid G;
+  G.g = std::max(1, (int)std::ceil(std::cbrt((double)N / 4.0)));
+  double ext = 0.0;
+  for (int c = 0; c < 3; ++c) ext = std::max(ext, hb[3 + c] - hb[c]);
+  ext = ext > 0.0 ? ext * (1.0 + 1e-9) : 1.0;
+  G.h = ext / G.g;
+  G.inv_h = 1.0 / G.h;
+  for (int c = 0; c < 3; ++c) G.lo[c] = hb[c];
+  const int64_t M = (int64_t)G.g * G.g * G.g;
+  int *cell = nullptr, *cntb = nullptr, *start = nullptr;
+  double4* cp = nullptr;
+  if ((s = dalloc((void**)&cell, sizeof(int) * N, st)) != AFN_OK) return s;
+  if ((s = dalloc((void**)&cntb, sizeof(int) * 2 * M, st)) != AFN_OK) { dfree(cell, st); return s; }
+  if ((s = dalloc((void**)&start, sizeof(int) * (M + 1), st)) != AFN_OK) { dfree(cell, st); dfree(cntb, st); return s; }
+  if ((s = dalloc((void**)&cp, sizeof(double4) * N, st)) != AFN_OK) {
+    dfree(cell, st); dfree(cntb, st); dfree(start, st);
+    return s;
+  }
+  struct Free {
+    void* p[4];
+    cudaStream_t st;
+    ~Free() { for (void* q : p) dfree(q, st); }
+  } fr{{cell, cntb, start, cp}, st};
+  AFN_CUDA(cudaMemsetAsync(cntb, 0, sizeof(int) * 2 * M, st));
+  knn_cell_count_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(P, N, G, cell, cntb);
+  AFN_LAUNCH_CHECK("knn_cell_count_kernel");
+  knn_cell_scan_kernel<<<1, 1024, 0, st>>>(cntb, M, start);
+  AFN_LAUNCH_CHECK("knn_cell_scan_kernel");
+  knn_cell_fill_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(P, N, cell, start, cntb + M, cp);
+  AFN_LAUNCH_CHECK("knn_cell_fill_kernel");
+  const int64_t blocks = (hi - lo + KNN_NW - 1) / KNN_NW;
+  knn_grid_kernel<<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(P, lo, hi, N, w, G, start, cp, col);
+  AFN_LAUNCH_CHECK("knn_grid_kernel");
+  return AFN_OK;
+}
+
 __global__ void knn_rowptr_kernel(int64_t N, int w, int64_t* __restrict__ rp) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i > N) return;
@@ -183,6 +434,12 @@ afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, i
   AFN_LAUNCH_CHECK("knn_rowptr_kernel");
   if (row_hi <= row_lo) return AFN_OK;
   const int64_t lo = row_lo, hi = row_hi;
+  static const int64_t grid_min = getenv("AFN_KNN_GRID_MIN") ? atoll(getenv("AFN_KNN_GRID_MIN")) : 50000;
+  if (d == 3 && N >= grid_min && w > 1) {
+    afn_status s = knn_grid_run(P, N, w, col, lo, hi, st);
+    if (s != AFN_OK) return s;
+    return AFN_OK;
+  }
   if (d <= 1) launch_knn<1>(P, lo, hi, d, w, col, st);
   else if (d <= 2) launch_knn<2>(P, lo, hi, d, w, col, st);
   else if (d <= 3) launch_knn<3>(P, lo, hi, d, w, col, st);

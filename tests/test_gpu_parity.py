@@ -109,6 +109,30 @@ def test_knn_bit_exact(N, d, w):
     assert np.array_equal(col.cpu().numpy().astype(np.int64), colo)
 
 
+@pytest.mark.parametrize("N,w,seed", [(60000, 100, 1), (120000, 50, 2), (70000, 1, 3)])
+def test_knn_grid_path_rows(N, w, seed):
+    """d = 3, N >= 50000 takes the grid search (knn.cu): sampled rows, small and
+    large i, bit-exact against the brute-force definition."""
+    P, _ = gen_points(N, 3, "cube", seed)
+    rp, col = afn.afn_knn_pattern(T(P), w)
+    rp, col = rp.cpu().numpy(), col.cpu().numpy()
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([np.arange(0, 300), rng.integers(0, N, 200), [N - 1]]))
+    for i in rows:
+        assert np.array_equal(col[rp[i]:rp[i + 1]].astype(np.int64), O.knn_row(P, int(i), w)), i
+
+
+def test_knn_grid_ties_lattice():
+    """Integer lattice (many equal distances) through the grid path: the lowest
+    position must win exactly as in the brute-force kernel."""
+    g = np.stack(np.meshgrid(np.arange(40.0), np.arange(40.0), np.arange(40.0), indexing="ij"), -1).reshape(-1, 3)
+    P = g[np.random.default_rng(0).permutation(len(g))]
+    rp, col = afn.afn_knn_pattern(T(P), 27)
+    rp, col = rp.cpu().numpy(), col.cpu().numpy()
+    for i in list(range(0, 200)) + list(range(63000, 64000, 37)):
+        assert np.array_equal(col[rp[i]:rp[i + 1]].astype(np.int64), O.knn_row(P, i, 27)), i
+
+
 def test_knn_ties_lattice():
     """Integer lattice: many equal distances -> lowest position must win."""
     g = np.stack(np.meshgrid(np.arange(9.0), np.arange(9.0), indexing="ij"), -1).reshape(-1, 2)
