@@ -299,6 +299,16 @@ cudaStream_t side_stream() {
   return ss[dev];
 }
 
+// two pinned int64 per host thread (FPS early-stop value)
+int64_t* pinned_i64() {
+  static thread_local int64_t* buf = nullptr;
+  if (!buf && cudaMallocHost((void**)&buf, sizeof(int64_t) * 2) != cudaSuccess) {
+    cudaGetLastError();
+    buf = nullptr;
+  }
+  return buf;
+}
+
 // one small pinned buffer per host thread (PCG scalars), allocated once
 double* pinned_scalars() {
   static thread_local double* buf = nullptr;
@@ -652,13 +662,23 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     ~EvG3() { cudaEventDestroy(a); cudaEventDestroy(b); }
   } eg3{efps0, efps1};
   AFN_CUDA(cudaEventRecord(efps0, st));
+  int64_t* kstop = nullptr;  // lowered to k once Alg. 1 is done (FPS early stop)
+  int64_t* hk = pinned_i64();
+  if (!hk) {
+    set_error("pinned host allocation failed");
+    return AFN_ERR_NOMEM;
+  }
   if (kfps > 0) {
+    TRY(ralloc(h->rk[0], &kstop, 1, st));
+    hk[0] = kfps;
+    AFN_CUDA(cudaMemcpyAsync(kstop, hk, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
     kt_begin(KT_FPS, st);
     for (int q = 0; q < nlocal; ++q) {
       RankSt& s = h->rk[q];
       TRY(ralloc(s, &idx[q], (size_t)kfps, st));
       TRY(ralloc(s, &s.fill, (size_t)kfps, st));
-      TRY(fps_run(X, n, d, kfps, P.fps_seed, idx[q], s.fill, st));
+      TRY(fps_run(X, n, d, kfps, P.fps_seed, idx[q], s.fill, st, kstop));
     }
     kt_end(KT_FPS, st, 0.0);
     AFN_CUDA(cudaEventRecord(efps1, st));
@@ -680,6 +700,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_begin(KT_ALG1, s2);
     TRY(alg1_run(X, n, d, kn, m, P.rng_seed, kthr, &h->a1, s2));
     kt_end(KT_ALG1, s2, 0.0);
+    if (kstop) {  // the running FPS may stop at min(k_cap, khat)
+      hk[1] = std::min<int64_t>(kfps, std::max<int64_t>(1, h->a1.khat));
+      AFN_CUDA(cudaMemcpyAsync(kstop, hk + 1, sizeof(int64_t), cudaMemcpyHostToDevice, s2));
+    }
     AFN_CUDA(cudaEventRecord(a1, s2));
     AFN_CUDA(cudaStreamWaitEvent(st, a1, 0));
     AFN_CUDA(cudaEventSynchronize(a1));

@@ -82,8 +82,10 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
                       double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st);
 
 // ---- FPS (fps.cu) ---------------------------------------------------------
+// kstop (optional, device): the run may stop early once *kstop (which another
+// stream may lower while it runs) is reached -- entries below it are complete
 afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
-                   double* fill, cudaStream_t st);
+                   double* fill, cudaStream_t st, const int64_t* kstop = nullptr);
 
 // ---- kNN pattern (knn.cu) -------------------------------------------------
 int64_t knn_nnz(int64_t N, int w);

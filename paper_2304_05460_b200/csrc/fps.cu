@@ -270,12 +270,18 @@ namespace cg = cooperative_groups;
 template <int DP, int P, int NT>
 __global__ void __launch_bounds__(NT, 1)
 fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
-                   int64_t* __restrict__ idx_out, double* __restrict__ fill_out) {
+                   int64_t* __restrict__ idx_out, double* __restrict__ fill_out,
+                   const int64_t* __restrict__ kstop) {
   constexpr int S = Slot<DP>::S;
   constexpr int NW = NT / 32;
   __shared__ double s_w[NW][S];
   __shared__ double s_slot[2][S];
   __shared__ double s_new[S];
+  // early stop: a host-side writer may lower *kstop while the kernel runs
+  // (Alg. 1 finishing on another stream); rank 0 samples it every 8 steps and
+  // every CTA reads rank 0's sample after the same cluster barrier
+  __shared__ long long s_stop[2];
+  __shared__ long long s_kend;
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
@@ -302,9 +308,15 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
     }
   }
   if (crank == 0 && tid == 0) idx_out[0] = seed;
+  if (tid == 0) s_stop[0] = s_stop[1] = k;
 
   for (int64_t step = 1; step <= k; ++step) {
     const int par = (int)(step & 1);
+    if (crank == 0 && tid == 0) {
+      long long ks = s_stop[par ^ 1];
+      if (kstop != nullptr && (step & 7) == 0) ks = min(ks, *reinterpret_cast<const volatile long long*>(kstop));
+      s_stop[par] = ks;
+    }
     // thread-local best (indices ascend with s: strict > keeps the lowest)
     double bd = -3.0;
     unsigned bi = 0xffffffffu;
@@ -345,6 +357,7 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
       warp_argmax_key(fps_key(gd), gi, k3, i3);
       const int src = __ffs(__ballot_sync(0xffffffffu, lane < CL && gi == i3)) - 1;
       if (lane < S) s_new[lane] = cl.map_shared_rank(&s_slot[par][0], src)[lane];
+      if (lane == 0) s_kend = *cl.map_shared_rank(&s_stop[par], 0);
     }
     __syncthreads();
     const double nd = s_new[0];
@@ -353,7 +366,7 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
       fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
       if (step < k) idx_out[step] = ni;
     }
-    if (step == k) break;
+    if (step >= s_kend) break;
 #pragma unroll
     for (int c = 0; c < DP; ++c) y[c] = s_new[2 + c];
 #pragma unroll
@@ -370,7 +383,7 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
 
 template <int DP, int P, int NT>
 afn_status launch_fps_cluster(const double* X, int64_t n, int d, int64_t k, int64_t seed,
-                              int64_t* idx, double* fill, int CL, cudaStream_t st) {
+                              int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st) {
   auto kern = fps_cluster_kernel<DP, P, NT>;
   if (CL > 8) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchConfig_t cfg = {};
@@ -385,14 +398,14 @@ afn_status launch_fps_cluster(const double* X, int64_t n, int d, int64_t k, int6
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill));
+  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop));
   AFN_LAUNCH_CHECK("fps_cluster_kernel");
   return AFN_OK;
 }
 
 template <int DP>
 afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
-                          double* fill, cudaStream_t st) {
+                          double* fill, const int64_t* kstop, cudaStream_t st) {
   const int sms = num_sms();
   // cluster path: one cluster of CL <= 16 CTAs, 1 or 2 points per thread
   {
@@ -400,8 +413,8 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
     if (n > (int64_t)FPS_NT * 8 && n <= (int64_t)16 * CNT * 2) {
       const int P2 = n <= (int64_t)8 * CNT ? 1 : 2;
       const int CL = (int)((n + (int64_t)CNT * P2 - 1) / ((int64_t)CNT * P2));
-      if (P2 == 1) return launch_fps_cluster<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, st);
-      return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, st);
+      if (P2 == 1) return launch_fps_cluster<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
     }
   }
   // choose points per thread P and grid G (G = 1 needs no grid barrier)
@@ -450,14 +463,14 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
 }  // namespace
 
 afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, int64_t* idx,
-                   double* fill, cudaStream_t st) {
+                   double* fill, cudaStream_t st, const int64_t* kstop) {
   // coordinates are zero-padded to DP: adding +0.0 terms leaves d2 bit-identical
-  if (d <= 1) return fps_dispatch_p<1>(X, n, d, k, seed, idx, fill, st);
-  if (d <= 2) return fps_dispatch_p<2>(X, n, d, k, seed, idx, fill, st);
-  if (d <= 3) return fps_dispatch_p<3>(X, n, d, k, seed, idx, fill, st);
-  if (d <= 4) return fps_dispatch_p<4>(X, n, d, k, seed, idx, fill, st);
-  if (d <= 8) return fps_dispatch_p<8>(X, n, d, k, seed, idx, fill, st);
-  if (d <= 16) return fps_dispatch_p<16>(X, n, d, k, seed, idx, fill, st);
+  if (d <= 1) return fps_dispatch_p<1>(X, n, d, k, seed, idx, fill, kstop, st);
+  if (d <= 2) return fps_dispatch_p<2>(X, n, d, k, seed, idx, fill, kstop, st);
+  if (d <= 3) return fps_dispatch_p<3>(X, n, d, k, seed, idx, fill, kstop, st);
+  if (d <= 4) return fps_dispatch_p<4>(X, n, d, k, seed, idx, fill, kstop, st);
+  if (d <= 8) return fps_dispatch_p<8>(X, n, d, k, seed, idx, fill, kstop, st);
+  if (d <= 16) return fps_dispatch_p<16>(X, n, d, k, seed, idx, fill, kstop, st);
   set_error("fps: d=%d unsupported (1..16)", d);
   return AFN_ERR_ARG;
 }
