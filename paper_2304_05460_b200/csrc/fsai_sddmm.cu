@@ -34,7 +34,7 @@ namespace {
 constexpr int GA_MAX = 32;   // largest group size (points a per group)
 constexpr int UCAP = 4096;   // max |U_g|
 constexpr int HC = 8192;     // hash capacity (power of two)
-constexpr int UT = 512;      // U columns per GEMM pass (2 per thread)
+constexpr int UT = 512;      // U columns per GEMM pass (2 per thread; BC = 4: 1024)
 constexpr int KC2 = 8;       // k per pipeline stage
 constexpr int NST = 3;       // pipeline stages
 
@@ -150,9 +150,9 @@ __global__ void cell_scatter_kernel(const int* __restrict__ key, int64_t N, cons
   sorder[off[k] + p] = (int)i;
 }
 
-__global__ void pass_count_kernel(const int* __restrict__ Ucount, int64_t G, int* __restrict__ pc) {
+__global__ void pass_count_kernel(const int* __restrict__ Ucount, int64_t G, int ut, int* __restrict__ pc) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < G) pc[g] = (Ucount[g] + UT - 1) / UT;
+  if (g < G) pc[g] = (Ucount[g] + ut - 1) / ut;
 }
 
 __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int ga, int* __restrict__ grp,
@@ -254,14 +254,15 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-template <int GA>
-__global__ void __launch_bounds__(256, GA <= 16 ? 2 : 1) group_gemm_kernel(const int* __restrict__ sorder, int64_t N,
+template <int GA, int BC>
+__global__ void __launch_bounds__(256, (GA <= 16 && BC <= 2) ? 2 : 1) group_gemm_kernel(const int* __restrict__ sorder, int64_t N,
                                                             const double* __restrict__ W, int64_t k,
                                                             const int* __restrict__ Ucount,
                                                             const int* __restrict__ Ulist,
                                                             const int64_t* __restrict__ Doff,
                                                             const int64_t* __restrict__ Poff, int64_t G,
                                                             double* __restrict__ D) {
+  constexpr int UT = 256 * BC;  // U columns per pass: BC per thread
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                    // [NST][KC2/2][GA][2]
   double* sB = gs + NST * KC2 * GA;   // [NST][KC2/2][UT][2]
@@ -320,9 +321,11 @@ __global__ void __launch_bounds__(256, GA <= 16 ? 2 : 1) group_gemm_kernel(const
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    double acc[GA][2];
+    double acc[GA][BC];
 #pragma unroll
-    for (int j = 0; j < GA; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int j = 0; j < GA; ++j)
+#pragma unroll
+      for (int q = 0; q < BC; ++q) acc[j][q] = 0.0;
 #pragma unroll
     for (int s0 = 0; s0 < NST - 1; ++s0) {
       if (s0 < nch) issue(s0, s0);
@@ -338,15 +341,17 @@ __global__ void __launch_bounds__(256, GA <= 16 ? 2 : 1) group_gemm_kernel(const
       const double* b = sB + (int)(ch % NST) * KC2 * UT;
 #pragma unroll
       for (int k2 = 0; k2 < KC2 / 2; ++k2) {
-        const double2 b0 = *reinterpret_cast<const double2*>(&b[(k2 * UT + tid) * 2]);
-        const double2 b1 = *reinterpret_cast<const double2*>(&b[(k2 * UT + tid + 256) * 2]);
+        double2 bq[BC];
+#pragma unroll
+        for (int q = 0; q < BC; ++q) bq[q] = *reinterpret_cast<const double2*>(&b[(k2 * UT + tid + 256 * q) * 2]);
 #pragma unroll
         for (int j = 0; j < GA; ++j) {
           const double2 av = *reinterpret_cast<const double2*>(&a[(k2 * GA + j) * 2]);
-          acc[j][0] = fma(av.x, b0.x, acc[j][0]);
-          acc[j][1] = fma(av.x, b1.x, acc[j][1]);
-          acc[j][0] = fma(av.y, b0.y, acc[j][0]);
-          acc[j][1] = fma(av.y, b1.y, acc[j][1]);
+#pragma unroll
+          for (int q = 0; q < BC; ++q) {
+            acc[j][q] = fma(av.x, bq[q].x, acc[j][q]);
+            acc[j][q] = fma(av.y, bq[q].y, acc[j][q]);
+          }
         }
       }
     }
@@ -354,8 +359,9 @@ __global__ void __launch_bounds__(256, GA <= 16 ? 2 : 1) group_gemm_kernel(const
 #pragma unroll
     for (int j = 0; j < GA; ++j) {
       if (j >= cnt) break;
-      if (tid < un) Dg[(int64_t)j * nu + u0 + tid] = acc[j][0];
-      if (tid + 256 < un) Dg[(int64_t)j * nu + u0 + tid + 256] = acc[j][1];
+#pragma unroll
+      for (int q = 0; q < BC; ++q)
+        if (tid + 256 * q < un) Dg[(int64_t)j * nu + u0 + tid + 256 * q] = acc[j][q];
     }
   }
 }
@@ -753,7 +759,12 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   int64_t* Poff;
   if ((s = get((void**)&pc, sizeof(int) * G)) != AFN_OK) return s;
   if ((s = get((void**)&Poff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
-  pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, pc);
+  // columns of U per GEMM work item: 256 x BC.  BC = 4 reads the broadcast
+  // W_g operand once per 4 columns (0.16 LDS per DFMA instead of 0.28) but
+  // needs 244 registers (1 CTA/SM) and measured slower (C2 10.5 vs 7.0 ms)
+  static const int BC = getenv("AFN_FSAI_BC") ? std::max(2, std::min(4, atoi(getenv("AFN_FSAI_BC")))) : 2;
+  const int ut = 256 * (BC >= 4 ? 4 : 2);
+  pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, ut, pc);
   AFN_LAUNCH_CHECK("pass_count_kernel");
   scan_i64_kernel<<<1, 1024, 0, st>>>(pc, G, 1, Poff);
   AFN_LAUNCH_CHECK("scan_i64_kernel");
@@ -765,8 +776,9 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   double* D;
   if ((s = get((void**)&D, sizeof(double) * (totD > 0 ? totD : 1))) != AFN_OK) return s;
   {
-    const int bytes = (int)(sizeof(double) * NST * KC2 * (GA + UT));
-    auto kern = GA == 32 ? group_gemm_kernel<32> : group_gemm_kernel<16>;
+    const int bytes = (int)(sizeof(double) * NST * KC2 * (GA + ut));
+    auto kern = GA == 32 ? (ut == 1024 ? group_gemm_kernel<32, 4> : group_gemm_kernel<32, 2>)
+                         : (ut == 1024 ? group_gemm_kernel<16, 4> : group_gemm_kernel<16, 2>);
     AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0) {
