@@ -228,6 +228,15 @@ using namespace afn;
 // rank; W holds the rank's own non-landmark rows; the PCG vectors are full
 // length with only the rank's own rows (RankSt::own) computed locally.
 #define AFN_NYS_NU 1e-10  // K11 shift of the Nystrom branch (reading R30)
+// AFN_DEBUG_PHASES=1: synchronise and report after every build phase (debugging)
+#define AFN_PHASE(name)                                                          \
+  do {                                                                           \
+    static const bool dbg_ = getenv("AFN_DEBUG_PHASES") != nullptr;              \
+    if (dbg_) {                                                                  \
+      cudaError_t e_ = cudaStreamSynchronize(st);                                \
+      fprintf(stderr, "afn_build phase %s done (%s)\n", name, cudaGetErrorString(e_)); \
+    }                                                                            \
+  } while (0)
 
 struct RankSt {
   int rank = 0;
@@ -641,6 +650,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   } hg{&h};
 
   AFN_CUDA(cudaEventRecord(ev[0], st));
+  AFN_PHASE("ev0");
   // ---- a2: adaptive k (Alg. 1) -- replicated: every rank computes the same k
   const Kern kn = h->kn;
   int64_t k = std::min<int64_t>(P.k_cap, n);
@@ -687,7 +697,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   if (adaptive) {
     int m = P.m > 0 ? P.m : alg1_default_m(n);
     REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
-    cudaStream_t s2 = side_stream();
+    static const bool serial = getenv("AFN_NO_OVERLAP") != nullptr;
+    cudaStream_t s2 = serial ? st : side_stream();
     cudaEvent_t a0, a1;
     AFN_CUDA(cudaEventCreate(&a0));
     AFN_CUDA(cudaEventCreate(&a1));
@@ -745,6 +756,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     AFN_CUDA(cudaEventRecord(efps1, st));
   }
   AFN_CUDA(cudaEventRecord(ev[2], st));
+  AFN_PHASE("ev2");
 
   // ---- a1: permutation, permuted + prescaled points; a4: L L^T = K11 + mu I, L^{-T}
   for (int q = 0; q < nlocal; ++q) {
@@ -786,6 +798,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_end(KT_LINV, st, (double)k * k * k / 3.0);
   }
   AFN_CUDA(cudaEventRecord(ev[3], st));
+  AFN_PHASE("ev3");
   for (auto& s : h->rk) {
     int info = 0;
     AFN_CUDA(cudaMemcpyAsync(&info, s.dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -798,10 +811,15 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   if (nys) {
     TRY(build_nystrom(h, st));
     AFN_CUDA(cudaEventRecord(ev[4], st));
+    AFN_PHASE("ev4");
     AFN_CUDA(cudaEventRecord(ev[5], st));
+    AFN_PHASE("ev5");
     AFN_CUDA(cudaEventRecord(ev[6], st));
+    AFN_PHASE("ev6");
     AFN_CUDA(cudaEventRecord(ev[7], st));
+    AFN_PHASE("ev7");
     AFN_CUDA(cudaEventRecord(ev[8], st));
+    AFN_PHASE("ev8");
   } else {
 
   // ---- a5: W = K21 L^{-T}, own rows (into a full-height buffer when sharded:
@@ -820,6 +838,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   }
   kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k / h->R);  // (N2/R) k^2/2 FMA per rank
   AFN_CUDA(cudaEventRecord(ev[4], st));
+  AFN_PHASE("ev4");
 
   // ---- a6: kNN pattern (own rows; row_ptr in closed form)
   kt_begin(KT_KNN, st);
@@ -831,6 +850,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   }
   kt_end(KT_KNN, st, 0.0);
   AFN_CUDA(cudaEventRecord(ev[5], st));
+  AFN_PHASE("ev5");
   if (N2 > 0) {
     // exchange W rows and pattern rows
     {
@@ -845,6 +865,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
   }
   AFN_CUDA(cudaEventRecord(ev[6], st));
+  AFN_PHASE("ev6");
 
   // ---- a7: FSAI rows (own), then G^T
   std::vector<int64_t*> tmap(nlocal, nullptr);
@@ -863,6 +884,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
   }
   AFN_CUDA(cudaEventRecord(ev[7], st));
+  AFN_PHASE("ev7");
   if (N2 > 0) {
     static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : -1;
     for (int q = 0; q < nlocal; ++q) {
@@ -882,6 +904,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
   }
   AFN_CUDA(cudaEventRecord(ev[8], st));
+  AFN_PHASE("ev8");
   if (N2 > 0) {
     TRY(exchange(h, [](RankSt& s) { return s.gval; }, [&](int s) { return nnz_ranges(h, s, 8); }, st));
     for (int q = 0; q < nlocal; ++q) {
@@ -938,6 +961,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     return AFN_ERR_NOMEM;
   }
   AFN_CUDA(cudaEventRecord(ev[9], st));
+  AFN_PHASE("ev9");
   AFN_CUDA(cudaStreamSynchronize(st));
   for (auto& s : h->rk) {
     int e = 0;

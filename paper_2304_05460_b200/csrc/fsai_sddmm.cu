@@ -18,6 +18,8 @@
 //      blocked Cholesky in shared memory, g = L^{-T} e_last.
 // Values are independent of the grouping (each dot has a fixed summation
 // order), so the result is deterministic even though the cell sort uses atomics.
+#include <math_constants.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -180,40 +182,43 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
                                                           int2* __restrict__ Htab, int* overflow) {
   extern __shared__ int hs[];  // HC keys
-  __shared__ int s_n;
+  __shared__ int s_n, s_ovf;
   __shared__ int s_scan[256];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t g = blockIdx.x;
   for (int t = tid; t < HC; t += 256) hs[t] = -1;
-  if (tid == 0) s_n = 0;
+  if (tid == 0) s_n = 0, s_ovf = 0;
   __syncthreads();
   const int64_t m0 = g * ga;
   const int cnt = (int)min((int64_t)ga, N - m0);
-  for (int j = 0; j < cnt; ++j) {
+  // at most UCAP keys fit (load factor <= 1/2): once s_n passes it every loop
+  // stops (a hub point of a high-dimensional pattern can be in thousands of
+  // rows) and the caller falls back to the per-row Gram
+  for (int j = 0; j < cnt && !*(volatile int*)&s_ovf; ++j) {
     const int a = sorder[m0 + j];
-    for (int64_t e = trp[a] + wid; e < trp[a + 1]; e += 8) {
+    for (int64_t e = trp[a] + wid; e < trp[a + 1] && !*(volatile int*)&s_ovf; e += 8) {
       const int i = tcol[e];
       if (i < row_lo || i >= row_hi) continue;  // rows this rank factors
       for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
         const int b = col[q];
         if (b > a) break;  // columns ascending
         unsigned h = ((unsigned)b * 2654435761u) & (HC - 1);
-        while (true) {
+        for (int probe = 0; probe < HC; ++probe) {
           const int old = atomicCAS(&hs[h], -1, b);
           if (old == -1) {
-            atomicAdd(&s_n, 1);
+            if (atomicAdd(&s_n, 1) >= UCAP) s_ovf = 1;
             break;
           }
           if (old == b) break;
           h = (h + 1) & (HC - 1);
         }
+        if (*(volatile int*)&s_ovf) break;
       }
-      if (s_n > (HC * 3) / 4) break;  // overflow guard (checked below)
     }
   }
   __syncthreads();
   const int nu = s_n;
-  if (nu > UCAP || nu > (HC * 3) / 4) {
+  if (s_ovf || nu > UCAP) {
     if (tid == 0) atomicExch(overflow, 1);
     return;
   }
@@ -483,11 +488,14 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       for (int t = 0; t < B; ++t) {
         const int b = sJ[qq[t]];
         const int2* H = Htab + (int64_t)s_g[pp[t]] * HC;
-        while (hv[t].x != b) {  // b is in U_g by construction
+        int probe = 0;
+        while (hv[t].x != b && probe < HC) {  // b is in U_g by construction
           hh[t] = (hh[t] + 1) & (HC - 1);
           hv[t] = __ldg(&H[hh[t]]);
+          ++probe;
         }
-        gram[t] = D[s_db[pp[t]] + hv[t].y];
+        // (never taken; a missing key poisons the row -> NOT_SPD, not a hang)
+        gram[t] = hv[t].x == b ? D[s_db[pp[t]] + hv[t].y] : CUDART_NAN;
       }
 #pragma unroll
       for (int t = 0; t < B; ++t) {
