@@ -410,11 +410,16 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
   // cluster path: one cluster of CL <= 16 CTAs, 1 or 2 points per thread
   {
     constexpr int CNT = DP <= 4 ? 1024 : 512;
-    if (n > (int64_t)FPS_NT * 8 && n <= (int64_t)16 * CNT * 2) {
-      const int P2 = n <= (int64_t)8 * CNT ? 1 : 2;
+    // points per thread: fewer CTAs in the cluster (cheaper per-step cluster
+    // barrier) against more distance updates per thread
+    static const int pmin = getenv("AFN_FPS_PPT") ? atoi(getenv("AFN_FPS_PPT")) : 1;
+    if (n > (int64_t)FPS_NT * 8 && n <= (int64_t)16 * CNT * 4) {
+      int P2 = 1;
+      while (P2 < 4 && (n > (int64_t)16 * CNT * P2 || P2 < pmin)) P2 *= 2;
       const int CL = (int)((n + (int64_t)CNT * P2 - 1) / ((int64_t)CNT * P2));
       if (P2 == 1) return launch_fps_cluster<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-      return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      if (P2 == 2) return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      return launch_fps_cluster<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
     }
   }
   // choose points per thread P and grid G (G = 1 needs no grid barrier)
