@@ -421,12 +421,15 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
                                                          const int2* __restrict__ Htab,
                                                          const int64_t* __restrict__ Doff,
                                                          const double* __restrict__ D, double* __restrict__ gval,
-                                                         int* info) {
+                                                         int* info, int lsz) {
   constexpr int WP = MT * 16;
-  constexpr int LSZ = WP * (WP + 1) / 2 + WP;  // packed lower, rows padded to even length
   extern __shared__ __align__(16) double fsm[];
-  double* Lm = fsm;            // [LSZ]
-  double* sX = fsm + LSZ;      // [WP * d]
+  // Lm: packed lower S_JJ / L of the wp real rows (rows padded to even length),
+  // then one zero row of 16 (stands for the implicit identity rows wp..WP-1
+  // of the 16-column blocking); sX: the wp points.  lsz = Lm doubles.
+  double* Lm = fsm;
+  const double* zrow = fsm + lsz - 16;
+  double* sX = fsm + lsz;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   __shared__ double s_inv[WP];
   __shared__ int sJ[WP];
@@ -443,12 +446,13 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
   if (tid == 0) {
     s_bad = 0;
     int o = 0;
-    for (int a = 0; a < WP; ++a) {
+    for (int a = 0; a < wp; ++a) {
       s_off[a] = o;
       o += (a + 2) & ~1;  // row a holds a+1 entries, padded to even
     }
-    s_off[WP] = o;
+    s_off[wp] = o;
   }
+  if (tid < 16) fsm[lsz - 16 + tid] = 0.0;
   for (int a = tid; a < wp; a += FT2) sJ[a] = col[beg + a];
   __syncthreads();
   for (int e = tid; e < wp * d; e += FT2) {
@@ -512,34 +516,38 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       }
     }
   }
-  for (int p = wp + tid; p < WP; p += FT2)
-    for (int q = 0; q <= p; ++q) Lm[s_off[p] + q] = (p == q) ? 1.0 : 0.0;
   __syncthreads();
-  // ---- 2. blocked right-looking Cholesky of diag(S_JJ, I) (WP x WP)
+  // ---- 2. blocked right-looking Cholesky of diag(S_JJ, I) in 16-column
+  // blocks; the identity rows wp..WP-1 are implicit (never stored: their
+  // entries left of the diagonal are 0 and stay 0)
+  auto rowp = [&](int a, int kb) -> const double* { return a < wp ? Lm + s_off[a] + kb : zrow; };
 #pragma unroll 1
-  for (int kb = 0; kb < WP; kb += 16) {
+  for (int kb = 0; kb < wp; kb += 16) {
     {  // diagonal block, every warp (warp 0 stores)
       double dr[16], myinv = 1.0;
-      const double* row = Lm + s_off[kb + lr] + kb;
+      const bool real = kb + lr < wp;
+      const double* row = rowp(kb + lr, kb);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) dr[c] = (c <= lr) ? row[c] : 0.0;
+      for (int c = 0; c < 16; ++c) dr[c] = (c <= lr) ? (real ? row[c] : (c == lr ? 1.0 : 0.0)) : 0.0;
       const bool bad = factor_diag16(dr, myinv, lr);
       __syncthreads();  // every warp has read the block before warp 0 overwrites it
       if (tid < 16) {
-        double* wrow = Lm + s_off[kb + tid] + kb;
+        if (kb + tid < wp) {
+          double* wrow = Lm + s_off[kb + tid] + kb;
 #pragma unroll
-        for (int c = 0; c < 16; ++c)
-          if (c <= tid) wrow[c] = dr[c];
+          for (int c = 0; c < 16; ++c)
+            if (c <= tid) wrow[c] = dr[c];
+        }
         s_inv[kb + tid] = myinv;
         if (bad) s_bad = 1;
       }
     }
     __syncthreads();
     const int r0 = kb + 16;
-    const int m = WP - r0;
+    const int m = wp - r0;
     if (m <= 0) break;
     // panel: rows a >= r0, columns kb..kb+15: x L_diag^T = A
-    for (int a = r0 + tid; a < WP; a += FT2) {
+    for (int a = r0 + tid; a < wp; a += FT2) {
       double x[16];
       double* row = Lm + s_off[a] + kb;
 #pragma unroll
@@ -551,7 +559,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         double sacc = x[c];
-        const double* lrow = Lm + s_off[kb + c] + kb;
+        const double* lrow = rowp(kb + c, kb);
 #pragma unroll
         for (int c2 = 0; c2 < c; ++c2) sacc = fma(-x[c2], lrow[c2], sacc);
         x[c] = sacc * s_inv[kb + c];
@@ -560,8 +568,8 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(x[c], x[c + 1]);
     }
     __syncthreads();
-    // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], a >= b >= r0, 4x4 tiles
-    const int mt = m >> 2;
+    // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], wp > a >= b >= r0, 4x4 tiles
+    const int mt = (m + 3) >> 2;
     const int ntile = mt * (mt + 1) / 2;
     for (int t = tid; t < ntile; t += FT2) {
       int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
@@ -573,8 +581,8 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       const double* pb[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        pa[r] = Lm + s_off[a0 + r] + kb;
-        pb[r] = Lm + s_off[b0 + r] + kb;
+        pa[r] = rowp(a0 + r, kb);
+        pb[r] = rowp(b0 + r, kb);
       }
       double acc[4][4];
 #pragma unroll
@@ -601,7 +609,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       for (int r = 0; r < 4; ++r)
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          if (b0 + c <= a0 + r) Lm[s_off[a0 + r] + b0 + c] -= acc[r][c];
+          if (b0 + c <= a0 + r && a0 + r < wp) Lm[s_off[a0 + r] + b0 + c] -= acc[r][c];
     }
     __syncthreads();
   }
@@ -632,18 +640,20 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
 }
 
 template <int MT>
-afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t row_hi, cudaStream_t st,
+afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t row_hi, int wcap, cudaStream_t st,
                          const double* X2, int d, KernelFn kf, double mu, const int64_t* rp, const int32_t* col,
                          const int* grp, const int* loc, const int* Ucount, const int2* Htab,
                          const int64_t* Doff, const double* D, double* gval, int* info) {
   constexpr int WP = MT * 16;
-  const size_t bytes = sizeof(double) * ((size_t)WP * (WP + 1) / 2 + WP + (size_t)WP * d);
+  const int wmax = std::min(WP, wcap);
+  const int lsz = ((wmax * (wmax + 1) / 2 + (wmax + 1) / 2 + 16) + 1) & ~1;
+  const size_t bytes = sizeof(double) * ((size_t)lsz + (size_t)wmax * d);
   auto kern = fsai_factor_kernel<MT>;
   AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   for (int64_t r0 = 0; r0 < N; r0 += 1 << 30) {
     const int64_t nr = std::min<int64_t>(N - r0, 1 << 30);
     kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, kf, mu, rp, col, grp, loc,
-                                          Ucount, Htab, Doff, D, gval, info);
+                                          Ucount, Htab, Doff, D, gval, info, lsz);
     AFN_LAUNCH_CHECK("fsai_factor_kernel");
   }
   return AFN_OK;
@@ -802,9 +812,9 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   kt_begin(KT_FSAI_CHOL, st);
   switch (MT) {
 #define AFN_FACTOR(M) \
-    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
     AFN_FACTOR(1) AFN_FACTOR(2) AFN_FACTOR(3) AFN_FACTOR(4) AFN_FACTOR(5) AFN_FACTOR(6) AFN_FACTOR(7)
-    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
 #undef AFN_FACTOR
   }
   if (s != AFN_OK) return s;
