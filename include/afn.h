@@ -73,6 +73,11 @@ enum { AFN_LANDMARKS_FPS = 0, AFN_LANDMARKS_UNIFORM = 1 };
  *   AFN_METHOD_FSAI     plain FSAI of K + mu I on the kNN pattern of all
  *                       points in the original order (k = 0)    */
 enum { AFN_METHOD_AFN = 0, AFN_METHOD_ALG2 = 1, AFN_METHOD_NYSTROM = 2, AFN_METHOD_FSAI = 3 };
+/* Order of the non-landmark points, which fixes "numbered less than i" of the
+ * FSAI pattern: ascending original index (reading R14) or the
+ * MaxMin order, i.e. FPS continued through all n points ("MaxMin
+ * Ordering"; needs FPS landmarks).                                          */
+enum { AFN_ORDER_INDEX = 0, AFN_ORDER_MAXMIN = 1 };
 
 /* Build parameters.  Cite: l, mu; k_cap "limit ... such as 2000"
  * (P:L209-210); w "the w-1 nearest neighbors" (w counts the
@@ -91,7 +96,7 @@ typedef struct {
   int32_t kernel;       /* AFN_KERNEL_*                                        */
   int32_t landmarks;    /* AFN_LANDMARKS_*                                     */
   int32_t method;       /* AFN_METHOD_*                                        */
-  int32_t reserved;     /* 0                                                   */
+  int32_t ordering;     /* AFN_ORDER_*: order of the non-landmark points         */
 } afn_params;
 
 /* Information about a built handle (host struct). */

@@ -339,7 +339,8 @@ def _landmarks(X, k, landmarks, fps_seed, rng_seed):
 
 
 def build_afn(X: np.ndarray, l: float, mu: float, k: int, w: int, fps_seed: int = 0,
-              kernel: str = "gaussian", landmarks: str = "fps", rng_seed: int = 0):
+              kernel: str = "gaussian", landmarks: str = "fps", rng_seed: int = 0,
+              ordering: str = "index"):
     """Build the AFN factors, paper-literal.
 
     * X_k by FPS; landmarks indexed first, the rest
@@ -353,11 +354,19 @@ def build_afn(X: np.ndarray, l: float, mu: float, k: int, w: int, fps_seed: int 
     X = np.asarray(X, dtype=np.float64)
     n = X.shape[0]
     k = int(min(k, n))  # k = 0: plain FSAI of K + mu I
-    idx, fill = _landmarks(X, k, landmarks, fps_seed, rng_seed)
-    mask = np.ones(n, bool)
-    mask[idx] = False
-    rest = np.nonzero(mask)[0].astype(np.int64)
-    perm = np.concatenate([idx, rest]).astype(np.int64)
+    if ordering == "maxmin":
+        # MaxMin ordering: FPS continued through all n points; the
+        # first k are the landmarks, the rest keep their FPS order
+        if landmarks != "fps":
+            raise ValueError("the MaxMin ordering continues FPS")
+        perm, fill_all = fps(X, n, fps_seed)
+        idx, fill = perm[:k], fill_all[:k]
+    else:  # ascending original index after the landmarks (R14)
+        idx, fill = _landmarks(X, k, landmarks, fps_seed, rng_seed)
+        mask = np.ones(n, bool)
+        mask[idx] = False
+        rest = np.nonzero(mask)[0].astype(np.int64)
+        perm = np.concatenate([idx, rest]).astype(np.int64)
     Xp = X[perm]
     X1, X2 = Xp[:k], Xp[k:]
     A11 = kernel_block(X1, X1, l, kernel) + mu * np.eye(k)
@@ -446,13 +455,13 @@ def choose_method(khat: int, k_threshold: int = 2000) -> str:
 
 
 def build_precond(X, l, mu, k, w, method="afn", kernel="gaussian", landmarks="fps",
-                  fps_seed=0, rng_seed=0):
+                  fps_seed=0, rng_seed=0, ordering="index"):
     """AFN (eq:factorized-form), Nystrom or plain FSAI (k = 0)."""
     if method == "nystrom":
         return build_nystrom(X, l, mu, k, fps_seed, kernel, landmarks, rng_seed)
     if method == "fsai":
-        return build_afn(X, l, mu, 0, w, fps_seed, kernel, landmarks, rng_seed)
-    return build_afn(X, l, mu, k, w, fps_seed, kernel, landmarks, rng_seed)
+        return build_afn(X, l, mu, 0, w, fps_seed, kernel, landmarks, rng_seed, ordering)
+    return build_afn(X, l, mu, k, w, fps_seed, kernel, landmarks, rng_seed, ordering)
 
 
 def apply_precond(B: dict, r: np.ndarray) -> np.ndarray:

@@ -30,6 +30,7 @@ COMM_ID_BYTES = 128
 KERNEL_GAUSSIAN, KERNEL_MATERN32 = 0, 1
 LANDMARKS_FPS, LANDMARKS_UNIFORM = 0, 1
 METHOD_AFN, METHOD_ALG2, METHOD_NYSTROM, METHOD_FSAI = 0, 1, 2, 3
+ORDER_INDEX, ORDER_MAXMIN = 0, 1
 _KERNELS = {"gaussian": KERNEL_GAUSSIAN, "matern32": KERNEL_MATERN32}
 
 
@@ -50,7 +51,7 @@ class Params(C.Structure):
                 ("k_adaptive", C.c_int32), ("w", C.c_int32), ("m", C.c_int32),
                 ("k_threshold", C.c_int32), ("fps_seed", C.c_int64), ("rng_seed", C.c_uint64),
                 ("kernel", C.c_int32), ("landmarks", C.c_int32), ("method", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("ordering", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -243,10 +244,10 @@ def afn_estimate_rank(X, l, m=0, rng_seed=0, k_threshold=2000, stream=None, kern
 
 
 def make_params(l, mu, k_cap, w, k_adaptive=False, m=0, k_threshold=2000, fps_seed=0, rng_seed=0,
-                kernel="gaussian", landmarks=LANDMARKS_FPS, method=METHOD_AFN):
+                kernel="gaussian", landmarks=LANDMARKS_FPS, method=METHOD_AFN, ordering=ORDER_INDEX):
     return Params(float(l), float(mu), int(k_cap), int(bool(k_adaptive)), int(w), int(m),
                   int(k_threshold), int(fps_seed), int(rng_seed), _kernel_id(kernel), int(landmarks),
-                  int(method), 0)
+                  int(method), int(ordering))
 
 
 def nccl_library_path():

@@ -614,7 +614,9 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   REQ(P.landmarks == AFN_LANDMARKS_FPS || P.landmarks == AFN_LANDMARKS_UNIFORM, "unknown landmarks %d",
       P.landmarks);
   REQ(P.method != AFN_METHOD_ALG2 || P.k_adaptive, "AFN_METHOD_ALG2 needs k_adaptive = 1");
-  REQ(P.reserved == 0, "reserved must be 0");
+  REQ(P.ordering == AFN_ORDER_INDEX || P.ordering == AFN_ORDER_MAXMIN, "unknown ordering %d", P.ordering);
+  REQ(P.ordering == AFN_ORDER_INDEX || P.landmarks == AFN_LANDMARKS_FPS,
+      "the MaxMin ordering continues FPS: it needs FPS landmarks");
   cudaStream_t st = (cudaStream_t)stream;
   int dev = 0;
   AFN_CUDA(cudaGetDevice(&dev));
@@ -662,7 +664,9 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   // FPS landmarks are nested (X_{k-1} in X_k): with an adaptive k the
   // FPS for min(k_cap, n) points runs on the build stream WHILE Alg. 1 runs on
   // a side stream; the first k of them are exactly FPS(k).
-  const int64_t kfps = (adaptive && P.landmarks == AFN_LANDMARKS_FPS) ? std::min<int64_t>(P.k_cap, n) : 0;
+  // MaxMin ordering: FPS through all n points, the first k are the landmarks
+  const bool maxmin = P.ordering == AFN_ORDER_MAXMIN;
+  const int64_t kfps = maxmin ? n : (adaptive && P.landmarks == AFN_LANDMARKS_FPS) ? std::min<int64_t>(P.k_cap, n) : 0;
   std::vector<int64_t*> idx(nlocal, nullptr);
   cudaEvent_t efps0, efps1;
   AFN_CUDA(cudaEventCreate(&efps0));
@@ -711,7 +715,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_begin(KT_ALG1, s2);
     TRY(alg1_run(X, n, d, kn, m, P.rng_seed, kthr, &h->a1, s2));
     kt_end(KT_ALG1, s2, 0.0);
-    if (kstop) {  // the running FPS may stop at min(k_cap, khat)
+    if (kstop && !maxmin) {  // the running FPS may stop at min(k_cap, khat)
       hk[1] = std::min<int64_t>(kfps, std::max<int64_t>(1, h->a1.khat));
       AFN_CUDA(cudaMemcpyAsync(kstop, hk + 1, sizeof(int64_t), cudaMemcpyHostToDevice, s2));
     }
@@ -775,8 +779,12 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     flag8_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(flag32, n, flag);
     AFN_LAUNCH_CHECK("flag8_kernel");
     TRY(ralloc(s, &s.perm, (size_t)n, st));
-    perm_kernel<<<1, 1024, 0, st>>>(flag, idx[q], n, k, s.perm);
-    AFN_LAUNCH_CHECK("perm_kernel");
+    if (maxmin) {  // the FPS order of all n points
+      AFN_CUDA(cudaMemcpyAsync(s.perm, idx[q], sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+    } else {
+      perm_kernel<<<1, 1024, 0, st>>>(flag, idx[q], n, k, s.perm);
+      AFN_LAUNCH_CHECK("perm_kernel");
+    }
     rfree(s, flag, st);
     rfree(s, flag32, st);
     TRY(ralloc(s, &s.Xp, (size_t)n * d, st));

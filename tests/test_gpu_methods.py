@@ -161,3 +161,23 @@ def test_emulated_ranks_new_methods(R, method):
     assert rel(aR.cpu().numpy(), a1.cpu().numpy()) <= 1e-6
     hR.close()
     comm.close()
+
+
+@pytest.mark.parametrize("n,l,mu,k,w,adaptive", [(1000, 1.0, 1e-4, 100, 50, False),
+                                                  (1500, 2.0, 1e-3, 200, 40, False),
+                                                  (2000, 1.0, 1e-4, 2000, 60, True)])
+def test_maxmin_ordering_parity(n, l, mu, k, w, adaptive):
+    """MaxMin ordering (f4): FPS through all n points fixes the order of
+    the non-landmark points; permutation bit-exact, G rows, apply, PCG."""
+    X, b = gen_small(n, 3, seed=13)
+    h = afn.afn_build(T(X), afn.make_params(l, mu, k, w, k_adaptive=adaptive, ordering=afn.ORDER_MAXMIN))
+    kk = h.info()["k"]
+    B = O.build_afn(X, l, mu, kk, w, ordering="maxmin")
+    _check_afn(h, B, n)
+    r = np.random.default_rng(2).standard_normal(n)
+    zo = np.empty(n)
+    zo[B["perm"]] = O.apply_afn(B, r[B["perm"]])
+    assert rel(h.apply(T(r)).cpu().numpy(), zo) <= 1e-10
+    a, rep = h.pcg_solve(T(b), tol=1e-4)
+    ao, ro, _ = O.afn_pcg_solve(X, b, l, mu, kk, w, B=B)
+    assert rep["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 2

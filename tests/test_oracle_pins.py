@@ -474,3 +474,20 @@ def test_algorithm2_threshold():
     """Alg. 2: AFN when k >= 2000, Nystrom below."""
     assert O.choose_method(2000) == "afn" and O.choose_method(1999) == "nystrom"
     assert O.choose_method(10, k_threshold=10) == "afn"
+
+
+def test_maxmin_ordering_is_fps_of_all_points():
+    """MaxMin ordering: the permutation is FPS run through all n points,
+    its first k entries are the FPS landmarks, and (Thm 3.3) the fill
+    distance of every prefix is non-increasing."""
+    X, _ = gen_points(300, 3, "cube", 4)
+    B = O.build_afn(X, 1.0, 1e-3, 40, 20, ordering="maxmin")
+    idx, _ = O.fps(X, 40, 0)
+    assert np.array_equal(B["perm"][:40], idx)
+    assert sorted(B["perm"].tolist()) == list(range(300))
+    _, fill = O.fps(X, 300, 0)
+    assert np.all(np.diff(fill) <= 0)
+    # pattern rows are the nearest earlier points in the MaxMin order
+    Xp = X[B["perm"]][40:]
+    for i in (0, 5, 100, 259):
+        assert np.array_equal(B["col"][B["row_ptr"][i]:B["row_ptr"][i + 1]], O.knn_row(Xp, i, 20))
