@@ -28,6 +28,7 @@ __all__ = [
     "fsai_rows", "build_afn", "apply_afn", "dense_B", "pcg", "afn_pcg_solve",
     "cg_solve", "kernel_from_d2", "uniform_landmarks", "build_nystrom", "apply_nystrom",
     "choose_method", "build_precond", "apply_precond", "KERNELS", "NYS_NU", "UNIFORM_SEED_XOR",
+    "build_ran", "apply_ran",
 ]
 
 KERNELS = ("gaussian", "matern32")
@@ -449,6 +450,33 @@ def apply_nystrom(N: dict, r: np.ndarray) -> np.ndarray:
     return r / mu - (A.T @ np.linalg.solve(inner, A @ r)) / (mu * mu)
 
 
+def build_ran(X: np.ndarray, l: float, mu: float, k: int, kernel: str = "gaussian",
+              landmarks: str = "uniform", fps_seed: int = 0, rng_seed: int = 0,
+              nu: float = NYS_NU):
+    """RAN comparison preconditioner: rank-k Nystrom approximation
+    on randomly sampled landmarks, K_nys = U Lam U^T its eigendecomposition,
+    lam_k the k-th largest eigenvalue.  K_nys as in build_nystrom (R30); its
+    eigenpairs from the thin SVD of F = K_{X,Xk} L^{-T}, L L^T = K11 + nu I
+    (K_nys = F F^T)."""
+    N = build_nystrom(X, l, mu, k, fps_seed, kernel, landmarks, rng_seed, nu)
+    k = N["k"]
+    C = np.vstack([N["K11"], N["K12"].T])  # K_{X, Xk} in the permuted order
+    L = np.linalg.cholesky(N["K11"] + nu * np.eye(k))
+    F = sla.solve_triangular(L, C.T, lower=True).T
+    U, sig, _ = np.linalg.svd(F, full_matrices=False)
+    lam = sig * sig
+    N.update(method="ran", U=U, lam=lam, lam_k=float(lam.min()))
+    return N
+
+
+def apply_ran(R: dict, r: np.ndarray) -> np.ndarray:
+    """(lam_k + mu) U (Lam + mu I)^{-1} U^T r + (I - U U^T) r."""
+    U, lam, lam_k, mu = R["U"], R["lam"], R["lam_k"], R["mu"]
+    r = np.asarray(r, dtype=np.float64)
+    Ur = U.T @ r
+    return (lam_k + mu) * (U @ (Ur / (lam + mu))) + r - U @ Ur
+
+
 def choose_method(khat: int, k_threshold: int = 2000) -> str:
     """Algorithm 2: AFN if the estimated rank is >= 2000, else Nystrom."""
     return "afn" if khat >= k_threshold else "nystrom"
@@ -459,6 +487,8 @@ def build_precond(X, l, mu, k, w, method="afn", kernel="gaussian", landmarks="fp
     """AFN (eq:factorized-form), Nystrom or plain FSAI (k = 0)."""
     if method == "nystrom":
         return build_nystrom(X, l, mu, k, fps_seed, kernel, landmarks, rng_seed)
+    if method == "ran":
+        return build_ran(X, l, mu, k, kernel, landmarks, fps_seed, rng_seed)
     if method == "fsai":
         return build_afn(X, l, mu, 0, w, fps_seed, kernel, landmarks, rng_seed, ordering)
     return build_afn(X, l, mu, k, w, fps_seed, kernel, landmarks, rng_seed, ordering)
@@ -467,6 +497,8 @@ def build_precond(X, l, mu, k, w, method="afn", kernel="gaussian", landmarks="fp
 def apply_precond(B: dict, r: np.ndarray) -> np.ndarray:
     if B.get("method") == "nystrom":
         return apply_nystrom(B, r)
+    if B.get("method") == "ran":
+        return apply_ran(B, r)
     return apply_afn(B, r)
 
 

@@ -491,3 +491,23 @@ def test_maxmin_ordering_is_fps_of_all_points():
     Xp = X[B["perm"]][40:]
     for i in (0, 5, 100, 259):
         assert np.array_equal(B["col"][B["row_ptr"][i]:B["row_ptr"][i + 1]], O.knn_row(Xp, i, 20))
+
+
+def test_ran_eigendecomposition_and_exact_limit():
+    """RAN: U Lam U^T reproduces the explicit K_nys, lam_k is its k-th
+    largest eigenvalue (dense eigvalsh), and with every point a landmark the
+    preconditioner is (lam_n + mu)(K + mu I)^{-1}, so PCG stops at once."""
+    X, _ = gen_points(200, 3, "cube", 6, edge=5.0)
+    R = O.build_ran(X, 1.0, 1e-2, 60)
+    Xp = R["Xp"]
+    C = O.kernel_block(Xp, Xp[:60], 1.0)
+    Knys = C @ np.linalg.solve(R["K11"] + R["nu"] * np.eye(60), C.T)
+    assert np.allclose(R["U"] @ np.diag(R["lam"]) @ R["U"].T, Knys, atol=1e-10 * np.abs(Knys).max())
+    ev = np.sort(np.linalg.eigvalsh(Knys))[::-1]
+    assert abs(ev[59] - R["lam_k"]) <= 1e-8 * ev[0]
+    r = np.random.default_rng(3).standard_normal(200)
+    s = np.random.default_rng(4).standard_normal(200)
+    assert abs(s @ O.apply_ran(R, r) - r @ O.apply_ran(R, s)) <= 1e-9 * np.linalg.norm(r) * np.linalg.norm(s)
+    b = np.random.default_rng(5).standard_normal(200)
+    a, rep, _ = O.afn_pcg_solve(X, b, 1.0, 1e-2, 200, 10, method="ran", tol=1e-8)
+    assert rep["iterations"] <= 2
