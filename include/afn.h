@@ -71,8 +71,12 @@ enum { AFN_LANDMARKS_FPS = 0, AFN_LANDMARKS_UNIFORM = 1 };
  *   AFN_METHOD_NYSTROM  Nystrom preconditioner K_nys + mu I
  *                       applied exactly through an equivalent stable SMW form
  *   AFN_METHOD_FSAI     plain FSAI of K + mu I on the kNN pattern of all
- *                       points in the original order (k = 0)    */
-enum { AFN_METHOD_AFN = 0, AFN_METHOD_ALG2 = 1, AFN_METHOD_NYSTROM = 2, AFN_METHOD_FSAI = 3 };
+ *                       points in the original order (k = 0)
+ *   AFN_METHOD_RAN      the paper's RAN comparison preconditioner:
+ *                       (lam_k + mu) U (Lam + mu I)^{-1} U^T + (I - U U^T) for
+ *                       K_nys = U Lam U^T on k landmarks (use uniform ones)  */
+enum { AFN_METHOD_AFN = 0, AFN_METHOD_ALG2 = 1, AFN_METHOD_NYSTROM = 2, AFN_METHOD_FSAI = 3,
+       AFN_METHOD_RAN = 4 };
 /* Order of the non-landmark points, which fixes "numbered less than i" of the
  * FSAI pattern: ascending original index (reading R14) or the
  * MaxMin order, i.e. FPS continued through all n points ("MaxMin

@@ -29,7 +29,7 @@ STATUS = {0: "AFN_OK", 1: "AFN_ERR_ARG", 2: "AFN_ERR_CUDA", 3: "AFN_ERR_NOMEM",
 COMM_ID_BYTES = 128
 KERNEL_GAUSSIAN, KERNEL_MATERN32 = 0, 1
 LANDMARKS_FPS, LANDMARKS_UNIFORM = 0, 1
-METHOD_AFN, METHOD_ALG2, METHOD_NYSTROM, METHOD_FSAI = 0, 1, 2, 3
+METHOD_AFN, METHOD_ALG2, METHOD_NYSTROM, METHOD_FSAI, METHOD_RAN = 0, 1, 2, 3, 4
 ORDER_INDEX, ORDER_MAXMIN = 0, 1
 _KERNELS = {"gaussian": KERNEL_GAUSSIAN, "matern32": KERNEL_MATERN32}
 

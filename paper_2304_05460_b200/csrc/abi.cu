@@ -277,6 +277,8 @@ struct RankSt {
   // local order), RinvT = R^{-T} with R R^T = mu I + F^T F
   double* F = nullptr;
   double* RinvT = nullptr;
+  // RAN (AFN_METHOD_RAN): R1invT = R1^{-T}, R1 R1^T = F^T F + nu I
+  double* R1invT = nullptr;
   std::vector<void*> allocs;
 };
 
@@ -286,7 +288,8 @@ struct afn_handle_s {
   int d = 0;
   double l = 0, mu = 0;
   Kern kn{};
-  int method = AFN_METHOD_AFN;  // the preconditioner built (AFN, NYSTROM or FSAI)
+  int method = AFN_METHOD_AFN;  // the preconditioner built (AFN, NYSTROM, FSAI or RAN)
+  double lam_k = 0.0;           // RAN: k-th largest eigenvalue of K_nys
   afn_params params{};
   Alg1Result a1{};
   const Comm* comm = nullptr;  // not owned; null = single GPU
@@ -514,9 +517,57 @@ afn_status apply_nystrom_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   return AFN_OK;
 }
 
+// RAN: z = (lam_k + mu) U (Lam + mu I)^{-1} U^T r + (I - U U^T) r with
+// K_nys = U Lam U^T = F F^T, i.e. with G = F^T F:
+//   z = r + F ((lam_k + mu) (G + mu I)^{-1} G^{-1} - G^{-1}) F^T r.
+template <class RF, class ZF>
+afn_status apply_ran_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
+  const int64_t k = h->k;
+  const int R = h->R;
+  for (auto& s : h->rk) {  // t = F^T r (own rows)
+    const double* r = r_of(s);
+    double* tdst = R == 1 ? s.tvec : s.kpart + (size_t)s.rank * k;
+    const Seg2 g = s.own;
+    if (g.size() == 0) {
+      AFN_CUDA(cudaMemsetAsync(tdst, 0, sizeof(double) * k, st));
+    } else if (g.a0 + g.na == g.b0 || g.nb == 0) {
+      TRY(gemv_t(s.F, g.size(), k, r + g.a0, nullptr, 1.0, tdst, s.gws, st));
+    } else if (g.na == 0) {
+      TRY(gemv_t(s.F, g.nb, k, r + g.b0, nullptr, 1.0, tdst, s.gws, st));
+    } else {
+      TRY(gemv_t(s.F, g.na, k, r + g.a0, nullptr, 1.0, s.vvec, s.gws, st));
+      TRY(gemv_t(s.F + (size_t)g.na * k, g.nb, k, r + g.b0, s.vvec, 1.0, tdst, s.gws, st));
+    }
+  }
+  if (R > 1) {
+    TRY(exchange(h, [](RankSt& s) { return s.kpart; },
+                 [&](int s) { return RankRanges{{8 * (size_t)s * k, 8 * (size_t)k}}; }, st));
+    for (auto& s : h->rk) {
+      TRY(combine_sub(s.kpart, R, k, nullptr, s.tvec, st));
+      TRY(vec_scale(s.tvec, -1.0, s.tvec, seg_range(0, k), st));
+    }
+  }
+  for (auto& s : h->rk) {
+    const double* r = r_of(s);
+    double* z = z_of(s);
+    // a = G^{-1} t ; b = (G + mu I)^{-1} a ; w = (lam_k + mu) b - a
+    TRY(gemv_t(s.R1invT, k, k, s.tvec, nullptr, 1.0, s.uvec, s.gws, st));
+    TRY(gemv_n(s.R1invT, k, k, s.uvec, nullptr, 1.0, s.vvec, st));  // a (vvec)
+    TRY(gemv_t(s.RinvT, k, k, s.vvec, nullptr, 1.0, s.uvec, s.gws, st));
+    TRY(gemv_n(s.RinvT, k, k, s.uvec, nullptr, h->lam_k + h->mu, s.tvec, st));  // (lam_k+mu) b
+    TRY(vec_axpby(s.tvec, -1.0, s.vvec, 1.0, seg_range(0, k), st));              // w (tvec)
+    const Seg2 g = s.own;
+    if (g.na > 0) TRY(gemv_n(s.F, g.na, k, s.tvec, nullptr, 1.0, z + g.a0, st));
+    if (g.nb > 0) TRY(gemv_n(s.F + (size_t)g.na * k, g.nb, k, s.tvec, nullptr, 1.0, z + g.b0, st));
+    TRY(vec_axpby(z, 1.0, r, 1.0, g, st));  // z = F w + r
+  }
+  return AFN_OK;
+}
+
 template <class RF, class ZF>
 afn_status apply_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   if (h->method == AFN_METHOD_NYSTROM) return apply_nystrom_perm(h, r_of, z_of, st);
+  if (h->method == AFN_METHOD_RAN) return apply_ran_perm(h, r_of, z_of, st);
   return apply_afn_perm(h, r_of, z_of, st);
 }
 
@@ -584,6 +635,46 @@ afn_status build_nystrom(afn_handle h, cudaStream_t st) {
       TRY(vec_scale(Gm[q2], -1.0, Gm[q2], seg_range(0, k * k), st));
     }
   }
+  if (h->method == AFN_METHOD_RAN) {
+    // G^{-1} (G + nu I = R1 R1^T) and lambda_k = lambda_min(G) (the nonzero
+    // eigenvalues of K_nys = F F^T are those of G = F^T F): power iteration
+    // on G^{-1} = R1^{-T} R1^{-1}, then the Rayleigh quotient of G
+    for (size_t q = 0; q < h->rk.size(); ++q) {
+      RankSt& s = h->rk[q];
+      double* G1;
+      TRY(ralloc(s, &G1, (size_t)k * k, st));
+      AFN_CUDA(cudaMemcpyAsync(G1, Gm[q], sizeof(double) * k * k, cudaMemcpyDeviceToDevice, st));
+      TRY(add_diag(G1, k, AFN_NYS_NU, st));
+      TRY(potrf_lower(G1, k, s.dinfo + 1, st));
+      TRY(ralloc(s, &s.R1invT, (size_t)k * k, st));
+      TRY(trsm_linvt(G1, k, s.R1invT, st));
+      rfree(s, G1, st);
+      double *v, *y, *sc2, *gw, *dw;
+      unsigned* dc;
+      TRY(ralloc(s, &v, (size_t)k, st));
+      TRY(ralloc(s, &y, (size_t)k, st));
+      TRY(ralloc(s, &sc2, 4, st));
+      TRY(ralloc(s, &gw, (size_t)gemv_t_ws(k, k), st));
+      TRY(ralloc(s, &dw, (size_t)dot_ws(), st));
+      TRY(ralloc(s, &dc, 4, st));
+      AFN_CUDA(cudaMemsetAsync(dc, 0, sizeof(unsigned) * 4, st));
+      TRY(vec_fill(v, 1.0, k, st));
+      const int iters = 400;
+      for (int it = 0; it < iters; ++it) {
+        TRY(gemv_t(s.R1invT, k, k, v, nullptr, 1.0, y, gw, st));  // y = R1^{-1} v
+        TRY(gemv_n(s.R1invT, k, k, y, nullptr, 1.0, v, st));      // v = R1^{-T} y
+        TRY(dot(v, v, seg_range(0, k), sc2, dw, dc, st));
+        TRY(vec_scale_rsqrt(v, sc2, k, st));                      // v /= ||v||
+      }
+      TRY(gemv_n(Gm[q], k, k, v, nullptr, 1.0, y, st));
+      TRY(dot(v, y, seg_range(0, k), sc2 + 1, dw, dc, st));
+      double hv[2];
+      AFN_CUDA(cudaMemcpyAsync(hv, sc2, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+      AFN_CUDA(cudaStreamSynchronize(st));
+      h->lam_k = hv[1];  // v has unit norm
+      for (void* t : {(void*)v, (void*)y, (void*)sc2, (void*)gw, (void*)dw, (void*)dc}) rfree(s, t, st);
+    }
+  }
   for (size_t q = 0; q < h->rk.size(); ++q) {
     RankSt& s = h->rk[q];
     TRY(add_diag(Gm[q], k, h->mu, st));
@@ -605,7 +696,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   const afn_params P = *prm;
   REQ(P.l > 0 && std::isfinite(P.l), "l must be > 0");
   REQ(P.mu > 0 && std::isfinite(P.mu), "mu must be > 0");
-  REQ(P.method >= AFN_METHOD_AFN && P.method <= AFN_METHOD_FSAI, "unknown method %d", P.method);
+  REQ(P.method >= AFN_METHOD_AFN && P.method <= AFN_METHOD_RAN, "unknown method %d", P.method);
   REQ(P.k_cap >= 1 || P.method == AFN_METHOD_FSAI, "k_cap must be >= 1");
   REQ(P.w >= 1 && P.w <= 128, "w must be in 1..128");
   REQ(P.fps_seed >= 0 && P.fps_seed < n, "need 0 <= fps_seed < n");
@@ -659,6 +750,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   const int kthr = P.k_threshold > 0 ? P.k_threshold : 2000;
   h->method = P.method == AFN_METHOD_NYSTROM ? AFN_METHOD_NYSTROM
               : P.method == AFN_METHOD_FSAI  ? AFN_METHOD_FSAI
+              : P.method == AFN_METHOD_RAN   ? AFN_METHOD_RAN
                                              : AFN_METHOD_AFN;
   const bool adaptive = P.k_adaptive && P.method != AFN_METHOD_FSAI;
   // FPS landmarks are nested (X_{k-1} in X_k): with an adaptive k the
@@ -729,7 +821,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     if (P.method == AFN_METHOD_ALG2) h->method = h->a1.khat >= kthr ? AFN_METHOD_AFN : AFN_METHOD_NYSTROM;
   }
   if (h->method == AFN_METHOD_FSAI) k = 0;  // plain FSAI of K + mu I
-  const bool nys = h->method == AFN_METHOD_NYSTROM;
+  const bool nys = h->method == AFN_METHOD_NYSTROM || h->method == AFN_METHOD_RAN;  // F-form
   h->k = k;
   const int64_t N2 = nys ? 0 : n - k;  // the Nystrom branch has no Schur complement
   h->N2 = N2;

@@ -164,6 +164,9 @@ afn_status vec_copy(double* y, const double* x, Seg2 g, cudaStream_t st);
 afn_status vec_axpby(double* y, double a, const double* x, double b, Seg2 g, cudaStream_t st);
 // y = a x over g
 afn_status vec_scale(double* y, double a, const double* x, Seg2 g, cudaStream_t st);
+// y[i] = v ; y *= 1/sqrt(*s) (s device scalar)
+afn_status vec_fill(double* y, double v, int64_t n, cudaStream_t st);
+afn_status vec_scale_rsqrt(double* y, const double* s, int64_t n, cudaStream_t st);
 // A[i][i] += v (k x k row-major)
 afn_status add_diag(double* A, int64_t k, double v, cudaStream_t st);
 // sc[slot] = sum_{s < R} part[s * stride + slot] (rank order) for each slot in mask

@@ -220,6 +220,16 @@ __global__ void scale_kernel(double* __restrict__ y, double a, const double* __r
   }
 }
 
+__global__ void fill_kernel(double* __restrict__ y, double v, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = v;
+}
+__global__ void scale_rsqrt_kernel(double* __restrict__ y, const double* __restrict__ s, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const double f = 1.0 / sqrt(*s);
+  if (i < n) y[i] *= f;
+}
+
 __global__ void add_diag_kernel(double* __restrict__ A, int64_t k, double v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) A[i * k + i] += v;
@@ -328,6 +338,20 @@ afn_status vec_scale(double* y, double a, const double* x, Seg2 g, cudaStream_t 
   if (g.size() <= 0) return AFN_OK;
   scale_kernel<<<grid_for(g.size(), 256, 1184), 256, 0, st>>>(y, a, x, g);
   AFN_LAUNCH_CHECK("scale_kernel");
+  return AFN_OK;
+}
+
+afn_status vec_fill(double* y, double v, int64_t n, cudaStream_t st) {
+  if (n <= 0) return AFN_OK;
+  fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, v, n);
+  AFN_LAUNCH_CHECK("fill_kernel");
+  return AFN_OK;
+}
+
+afn_status vec_scale_rsqrt(double* y, const double* s, int64_t n, cudaStream_t st) {
+  if (n <= 0) return AFN_OK;
+  scale_rsqrt_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, s, n);
+  AFN_LAUNCH_CHECK("scale_rsqrt_kernel");
   return AFN_OK;
 }
 

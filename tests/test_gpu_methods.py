@@ -181,3 +181,27 @@ def test_maxmin_ordering_parity(n, l, mu, k, w, adaptive):
     a, rep = h.pcg_solve(T(b), tol=1e-4)
     ao, ro, _ = O.afn_pcg_solve(X, b, l, mu, kk, w, B=B)
     assert rep["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 2
+
+
+@pytest.mark.parametrize("n,l,mu,k,R", [(1000, 2.0, 1e-2, 150, 1), (1500, 1.0, 1e-3, 300, 1),
+                                        (300, 1.0, 1e-2, 300, 1), (1000, 2.0, 1e-2, 150, 3)])
+def test_ran_parity(n, l, mu, k, R):
+    """RAN (f3): lambda_k and the apply against the oracle's SVD route,
+    PCG iterations +-2; k = n gives the scaled exact inverse (one iteration)."""
+    X, b = gen_small(n, 3, seed=17)
+    prm = afn.make_params(l, mu, k, 10, landmarks=afn.LANDMARKS_UNIFORM, method=afn.METHOD_RAN)
+    comm = afn.Comm.emulated(R) if R > 1 else None
+    h = afn.afn_build(T(X), prm, comm=comm)
+    assert h.info()["method"] == afn.METHOD_RAN
+    Ro = O.build_ran(X, l, mu, k)
+    assert np.array_equal(h.copy_out(afn.OUT_PERM), Ro["perm"])
+    r = np.random.default_rng(3).standard_normal(n)
+    zo = np.empty(n)
+    zo[Ro["perm"]] = O.apply_ran(Ro, r[Ro["perm"]])
+    assert rel(h.apply(T(r)).cpu().numpy(), zo) <= 1e-8
+    a, rep = h.pcg_solve(T(b), tol=1e-4)
+    ao, ro, _ = O.afn_pcg_solve(X, b, l, mu, k, 10, B=Ro)
+    assert rep["converged"] and abs(rep["iterations"] - ro["iterations"]) <= 2
+    if k == n:
+        assert rep["iterations"] <= 2
+    h.close()
