@@ -87,9 +87,11 @@ __device__ __forceinline__ double exp2_neg(double s, const double* tab) {
   p = fma(p, f, AFN_E2C0);
   p = (p * tab[(n256 >> 4) & 15]) * tab[16 + (n256 & 15)];
   int hi = __double2hiint(p) + ((n256 >> 8) << 20);
-  double r = __hiloint2double(hi, __double2loint(p));
-  // s >= 1020 (hi word of 1020.0 is 0x408FE000) -> +0; also covers huge s / inf
-  return (__double2hiint(s) >= 0x408FE000) ? 0.0 : r;
+  // s >= 1020 (hi word of 1020.0 is 0x408FE000) -> clear the high word only:
+  // the result is +0 or a denormal below 2^-1042 (absolute error < 1e-313);
+  // also covers huge s / inf.  One select instead of two.
+  hi = (__double2hiint(s) >= 0x408FE000) ? 0 : hi;
+  return __hiloint2double(hi, __double2loint(p));
 }
 
 #define AFN_SQRT3 0x1.bb67ae8584caap+0

@@ -74,7 +74,7 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
       s_col[e] = val;
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll 4
     for (int j = 0; j < tcn; ++j) {
       double xj[CS];
 #pragma unroll
