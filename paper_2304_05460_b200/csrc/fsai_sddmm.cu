@@ -371,6 +371,135 @@ __global__ void __launch_bounds__(256, (GA <= 16 && BC <= 2) ? 2 : 1) group_gemm
   }
 }
 
+// Same product with 4 x 8 register tiles (GA = 16 or 32): thread (warp w,
+// lane) owns rows 4 rg + r (rg = lane % RG, RG = GA/4, r < 4) and columns
+// cb + q (cb = 8 (w CGW + lane / RG), CGW = 32/RG column groups per warp,
+// q < 8) of a pass of UTP = 64 CGW columns.  Per k-pair a thread issues
+// 4 + 8 LDS.128 for 64 DFMA (the 16 x 2 layout: 18), and every LDS is one
+// wavefront: W_g rows are stored in the order (r, rg) so the RG row groups of
+// a read are contiguous, and column u sits at the XOR-swizzled slot
+// (u & ~7) | ((u ^ (u >> 3)) & 7) so the column groups of a read hit
+// distinct 16-byte bank groups.  A warp whose columns are all past |U_g|
+// skips the arithmetic (the last pass of a group is partial).  GA = 32 reads
+// each W column once per 32 rows instead of 16 (L2 -> SM traffic is what
+// bounds the 16-row product: 2 DFMA per byte).
+__device__ __forceinline__ int t48_swz(int u) { return (u & ~7) | ((u ^ (u >> 3)) & 7); }
+
+template <int GA, int KC>
+__global__ void __launch_bounds__(256, 2) group_gemm48_kernel(const int* __restrict__ sorder, int64_t N,
+                                                              const double* __restrict__ W, int64_t k,
+                                                              const int* __restrict__ Ucount,
+                                                              const int* __restrict__ Ulist,
+                                                              const int64_t* __restrict__ Doff,
+                                                              const int64_t* __restrict__ Poff, int64_t G,
+                                                              double* __restrict__ D) {
+  constexpr int RG = GA / 4, CGW = 32 / RG, UTP = 64 * CGW;
+  extern __shared__ __align__(16) double gs[];
+  double* sA = gs;                   // [NST][KC/2][GA slots][2]
+  double* sB = gs + NST * KC * GA;   // [NST][KC/2][UTP slots][2]
+  __shared__ int s_a[GA];
+  __shared__ int s_u[UTP];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int rg = lane % RG, cgl = lane / RG;
+  const int64_t item = blockIdx.x;
+  int64_t glo = 0, ghi = G;
+  while (ghi - glo > 1) {
+    const int64_t mid = (glo + ghi) >> 1;
+    if (Poff[mid] <= item) glo = mid; else ghi = mid;
+  }
+  const int64_t g = glo;
+  const int pass = (int)(item - Poff[g]);
+  const int64_t m0 = g * GA;
+  const int cnt = (int)min((int64_t)GA, N - m0);
+  const int nu = Ucount[g];
+  double* Dg = D + Doff[g];
+  const int u0 = pass * UTP;
+  const int un = min(UTP, nu - u0);
+  if (tid < GA) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
+  for (int t = tid; t < UTP; t += 256) s_u[t] = t < un ? Ulist[g * UCAP + u0 + t] : -1;
+  __syncthreads();
+  const int64_t nch = (k + KC - 1) / KC;
+  const bool even = (k & 1) == 0;
+  auto issue = [&](int64_t ch, int buf) {
+    const int64_t c0 = ch * KC;
+    double* a = sA + buf * KC * GA;
+    double* b = sB + buf * KC * UTP;
+    for (int e = tid; e < (KC / 2) * GA; e += 256) {
+      const int j = e / (KC / 2), k2 = e - j * (KC / 2);
+      const int aj = s_a[j];
+      const int64_t c = c0 + 2 * k2;
+      double* dst = &a[(k2 * GA + (j & 3) * RG + (j >> 2)) * 2];
+      if (aj >= 0 && c + 1 < k && even) {
+        cpa16(dst, &W[(int64_t)aj * k + c]);
+      } else {
+        dst[0] = (aj >= 0 && c < k) ? W[(int64_t)aj * k + c] : 0.0;
+        dst[1] = (aj >= 0 && c + 1 < k) ? W[(int64_t)aj * k + c + 1] : 0.0;
+      }
+    }
+    for (int e = tid; e < (KC / 2) * un; e += 256) {  // idle columns are never read back
+      const int u = e / (KC / 2), k2 = e - u * (KC / 2);
+      const int bu = s_u[u];
+      const int64_t c = c0 + 2 * k2;
+      double* dst = &b[(k2 * UTP + t48_swz(u)) * 2];
+      if (c + 1 < k && even) {
+        cpa16(dst, &W[(int64_t)bu * k + c]);
+      } else {
+        dst[0] = c < k ? W[(int64_t)bu * k + c] : 0.0;
+        dst[1] = c + 1 < k ? W[(int64_t)bu * k + c + 1] : 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[r][q] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < NST - 1; ++s0) {
+    if (s0 < nch) issue(s0, s0);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const bool wact = wid * CGW * 8 < un;
+  const int cb = (wid * CGW + cgl) * 8;  // first column of this thread
+  const int sw = (cb >> 3) & 7;
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
+    __syncthreads();
+    const int64_t nx = ch + NST - 1;
+    if (nx < nch) issue(nx, (int)(nx % NST));
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    if (!wact) continue;
+    const double* a = sA + (int)(ch % NST) * KC * GA;
+    const double* b = sB + (int)(ch % NST) * KC * UTP;
+#pragma unroll
+    for (int k2 = 0; k2 < KC / 2; ++k2) {
+      double2 av[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) av[r] = *reinterpret_cast<const double2*>(&a[(k2 * GA + r * RG + rg) * 2]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 bq = *reinterpret_cast<const double2*>(&b[(k2 * UTP + cb + (q ^ sw)) * 2]);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          acc[r][q] = fma(av[r].x, bq.x, acc[r][q]);
+          acc[r][q] = fma(av[r].y, bq.y, acc[r][q]);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (!wact) return;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int j = rg * 4 + r;
+    if (j >= cnt) break;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (cb + q < un) Dg[(int64_t)j * nu + u0 + cb + q] = acc[r][q];
+  }
+}
+
 // ---------------------------------------------------------------- factor
 // One CTA (FT2 threads) per FSAI row i with pattern J (|J| = wp <= 16 MT,
 // ascending, i last).  CTAs take the rows in the spatial (cell) order of the
@@ -777,11 +906,14 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   int64_t* Poff;
   if ((s = get((void**)&pc, sizeof(int) * G)) != AFN_OK) return s;
   if ((s = get((void**)&Poff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
-  // columns of U per GEMM work item: 256 x BC.  BC = 4 reads the broadcast
-  // W_g operand once per 4 columns (0.16 LDS per DFMA instead of 0.28) but
-  // needs 244 registers (1 CTA/SM) and measured slower (C2 10.5 vs 7.0 ms)
+  // columns of U per GEMM work item.  Default: the 4 x 8 register-tiled
+  // kernel (512 columns per pass at GA = 16, 256 at GA = 32).  AFN_FSAI_T48=0
+  // selects the 16 x 2 layout (256 x BC columns); its BC = 4 reads the
+  // broadcast W_g operand once per 4 columns but needs 244 registers (1 CTA/SM)
+  // and measured slower (C2 10.5 vs 7.0 ms)
+  static const bool t48 = !(getenv("AFN_FSAI_T48") && atoi(getenv("AFN_FSAI_T48")) == 0);
   static const int BC = getenv("AFN_FSAI_BC") ? std::max(2, std::min(4, atoi(getenv("AFN_FSAI_BC")))) : 2;
-  const int ut = 256 * (BC >= 4 ? 4 : 2);
+  const int ut = t48 ? (GA == 32 ? 256 : 512) : 256 * (BC >= 4 ? 4 : 2);
   pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, ut, pc);
   AFN_LAUNCH_CHECK("pass_count_kernel");
   scan_i64_kernel<<<1, 1024, 0, st>>>(pc, G, 1, Poff);
@@ -794,9 +926,16 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   double* D;
   if ((s = get((void**)&D, sizeof(double) * (totD > 0 ? totD : 1))) != AFN_OK) return s;
   {
-    const int bytes = (int)(sizeof(double) * NST * KC2 * (GA + ut));
-    auto kern = GA == 32 ? (ut == 1024 ? group_gemm_kernel<32, 4> : group_gemm_kernel<32, 2>)
-                         : (ut == 1024 ? group_gemm_kernel<16, 4> : group_gemm_kernel<16, 2>);
+    int kc = KC2;
+    decltype(&group_gemm48_kernel<16, 8>) kern;
+    if (t48) {  // (launch_bounds(256, 1) with deeper stages measured slower: 8 warps/SM)
+      kc = GA == 32 ? 16 : 8;
+      kern = GA == 32 ? group_gemm48_kernel<32, 16> : group_gemm48_kernel<16, 8>;
+    } else {
+      kern = GA == 32 ? (ut == 1024 ? group_gemm_kernel<32, 4> : group_gemm_kernel<32, 2>)
+                      : (ut == 1024 ? group_gemm_kernel<16, 4> : group_gemm_kernel<16, 2>);
+    }
+    const int bytes = (int)(sizeof(double) * NST * kc * (GA + ut));
     AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0) {
