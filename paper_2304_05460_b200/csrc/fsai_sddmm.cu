@@ -518,24 +518,29 @@ __global__ void __launch_bounds__(256, 2) group_gemm48_kernel(const int* __restr
 constexpr int FT2 = 128;
 
 // Unblocked Cholesky of a 16x16 block held one row per lane (row lr =
-// lane & 15 in dr[0..lr]; lanes 16..31 mirror 0..15).  myinv = 1 / L_{lr,lr}.
-// Returns true on a non-positive pivot (replaced by 1 so the warp stays in step).
-__device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, int lr) {
+// lane & 15 in dr[0..lr]; lanes 16..31 mirror 0..15), one warp.  Column c is
+// broadcast through shared memory (col: 2 x 16 doubles, alternating so one
+// __syncwarp per step suffices): L[lr][c2] -= L[lr][c] L[c2][c] with
+// L[x][c] = A[x][c] / sqrt(A[c][c]).  myinv = 1 / L_{lr,lr}.  Returns true
+// on a non-positive pivot (replaced by 1 so the warp stays in step).
+__device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, int lane, double* col) {
+  const int lr = lane & 15;
   bool bad = false;
-#pragma unroll 16
+#pragma unroll
   for (int c = 0; c < 16; ++c) {
-    double piv = __shfl_sync(0xffffffffu, dr[c], c);
+    double* cb = col + (c & 1) * 16;
+    if (lane < 16) cb[lane] = dr[c];
+    __syncwarp();
+    double piv = cb[c];
     if (!(piv > 0.0)) { bad = true; piv = 1.0; }
     const double inv = rsqrt(piv);
+    const double lrc = dr[c] * inv;  // L[lr][c]
+    const double f = lrc * inv;      // L[lr][c] L[c2][c] = f A[c2][c]
     if (lr == c) myinv = inv;
-    dr[c] = (lr == c) ? piv * inv : (lr > c ? dr[c] * inv : dr[c]);
-#pragma unroll 16
-    for (int c2 = 1; c2 < 16; ++c2) {  // fixed trip count (c2 > c active) keeps dr[] in registers
-      if (c2 > c) {
-        const double v = __shfl_sync(0xffffffffu, dr[c], c2);
-        dr[c2] = (lr >= c2) ? fma(-dr[c], v, dr[c2]) : dr[c2];
-      }
-    }
+#pragma unroll
+    for (int c2 = c + 1; c2 < 16; ++c2)
+      if (lr >= c2) dr[c2] = fma(-f, cb[c2], dr[c2]);
+    dr[c] = (lr == c) ? piv * inv : (lr > c ? lrc : dr[c]);
   }
   return bad;
 }
@@ -550,8 +555,10 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
                                                          const int2* __restrict__ Htab,
                                                          const int64_t* __restrict__ Doff,
                                                          const double* __restrict__ D, double* __restrict__ gval,
-                                                         int* info, int lsz) {
+                                                         int* info, int lsz, long long* prof) {
   constexpr int WP = MT * 16;
+  // prof (debug, AFN_FACTOR_PROF): per CTA clock64 spans of the phases
+  long long pt0 = clock64(), pdiag = 0, ppanel = 0, ptrail = 0, pasm = 0, pm, ppro = 0, pgat = 0;
   extern __shared__ __align__(16) double fsm[];
   // Lm: packed lower S_JJ / L of the wp real rows (rows padded to even length),
   // then one zero row of 16 (stands for the implicit identity rows wp..WP-1
@@ -561,12 +568,13 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
   double* sX = fsm + lsz;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   __shared__ double s_inv[WP];
+  __shared__ __align__(16) double s_col[32];
   __shared__ int sJ[WP];
   __shared__ int s_off[WP + 1];
   __shared__ int s_g[WP];
   __shared__ int64_t s_db[WP];
   __shared__ int s_bad;
-  const int tid = threadIdx.x, lane = tid & 31, lr = lane & 15;
+  const int tid = threadIdx.x, lane = tid & 31, lr = lane & 15, wid = tid >> 5;
   const int64_t i = rorder[blockIdx.x];
   if (i < row_lo || i >= row_hi) return;  // another rank's row
   const int64_t beg = rp[i];
@@ -599,79 +607,96 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
   }
   __syncthreads();
   {
+    // entry e of the packed lower triangle <-> (p, q), q <= p; a thread takes
+    // B consecutive entries, (p, q) advanced incrementally.  Pass 1: B hash
+    // probes, then B D loads, Lm <- W_a . W_b.  Pass 2 (rolled, one copy of
+    // the kernel code): Lm <- K(x_a, x_b) + mu delta - Lm.
     constexpr int B = 8;
     const int ne = wp * (wp + 1) / 2;
+    if (prof) ppro = clock64() - pt0;
     for (int e0 = tid * B; e0 < ne; e0 += FT2 * B) {
-      int pp[B], qq[B];
+      if (prof) pm = clock64();
+      int p0 = (int)((sqrtf(8.0f * (float)e0 + 1.0f) - 1.0f) * 0.5f);
+      while (p0 * (p0 + 1) / 2 > e0) --p0;
+      while ((p0 + 1) * (p0 + 2) / 2 <= e0) ++p0;
+      const int q0 = e0 - p0 * (p0 + 1) / 2;
+      int pp[B], bb[B];
       unsigned hh[B];
       int2 hv[B];
+      {
+        int p = p0, q = q0;
 #pragma unroll
-      for (int t = 0; t < B; ++t) {
-        const int e = min(e0 + t, ne - 1);
-        int p = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-        while (p * (p + 1) / 2 > e) --p;
-        while ((p + 1) * (p + 2) / 2 <= e) ++p;
-        pp[t] = p;
-        qq[t] = e - p * (p + 1) / 2;
-        hh[t] = ((unsigned)sJ[qq[t]] * 2654435761u) & (HC - 1);
-        hv[t] = __ldg(&Htab[(int64_t)s_g[p] * HC + hh[t]]);
+        for (int t = 0; t < B; ++t) {
+          const bool ok = e0 + t < ne;
+          pp[t] = ok ? p : 0;
+          bb[t] = sJ[ok ? q : 0];
+          hh[t] = ((unsigned)bb[t] * 2654435761u) & (HC - 1);
+          hv[t] = __ldg(&Htab[(int64_t)s_g[pp[t]] * HC + hh[t]]);
+          if (++q > p) { ++p; q = 0; }
+        }
       }
       double gram[B];
 #pragma unroll
       for (int t = 0; t < B; ++t) {
-        const int b = sJ[qq[t]];
         const int2* H = Htab + (int64_t)s_g[pp[t]] * HC;
         int probe = 0;
-        while (hv[t].x != b && probe < HC) {  // b is in U_g by construction
+        while (hv[t].x != bb[t] && probe < HC) {  // b is in U_g by construction
           hh[t] = (hh[t] + 1) & (HC - 1);
           hv[t] = __ldg(&H[hh[t]]);
           ++probe;
         }
         // (never taken; a missing key poisons the row -> NOT_SPD, not a hang)
-        gram[t] = hv[t].x == b ? D[s_db[pp[t]] + hv[t].y] : CUDART_NAN;
+        gram[t] = hv[t].x == bb[t] ? D[s_db[pp[t]] + hv[t].y] : CUDART_NAN;
       }
+      {  // rows are padded to even length: slots from (p, q)
+        int p = p0, q = q0;
 #pragma unroll
-      for (int t = 0; t < B; ++t) {
-        if (e0 + t >= ne) break;
-        const int p = pp[t], q = qq[t];
-        double kv;
-        if (p == q) {
-          kv = 1.0 + mu;
-        } else {
-          const double sd = d2_exact_rt(&sX[p * d], &sX[q * d], d);
-          kv = kern_from_d2(kf, sd, s_tab);
+        for (int t = 0; t < B; ++t) {
+          if (e0 + t < ne) Lm[s_off[p] + q] = gram[t];
+          if (++q > p) { ++p; q = 0; }
         }
-        Lm[s_off[p] + q] = kv - gram[t];
+      }
+      if (prof) pgat += clock64() - pm;
+      int p = p0, q = q0;
+#pragma unroll 1  // (unrolled: 22 KB more code, slower -- instruction cache)
+      for (int t = 0; t < B && e0 + t < ne; ++t) {
+        const double kv = p == q ? 1.0 + mu : kern_from_d2(kf, d2_exact_rt(&sX[p * d], &sX[q * d], d), s_tab);
+        double* dst = &Lm[s_off[p] + q];
+        *dst = kv - *dst;
+        if (++q > p) { ++p; q = 0; }
       }
     }
   }
   __syncthreads();
+  if (prof) pasm = clock64() - pt0;
   // ---- 2. blocked right-looking Cholesky of diag(S_JJ, I) in 16-column
   // blocks; the identity rows wp..WP-1 are implicit (never stored: their
   // entries left of the diagonal are 0 and stay 0)
   auto rowp = [&](int a, int kb) -> const double* { return a < wp ? Lm + s_off[a] + kb : zrow; };
 #pragma unroll 1
   for (int kb = 0; kb < wp; kb += 16) {
-    {  // diagonal block, every warp (warp 0 stores)
+    if (prof) pm = clock64();
+    // diagonal block: one warp (the others wait at the barrier)
+    if (wid == 0) {
       double dr[16], myinv = 1.0;
       const bool real = kb + lr < wp;
       const double* row = rowp(kb + lr, kb);
 #pragma unroll
       for (int c = 0; c < 16; ++c) dr[c] = (c <= lr) ? (real ? row[c] : (c == lr ? 1.0 : 0.0)) : 0.0;
-      const bool bad = factor_diag16(dr, myinv, lr);
-      __syncthreads();  // every warp has read the block before warp 0 overwrites it
-      if (tid < 16) {
-        if (kb + tid < wp) {
-          double* wrow = Lm + s_off[kb + tid] + kb;
+      const bool bad = factor_diag16(dr, myinv, lane, s_col);
+      if (lane < 16) {
+        if (kb + lane < wp) {
+          double* wrow = Lm + s_off[kb + lane] + kb;
 #pragma unroll
           for (int c = 0; c < 16; ++c)
-            if (c <= tid) wrow[c] = dr[c];
+            if (c <= lane) wrow[c] = dr[c];
         }
-        s_inv[kb + tid] = myinv;
+        s_inv[kb + lane] = myinv;
         if (bad) s_bad = 1;
       }
     }
     __syncthreads();
+    if (prof) { const long long t = clock64(); pdiag += t - pm; pm = t; }
     const int r0 = kb + 16;
     const int m = wp - r0;
     if (m <= 0) break;
@@ -697,11 +722,12 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(x[c], x[c + 1]);
     }
     __syncthreads();
+    if (prof) { const long long t = clock64(); ppanel += t - pm; pm = t; }
     // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], wp > a >= b >= r0, 4x4 tiles
     const int mt = (m + 3) >> 2;
     const int ntile = mt * (mt + 1) / 2;
     for (int t = tid; t < ntile; t += FT2) {
-      int I = (int)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+      int I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
       while (I * (I + 1) / 2 > t) --I;
       while ((I + 1) * (I + 2) / 2 <= t) ++I;
       const int J = t - I * (I + 1) / 2;
@@ -741,6 +767,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
           if (b0 + c <= a0 + r && a0 + r < wp) Lm[s_off[a0 + r] + b0 + c] -= acc[r][c];
     }
     __syncthreads();
+    if (prof) ptrail += clock64() - pm;
   }
   if (s_bad) {
     if (tid == 0) atomicCAS(info, 0, (int)(i + 1));
@@ -766,6 +793,11 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
       if (j < t) rhs[r] = fma(-lrw[j], gt, rhs[r]);
     }
   }
+  if (prof && tid == 0) {
+    long long* o = prof + 8 * blockIdx.x;
+    o[0] = wp; o[1] = pasm; o[2] = pdiag; o[3] = ppanel; o[4] = ptrail;
+    o[5] = clock64() - pt0 - pasm - pdiag - ppanel - ptrail; o[6] = ppro; o[7] = pgat;
+  }
 }
 
 template <int MT>
@@ -779,11 +811,26 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
   const size_t bytes = sizeof(double) * ((size_t)lsz + (size_t)wmax * d);
   auto kern = fsai_factor_kernel<MT>;
   AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  // debug: AFN_FACTOR_PROF=file appends per-row phase cycles (wp, assembly,
+  // diagonal blocks, panels, trailing updates, back substitution, start)
+  static const char* pfile = getenv("AFN_FACTOR_PROF");
+  long long* prof = nullptr;
+  if (pfile && N <= (1 << 24)) AFN_CUDA(cudaMalloc(&prof, sizeof(long long) * 8 * N));
   for (int64_t r0 = 0; r0 < N; r0 += 1 << 30) {
     const int64_t nr = std::min<int64_t>(N - r0, 1 << 30);
     kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, kf, mu, rp, col, grp, loc,
-                                          Ucount, Htab, Doff, D, gval, info, lsz);
+                                          Ucount, Htab, Doff, D, gval, info, lsz, prof ? prof + 8 * r0 : nullptr);
     AFN_LAUNCH_CHECK("fsai_factor_kernel");
+  }
+  if (prof) {
+    std::vector<long long> h((size_t)8 * N);
+    AFN_CUDA(cudaMemcpyAsync(h.data(), prof, sizeof(long long) * 8 * N, cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaStreamSynchronize(st));
+    cudaFree(prof);
+    if (FILE* f = fopen(pfile, "ab")) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
   }
   return AFN_OK;
 }
