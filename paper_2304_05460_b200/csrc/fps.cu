@@ -381,6 +381,171 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
   cl.sync();  // no CTA leaves while its slots may still be read remotely
 }
 
+// Push variant of the cluster kernel: after its CTA-level argmax, warp 0 of
+// every CTA stores its winner slot (d2, index, point, early-stop sample) into
+// every CTA's inbox (st.shared::cluster) and arrives on that CTA's mbarrier
+// (release.cluster); each warp then waits on its own CTA's mbarrier and
+// reduces the CL slots from local shared memory.  One DSMEM store round trip
+// per step instead of a cluster barrier plus two DSMEM loads.  Inboxes and
+// mbarriers alternate with the step parity: a CTA can only write step t+2's
+// slot into an inbox after it has received every CTA's step t+1 slot, which
+// each CTA sends after it has finished reading its step t inbox.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, int r) {
+  unsigned o;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
+  return o;
+}
+__device__ __forceinline__ void st_cluster_f64(unsigned a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(unsigned a) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned a, unsigned ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(ph)
+      : "memory");
+}
+
+template <int DP, int P, int NT>
+__global__ void __launch_bounds__(NT, 1)
+fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
+                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop) {
+  constexpr int S = Slot<DP>::S + 1;  // d2, index, point, early-stop sample
+  constexpr int NW = NT / 32;
+  constexpr int CLX = 16;
+  __shared__ double s_w[NW][S];
+  __shared__ double s_in[2][CLX][S];
+  __shared__ __align__(8) unsigned long long s_bar[2];
+  cg::cluster_group cl = cg::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const int CL = (int)cl.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t stride = (int64_t)CL * NT;
+  const int64_t gtid = (int64_t)crank * NT + tid;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_bar[0])), "r"(CL) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_bar[1])), "r"(CL) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double pts[P][DP];
+  double mind[P];
+  double y[DP];
+#pragma unroll
+  for (int c = 0; c < DP; ++c) y[c] = c < d ? X[seed * d + c] : 0.0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int64_t i = gtid + s * stride;
+    if (i < n) {
+#pragma unroll
+      for (int c = 0; c < DP; ++c) pts[s][c] = c < d ? X[i * d + c] : 0.0;
+      mind[s] = (i == seed) ? -1.0 : d2_exact<DP>(pts[s], y);
+    } else {
+#pragma unroll
+      for (int c = 0; c < DP; ++c) pts[s][c] = 0.0;
+      mind[s] = -2.0;
+    }
+  }
+  if (crank == 0 && tid == 0) idx_out[0] = seed;
+  cl.sync();  // every CTA's mbarriers are initialised before the first push
+  unsigned ph0 = 0, ph1 = 0;
+  long long kend = k;  // rank 0's running early-stop sample
+  for (int64_t step = 1; step <= k; ++step) {
+    const int par = (int)(step & 1);
+    double bd = -3.0;
+    unsigned bi = 0xffffffffu;
+    int bs = 0;
+#pragma unroll
+    for (int s = 0; s < P; ++s)
+      if (mind[s] > bd) { bd = mind[s]; bi = (unsigned)(gtid + s * stride); bs = s; }
+    unsigned long long wkey;
+    unsigned widx;
+    warp_argmax_key(fps_key(bd), bi, wkey, widx);
+    if (bi == widx) {
+      s_w[wid][0] = bd;
+      s_w[wid][1] = __longlong_as_double((long long)widx);
+#pragma unroll
+      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pts[bs][c];
+    }
+    __syncthreads();
+    if (wid == 0) {
+      const double vd = lane < NW ? s_w[lane][0] : -3.0;
+      const unsigned vi = lane < NW ? (unsigned)__double_as_longlong(s_w[lane][1]) : 0xffffffffu;
+      unsigned long long k2;
+      unsigned i2;
+      warp_argmax_key(fps_key(vd), vi, k2, i2);
+      const int src = __ffs(__ballot_sync(0xffffffffu, lane < NW && vi == i2)) - 1;
+      if (crank == 0 && kstop != nullptr && (step & 7) == 0)
+        kend = min(kend, *reinterpret_cast<const volatile long long*>(kstop));
+      double msg[S];
+#pragma unroll
+      for (int c = 0; c < S - 1; ++c) msg[c] = s_w[src][c];
+      msg[S - 1] = __longlong_as_double(kend);
+      if (lane < CL) {  // lane j pushes to CTA j
+        const unsigned dst = mapa_u32(smem_u32(&s_in[par][crank][0]), lane);
+#pragma unroll
+        for (int c = 0; c < S; ++c) st_cluster_f64(dst + 8 * c, msg[c]);
+        mbar_arrive_remote(mapa_u32(smem_u32(&s_bar[par]), lane));
+      }
+    }
+    mbar_wait_parity(smem_u32(&s_bar[par]), par ? ph1 : ph0);
+    if (par) ph1 ^= 1; else ph0 ^= 1;
+    // every warp reduces the CL slots itself (no second CTA barrier)
+    const double gd = lane < CL ? s_in[par][lane][0] : -3.0;
+    const unsigned gi = lane < CL ? (unsigned)__double_as_longlong(s_in[par][lane][1]) : 0xffffffffu;
+    unsigned long long k3;
+    unsigned i3;
+    warp_argmax_key(fps_key(gd), gi, k3, i3);
+    const int src = __ffs(__ballot_sync(0xffffffffu, lane < CL && gi == i3)) - 1;
+    const double nd = s_in[par][src][0];
+    const long long ni = (long long)i3;
+    const long long kst = __double_as_longlong(s_in[par][0][S - 1]);
+    if (crank == 0 && tid == 0) {
+      fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
+      if (step < k) idx_out[step] = ni;
+    }
+    if (step >= kst) break;
+#pragma unroll
+    for (int c = 0; c < DP; ++c) y[c] = s_in[par][src][2 + c];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int64_t i = gtid + s * stride;
+      if (i < n) {
+        const double dd = d2_exact<DP>(pts[s], y);
+        mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
+      }
+    }
+  }
+  cl.sync();  // no CTA leaves while a push into it may be in flight
+}
+
+template <int DP, int P, int NT>
+afn_status launch_fps_push(const double* X, int64_t n, int d, int64_t k, int64_t seed,
+                           int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st) {
+  auto kern = fps_push_kernel<DP, P, NT>;
+  if (CL > 8) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop));
+  AFN_LAUNCH_CHECK("fps_push_kernel");
+  return AFN_OK;
+}
+
 template <int DP, int P, int NT>
 afn_status launch_fps_cluster(const double* X, int64_t n, int d, int64_t k, int64_t seed,
                               int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st) {
@@ -417,6 +582,13 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
       int P2 = 1;
       while (P2 < 4 && (n > (int64_t)16 * CNT * P2 || P2 < pmin)) P2 *= 2;
       const int CL = (int)((n + (int64_t)CNT * P2 - 1) / ((int64_t)CNT * P2));
+      // AFN_FPS_PUSH=0: the cluster-barrier exchange instead of the mbarrier pushes
+      static const bool push = !(getenv("AFN_FPS_PUSH") && atoi(getenv("AFN_FPS_PUSH")) == 0);
+      if (push) {
+        if (P2 == 1) return launch_fps_push<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+        if (P2 == 2) return launch_fps_push<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+        return launch_fps_push<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      }
       if (P2 == 1) return launch_fps_cluster<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       if (P2 == 2) return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       return launch_fps_cluster<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
