@@ -112,6 +112,17 @@ void kt_end(int id, cudaStream_t st, double work) {
   cudaEventRecord(e1, st);
   g_kt_pending.push_back({id, g_kt_open[id], e1, work});
 }
+// forget the last `count` pending timings of `id` (launches that were queued
+// but skipped on the device)
+void kt_drop_last(int id, int count) {
+  for (int64_t j = (int64_t)g_kt_pending.size() - 1; j >= 0 && count > 0; --j) {
+    if (g_kt_pending[j].id != id) continue;
+    g_kt_pool.push_back(g_kt_pending[j].e0);
+    g_kt_pool.push_back(g_kt_pending[j].e1);
+    g_kt_pending.erase(g_kt_pending.begin() + j);
+    --count;
+  }
+}
 void kt_collect() {
   for (auto& p : g_kt_pending) {
     cudaEventSynchronize(p.e1);
@@ -248,6 +259,7 @@ struct RankSt {
   double* Xs = nullptr;     // prescaled permuted points (kmv)
   double* L = nullptr;      // k x k lower (row-major)
   double* LinvT = nullptr;  // k x k, L^{-T}
+  double* Linv = nullptr;   // k x k, L^{-1} (AFN apply: t = L^{-1} r1 as a row-major GEMV)
   double* W = nullptr;      // own rows (hi - lo) x k of W = K21 L^{-T}
   int64_t* rp = nullptr;
   int32_t* col = nullptr;
@@ -442,7 +454,7 @@ afn_status apply_afn_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   TRY(exchange(h, r_of, [&](int s) { return landmark_ranges(h, s); }, st));
   for (auto& s : h->rk) {
     const double* r = r_of(s);
-    TRY(gemv_t(s.LinvT, k, k, r, nullptr, 1.0, s.tvec, s.gws, st));
+    TRY(gemv_n(s.Linv, k, k, r, nullptr, 1.0, s.tvec, st, 2));
     // u = r2 - W t (own rows)
     if (s.hi > s.lo) TRY(gemv_n(s.W, s.hi - s.lo, k, s.tvec, r + k + s.lo, -1.0, s.uvec + s.lo, st));
   }
@@ -468,9 +480,9 @@ afn_status apply_afn_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
                    [&](int s) { return RankRanges{{8 * (size_t)s * k, 8 * (size_t)k}}; }, st));
       for (auto& s : h->rk) TRY(combine_sub(s.kpart, R, k, s.tvec, s.vvec, st));
     }
-    for (auto& s : h->rk) TRY(gemv_n(s.LinvT, k, k, s.vvec, nullptr, 1.0, z_of(s), st));  // s1
+    for (auto& s : h->rk) TRY(gemv_n(s.LinvT, k, k, s.vvec, nullptr, 1.0, z_of(s), st, 1));  // s1
   } else {
-    for (auto& s : h->rk) TRY(gemv_n(s.LinvT, k, k, s.tvec, nullptr, 1.0, z_of(s), st));
+    for (auto& s : h->rk) TRY(gemv_n(s.LinvT, k, k, s.tvec, nullptr, 1.0, z_of(s), st, 1));
   }
   return AFN_OK;
 }
@@ -895,6 +907,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_end(KT_POTRF, st, (double)k * k * k / 3.0);
     kt_begin(KT_LINV, st);
     TRY(trsm_linvt(s.L, k, s.LinvT, st));
+    if (!nys) {
+      TRY(ralloc(s, &s.Linv, (size_t)k * k, st));
+      TRY(transpose_sq(s.LinvT, k, s.Linv, st));
+    }
     kt_end(KT_LINV, st, (double)k * k * k / 3.0);
   }
   AFN_CUDA(cudaEventRecord(ev[3], st));
@@ -1225,21 +1241,18 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     set_error("pinned host allocation failed");
     return AFN_ERR_NOMEM;
   }
-  cudaEvent_t e0, e1, km0, km1, ap0, ap1;
+  cudaEvent_t e0, e1, ap0, ap1;
   AFN_CUDA(cudaEventCreate(&e0));
   AFN_CUDA(cudaEventCreate(&e1));
-  AFN_CUDA(cudaEventCreate(&km0));
-  AFN_CUDA(cudaEventCreate(&km1));
   AFN_CUDA(cudaEventCreate(&ap0));
   AFN_CUDA(cudaEventCreate(&ap1));
   struct EvG {
-    cudaEvent_t e[6];
+    cudaEvent_t e[4];
     ~EvG() { for (auto x : e) cudaEventDestroy(x); }
-  } evg{{e0, e1, km0, km1, ap0, ap1}};
+  } evg{{e0, e1, ap0, ap1}};
   EvPairs cm;  // the per-iteration all-gathers of p (multi-rank)
   double mv_ms = 0.0, ap_ms = 0.0;
   int napply = 0;
-  bool ap_pending = false;
   auto sc_to_host = [&]() -> afn_status {
     AFN_CUDA(cudaMemcpyAsync(hsc, h->rk[0].sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
@@ -1263,69 +1276,113 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   int it = 0;
   double rel = nb > 0 ? 1.0 : 0.0;
   if (nb > 0) {
+    // Iterations are queued in chunks (1, 2, 4, then PCG_CHUNK) with the
+    // stopping test on the device (pcg_check: the same test as P:L788's loop,
+    // history written on the device); the matvec and apply kernels of queued
+    // iterations after the stop return at once (skip flag sc[SC_DONE]), x and
+    // r stay at the stopping iterate.  One host round trip per chunk instead
+    // of one per iteration.
+    static const int PCG_CHUNK = getenv("AFN_PCG_CHUNK") ? std::max(1, atoi(getenv("AFN_PCG_CHUNK"))) : 8;
+    double* dhist = nullptr;
+    TRY(dalloc((void**)&dhist, sizeof(double) * ((size_t)maxit + 1), st));
+    struct HFree {
+      double* p;
+      cudaStream_t st;
+      ~HFree() { dfree(p, st); }
+    } hfree{dhist, st};
+    for (auto& s : h->rk) AFN_CUDA(cudaMemsetAsync(s.sc + SC_DONE, 0, sizeof(double) * 2, st));
+    std::vector<cudaEvent_t> evs;  // per queued iteration: kmv begin/end, apply begin/end
+    struct EvFree {
+      std::vector<cudaEvent_t>* v;
+      ~EvFree() { for (auto e : *v) cudaEventDestroy(e); }
+    } evfree{&evs};
+    auto new_ev = [&]() -> cudaEvent_t {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      evs.push_back(e);
+      return e;
+    };
     AFN_CUDA(cudaEventRecord(ap0, st));
     TRY(apply());
     AFN_CUDA(cudaEventRecord(ap1, st));
-    ap_pending = true;
-    ++napply;
     int cur = SC_RZ0;
     for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, cur), s.dws, s.dcnt, st));
     TRY(reduce_slots(h, 1u << cur, st));
     for (auto& s : h->rk) TRY(vec_copy(s.p, s.z, s.own, st));
-    for (it = 1; it <= maxit; ++it) {
-      AFN_CUDA(cudaEventRecord(km0, st));
-      if (h->R > 1) {  // p: every rank's rows (the north star's per-iteration all-gather)
-        AFN_CUDA(cudaEventRecord(cm.next(), st));
-        TRY(exchange(h, [](RankSt& s) { return s.p; }, [&](int s) { return vec_ranges(h, s); }, st));
-        AFN_CUDA(cudaEventRecord(cm.next(), st));
-      }
-      kt_begin(KT_KMV, st);
-      for (auto& s : h->rk)
-        TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
-      kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0) / h->R);
-      AFN_CUDA(cudaEventRecord(km1, st));
-      for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
-      TRY(reduce_slots(h, 1u << SC_PQ, st));
-      for (auto& s : h->rk)
-        TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
-      TRY(reduce_slots(h, 1u << SC_RR, st));
-      TRY(sc_to_host());
-      mv_ms += ev_ms(km0, km1);
-      if (ap_pending) {
-        ap_ms += ev_ms(ap0, ap1);
-        ap_pending = false;
-      }
-      const double pq = hsc[SC_PQ];
-      if (!(pq > 0.0) || !std::isfinite(pq) || !std::isfinite(hsc[SC_RR])) {
-        R.breakdown = 1;
-        --it;
-        break;
-      }
-      rel = std::sqrt(hsc[SC_RR]) / nb;
-      if (R.history) R.history[it] = rel;
-      if (fixed_iters > 0) {
-        if (it >= fixed_iters) {
-          R.converged = rel <= tol;
-          break;
+    int queued = 0, chunk = 1, code = 0;
+    std::vector<cudaEvent_t> kmE, apE;
+    while (queued < maxit) {
+      const int upto = std::min(maxit, queued + chunk);
+      set_skip(h->rk[0].sc + SC_DONE);
+      struct SkipOff {
+        ~SkipOff() { set_skip(nullptr); }
+      } skipoff;
+      for (int t = queued + 1; t <= upto; ++t) {
+        kmE.push_back(new_ev());
+        AFN_CUDA(cudaEventRecord(kmE.back(), st));
+        if (h->R > 1) {  // p: every rank's rows (the north star's per-iteration all-gather)
+          AFN_CUDA(cudaEventRecord(cm.next(), st));
+          TRY(exchange(h, [](RankSt& s) { return s.p; }, [&](int s) { return vec_ranges(h, s); }, st));
+          AFN_CUDA(cudaEventRecord(cm.next(), st));
         }
-      } else if (rel <= tol) {
-        R.converged = 1;
-        break;
+        kt_begin(KT_KMV, st);
+        for (auto& s : h->rk)
+          TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+        kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0) / h->R);
+        kmE.push_back(new_ev());
+        AFN_CUDA(cudaEventRecord(kmE.back(), st));
+        for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
+        TRY(reduce_slots(h, 1u << SC_PQ, st));
+        for (auto& s : h->rk)
+          TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
+        TRY(reduce_slots(h, 1u << SC_RR, st));
+        for (auto& s : h->rk) TRY(pcg_check(s.sc, t, nb, tol, maxit, fixed_iters, dhist, st));
+        apE.push_back(new_ev());
+        AFN_CUDA(cudaEventRecord(apE.back(), st));
+        kt_begin(KT_APPLY, st);
+        TRY(apply());
+        kt_end(KT_APPLY, st, apply_bytes(h) / h->R);
+        apE.push_back(new_ev());
+        AFN_CUDA(cudaEventRecord(apE.back(), st));
+        const int nxt = cur ^ 1;
+        for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, nxt), s.dws, s.dcnt, st));
+        TRY(reduce_slots(h, 1u << nxt, st));
+        for (auto& s : h->rk) TRY(pcg_update_p(s.p, s.z, s.own, s.sc, nxt, cur, st));
+        cur = nxt;
       }
-      AFN_CUDA(cudaEventRecord(ap0, st));
-      kt_begin(KT_APPLY, st);
-      TRY(apply());
-      kt_end(KT_APPLY, st, apply_bytes(h) / h->R);
-      AFN_CUDA(cudaEventRecord(ap1, st));
-      ap_pending = true;
-      ++napply;
-      const int nxt = cur ^ 1;
-      for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, nxt), s.dws, s.dcnt, st));
-      TRY(reduce_slots(h, 1u << nxt, st));
-      for (auto& s : h->rk) TRY(pcg_update_p(s.p, s.z, s.own, s.sc, nxt, cur, st));
-      cur = nxt;
+      queued = upto;
+      TRY(sc_to_host());
+      code = (int)hsc[SC_DONE];
+      if (code != 0) break;
+      chunk = std::min(chunk * 2, PCG_CHUNK);
     }
-    if (it > maxit) it = maxit;
+    if (code == 0) {  // (cannot happen: the check stops at maxit)
+      set_error("pcg: no stop after maxit");
+      return AFN_ERR_STATE;
+    }
+    it = (int)hsc[SC_ITS];
+    R.breakdown = code == 2;
+    // launches that really ran: the matvec of every iteration up to the stop
+    // (breakdown: also the failing one), the apply of every iteration that
+    // continued (breakdown and maxit exhaustion: also the last one)
+    const int kmv_real = it + (code == 2 ? 1 : 0);
+    const int ap_real = it - 1 + (code == 2 || code == 3 ? 1 : 0);
+    napply = 1 + ap_real;
+    std::vector<double> hh((size_t)it + 1, 0.0);
+    if (it > 0) {
+      AFN_CUDA(cudaMemcpyAsync(hh.data(), dhist, sizeof(double) * ((size_t)it + 1), cudaMemcpyDeviceToHost, st));
+      AFN_CUDA(cudaStreamSynchronize(st));
+      rel = hh[it];
+    }
+    if (R.history)
+      for (int t = 1; t <= it; ++t) R.history[t] = hh[t];
+    R.converged = code == 1 && rel <= tol;
+    mv_ms = 0.0;
+    for (int t = 0; t < kmv_real; ++t) mv_ms += ev_ms(kmE[2 * t], kmE[2 * t + 1]);
+    ap_ms = ev_ms(ap0, ap1);
+    for (int t = 0; t < ap_real; ++t) ap_ms += ev_ms(apE[2 * t], apE[2 * t + 1]);
+    kt_drop_last(KT_KMV, queued - kmv_real);
+    kt_drop_last(KT_APPLY, queued - ap_real);
   } else {
     R.converged = 1;
   }
@@ -1347,7 +1404,6 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   R.relres = rel;
   R.relres_true = nb > 0 ? std::sqrt(hsc[SC_TMP]) / nb : 0.0;
   R.solve_ms = ev_ms(e0, e1);
-  if (ap_pending) ap_ms += ev_ms(ap0, ap1);
   R.matvec_ms = mv_ms;
   R.apply_ms = ap_ms;
   R.comm_ms = cm.total_ms();

@@ -135,8 +135,11 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
 
 // ---- BLAS-2 / SpMV / vectors (blas.cu) ------------------------------------
 // y = ybase + alpha * A x, A: R x C row-major (lda = C).  ybase may be null (0)
+// tri: 0 full, 1 A upper triangular (columns >= row), 2 lower (columns <= row);
+// the excluded triangle must be stored as zeros
 afn_status gemv_n(const double* A, int64_t R, int64_t C, const double* x, const double* ybase,
-                  double alpha, double* y, cudaStream_t st);
+                  double alpha, double* y, cudaStream_t st, int tri = 0);
+afn_status transpose_sq(const double* A, int64_t k, double* At, cudaStream_t st);
 // y = ybase + alpha * A^T x; ws >= gemv_t_ws(R, C) doubles
 int64_t gemv_t_ws(int64_t R, int64_t C);
 afn_status gemv_t(const double* A, int64_t R, int64_t C, const double* x, const double* ybase,
@@ -152,7 +155,13 @@ int64_t dot_ws();
 afn_status dot(const double* a, const double* b, Seg2 g, double* out, double* ws, unsigned* cnt,
                cudaStream_t st);
 // PCG scalar slots (device doubles): rz alternates between slots 0 and 1
-enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_N = 8 };
+enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_DONE = 6, SC_ITS = 7, SC_N = 8 };
+// Device-side skip flag for the apply / matvec kernels queued by the PCG loop
+// (kernels return at once when *flag != 0); nullptr = never skip.  Per host thread.
+void set_skip(const double* flag);
+const double* get_skip();
+afn_status pcg_check(double* sc, int it, double nb, double tol, int maxit, int fixed, double* hist,
+                     cudaStream_t st);
 // x += a p; r -= a q over g with a = sc[rz_slot]/sc[PQ] (0 if PQ <= 0); *rr = r.r over g
 afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, Seg2 g,
                          const double* sc, int rz_slot, double* rr, double* ws, unsigned* cnt,

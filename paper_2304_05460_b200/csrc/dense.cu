@@ -902,6 +902,14 @@ afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_
   return AFN_OK;
 }
 
+afn_status transpose_sq(const double* A, int64_t k, double* At, cudaStream_t st) {
+  if (k <= 0) return AFN_OK;
+  dim3 tg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
+  transpose_k_kernel<<<tg, dim3(32, 8), 0, st>>>(A, k, k, At);
+  AFN_LAUNCH_CHECK("transpose_k_kernel");
+  return AFN_OK;
+}
+
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st) {
   static const bool legacy = getenv("AFN_LINV_TRSM") != nullptr;
   if (!legacy) {

@@ -38,7 +38,8 @@ struct KmvTraits {
 template <int D, int RB, int KER>
 __global__ void __launch_bounds__(KMV_NT, 2)
 kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int64_t n,
-                   Seg2 rows, int64_t chunk_cols, double* __restrict__ partial) {
+                   Seg2 rows, int64_t chunk_cols, double* __restrict__ partial, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;  // PCG already stopped (device-side flag)
   constexpr int CS = KmvTraits<D>::CS;
   constexpr int KMV_TC = KmvTraits<D>::TC;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
@@ -111,7 +112,8 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
 
 __global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, Seg2 rows,
                                   const double* __restrict__ v, double mu, bool y_phys,
-                                  double* __restrict__ y) {
+                                  double* __restrict__ y, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
   const int64_t nrows = rows.size();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
@@ -133,8 +135,8 @@ void launch_partial(const KmvPlan& p, cudaStream_t st, const double* Xs, const d
   constexpr int RB = KmvTraits<D>::RB;
   const int64_t rows_per_cta = (int64_t)KMV_NT * RB;
   dim3 grid((unsigned)((rows.size() + rows_per_cta - 1) / rows_per_cta), (unsigned)p.chunks);
-  if (kind == 1) kmv_partial_kernel<D, RB, 1><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial);
-  else kmv_partial_kernel<D, RB, 0><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial);
+  if (kind == 1) kmv_partial_kernel<D, RB, 1><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial, get_skip());
+  else kmv_partial_kernel<D, RB, 0><<<grid, KMV_NT, 0, st>>>(Xs, v, n, rows, p.chunk_cols, partial, get_skip());
 }
 
 int rows_per_thread(int d) { return d <= 4 ? 4 : (d <= 8 ? 2 : 1); }
@@ -217,7 +219,7 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
   AFN_LAUNCH_CHECK("kmv_partial_kernel");
   const int nt = 256;
   kmv_reduce_kernel<<<(unsigned)((nrows + nt - 1) / nt), nt, 0, st>>>(partial, (int)p.chunks, rows, v,
-                                                                     mu, y_phys, y);
+                                                                     mu, y_phys, y, get_skip());
   AFN_LAUNCH_CHECK("kmv_reduce_kernel");
   return AFN_OK;
 }
