@@ -57,6 +57,10 @@ __global__ void gen_k11_kernel(const double* __restrict__ X1, int64_t k, int d, 
 // Each row is solved by 4 threads owning columns c = q (mod 4).
 __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
   const int tid = threadIdx.x;
+  // reciprocals of the diagonal first: a multiply (not a division) per step
+  __shared__ double s_rinv[NB];
+  if (tid < NB) s_rinv[tid] = 1.0 / Lbb[tid * TP + tid];
+  __syncthreads();
   const int r = tid >> 2, q = tid & 3;
   const int lane = tid & 31;
   double a[16];
@@ -70,7 +74,7 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
       const int j = 4 * s + qq;
       double xj = 0.0;
       if (q == qq) {
-        a[s] = a[s] / Lbb[j * TP + j];
+        a[s] = a[s] * s_rinv[j];
         xj = a[s];
       }
       xj = __shfl_sync(0xffffffffu, xj, (lane & ~3) | qq);
@@ -90,16 +94,17 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
 // Each of the 2080 lower entries is owned by one thread (in a register);
 // step j subtracts a_ij a_tj / p_j (unscaled columns, one barrier per step);
 // the scaling L_ij = a_ij / sqrt(p_j) is applied at the end.
-constexpr int DG_T = 1024;
+constexpr int DG_T = 1024;  // (256: 34 us, 512: 26 us, 1024: 25 us per 64-block on C2)
 __global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, int64_t kb, int* info) {
   __shared__ double s[NB * TP];
   const int nb = (int)min((int64_t)NB, k - kb);
   const int tid = threadIdx.x;
   constexpr int NE = NB * (NB + 1) / 2;  // 2080
-  int ei[3], et[3];
-  double av[3];
+  constexpr int NU = (NE + DG_T - 1) / DG_T;
+  int ei[NU], et[NU];
+  double av[NU];
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
+  for (int u = 0; u < NU; ++u) {
     const int e = tid + u * DG_T;
     int i = -1, t = 0;
     if (e < NE) {
@@ -121,7 +126,7 @@ __global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, 
     if (!(p > 0.0)) p = 1.0;  // breakdown is reported below; keep the values finite
     const double ip = 1.0 / p;
 #pragma unroll
-    for (int u = 0; u < 3; ++u) {
+    for (int u = 0; u < NU; ++u) {
       const int i = ei[u], t = et[u];
       if (i >= 0 && t > j) {
         av[u] = fma(-s[i * TP + j], s[t * TP + j] * ip, av[u]);
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, 
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
+  for (int u = 0; u < NU; ++u) {
     const int i = ei[u], t = et[u];
     if (i < 0 || i >= nb) continue;
     const double p = s[t * TP + t];
