@@ -12,6 +12,7 @@
 // Bit-exact with the readings R3: squared distances are sums in coordinate
 // order of individually rounded (x_c - y_c)^2; selected points carry mind = -1
 // and are never re-picked; ties go to the lowest index.
+#include <cstdio>
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -382,25 +383,30 @@ fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, in
 }
 
 // Push variant of the cluster kernel: after its CTA-level argmax, warp 0 of
-// every CTA stores its winner slot (d2, index, point, early-stop sample) into
-// every CTA's inbox (st.shared::cluster) and arrives on that CTA's mbarrier
-// (release.cluster); each warp then waits on its own CTA's mbarrier and
-// reduces the CL slots from local shared memory.  One DSMEM store round trip
-// per step instead of a cluster barrier plus two DSMEM loads.  Inboxes and
-// mbarriers alternate with the step parity: a CTA can only write step t+2's
-// slot into an inbox after it has received every CTA's step t+1 slot, which
-// each CTA sends after it has finished reading its step t inbox.
+// every CTA writes its winner slot (d2, index, point, early-stop sample) into
+// every CTA's inbox with st.async (asynchronous distributed-shared-memory
+// stores that complete bytes on the destination's mbarrier: no fence, no
+// round trip on the sender); each warp waits on its own CTA's mbarrier
+// (one local arrival with the expected byte count per phase) and reduces the
+// CL slots from local shared memory.  Inboxes and mbarriers alternate with
+// the step parity: a CTA can only write step t+2's slot into an inbox after it
+// has received every CTA's step t+1 slot, which each CTA sends after it has
+// finished reading its step t inbox.  The index / fill outputs and the
+// early-stop polling are done by other warps of CTA 0 (off the critical path
+// of warp 0, which pushes the next step).
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ unsigned mapa_u32(unsigned a, int r) {
   unsigned o;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
   return o;
 }
-__device__ __forceinline__ void st_cluster_f64(unsigned a, double v) {
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+__device__ __forceinline__ void st_async_v2(unsigned a, double x, double y, unsigned bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(a),
+               "d"(x), "d"(y), "r"(bar)
+               : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_remote(unsigned a) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+__device__ __forceinline__ void mbar_expect(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_parity(unsigned a, unsigned ph) {
   asm volatile(
@@ -415,23 +421,31 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned a, unsigned ph) {
 template <int DP, int P, int NT>
 __global__ void __launch_bounds__(NT, 1)
 fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
-                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop) {
-  constexpr int S = Slot<DP>::S + 1;  // d2, index, point, early-stop sample
+                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop,
+                long long* prof) {
+  // prof (debug, AFN_FPS_PROF): CTA 0 / warp 0 clock64 totals of the step phases
+  long long pc[6] = {0, 0, 0, 0, 0, 0}, pt = 0;
+  constexpr int KI = DP + 2;          // slot: d2, index, point (DP), early-stop sample (KI)
+  constexpr int S = (KI + 2) & ~1;    // even length (16-byte stores)
   constexpr int NW = NT / 32;
   constexpr int CLX = 16;
-  __shared__ double s_w[NW][S];
-  __shared__ double s_in[2][CLX][S];
+  static_assert(NW >= 3, "needs a pusher, a poller and an output warp");
+  __shared__ __align__(16) double s_w[NW][S];
+  __shared__ __align__(16) double s_in[2][CLX][S];
   __shared__ __align__(8) unsigned long long s_bar[2];
+  __shared__ long long s_kend;
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t stride = (int64_t)CL * NT;
   const int64_t gtid = (int64_t)crank * NT + tid;
+  const unsigned txb = (unsigned)(CL * S * 8);
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_bar[0])), "r"(CL) : "memory");
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_bar[1])), "r"(CL) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_bar[0])), "r"(1) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&s_bar[1])), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_kend = k;
   }
   double pts[P][DP];
   double mind[P];
@@ -453,10 +467,17 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
   }
   if (crank == 0 && tid == 0) idx_out[0] = seed;
   cl.sync();  // every CTA's mbarriers are initialised before the first push
+  if (tid == 0) {  // the local arrivals (with the inbox byte count) of steps 1 and 2
+    mbar_expect(smem_u32(&s_bar[1]), txb);
+    mbar_expect(smem_u32(&s_bar[0]), txb);
+  }
   unsigned ph0 = 0, ph1 = 0;
-  long long kend = k;  // rank 0's running early-stop sample
+  const bool pr = prof != nullptr && crank == 0 && tid == 0;
+  if (pr) pt = clock64();
   for (int64_t step = 1; step <= k; ++step) {
     const int par = (int)(step & 1);
+    if (crank == 0 && wid == 1 && lane == 0 && kstop != nullptr && (step & 7) == 0)  // early-stop poll
+      s_kend = min(s_kend, *reinterpret_cast<const volatile long long*>(kstop));
     double bd = -3.0;
     unsigned bi = 0xffffffffu;
     int bs = 0;
@@ -472,7 +493,9 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
 #pragma unroll
       for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pts[bs][c];
     }
+    if (pr) { const long long t = clock64(); pc[0] += t - pt; pt = t; }
     __syncthreads();
+    if (pr) { const long long t = clock64(); pc[1] += t - pt; pt = t; }
     if (wid == 0) {
       const double vd = lane < NW ? s_w[lane][0] : -3.0;
       const unsigned vi = lane < NW ? (unsigned)__double_as_longlong(s_w[lane][1]) : 0xffffffffu;
@@ -480,21 +503,23 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
       unsigned i2;
       warp_argmax_key(fps_key(vd), vi, k2, i2);
       const int src = __ffs(__ballot_sync(0xffffffffu, lane < NW && vi == i2)) - 1;
-      if (crank == 0 && kstop != nullptr && (step & 7) == 0)
-        kend = min(kend, *reinterpret_cast<const volatile long long*>(kstop));
-      double msg[S];
-#pragma unroll
-      for (int c = 0; c < S - 1; ++c) msg[c] = s_w[src][c];
-      msg[S - 1] = __longlong_as_double(kend);
       if (lane < CL) {  // lane j pushes to CTA j
-        const unsigned dst = mapa_u32(smem_u32(&s_in[par][crank][0]), lane);
+        double msg[S];
 #pragma unroll
-        for (int c = 0; c < S; ++c) st_cluster_f64(dst + 8 * c, msg[c]);
-        mbar_arrive_remote(mapa_u32(smem_u32(&s_bar[par]), lane));
+        for (int c = 0; c < KI; ++c) msg[c] = s_w[src][c];
+#pragma unroll
+        for (int c = KI; c < S; ++c) msg[c] = __longlong_as_double(s_kend);
+        const unsigned dst = mapa_u32(smem_u32(&s_in[par][crank][0]), lane);
+        const unsigned bar = mapa_u32(smem_u32(&s_bar[par]), lane);
+#pragma unroll
+        for (int c = 0; c < S; c += 2) st_async_v2(dst + 8 * c, msg[c], msg[c + 1], bar);
       }
     }
+    if (pr) { const long long t = clock64(); pc[2] += t - pt; pt = t; }
     mbar_wait_parity(smem_u32(&s_bar[par]), par ? ph1 : ph0);
     if (par) ph1 ^= 1; else ph0 ^= 1;
+    if (tid == 0 && step + 2 <= k) mbar_expect(smem_u32(&s_bar[par]), txb);  // arrival of step + 2
+    if (pr) { const long long t = clock64(); pc[3] += t - pt; pt = t; }
     // every warp reduces the CL slots itself (no second CTA barrier)
     const double gd = lane < CL ? s_in[par][lane][0] : -3.0;
     const unsigned gi = lane < CL ? (unsigned)__double_as_longlong(s_in[par][lane][1]) : 0xffffffffu;
@@ -502,13 +527,14 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
     unsigned i3;
     warp_argmax_key(fps_key(gd), gi, k3, i3);
     const int src = __ffs(__ballot_sync(0xffffffffu, lane < CL && gi == i3)) - 1;
-    const double nd = s_in[par][src][0];
     const long long ni = (long long)i3;
-    const long long kst = __double_as_longlong(s_in[par][0][S - 1]);
-    if (crank == 0 && tid == 0) {
+    const long long kst = __double_as_longlong(s_in[par][0][KI]);
+    if (crank == 0 && wid == NW - 1 && lane == 0) {  // outputs (off warp 0's path)
+      const double nd = s_in[par][src][0];
       fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
       if (step < k) idx_out[step] = ni;
     }
+    if (pr) { const long long t = clock64(); pc[4] += t - pt; pt = t; }
     if (step >= kst) break;
 #pragma unroll
     for (int c = 0; c < DP; ++c) y[c] = s_in[par][src][2 + c];
@@ -520,7 +546,10 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
         mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
       }
     }
+    if (pr) { const long long t = clock64(); pc[5] += t - pt; pt = t; }
   }
+  if (pr)
+    for (int j = 0; j < 6; ++j) prof[j] = pc[j];
   cl.sync();  // no CTA leaves while a push into it may be in flight
 }
 
@@ -541,8 +570,22 @@ afn_status launch_fps_push(const double* X, int64_t n, int d, int64_t k, int64_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop));
+  static const bool profon = getenv("AFN_FPS_PROF") != nullptr;
+  long long* prof = nullptr;
+  if (profon) {
+    AFN_CUDA(cudaMalloc(&prof, sizeof(long long) * 6));
+    AFN_CUDA(cudaMemset(prof, 0, sizeof(long long) * 6));
+  }
+  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop, prof));
   AFN_LAUNCH_CHECK("fps_push_kernel");
+  if (profon) {
+    long long h[6];
+    AFN_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
+    cudaFree(prof);
+    fprintf(stderr, "fps_push k=%lld CL=%d cycles/step: local %.0f sync %.0f cta+push %.0f wait %.0f reduce %.0f update %.0f\n",
+            (long long)k, CL, h[0] / (double)k, h[1] / (double)k, h[2] / (double)k, h[3] / (double)k,
+            h[4] / (double)k, h[5] / (double)k);
+  }
   return AFN_OK;
 }
 
