@@ -218,10 +218,10 @@ __global__ void __launch_bounds__(AT) tridiag_kernel(double* Ag, int m, double* 
     const double K = 0.5 * beta * pv;
     for (int t = tid; t < L; t += AT) p[t] = p[t] - K * v[t];  // w
     __syncthreads();
-    for (int64_t e = tid; e < (int64_t)L * L; e += AT) {
-      const int i = (int)(e / L), t = (int)(e - (int64_t)i * L);
-      double* a = A + (int64_t)(j + 1 + i) * m + (j + 1 + t);
-      *a = *a - v[i] * p[t] - p[i] * v[t];
+    for (int i = wid; i < L; i += AT / 32) {  // warp per row (no 64-bit index division)
+      const double vi = v[i], pi = p[i];
+      double* a = A + (int64_t)(j + 1 + i) * m + (j + 1);
+      for (int t = lane; t < L; t += 32) a[t] = a[t] - vi * p[t] - pi * v[t];
     }
     __syncthreads();
   }
