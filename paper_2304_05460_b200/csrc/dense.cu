@@ -500,7 +500,9 @@ __global__ void __launch_bounds__(256, 1) gemm128_bupper_kernel(const double* __
     }
     __syncthreads();
     const double* a = sA + buf * HK * HPA + ty * 4;
-    const double* b = sB + buf * HK * HPB + tx * 4;
+    // B columns of thread tx: 2 tx + {0, 1} + 32 q (q < 4): the 16 threads of
+    // a row read 256 contiguous bytes per LDS.128 (2 wavefronts, no conflicts)
+    const double* b = sB + buf * HK * HPB + tx * 2;
     // operands of step kk+1 are loaded while step kk's 64 DFMA run (the
     // two CTA warps per scheduler cannot hide the LDS latency otherwise)
     double2 ca[4], cb[4];
@@ -509,9 +511,9 @@ __global__ void __launch_bounds__(256, 1) gemm128_bupper_kernel(const double* __
     ca[2] = *reinterpret_cast<const double2*>(a + 64);
     ca[3] = *reinterpret_cast<const double2*>(a + 66);
     cb[0] = *reinterpret_cast<const double2*>(b);
-    cb[1] = *reinterpret_cast<const double2*>(b + 2);
+    cb[1] = *reinterpret_cast<const double2*>(b + 32);
     cb[2] = *reinterpret_cast<const double2*>(b + 64);
-    cb[3] = *reinterpret_cast<const double2*>(b + 66);
+    cb[3] = *reinterpret_cast<const double2*>(b + 96);
 #pragma unroll
     for (int kk = 0; kk < HK; ++kk) {
       double2 na[4], nb[4];
@@ -523,9 +525,9 @@ __global__ void __launch_bounds__(256, 1) gemm128_bupper_kernel(const double* __
         na[2] = *reinterpret_cast<const double2*>(an + 64);
         na[3] = *reinterpret_cast<const double2*>(an + 66);
         nb[0] = *reinterpret_cast<const double2*>(bn);
-        nb[1] = *reinterpret_cast<const double2*>(bn + 2);
+        nb[1] = *reinterpret_cast<const double2*>(bn + 32);
         nb[2] = *reinterpret_cast<const double2*>(bn + 64);
-        nb[3] = *reinterpret_cast<const double2*>(bn + 66);
+        nb[3] = *reinterpret_cast<const double2*>(bn + 96);
       }
       const double av[8] = {ca[0].x, ca[0].y, ca[1].x, ca[1].y, ca[2].x, ca[2].y, ca[3].x, ca[3].y};
       const double bv[8] = {cb[0].x, cb[0].y, cb[1].x, cb[1].y, cb[2].x, cb[2].y, cb[3].x, cb[3].y};
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(256, 1) gemm128_bupper_kernel(const double* __
     if (r >= M) continue;
 #pragma unroll
     for (int j = 0; j < 8; j += 2) {
-      const int64_t c = C0 + tx * 4 + (j & 3) + (j >> 2) * 64;
+      const int64_t c = C0 + tx * 2 + (j >> 1) * 32;
       if (c + 1 < N && (N & 1) == 0) {
         *reinterpret_cast<double2*>(&Cm[r * N + c]) = make_double2(acc[i][j], acc[i][j + 1]);
       } else {

@@ -500,6 +500,116 @@ __global__ void __launch_bounds__(256, 2) group_gemm48_kernel(const int* __restr
   }
 }
 
+// FP64 tensor-core variant (GA = 16): D_g = W_g W_U^T with mma.sync m8n8k4
+// f64 (SASS DMMA.8x8x4, 256 FMA per warp instruction -- the instruction and
+// operand traffic of the DFMA kernels was their limit, not the FP64 rate).
+// Warp w owns the 64 columns [64 w, 64 w + 64) of a 512-column pass: 2 x 8
+// m8n8 tiles, 32 accumulators per thread.  Stages hold k-chunks of 8 per row
+// at a 12-double stride (A/B fragment loads: 8 rows x 4 consecutive k per
+// LDS.64 = 2 wavefronts, conflict-free).  Each dot is summed in k order in
+// groups of 4 (the DMMA k-step).
+constexpr int DKC = 8, DKP = 12;
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NS>
+__global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
+    const int* __restrict__ sorder, int64_t N, const double* __restrict__ W, int64_t k,
+    const int* __restrict__ Ucount, const int* __restrict__ Ulist, const int64_t* __restrict__ Doff,
+    const int64_t* __restrict__ Poff, int64_t G, double* __restrict__ D) {
+  constexpr int GA = 16, UTP = 512;
+  extern __shared__ __align__(16) double gs[];
+  double* sA = gs;                         // [NS][GA][DKP]
+  double* sB = gs + NS * GA * DKP;         // [NS][UTP][DKP]
+  __shared__ int s_a[GA];
+  __shared__ int s_u[UTP];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t item = blockIdx.x;
+  int64_t glo = 0, ghi = G;
+  while (ghi - glo > 1) {
+    const int64_t mid = (glo + ghi) >> 1;
+    if (Poff[mid] <= item) glo = mid; else ghi = mid;
+  }
+  const int64_t g = glo;
+  const int pass = (int)(item - Poff[g]);
+  const int64_t m0 = g * GA;
+  const int cnt = (int)min((int64_t)GA, N - m0);
+  const int nu = Ucount[g];
+  double* Dg = D + Doff[g];
+  const int u0 = pass * UTP;
+  const int un = min(UTP, nu - u0);
+  if (tid < GA) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
+  for (int t = tid; t < UTP; t += 256) s_u[t] = t < un ? Ulist[g * UCAP + u0 + t] : -1;
+  __syncthreads();
+  const int64_t nch = (k + DKC - 1) / DKC;
+  const bool even = (k & 1) == 0;
+  auto issue = [&](int64_t ch, int buf) {
+    const int64_t c0 = ch * DKC;
+    for (int e = tid; e < (GA + un) * (DKC / 2); e += 256) {
+      const int row = e / (DKC / 2), part = e - row * (DKC / 2);
+      const int id = row < GA ? s_a[row] : s_u[row - GA];
+      double* dst = row < GA ? sA + (buf * GA + row) * DKP + 2 * part
+                             : sB + ((int64_t)buf * UTP + (row - GA)) * DKP + 2 * part;
+      const int64_t c = c0 + 2 * part;
+      if (id >= 0 && c + 1 < k && even) {
+        cpa16(dst, &W[(int64_t)id * k + c]);
+      } else {
+        dst[0] = (id >= 0 && c < k) ? W[(int64_t)id * k + c] : 0.0;
+        dst[1] = (id >= 0 && c + 1 < k) ? W[(int64_t)id * k + c + 1] : 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[2][8][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int n = 0; n < 8; ++n) acc[mt][n][0] = acc[mt][n][1] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < NS - 1; ++s0) {
+    if (s0 < nch) issue(s0, s0);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const bool wact = wid * 64 < un;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
+  for (int64_t ch = 0; ch < nch; ++ch) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    __syncthreads();
+    const int64_t nx = ch + NS - 1;
+    if (nx < nch) issue(nx, (int)(nx % NS));
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    if (!wact) continue;
+    const double* a = sA + (int)(ch % NS) * GA * DKP;
+    const double* b = sB + ((int64_t)(ch % NS) * UTP + wid * 64) * DKP;
+#pragma unroll
+    for (int k4 = 0; k4 < DKC; k4 += 4) {
+      const double a0 = a[fr * DKP + k4 + fk], a1 = a[(8 + fr) * DKP + k4 + fk];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const double bv = b[(n * 8 + fr) * DKP + k4 + fk];
+        dmma884(acc[0][n][0], acc[0][n][1], a0, bv);
+        dmma884(acc[1][n][0], acc[1][n][1], a1, bv);
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  if (!wact) return;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int j = mt * 8 + fr;
+    if (j >= cnt) continue;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const int u = wid * 64 + n * 8 + 2 * fk;
+      if (u < un) Dg[(int64_t)j * nu + u0 + u] = acc[mt][n][0];
+      if (u + 1 < un) Dg[(int64_t)j * nu + u0 + u + 1] = acc[mt][n][1];
+    }
+  }
+}
+
 // ---------------------------------------------------------------- factor
 // One CTA (FT2 threads) per FSAI row i with pattern J (|J| = wp <= 16 MT,
 // ascending, i last).  CTAs take the rows in the spatial (cell) order of the
@@ -982,7 +1092,13 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
       kern = GA == 32 ? (ut == 1024 ? group_gemm_kernel<32, 4> : group_gemm_kernel<32, 2>)
                       : (ut == 1024 ? group_gemm_kernel<16, 4> : group_gemm_kernel<16, 2>);
     }
-    const int bytes = (int)(sizeof(double) * NST * kc * (GA + ut));
+    int bytes = (int)(sizeof(double) * NST * kc * (GA + ut));
+    // FP64 tensor cores (DMMA) for GA = 16 unless AFN_FSAI_DMMA=0; AFN_FSAI_DMMA=3: 3 stages
+    static const int dm = getenv("AFN_FSAI_DMMA") ? atoi(getenv("AFN_FSAI_DMMA")) : 2;
+    if (t48 && dm > 0 && GA == 16) {
+      kern = dm == 3 ? group_gemm_dmma_kernel<3> : group_gemm_dmma_kernel<2>;
+      bytes = (int)(sizeof(double) * (dm == 3 ? 3 : 2) * DKP * (16 + 512));
+    }
     AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0) {
