@@ -345,6 +345,10 @@ afn_status set_smem_once() {
 constexpr int GM = 128, GN = 64, GK = 16;
 constexpr int GPA = GM + 4, GPB = GN + 4;  // smem pitches
 
+__device__ __forceinline__ void cpa16_d(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
@@ -831,6 +835,114 @@ afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr
   return AFN_OK;
 }
 
+// C (M x N) = A (M x K) B (K x N), all row-major, B upper triangular
+// (B[t][c] = 0 for t > c: a tile's K range ends at its last column), on the
+// FP64 tensor cores: mma.sync m8n8k4 f64 (DMMA.8x8x4).  CTA tile 64 x 64,
+// 4 warps of 32 x 32 (4 x 4 m8n8 tiles, 32 accumulators per thread), k-chunks
+// of 16 through 4 cp.async stages.  A chunk at a 20-double row stride and B
+// chunk at a 72-double row stride: each fragment LDS.64 (8 rows x 4 k, or
+// 4 k x 8 columns) is two conflict-free wavefronts.
+constexpr int TM = 64, TN = 64, TK = 16, TKP = 20, TNP = 72, TS = 3;
+__device__ __forceinline__ void dmma884d(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(128) gemm_dmma_bupper_kernel(const double* __restrict__ A,
+                                                              const double* __restrict__ B,
+                                                              double* __restrict__ Cm, int64_t M, int64_t N,
+                                                              int64_t K) {
+  extern __shared__ __align__(16) double tsm[];
+  double* sA = tsm;                    // [TS][TM][TKP]
+  double* sB = tsm + TS * TM * TKP;    // [TS][TK][TNP]
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wm = wid >> 1, wn = wid & 1;
+  const int64_t R0 = (int64_t)blockIdx.y * TM, C0 = (int64_t)blockIdx.x * TN;
+  const int64_t kend = min(K, C0 + TN);
+  const int64_t nkb = (kend + TK - 1) / TK;
+  const bool vec = (K & 1) == 0 && (N & 1) == 0;
+  auto stage = [&](int64_t kb, int buf) {
+    const int64_t k0 = kb * TK;
+    double* a = sA + buf * TM * TKP;
+    double* b = sB + buf * TK * TNP;
+#pragma unroll
+    for (int u = 0; u < (TM * TK / 2) / 128; ++u) {  // A: 16-byte copies, row r, k pair
+      const int e = tid + 128 * u;
+      const int r = e / (TK / 2), kp = 2 * (e - r * (TK / 2));
+      const int64_t gr = R0 + r, gk = k0 + kp;
+      double* dst = &a[r * TKP + kp];
+      if (vec && gr < M && gk + 1 < kend) {
+        cpa16_d(dst, &A[gr * K + gk]);
+      } else {
+        dst[0] = (gr < M && gk < kend) ? A[gr * K + gk] : 0.0;
+        dst[1] = (gr < M && gk + 1 < kend) ? A[gr * K + gk + 1] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < (TK * TN / 2) / 128; ++u) {  // B: 16-byte copies, k row, column pair
+      const int e = tid + 128 * u;
+      const int kk = e / (TN / 2), c = 2 * (e - kk * (TN / 2));
+      const int64_t gk = k0 + kk, gc = C0 + c;
+      double* dst = &b[kk * TNP + c];
+      if (vec && gk < kend && gc + 1 < N) {
+        cpa16_d(dst, &B[gk * N + gc]);
+      } else {
+        dst[0] = (gk < kend && gc < N) ? B[gk * N + gc] : 0.0;
+        dst[1] = (gk < kend && gc + 1 < N) ? B[gk * N + gc + 1] : 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s0 = 0; s0 < TS - 1; ++s0) {
+    if (s0 < nkb) stage(s0, s0);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int64_t kb = 0; kb < nkb; ++kb) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(TS - 2) : "memory");
+    __syncthreads();
+    const int64_t nx = kb + TS - 1;
+    if (nx < nkb) stage(nx, (int)(nx % TS));
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* a = sA + (int)(kb % TS) * TM * TKP + (wm * 32 + fr) * TKP + fk;
+    const double* b = sB + (int)(kb % TS) * TK * TNP + fk * TNP + wn * 32 + fr;
+#pragma unroll
+    for (int k4 = 0; k4 < TK; k4 += 4) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = a[i * 8 * TKP + k4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = b[k4 * TNP + j * 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884d(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = R0 + wm * 32 + i * 8 + fr;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = C0 + wn * 32 + j * 8 + 2 * fk;
+      if (vec && c + 1 < N) {
+        *reinterpret_cast<double2*>(&Cm[r * N + c]) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < N) Cm[r * N + c] = acc[i][j][0];
+        if (c + 1 < N) Cm[r * N + c + 1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st) {
   if (N <= 0 || k <= 0) return AFN_OK;
@@ -842,8 +954,11 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
   afn_status s = dalloc((void**)&Kb, sizeof(double) * rb * k, st);
   if (s != AFN_OK) return s;
   static const bool legacy = getenv("AFN_W_GEMM64") != nullptr;
+  static const bool simt = getenv("AFN_W_SIMT") != nullptr;  // the DFMA 128 x 128 kernel
   static bool attr = false;
   if (!attr) {
+    AFN_CUDA(cudaFuncSetAttribute(gemm_dmma_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * TS * (TM * TKP + TK * TNP))));
     AFN_CUDA(cudaFuncSetAttribute(gemm_nn_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * 2 * GK * (GPA + GPB))));
     AFN_CUDA(cudaFuncSetAttribute(gemm128_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -859,11 +974,16 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
       gemm_nn_bupper_kernel<<<grid, 256, (int)(sizeof(double) * 2 * GK * (GPA + GPB)), st>>>(
           Kb, LinvT, W + r0 * k, nr, k, k);
       AFN_LAUNCH_CHECK("gemm_nn_bupper_kernel");
-    } else {
+    } else if (simt) {
       dim3 grid((unsigned)((k + HN - 1) / HN), (unsigned)((nr + HM - 1) / HM));
       gemm128_bupper_kernel<<<grid, 256, (int)(sizeof(double) * 2 * HK * (HPA + HPB)), st>>>(
           Kb, LinvT, W + r0 * k, nr, k, k);
       AFN_LAUNCH_CHECK("gemm128_bupper_kernel");
+    } else {  // FP64 tensor cores
+      dim3 grid((unsigned)((k + TN - 1) / TN), (unsigned)((nr + TM - 1) / TM));
+      gemm_dmma_bupper_kernel<<<grid, 128, (int)(sizeof(double) * TS * (TM * TKP + TK * TNP)), st>>>(
+          Kb, LinvT, W + r0 * k, nr, k, k);
+      AFN_LAUNCH_CHECK("gemm_dmma_bupper_kernel");
     }
   }
   dfree(Kb, st);
