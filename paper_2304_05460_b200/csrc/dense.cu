@@ -848,21 +848,29 @@ __device__ __forceinline__ void dmma884d(double& c0, double& c1, double a, doubl
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
-__global__ void __launch_bounds__(128) gemm_dmma_bupper_kernel(const double* __restrict__ A,
-                                                              const double* __restrict__ B,
-                                                              double* __restrict__ Cm, int64_t M, int64_t N,
-                                                              int64_t K) {
+// MODE 0: B upper (K range ends at the tile's last column); 1: A lower (ends
+// at the tile's last row); 2: B lower (starts at the tile's first column).
+// Batched over blockIdx.z with element strides sA, sB, sC; C = alpha A B.
+template <int MODE>
+__global__ void __launch_bounds__(128) gemm_dmma_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                       double* __restrict__ Cm, int64_t M, int64_t N, int64_t K,
+                                                       int64_t lda, int64_t ldb, int64_t ldc, int64_t sAz,
+                                                       int64_t sBz, int64_t sCz, double alpha) {
   extern __shared__ __align__(16) double tsm[];
   double* sA = tsm;                    // [TS][TM][TKP]
   double* sB = tsm + TS * TM * TKP;    // [TS][TK][TNP]
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int wm = wid >> 1, wn = wid & 1;
+  A += (int64_t)blockIdx.z * sAz;
+  B += (int64_t)blockIdx.z * sBz;
+  Cm += (int64_t)blockIdx.z * sCz;
   const int64_t R0 = (int64_t)blockIdx.y * TM, C0 = (int64_t)blockIdx.x * TN;
-  const int64_t kend = min(K, C0 + TN);
-  const int64_t nkb = (kend + TK - 1) / TK;
-  const bool vec = (K & 1) == 0 && (N & 1) == 0;
+  const int64_t kend = MODE == 0 ? min(K, C0 + TN) : (MODE == 1 ? min(K, R0 + TM) : K);
+  const int64_t kbeg = MODE == 2 ? (min(K, C0) / TK) * TK : 0;
+  const int64_t nkb = (kend - kbeg + TK - 1) / TK;
+  const bool vec = (lda & 1) == 0 && (ldb & 1) == 0 && (ldc & 1) == 0;
   auto stage = [&](int64_t kb, int buf) {
-    const int64_t k0 = kb * TK;
+    const int64_t k0 = kbeg + kb * TK;
     double* a = sA + buf * TM * TKP;
     double* b = sB + buf * TK * TNP;
 #pragma unroll
@@ -872,10 +880,10 @@ __global__ void __launch_bounds__(128) gemm_dmma_bupper_kernel(const double* __r
       const int64_t gr = R0 + r, gk = k0 + kp;
       double* dst = &a[r * TKP + kp];
       if (vec && gr < M && gk + 1 < kend) {
-        cpa16_d(dst, &A[gr * K + gk]);
+        cpa16_d(dst, &A[gr * lda + gk]);
       } else {
-        dst[0] = (gr < M && gk < kend) ? A[gr * K + gk] : 0.0;
-        dst[1] = (gr < M && gk + 1 < kend) ? A[gr * K + gk + 1] : 0.0;
+        dst[0] = (gr < M && gk < kend) ? A[gr * lda + gk] : 0.0;
+        dst[1] = (gr < M && gk + 1 < kend) ? A[gr * lda + gk + 1] : 0.0;
       }
     }
 #pragma unroll
@@ -885,10 +893,10 @@ __global__ void __launch_bounds__(128) gemm_dmma_bupper_kernel(const double* __r
       const int64_t gk = k0 + kk, gc = C0 + c;
       double* dst = &b[kk * TNP + c];
       if (vec && gk < kend && gc + 1 < N) {
-        cpa16_d(dst, &B[gk * N + gc]);
+        cpa16_d(dst, &B[gk * ldb + gc]);
       } else {
-        dst[0] = (gk < kend && gc < N) ? B[gk * N + gc] : 0.0;
-        dst[1] = (gk < kend && gc + 1 < N) ? B[gk * N + gc + 1] : 0.0;
+        dst[0] = (gk < kend && gc < N) ? B[gk * ldb + gc] : 0.0;
+        dst[1] = (gk < kend && gc + 1 < N) ? B[gk * ldb + gc + 1] : 0.0;
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -934,10 +942,10 @@ __global__ void __launch_bounds__(128) gemm_dmma_bupper_kernel(const double* __r
     for (int j = 0; j < 4; ++j) {
       const int64_t c = C0 + wn * 32 + j * 8 + 2 * fk;
       if (vec && c + 1 < N) {
-        *reinterpret_cast<double2*>(&Cm[r * N + c]) = make_double2(acc[i][j][0], acc[i][j][1]);
+        *reinterpret_cast<double2*>(&Cm[r * ldc + c]) = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
       } else {
-        if (c < N) Cm[r * N + c] = acc[i][j][0];
-        if (c + 1 < N) Cm[r * N + c + 1] = acc[i][j][1];
+        if (c < N) Cm[r * ldc + c] = alpha * acc[i][j][0];
+        if (c + 1 < N) Cm[r * ldc + c + 1] = alpha * acc[i][j][1];
       }
     }
   }
@@ -957,8 +965,9 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
   static const bool simt = getenv("AFN_W_SIMT") != nullptr;  // the DFMA 128 x 128 kernel
   static bool attr = false;
   if (!attr) {
-    AFN_CUDA(cudaFuncSetAttribute(gemm_dmma_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * TS * (TM * TKP + TK * TNP))));
+    for (auto kf2 : {gemm_dmma_kernel<0>, gemm_dmma_kernel<1>, gemm_dmma_kernel<2>})
+      AFN_CUDA(cudaFuncSetAttribute(kf2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(sizeof(double) * TS * (TM * TKP + TK * TNP))));
     AFN_CUDA(cudaFuncSetAttribute(gemm_nn_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(sizeof(double) * 2 * GK * (GPA + GPB))));
     AFN_CUDA(cudaFuncSetAttribute(gemm128_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -981,9 +990,9 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
       AFN_LAUNCH_CHECK("gemm128_bupper_kernel");
     } else {  // FP64 tensor cores
       dim3 grid((unsigned)((k + TN - 1) / TN), (unsigned)((nr + TM - 1) / TM));
-      gemm_dmma_bupper_kernel<<<grid, 128, (int)(sizeof(double) * TS * (TM * TKP + TK * TNP)), st>>>(
-          Kb, LinvT, W + r0 * k, nr, k, k);
-      AFN_LAUNCH_CHECK("gemm_dmma_bupper_kernel");
+      gemm_dmma_kernel<0><<<grid, 128, (int)(sizeof(double) * TS * (TM * TKP + TK * TNP)), st>>>(
+          Kb, LinvT, W + r0 * k, nr, k, k, k, k, k, 0, 0, 0, 1.0);
+      AFN_LAUNCH_CHECK("gemm_dmma_kernel<0>");
     }
   }
   dfree(Kb, st);
@@ -1011,9 +1020,27 @@ afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_
     AFN_CUDA(cudaFuncSetAttribute(gemm_nn_batched_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     attr = true;
   }
+  static const bool simt = getenv("AFN_LINV_SIMT") != nullptr;  // the DFMA batched kernels
+  static bool dattr = false;
+  const int dbytes = (int)(sizeof(double) * TS * (TM * TKP + TK * TNP));
+  if (!dattr) {
+    AFN_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dbytes));
+    AFN_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dbytes));
+    dattr = true;
+  }
   for (int64_t h = NB; h < kp; h <<= 1) {
     const int64_t pairs = kp / (2 * h);
     const int64_t stride = 2 * h * kp + 2 * h;  // next diagonal pair
+    if (!simt) {  // FP64 tensor cores
+      dim3 grid((unsigned)((h + TN - 1) / TN), (unsigned)((h + TM - 1) / TM), (unsigned)pairs);
+      gemm_dmma_kernel<2><<<grid, 128, dbytes, st>>>(Lp + h * kp, X, Tt, h, h, h, kp, kp, kp, stride, stride,
+                                                     stride, 1.0);
+      AFN_LAUNCH_CHECK("gemm_dmma_kernel<2>");
+      gemm_dmma_kernel<1><<<grid, 128, dbytes, st>>>(X + h * kp + h, Tt, X + h * kp, h, h, h, kp, kp, kp, stride,
+                                                     stride, stride, -1.0);
+      AFN_LAUNCH_CHECK("gemm_dmma_kernel<1>");
+      continue;
+    }
     dim3 grid((unsigned)((h + GN - 1) / GN), (unsigned)((h + GM - 1) / GM), (unsigned)pairs);
     // T = B * A^{-1}   (B = Lp[h.., 0..h), A^{-1} = X[0..h, 0..h) lower -> K >= col start)
     gemm_nn_batched_kernel<2><<<grid, 256, bytes, st>>>(Lp + h * kp, X, Tt, h, kp, stride, stride, stride, 1.0);
