@@ -349,6 +349,12 @@ __device__ __forceinline__ void cpa16_d(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void dmma884d(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+// FP64 tensor-core MMA (SASS DMMA.8x8x4): D(8x8) += A(8x4, row) B(4x8, col)
 __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
@@ -806,7 +812,80 @@ afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, doubl
   return AFN_OK;
 }
 
+// Trailing update on the FP64 tensor cores: tile (I, J), J <= I, of the
+// lower part: A[I, J] -= A[I, P] A[J, P]^T, P = [kb, kb + NB).  The two 64 x 64
+// panel slices are staged whole (68-double row stride: every fragment LDS.64
+// -- 8 rows x 4 consecutive k -- is two conflict-free wavefronts); 4 warps of
+// 32 x 32 (16 DMMA per k-step of 4).
+constexpr int PUP = NB + 4;
+__global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64_t k, int64_t kb) {
+  extern __shared__ __align__(16) double usm[];
+  double* sI = usm;              // [NB][PUP]
+  double* sJ = usm + NB * PUP;   // [NB][PUP]
+  const int64_t t = blockIdx.x;
+  int64_t bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
+  while (bi * (bi + 1) / 2 > t) --bi;
+  while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+  const int64_t bj = t - bi * (bi + 1) / 2;
+  const int64_t base = kb + NB;
+  const int64_t I0 = base + bi * NB, J0 = base + bj * NB;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int wm = wid >> 1, wn = wid & 1;
+  const bool vec = (k & 1) == 0;
+  for (int e = tid; e < NB * NB / 2; e += 128) {
+    const int r = e / (NB / 2), c = 2 * (e - r * (NB / 2));
+    const int64_t ri = I0 + r, rj = J0 + r;
+    double* di = &sI[r * PUP + c];
+    double* dj = &sJ[r * PUP + c];
+    if (vec && ri < k) cpa16_d(di, &A[ri * k + kb + c]);
+    else { di[0] = ri < k ? A[ri * k + kb + c] : 0.0; di[1] = ri < k ? A[ri * k + kb + c + 1] : 0.0; }
+    if (vec && rj < k) cpa16_d(dj, &A[rj * k + kb + c]);
+    else { dj[0] = rj < k ? A[rj * k + kb + c] : 0.0; dj[1] = rj < k ? A[rj * k + kb + c + 1] : 0.0; }
+  }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (bi == bj && wm < wn) return;  // strictly upper 32 x 32 block of a diagonal tile
+  const int fr = lane >> 2, fk = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double* a = sI + (wm * 32 + fr) * PUP + fk;
+  const double* b = sJ + (wn * 32 + fr) * PUP + fk;
+#pragma unroll 4
+  for (int k4 = 0; k4 < NB; k4 += 4) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) av[i] = a[i * 8 * PUP + k4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bv[j] = b[j * 8 * PUP + k4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma884d(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = I0 + wm * 32 + i * 8 + fr;
+    if (r >= k) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t c = J0 + wn * 32 + j * 8 + 2 * fk;
+      if (c < k && c <= r) A[r * k + c] -= acc[i][j][0];
+      if (c + 1 < k && c + 1 <= r) A[r * k + c + 1] -= acc[i][j][1];
+    }
+  }
+}
+
 afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
+  static const bool simt = getenv("AFN_POTRF_SIMT") != nullptr;
+  static bool uattr = false;
+  if (!uattr) {
+    AFN_CUDA(cudaFuncSetAttribute(potrf_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(sizeof(double) * 2 * NB * PUP)));
+    uattr = true;
+  }
   TRY_SMEM();
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
   for (int64_t kb = 0; kb < k; kb += NB) {
@@ -817,8 +896,14 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
     const int64_t T = (rem + NB - 1) / NB;
     potrf_panel_kernel<<<(unsigned)T, DT, SMEM2, st>>>(A, k, kb);
     AFN_LAUNCH_CHECK("potrf_panel_kernel");
-    potrf_update_kernel<<<(unsigned)(T * (T + 1) / 2), DT, SMEM2, st>>>(A, k, kb);
-    AFN_LAUNCH_CHECK("potrf_update_kernel");
+    if (simt) {
+      potrf_update_kernel<<<(unsigned)(T * (T + 1) / 2), DT, SMEM2, st>>>(A, k, kb);
+      AFN_LAUNCH_CHECK("potrf_update_kernel");
+    } else {  // FP64 tensor cores
+      potrf_update_dmma_kernel<<<(unsigned)(T * (T + 1) / 2), 128, (int)(sizeof(double) * 2 * NB * PUP), st>>>(A, k,
+                                                                                                         kb);
+      AFN_LAUNCH_CHECK("potrf_update_dmma_kernel");
+    }
   }
   zero_upper_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, st>>>(A, k);
   AFN_LAUNCH_CHECK("zero_upper_kernel");
@@ -843,11 +928,6 @@ afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr
 // chunk at a 72-double row stride: each fragment LDS.64 (8 rows x 4 k, or
 // 4 k x 8 columns) is two conflict-free wavefronts.
 constexpr int TM = 64, TN = 64, TK = 16, TKP = 20, TNP = 72, TS = 3;
-__device__ __forceinline__ void dmma884d(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 // MODE 0: B upper (K range ends at the tile's last column); 1: A lower (ends
 // at the tile's last row); 2: B lower (starts at the tile's first column).
 // Batched over blockIdx.z with element strides sA, sB, sC; C = alpha A B.
