@@ -626,6 +626,11 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
 //      contiguous rows of L (every warp, warp 0 stores) -- the
 //      Kolotilina-Yeremin row with diag(G S G^T) = 1 (reading R16).
 constexpr int FT2 = 128;
+__device__ __forceinline__ void dmma884f(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 // Unblocked Cholesky of a 16x16 block held one row per lane (row lr =
 // lane & 15 in dr[0..lr]; lanes 16..31 mirror 0..15), one warp.  Column c is
@@ -833,48 +838,47 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
     }
     __syncthreads();
     if (prof) { const long long t = clock64(); ppanel += t - pm; pm = t; }
-    // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], wp > a >= b >= r0, 4x4 tiles
-    const int mt = (m + 3) >> 2;
-    const int ntile = mt * (mt + 1) / 2;
-    for (int t = tid; t < ntile; t += FT2) {
-      int I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], wp > a >= b >= r0:
+    // 8x8 tiles on the FP64 tensor cores (DMMA, 4 k-steps of 4), a warp per
+    // tile, two tiles in flight per warp; rows past wp read the zero row
+    const int mt8 = (m + 7) >> 3;
+    const int nt8 = mt8 * (mt8 + 1) / 2;
+    const int fr = lane >> 2, fk = lane & 3;
+    auto tile_ij = [&](int t, int& I, int& J) {
+      I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
       while (I * (I + 1) / 2 > t) --I;
       while ((I + 1) * (I + 2) / 2 <= t) ++I;
-      const int J = t - I * (I + 1) / 2;
-      const int a0 = r0 + 4 * I, b0 = r0 + 4 * J;
-      const double* pa[4];
-      const double* pb[4];
+      J = t - I * (I + 1) / 2;
+    };
+    for (int t0 = wid; t0 < nt8; t0 += 2 * (FT2 / 32)) {
+      const int t1 = t0 + FT2 / 32;
+      int I0, J0, I1, J1;
+      tile_ij(t0, I0, J0);
+      tile_ij(t1 < nt8 ? t1 : t0, I1, J1);
+      const double* pa0 = rowp(r0 + 8 * I0 + fr, kb) + fk;
+      const double* pb0 = rowp(r0 + 8 * J0 + fr, kb) + fk;
+      const double* pa1 = rowp(r0 + 8 * I1 + fr, kb) + fk;
+      const double* pb1 = rowp(r0 + 8 * J1 + fr, kb) + fk;
+      double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        pa[r] = rowp(a0 + r, kb);
-        pb[r] = rowp(b0 + r, kb);
+      for (int k4 = 0; k4 < 16; k4 += 4) {
+        dmma884f(c00, c01, pa0[k4], pb0[k4]);
+        dmma884f(c10, c11, pa1[k4], pb1[k4]);
       }
-      double acc[4][4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-#pragma unroll
-      for (int kk = 0; kk < 16; kk += 2) {
-        double2 va[4], vb[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          va[r] = *reinterpret_cast<const double2*>(pa[r] + kk);
-          vb[r] = *reinterpret_cast<const double2*>(pb[r] + kk);
+      {
+        const int row = r0 + 8 * I0 + fr, col = r0 + 8 * J0 + 2 * fk;
+        if (row < wp) {
+          if (col <= row) Lm[s_off[row] + col] -= c00;
+          if (col + 1 <= row) Lm[s_off[row] + col + 1] -= c01;
         }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            acc[r][c] = fma(va[r].x, vb[c].x, acc[r][c]);
-            acc[r][c] = fma(va[r].y, vb[c].y, acc[r][c]);
-          }
       }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (b0 + c <= a0 + r && a0 + r < wp) Lm[s_off[a0 + r] + b0 + c] -= acc[r][c];
+      if (t1 < nt8) {
+        const int row = r0 + 8 * I1 + fr, col = r0 + 8 * J1 + 2 * fk;
+        if (row < wp) {
+          if (col <= row) Lm[s_off[row] + col] -= c10;
+          if (col + 1 <= row) Lm[s_off[row] + col + 1] -= c11;
+        }
+      }
     }
     __syncthreads();
     if (prof) ptrail += clock64() - pm;
