@@ -519,7 +519,11 @@ template <int NS>
 __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ W, int64_t k,
     const int* __restrict__ Ucount, const int* __restrict__ Ulist, const int64_t* __restrict__ Doff,
-    const int64_t* __restrict__ Poff, int64_t G, double* __restrict__ D) {
+    const int64_t* __restrict__ Poff, int64_t G, double* __restrict__ D, const double* __restrict__ X2, int d,
+    KernelFn kf, double mu) {
+  // epilogue: D_g holds the Schur entries S_ab = K(x_a, x_b) + mu delta_ab - W_a . W_b
+  // themselves (the factor kernel then only gathers them)
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
   constexpr int GA = 16, UTP = 512;
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                         // [NS][GA][DKP]
@@ -596,16 +600,33 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();  // the stage buffers now hold the points of the rows and columns
+  double* sxa = gs;             // [GA][d]
+  double* sxb = gs + GA * d;    // [UTP][d]
+  load_exp2_tab(s_tab);
+  for (int e = tid; e < (GA + un) * d; e += 256) {
+    const int row = e / d, c = e - row * d;
+    const int id = row < GA ? s_a[row] : s_u[row - GA];
+    (row < GA ? sxa : sxb - GA * d)[e] = id >= 0 ? X2[(int64_t)id * d + c] : 0.0;
+  }
+  __syncthreads();
   if (!wact) return;
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
     const int j = mt * 8 + fr;
     if (j >= cnt) continue;
+    const int a = s_a[j];
 #pragma unroll
     for (int n = 0; n < 8; ++n) {
-      const int u = wid * 64 + n * 8 + 2 * fk;
-      if (u < un) Dg[(int64_t)j * nu + u0 + u] = acc[mt][n][0];
-      if (u + 1 < un) Dg[(int64_t)j * nu + u0 + u + 1] = acc[mt][n][1];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int u = wid * 64 + n * 8 + 2 * fk + h;
+        if (u < un) {
+          const int b = s_u[u];
+          const double kv = a == b ? 1.0 + mu : kern_from_d2(kf, d2_exact_rt(&sxa[j * d], &sxb[u * d], d), s_tab);
+          Dg[(int64_t)j * nu + u0 + u] = kv - acc[mt][n][h];
+        }
+      }
     }
   }
 }
@@ -670,7 +691,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
                                                          const int2* __restrict__ Htab,
                                                          const int64_t* __restrict__ Doff,
                                                          const double* __restrict__ D, double* __restrict__ gval,
-                                                         int* info, int lsz, long long* prof) {
+                                                         int* info, int lsz, long long* prof, int dS) {
   constexpr int WP = MT * 16;
   // prof (debug, AFN_FACTOR_PROF): per CTA clock64 spans of the phases
   long long pt0 = clock64(), pdiag = 0, ppanel = 0, ptrail = 0, pasm = 0, pm, ppro = 0, pgat = 0;
@@ -772,6 +793,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
         }
       }
       if (prof) pgat += clock64() - pm;
+      if (dS) continue;  // D already holds S_ab (tensor-core group product's epilogue)
       int p = p0, q = q0;
 #pragma unroll 1  // (unrolled: 22 KB more code, slower -- instruction cache)
       for (int t = 0; t < B && e0 + t < ne; ++t) {
@@ -918,7 +940,7 @@ template <int MT>
 afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t row_hi, int wcap, cudaStream_t st,
                          const double* X2, int d, KernelFn kf, double mu, const int64_t* rp, const int32_t* col,
                          const int* grp, const int* loc, const int* Ucount, const int2* Htab,
-                         const int64_t* Doff, const double* D, double* gval, int* info) {
+                         const int64_t* Doff, const double* D, double* gval, int* info, int dS) {
   constexpr int WP = MT * 16;
   const int wmax = std::min(WP, wcap);
   const int lsz = ((wmax * (wmax + 1) / 2 + (wmax + 1) / 2 + 16) + 1) & ~1;
@@ -933,7 +955,8 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
   for (int64_t r0 = 0; r0 < N; r0 += 1 << 30) {
     const int64_t nr = std::min<int64_t>(N - r0, 1 << 30);
     kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, kf, mu, rp, col, grp, loc,
-                                          Ucount, Htab, Doff, D, gval, info, lsz, prof ? prof + 8 * r0 : nullptr);
+                                          Ucount, Htab, Doff, D, gval, info, lsz, prof ? prof + 8 * r0 : nullptr,
+                                          dS);
     AFN_LAUNCH_CHECK("fsai_factor_kernel");
   }
   if (prof) {
@@ -1084,6 +1107,8 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   AFN_CUDA(cudaMemcpyAsync(&totD, Doff + G, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaStreamSynchronize(st));
   // ---- 3. dense group products
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
+  int dS = 0;  // 1: D holds S_ab (DMMA kernel epilogue), 0: the Gram W_a . W_b
   double* D;
   if ((s = get((void**)&D, sizeof(double) * (totD > 0 ? totD : 1))) != AFN_OK) return s;
   {
@@ -1099,13 +1124,20 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
     int bytes = (int)(sizeof(double) * NST * kc * (GA + ut));
     // FP64 tensor cores (DMMA) for GA = 16 unless AFN_FSAI_DMMA=0; AFN_FSAI_DMMA=3: 3 stages
     static const int dm = getenv("AFN_FSAI_DMMA") ? atoi(getenv("AFN_FSAI_DMMA")) : 2;
-    if (t48 && dm > 0 && GA == 16) {
-      kern = dm == 3 ? group_gemm_dmma_kernel<3> : group_gemm_dmma_kernel<2>;
+    if (t48 && dm > 0 && GA == 16 && d <= 16) {
+      dS = 1;
       bytes = (int)(sizeof(double) * (dm == 3 ? 3 : 2) * DKP * (16 + 512));
+      AFN_CUDA(cudaFuncSetAttribute(dm == 3 ? group_gemm_dmma_kernel<3> : group_gemm_dmma_kernel<2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    } else {
+      AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     }
-    AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     kt_begin(KT_FSAI_GEMM, st);
-    if (items > 0) {
+    if (items > 0 && dS) {
+      auto dk = dm == 3 ? group_gemm_dmma_kernel<3> : group_gemm_dmma_kernel<2>;
+      dk<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D, X2, d, kf, mu);
+      AFN_LAUNCH_CHECK("group_gemm_dmma_kernel");
+    } else if (items > 0) {
       kern<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D);
       AFN_LAUNCH_CHECK("group_gemm_kernel");
     }
@@ -1113,14 +1145,13 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   }
   // ---- 4. per-row assembly + Cholesky + g (one CTA per row, rows in the
   // spatial order sorder; CTAs of other ranks' rows exit at once)
-  const KernelFn kf = kernel_fn(kn.kind, kn.l);
   const int64_t NR = row_hi - row_lo;
   kt_begin(KT_FSAI_CHOL, st);
   switch (MT) {
 #define AFN_FACTOR(M) \
-    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info, dS); break;
     AFN_FACTOR(1) AFN_FACTOR(2) AFN_FACTOR(3) AFN_FACTOR(4) AFN_FACTOR(5) AFN_FACTOR(6) AFN_FACTOR(7)
-    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
+    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info, dS); break;
 #undef AFN_FACTOR
   }
   if (s != AFN_OK) return s;
