@@ -25,6 +25,27 @@ namespace {
 
 constexpr int KMV_NT = 256;
 
+// 2^(r/256), r = 0..255 (one table lookup and one multiply per exp2 in the
+// matvec instead of two of each with the 2 x 16-entry tables); filled once.
+__device__ double g_exp2_256[256];
+__global__ void exp2_256_init_kernel() { g_exp2_256[threadIdx.x] = exp2((double)threadIdx.x / 256.0); }
+__device__ __forceinline__ double exp2_neg256(double s, const double* tab) {
+  const double magic = 0x1.8p52;
+  double t = fma(s, -256.0, magic);   // rint(-256 s) in the low word
+  double nf = t - magic;
+  double f = fma(nf, -0x1.0p-8, -s);  // exact, |f| <= 1/512
+  const int n256 = __double2loint(t);
+  double p = AFN_E2C4;
+  p = fma(p, f, AFN_E2C3);
+  p = fma(p, f, AFN_E2C2);
+  p = fma(p, f, AFN_E2C1);
+  p = fma(p, f, AFN_E2C0);
+  p = p * tab[n256 & 255];
+  int hi = __double2hiint(p) + ((n256 >> 8) << 20);
+  hi = (__double2hiint(s) >= 0x408FE000) ? 0 : hi;  // s >= 1020 -> ~0 (as exp2_neg)
+  return __hiloint2double(hi, __double2loint(p));
+}
+
 template <int D>
 struct KmvTraits {
   static constexpr int CS = ((D + 1) + 1) & ~1;   // coords + v, padded to even
@@ -43,8 +64,10 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
   constexpr int CS = KmvTraits<D>::CS;
   constexpr int KMV_TC = KmvTraits<D>::TC;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
+  __shared__ double s_t256[256];
   __shared__ __align__(16) double s_col[KMV_TC * CS];
   load_exp2_tab(s_tab);
+  for (int t = threadIdx.x; t < 256; t += KMV_NT) s_t256[t] = g_exp2_256[t];
 
   // local row t -> physical row rows.phys(t) (two blocks when row-sharded)
   const int64_t nrows = rows.size();
@@ -98,7 +121,7 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
           const double tt = sqrt(s);
           acc[t] = fma((1.0 + tt) * exp2_neg(tt * AFN_LOG2E, s_tab), vj, acc[t]);
         } else {
-          acc[t] = fma(exp2_neg(s, s_tab), vj, acc[t]);
+          acc[t] = fma(exp2_neg256(s, s_t256), vj, acc[t]);
         }
       }
     }
@@ -197,6 +220,14 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
                       double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st) {
   const int64_t nrows = rows.size();
   if (nrows <= 0) return AFN_OK;
+  static unsigned long long t256 = 0;  // devices whose table is filled (a __device__ global)
+  int dev = 0;
+  AFN_CUDA(cudaGetDevice(&dev));
+  if (dev < 64 && !(t256 & (1ULL << dev))) {
+    exp2_256_init_kernel<<<1, 256, 0, st>>>();
+    AFN_LAUNCH_CHECK("exp2_256_init_kernel");
+    t256 |= 1ULL << dev;
+  }
   switch (d) {
     case 1: launch_partial<1>(p, st, Xs, v, n, rows, partial, kind); break;
     case 2: launch_partial<2>(p, st, Xs, v, n, rows, partial, kind); break;
