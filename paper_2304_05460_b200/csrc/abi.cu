@@ -866,6 +866,46 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   AFN_CUDA(cudaEventRecord(ev[2], st));
   AFN_PHASE("ev2");
 
+  // kNN pattern of the non-landmark points (own rows; row_ptr in closed form),
+  // then its transpose (the pair-union FSAI needs "rows containing a")
+  std::vector<int64_t*> tmap(nlocal, nullptr);
+  auto pattern_phase = [&](RankSt& s, cudaStream_t ss) -> afn_status {
+    kt_begin(KT_KNN, ss);
+    TRY(ralloc(s, &s.rp, (size_t)N2 + 1, ss));
+    TRY(ralloc(s, &s.col, (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
+    if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, ss, s.lo, s.hi));
+    else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), ss));
+    kt_end(KT_KNN, ss, 0.0);
+    return AFN_OK;
+  };
+  auto transpose_phase = [&](RankSt& s, int q, cudaStream_t ss) -> afn_status {
+    TRY(ralloc(s, &s.gval, (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
+    TRY(ralloc(s, &s.trp, (size_t)N2 + 1, ss));
+    TRY(ralloc(s, &s.tcol, (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
+    TRY(ralloc(s, &s.tval, (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
+    if (N2 > 0) {
+      TRY(ralloc(s, &tmap[q], (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
+      check_pattern_kernel<<<(unsigned)((N2 + 255) / 256), 256, 0, ss>>>(s.rp, s.col, N2, s.derr);
+      AFN_LAUNCH_CHECK("check_pattern_kernel");
+      TRY(csr_transpose(s.rp, s.col, nullptr, N2, h->nnz, s.trp, s.tcol, nullptr, ss, tmap[q]));
+    } else {
+      AFN_CUDA(cudaMemsetAsync(s.trp, 0, sizeof(int64_t), ss));
+    }
+    return AFN_OK;
+  };
+  // single rank, AFN: the pattern does not depend on L or W -> overlap it
+  static const bool no_ovl = getenv("AFN_NO_OVERLAP") != nullptr;
+  const bool povl = !no_ovl && h->R == 1 && !nys && N2 > 0 && k > 0;
+  cudaEvent_t e_pat0 = nullptr, e_pat1 = nullptr;
+  if (povl) {
+    AFN_CUDA(cudaEventCreateWithFlags(&e_pat0, cudaEventDisableTiming));
+    AFN_CUDA(cudaEventCreateWithFlags(&e_pat1, cudaEventDisableTiming));
+  }
+  struct EvPat {
+    cudaEvent_t a, b;
+    ~EvPat() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+  } evpat{e_pat0, e_pat1};
+
   // ---- a1: permutation, permuted + prescaled points; a4: L L^T = K11 + mu I, L^{-T}
   for (int q = 0; q < nlocal; ++q) {
     RankSt& s = h->rk[q];
@@ -897,6 +937,13 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(kmv_prescale(s.Xp, n, d, kn, s.Xs, st));
     TRY(ralloc(s, &s.dinfo, 2, st));
     AFN_CUDA(cudaMemsetAsync(s.dinfo, 0, sizeof(int) * 2, st));
+    if (povl) {  // kNN pattern + its transpose on the side stream, concurrently with L, L^{-1}, W
+      AFN_CUDA(cudaEventRecord(e_pat0, st));
+      AFN_CUDA(cudaStreamWaitEvent(side_stream(), e_pat0, 0));
+      TRY(pattern_phase(s, side_stream()));
+      TRY(transpose_phase(s, q, side_stream()));
+      AFN_CUDA(cudaEventRecord(e_pat1, side_stream()));
+    }
     TRY(ralloc(s, &s.L, (size_t)k * k, st));
     TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
     if (k == 0) continue;
@@ -956,18 +1003,15 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   AFN_CUDA(cudaEventRecord(ev[4], st));
   AFN_PHASE("ev4");
 
-  // ---- a6: kNN pattern (own rows; row_ptr in closed form)
-  kt_begin(KT_KNN, st);
-  for (auto& s : h->rk) {
-    TRY(ralloc(s, &s.rp, (size_t)N2 + 1, st));
-    TRY(ralloc(s, &s.col, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
-    if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, st, s.lo, s.hi));
-    else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), st));
+  // ---- a6: kNN pattern (already queued on the side stream when povl)
+  if (povl) {
+    AFN_CUDA(cudaStreamWaitEvent(st, e_pat1, 0));
+  } else {
+    for (auto& s : h->rk) TRY(pattern_phase(s, st));
   }
-  kt_end(KT_KNN, st, 0.0);
   AFN_CUDA(cudaEventRecord(ev[5], st));
   AFN_PHASE("ev5");
-  if (N2 > 0) {
+  if (N2 > 0 && !povl) {
     // exchange W rows and pattern rows
     {
       int q = 0;
@@ -984,21 +1028,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   AFN_PHASE("ev6");
 
   // ---- a7: FSAI rows (own), then G^T
-  std::vector<int64_t*> tmap(nlocal, nullptr);
-  for (int q = 0; q < nlocal; ++q) {
-    RankSt& s = h->rk[q];
-    TRY(ralloc(s, &s.gval, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
-    TRY(ralloc(s, &s.trp, (size_t)N2 + 1, st));
-    TRY(ralloc(s, &s.tcol, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
-    TRY(ralloc(s, &s.tval, (size_t)(h->nnz > 0 ? h->nnz : 1), st));
-    if (N2 > 0) {
-      TRY(ralloc(s, &tmap[q], (size_t)(h->nnz > 0 ? h->nnz : 1), st));
-      // transposed pattern first (the pair-union FSAI needs "rows containing a")
-      TRY(csr_transpose(s.rp, s.col, nullptr, N2, h->nnz, s.trp, s.tcol, nullptr, st, tmap[q]));
-    } else {
-      AFN_CUDA(cudaMemsetAsync(s.trp, 0, sizeof(int64_t), st));
-    }
-  }
+  if (!povl)
+    for (int q = 0; q < nlocal; ++q) TRY(transpose_phase(h->rk[q], q, st));
   AFN_CUDA(cudaEventRecord(ev[7], st));
   AFN_PHASE("ev7");
   if (N2 > 0) {
