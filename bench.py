@@ -435,7 +435,7 @@ def main():
     roofline = roof(dom) if dom else None
     if roofline is not None:
         roofline["traffic"] = traffic
-    r_kmv = roof("kmv_partial_kernel")
+    r_kmv = roof("kmv_kernel")
     kernel_ms = {k: round(v["ms"], 3) for k, v in kt.items() if v["count"] > 0}
 
     # ---- e2e: host buffers through the C ABI (copies inside the timed region)

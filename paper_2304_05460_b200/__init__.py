@@ -154,8 +154,8 @@ def _stream(stream=None):
     return C.c_void_p(s.cuda_stream)
 
 
-KT_NAMES = ("kmv_partial_kernel", "group_gemm_kernel", "fsai_assemble_kernel", "fsai_chol_kernel",
-            "fsai_gram_kernel", "fps_kernel", "gemm128_bupper_kernel", "trsm_rows_kernel<1>",
+KT_NAMES = ("kmv_kernel", "group_gemm_kernel", "fsai_assemble_kernel", "fsai_chol_kernel",
+            "fsai_gram_kernel", "fps_kernel", "w_gemm_kernel", "trsm_rows_kernel<1>",
             "potrf", "knn_kernel", "apply", "alg1")
 
 

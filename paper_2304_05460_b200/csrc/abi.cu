@@ -435,6 +435,14 @@ afn_status reduce_slots(afn_handle h, unsigned mask, cudaStream_t st) {
   return AFN_OK;
 }
 
+// algorithmic flops of one kernel matvec launch: (3d + 19) per evaluated
+// ordered pair; the symmetric plan evaluates each unordered pair
+// once with one more FMA (column sum): (3d + 21) n (n - 1) / 2
+double kmv_work(afn_handle h, int64_t n, int d) {
+  if (h->rk[0].plan.sym) return (double)n * (double)(n - 1) / 2.0 * (3.0 * d + 21.0);
+  return (double)n * (double)n * (3.0 * d + 19.0) / h->R;
+}
+
 // algorithmic HBM bytes of one apply: W read twice, L^{-T} twice (upper half),
 // G and G^T (values + 4-byte columns) once each, plus the vectors
 double apply_bytes(afn_handle h) {
@@ -1079,8 +1087,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   // ---- workspaces for apply / PCG
   for (auto& s : h->rk) {
     const int64_t nl = s.own.size();
-    s.plan = kmv_plan(n, nl, d, num_sms());
-    TRY(ralloc(s, &s.kmv_part, (size_t)s.plan.chunks * std::max<int64_t>(1, nl), st));
+    s.plan = kmv_plan(n, nl, d, num_sms(), h->R == 1);
+    TRY(ralloc(s, &s.kmv_part, (size_t)std::max<int64_t>(1, s.plan.ws), st));
     const int64_t gw = std::max(std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k)),
                                 nys ? gemv_t_ws(nl, k) : (int64_t)1);
     TRY(ralloc(s, &s.gws, (size_t)gw, st));
@@ -1166,8 +1174,9 @@ int32_t afn_kt_read(double* ms, double* work, int64_t* count, int32_t n) {
 const char* afn_last_error(void) { return g_err; }
 int64_t afn_launch_count(void) { return g_launches.load(); }
 
-afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
-                              const double* v, int64_t row0, int64_t nrows, double* y, void* stream) {
+namespace {
+afn_status kmv_rows_impl(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
+                         const double* v, int64_t row0, int64_t nrows, double* y, void* stream, bool sym_ok) {
   TRY(validate_X(X, n, d));
   REQ(kernel == AFN_KERNEL_GAUSSIAN || kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", kernel);
   REQ(l > 0 && std::isfinite(l), "l must be > 0");
@@ -1180,16 +1189,24 @@ afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t ker
   double* Xs;
   TRY(t.get(&Xs, (size_t)n * d));
   TRY(kmv_prescale(X, n, d, Kern{kernel, l}, Xs, st));
-  KmvPlan plan = kmv_plan(n, nrows, d, num_sms());
+  KmvPlan plan = kmv_plan(n, nrows, d, num_sms(), sym_ok);
   double* part;
-  TRY(t.get(&part, (size_t)plan.chunks * (nrows > 0 ? nrows : 1)));
+  TRY(t.get(&part, (size_t)std::max<int64_t>(1, plan.ws)));
   TRY(kmv_launch(Xs, n, d, kernel, v, mu, seg_range(row0, nrows), y, false, part, plan, st));
   return AFN_OK;
+}
+}  // namespace
+
+// explicit row ranges never use the symmetric plan: a shard's rows are then
+// bit-identical to the same rows of any other row-range evaluation
+afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
+                              const double* v, int64_t row0, int64_t nrows, double* y, void* stream) {
+  return kmv_rows_impl(X, n, d, kernel, l, mu, v, row0, nrows, y, stream, false);
 }
 
 afn_status kernel_matvec(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
                          const double* v, double* y, void* stream) {
-  return kernel_matvec_rows(X, n, d, kernel, l, mu, v, 0, n, y, stream);
+  return kmv_rows_impl(X, n, d, kernel, l, mu, v, 0, n, y, stream, true);
 }
 
 afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t seed, int64_t* idx,
@@ -1359,7 +1376,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
         kt_begin(KT_KMV, st);
         for (auto& s : h->rk)
           TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
-        kt_end(KT_KMV, st, (double)n * (double)n * (3.0 * d + 19.0) / h->R);
+        kt_end(KT_KMV, st, kmv_work(h, n, d));
         kmE.push_back(new_ev());
         AFN_CUDA(cudaEventRecord(kmE.back(), st));
         for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));

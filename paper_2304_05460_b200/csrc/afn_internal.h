@@ -72,8 +72,15 @@ void dfree(void* p, cudaStream_t st);
 // ---- kernel matvec (kmv.cu) ----------------------------------------------
 struct KmvPlan {
   int64_t row_tiles = 0, chunks = 1, chunk_cols = 0;
+  // symmetric full matvec (each unordered pair once, row and column sums):
+  // row blocks of sym_rbw rows x column chunks of sym_cw (sym_rbw = m sym_cw)
+  bool sym = false;
+  int64_t sym_rbw = 0, sym_cw = 0, sym_nc = 0, sym_nrb = 0, sym_items = 0;
+  int64_t ws = 0;  // workspace doubles for kmv_launch
 };
-KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms);
+// sym_ok: a full matvec (nrows == n) may use the symmetric kernel (its row
+// sums differ from a row shard's by rounding; kernel_matvec_rows never uses it)
+KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok = false);
 // Xs = X * sqrt(log2 e)/l   (n x d)
 afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st);
 // rows `rows` of (K + mu I) v (v: all n entries); partial: chunks*rows.size() doubles.

@@ -14,6 +14,7 @@
 // per pair (d=3: 28; the direct-difference + degree-6/16-entry-table exp
 // formulation of DESIGN.md, FMA = 2), independent of later instruction savings.
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 
 #include "afn_common.cuh"
@@ -133,6 +134,141 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
   }
 }
 
+// Symmetric variant for the full matvec: K is symmetric, so every unordered
+// pair (i < j) is evaluated once and feeds both q_i (+= K_ij v_j, row sums in
+// registers) and q_j (+= K_ij v_i, column sums: a warp butterfly per column,
+// then the 8 warps in order through shared memory) -- half the exp2 work.
+// Work item (I, c): row block I (RBW = KMV_NT RB rows) x column chunk c >= m I
+// (CW = RBW / m columns); in the chunks inside block I only j > i counts.
+// R[c][i]: row sums of item (I(i), c); Cb[I][j]: column sums of item (I, c(j)).
+template <int D, int RB, int KER>
+__global__ void __launch_bounds__(KMV_NT, 2)
+kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int64_t n, int64_t nrb,
+               int64_t nc, int64_t cw, int m, double* __restrict__ R, double* __restrict__ Cb,
+               const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;  // PCG already stopped (device-side flag)
+  constexpr int CS = KmvTraits<D>::CS;
+  constexpr int KMV_TC = 256;  // columns per shared-memory tile (+ 8 x 256 column partials)
+  constexpr int NW = KMV_NT / 32;
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+  __shared__ double s_t256[256];
+  __shared__ __align__(16) double s_col[KMV_TC * CS];
+  __shared__ double s_cs[NW][KMV_TC];
+  load_exp2_tab(s_tab);
+  for (int t = threadIdx.x; t < 256; t += KMV_NT) s_t256[t] = g_exp2_256[t];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // item -> (I, c): block I owns the items c = m I .. nc - 1
+  int64_t it = blockIdx.x, I = 0;
+  while (I < nrb && it >= nc - m * I) { it -= nc - m * I; ++I; }
+  const int64_t c = m * I + it;
+  const bool diag = c < m * (I + 1);
+  const int64_t rb0 = I * (int64_t)(KMV_NT * RB);
+  double xi[RB][D], vi[RB], acc[RB];
+  int64_t ri[RB];
+#pragma unroll
+  for (int t = 0; t < RB; ++t) {
+    ri[t] = rb0 + threadIdx.x + (int64_t)t * KMV_NT;
+    const bool ok = ri[t] < n;
+#pragma unroll
+    for (int q = 0; q < D; ++q) xi[t][q] = ok ? Xs[ri[t] * D + q] : 0.0;
+    vi[t] = ok ? v[ri[t]] : 0.0;
+    acc[t] = 0.0;
+  }
+  const int64_t c0 = c * cw, c1 = min(n, c0 + cw);
+  for (int64_t tb = c0; tb < c1; tb += KMV_TC) {
+    const int tcn = (int)min((int64_t)KMV_TC, c1 - tb);
+    __syncthreads();
+    for (int e = threadIdx.x; e < KMV_TC * CS; e += KMV_NT) {
+      const int j = e / CS, q = e - j * CS;
+      double val = 0.0;
+      if (j < tcn) {
+        if (q < D) val = Xs[(tb + j) * D + q];
+        else if (q == D) val = v[tb + j];
+      }
+      s_col[e] = val;
+    }
+    __syncthreads();
+    // 4 columns at a time; their column sums are reduced across the warp
+    // together (a 2-level exchange leaves each lane one column summed over 4
+    // lanes, then 3 butterfly levels): 12 shuffles per 4 columns instead of 40
+    auto body = [&](auto masked) {
+#pragma unroll 2
+      for (int j0 = 0; j0 < tcn; j0 += 4) {
+        double cs[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = j0 + u;  // (tile padded with zero columns: v_j = 0, x_j = 0)
+          double xj[CS];
+#pragma unroll
+          for (int q = 0; q < CS; q += 2) {
+            const double2 w2 = *reinterpret_cast<const double2*>(&s_col[j * CS + q]);
+            xj[q] = w2.x;
+            xj[q + 1] = w2.y;
+          }
+          const double vj = xj[D];
+          const int64_t gj = tb + j;
+          double csu = 0.0;
+#pragma unroll
+          for (int t = 0; t < RB; ++t) {
+            double dd = xi[t][0] - xj[0];
+            double s = dd * dd;
+#pragma unroll
+            for (int q = 1; q < D; ++q) {
+              dd = xi[t][q] - xj[q];
+              s = fma(dd, dd, s);
+            }
+            double kv;
+            if (KER == 1) {
+              const double tt = sqrt(s);
+              kv = (1.0 + tt) * exp2_neg(tt * AFN_LOG2E, s_tab);
+            } else {
+              kv = exp2_neg256(s, s_t256);
+            }
+            if (decltype(masked)::value && gj <= ri[t]) kv = 0.0;  // block-diagonal chunk: j > i only
+            acc[t] = fma(kv, vj, acc[t]);
+            csu = fma(kv, vi[t], csu);
+          }
+          cs[u] = csu;
+        }
+        const bool b0 = lane & 1, b1 = (lane >> 1) & 1;
+        const double k0 = (b0 ? cs[2] : cs[0]) + __shfl_xor_sync(0xffffffffu, b0 ? cs[0] : cs[2], 1);
+        const double k1 = (b0 ? cs[3] : cs[1]) + __shfl_xor_sync(0xffffffffu, b0 ? cs[1] : cs[3], 1);
+        double c = (b1 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
+        c += __shfl_xor_sync(0xffffffffu, c, 4);
+        c += __shfl_xor_sync(0xffffffffu, c, 8);
+        c += __shfl_xor_sync(0xffffffffu, c, 16);
+        if (lane < 4) s_cs[wid][j0 + 2 * b0 + b1] = c;  // column j0 + 2 b0 + b1
+      }
+    };
+    if (diag) body(std::true_type{});
+    else body(std::false_type{});
+    __syncthreads();
+    for (int j = threadIdx.x; j < tcn; j += KMV_NT) {
+      double t2 = s_cs[0][j];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) t2 += s_cs[w][j];
+      Cb[I * n + tb + j] = t2;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < RB; ++t)
+    if (ri[t] < n) R[c * n + ri[t]] = acc[t];
+}
+
+// q_i = (1 + mu) v_i + sum_{c >= m I(i)} R[c][i] + sum_{I <= I(i)} Cb[I][i]  (fixed order)
+__global__ void kmv_sym_reduce_kernel(const double* __restrict__ R, const double* __restrict__ Cb, int64_t n,
+                                      int64_t nc, int64_t rbw, int64_t cw, const double* __restrict__ v,
+                                      double mu, double* __restrict__ y, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t Ii = i / rbw, m = rbw / cw;
+  double s = 0.0;
+  for (int64_t c = m * Ii; c < nc; ++c) s += R[c * n + i];
+  for (int64_t I = 0; I <= Ii; ++I) s += Cb[I * n + i];
+  y[i] = fma(1.0 + mu, v[i], s);
+}
+
 __global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, Seg2 rows,
                                   const double* __restrict__ v, double mu, bool y_phys,
                                   double* __restrict__ y, const double* skip) {
@@ -197,14 +333,43 @@ KmvPlan plan_for(int64_t n, int64_t nrows, int d, int num_sms) {
 // the chunking of the full n-row plan (so sharded rows are bit-identical to
 // the single-GPU matvec) unless that would leave it under two waves of CTAs,
 // in which case the shard gets its own plan.
-KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms) {
-  const KmvPlan full = plan_for(n, n, d, num_sms);
+KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
+  static const bool nosym = getenv("AFN_KMV_NOSYM") != nullptr;
+  if (sym_ok && !nosym && nrows == n && n >= 2048) {
+    // symmetric plan: the widest column chunk (RBW, RBW/2, ..., 128) that
+    // still gives >= 1.5 waves of 2 CTAs/SM (C2: 256 -> 544 items; measured
+    // 1024: 0.286, 512: 0.237, 256: 0.230, 128: 0.233 ms)
+    KmvPlan p;
+    p.sym = true;
+    p.sym_rbw = (int64_t)KMV_NT * rows_per_thread(d);
+    p.sym_nrb = (n + p.sym_rbw - 1) / p.sym_rbw;
+    const int64_t slots = (int64_t)num_sms * 2;
+    static const int64_t force_cw = getenv("AFN_KMV_SYM_CW") ? atoll(getenv("AFN_KMV_SYM_CW")) : 0;
+    for (int64_t cw = p.sym_rbw; cw >= 128; cw /= 2) {
+      if (force_cw > 0 && cw != force_cw) continue;
+      const int64_t m = p.sym_rbw / cw;
+      const int64_t nc = (n + cw - 1) / cw;
+      int64_t items = 0;
+      for (int64_t I = 0; I < p.sym_nrb; ++I) items += std::max<int64_t>(0, nc - m * I);
+      p.sym_cw = cw;
+      p.sym_nc = nc;
+      p.sym_items = items;
+      if (2 * items >= 3 * slots) break;
+    }
+    p.ws = (p.sym_nc + p.sym_nrb) * n;
+    return p;
+  }
+  KmvPlan full = plan_for(n, n, d, num_sms);
+  full.ws = full.chunks * std::max<int64_t>(1, nrows);
   if (nrows == n) return full;
   KmvPlan p = full;
   const int64_t rows_per_cta = (int64_t)KMV_NT * rows_per_thread(d);
   p.row_tiles = (nrows + rows_per_cta - 1) / rows_per_cta;
+  p.ws = p.chunks * std::max<int64_t>(1, nrows);
   if (p.row_tiles * p.chunks >= 2 * 2 * (int64_t)num_sms) return p;
-  return plan_for(n, nrows, d, num_sms);
+  KmvPlan q = plan_for(n, nrows, d, num_sms);
+  q.ws = q.chunks * std::max<int64_t>(1, nrows);
+  return q;
 }
 
 afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st) {
@@ -227,6 +392,35 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
     exp2_256_init_kernel<<<1, 256, 0, st>>>();
     AFN_LAUNCH_CHECK("exp2_256_init_kernel");
     t256 |= 1ULL << dev;
+  }
+  if (p.sym) {
+    if (!(rows.na + rows.nb == n && rows.a0 == 0 && (rows.nb == 0 || rows.b0 == rows.na))) {
+      set_error("kernel_matvec: symmetric plan needs all rows");
+      return AFN_ERR_ARG;
+    }
+    double* R = partial;
+    double* Cb = partial + p.sym_nc * n;
+    const int m = (int)(p.sym_rbw / p.sym_cw);
+    switch (d) {
+#define AFN_SYM(DD)                                                                                     \
+  case DD:                                                                                              \
+    if (kind == 1)                                                                                      \
+      kmv_sym_kernel<DD, KmvTraits<DD>::RB, 1><<<(unsigned)p.sym_items, KMV_NT, 0, st>>>(                \
+          Xs, v, n, p.sym_nrb, p.sym_nc, p.sym_cw, m, R, Cb, get_skip());                                \
+    else                                                                                                \
+      kmv_sym_kernel<DD, KmvTraits<DD>::RB, 0><<<(unsigned)p.sym_items, KMV_NT, 0, st>>>(                \
+          Xs, v, n, p.sym_nrb, p.sym_nc, p.sym_cw, m, R, Cb, get_skip());                                \
+    break;
+      AFN_SYM(1) AFN_SYM(2) AFN_SYM(3) AFN_SYM(4) AFN_SYM(5) AFN_SYM(6) AFN_SYM(7) AFN_SYM(8)
+#undef AFN_SYM
+      default: set_error("kernel_matvec: symmetric plan for d=%d unsupported (1..8)", d); return AFN_ERR_ARG;
+    }
+    AFN_LAUNCH_CHECK("kmv_sym_kernel");
+    const int nt = 256;
+    kmv_sym_reduce_kernel<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(R, Cb, n, p.sym_nc, p.sym_rbw, p.sym_cw, v,
+                                                                        mu, y, get_skip());
+    AFN_LAUNCH_CHECK("kmv_sym_reduce_kernel");
+    return AFN_OK;
   }
   switch (d) {
     case 1: launch_partial<1>(p, st, Xs, v, n, rows, partial, kind); break;
