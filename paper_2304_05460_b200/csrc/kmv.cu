@@ -142,7 +142,7 @@ kmv_partial_kernel(const double* __restrict__ Xs, const double* __restrict__ v, 
 // (CW = RBW / m columns); in the chunks inside block I only j > i counts.
 // R[c][i]: row sums of item (I(i), c); Cb[I][j]: column sums of item (I, c(j)).
 template <int D, int RB, int KER>
-__global__ void __launch_bounds__(KMV_NT, 2)
+__global__ void __launch_bounds__(KMV_NT, RB <= 2 ? 3 : 2)
 kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int64_t n, int64_t nrb,
                int64_t nc, int64_t cw, int m, double* __restrict__ R, double* __restrict__ Cb,
                const double* skip) {
@@ -299,6 +299,11 @@ void launch_partial(const KmvPlan& p, cudaStream_t st, const double* Xs, const d
 }
 
 int rows_per_thread(int d) { return d <= 4 ? 4 : (d <= 8 ? 2 : 1); }
+// symmetric kernel: AFN_KMV_SYM_RB=2 -> 2 rows per thread (3 CTAs/SM)
+int sym_rows_per_thread(int d) {
+  static const int rb = getenv("AFN_KMV_SYM_RB") ? atoi(getenv("AFN_KMV_SYM_RB")) : 4;
+  return (rb == 2 || d > 4) ? std::min(2, rows_per_thread(d)) : rows_per_thread(d);
+}
 
 }  // namespace
 
@@ -341,7 +346,7 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
     // 1024: 0.286, 512: 0.237, 256: 0.230, 128: 0.233 ms)
     KmvPlan p;
     p.sym = true;
-    p.sym_rbw = (int64_t)KMV_NT * rows_per_thread(d);
+    p.sym_rbw = (int64_t)KMV_NT * sym_rows_per_thread(d);
     p.sym_nrb = (n + p.sym_rbw - 1) / p.sym_rbw;
     const int64_t slots = (int64_t)num_sms * 2;
     static const int64_t force_cw = getenv("AFN_KMV_SYM_CW") ? atoll(getenv("AFN_KMV_SYM_CW")) : 0;
@@ -371,6 +376,20 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
   q.ws = q.chunks * std::max<int64_t>(1, nrows);
   return q;
 }
+
+namespace {
+template <int D, int KER>
+void sym_launch(const KmvPlan& p, cudaStream_t st, const double* Xs, const double* v, int64_t n, int m, double* R,
+                double* Cb) {
+  constexpr int RB = KmvTraits<D>::RB;
+  if (p.sym_rbw == (int64_t)KMV_NT * RB)
+    kmv_sym_kernel<D, RB, KER><<<(unsigned)p.sym_items, KMV_NT, 0, st>>>(Xs, v, n, p.sym_nrb, p.sym_nc, p.sym_cw,
+                                                                        m, R, Cb, get_skip());
+  else
+    kmv_sym_kernel<D, (RB >= 2 ? 2 : 1), KER><<<(unsigned)p.sym_items, KMV_NT, 0, st>>>(
+        Xs, v, n, p.sym_nrb, p.sym_nc, p.sym_cw, m, R, Cb, get_skip());
+}
+}  // namespace
 
 afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st) {
   const double f = kn.kind == 1 ? AFN_SQRT3 / kn.l : AFN_SQRT_LOG2E / kn.l;
@@ -405,11 +424,9 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
 #define AFN_SYM(DD)                                                                                     \
   case DD:                                                                                              \
     if (kind == 1)                                                                                      \
-      kmv_sym_kernel<DD, KmvTraits<DD>::RB, 1><<<(unsigned)p.sym_items, KMV_NT, 0, st>>>(                \
-          Xs, v, n, p.sym_nrb, p.sym_nc, p.sym_cw, m, R, Cb, get_skip());                                \
+      sym_launch<DD, 1>(p, st, Xs, v, n, m, R, Cb);                                                    \
     else                                                                                                \
-      kmv_sym_kernel<DD, KmvTraits<DD>::RB, 0><<<(unsigned)p.sym_items, KMV_NT, 0, st>>>(                \
-          Xs, v, n, p.sym_nrb, p.sym_nc, p.sym_cw, m, R, Cb, get_skip());                                \
+      sym_launch<DD, 0>(p, st, Xs, v, n, m, R, Cb);                                                    \
     break;
       AFN_SYM(1) AFN_SYM(2) AFN_SYM(3) AFN_SYM(4) AFN_SYM(5) AFN_SYM(6) AFN_SYM(7) AFN_SYM(8)
 #undef AFN_SYM
