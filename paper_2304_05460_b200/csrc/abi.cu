@@ -112,6 +112,13 @@ void kt_end(int id, cudaStream_t st, double work) {
   cudaEventRecord(e1, st);
   g_kt_pending.push_back({id, g_kt_open[id], e1, work});
 }
+// add a timing measured elsewhere (events of a replayed CUDA graph)
+void kt_add(int id, double ms, double work) {
+  if (!kt_enabled()) return;
+  g_kt_ms[id] += ms;
+  g_kt_work[id] += work;
+  g_kt_cnt[id] += 1;
+}
 // forget the last `count` pending timings of `id` (launches that were queued
 // but skipped on the device)
 void kt_drop_last(int id, int count) {
@@ -321,6 +328,16 @@ cudaStream_t side_stream() {
   if (dev < 0 || dev >= 64) dev = 0;
   if (!ss[dev]) cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
   return ss[dev];
+}
+
+// non-blocking stream per device and host thread for PCG graph capture / replay
+cudaStream_t graph_stream() {
+  static thread_local cudaStream_t gs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!gs[dev]) cudaStreamCreateWithFlags(&gs[dev], cudaStreamNonBlocking);
+  return gs[dev];
 }
 
 // two pinned int64 per host thread (FPS early-stop value)
@@ -1338,7 +1355,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
       cudaStream_t st;
       ~HFree() { dfree(p, st); }
     } hfree{dhist, st};
-    for (auto& s : h->rk) AFN_CUDA(cudaMemsetAsync(s.sc + SC_DONE, 0, sizeof(double) * 2, st));
+    for (auto& s : h->rk) AFN_CUDA(cudaMemsetAsync(s.sc + SC_DONE, 0, sizeof(double) * 3, st));  // DONE, ITS, IT
     std::vector<cudaEvent_t> evs;  // per queued iteration: kmv begin/end, apply begin/end
     struct EvFree {
       std::vector<cudaEvent_t>* v;
@@ -1358,49 +1375,158 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     TRY(reduce_slots(h, 1u << cur, st));
     for (auto& s : h->rk) TRY(vec_copy(s.p, s.z, s.own, st));
     int queued = 0, chunk = 1, code = 0;
+    // per queued iteration: kmv begin/end, apply begin/end (host-side loop) ...
     std::vector<cudaEvent_t> kmE, apE;
+    double kmv_ms_acc = 0.0, ap_ms_acc = 0.0;
+    int kmv_seen = 0;  // host-loop iterations queued so far (index into kmE / apE)
+    // ... and a CUDA graph of PCG_CHUNK iterations (one rank): captured once per
+    // solve, replayed per chunk (the iteration number lives on the device);
+    // its event nodes are read after each replay.  AFN_PCG_GRAPH=0 disables.
+    static const bool use_graph = !(getenv("AFN_PCG_GRAPH") && atoi(getenv("AFN_PCG_GRAPH")) == 0);
+    cudaGraphExec_t gexec = nullptr;
+    int64_t glaunches = 0;
+    std::vector<cudaEvent_t> gE;
+    cudaEvent_t gj0 = nullptr, gj1 = nullptr;
+    struct GFree {
+      cudaGraphExec_t* g;
+      std::vector<cudaEvent_t>* e;
+      cudaEvent_t* j0;
+      cudaEvent_t* j1;
+      ~GFree() {
+        if (*g) cudaGraphExecDestroy(*g);
+        for (auto x : *e) cudaEventDestroy(x);
+        if (*j0) cudaEventDestroy(*j0);
+        if (*j1) cudaEventDestroy(*j1);
+      }
+    } gfree{&gexec, &gE, &gj0, &gj1};
+    // one iteration; events ek0..ea1 bracket the matvec and the apply; kt: per-launch timers
+    auto enqueue_iter = [&](cudaEvent_t ek0, cudaEvent_t ek1, cudaEvent_t ea0, cudaEvent_t ea1,
+                            bool kt) -> afn_status {
+      // (in a capture, kt == false: event record nodes need cudaEventRecordExternal)
+      const unsigned ef = kt ? cudaEventRecordDefault : cudaEventRecordExternal;
+      AFN_CUDA(cudaEventRecordWithFlags(ek0, st, ef));
+      if (h->R > 1) {  // p: every rank's rows (the north star's per-iteration all-gather)
+        AFN_CUDA(cudaEventRecord(cm.next(), st));
+        TRY(exchange(h, [](RankSt& s) { return s.p; }, [&](int s) { return vec_ranges(h, s); }, st));
+        AFN_CUDA(cudaEventRecord(cm.next(), st));
+      }
+      if (kt) kt_begin(KT_KMV, st);
+      for (auto& s : h->rk)
+        TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+      if (kt) kt_end(KT_KMV, st, kmv_work(h, n, d));
+      AFN_CUDA(cudaEventRecordWithFlags(ek1, st, ef));
+      for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
+      TRY(reduce_slots(h, 1u << SC_PQ, st));
+      for (auto& s : h->rk)
+        TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
+      TRY(reduce_slots(h, 1u << SC_RR, st));
+      for (auto& s : h->rk) TRY(pcg_check(s.sc, nb, tol, maxit, fixed_iters, dhist, st));
+      AFN_CUDA(cudaEventRecordWithFlags(ea0, st, ef));
+      if (kt) kt_begin(KT_APPLY, st);
+      TRY(apply());
+      if (kt) kt_end(KT_APPLY, st, apply_bytes(h) / h->R);
+      AFN_CUDA(cudaEventRecordWithFlags(ea1, st, ef));
+      const int nxt = cur ^ 1;
+      for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, nxt), s.dws, s.dcnt, st));
+      TRY(reduce_slots(h, 1u << nxt, st));
+      for (auto& s : h->rk) TRY(pcg_update_p(s.p, s.z, s.own, s.sc, nxt, cur, st));
+      cur = nxt;
+      return AFN_OK;
+    };
     while (queued < maxit) {
       const int upto = std::min(maxit, queued + chunk);
       set_skip(h->rk[0].sc + SC_DONE);
       struct SkipOff {
         ~SkipOff() { set_skip(nullptr); }
       } skipoff;
-      for (int t = queued + 1; t <= upto; ++t) {
-        kmE.push_back(new_ev());
-        AFN_CUDA(cudaEventRecord(kmE.back(), st));
-        if (h->R > 1) {  // p: every rank's rows (the north star's per-iteration all-gather)
-          AFN_CUDA(cudaEventRecord(cm.next(), st));
-          TRY(exchange(h, [](RankSt& s) { return s.p; }, [&](int s) { return vec_ranges(h, s); }, st));
-          AFN_CUDA(cudaEventRecord(cm.next(), st));
+      const bool graph = use_graph && h->R == 1 && chunk == PCG_CHUNK && upto - queued == PCG_CHUNK &&
+                         (PCG_CHUNK & 1) == 0;
+      if (graph) {
+        // capture / replay on a private non-blocking stream (the caller's
+        // stream may be the legacy default stream, which cannot capture),
+        // ordered after and before the caller's stream by events
+        const cudaStream_t user_st = st;
+        cudaStream_t gs = graph_stream();
+        if (!gj0) {
+          AFN_CUDA(cudaEventCreateWithFlags(&gj0, cudaEventDisableTiming));
+          AFN_CUDA(cudaEventCreateWithFlags(&gj1, cudaEventDisableTiming));
         }
-        kt_begin(KT_KMV, st);
-        for (auto& s : h->rk)
-          TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
-        kt_end(KT_KMV, st, kmv_work(h, n, d));
-        kmE.push_back(new_ev());
-        AFN_CUDA(cudaEventRecord(kmE.back(), st));
-        for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
-        TRY(reduce_slots(h, 1u << SC_PQ, st));
-        for (auto& s : h->rk)
-          TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
-        TRY(reduce_slots(h, 1u << SC_RR, st));
-        for (auto& s : h->rk) TRY(pcg_check(s.sc, t, nb, tol, maxit, fixed_iters, dhist, st));
-        apE.push_back(new_ev());
-        AFN_CUDA(cudaEventRecord(apE.back(), st));
-        kt_begin(KT_APPLY, st);
-        TRY(apply());
-        kt_end(KT_APPLY, st, apply_bytes(h) / h->R);
-        apE.push_back(new_ev());
-        AFN_CUDA(cudaEventRecord(apE.back(), st));
-        const int nxt = cur ^ 1;
-        for (auto& s : h->rk) TRY(dot(s.r, s.z, s.own, part_dst(h, s, nxt), s.dws, s.dcnt, st));
-        TRY(reduce_slots(h, 1u << nxt, st));
-        for (auto& s : h->rk) TRY(pcg_update_p(s.p, s.z, s.own, s.sc, nxt, cur, st));
-        cur = nxt;
+        AFN_CUDA(cudaEventRecord(gj0, user_st));
+        AFN_CUDA(cudaStreamWaitEvent(gs, gj0, 0));
+        st = gs;
+        struct Restore {
+          cudaStream_t* p;
+          cudaStream_t v;
+          ~Restore() { *p = v; }
+        } restore{&st, user_st};
+        if (!gexec) {  // capture PCG_CHUNK iterations (cur returns to its value: even count)
+          for (int e = 0; e < 4 * PCG_CHUNK; ++e) {
+            cudaEvent_t x;
+            AFN_CUDA(cudaEventCreate(&x));
+            gE.push_back(x);
+          }
+          cudaGraph_t g = nullptr;
+          const int64_t l0 = afn_launch_count();
+          AFN_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+          afn_status cs = AFN_OK;
+          for (int t = 0; t < PCG_CHUNK && cs == AFN_OK; ++t)
+            cs = enqueue_iter(gE[4 * t], gE[4 * t + 1], gE[4 * t + 2], gE[4 * t + 3], false);
+          const cudaError_t ce = cudaStreamEndCapture(st, &g);
+          if (cs != AFN_OK) {
+            if (g) cudaGraphDestroy(g);
+            return cs;
+          }
+          AFN_CUDA(ce);
+          const cudaError_t ie = cudaGraphInstantiate(&gexec, g, 0);
+          cudaGraphDestroy(g);
+          AFN_CUDA(ie);
+          glaunches = afn_launch_count() - l0;  // kernels per replay
+          note_launch((int)-glaunches);          // (counted per replay below)
+        }
+        AFN_CUDA(cudaGraphLaunch(gexec, st));
+        note_launch((int)glaunches);
+        AFN_CUDA(cudaEventRecord(gj1, gs));
+        AFN_CUDA(cudaStreamWaitEvent(user_st, gj1, 0));
+      } else {
+        for (int t = queued + 1; t <= upto; ++t) {
+          kmE.push_back(new_ev());
+          kmE.push_back(new_ev());
+          apE.push_back(new_ev());
+          apE.push_back(new_ev());
+          TRY(enqueue_iter(kmE[kmE.size() - 2], kmE.back(), apE[apE.size() - 2], apE.back(), true));
+        }
       }
-      queued = upto;
       TRY(sc_to_host());
       code = (int)hsc[SC_DONE];
+      // the chunk's iterations that really ran (the rest returned at once)
+      const int its_now = code != 0 ? (int)hsc[SC_ITS] : upto;
+      const int kmv_last = std::min(upto, its_now + (code == 2 ? 1 : 0));
+      const int ap_last = code == 0 ? upto : std::min(upto, its_now - 1 + (code == 2 || code == 3 ? 1 : 0));
+      if (graph) {
+        for (int t = queued + 1; t <= upto; ++t) {
+          const int q = t - queued - 1;
+          if (t <= kmv_last) {
+            const double ms = ev_ms(gE[4 * q], gE[4 * q + 1]);
+            kmv_ms_acc += ms;
+            kt_add(KT_KMV, ms, kmv_work(h, n, d));
+          }
+          if (t <= ap_last) {
+            const double ms = ev_ms(gE[4 * q + 2], gE[4 * q + 3]);
+            ap_ms_acc += ms;
+            kt_add(KT_APPLY, ms, apply_bytes(h) / h->R);
+          }
+        }
+      } else {
+        for (int t = queued + 1; t <= upto; ++t) {
+          const size_t q = (size_t)(kmv_seen + (t - queued - 1));
+          if (t <= kmv_last) kmv_ms_acc += ev_ms(kmE[2 * q], kmE[2 * q + 1]);
+          if (t <= ap_last) ap_ms_acc += ev_ms(apE[2 * q], apE[2 * q + 1]);
+        }
+        kt_drop_last(KT_KMV, upto - std::max(queued, kmv_last));
+        kt_drop_last(KT_APPLY, upto - std::max(queued, ap_last));
+        kmv_seen += upto - queued;
+      }
+      queued = upto;
       if (code != 0) break;
       chunk = std::min(chunk * 2, PCG_CHUNK);
     }
@@ -1425,12 +1551,9 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     if (R.history)
       for (int t = 1; t <= it; ++t) R.history[t] = hh[t];
     R.converged = code == 1 && rel <= tol;
-    mv_ms = 0.0;
-    for (int t = 0; t < kmv_real; ++t) mv_ms += ev_ms(kmE[2 * t], kmE[2 * t + 1]);
-    ap_ms = ev_ms(ap0, ap1);
-    for (int t = 0; t < ap_real; ++t) ap_ms += ev_ms(apE[2 * t], apE[2 * t + 1]);
-    kt_drop_last(KT_KMV, queued - kmv_real);
-    kt_drop_last(KT_APPLY, queued - ap_real);
+    (void)kmv_real;
+    mv_ms = kmv_ms_acc;
+    ap_ms = ev_ms(ap0, ap1) + ap_ms_acc;
   } else {
     R.converged = 1;
   }

@@ -162,13 +162,13 @@ int64_t dot_ws();
 afn_status dot(const double* a, const double* b, Seg2 g, double* out, double* ws, unsigned* cnt,
                cudaStream_t st);
 // PCG scalar slots (device doubles): rz alternates between slots 0 and 1
-enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_DONE = 6, SC_ITS = 7, SC_N = 8 };
+enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_DONE = 6, SC_ITS = 7, SC_IT = 8, SC_N = 16 };
 // Device-side skip flag for the apply / matvec kernels queued by the PCG loop
 // (kernels return at once when *flag != 0); nullptr = never skip.  Per host thread.
 void set_skip(const double* flag);
 const double* get_skip();
-afn_status pcg_check(double* sc, int it, double nb, double tol, int maxit, int fixed, double* hist,
-                     cudaStream_t st);
+// advances the device iteration counter sc[SC_IT] (graph-replayable)
+afn_status pcg_check(double* sc, double nb, double tol, int maxit, int fixed, double* hist, cudaStream_t st);
 // x += a p; r -= a q over g with a = sc[rz_slot]/sc[PQ] (0 if PQ <= 0); *rr = r.r over g
 afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q, Seg2 g,
                          const double* sc, int rz_slot, double* rr, double* ws, unsigned* cnt,

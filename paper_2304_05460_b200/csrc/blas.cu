@@ -389,8 +389,9 @@ int64_t gemv_t_rows_per_block(int64_t R) {
 // without a host round trip per iteration.  sc[SC_DONE]: 0 running, 1 stop
 // test met (rel <= tol, or fixed_iters reached), 2 breakdown, 3 maxit
 // exhausted; sc[SC_ITS]: the iteration count of the result.
-__global__ void pcg_check_kernel(double* sc, int it, double nb, double tol, int maxit, int fixed,
-                                 double* hist) {
+__global__ void pcg_check_kernel(double* sc, double nb, double tol, int maxit, int fixed, double* hist) {
+  const int it = (int)sc[SC_IT] + 1;  // this iteration's number (device counter)
+  sc[SC_IT] = it;
   if (sc[SC_DONE] != 0.0) return;
   const double pq = sc[SC_PQ], rr = sc[SC_RR];
   if (!(pq > 0.0) || !isfinite(pq) || !isfinite(rr)) {
@@ -414,9 +415,8 @@ thread_local const double* t_skip = nullptr;
 void set_skip(const double* flag) { t_skip = flag; }
 const double* get_skip() { return t_skip; }
 
-afn_status pcg_check(double* sc, int it, double nb, double tol, int maxit, int fixed, double* hist,
-                     cudaStream_t st) {
-  pcg_check_kernel<<<1, 1, 0, st>>>(sc, it, nb, tol, maxit, fixed, hist);
+afn_status pcg_check(double* sc, double nb, double tol, int maxit, int fixed, double* hist, cudaStream_t st) {
+  pcg_check_kernel<<<1, 1, 0, st>>>(sc, nb, tol, maxit, fixed, hist);
   AFN_LAUNCH_CHECK("pcg_check_kernel");
   return AFN_OK;
 }
