@@ -987,15 +987,20 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   }
   AFN_CUDA(cudaEventRecord(ev[3], st));
   AFN_PHASE("ev3");
-  for (auto& s : h->rk) {
-    int info = 0;
-    AFN_CUDA(cudaMemcpyAsync(&info, s.dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
-    AFN_CUDA(cudaStreamSynchronize(st));
-    if (info) {
-      set_error("Cholesky of K11 + %s I broke down at row %d", nys ? "nu" : "mu", info - 1);
-      return AFN_ERR_NOT_SPD;
+  auto chol_check = [&]() -> afn_status {
+    for (auto& s : h->rk) {
+      int info = 0;
+      AFN_CUDA(cudaMemcpyAsync(&info, s.dinfo, sizeof(int), cudaMemcpyDeviceToHost, st));
+      AFN_CUDA(cudaStreamSynchronize(st));
+      if (info) {
+        set_error("Cholesky of K11 + %s I broke down at row %d", nys ? "nu" : "mu", info - 1);
+        return AFN_ERR_NOT_SPD;
+      }
     }
-  }
+    return AFN_OK;
+  };
+  // (AFN, one rank: checked after the FSAI work is queued, see below)
+  if (nys || !povl) TRY(chol_check());
   if (nys) {
     TRY(build_nystrom(h, st));
     AFN_CUDA(cudaEventRecord(ev[4], st));
@@ -1065,7 +1070,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       afn_status fs = AFN_ERR_STATE;
       if (variant < 0) {
         fs = fsai_sddmm_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo, s.hi,
-                            s.gval, s.dinfo + 1, st);
+                            s.gval, s.dinfo + 1, st, povl ? side_stream() : st);
         if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
       }
       if (fs != AFN_OK) {
@@ -1077,6 +1082,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   }
   AFN_CUDA(cudaEventRecord(ev[8], st));
   AFN_PHASE("ev8");
+  // (AFN, one rank: the Cholesky breakdown check waits until here so that the
+  // host has queued W and the FSAI work first -- a failed Cholesky only makes
+  // the queued work useless, it is reported before anything is used)
+  if (povl) TRY(chol_check());
   if (N2 > 0) {
     TRY(exchange(h, [](RankSt& s) { return s.gval; }, [&](int s) { return nnz_ranges(h, s, 8); }, st));
     for (int q = 0; q < nlocal; ++q) {

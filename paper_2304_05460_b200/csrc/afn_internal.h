@@ -138,7 +138,7 @@ afn_status gather_map(const double* v, const int64_t* map, int64_t nnz, double* 
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval,
-                          int* d_info, cudaStream_t st);
+                          int* d_info, cudaStream_t st, cudaStream_t pst = nullptr);
 
 // ---- BLAS-2 / SpMV / vectors (blas.cu) ------------------------------------
 // y = ybase + alpha * A x, A: R x C row-major (lda = C).  ybase may be null (0)

@@ -977,8 +977,14 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval, int* d_info,
-                          cudaStream_t st) {
+                          cudaStream_t st, cudaStream_t pst) {
   if (N <= 0 || row_hi <= row_lo) return AFN_OK;
+  // steps 1-2 (spatial order, unions, pass offsets; they need only the
+  // pattern) run on pst -- concurrently with W on st when pst != st; the
+  // products and the factor run on st after pst's work
+  const cudaStream_t mst = st;
+  if (pst == nullptr) pst = st;
+  st = pst;
   // group size (16; 32 trades ~27% more dots for ~37% less W traffic)
   static const int GA = getenv("AFN_FSAI_GA") && atoi(getenv("AFN_FSAI_GA")) == 32 ? 32 : 16;
   if (d > 16) {
@@ -993,7 +999,7 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
     ~Free() {
       for (void* p : *t) dfree(p, st);
     }
-  } fr{&tmp, st};
+  } fr{&tmp, mst};  // (freed in the main stream's order, after the products and the factor)
   auto get = [&](void** p, size_t bytes) {
     afn_status s = dalloc(p, bytes, st);
     if (s == AFN_OK) tmp.push_back(*p);
@@ -1111,6 +1117,14 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   int dS = 0;  // 1: D holds S_ab (DMMA kernel epilogue), 0: the Gram W_a . W_b
   double* D;
   if ((s = get((void**)&D, sizeof(double) * (totD > 0 ? totD : 1))) != AFN_OK) return s;
+  if (pst != mst) {  // join: the main stream continues after the preparation
+    cudaEvent_t ej;
+    AFN_CUDA(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+    AFN_CUDA(cudaEventRecord(ej, pst));
+    AFN_CUDA(cudaStreamWaitEvent(mst, ej, 0));
+    cudaEventDestroy(ej);
+  }
+  st = mst;
   {
     int kc = KC2;
     decltype(&group_gemm48_kernel<16, 8>) kern;
