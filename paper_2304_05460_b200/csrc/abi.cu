@@ -1419,17 +1419,27 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
         TRY(exchange(h, [](RankSt& s) { return s.p; }, [&](int s) { return vec_ranges(h, s); }, st));
         AFN_CUDA(cudaEventRecord(cm.next(), st));
       }
+      // one rank with the symmetric matvec: p.q fused into the matvec's reduce,
+      // the stopping test fused into the x/r update
+      const bool fused = h->R == 1 && h->rk[0].plan.sym;
       if (kt) kt_begin(KT_KMV, st);
       for (auto& s : h->rk)
-        TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
+        TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st,
+                       fused ? s.sc + SC_PQ : nullptr, s.dws, s.dcnt));
       if (kt) kt_end(KT_KMV, st, kmv_work(h, n, d));
       AFN_CUDA(cudaEventRecordWithFlags(ek1, st, ef));
-      for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
-      TRY(reduce_slots(h, 1u << SC_PQ, st));
-      for (auto& s : h->rk)
-        TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
-      TRY(reduce_slots(h, 1u << SC_RR, st));
-      for (auto& s : h->rk) TRY(pcg_check(s.sc, nb, tol, maxit, fixed_iters, dhist, st));
+      if (fused) {
+        RankSt& s = h->rk[0];
+        TRY(pcg_update_xr_check(s.x, s.r, s.p, s.q, s.own, s.sc, cur, s.dws, s.dcnt, nb, tol, maxit, fixed_iters,
+                                dhist, st));
+      } else {
+        for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
+        TRY(reduce_slots(h, 1u << SC_PQ, st));
+        for (auto& s : h->rk)
+          TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
+        TRY(reduce_slots(h, 1u << SC_RR, st));
+        for (auto& s : h->rk) TRY(pcg_check(s.sc, nb, tol, maxit, fixed_iters, dhist, st));
+      }
       AFN_CUDA(cudaEventRecordWithFlags(ea0, st, ef));
       if (kt) kt_begin(KT_APPLY, st);
       TRY(apply());

@@ -137,6 +137,29 @@ __device__ __forceinline__ double block_sum(double v, double* sh /*>= NT/32*/) {
   return r;  // valid in warp 0
 }
 
+// last-block-done deterministic finish: partials in block order
+__device__ __forceinline__ void finish_sum(double partial, double* ws, unsigned* cnt, double* out) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    ws[blockIdx.x] = partial;
+    __threadfence();
+    const unsigned t = atomicAdd(cnt, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += __ldcg(&ws[b]);
+    s = warp_sum(s);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *cnt = 0u;
+    }
+  }
+}
+
+
 }  // namespace afn
 
 // ---------------------------------------------------------------------------

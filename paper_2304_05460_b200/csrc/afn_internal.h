@@ -85,8 +85,10 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok = fal
 afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st);
 // rows `rows` of (K + mu I) v (v: all n entries); partial: chunks*rows.size() doubles.
 // y_phys: y[rows.phys(t)] (true) or y[t] (false) receives row t.
+// dout (symmetric plan only): also v . y into *dout (dws/dcnt: dot workspace)
 afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double* v, double mu, Seg2 rows,
-                      double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st);
+                      double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st,
+                      double* dout = nullptr, double* dws = nullptr, unsigned* dcnt = nullptr);
 
 // ---- FPS (fps.cu) ---------------------------------------------------------
 // kstop (optional, device): the run may stop early once *kstop (which another
@@ -167,6 +169,10 @@ enum { SC_RZ0 = 0, SC_RZ1 = 1, SC_PQ = 2, SC_RR = 3, SC_BB = 4, SC_TMP = 5, SC_D
 // (kernels return at once when *flag != 0); nullptr = never skip.  Per host thread.
 void set_skip(const double* flag);
 const double* get_skip();
+// x += alpha p, r -= alpha q, rr = r.r and the stopping test (one rank)
+afn_status pcg_update_xr_check(double* x, double* r, const double* p, const double* q, Seg2 g, double* sc,
+                               int rz_slot, double* ws, unsigned* cnt, double nb, double tol, int maxit, int fixed,
+                               double* hist, cudaStream_t st);
 // advances the device iteration counter sc[SC_IT] (graph-replayable)
 afn_status pcg_check(double* sc, double nb, double tol, int maxit, int fixed, double* hist, cudaStream_t st);
 // x += a p; r -= a q over g with a = sc[rz_slot]/sc[PQ] (0 if PQ <= 0); *rr = r.r over g

@@ -247,28 +247,6 @@ __global__ void scatter_vec_kernel(const double* __restrict__ x, const int64_t* 
   if (i < n) y[perm[i]] = x[i];
 }
 
-// last-block-done deterministic finish: partials in block order
-__device__ void finish_sum(double partial, double* ws, unsigned* cnt, double* out) {
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    ws[blockIdx.x] = partial;
-    __threadfence();
-    const unsigned t = atomicAdd(cnt, 1u);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last && threadIdx.x < 32) {
-    __threadfence();
-    double s = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) s += __ldcg(&ws[b]);
-    s = warp_sum(s);
-    if (threadIdx.x == 0) {
-      *out = s;
-      *cnt = 0u;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(VT) dot_kernel(const double* __restrict__ a, const double* __restrict__ b,
                                                 Seg2 g, double* out, double* ws, unsigned* cnt) {
   __shared__ double sh[VT / 32];
@@ -302,6 +280,62 @@ __global__ void __launch_bounds__(VT) update_xr_kernel(double* __restrict__ x, d
   }
   s = block_sum<VT>(s, sh);
   finish_sum(s, ws, cnt, rr);
+}
+
+// update_xr + the stopping test in one kernel (one rank): the last block,
+// which finishes rr, runs pcg_check's logic (same order of operations)
+__global__ void __launch_bounds__(VT) update_xr_check_kernel(double* __restrict__ x, double* __restrict__ r,
+                                                            const double* __restrict__ p,
+                                                            const double* __restrict__ q, Seg2 g, double* sc,
+                                                            int rz_slot, double* ws, unsigned* cnt, double nb,
+                                                            double tol, int maxit, int fixed, double* hist) {
+  __shared__ double sh[VT / 32];
+  __shared__ bool last;
+  if (sc[SC_DONE] != 0.0) {  // stopped: x and r stay; only the iteration counter moves
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc[SC_IT] += 1.0;
+    return;
+  }
+  const double pq = sc[SC_PQ];
+  const double alpha = (pq > 0.0 && isfinite(pq)) ? sc[rz_slot] / pq : 0.0;
+  double s = 0.0;
+  const int64_t n = g.size();
+  for (int64_t t = (int64_t)blockIdx.x * VT + threadIdx.x; t < n; t += (int64_t)gridDim.x * VT) {
+    const int64_t i = g.phys(t);
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    s = fma(ri, ri, s);
+  }
+  s = block_sum<VT>(s, sh);
+  if (threadIdx.x == 0) {
+    ws[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(cnt, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  double t2 = 0.0;
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t2 += __ldcg(&ws[b]);
+  t2 = warp_sum(t2);
+  if (threadIdx.x != 0) return;
+  *cnt = 0u;
+  const double rr = t2;
+  sc[SC_RR] = rr;
+  const int it = (int)sc[SC_IT] + 1;  // (pcg_check_kernel's logic)
+  sc[SC_IT] = it;
+  if (!(pq > 0.0) || !isfinite(pq) || !isfinite(rr)) {
+    sc[SC_DONE] = 2.0;
+    sc[SC_ITS] = it - 1;
+    return;
+  }
+  const double rel = sqrt(rr) / nb;
+  hist[it] = rel;
+  const bool stop = fixed > 0 ? it >= fixed : rel <= tol;
+  if (stop || it >= maxit) {
+    sc[SC_DONE] = stop ? 1.0 : 3.0;
+    sc[SC_ITS] = it;
+  }
 }
 
 __global__ void update_p_kernel(double* __restrict__ p, const double* __restrict__ z, Seg2 g,
@@ -500,6 +534,15 @@ afn_status pcg_update_xr(double* x, double* r, const double* p, const double* q,
                          cudaStream_t st) {
   update_xr_kernel<<<DOT_BLOCKS, VT, 0, st>>>(x, r, p, q, g, sc, rz_slot, rr, ws, cnt);
   AFN_LAUNCH_CHECK("update_xr_kernel");
+  return AFN_OK;
+}
+
+afn_status pcg_update_xr_check(double* x, double* r, const double* p, const double* q, Seg2 g, double* sc,
+                               int rz_slot, double* ws, unsigned* cnt, double nb, double tol, int maxit, int fixed,
+                               double* hist, cudaStream_t st) {
+  update_xr_check_kernel<<<DOT_BLOCKS, VT, 0, st>>>(x, r, p, q, g, sc, rz_slot, ws, cnt, nb, tol, maxit, fixed,
+                                                    hist);
+  AFN_LAUNCH_CHECK("update_xr_check_kernel");
   return AFN_OK;
 }
 

@@ -255,18 +255,29 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
     if (ri[t] < n) R[c * n + ri[t]] = acc[t];
 }
 
-// q_i = (1 + mu) v_i + sum_{c >= m I(i)} R[c][i] + sum_{I <= I(i)} Cb[I][i]  (fixed order)
-__global__ void kmv_sym_reduce_kernel(const double* __restrict__ R, const double* __restrict__ Cb, int64_t n,
-                                      int64_t nc, int64_t rbw, int64_t cw, const double* __restrict__ v,
-                                      double mu, double* __restrict__ y, const double* skip) {
+// q_i = (1 + mu) v_i + sum_{c >= m I(i)} R[c][i] + sum_{I <= I(i)} Cb[I][i]  (fixed order);
+// with dout: also v . q (block partials, last block sums them in block order)
+__global__ void __launch_bounds__(256) kmv_sym_reduce_kernel(const double* __restrict__ R,
+                                                            const double* __restrict__ Cb, int64_t n, int64_t nc,
+                                                            int64_t rbw, int64_t cw, const double* __restrict__ v,
+                                                            double mu, double* __restrict__ y, const double* skip,
+                                                            double* dout, double* dws, unsigned* dcnt) {
+  __shared__ double sh[8];
   if (skip != nullptr && *skip != 0.0) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int64_t Ii = i / rbw, m = rbw / cw;
-  double s = 0.0;
-  for (int64_t c = m * Ii; c < nc; ++c) s += R[c * n + i];
-  for (int64_t I = 0; I <= Ii; ++I) s += Cb[I * n + i];
-  y[i] = fma(1.0 + mu, v[i], s);
+  const int64_t m = rbw / cw;
+  double dsum = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t Ii = i / rbw;
+    double s = 0.0;
+    for (int64_t c = m * Ii; c < nc; ++c) s += R[c * n + i];
+    for (int64_t I = 0; I <= Ii; ++I) s += Cb[I * n + i];
+    const double yi = fma(1.0 + mu, v[i], s);
+    y[i] = yi;
+    dsum = fma(v[i], yi, dsum);
+  }
+  if (dout == nullptr) return;
+  dsum = block_sum<256>(dsum, sh);
+  finish_sum(dsum, dws, dcnt, dout);
 }
 
 __global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, Seg2 rows,
@@ -401,7 +412,8 @@ afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, 
 }
 
 afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double* v, double mu, Seg2 rows,
-                      double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st) {
+                      double* y, bool y_phys, double* partial, const KmvPlan& p, cudaStream_t st, double* dout,
+                      double* dws, unsigned* dcnt) {
   const int64_t nrows = rows.size();
   if (nrows <= 0) return AFN_OK;
   static unsigned long long t256 = 0;  // devices whose table is filled (a __device__ global)
@@ -434,8 +446,9 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
     }
     AFN_LAUNCH_CHECK("kmv_sym_kernel");
     const int nt = 256;
-    kmv_sym_reduce_kernel<<<(unsigned)((n + nt - 1) / nt), nt, 0, st>>>(R, Cb, n, p.sym_nc, p.sym_rbw, p.sym_cw, v,
-                                                                        mu, y, get_skip());
+    const int64_t nbk = std::min<int64_t>((n + nt - 1) / nt, dot_ws());  // (dws holds dot_ws() partials)
+    kmv_sym_reduce_kernel<<<(unsigned)nbk, nt, 0, st>>>(R, Cb, n, p.sym_nc, p.sym_rbw, p.sym_cw, v, mu, y,
+                                                        get_skip(), dout, dws, dcnt);
     AFN_LAUNCH_CHECK("kmv_sym_reduce_kernel");
     return AFN_OK;
   }
