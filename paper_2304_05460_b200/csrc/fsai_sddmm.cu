@@ -515,7 +515,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "d"(a), "d"(b));
 }
 
-template <int NS>
+template <int GA, int NS>
 __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ W, int64_t k,
     const int* __restrict__ Ucount, const int* __restrict__ Ulist, const int64_t* __restrict__ Doff,
@@ -524,7 +524,8 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
   // epilogue: D_g holds the Schur entries S_ab = K(x_a, x_b) + mu delta_ab - W_a . W_b
   // themselves (the factor kernel then only gathers them)
   __shared__ double s_tab[AFN_EXP2_TAB_N];
-  constexpr int GA = 16, UTP = 512;
+  // GA = 16: warp = 2 x 8 m8n8 tiles (64 columns); GA = 32: 4 x 4 (32 columns)
+  constexpr int MTL = GA / 8, NTL = GA == 16 ? 8 : 4, UTP = 8 * NTL * 8;
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                         // [NS][GA][DKP]
   double* sB = gs + NS * GA * DKP;         // [NS][UTP][DKP]
@@ -567,17 +568,17 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  double acc[2][8][2];
+  double acc[MTL][NTL][2];
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt)
+  for (int mt = 0; mt < MTL; ++mt)
 #pragma unroll
-    for (int n = 0; n < 8; ++n) acc[mt][n][0] = acc[mt][n][1] = 0.0;
+    for (int n = 0; n < NTL; ++n) acc[mt][n][0] = acc[mt][n][1] = 0.0;
 #pragma unroll
   for (int s0 = 0; s0 < NS - 1; ++s0) {
     if (s0 < nch) issue(s0, s0);
     else asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  const bool wact = wid * 64 < un;
+  const bool wact = wid * NTL * 8 < un;
   const int fr = lane >> 2, fk = lane & 3;  // fragment row / k index
   for (int64_t ch = 0; ch < nch; ++ch) {
     asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
@@ -587,15 +588,17 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
     else asm volatile("cp.async.commit_group;" ::: "memory");
     if (!wact) continue;
     const double* a = sA + (int)(ch % NS) * GA * DKP;
-    const double* b = sB + ((int64_t)(ch % NS) * UTP + wid * 64) * DKP;
+    const double* b = sB + ((int64_t)(ch % NS) * UTP + wid * NTL * 8) * DKP;
 #pragma unroll
     for (int k4 = 0; k4 < DKC; k4 += 4) {
-      const double a0 = a[fr * DKP + k4 + fk], a1 = a[(8 + fr) * DKP + k4 + fk];
+      double av[MTL];
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
+      for (int mt = 0; mt < MTL; ++mt) av[mt] = a[(mt * 8 + fr) * DKP + k4 + fk];
+#pragma unroll
+      for (int n = 0; n < NTL; ++n) {
         const double bv = b[(n * 8 + fr) * DKP + k4 + fk];
-        dmma884(acc[0][n][0], acc[0][n][1], a0, bv);
-        dmma884(acc[1][n][0], acc[1][n][1], a1, bv);
+#pragma unroll
+        for (int mt = 0; mt < MTL; ++mt) dmma884(acc[mt][n][0], acc[mt][n][1], av[mt], bv);
       }
     }
   }
@@ -612,15 +615,15 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
   __syncthreads();
   if (!wact) return;
 #pragma unroll
-  for (int mt = 0; mt < 2; ++mt) {
+  for (int mt = 0; mt < MTL; ++mt) {
     const int j = mt * 8 + fr;
     if (j >= cnt) continue;
     const int a = s_a[j];
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
+    for (int n = 0; n < NTL; ++n) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int u = wid * 64 + n * 8 + 2 * fk + h;
+        const int u = wid * NTL * 8 + n * 8 + 2 * fk + h;
         if (u < un) {
           const int b = s_u[u];
           const double kv = a == b ? 1.0 + mu : kern_from_d2(kf, d2_exact_rt(&sxa[j * d], &sxb[u * d], d), s_tab);
@@ -681,6 +684,10 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
   return bad;
 }
 
+#ifndef AFN_FACTOR_B
+#define AFN_FACTOR_B 8
+#endif
+constexpr int FB = AFN_FACTOR_B;  // gather batch: independent hash probes / D loads in flight per thread
 template <int MT>
 __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
                                                          int64_t row_hi, const double* __restrict__ X2, int d,
@@ -747,7 +754,7 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
     // B consecutive entries, (p, q) advanced incrementally.  Pass 1: B hash
     // probes, then B D loads, Lm <- W_a . W_b.  Pass 2 (rolled, one copy of
     // the kernel code): Lm <- K(x_a, x_b) + mu delta - Lm.
-    constexpr int B = 8;
+    constexpr int B = FB;
     const int ne = wp * (wp + 1) / 2;
     if (prof) ppro = clock64() - pt0;
     for (int e0 = tid * B; e0 < ne; e0 += FT2 * B) {
@@ -974,6 +981,13 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
 
 }  // namespace
 
+namespace {
+auto dmk(int GA, int dm) -> decltype(&group_gemm_dmma_kernel<16, 2>) {
+  if (GA == 32) return dm == 3 ? group_gemm_dmma_kernel<32, 3> : group_gemm_dmma_kernel<32, 2>;
+  return dm == 3 ? group_gemm_dmma_kernel<16, 3> : group_gemm_dmma_kernel<16, 2>;
+}
+}  // namespace
+
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval, int* d_info,
@@ -1138,17 +1152,16 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
     int bytes = (int)(sizeof(double) * NST * kc * (GA + ut));
     // FP64 tensor cores (DMMA) for GA = 16 unless AFN_FSAI_DMMA=0; AFN_FSAI_DMMA=3: 3 stages
     static const int dm = getenv("AFN_FSAI_DMMA") ? atoi(getenv("AFN_FSAI_DMMA")) : 2;
-    if (t48 && dm > 0 && GA == 16 && d <= 16) {
+    if (t48 && dm > 0 && d <= 16) {
       dS = 1;
-      bytes = (int)(sizeof(double) * (dm == 3 ? 3 : 2) * DKP * (16 + 512));
-      AFN_CUDA(cudaFuncSetAttribute(dm == 3 ? group_gemm_dmma_kernel<3> : group_gemm_dmma_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      bytes = (int)(sizeof(double) * (dm == 3 ? 3 : 2) * DKP * (GA + ut));
+      AFN_CUDA(cudaFuncSetAttribute(dmk(GA, dm), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     } else {
       AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     }
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0 && dS) {
-      auto dk = dm == 3 ? group_gemm_dmma_kernel<3> : group_gemm_dmma_kernel<2>;
+      auto dk = dmk(GA, dm);
       dk<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D, X2, d, kf, mu);
       AFN_LAUNCH_CHECK("group_gemm_dmma_kernel");
     } else if (items > 0) {
