@@ -627,6 +627,17 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
       const int CL = (int)((n + (int64_t)CNT * P2 - 1) / ((int64_t)CNT * P2));
       // AFN_FPS_PUSH=0: the cluster-barrier exchange instead of the mbarrier pushes
       static const bool push = !(getenv("AFN_FPS_PUSH") && atoi(getenv("AFN_FPS_PUSH")) == 0);
+      // smaller CTAs with more points per thread (same cluster): fewer warps to
+      // reduce per step.  AFN_FPS_NT: 1024 | 512 (default) | 256
+      // (C2, k = 2000: 1024 threads 2.52 ms, 512: 2.08, 256: 2.04)
+      static const int ntenv = getenv("AFN_FPS_NT") ? atoi(getenv("AFN_FPS_NT")) : 0;
+      const int ntc = ntenv > 0 ? ntenv : (P2 == 1 ? 256 : 512);
+      if (push && CNT == 1024 && ntc == 512 && P2 <= 2) {
+        if (P2 == 1) return launch_fps_push<DP, 2, 512>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+        return launch_fps_push<DP, 4, 512>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      }
+      if (push && CNT == 1024 && ntc == 256 && P2 == 1)
+        return launch_fps_push<DP, 4, 256>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       if (push) {
         if (P2 == 1) return launch_fps_push<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
         if (P2 == 2) return launch_fps_push<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
