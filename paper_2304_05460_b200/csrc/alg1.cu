@@ -161,8 +161,20 @@ __device__ double block_sum_1024(double v, double* sh) {
 
 // Householder tridiagonalisation of the symmetric m x m A (destroyed);
 // diag -> dgl[0..m), offdiag -> off[0..m-1).  SM: A copied into shared memory.
-template <bool SM>
-__global__ void __launch_bounds__(AT) tridiag_kernel(double* Ag, int m, double* dgl, double* off) {
+template <int TT>
+__device__ double block_sum_all(double v, double* sh) {  // every thread gets the total
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double r = lane < TT / 32 ? sh[lane] : 0.0;
+  r = warp_sum(r);
+  return r;
+}
+
+template <bool SM, int TT>
+__global__ void __launch_bounds__(TT) tridiag_kernel(double* Ag, int m, double* dgl, double* off) {
   extern __shared__ double dsm[];
   __shared__ double sh[32];
   __shared__ double s_beta, s_alpha;
@@ -171,18 +183,18 @@ __global__ void __launch_bounds__(AT) tridiag_kernel(double* Ag, int m, double* 
   double* p = v + m;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (SM) {
-    for (int64_t e = tid; e < (int64_t)m * m; e += AT) A[e] = Ag[e];
+    for (int64_t e = tid; e < (int64_t)m * m; e += TT) A[e] = Ag[e];
     __syncthreads();
   }
   for (int j = 0; j + 2 < m; ++j) {
     const int L = m - j - 1;  // length of the column below the diagonal
     double loc = 0.0;
-    for (int t = tid; t < L; t += AT) {
+    for (int t = tid; t < L; t += TT) {
       const double x = A[(int64_t)(j + 1 + t) * m + j];
       v[t] = x;
       loc += x * x;
     }
-    const double nrm2 = block_sum_1024(loc, sh);
+    const double nrm2 = block_sum_all<TT>(loc, sh);
     if (tid == 0) {
       const double x0 = v[0];
       const double nrm = sqrt(nrm2);
@@ -204,7 +216,7 @@ __global__ void __launch_bounds__(AT) tridiag_kernel(double* Ag, int m, double* 
     const double beta = s_beta;
     if (beta == 0.0) continue;
     // p = beta * A22 v   (warp per row, lanes over columns)
-    for (int i = wid; i < L; i += AT / 32) {
+    for (int i = wid; i < L; i += TT / 32) {
       const double* row = A + (int64_t)(j + 1 + i) * m + (j + 1);
       double s = 0.0;
       for (int t = lane; t < L; t += 32) s = fma(row[t], v[t], s);
@@ -213,12 +225,12 @@ __global__ void __launch_bounds__(AT) tridiag_kernel(double* Ag, int m, double* 
     }
     __syncthreads();
     double loc2 = 0.0;
-    for (int t = tid; t < L; t += AT) loc2 += p[t] * v[t];
-    const double pv = block_sum_1024(loc2, sh);
+    for (int t = tid; t < L; t += TT) loc2 += p[t] * v[t];
+    const double pv = block_sum_all<TT>(loc2, sh);
     const double K = 0.5 * beta * pv;
-    for (int t = tid; t < L; t += AT) p[t] = p[t] - K * v[t];  // w
+    for (int t = tid; t < L; t += TT) p[t] = p[t] - K * v[t];  // w
     __syncthreads();
-    for (int i = wid; i < L; i += AT / 32) {  // warp per row (no 64-bit index division)
+    for (int i = wid; i < L; i += TT / 32) {  // warp per row (no 64-bit index division)
       const double vi = v[i], pi = p[i];
       double* a = A + (int64_t)(j + 1 + i) * m + (j + 1);
       for (int t = lane; t < L; t += 32) a[t] = a[t] - vi * p[t] - pi * v[t];
@@ -349,12 +361,20 @@ constexpr int SM_MAX_M = 164;  // (m^2 + 2m) doubles of dynamic smem <= 227 KB
   } while (0)
 
 afn_status launch_tridiag(double* A, int m, double* dgl, double* off, cudaStream_t st) {
+  // AFN_TRIDIAG_T: threads of the single CTA (1024 default: 0.75 ms at m = 163; 256: 1.14 ms)
+  static const int tt = getenv("AFN_TRIDIAG_T") ? atoi(getenv("AFN_TRIDIAG_T")) : 1024;
   if (m <= SM_MAX_M) {
     const size_t bytes = sizeof(double) * ((size_t)m * m + 2 * (size_t)m);
-    AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-    tridiag_kernel<true><<<1, AT, bytes, st>>>(A, m, dgl, off);
+    if (tt == 1024) {
+      AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      tridiag_kernel<true, 1024><<<1, 1024, bytes, st>>>(A, m, dgl, off);
+    } else {
+      AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      tridiag_kernel<true, 256><<<1, 256, bytes, st>>>(A, m, dgl, off);
+    }
   } else {
-    tridiag_kernel<false><<<1, AT, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
+    if (tt == 1024) tridiag_kernel<false, 1024><<<1, 1024, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
+    else tridiag_kernel<false, 256><<<1, 256, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
   }
   AFN_LAUNCH_CHECK("tridiag_kernel");
   return AFN_OK;
