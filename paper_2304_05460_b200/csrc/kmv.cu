@@ -147,7 +147,10 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
                int64_t nc, int64_t cw, int m, double* __restrict__ R, double* __restrict__ Cb,
                const double* skip) {
   if (skip != nullptr && *skip != 0.0) return;  // PCG already stopped (device-side flag)
-  constexpr int CS = KmvTraits<D>::CS;
+  // column record stride: an odd number of 16-byte units, so 8 consecutive
+  // columns read by 8 lanes fall in 8 distinct bank groups
+  constexpr int CS0 = KmvTraits<D>::CS;
+  constexpr int CS = ((CS0 / 2) % 2 == 0) ? CS0 + 2 : CS0;
   constexpr int KMV_TC = 256;  // columns per shared-memory tile (+ 8 x 256 column partials)
   constexpr int NW = KMV_NT / 32;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
@@ -188,56 +191,49 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
       s_col[e] = val;
     }
     __syncthreads();
-    // 4 columns at a time; their column sums are reduced across the warp
-    // together (a 2-level exchange leaves each lane one column summed over 4
-    // lanes, then 3 butterfly levels): 12 shuffles per 4 columns instead of 40
+    // Blocks of 32 columns: at step s lane l pairs its rows with column
+    // (l + s) mod 32 and adds to a column accumulator that then moves one lane
+    // down (one shuffle per step), so after 32 steps lane l holds column l
+    // summed over the whole warp -- no reduction tree, no extra dependency
+    // chain per column (each column is summed in a fixed lane order).
     auto body = [&](auto masked) {
-#pragma unroll 2
-      for (int j0 = 0; j0 < tcn; j0 += 4) {
-        double cs[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int j = j0 + u;  // (tile padded with zero columns: v_j = 0, x_j = 0)
+      for (int cb = 0; cb < tcn; cb += 32) {
+        double ca = 0.0;
+#pragma unroll 4
+        for (int st = 0; st < 32; ++st) {
+          const int j = cb + ((lane + st) & 31);
           double xj[CS];
 #pragma unroll
-          for (int q = 0; q < CS; q += 2) {
+          for (int q = 0; q < CS0; q += 2) {
             const double2 w2 = *reinterpret_cast<const double2*>(&s_col[j * CS + q]);
             xj[q] = w2.x;
             xj[q + 1] = w2.y;
           }
           const double vj = xj[D];
           const int64_t gj = tb + j;
-          double csu = 0.0;
 #pragma unroll
           for (int t = 0; t < RB; ++t) {
             double dd = xi[t][0] - xj[0];
-            double s = dd * dd;
+            double s2 = dd * dd;
 #pragma unroll
             for (int q = 1; q < D; ++q) {
               dd = xi[t][q] - xj[q];
-              s = fma(dd, dd, s);
+              s2 = fma(dd, dd, s2);
             }
             double kv;
             if (KER == 1) {
-              const double tt = sqrt(s);
+              const double tt = sqrt(s2);
               kv = (1.0 + tt) * exp2_neg(tt * AFN_LOG2E, s_tab);
             } else {
-              kv = exp2_neg256(s, s_t256);
+              kv = exp2_neg256(s2, s_t256);
             }
             if (decltype(masked)::value && gj <= ri[t]) kv = 0.0;  // block-diagonal chunk: j > i only
             acc[t] = fma(kv, vj, acc[t]);
-            csu = fma(kv, vi[t], csu);
+            ca = fma(kv, vi[t], ca);
           }
-          cs[u] = csu;
+          ca = __shfl_sync(0xffffffffu, ca, (lane + 1) & 31);  // follow the column to lane - 1
         }
-        const bool b0 = lane & 1, b1 = (lane >> 1) & 1;
-        const double k0 = (b0 ? cs[2] : cs[0]) + __shfl_xor_sync(0xffffffffu, b0 ? cs[0] : cs[2], 1);
-        const double k1 = (b0 ? cs[3] : cs[1]) + __shfl_xor_sync(0xffffffffu, b0 ? cs[1] : cs[3], 1);
-        double c = (b1 ? k1 : k0) + __shfl_xor_sync(0xffffffffu, b1 ? k0 : k1, 2);
-        c += __shfl_xor_sync(0xffffffffu, c, 4);
-        c += __shfl_xor_sync(0xffffffffu, c, 8);
-        c += __shfl_xor_sync(0xffffffffu, c, 16);
-        if (lane < 4) s_cs[wid][j0 + 2 * b0 + b1] = c;  // column j0 + 2 b0 + b1
+        s_cs[wid][cb + lane] = ca;  // column cb + lane (tile padded: cb + 31 < KMV_TC)
       }
     };
     if (diag) body(std::true_type{});
@@ -351,7 +347,7 @@ KmvPlan plan_for(int64_t n, int64_t nrows, int d, int num_sms) {
 // in which case the shard gets its own plan.
 KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
   static const bool nosym = getenv("AFN_KMV_NOSYM") != nullptr;
-  if (sym_ok && !nosym && nrows == n && n >= 2048) {
+  if (sym_ok && !nosym && nrows == n && n >= 2048 && d <= 8) {
     // symmetric plan: the widest column chunk (RBW, RBW/2, ..., 128) that
     // still gives >= 1.5 waves of 2 CTAs/SM (C2: 256 -> 544 items; measured
     // 1024: 0.286, 512: 0.237, 256: 0.230, 128: 0.233 ms)
