@@ -299,3 +299,22 @@ def test_adaptive_build_uses_alg1_k():
     assert inf["khat"] == ro["khat"] and inf["k"] == min(2000, max(1, ro["khat"]))
     a, rep = h.pcg_solve(T(b))
     assert rep["converged"] and rep["relres_true"] <= 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,d,l,kernel", [(2048, 3, 1.0, "gaussian"), (5000, 3, 0.3, "gaussian"),
+                                          (4099, 5, 2.0, "gaussian"), (3333, 8, 3.0, "gaussian"),
+                                          (6000, 3, 1.0, "matern32"), (2500, 2, 0.7, "matern32")])
+def test_kmv_symmetric_plan(n, d, l, kernel):
+    """The full matvec uses the symmetric kernel (each unordered pair once, row
+    and column sums); it must agree with the oracle and, to rounding, with the
+    non-symmetric row-range kernel on the same rows (ragged n, d up to 8, both
+    kernels)."""
+    X, _ = gen_points(n, d, "cube", 11)
+    v = np.random.default_rng(n + d).standard_normal(n)
+    y = afn.kernel_matvec(T(X), l, 1e-3, T(v), kernel=kernel).cpu().numpy()
+    y_rows = afn.kernel_matvec_rows(T(X), l, 1e-3, T(v), 0, n, kernel=kernel).cpu().numpy()
+    assert rel(y, y_rows) <= 1e-14
+    rows = np.random.default_rng(3).choice(n, 200, replace=False)
+    yo = O.kmv_rows(X, l, 1e-3, v, rows, kernel=kernel)
+    assert rel(y[rows], yo) <= 1e-12
