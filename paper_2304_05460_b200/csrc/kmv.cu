@@ -369,7 +369,9 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
       if (2 * items >= 3 * slots) break;
     }
     p.ws = (p.sym_nc + p.sym_nrb) * n;
-    return p;
+    // the row/column partials grow like n^2 / 512 doubles: beyond 16 GiB
+    // (n ~ 1.5 M) use the non-symmetric plan
+    if ((double)p.ws * 8.0 <= 16.0 * 1073741824.0) return p;
   }
   KmvPlan full = plan_for(n, n, d, num_sms);
   full.ws = full.chunks * std::max<int64_t>(1, nrows);
