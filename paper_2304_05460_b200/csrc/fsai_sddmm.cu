@@ -687,9 +687,12 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
 #ifndef AFN_FACTOR_B
 #define AFN_FACTOR_B 8
 #endif
-constexpr int FB = AFN_FACTOR_B;  // gather batch: independent hash probes / D loads in flight per thread
+constexpr int FB = AFN_FACTOR_B;
+#ifndef AFN_FACTOR_MINB
+#define AFN_FACTOR_MINB 4  // <= 128 registers (5 rows per SM forces <= 96: spills, 2.63 vs 2.18 ms on C2)
+#endif  // gather batch: independent hash probes / D loads in flight per thread
 template <int MT>
-__global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
+__global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
                                                          int64_t row_hi, const double* __restrict__ X2, int d,
                                                          KernelFn kf, double mu, const int64_t* __restrict__ rp,
                                                          const int32_t* __restrict__ col,
@@ -735,10 +738,11 @@ __global__ void __launch_bounds__(FT2) fsai_factor_kernel(const int* __restrict_
   if (tid < 16) fsm[lsz - 16 + tid] = 0.0;
   for (int a = tid; a < wp; a += FT2) sJ[a] = col[beg + a];
   __syncthreads();
-  for (int e = tid; e < wp * d; e += FT2) {
-    const int a = e / d, c = e - a * d;
-    sX[e] = X2[(int64_t)sJ[a] * d + c];
-  }
+  if (!dS)  // (the points are only needed to form kernel values here)
+    for (int e = tid; e < wp * d; e += FT2) {
+      const int a = e / d, c = e - a * d;
+      sX[e] = X2[(int64_t)sJ[a] * d + c];
+    }
   // ---- 1. assemble S_JJ (lower).  Per row p (point a = J_p): the group
   // g(a) and the offset of a's row in D_g; then 8 entries per thread at a
   // time (8 independent hash probes, then 8 independent D loads).
@@ -951,7 +955,8 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
   constexpr int WP = MT * 16;
   const int wmax = std::min(WP, wcap);
   const int lsz = ((wmax * (wmax + 1) / 2 + (wmax + 1) / 2 + 16) + 1) & ~1;
-  const size_t bytes = sizeof(double) * ((size_t)lsz + (size_t)wmax * d);
+  // (dS: no point coordinates in shared memory -> 5 rows per SM at wp = 100)
+  const size_t bytes = sizeof(double) * ((size_t)lsz + (dS ? 0 : (size_t)wmax * d));
   auto kern = fsai_factor_kernel<MT>;
   AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   // debug: AFN_FACTOR_PROF=file appends per-row phase cycles (wp, assembly,
