@@ -428,6 +428,17 @@ int alg1_default_m(int64_t n) {
   return (int)std::min<int64_t>(m, n);
 }
 
+namespace {
+cudaStream_t alg1_stream() {  // per device and host thread
+  static thread_local cudaStream_t a1[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!a1[dev]) cudaStreamCreateWithFlags(&a1[dev], cudaStreamNonBlocking);
+  return a1[dev];
+}
+}  // namespace
+
 afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t rng_seed,
                     int k_threshold, Alg1Result* res, cudaStream_t st) {
   if (m < 2 || m > 1024 || m > n) {
@@ -497,12 +508,45 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   if ((s = get((void**)&ord, sizeof(int64_t) * m)) != AFN_OK) return s;
   if ((s = get((void**)&fill, sizeof(double) * m)) != AFN_OK) return s;
   if ((s = get((void**)&pass, sizeof(int) * 2)) != AFN_OK) return s;
+  double *Wk2, *dgl2, *off2, *summ2;  // the refinement's (unscaled K_m) eigen-summary
+  if ((s = get((void**)&Wk2, sizeof(double) * mm)) != AFN_OK) return s;
+  if ((s = get((void**)&dgl2, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&off2, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&summ2, sizeof(double) * 4)) != AFN_OK) return s;
   gather_scale_kernel<<<(m * d + 255) / 256, 256, 0, st>>>(X, d, ids, m, scale, Xm, Xu);
   AFN_LAUNCH_CHECK("gather_scale_kernel");
   if ((s = gen_k11(Xm, m, d, kn, 0.0, Km, st)) != AFN_OK) return s;
-  if ((s = fps_run(Xm, m, d, m, 0, ord, fill, st)) != AFN_OK) return s;
-  permute_sym_kernel<<<(unsigned)((mm + 255) / 256), 256, 0, st>>>(Km, m, ord, Kp);
+  // Concurrently on a second stream: FPS order of X_m and the permuted K_m
+  // (needed by the Schur tests), then -- speculatively, it only matters when
+  // khat < k_threshold -- the eigen-summary of the unscaled K_m for the
+  // refinement.  The main stream computes ||K_m||_2 meanwhile.
+  static const bool a1_serial = getenv("AFN_ALG1_SERIAL") != nullptr;
+  cudaStream_t s3 = a1_serial ? st : alg1_stream();
+  cudaEvent_t eA = nullptr, eP = nullptr, eR = nullptr;
+  AFN_CUDA(cudaEventCreateWithFlags(&eA, cudaEventDisableTiming));
+  AFN_CUDA(cudaEventCreateWithFlags(&eP, cudaEventDisableTiming));
+  AFN_CUDA(cudaEventCreateWithFlags(&eR, cudaEventDisableTiming));
+  struct EvF {
+    cudaEvent_t a, b, c;
+    cudaStream_t st;
+    ~EvF() {
+      cudaStreamWaitEvent(st, c, 0);  // (the temporaries are freed in st's order)
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      cudaEventDestroy(c);
+    }
+  } evf{eA, eP, eR, st};
+  AFN_CUDA(cudaEventRecord(eA, st));
+  AFN_CUDA(cudaStreamWaitEvent(s3, eA, 0));
+  if ((s = fps_run(Xm, m, d, m, 0, ord, fill, s3)) != AFN_OK) return s;
+  permute_sym_kernel<<<(unsigned)((mm + 255) / 256), 256, 0, s3>>>(Km, m, ord, Kp);
   AFN_LAUNCH_CHECK("permute_sym_kernel");
+  AFN_CUDA(cudaEventRecord(eP, s3));
+  if ((s = gen_k11(Xu, m, d, kn, 0.0, Wk2, s3)) != AFN_OK) return s;
+  TRY_A(launch_tridiag(Wk2, m, dgl2, off2, s3));
+  eig_summary_kernel<<<1, 32, 0, s3>>>(dgl2, off2, m, 0.1, summ2);
+  AFN_LAUNCH_CHECK("eig_summary_kernel");
+  AFN_CUDA(cudaEventRecord(eR, s3));
   // ||K_m||_2 = lambda_max (tridiagonal + bisection)
   AFN_CUDA(cudaMemcpyAsync(Wk, Km, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
   TRY_A(launch_tridiag(Wk, m, dgl, off, st));
@@ -517,6 +561,7 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
 
   // ---- 3. smallest r in [1, m] with ||S^(r)|| < 0.1 ||K_m|| (pass(m) = true).
   // Multisection: up to 32 probes per round run as independent CTAs.
+  AFN_CUDA(cudaStreamWaitEvent(st, eP, 0));  // K_p from the second stream
   constexpr int NPROBE = 32;
   int* rdev;
   int* pdev;
@@ -554,12 +599,9 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   int64_t khat = (2LL * r * n + m) / (2LL * m);
   int refined = 0;
   // ---- 4. refined branch: #{eig(K_m on unscaled points) > 0.1}
-  if (khat < k_threshold) {
-    if ((s = gen_k11(Xu, m, d, kn, 0.0, Wk, st)) != AFN_OK) return s;
-    TRY_A(launch_tridiag(Wk, m, dgl, off, st));
-    eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
-    AFN_LAUNCH_CHECK("eig_summary_kernel");
-    AFN_CUDA(cudaMemcpyAsync(hs, summ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
+  if (khat < k_threshold) {  // (eigen-summary computed above on the second stream)
+    AFN_CUDA(cudaStreamWaitEvent(st, eR, 0));
+    AFN_CUDA(cudaMemcpyAsync(hs, summ2, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
     khat = (int64_t)hs[1];
     refined = 1;
