@@ -638,6 +638,8 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
       }
       if (push && CNT == 1024 && ntc == 256 && P2 == 1)
         return launch_fps_push<DP, 4, 256>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      if (push && CNT == 1024 && ntc == 128 && P2 == 1)
+        return launch_fps_push<DP, 8, 128>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       if (push) {
         if (P2 == 1) return launch_fps_push<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
         if (P2 == 2) return launch_fps_push<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
