@@ -330,6 +330,16 @@ cudaStream_t side_stream() {
   return ss[dev];
 }
 
+// non-blocking stream per device and host thread for the kNN candidate lists
+cudaStream_t cand_stream() {
+  static thread_local cudaStream_t cs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cs[dev]) cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking);
+  return cs[dev];
+}
+
 // non-blocking stream per device and host thread for PCG graph capture / replay
 cudaStream_t graph_stream() {
   static thread_local cudaStream_t gs[64] = {nullptr};
@@ -781,6 +791,40 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
 
   AFN_CUDA(cudaEventRecord(ev[0], st));
   AFN_PHASE("ev0");
+  // kNN candidate lists on the original points (one rank, FPS landmarks, index
+  // ordering, brute-force regime): computed while FPS / Alg. 1 run, filtered
+  // once the landmarks are known (knn_from_candidates).  Opt-in (AFN_KNN_CAND=1):
+  // exact, and it takes the kNN off the Cholesky chain (C2: 3.95 -> 2.64 ms),
+  // but the concurrent kNN slows FPS (2.04 -> 3.7 ms) and Alg. 1 (its 200 KB
+  // single-CTA kernels wait for a free SM), a net loss on C2
+  static const bool cand_env = getenv("AFN_KNN_CAND") && atoi(getenv("AFN_KNN_CAND")) == 1;
+  const int cand_kc = std::min(191, P.w - 1 + 40);
+  const bool cand_on = cand_env && h->R == 1 && P.landmarks == AFN_LANDMARKS_FPS && P.ordering == AFN_ORDER_INDEX &&
+                       (P.method == AFN_METHOD_AFN || P.method == AFN_METHOD_ALG2) && P.w > 1 &&
+                       (d != 3 || n < 50000) && d <= 16 && n >= 1024;
+  int32_t* cand = nullptr;
+  unsigned char* lflag_keep = nullptr;  // landmark flags (original order), kept for the filter
+  cudaEvent_t e_cand = nullptr;
+  struct CandFree {
+    int32_t** c;
+    cudaEvent_t* e;
+    cudaStream_t st;
+    ~CandFree() {
+      if (*e) {
+        cudaStreamWaitEvent(st, *e, 0);
+        cudaEventDestroy(*e);
+      }
+      if (*c) dfree(*c, st);
+    }
+  } candfree{&cand, &e_cand, st};
+  if (cand_on) {
+    cudaStream_t cs = cand_stream();
+    AFN_CUDA(cudaEventCreateWithFlags(&e_cand, cudaEventDisableTiming));
+    AFN_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+    TRY(dalloc((void**)&cand, sizeof(int32_t) * (size_t)n * cand_kc, cs));
+    TRY(knn_candidates(X, n, d, cand_kc, cand, cs));
+    AFN_CUDA(cudaEventRecord(e_cand, cs));
+  }
   // ---- a2: adaptive k (Alg. 1) -- replicated: every rank computes the same k
   const Kern kn = h->kn;
   int64_t k = std::min<int64_t>(P.k_cap, n);
@@ -898,8 +942,24 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_begin(KT_KNN, ss);
     TRY(ralloc(s, &s.rp, (size_t)N2 + 1, ss));
     TRY(ralloc(s, &s.col, (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
-    if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, ss, s.lo, s.hi));
-    else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), ss));
+    bool done = false;
+    if (N2 > 0 && cand && lflag_keep && !nys) {  // filter the candidate lists
+      int64_t* inv = nullptr;
+      int* fb = nullptr;
+      TRY(dalloc((void**)&inv, sizeof(int64_t) * (size_t)n + sizeof(int) * 4, ss));
+      fb = reinterpret_cast<int*>(inv + n);
+      AFN_CUDA(cudaStreamWaitEvent(ss, e_cand, 0));
+      TRY(knn_from_candidates(cand, cand_kc, lflag_keep, s.perm, n, k, P.w, s.rp, s.col, inv, fb, ss));
+      int hfb = 0;
+      AFN_CUDA(cudaMemcpyAsync(&hfb, fb, sizeof(int), cudaMemcpyDeviceToHost, ss));
+      AFN_CUDA(cudaStreamSynchronize(ss));
+      dfree(inv, ss);
+      done = hfb == 0;  // else: a list ran short -> the exact kNN below
+    }
+    if (!done) {
+      if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, ss, s.lo, s.hi));
+      else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), ss));
+    }
     kt_end(KT_KNN, ss, 0.0);
     return AFN_OK;
   };
@@ -954,7 +1014,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       perm_kernel<<<1, 1024, 0, st>>>(flag, idx[q], n, k, s.perm);
       AFN_LAUNCH_CHECK("perm_kernel");
     }
-    rfree(s, flag, st);
+    if (cand_on) lflag_keep = flag;  // (the landmark flags feed the kNN filter)
+    else rfree(s, flag, st);
     rfree(s, flag32, st);
     TRY(ralloc(s, &s.Xp, (size_t)n * d, st));
     TRY(gather_rows(X, n, d, s.perm, s.Xp, st));

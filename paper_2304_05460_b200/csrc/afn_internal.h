@@ -99,6 +99,15 @@ afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, i
 // ---- kNN pattern (knn.cu) -------------------------------------------------
 int64_t knn_nnz(int64_t N, int w);
 // row_ptr for all N rows (closed form); col for rows [row_lo, row_hi) (default: all)
+// Candidate lists: for every point i of X (original order), its min(KC, i)
+// nearest earlier points (j < i) in (d2, j) order, cand[i KC + t].
+afn_status knn_candidates(const double* X, int64_t n, int d, int KC, int32_t* cand, cudaStream_t st);
+// The kNN pattern of the non-landmark points (perm = [landmarks; the rest in
+// ascending original order]) from the candidate lists: drop landmarks (lflag),
+// map to permuted positions; *fallback = 1 if a list ran short (then call knn_run).
+afn_status knn_from_candidates(const int32_t* cand, int KC, const unsigned char* lflag, const int64_t* perm,
+                               int64_t n, int64_t k, int w, int64_t* row_ptr, int32_t* col, int64_t* inv_ws,
+                               int* fallback, cudaStream_t st);
 afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, int32_t* col,
                    cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = -1);
 

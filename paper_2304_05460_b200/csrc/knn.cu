@@ -66,7 +66,9 @@ __device__ void warp_bitonic_int(int* v) {
   }
 }
 
-template <int DP>
+// CAND: candidate lists instead of the pattern -- row i keeps its min(w - 1, i)
+// nearest earlier points in (d2, j) order, written to col[(i - row_lo) (w - 1) + t]
+template <int DP, bool CAND = false>
 __global__ void __launch_bounds__(KNN_NW * 32)
 knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, int w,
            int32_t* __restrict__ col) {
@@ -135,6 +137,11 @@ knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, 
     }
   }
   if (!active) return;
+  if (CAND) {  // key order, no self entry
+    if (W1 > 0) compact();
+    for (int t = lane; t < W1; t += 32) col[(i - row_lo) * (int64_t)(w - 1) + t] = idx[t];
+    return;
+  }
   if (W1 > 0) {
     compact();
     // ascending positions of the kept neighbours
@@ -415,7 +422,102 @@ void launch_knn(const double* P, int64_t lo, int64_t hi, int d, int w, int32_t* 
   knn_kernel<DP><<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(P, lo, hi, d, w, col);
 }
 
+// Landmark filter (AFN, FPS landmarks, non-landmarks in ascending original
+// order): row i of the pattern is the non-landmark point o = perm[k + i]; the
+// candidate list of o (its KC nearest EARLIER points of the original set, in
+// (d2, j) order) minus the landmarks, first min(w - 1, i), mapped to positions
+// i' = inv[j] - k and sorted, plus i itself -- exactly the pattern knn_kernel
+// computes on the permuted non-landmark points (same distances; the original
+// order restricted to non-landmarks is the permuted order, so ties break the
+// same way).  A list that runs out before w - 1 survivors (too many landmarks
+// among the KC candidates) sets *fallback.
+__global__ void __launch_bounds__(KNN_NW * 32)
+knn_filter_kernel(const int32_t* __restrict__ cand, int KC, const unsigned char* __restrict__ lflag,
+                  const int64_t* __restrict__ inv, const int64_t* __restrict__ perm, int64_t k, int64_t N2,
+                  int w, int32_t* __restrict__ col, int* fallback) {
+  __shared__ int s_v[KNN_NW][KNN_CAP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * KNN_NW + wid;
+  if (i >= N2) return;
+  const int64_t o = perm[k + i];
+  const int W1 = (int)min((int64_t)w - 1, i);
+  const int kc = (int)min((int64_t)KC, o);
+  int* v = s_v[wid];
+  int got = 0;
+  for (int b = 0; b < kc && got < W1; b += 32) {
+    const int t = b + lane;
+    int j = -1;
+    bool keep = false;
+    if (t < kc) {
+      j = cand[o * (int64_t)KC + t];
+      keep = !lflag[j];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    const int pos = got + __popc(m & ((1u << lane) - 1u));
+    if (keep && pos < W1) v[pos] = (int)(inv[j] - k);
+    got += __popc(m);
+  }
+  if (got < W1) {
+    if (lane == 0) atomicExch(fallback, 1);
+    return;
+  }
+  for (int t = W1 + lane; t < KNN_CAP; t += 32) v[t] = 0x7fffffff;
+  __syncwarp();
+  warp_bitonic_int(v);
+  const int64_t wl = w;
+  const int64_t start = (i < wl) ? i * (i + 1) / 2 : wl * (wl + 1) / 2 + (i - wl) * wl;
+  for (int t = lane; t < W1; t += 32) col[start + t] = v[t];
+  if (lane == 0) col[start + W1] = (int32_t)i;
+}
+
+__global__ void inv_perm_kernel(const int64_t* __restrict__ perm, int64_t n, int64_t* __restrict__ inv) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) inv[perm[p]] = p;
+}
+
+template <int DP>
+void launch_knn_cand(const double* X, int64_t n, int d, int KC, int32_t* cand, cudaStream_t st) {
+  const int64_t blocks = (n + KNN_NW - 1) / KNN_NW;
+  knn_kernel<DP, true><<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(X, 0, n, d, KC + 1, cand);
+}
+
 }  // namespace
+
+afn_status knn_candidates(const double* X, int64_t n, int d, int KC, int32_t* cand, cudaStream_t st) {
+  if (KC < 1 || KC > 191) {
+    set_error("knn_candidates: KC=%d unsupported (1..191)", KC);
+    return AFN_ERR_ARG;
+  }
+  if (n <= 0) return AFN_OK;
+  if (d <= 1) launch_knn_cand<1>(X, n, d, KC, cand, st);
+  else if (d <= 2) launch_knn_cand<2>(X, n, d, KC, cand, st);
+  else if (d <= 3) launch_knn_cand<3>(X, n, d, KC, cand, st);
+  else if (d <= 4) launch_knn_cand<4>(X, n, d, KC, cand, st);
+  else if (d <= 8) launch_knn_cand<8>(X, n, d, KC, cand, st);
+  else if (d <= 16) launch_knn_cand<16>(X, n, d, KC, cand, st);
+  else {
+    set_error("knn_candidates: d=%d unsupported (1..16)", d);
+    return AFN_ERR_ARG;
+  }
+  AFN_LAUNCH_CHECK("knn_kernel<cand>");
+  return AFN_OK;
+}
+
+afn_status knn_from_candidates(const int32_t* cand, int KC, const unsigned char* lflag, const int64_t* perm,
+                               int64_t n, int64_t k, int w, int64_t* row_ptr, int32_t* col, int64_t* inv_ws,
+                               int* fallback, cudaStream_t st) {
+  const int64_t N2 = n - k;
+  if (N2 <= 0) return AFN_OK;
+  knn_rowptr_kernel<<<(unsigned)((N2 + 1 + 255) / 256), 256, 0, st>>>(N2, w, row_ptr);
+  AFN_LAUNCH_CHECK("knn_rowptr_kernel");
+  inv_perm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(perm, n, inv_ws);
+  AFN_LAUNCH_CHECK("inv_perm_kernel");
+  AFN_CUDA(cudaMemsetAsync(fallback, 0, sizeof(int), st));
+  knn_filter_kernel<<<(unsigned)((N2 + KNN_NW - 1) / KNN_NW), KNN_NW * 32, 0, st>>>(cand, KC, lflag, inv_ws, perm, k,
+                                                                                   N2, w, col, fallback);
+  AFN_LAUNCH_CHECK("knn_filter_kernel");
+  return AFN_OK;
+}
 
 int64_t knn_nnz(int64_t N, int w) {
   const int64_t wl = w;
