@@ -29,7 +29,29 @@ constexpr int KMV_NT = 256;
 // 2^(r/256), r = 0..255 (one table lookup and one multiply per exp2 in the
 // matvec instead of two of each with the 2 x 16-entry tables); filled once.
 __device__ double g_exp2_256[256];
-__global__ void exp2_256_init_kernel() { g_exp2_256[threadIdx.x] = exp2((double)threadIdx.x / 256.0); }
+__device__ double g_exp2_2048[2048];
+__global__ void exp2_256_init_kernel() {
+  g_exp2_256[threadIdx.x] = exp2((double)threadIdx.x / 256.0);
+  for (int r = threadIdx.x; r < 2048; r += blockDim.x) g_exp2_2048[r] = exp2((double)r / 2048.0);
+}
+// 2^(-s) with a 2048-entry table and a degree-3 polynomial: |f| <= 1/4096, the
+// first omitted Taylor term is ln(2)^4 f^4 / 24 < 3.4e-17 (7 FP64 instructions
+// instead of 8)
+__device__ __forceinline__ double exp2_neg2048(double s, const double* tab) {
+  const double magic = 0x1.8p52;
+  double t = fma(s, -2048.0, magic);  // rint(-2048 s) in the low word
+  double nf = t - magic;
+  double f = fma(nf, -0x1.0p-11, -s);  // exact, |f| <= 1/4096
+  const int n = __double2loint(t);
+  double p = AFN_E2C3;
+  p = fma(p, f, AFN_E2C2);
+  p = fma(p, f, AFN_E2C1);
+  p = fma(p, f, AFN_E2C0);
+  p = p * tab[n & 2047];
+  int hi = __double2hiint(p) + ((n >> 11) << 20);
+  hi = (__double2hiint(s) >= 0x408FE000) ? 0 : hi;  // s >= 1020 -> ~0 (as exp2_neg)
+  return __hiloint2double(hi, __double2loint(p));
+}
 __device__ __forceinline__ double exp2_neg256(double s, const double* tab) {
   const double magic = 0x1.8p52;
   double t = fma(s, -256.0, magic);   // rint(-256 s) in the low word
@@ -154,11 +176,12 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
   constexpr int KMV_TC = 256;  // columns per shared-memory tile (+ 8 x 256 column partials)
   constexpr int NW = KMV_NT / 32;
   __shared__ double s_tab[AFN_EXP2_TAB_N];
-  __shared__ double s_t256[256];
+  constexpr int TABN = D <= 4 ? 2048 : 256;  // (static shared memory <= 48 KB)
+  __shared__ double s_tx[TABN];
   __shared__ __align__(16) double s_col[KMV_TC * CS];
   __shared__ double s_cs[NW][KMV_TC];
   load_exp2_tab(s_tab);
-  for (int t = threadIdx.x; t < 256; t += KMV_NT) s_t256[t] = g_exp2_256[t];
+  for (int t = threadIdx.x; t < TABN; t += KMV_NT) s_tx[t] = TABN == 2048 ? g_exp2_2048[t] : g_exp2_256[t];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // item -> (I, c): block I owns the items c = m I .. nc - 1
   int64_t it = blockIdx.x, I = 0;
@@ -225,7 +248,7 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
               const double tt = sqrt(s2);
               kv = (1.0 + tt) * exp2_neg(tt * AFN_LOG2E, s_tab);
             } else {
-              kv = exp2_neg256(s2, s_t256);
+              kv = TABN == 2048 ? exp2_neg2048(s2, s_tx) : exp2_neg256(s2, s_tx);
             }
             if (decltype(masked)::value && gj <= ri[t]) kv = 0.0;  // block-diagonal chunk: j > i only
             acc[t] = fma(kv, vj, acc[t]);
