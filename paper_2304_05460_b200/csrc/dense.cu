@@ -94,7 +94,7 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
 // Each of the 2080 lower entries is owned by one thread (in a register);
 // step j subtracts a_ij a_tj / p_j (unscaled columns, one barrier per step);
 // the scaling L_ij = a_ij / sqrt(p_j) is applied at the end.
-constexpr int DG_T = 1024;  // (256: 34 us, 512: 26 us, 1024: 25 us per 64-block on C2)
+constexpr int DG_T = 1024;  // (256: 34 us, 512: 26 us, 1024: 25 us per 64-block on C2; 256 is no better next to the concurrent kNN)
 __global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, int64_t kb, int* info) {
   __shared__ double s[NB * TP];
   const int nb = (int)min((int64_t)NB, k - kb);
