@@ -54,6 +54,12 @@ static void pool_setup_once() {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // no hidden cross-stream waits: a block freed on one stream (e.g. the
+    // side stream's kNN temporaries) must not be handed to another stream's
+    // allocation with an inserted dependency on the first stream's work
+    int zero = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &zero);
   }
   done[dev] = true;
 }
