@@ -276,26 +276,37 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
 
 // q_i = (1 + mu) v_i + sum_{c >= m I(i)} R[c][i] + sum_{I <= I(i)} Cb[I][i]  (fixed order);
 // with dout: also v . q (block partials, last block sums them in block order)
-__global__ void __launch_bounds__(256) kmv_sym_reduce_kernel(const double* __restrict__ R,
+constexpr int SRT = 256;  // threads per block of the symmetric reduce
+constexpr int SRL = 8;    // threads per row (partial sums over strided chunks, then a fixed butterfly)
+__global__ void __launch_bounds__(SRT) kmv_sym_reduce_kernel(const double* __restrict__ R,
                                                             const double* __restrict__ Cb, int64_t n, int64_t nc,
                                                             int64_t rbw, int64_t cw, const double* __restrict__ v,
                                                             double mu, double* __restrict__ y, const double* skip,
                                                             double* dout, double* dws, unsigned* dcnt) {
-  __shared__ double sh[8];
+  __shared__ double sh[SRT / 32];
   if (skip != nullptr && *skip != 0.0) return;
   const int64_t m = rbw / cw;
+  const int sub = threadIdx.x % SRL;
   double dsum = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t Ii = i / rbw;
+  const int64_t rows_per_pass = (int64_t)gridDim.x * (SRT / SRL);
+  for (int64_t i0 = (int64_t)blockIdx.x * (SRT / SRL); i0 < n; i0 += rows_per_pass) {
+    const int64_t i = i0 + threadIdx.x / SRL;
     double s = 0.0;
-    for (int64_t c = m * Ii; c < nc; ++c) s += R[c * n + i];
-    for (int64_t I = 0; I <= Ii; ++I) s += Cb[I * n + i];
-    const double yi = fma(1.0 + mu, v[i], s);
-    y[i] = yi;
-    dsum = fma(v[i], yi, dsum);
+    if (i < n) {
+      const int64_t Ii = i / rbw;
+      for (int64_t c = m * Ii + sub; c < nc; c += SRL) s += R[c * n + i];
+      for (int64_t I = sub; I <= Ii; I += SRL) s += Cb[I * n + i];
+    }
+#pragma unroll
+    for (int o = 1; o < SRL; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (sub == 0 && i < n) {
+      const double yi = fma(1.0 + mu, v[i], s);
+      y[i] = yi;
+      dsum = fma(v[i], yi, dsum);
+    }
   }
   if (dout == nullptr) return;
-  dsum = block_sum<256>(dsum, sh);
+  dsum = block_sum<SRT>(dsum, sh);
   finish_sum(dsum, dws, dcnt, dout);
 }
 
@@ -466,8 +477,9 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
       default: set_error("kernel_matvec: symmetric plan for d=%d unsupported (1..8)", d); return AFN_ERR_ARG;
     }
     AFN_LAUNCH_CHECK("kmv_sym_kernel");
-    const int nt = 256;
-    const int64_t nbk = std::min<int64_t>((n + nt - 1) / nt, dot_ws());  // (dws holds dot_ws() partials)
+    const int nt = SRT;
+    const int64_t rows_per_block = SRT / SRL;
+    const int64_t nbk = std::min<int64_t>((n + rows_per_block - 1) / rows_per_block, dot_ws());  // (dws: dot_ws() partials)
     kmv_sym_reduce_kernel<<<(unsigned)nbk, nt, 0, st>>>(R, Cb, n, p.sym_nc, p.sym_rbw, p.sym_cw, v, mu, y,
                                                         get_skip(), dout, dws, dcnt);
     AFN_LAUNCH_CHECK("kmv_sym_reduce_kernel");
