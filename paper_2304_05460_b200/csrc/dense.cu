@@ -147,6 +147,96 @@ __global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, 
   }
 }
 
+// Blocked diagonal-block Cholesky (256 threads): the 64 x 64 block in shared
+// memory is factored in four 16-column steps -- warp 0 factors the 16 x 16
+// diagonal sub-block (one row per lane in registers, columns broadcast through
+// shared memory, one rsqrt per column), every thread then solves one panel row
+// (16 columns, multiplies by the stored reciprocal pivots) and the trailing
+// lower part is updated (16-term dots).  A non-positive pivot is reported in
+// *info (global row) and replaced by 1 so the block stays finite.
+constexpr int DB_T = 256;
+__global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t k, int64_t kb, int* info) {
+  __shared__ double s[NB * TP];
+  __shared__ double s_inv[NB];
+  __shared__ __align__(16) double s_col[32];
+  const int nb = (int)min((int64_t)NB, k - kb);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < NB * NB; e += DB_T) {
+    const int i = e / NB, t = e - i * NB;
+    double v = 0.0;
+    if (t <= i) v = (i < nb && t < nb) ? A[(kb + i) * k + kb + t] : (i == t ? 1.0 : 0.0);
+    s[i * TP + t] = v;
+  }
+  __syncthreads();
+  for (int b0 = 0; b0 < NB; b0 += 16) {
+    if (wid == 0) {  // 16 x 16 diagonal sub-block: lane lr owns row b0 + lr
+      const int lr = lane & 15;
+      double dr[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) dr[c] = c <= lr ? s[(b0 + lr) * TP + b0 + c] : 0.0;
+      double myinv = 1.0;
+      bool bad = false;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        double* cb = s_col + (c & 1) * 16;
+        if (lane < 16) cb[lane] = dr[c];
+        __syncwarp();
+        double piv = cb[c];
+        if (!(piv > 0.0)) { bad = true; piv = 1.0; }
+        const double inv = rsqrt(piv);
+        const double lrc = dr[c] * inv;
+        const double f = lrc * inv;
+        if (lr == c) myinv = inv;
+#pragma unroll
+        for (int c2 = c + 1; c2 < 16; ++c2)
+          if (lr >= c2) dr[c2] = fma(-f, cb[c2], dr[c2]);
+        dr[c] = (lr == c) ? piv * inv : (lr > c ? lrc : dr[c]);
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c <= lr) s[(b0 + lr) * TP + b0 + c] = dr[c];
+        s_inv[b0 + lr] = myinv;
+        if (bad && b0 + lr < nb) atomicCAS(info, 0, (int)(kb + b0 + lr + 1));
+      }
+    }
+    __syncthreads();
+    const int r0 = b0 + 16;
+    if (r0 >= NB) break;
+    // panel: rows r >= r0, columns b0..b0+15: x L_d^T = a (one row per thread)
+    for (int r = r0 + tid; r < NB; r += DB_T) {
+      double x[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) x[c] = s[r * TP + b0 + c];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        double a = x[c];
+#pragma unroll
+        for (int c2 = 0; c2 < c; ++c2) a = fma(-x[c2], s[(b0 + c) * TP + b0 + c2], a);
+        x[c] = a * s_inv[b0 + c];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) s[r * TP + b0 + c] = x[c];
+    }
+    __syncthreads();
+    // trailing lower part: s[r][c] -= sum_t L[r][b0+t] L[c][b0+t], r0 <= c <= r < NB
+    const int m = NB - r0;
+    for (int e = tid; e < m * m; e += DB_T) {
+      const int r = r0 + e / m, c = r0 + e % m;
+      if (c > r) continue;
+      double a = 0.0;
+#pragma unroll
+      for (int t = 0; t < 16; ++t) a = fma(s[r * TP + b0 + t], s[c * TP + b0 + t], a);
+      s[r * TP + c] -= a;
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < NB * NB; e += DB_T) {
+    const int i = e / NB, t = e - i * NB;
+    if (i < nb && t < nb) A[(kb + i) * k + kb + t] = t <= i ? s[i * TP + t] : 0.0;
+  }
+}
+
 // Panel below the diagonal block: A[i, kb:kb+nb] <- A[i, kb:kb+nb] L_kk^{-T}.
 __global__ void __launch_bounds__(DT) potrf_panel_kernel(double* A, int64_t k, int64_t kb) {
   extern __shared__ double dsm[];
@@ -889,7 +979,9 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
   TRY_SMEM();
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
   for (int64_t kb = 0; kb < k; kb += NB) {
-    potrf_diag_kernel<<<1, DG_T, 0, st>>>(A, k, kb, d_info);
+    static const bool diag_old = getenv("AFN_POTRF_DIAG_OLD") != nullptr;
+    if (diag_old) potrf_diag_kernel<<<1, DG_T, 0, st>>>(A, k, kb, d_info);
+    else potrf_diag_blk_kernel<<<1, DB_T, 0, st>>>(A, k, kb, d_info);
     AFN_LAUNCH_CHECK("potrf_diag_kernel");
     const int64_t rem = k - kb - NB;
     if (rem <= 0) break;
