@@ -222,7 +222,7 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
     auto body = [&](auto masked) {
       for (int cb = 0; cb < tcn; cb += 32) {
         double ca = 0.0;
-#pragma unroll 4
+#pragma unroll 2
         for (int st = 0; st < 32; ++st) {
           const int j = cb + ((lane + st) & 31);
           double xj[CS];
