@@ -368,6 +368,9 @@ afn_status launch_tridiag(double* A, int m, double* dgl, double* off, cudaStream
     if (tt == 1024) {
       AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
       tridiag_kernel<true, 1024><<<1, 1024, bytes, st>>>(A, m, dgl, off);
+    } else if (tt == 512) {
+      AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      tridiag_kernel<true, 512><<<1, 512, bytes, st>>>(A, m, dgl, off);
     } else {
       AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
       tridiag_kernel<true, 256><<<1, 256, bytes, st>>>(A, m, dgl, off);
