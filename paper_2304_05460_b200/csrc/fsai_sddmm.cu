@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(256, 2) group_gemm48_kernel(const int* __restr
 // LDS.64 = 2 wavefronts, conflict-free).  Each dot is summed in k order in
 // groups of 4 (the DMMA k-step).
 constexpr int DKC = 8, DKP = 12;
+#ifndef G16_NTL
+#define G16_NTL 8  // n-tiles per warp at GA = 16 (4: 256-column passes, measured 4.31 vs 3.89 ms)
+#endif
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -525,7 +528,7 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
   // themselves (the factor kernel then only gathers them)
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   // GA = 16: warp = 2 x 8 m8n8 tiles (64 columns); GA = 32: 4 x 4 (32 columns)
-  constexpr int MTL = GA / 8, NTL = GA == 16 ? 8 : 4, UTP = 8 * NTL * 8;
+  constexpr int MTL = GA / 8, NTL = GA == 16 ? G16_NTL : 4, UTP = 8 * NTL * 8;
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                         // [NS][GA][DKP]
   double* sB = gs + NS * GA * DKP;         // [NS][UTP][DKP]
@@ -1122,7 +1125,8 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   // and measured slower (C2 10.5 vs 7.0 ms)
   static const bool t48 = !(getenv("AFN_FSAI_T48") && atoi(getenv("AFN_FSAI_T48")) == 0);
   static const int BC = getenv("AFN_FSAI_BC") ? std::max(2, std::min(4, atoi(getenv("AFN_FSAI_BC")))) : 2;
-  const int ut = t48 ? (GA == 32 ? 256 : 512) : 256 * (BC >= 4 ? 4 : 2);
+  static const int dm0 = getenv("AFN_FSAI_DMMA") ? atoi(getenv("AFN_FSAI_DMMA")) : 2;
+  const int ut = t48 ? (GA == 32 ? 256 : (dm0 > 0 ? 64 * G16_NTL : 512)) : 256 * (BC >= 4 ? 4 : 2);
   pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, ut, pc);
   AFN_LAUNCH_CHECK("pass_count_kernel");
   scan_i64_kernel<<<1, 1024, 0, st>>>(pc, G, 1, Poff);
