@@ -382,8 +382,8 @@ KmvPlan plan_for(int64_t n, int64_t nrows, int d, int num_sms) {
 KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
   static const bool nosym = getenv("AFN_KMV_NOSYM") != nullptr;
   // (measured, matvec ms per launch, symmetric vs not: C2 0.20 vs 0.30, C3
-  // 9.8 vs 17.4, C5 (n = 2^20) 1107 vs 629 -> up to n = 2^18)
-  if (sym_ok && !nosym && nrows == n && n >= 2048 && n <= (1 << 18) && d <= 8) {
+  // 9.8 vs 17.4, C5 (n = 2^20) 629 vs 1106)
+  if (sym_ok && !nosym && nrows == n && n >= 2048 && d <= 8) {
     // symmetric plan: the widest column chunk (RBW, RBW/2, ..., 128) that
     // still gives >= 1.5 waves of 2 CTAs/SM (C2: 256 -> 544 items; measured
     // 1024: 0.286, 512: 0.237, 256: 0.230, 128: 0.233 ms)
@@ -405,9 +405,9 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok) {
       if (2 * items >= 3 * slots) break;
     }
     p.ws = (p.sym_nc + p.sym_nrb) * n;
-    // the row/column partials grow like n^2 / 512 doubles: beyond 16 GiB
-    // (n ~ 1.5 M) use the non-symmetric plan
-    if ((double)p.ws * 8.0 <= 16.0 * 1073741824.0) return p;
+    // the row/column partials grow like n^2 / 512 doubles (C5, n = 2^20:
+    // 16 GiB of 180): beyond 24 GiB use the non-symmetric plan
+    if ((double)p.ws * 8.0 <= 24.0 * 1073741824.0) return p;
   }
   KmvPlan full = plan_for(n, n, d, num_sms);
   full.ws = full.chunks * std::max<int64_t>(1, nrows);
