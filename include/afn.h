@@ -135,13 +135,18 @@ typedef struct {
 /* ------------------------------------------------------------------------ */
 /* Kernel matvec  y = (K + mu I) v   */
 /* X: n x d device, v,y: n device (y must not alias v or X).  Stream-ordered. */
-/* Rows are evaluated with a fixed column-chunk order, so the output is       */
-/* bit-identical run to run.  n >= 1, 1 <= d <= 16, l > 0, mu >= 0.           */
+/* K is symmetric: for 2048 <= n and d <= 8 each unordered pair is evaluated */
+/* once (row and column sums, fixed summation order); otherwise rows use a    */
+/* fixed column-chunk order.  Either way the output is bit-identical run to   */
+/* run (it may differ from kernel_matvec_rows at rounding level).             */
+/* n >= 1, 1 <= d <= 16, l > 0, mu >= 0.                                      */
 afn_status kernel_matvec(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
                          const double* v, double* y, void* stream);
 
 /* Rows [row0, row0+nrows) of y = (K + mu I) v against all n columns (the row
- * shard a rank owns in the multi-GPU layout).  y has nrows entries. */
+ * shard a rank owns in the multi-GPU layout).  y has nrows entries.  Always
+ * the row-wise (non-symmetric) kernel: a row's value does not depend on which
+ * shard it is evaluated in (shards of >= two waves are bit-identical). */
 afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t kernel, double l, double mu,
                               const double* v, int64_t row0, int64_t nrows, double* y,
                               void* stream);
