@@ -12,6 +12,7 @@ SURVEY.md 8(c) (``R<n>`` below refers to that list).
 
 Pinned by ``tests/test_oracle_*.py`` (run with ``-m "not gpu"``).  Parity
 status of each function is recorded in DESIGN.md; ``alg1``'s refined branch is
-"parity unpinned" against the paper (its printed values need m > 500, R13).
+pinned by closed forms (separated clusters, two points) but not by the paper's
+printed values (they need m > 500, R13).
 """
 from .afn_oracle import *  # noqa: F401,F403

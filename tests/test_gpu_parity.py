@@ -3,6 +3,7 @@ same seeded inputs.  Tolerances are those of BASELINE.json's north star:
 bit-exact FPS / kNN / permutation, kernel matvec rel <= 1e-12, FSAI entries
 rel <= 1e-10 per row, PCG iterations within +-2, solution rel <= 1e-6 at equal
 iteration counts, true residual <= tol.  Run on a B200: pytest -m gpu."""
+import math
 import numpy as np
 import pytest
 
@@ -289,6 +290,30 @@ def test_alg1_special_cases(n, d, l, m):
     res = afn.afn_estimate_rank(T(X), l, m=m)
     ro = O.alg1(X, l, m=m)
     assert (res["khat"], res["r"], res["refined"]) == (ro["khat"], ro["r"], ro["refined"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("c,size", [(3, 40), (6, 20), (11, 7)])
+def test_alg1_refined_branch_clusters(c, size):
+    """c tight clusters far apart, m = n: refined count = r = c (closed form,
+    see tests/test_oracle_pins.py) on the device, and the oracle agrees."""
+    rng = np.random.default_rng(3)
+    centres = 100.0 * np.arange(c)[:, None] * np.array([[1.0, 0.3, -0.2]])
+    X = np.repeat(centres, size, axis=0) + 1e-7 * rng.standard_normal((c * size, 3))
+    res = afn.afn_estimate_rank(T(X), 1.0, m=c * size)
+    assert (res["khat"], res["r"], res["refined"]) == (c, c, True)
+    ro = O.alg1(X, 1.0, m=c * size)
+    assert (ro["khat"], ro["r"], ro["refined"]) == (c, c, True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("l,f,want", [(0.5, 0.95, 1), (0.5, 1.05, 2), (1.0, 0.5, 1), (3.0, 3.0, 2)])
+def test_alg1_refined_branch_two_points(l, f, want):
+    """Two points: eigenvalues 1 +- exp(-r^2/l^2); count > 0.1 is 2 iff r^2/l^2 > ln(10/9)."""
+    r = l * math.sqrt(f * math.log(10.0 / 9.0))
+    X = np.array([[0.0, 0.0, 0.0], [r, 0.0, 0.0]])
+    res = afn.afn_estimate_rank(T(X), l, m=2)
+    assert res["refined"] and res["khat"] == want
 
 
 def test_adaptive_build_uses_alg1_k():

@@ -217,6 +217,34 @@ def test_alg1_special_cases():
     assert bb["r"] == 1 and not bb["refined"] and bb["khat"] == 2000
 
 
+def test_alg1_refined_branch_counts_separated_clusters():
+    """Refined branch (R13) on c tight clusters far apart: K_m is
+    block-diagonal with all-ones blocks up to ~1e-12, whose eigenvalues are the
+    cluster sizes and zeros, so the count of eigenvalues > 0.1 is c.  FPS
+     takes one point per cluster first, after which the Schur
+    complement vanishes (r = c), and before which the untouched cluster leaves
+    an error of s/s = 1 > 0.1."""
+    rng = np.random.default_rng(3)
+    for c, size in ((3, 40), (6, 20), (11, 7)):
+        centres = 100.0 * np.arange(c)[:, None] * np.array([[1.0, 0.3, -0.2]])
+        X = np.repeat(centres, size, axis=0) + 1e-7 * rng.standard_normal((c * size, 3))
+        res = O.alg1(X, 1.0, m=c * size)  # m = n: the subsample is every point, unscaled
+        assert res["refined"] and res["r"] == c and res["khat"] == c, (c, res["r"], res["khat"])
+
+
+def test_alg1_refined_branch_two_point_threshold():
+    """Two points at distance r: K_m = [[1, e], [e, 1]], e = exp(-r^2/l^2),
+    eigenvalues 1 +- e; the refined count #{lambda > 0.1} (R13) is 2 exactly when
+    r^2/l^2 > ln(10/9)."""
+    t = math.log(10.0 / 9.0)
+    for l in (0.5, 1.0, 3.0):
+        for f, want in ((0.95, 1), (1.05, 2), (0.5, 1), (3.0, 2)):
+            r = l * math.sqrt(f * t)
+            X = np.array([[0.0, 0.0, 0.0], [r, 0.0, 0.0]])
+            res = O.alg1(X, l, m=2)
+            assert res["refined"] and res["khat"] == want, (l, f, res["khat"])
+
+
 def test_alg1_schur_errors_match_explicit_nystrom():
     """errs[r-1] = ||K22 - K21 K11^{-1} K12||_2 / ||K_m||_2 for the FPS-ordered
     subsample; error curve non-increasing (nested landmarks)."""
