@@ -173,6 +173,10 @@ __device__ double block_sum_all(double v, double* sh) {  // every thread gets th
   return r;
 }
 
+constexpr int SM_MAX_M = 164;  // (m^2 + 2m) doubles of dynamic smem <= 227 KB
+#ifndef AFN_TRIDIAG_COLS
+#define AFN_TRIDIAG_COLS 1  // p = A v by columns with row slices (0: warp per row)
+#endif
 template <bool SM, int TT>
 __global__ void __launch_bounds__(TT) tridiag_kernel(double* Ag, int m, double* dgl, double* off) {
   extern __shared__ double dsm[];
@@ -215,19 +219,75 @@ __global__ void __launch_bounds__(TT) tridiag_kernel(double* Ag, int m, double* 
     __syncthreads();
     const double beta = s_beta;
     if (beta == 0.0) continue;
-    // p = beta * A22 v   (warp per row, lanes over columns)
-    for (int i = wid; i < L; i += TT / 32) {
-      const double* row = A + (int64_t)(j + 1 + i) * m + (j + 1);
-      double s = 0.0;
-      for (int t = lane; t < L; t += 32) s = fma(row[t], v[t], s);
-      s = warp_sum(s);
-      if (lane == 0) p[i] = beta * s;
-    }
-    __syncthreads();
     double loc2 = 0.0;
-    for (int t = tid; t < L; t += TT) loc2 += p[t] * v[t];
+    if (SM && AFN_TRIDIAG_COLS) {
+      // p = beta * A22 v by columns (A symmetric): thread (s, i) sums column
+      // i over the rows t = s, s + S, ..  (consecutive threads read consecutive
+      // words of a row: no bank conflicts, v[t] broadcast), then thread i adds
+      // the S partials in order
+      const int S = TT / L;
+      double* part = p + m;
+      if (tid < S * L) {
+        const int s = tid / L, i = tid - s * L;
+        const double* col = A + (int64_t)(j + 1) * m + (j + 1) + i;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int t = s;
+        for (; t + 3 * S < L; t += 4 * S) {
+          a0 = fma(col[(int64_t)t * m], v[t], a0);
+          a1 = fma(col[(int64_t)(t + S) * m], v[t + S], a1);
+          a2 = fma(col[(int64_t)(t + 2 * S) * m], v[t + 2 * S], a2);
+          a3 = fma(col[(int64_t)(t + 3 * S) * m], v[t + 3 * S], a3);
+        }
+        for (; t < L; t += S) a0 = fma(col[(int64_t)t * m], v[t], a0);
+        part[tid] = (a0 + a1) + (a2 + a3);
+      }
+      __syncthreads();
+      if (tid < L) {
+        double q = part[tid];
+        for (int s = 1; s < S; ++s) q += part[s * L + tid];
+        p[tid] = beta * q;
+        loc2 = p[tid] * v[tid];
+      }
+    } else {
+      // p = beta * A22 v   (warp per row, lanes over columns)
+      for (int i = wid; i < L; i += TT / 32) {
+        const double* row = A + (int64_t)(j + 1 + i) * m + (j + 1);
+        double s = 0.0;
+        for (int t = lane; t < L; t += 32) s = fma(row[t], v[t], s);
+        s = warp_sum(s);
+        if (lane == 0) p[i] = beta * s;
+      }
+      __syncthreads();
+      for (int t = tid; t < L; t += TT) loc2 += p[t] * v[t];
+    }
     const double pv = block_sum_all<TT>(loc2, sh);
     const double K = 0.5 * beta * pv;
+    if (SM && AFN_TRIDIAG_COLS) {
+      // A22 -= v w^T + w v^T with w = p - K v formed in registers (no pass over
+      // p, no barrier); each lane keeps its <= 6 columns' v_t, w_t for all its
+      // rows, and a row's loads are issued before its stores
+      constexpr int QN = (SM_MAX_M + 31) / 32;
+      double vt[QN], wt[QN];
+#pragma unroll
+      for (int q = 0; q < QN; ++q) {
+        const int t = lane + 32 * q;
+        vt[q] = t < L ? v[t] : 0.0;
+        wt[q] = t < L ? p[t] - K * v[t] : 0.0;
+      }
+      for (int i = wid; i < L; i += TT / 32) {
+        const double vi = v[i], wi = p[i] - K * v[i];
+        double* a = A + (int64_t)(j + 1 + i) * m + (j + 1);
+        double av[QN];
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+          if (lane + 32 * q < L) av[q] = a[lane + 32 * q];
+#pragma unroll
+        for (int q = 0; q < QN; ++q)
+          if (lane + 32 * q < L) a[lane + 32 * q] = av[q] - vi * wt[q] - wi * vt[q];
+      }
+      __syncthreads();
+      continue;
+    }
     for (int t = tid; t < L; t += TT) p[t] = p[t] - K * v[t];  // w
     __syncthreads();
     for (int i = wid; i < L; i += TT / 32) {  // warp per row (no 64-bit index division)
@@ -350,7 +410,6 @@ __global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict
   if (tid == 0) *pass = s_ok;
 }
 
-constexpr int SM_MAX_M = 164;  // (m^2 + 2m) doubles of dynamic smem <= 227 KB
 
 }  // namespace
 
@@ -364,7 +423,8 @@ afn_status launch_tridiag(double* A, int m, double* dgl, double* off, cudaStream
   // AFN_TRIDIAG_T: threads of the single CTA (1024 default: 0.75 ms at m = 163; 256: 1.14 ms)
   static const int tt = getenv("AFN_TRIDIAG_T") ? atoi(getenv("AFN_TRIDIAG_T")) : 1024;
   if (m <= SM_MAX_M) {
-    const size_t bytes = sizeof(double) * ((size_t)m * m + 2 * (size_t)m);
+    // (+ the column partials of p: <= 1024 doubles; 164^2 + 2 164 + 1024 doubles <= 227 KB)
+    const size_t bytes = sizeof(double) * ((size_t)m * m + 2 * (size_t)m + (AFN_TRIDIAG_COLS ? 1024 : 0));
     if (tt == 1024) {
       AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
       tridiag_kernel<true, 1024><<<1, 1024, bytes, st>>>(A, m, dgl, off);
