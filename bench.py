@@ -445,7 +445,8 @@ def main():
         bh = torch.from_numpy(b).pin_memory()
         E = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
              for _ in range(args.steps)]
-        afn.afn_solve_host(Xh.numpy(), bh.numpy(), params(my_ls[0]), tol=cfg.tol)  # warm
+        if my_ls:  # (ranks past the sweep's length have no problem: N > 6 GPUs)
+            afn.afn_solve_host(Xh.numpy(), bh.numpy(), params(my_ls[0]), tol=cfg.tol)  # warm
         for s in range(args.steps):
             flush.zero_()
             E[s][0].record(stream)
