@@ -238,7 +238,10 @@ def run_dist(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     import __graft_entry__ as ge
-    ge._build_module().build()
+    if local == 0:  # (one builder per node: ranks must not write the same objects)
+        ge._build_module().build()
+    if dist:
+        dist.barrier()
     import paper_2304_05460_b200 as afn
     from synth import CONFIGS, gen_problem
     cfg = CONFIGS[args.config]
@@ -328,7 +331,10 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     import __graft_entry__ as ge
-    ge._build_module().build()
+    if local == 0:  # (one builder per node: ranks must not write the same objects)
+        ge._build_module().build()
+    if dist:
+        dist.barrier()
     import paper_2304_05460_b200 as afn
     from synth import CONFIGS, gen_problem
 
