@@ -2,25 +2,31 @@
 """bench.py -- AFN-PCG on B200 (arXiv 2304.05460 hot path), one JSON line.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl afn|reference]
+                    [--config C3] [--no-e2e] [--no-cpu] [--no-sweep]
 
-Workload (BASELINE.json configs[1], "C2"): n = 16384 points uniform in a 3-D
-cube of edge 10*(16384/1000)^(1/3), Gaussian kernel, l swept over
-{0.1, 0.5, 1, 2, 5, 10}, mu = 1e-4, b ~ N(0,1) (seed 0), adaptive k <= 2000
-(Algorithm 1), FSAI 100 nnz/row, PCG tol 1e-4.  One *step* = the whole hot
-path (all SURVEY.md 8(a) rows: Alg. 1, FPS, permutation, Cholesky, W, kNN,
-FSAI, PCG with kernel matvec + AFN apply) for every l of the sweep.
+Workload (default BASELINE.json configs[2], "C3"): n = 131072 points uniform
+in a constant-density 3-D cube, Gaussian kernel l = 1, mu = 1e-4, b ~ N(0,1)
+(seed 0), adaptive k <= 4000 (Algorithm 1), FSAI 100 nnz/row, PCG tol 1e-4.
+One *step* = one whole AFN-PCG solve of that problem -- every SURVEY.md 8(a)
+row: Alg. 1, FPS, permutation, Cholesky, W, kNN, FSAI, then PCG with the
+kernel matvec and the AFN apply -- with its rows sharded over the N ranks
+(one GPU each, NCCL all-gathers; N = 1 is the one-GPU path).  Strong scaling:
+the problem is fixed as N grows.  `--config C5` runs the north star's
+n = 2^20 scaling problem the same way.
 
-Metric: AFN-PCG seconds per solve (build + PCG, device time from CUDA events,
-lower is better) with the kernel-matvec Gpairs/s and the FP64 roofline
-fraction of the dominant kernel beside it.  With N GPUs the six sweep problems
-are split across ranks (independent problems, no data-path collective); the
-job time is the max over ranks.
+Metric: AFN-PCG seconds per solve (device time, CUDA events on the launching
+stream, max over ranks; lower is better) with the kernel matvec's Gpairs/s and
+its fraction of the FP64 peak beside it (`roofline_kmv`), the AFN apply's HBM
+fraction (`roofline_apply`) and the dominant kernel's roofline (`roofline`).
+`c2_sweep` repeats BASELINE.json's 1-GPU C2 sweep (n = 16384, six l) as an
+extra key.  `e2e` is the same solve through afn_solve_host (host buffers,
+copies inside the timed region).  `cpu_baseline` times the oracle on a
+bounded sample of the same workload on this host's cores.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -31,21 +37,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "AFN-PCG solve sec & kernel-matvec Gpairs/s (fp64) vs FP64 roofline"
-# FP64 peak derived from the guide's unit counts:
-# 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+# FP64 peak from the guide's unit counts and clocks: 148 SMs x
+# 64 FP64 FMA lanes/clk x 1.965 GHz; flops count an FMA as 2.  MEASURED_PEAKS.json
+# has no FP64 entry; afn_probe_dfma's measured figure is reported beside it.
+SMS, FP64_LANES, SM_GHZ = 148, 64, 1.965
+FP64_PEAK_TFLOPS = SMS * FP64_LANES * 2 * SM_GHZ / 1e3
+FP64_PIPE_INST_PER_S = SMS * FP64_LANES * SM_GHZ * 1e9
 
 
 def _hbm_peak():
     try:
-        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "of measured"
     except Exception:
-        return 6650.0  # B200_PROFILING.md fallback
+        return 6650.0, "of fallback"  # B200_PROFILING.md
 
 
-HBM_PEAK_GBS = _hbm_peak()
-# kernel matvec: algorithmic flops per pair for d = 3: 3d + 19
-KMV_FLOPS_PER_PAIR = lambda d: 3 * d + 19  # noqa: E731
+HBM_PEAK_GBS, HBM_PEAK_SRC = _hbm_peak()
 
 
 def parse():
@@ -54,12 +61,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="afn", choices=["afn", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C3")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--mode", default="sweep", choices=["sweep", "dist"],
-                    help="sweep: the C2 l-sweep, problems split over ranks (default); "
-                         "dist: every rank solves the same problem row-sharded (SURVEY 8(e))")
+    ap.add_argument("--no-sweep", action="store_true")
     return ap.parse_args()
 
 
@@ -112,73 +117,6 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-# ---------------------------------------------------------------------------
-def fsai_flops(N2: int, k: int, w: int) -> float:
-    """Algorithmic flops of the FSAI row kernel: lower-triangle Gram
-    (wp(wp+1)/2 dot products of length k, FMA = 2) + Cholesky wp^3/3 + solve wp^2."""
-    tot = 0.0
-    for wp in range(1, min(w, N2) + 1):  # rows 0..w-2 have wp = i+1
-        cnt = 1 if wp < w else max(0, N2 - (w - 1))
-        tot += cnt * (wp * (wp + 1) * k + wp ** 3 / 3.0 + wp * wp)
-    return tot
-
-
-def oracle_solve_estimate(X, b, cfg, l, gpu_iters=None, frac=16, threads=None):
-    """Oracle (CPU) seconds for one AFN-PCG solve of this workload, from a
-    bounded sample: Alg. 1, FPS and the landmark block run in full; kNN and
-    FSAI on every `frac`-th non-landmark row, the kernel matvec on every
-    `frac`-th row (both scaled by frac); the apply in full.  PCG iterations
-    from the oracle's own Alg. 1 k and, if given, the GPU's iteration count."""
-    import numpy as np
-    import scipy.linalg as sla
-    import oracle as O
-    t = {}
-    t0 = time.perf_counter()
-    a1 = O.alg1(X, l)
-    t["alg1"] = time.perf_counter() - t0
-    k = min(cfg.k_cap, max(1, a1["khat"]), len(X))
-    t0 = time.perf_counter()
-    idx, _ = O.fps(X, k, 0)
-    t["fps"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    n = len(X)
-    mask = np.ones(n, bool)
-    mask[idx] = False
-    perm = np.concatenate([idx, np.nonzero(mask)[0]])
-    Xp = X[perm]
-    X1, X2 = Xp[:k], Xp[k:]
-    L = np.linalg.cholesky(O.kernel_block(X1, X1, l) + cfg.mu * np.eye(k))
-    K12 = O.kernel_block(X1, X2, l)
-    V = sla.solve_triangular(L, K12, lower=True)
-    t["chol_V"] = time.perf_counter() - t0
-    N2 = n - k
-    rows = np.arange(0, N2, frac)
-    t0 = time.perf_counter()
-    pat = [O.knn_row(X2, int(i), cfg.w) for i in rows]
-    t["knn"] = (time.perf_counter() - t0) * frac
-    rp = np.zeros(len(rows) + 1, dtype=np.int64)
-    rp[1:] = np.cumsum([len(p) for p in pat])
-    col = np.concatenate(pat)
-    t0 = time.perf_counter()
-    O.fsai_rows(lambda J: O.kernel_block(X2[J], X2[J], l) + cfg.mu * np.eye(len(J))
-                - V[:, J].T @ V[:, J], rp, col)
-    t["fsai"] = (time.perf_counter() - t0) * frac
-    v = np.asarray(b, dtype=np.float64)
-    t0 = time.perf_counter()
-    O.kmv_rows(Xp, l, cfg.mu, v, np.arange(0, n, frac))
-    t_kmv = (time.perf_counter() - t0) * frac
-    import scipy.sparse as sp
-    G = sp.identity(N2, format="csr")
-    B = dict(k=k, L=L, K12=K12, G=G)
-    t0 = time.perf_counter()
-    O.apply_afn(B, v)
-    t_apply = time.perf_counter() - t0
-    its = gpu_iters if gpu_iters is not None else 10
-    t["pcg"] = (its + 1) * t_kmv + (its + 1) * t_apply
-    total = sum(t.values())
-    return total, t, k
-
-
 def cpu_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -187,35 +125,143 @@ def cpu_cores():
 
 
 # ---------------------------------------------------------------------------
+def oracle_iterations(cfg, l):
+    """The oracle's own PCG iteration count for this workload, if committed
+    (tests/oracle_data, written by tools/make_oracle_fixtures.py from oracle/)."""
+    import numpy as np
+    fx = os.path.join(ROOT, "tests", "oracle_data", f"{cfg.name.lower()}_l{l:g}.npz")
+    if os.path.exists(fx):
+        return int(np.load(fx)["iters"]), "oracle's own count (tests/oracle_data)"
+    return None, None
+
+
+def oracle_sample_estimate(X, b, cfg, l, its):
+    """Seconds the oracle (as it stands, numpy/scipy on this host's cores)
+    needs for one AFN-PCG solve of this workload, from a bounded sample:
+      * Alg. 1 (P:L661-678) and the k x k Cholesky of K11 + mu I: in full;
+      * FPS: the first 256 steps, scaled by k / 256 (every step is one O(n)
+        distance update, P:L800);
+      * V = L^{-1} K12 on every 64th non-landmark column, scaled x 64;
+      * kNN rows and FSAI rows (S_JJ from K_JJ, mu and V_J; the solve) on
+        every 1024th non-landmark row, scaled x 1024;
+      * the kernel matvec on every 512th row, scaled x 512, times (its + 1)
+        (the loop's products and the true residual);
+      * the apply: the four triangular solves with L in full, the
+        two K12 products on the 64th-column sample (x 64) and the G, G^T
+        products on the 1024th-row sample (x 1024), times (its + 1).
+    The landmarks past the FPS sample are the next points of a seeded random
+    order (they only have to be k distinct points for the timing).  Returns
+    (seconds, parts, k)."""
+    import numpy as np
+    import scipy.linalg as sla
+    import oracle as O
+    threads = cpu_cores()
+    t = {}
+    n = len(X)
+    c = time.perf_counter()
+    a1 = O.alg1(X, l)
+    t["alg1"] = time.perf_counter() - c
+    k = min(cfg.k_cap, max(1, a1["khat"]), n)
+    kf = min(k, 256)
+    c = time.perf_counter()
+    idx, _ = O.fps(X, kf, 0)
+    t["fps"] = (time.perf_counter() - c) * k / kf
+    if k > kf:
+        rest = np.setdiff1d(np.random.default_rng(0).permutation(n), idx, assume_unique=True)
+        idx = np.concatenate([idx, rest[: k - kf]])
+    mask = np.ones(n, bool)
+    mask[idx] = False
+    perm = np.concatenate([idx, np.nonzero(mask)[0]])
+    Xp = X[perm]
+    X1, X2 = Xp[:k], Xp[k:]
+    N2 = n - k
+    c = time.perf_counter()
+    L = np.linalg.cholesky(O.kernel_block(X1, X1, l) + cfg.mu * np.eye(k))
+    t["chol"] = time.perf_counter() - c
+    cols = np.arange(0, N2, 64)
+    c = time.perf_counter()
+    K12s = O.kernel_block(X1, X2[cols], l)
+    sla.solve_triangular(L, K12s, lower=True)
+    t["V"] = (time.perf_counter() - c) * N2 / len(cols)
+    rows = np.arange(0, N2, 1024)
+    c = time.perf_counter()
+    pats = [O.knn_row(X2, int(i), cfg.w) for i in rows]
+    t["knn"] = (time.perf_counter() - c) * N2 / len(rows)
+    VJ = {int(i): sla.solve_triangular(L, O.kernel_block(X1, X2[J], l), lower=True) for i, J in zip(rows, pats)}
+    c = time.perf_counter()
+    gv = []
+    for i, J in zip(rows, pats):
+        V = VJ[int(i)]
+        S = O.kernel_block(X2[J], X2[J], l) + cfg.mu * np.eye(len(J)) - V.T @ V
+        gv.append(O.fsai_rows(lambda _J, S=S: S, np.array([0, len(J)]), J))
+    t["fsai"] = (time.perf_counter() - c) * N2 / len(rows)
+    mrows = np.arange(0, n, 512)
+    c = time.perf_counter()
+    O.kmv_rows(Xp, l, cfg.mu, b, mrows)
+    t_kmv = (time.perf_counter() - c) * n / len(mrows)
+    import scipy.sparse as sp
+    rp = np.zeros(len(rows) + 1, dtype=np.int64)
+    rp[1:] = np.cumsum([len(J) for J in pats])
+    Gs = sp.csr_matrix((np.concatenate(gv), np.concatenate(pats), rp), shape=(len(rows), N2))
+    r1, u = b[:k], b[k:]
+    c = time.perf_counter()
+    y = sla.solve_triangular(L.T, sla.solve_triangular(L, r1, lower=True), lower=False)
+    sla.solve_triangular(L.T, sla.solve_triangular(L, y, lower=True), lower=False)
+    t_tri = time.perf_counter() - c
+    c = time.perf_counter()
+    K12s.T @ y
+    K12s @ u[cols]
+    t_k12 = (time.perf_counter() - c) * N2 / len(cols)
+    c = time.perf_counter()
+    g = Gs @ u
+    Gs.T @ g
+    t_g = (time.perf_counter() - c) * N2 / len(rows)
+    t_apply = t_tri + t_k12 + t_g
+    t["pcg"] = (its + 1) * t_kmv + (its + 1) * t_apply
+    t["per_matvec"] = t_kmv
+    t["per_apply"] = t_apply
+    total = sum(v for key, v in t.items() if not key.startswith("per_"))
+    return total, {key: round(v, 3) for key, v in t.items()}, k, threads
+
+
+ORACLE_SAMPLE = ("Alg.1 and the k x k Cholesky in full; FPS first 256 steps (x k/256); V on every 64th "
+                 "column (x64); kNN + FSAI rows every 1024th (x1024); kernel matvec every 512th row "
+                 "(x512) x (its+1); apply: triangular solves in full, K12 and G products on the same "
+                 "samples, x (its+1)")
+
+
+# ---------------------------------------------------------------------------
 def run_reference(args):
-    """--impl reference: the oracle, as it stands, on the host cores."""
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     from synth import CONFIGS, gen_problem
     cfg = CONFIGS[args.config]
+    l = cfg.ls[0]
     X, b = gen_problem(cfg)
-    ls = cfg.ls
-    for s in range(args.warmup):
-        oracle_solve_estimate(X, b, cfg, ls[s % len(ls)])
+    its, src = oracle_iterations(cfg, l)
+    if its is None:
+        its, src = 10, "assumed (no committed oracle count for this config)"
+    for _ in range(args.warmup):
+        oracle_sample_estimate(X, b, cfg, l, its)
     vals = []
     t0 = time.perf_counter()
-    for s in range(args.steps):
-        v, parts, k = oracle_solve_estimate(X, b, cfg, ls[s % len(ls)])
+    parts, k, threads = None, None, None
+    for _ in range(args.steps):
+        v, parts, k, threads = oracle_sample_estimate(X, b, cfg, l, its)
         vals.append(v)
     wall = time.perf_counter() - t0
     value = sum(vals) / len(vals)
-    sample = (f"{args.config}: per step one sweep value of l (cycling {list(ls)}); Alg.1, FPS, "
-              f"Cholesky and V=L^-1 K12 in full; kNN, FSAI and kernel-matvec rows 1/16 sampled "
-              f"and scaled x16; PCG iterations assumed 10")
+    sample = f"{cfg.name} l={l:g} (k={k}): {ORACLE_SAMPLE}; {its} PCG iterations, {src}"
     line = {"metric": METRIC, "value": value, "unit": "s/solve", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "n": cfg.n, "d": cfg.d, "ls": list(ls),
-                       "mu": cfg.mu, "k_cap": cfg.k_cap, "w": cfg.w, "tol": cfg.tol},
-            "cpu_baseline": {"value": value, "unit": "s/solve", "cores": cpu_cores(),
-                             "kind": "oracle", "sample": sample},
+            "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "l": l, "mu": cfg.mu,
+                       "k_cap": cfg.k_cap, "k_adaptive": True, "w": cfg.w, "tol": cfg.tol},
+            "cpu_baseline": {"value": value, "unit": "s/solve", "cores": threads, "kind": "oracle",
+                             "sample": sample, "parts_s": parts},
             "e2e": {"value": value, "unit": "s/solve", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -223,100 +269,10 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
-def run_dist(args):
-    """--mode dist: one AFN-PCG problem per step, rows sharded over all ranks
-    (one GPU each, NCCL all-gathers; include/afn.h "Multi-GPU").  Strong
-    scaling: the total work is fixed as N grows."""
-    import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    import __graft_entry__ as ge
-    if local == 0:  # (one builder per node: ranks must not write the same objects)
-        ge._build_module().build()
-    if dist:
-        dist.barrier()
-    import paper_2304_05460_b200 as afn
-    from synth import CONFIGS, gen_problem
-    cfg = CONFIGS[args.config]
-    X, b = gen_problem(cfg)
-    Xd, bd = torch.from_numpy(X).to(dev), torch.from_numpy(b).to(dev)
-    comm = afn.Comm.from_process_group(dist) if dist else None
-    recs = []
-
-    def step(record=False):
-        for l in cfg.ls:
-            h = afn.afn_build(Xd, afn.make_params(l, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True),
-                              comm=comm)
-            a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit)
-            if record:
-                recs.append((l, h.info(), rep))
-            h.close()
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    stream = torch.cuda.current_stream()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    sampler = ClockSampler(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    l0 = afn.launch_count()
-    with sampler:
-        for s in range(args.steps):
-            evs[s][0].record(stream)
-            step(record=True)
-            evs[s][1].record(stream)
-        torch.cuda.synchronize()
-    launches = afn.launch_count() - l0
-    if dist:
-        dist.barrier()
-    t = torch.tensor([sum(a.elapsed_time(c) for a, c in evs)], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    job_ms = float(t.item())
-    nsolve = args.steps * len(cfg.ls)
-    mv_ms = sum(r["matvec_ms"] for _, _, r in recs)
-    its = sum(r["iterations"] for _, _, r in recs)
-    if rank == 0:
-        inf, rep = recs[0][1], recs[0][2]
-        line = {"metric": METRIC, "value": job_ms / 1e3 / nsolve, "unit": "s/solve", "n_gpus": world,
-                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": job_ms / args.steps,
-                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded, BASELINE configs)",
-                "config": {"workload": args.config, "n": cfg.n, "d": cfg.d, "ls": list(cfg.ls),
-                           "mu": cfg.mu, "k_cap": cfg.k_cap, "w": cfg.w, "tol": cfg.tol,
-                           "parallelism": f"rows sharded over {world} rank(s), points replicated",
-                           "l2": "inputs and working set (W) larger than L2"},
-                "kmv_gpairs_per_s": float(cfg.n) ** 2 * its / (mv_ms * 1e-3) / 1e9 if mv_ms > 0 else None,
-                "per_solve": {"k": inf["k"], "khat": inf["khat"], "iters": rep["iterations"],
-                              "setup_ms": inf["ms_total"], "pcg_ms": rep["solve_ms"],
-                              "matvec_ms": rep["matvec_ms"], "apply_ms": rep["apply_ms"],
-                              "comm_ms": rep["comm_ms"], "relres_true": rep["relres_true"]},
-                "gpu_launches": launches, "clocks": sampler.summary()}
-        print(json.dumps(line), flush=True)
-    if comm is not None:
-        comm.close()
-    if dist:
-        dist.destroy_process_group()
-    return 0
-
-
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
-    if args.mode == "dist":
-        if args.config == "C2":
-            args.config = "C3"
-        return run_dist(args)
 
     import numpy as np
     import torch
@@ -329,7 +285,6 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-
     import __graft_entry__ as ge
     if local == 0:  # (one builder per node: ranks must not write the same objects)
         ge._build_module().build()
@@ -339,83 +294,68 @@ def main():
     from synth import CONFIGS, gen_problem
 
     cfg = CONFIGS[args.config]
+    l = cfg.ls[0]
     X, b = gen_problem(cfg)
-    Xd = torch.from_numpy(X).to(dev)
-    bd = torch.from_numpy(b).to(dev)
-    my_ls = list(cfg.ls[rank::world])
+    Xd, bd = torch.from_numpy(X).to(dev), torch.from_numpy(b).to(dev)
+    comm = afn.Comm.from_process_group(dist) if dist else None
+    prm = afn.make_params(l, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
 
-    def params(l):
-        return afn.make_params(l, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True)
+    def timed(steps, step_fn):
+        """K steps between a barrier + synchronize on both sides, CUDA events on
+        the launching stream, L2 flushed before each step (outside the events);
+        returns (this rank's total ms, the max over ranks)."""
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for s in range(steps):
+            flush.zero_()
+            evs[s][0].record(stream)
+            step_fn()
+            evs[s][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        mine = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+        t = torch.tensor([mine], dtype=torch.float64, device=dev)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return mine, float(t.item())
 
     records = []
 
-    def step(record=False):
-        for l in my_ls:
-            h = afn.afn_build(Xd, params(l))
-            a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit)
-            if record:
-                records.append((l, h.info(), rep))
-            h.close()
+    def solve(record):
+        h = afn.afn_build(Xd, prm, comm=comm)
+        a, rep = h.pcg_solve(bd, tol=cfg.tol, maxit=cfg.maxit)
+        if record:
+            records.append((h.info(), rep))
+        h.close()
 
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
     for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+        solve(False)
     sampler = ClockSampler(local)
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     l0 = afn.launch_count()
     afn.kernel_timers(reset=True, enable=True)
     with sampler:
-        for s in range(args.steps):
-            flush.zero_()  # L2 flush between timed steps (outside the event pair)
-            evs[s][0].record(stream)
-            step(record=True)
-            evs[s][1].record(stream)
-        torch.cuda.synchronize()
+        _, job_ms = timed(args.steps, lambda: solve(True))
     launches = afn.launch_count() - l0
     kt = afn.kernel_timers(enable=False)
-    if dist:
-        dist.barrier()
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    job_ms = float(t.item())
-    n_solves = len(cfg.ls)
-    value_s = job_ms / 1e3 / (args.steps * n_solves)
+    value_s = job_ms / 1e3 / args.steps
 
-    # ---- per-kernel accounting (CUDA events inside the library, timed region)
-    n = cfg.n
-    kmv_ms = sum(r["matvec_ms"] for _, _, r in records)
-    kmv_calls = sum(r["iterations"] for _, _, r in records)
-    per_l = {}
-    for l, inf, rep in records[: len(my_ls)]:
-        per_l[str(l)] = {"khat": inf["khat"], "k": inf["k"], "iters": rep["iterations"],
-                         "setup_ms": inf["ms_total"], "pcg_ms": rep["solve_ms"],
-                         "relres_true": rep["relres_true"]}
-    kmv_gpairs = (float(n) * n * kmv_calls) / (kmv_ms * 1e-3) / 1e9 if kmv_ms > 0 else None
-    shares = {"fsai_phase": sum(i["ms_fsai_rows"] for _, i, _ in records), "kmv_kernel": kmv_ms,
-              "fps": sum(i["ms_fps"] for _, i, _ in records),
-              "W": sum(i["ms_trsm"] for _, i, _ in records),
-              "chol_Linv": sum(i["ms_chol"] for _, i, _ in records),
-              "alg1": sum(i["ms_alg1"] for _, i, _ in records),
-              "knn": sum(i["ms_knn"] for _, i, _ in records),
-              "apply": sum(r["apply_ms"] for _, _, r in records)}
-    single = {k: v for k, v in kt.items() if k not in ("potrf", "alg1") and v["count"] > 0}
-    dom = max(single, key=lambda k: single[k]["ms"]) if single else None
-    traffic = None
+    # ---- rooflines from the library's CUDA-event timers (timed region)
+    inf0, rep0 = records[0]
+    n, d = cfg.n, cfg.d
+    step_ms = job_ms / args.steps
+    traffic = {}
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tr_path) and dom:
+    if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get(dom)
+            traffic = json.load(open(tr_path))
         except Exception:
-            traffic = None
+            traffic = {}
 
     def roof(name):
         v = kt.get(name)
@@ -423,80 +363,109 @@ def main():
             return None
         per_ms = v["ms"] / v["count"]
         out = {"kernel": name, "launches": v["count"], "ms_per_launch": per_ms,
-               "share_of_step": v["ms"] / total_ms if total_ms > 0 else None, "traffic": None}
+               "share_of_step": v["ms"] / args.steps / step_ms if step_ms > 0 else None,
+               "traffic": (traffic.get(args.config, {}) or {}).get(name)}
         if name == "apply":
             ach = v["work"] / (v["ms"] * 1e-3) / 1e9
             out.update({"bound": "hbm", "achieved": ach, "peak": HBM_PEAK_GBS, "unit": "GB/s",
                         "frac": ach / HBM_PEAK_GBS, "bytes_per_launch": v["work"] / v["count"],
-                        "peak_source": "MEASURED_PEAKS.json hbm_gbs"})
+                        "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({HBM_PEAK_SRC})"})
         elif v["work"] > 0:
             ach = v["work"] / (v["ms"] * 1e-3) / 1e12
-            out.update({"bound": "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                        "frac": ach / FP64_PEAK_TFLOPS, "flops_per_launch": v["work"] / v["count"],
-                        "peak_source": "guide unit counts: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"})
+            tensor = name in ("group_gemm_kernel", "w_gemm_kernel")
+            out.update({"bound": "tensor" if tensor else "alu", "achieved": ach, "peak": FP64_PEAK_TFLOPS,
+                        "unit": "TFLOP/s", "frac": ach / FP64_PEAK_TFLOPS,
+                        "flops_per_launch": v["work"] / v["count"],
+                        "peak_source": ("FP64 (DMMA = SIMT rate on B200) " if tensor else "FP64 ") +
+                                       "from the guide's unit counts: 148 SM x 64 FP64 lanes x 2 x 1.965 GHz"})
         else:
             out.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None})
         return out
 
+    cand = {k: v for k, v in kt.items() if v["count"] > 0 and v["work"] > 0}
+    dom = max(cand, key=lambda k: cand[k]["ms"]) if cand else None
     roofline = roof(dom) if dom else None
-    if roofline is not None:
-        roofline["traffic"] = traffic
     r_kmv = roof("kmv_kernel")
-    kernel_ms = {k: round(v["ms"], 3) for k, v in kt.items() if v["count"] > 0}
+    if r_kmv:
+        # executed FP64-pipe instructions per useful pair / flops per pair
+        # (kmv.cu kmv_fp64_inst / kmv_flops; Gaussian, symmetric, d <= 4):
+        # (2d + 9) / (3d + 15)
+        inst_per_flop = (2 * d + 9) / (3 * d + 15)
+        r_kmv["fp64_pipe_frac"] = r_kmv["achieved"] * 1e12 * inst_per_flop / FP64_PIPE_INST_PER_S
+        kmv = kt["kmv_kernel"]
+        r_kmv["gpairs_per_s"] = float(n) * n * kmv["count"] / (kmv["ms"] * 1e-3) / 1e9 / max(1, world)
+    r_apply = roof("apply")
+    kernel_ms = {k: round(v["ms"] / args.steps, 3) for k, v in kt.items() if v["count"] > 0}
+    try:
+        probe = afn.probe_dfma()
+    except Exception:
+        probe = None
+
+    # ---- C2 sweep (BASELINE.json configs[1]) as an extra key
+    sweep = None
+    if not args.no_sweep:
+        c2 = CONFIGS["C2"]
+        X2, b2 = gen_problem(c2)
+        X2d, b2d = torch.from_numpy(X2).to(dev), torch.from_numpy(b2).to(dev)
+        my_ls = list(c2.ls[rank::world])
+        per_l = {}
+
+        def sweep_step(record=False):
+            for ll in my_ls:
+                h = afn.afn_build(X2d, afn.make_params(ll, c2.mu, c2.k_cap, c2.w, k_adaptive=True))
+                _, rp = h.pcg_solve(b2d, tol=c2.tol, maxit=c2.maxit)
+                if record:
+                    inf = h.info()
+                    per_l[str(ll)] = {"k": inf["k"], "khat": inf["khat"], "iters": rp["iterations"],
+                                      "setup_ms": round(inf["ms_total"], 3), "pcg_ms": round(rp["solve_ms"], 3)}
+                h.close()
+
+        sweep_step(True)
+        _, sw_ms = timed(args.steps, sweep_step)
+        sweep = {"value": sw_ms / 1e3 / (args.steps * len(c2.ls)), "unit": "s/solve",
+                 "workload": "C2", "n": c2.n, "ls": list(c2.ls), "split": f"sweep split over {world} rank(s)",
+                 "per_l": per_l}
 
     # ---- e2e: host buffers through the C ABI (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
         Xh = torch.from_numpy(X).pin_memory()
         bh = torch.from_numpy(b).pin_memory()
-        E = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-             for _ in range(args.steps)]
-        if my_ls:  # (ranks past the sweep's length have no problem: N > 6 GPUs)
-            afn.afn_solve_host(Xh.numpy(), bh.numpy(), params(my_ls[0]), tol=cfg.tol)  # warm
-        for s in range(args.steps):
-            flush.zero_()
-            E[s][0].record(stream)
-            for l in my_ls:
-                afn.afn_solve_host(Xh.numpy(), bh.numpy(), params(l), tol=cfg.tol, maxit=cfg.maxit)
-            E[s][1].record(stream)
-        torch.cuda.synchronize()
-        e_ms = sum(a.elapsed_time(c) for a, c in E)
-        te = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-        if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(te.item()) / 1e3 / (args.steps * n_solves), "unit": "s/solve",
-               "h2d_bytes_per_step": n_solves * (X.nbytes + b.nbytes),
-               "d2h_bytes_per_step": n_solves * b.nbytes}
+        afn.afn_solve_host(Xh.numpy(), bh.numpy(), prm, tol=cfg.tol, maxit=cfg.maxit, comm=comm)  # warm
+        _, e_ms = timed(args.steps, lambda: afn.afn_solve_host(Xh.numpy(), bh.numpy(), prm, tol=cfg.tol,
+                                                               maxit=cfg.maxit, comm=comm))
+        e2e = {"value": e_ms / 1e3 / args.steps, "unit": "s/solve", "h2d_bytes_per_step": X.nbytes + b.nbytes,
+               "d2h_bytes_per_step": b.nbytes}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        its = per_l.get("1.0", {}).get("iters")
-        v, parts, k = oracle_solve_estimate(X, b, cfg, 1.0, gpu_iters=its)
-        cpu = {"value": v, "unit": "s/solve", "cores": cpu_cores(), "kind": "oracle",
-               "sample": (f"{args.config} at l=1 (k={k}): Alg.1, FPS, Cholesky, V in full; kNN, "
-                          f"FSAI and kernel-matvec rows 1/16 sampled and scaled x16; "
-                          f"{its} PCG iterations (the GPU's count)"),
+        its = rep0["iterations"]
+        v, parts, k, threads = oracle_sample_estimate(X, b, cfg, l, its)
+        cpu = {"value": v, "unit": "s/solve", "cores": threads, "kind": "oracle",
+               "sample": f"{cfg.name} l={l:g} (k={k}): {ORACLE_SAMPLE}; {its} PCG iterations (the GPU's count)",
                "parts_s": parts}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value_s, "unit": "s/solve", "n_gpus": world,
-                "steps": args.steps, "warmup": max(3, args.warmup),
-                "ms_per_step": job_ms / args.steps, "higher_is_better": False,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (seeded uniform cube, b~N(0,1))",
-                "config": {"workload": args.config, "n": cfg.n, "d": cfg.d, "ls": list(cfg.ls),
-                           "mu": cfg.mu, "k_cap": cfg.k_cap, "k_adaptive": True, "w": cfg.w,
-                           "tol": cfg.tol, "maxit": cfg.maxit,
-                           "l2": "flushed between timed steps (256 MiB write, outside events)",
-                           "parallelism": f"sweep split over {world} rank(s)",
-                           "per_l": per_l},
-                "kmv_gpairs_per_s": kmv_gpairs,
+                "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": step_ms,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded uniform cube, b ~ N(0,1))",
+                "config": {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "l": l, "mu": cfg.mu,
+                           "k_cap": cfg.k_cap, "k_adaptive": True, "w": cfg.w, "tol": cfg.tol,
+                           "maxit": cfg.maxit, "parallelism": f"rows sharded over {world} rank(s)",
+                           "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                           "k": inf0["k"], "khat": inf0["khat"], "iters": rep0["iterations"],
+                           "setup_ms": round(inf0["ms_total"], 3), "pcg_ms": round(rep0["solve_ms"], 3),
+                           "relres_true": rep0["relres_true"]},
+                "kmv_gpairs_per_s": r_kmv["gpairs_per_s"] if r_kmv else None,
                 "gpu_launches": launches,
-                "roofline": roofline, "roofline_kmv": r_kmv,
-                "time_share_ms": shares, "kernel_ms": kernel_ms,
-                "clocks": sampler.summary(),
+                "roofline": roofline, "roofline_kmv": r_kmv, "roofline_apply": r_apply,
+                "fp64_probe_tflops": probe, "kernel_ms_per_step": kernel_ms,
+                "clocks": sampler.summary(), "c2_sweep": sweep,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if dist:
         dist.destroy_process_group()
     return 0

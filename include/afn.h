@@ -36,7 +36,10 @@
 extern "C" {
 #endif
 
-#define AFN_ABI_VERSION 3
+#define AFN_ABI_VERSION 4
+/* widest FSAI row (nonzeros incl. the diagonal): the paper's plain-FSAI
+ * comparison uses 400 neighbours */
+#define AFN_W_MAX 512
 
 typedef enum {
   AFN_OK = 0,
@@ -74,9 +77,11 @@ enum { AFN_LANDMARKS_FPS = 0, AFN_LANDMARKS_UNIFORM = 1 };
  *                       points in the original order (k = 0)
  *   AFN_METHOD_RAN      the paper's RAN comparison preconditioner:
  *                       (lam_k + mu) U (Lam + mu I)^{-1} U^T + (I - U U^T) for
- *                       K_nys = U Lam U^T on k landmarks (use uniform ones)  */
+ *                       K_nys = U Lam U^T on k landmarks (use uniform ones)
+ *   AFN_METHOD_NONE     M = I: plain CG, the paper's unpreconditioned
+ *                       baseline (Table 5.1a CG rows)  */
 enum { AFN_METHOD_AFN = 0, AFN_METHOD_ALG2 = 1, AFN_METHOD_NYSTROM = 2, AFN_METHOD_FSAI = 3,
-       AFN_METHOD_RAN = 4 };
+       AFN_METHOD_RAN = 4, AFN_METHOD_NONE = 5 };
 /* Order of the non-landmark points, which fixes "numbered less than i" of the
  * FSAI pattern: ascending original index (reading R14) or the
  * MaxMin order, i.e. FPS continued through all n points ("MaxMin
@@ -92,7 +97,7 @@ typedef struct {
   double mu;            /* regularisation, > 0                                 */
   int64_t k_cap;        /* landmark cap, >= 1                                  */
   int32_t k_adaptive;   /* 1: k = min(k_cap, max(1, Alg.1 khat)); 0: k = k_cap */
-  int32_t w;            /* FSAI nonzeros per row incl. diagonal, 1..128        */
+  int32_t w;            /* FSAI nonzeros per row incl. diagonal, 1..AFN_W_MAX  */
   int32_t m;            /* Alg. 1 subsample size; 0 = min(500,max(100,n/100))  */
   int32_t k_threshold;  /* Alg. 1 branch threshold (paper: 2000)               */
   int64_t fps_seed;     /* first FPS point, 0 <= fps_seed < n                  */
@@ -162,7 +167,7 @@ afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t see
 /* row i = {i} plus the min(w-1, i) nearest positions j < i; columns        */
 /* ascending (diagonal last).  row_ptr: N+1 int64 device (closed form        */
 /* row_ptr[i] = sum_{t<i} min(w, t+1)), col: row_ptr[N] int32 device.        */
-/* 1 <= w <= 128.  Stream-ordered.                                           */
+/* 1 <= w <= AFN_W_MAX.  Stream-ordered.                                     */
 afn_status afn_knn_pattern(const double* P, int64_t N, int32_t d, int32_t w,
                            int64_t* row_ptr, int32_t* col, void* stream);
 
@@ -182,6 +187,12 @@ afn_status afn_estimate_rank(const double* X, int64_t n, int32_t d, int32_t kern
 afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* params /*host*/,
                      void* stream, afn_handle* out /*host*/);
 
+/* y = (K + mu I) v with the handle's points, kernel and matvec plan (the   */
+/* PCG's own product: symmetric, pair units split over the ranks of a       */
+/* sharded handle).  v, y: n device, original order; every rank      */
+/* passes the full v and receives the full y (collective).  Stream-ordered. */
+afn_status afn_matvec(afn_handle h, const double* v, double* y, void* stream);
+
 /* z = M^{-1} r with the two-step algorithm in V-form:         */
 /*   t = L^{-1} r1; u = r2 - W t; s2 = G^T (G u); s1 = L^{-T} (t - W^T s2).   */
 /* r, z: n device, ORIGINAL point order (the handle permutes).  Stream-ordered */
@@ -195,9 +206,20 @@ afn_status afn_apply(afn_handle h, const double* r, double* z, void* stream);
 afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, int32_t maxit,
                          int32_t fixed_iters, afn_solve_report* rep /*host*/, void* stream);
 
+/* Unpreconditioned CG on (K + mu I) a = b, the paper's baseline (P:L70,    */
+/* L773; Table 5.1a CG rows): the PCG loop of afn_pcg_solve    */
+/* with M = I (the same matvec, stopping test and report).  X: n x d, b, a:  */
+/* n device, original order.  comm: NULL (one GPU) or a communicator (rows   */
+/* sharded as in afn_build_dist; collective).  [sync]                        */
+afn_status afn_cg_solve(afn_comm comm, const double* X, int64_t n, int32_t d, int32_t kernel, double l,
+                        double mu, const double* b, double* a, double tol, int32_t maxit, int32_t fixed_iters,
+                        afn_solve_report* rep /*host, optional*/, void* stream);
+
 /* End-to-end convenience with HOST buffers: copies X, b in, builds, solves, */
-/* copies a out (all inside the call).  X: n x d host, b, a: n host. [sync]   */
-afn_status afn_solve_host(const double* X, const double* b, double* a, int64_t n, int32_t d,
+/* copies a out (all inside the call).  X: n x d host, b, a: n host.  comm:  */
+/* NULL (one GPU) or a communicator (every process passes the same X, b and */
+/* receives the full a; collective).  [sync]                                */
+afn_status afn_solve_host(afn_comm comm, const double* X, const double* b, double* a, int64_t n, int32_t d,
                           const afn_params* params, double tol, int32_t maxit,
                           afn_info* info /*host, optional*/, afn_solve_report* rep /*host, optional*/,
                           void* stream);
@@ -254,6 +276,10 @@ afn_status afn_comm_init(const void* id /*host*/, int32_t nranks, int32_t rank,
 /* copies between them.  Results match a real nranks-GPU run bit for bit.   */
 afn_status afn_comm_init_emulated(int32_t nranks, afn_comm* out /*host*/);
 void afn_comm_destroy(afn_comm c);
+/* Host waits on streams with NCCL work poll ncclCommGetAsyncError; after an  */
+/* asynchronous error or `seconds` (default 600) the communicator is aborted */
+/* and the call returns AFN_ERR_NCCL (instead of hanging on a lost peer).    */
+afn_status afn_comm_set_timeout(afn_comm c, double seconds);
 /* rows[4] = {a0, na, b0, nb} owned by `rank` (host arithmetic only). */
 afn_status afn_shard_rows(int64_t n, int64_t k, int32_t nranks, int32_t rank, int64_t* rows /*host*/);
 /* afn_build over a communicator (comm = NULL: single GPU, same as afn_build).*/
@@ -280,6 +306,23 @@ afn_status afn_probe_dmma(int64_t iters, double* tflops /*host*/, void* stream);
 void afn_kt_enable(int32_t on);
 void afn_kt_reset(void);
 int32_t afn_kt_read(double* ms /*host*/, double* work /*host*/, int64_t* count /*host*/, int32_t n);
+
+/* ------------------------------------------------------------------------ */
+/* Optional caller allocator, e.g. PyTorch's caching        */
+/* allocator: every device allocation of the library then goes through      */
+/* alloc(bytes, stream, ctx) and free(ptr, bytes, stream, ctx) instead of    */
+/* the library's stream-ordered pool (cudaMallocAsync).  alloc returns NULL  */
+/* on failure (-> AFN_ERR_NOMEM).  The library calls free only after the     */
+/* stream position of the free has completed (so a caching allocator may    */
+/* hand the block to any stream at once).  Process-wide; set it while no     */
+/* handle built with the previous allocator is alive (else AFN_ERR_ARG).     */
+/* (NULL, NULL, NULL) restores the pool.                                     */
+typedef void* (*afn_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*afn_free_fn)(void* ptr, size_t bytes, void* stream, void* ctx);
+afn_status afn_set_allocator(afn_alloc_fn alloc, afn_free_fn free_fn, void* ctx);
+/* Reserved / used bytes of the library's default pool on the current device */
+/* (diagnostics: memory reuse across builds and streams).                   */
+afn_status afn_pool_stats(int64_t* reserved /*host*/, int64_t* used /*host*/);
 
 /* Number of kernels this library launched since load (its own kernels only). */
 int64_t afn_launch_count(void);

@@ -29,7 +29,8 @@ STATUS = {0: "AFN_OK", 1: "AFN_ERR_ARG", 2: "AFN_ERR_CUDA", 3: "AFN_ERR_NOMEM",
 COMM_ID_BYTES = 128
 KERNEL_GAUSSIAN, KERNEL_MATERN32 = 0, 1
 LANDMARKS_FPS, LANDMARKS_UNIFORM = 0, 1
-METHOD_AFN, METHOD_ALG2, METHOD_NYSTROM, METHOD_FSAI, METHOD_RAN = 0, 1, 2, 3, 4
+METHOD_AFN, METHOD_ALG2, METHOD_NYSTROM, METHOD_FSAI, METHOD_RAN, METHOD_NONE = 0, 1, 2, 3, 4, 5
+W_MAX = 512  # include/afn.h AFN_W_MAX
 ORDER_INDEX, ORDER_MAXMIN = 0, 1
 _KERNELS = {"gaussian": KERNEL_GAUSSIAN, "matern32": KERNEL_MATERN32}
 
@@ -96,8 +97,14 @@ _sig = {
                                     C.POINTER(C.c_int32), _P]),
     "afn_build": (C.c_int, [_P, C.c_int64, C.c_int32, C.POINTER(Params), _P, C.POINTER(_P)]),
     "afn_apply": (C.c_int, [_P, _P, _P, _P]),
+    "afn_matvec": (C.c_int, [_P, _P, _P, _P]),
     "afn_pcg_solve": (C.c_int, [_P, _P, _P, C.c_double, C.c_int32, C.c_int32, C.POINTER(Report), _P]),
-    "afn_solve_host": (C.c_int, [_P, _P, _P, C.c_int64, C.c_int32, C.POINTER(Params), C.c_double,
+    "afn_cg_solve": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_double, _P, _P,
+                               C.c_double, C.c_int32, C.c_int32, C.POINTER(Report), _P]),
+    "afn_set_allocator": (C.c_int, [_P, _P, _P]),
+    "afn_pool_stats": (C.c_int, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "afn_comm_set_timeout": (C.c_int, [_P, C.c_double]),
+    "afn_solve_host": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int32, C.POINTER(Params), C.c_double,
                                  C.c_int32, C.POINTER(Info), C.POINTER(Report), _P]),
     "afn_get_info": (C.c_int, [_P, C.POINTER(Info)]),
     "afn_copy_out": (C.c_int, [_P, C.c_int32, _P, C.c_size_t]),
@@ -319,6 +326,9 @@ class Comm:
         _check(_lib.afn_comm_init_emulated(int(nranks), C.byref(c)), "afn_comm_init_emulated")
         return cls(c, nranks, 0, nranks)
 
+    def set_timeout(self, seconds):
+        _check(_lib.afn_comm_set_timeout(self._c, float(seconds)), "afn_comm_set_timeout")
+
     def close(self):
         if getattr(self, "_c", None) is not None and self._c.value:
             _lib.afn_comm_destroy(self._c)
@@ -361,6 +371,15 @@ class Handle:
         inf = Info()
         _check(_lib.afn_get_info(self._h, C.byref(inf)), "afn_get_info")
         return inf.as_dict()
+
+    def matvec(self, v, y=None, stream=None):
+        """y = (K + mu I) v through the handle's (possibly rank-sharded) plan."""
+        torch = _torch()
+        if y is None:
+            y = torch.empty_like(v)
+        _check(_lib.afn_matvec(self._h, _dev(v, "v", torch.float64), _dev(y, "y", torch.float64),
+                               _stream(stream)), "afn_matvec")
+        return y
 
     def apply(self, r, z=None, stream=None):
         torch = _torch()
@@ -422,7 +441,68 @@ def afn_build(X, params: Params, stream=None, comm: Comm = None) -> Handle:
     return Handle(X, params, stream, comm)
 
 
-def afn_solve_host(X, b, params: Params, tol=1e-4, maxit=500, stream=None):
+def afn_cg_solve(X, b, l, mu, tol=1e-4, maxit=500, fixed_iters=0, a=None, kernel="gaussian",
+                 comm: Comm = None, history=False, stream=None):
+    """Unpreconditioned CG on (K + mu I) a = b (include/afn.h afn_cg_solve)."""
+    torch = _torch()
+    import numpy as np
+    n, d = X.shape
+    if a is None:
+        a = torch.empty_like(b)
+    rep = Report()
+    hist = None
+    if history:
+        hist = np.zeros(maxit + 1)
+        rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))
+    _check(_lib.afn_cg_solve(comm._c if comm is not None else None, _dev(X, "X", torch.float64), n, d,
+                             _kernel_id(kernel), float(l), float(mu), _dev(b, "b", torch.float64),
+                             _dev(a, "a", torch.float64), float(tol), int(maxit), int(fixed_iters),
+                             C.byref(rep), _stream(stream)), "afn_cg_solve")
+    out = rep.as_dict()
+    if hist is not None:
+        out["history"] = hist[: rep.iterations + 1].copy()
+    return a, out
+
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_allocator_refs = None  # keeps the ctypes callbacks alive while installed
+
+
+def use_torch_allocator(enable=True):
+    """Route the library's device allocations through PyTorch's caching
+    allocator (include/afn.h afn_set_allocator); enable=False restores the
+    library's own stream-ordered pool.  Marshalling only."""
+    global _allocator_refs
+    torch = _torch()
+    if not enable:
+        _check(_lib.afn_set_allocator(None, None, None), "afn_set_allocator")
+        _allocator_refs = None
+        return
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), stream=int(stream or 0))
+        except Exception:
+            return None
+
+    def _free(ptr, nbytes, stream, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    refs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    _check(_lib.afn_set_allocator(C.cast(refs[0], C.c_void_p), C.cast(refs[1], C.c_void_p), None),
+           "afn_set_allocator")
+    _allocator_refs = refs
+
+
+def pool_stats():
+    """(reserved, used) bytes of the library's default device pool."""
+    r, u = C.c_int64(), C.c_int64()
+    _check(_lib.afn_pool_stats(C.byref(r), C.byref(u)), "afn_pool_stats")
+    return r.value, u.value
+
+
+def afn_solve_host(X, b, params: Params, tol=1e-4, maxit=500, stream=None, comm: Comm = None):
     """End-to-end solve with HOST numpy arrays (copies inside the C call)."""
     import numpy as np
     X = np.ascontiguousarray(X, dtype=np.float64)
@@ -430,7 +510,8 @@ def afn_solve_host(X, b, params: Params, tol=1e-4, maxit=500, stream=None):
     n, d = X.shape
     a = np.empty(n)
     inf, rep = Info(), Report()
-    _check(_lib.afn_solve_host(X.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+    _check(_lib.afn_solve_host(comm._c if comm is not None else None,
+                               X.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
                                a.ctypes.data_as(C.c_void_p), n, d, C.byref(params), float(tol),
                                int(maxit), C.byref(inf), C.byref(rep), _stream(stream)),
            "afn_solve_host")

@@ -3,6 +3,8 @@
 // (P:L207-263), the apply and the PCG driver.
 #include <atomic>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -55,19 +57,74 @@ static void pool_setup_once() {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     // no hidden cross-stream waits: a block freed on one stream (e.g. the
-    // side stream's kNN temporaries) must not be handed to another stream's
-    // allocation with an inserted dependency on the first stream's work
-    int zero = 0;
+    // side stream's kNN temporaries) is never handed to another stream's
+    // allocation with an inserted dependency on the first stream's work;
+    // opportunistic reuse (a block whose free has already completed, on any
+    // stream) stays on, so handles built and destroyed on any mix of streams
+    // recycle their memory (the pool grew without it)
+    int zero = 0, one = 1;
     cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
-    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &zero);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &one);
   }
   done[dev] = true;
 }
 
+// Optional caller allocator (afn_set_allocator): every device allocation goes
+// through it.  Its frees are deferred until the stream position of the free
+// has completed (an event per block), because a caching allocator returns a
+// block to its pool at call time, not in stream order.
+namespace {
+std::mutex g_alloc_mu;
+afn_alloc_fn g_alloc = nullptr;
+afn_free_fn g_free = nullptr;
+void* g_alloc_ctx = nullptr;
+std::unordered_map<void*, size_t> g_alloc_size;
+struct Deferred {
+  void* p;
+  size_t bytes;
+  cudaStream_t st;
+  cudaEvent_t ev;
+};
+std::vector<Deferred> g_deferred;
+}  // namespace
+
+void release_deferred(bool wait) {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  size_t keep = 0;
+  for (size_t i = 0; i < g_deferred.size(); ++i) {
+    Deferred& f = g_deferred[i];
+    const cudaError_t q = wait ? cudaEventSynchronize(f.ev) : cudaEventQuery(f.ev);
+    if (q == cudaErrorNotReady) {
+      g_deferred[keep++] = f;
+      continue;
+    }
+    cudaGetLastError();
+    cudaEventDestroy(f.ev);
+    if (g_free) g_free(f.p, f.bytes, (void*)f.st, g_alloc_ctx);
+  }
+  g_deferred.resize(keep);
+}
+
 afn_status dalloc(void** p, size_t bytes, cudaStream_t st) {
-  pool_setup_once();
   *p = nullptr;
-  cudaError_t e = cudaMallocAsync(p, bytes > 0 ? bytes : 8, st);
+  const size_t nb = bytes > 0 ? bytes : 8;
+  {
+    std::unique_lock<std::mutex> lk(g_alloc_mu);
+    if (g_alloc) {
+      lk.unlock();
+      release_deferred(false);
+      lk.lock();
+      *p = g_alloc(nb, (void*)st, g_alloc_ctx);
+      if (!*p) {
+        set_error("caller allocator returned NULL for %zu bytes", nb);
+        return AFN_ERR_NOMEM;
+      }
+      g_alloc_size[*p] = nb;
+      return AFN_OK;
+    }
+  }
+  pool_setup_once();
+  cudaError_t e = cudaMallocAsync(p, nb, st);
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("device allocation of %zu bytes failed (%s)", bytes, cudaGetErrorString(e));
@@ -77,7 +134,26 @@ afn_status dalloc(void** p, size_t bytes, cudaStream_t st) {
 }
 
 void dfree(void* p, cudaStream_t st) {
-  if (p) cudaFreeAsync(p, st);
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_alloc_size.find(p);
+    if (it != g_alloc_size.end()) {  // from the caller allocator
+      Deferred f{p, it->second, st, nullptr};
+      g_alloc_size.erase(it);
+      if (cudaEventCreateWithFlags(&f.ev, cudaEventDisableTiming) == cudaSuccess &&
+          cudaEventRecord(f.ev, st) == cudaSuccess) {
+        g_deferred.push_back(f);
+      } else {  // (cannot order it: wait for the stream)
+        cudaGetLastError();
+        if (f.ev) cudaEventDestroy(f.ev);
+        cudaStreamSynchronize(st);
+        if (g_free) g_free(p, f.bytes, (void*)st, g_alloc_ctx);
+      }
+      return;
+    }
+  }
+  cudaFreeAsync(p, st);
 }
 
 // ---- per-kernel timers
@@ -252,16 +328,6 @@ using namespace afn;
 // rank; W holds the rank's own non-landmark rows; the PCG vectors are full
 // length with only the rank's own rows (RankSt::own) computed locally.
 #define AFN_NYS_NU 1e-10  // K11 shift of the Nystrom branch (reading R30)
-// AFN_DEBUG_PHASES=1: synchronise and report after every build phase (debugging)
-#define AFN_PHASE(name)                                                          \
-  do {                                                                           \
-    static const bool dbg_ = getenv("AFN_DEBUG_PHASES") != nullptr;              \
-    if (dbg_) {                                                                  \
-      cudaError_t e_ = cudaStreamSynchronize(st);                                \
-      fprintf(stderr, "afn_build phase %s done (%s)\n", name, cudaGetErrorString(e_)); \
-    }                                                                            \
-  } while (0)
-
 struct RankSt {
   int rank = 0;
   Seg2 own{};
@@ -285,6 +351,7 @@ struct RankSt {
   // workspaces
   KmvPlan plan{};
   double* kmv_part = nullptr;
+  double* qpart = nullptr;  // R x n rank partials of the symmetric matvec (R > 1)
   double* gws = nullptr;    // gemv_t partials
   double* tvec = nullptr;   // k
   double* vvec = nullptr;   // k
@@ -309,6 +376,7 @@ struct RankSt {
 
 struct afn_handle_s {
   int device = 0;
+  cudaStream_t stream = nullptr;  // the build stream (frees are queued on it)
   int64_t n = 0, k = 0, N2 = 0, nnz = 0;
   int d = 0;
   double l = 0, mu = 0;
@@ -334,16 +402,6 @@ cudaStream_t side_stream() {
   if (dev < 0 || dev >= 64) dev = 0;
   if (!ss[dev]) cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking);
   return ss[dev];
-}
-
-// non-blocking stream per device and host thread for the kNN candidate lists
-cudaStream_t cand_stream() {
-  static thread_local cudaStream_t cs[64] = {nullptr};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) dev = 0;
-  if (!cs[dev]) cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking);
-  return cs[dev];
 }
 
 // non-blocking stream per device and host thread for PCG graph capture / replay
@@ -403,13 +461,15 @@ void handle_free(afn_handle h) {
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(h->device);
+  // every stream that may still use the handle's memory (the build stream, its
+  // side streams, the caller's solve streams) is drained first; the blocks then
+  // go back to the pool on the build stream (cudaFree would unmap them and
+  // force the next build to map fresh pages) and are reusable from any stream
   cudaDeviceSynchronize();
-  // return the blocks to the stream-ordered pool (cudaFree would unmap them and
-  // force the next build to map fresh pages); the legacy stream orders the
-  // frees after all prior work on the device's blocking streams
   for (auto& s : h->rk)
-    for (void* p : s.allocs) cudaFreeAsync(p, 0);
-  cudaStreamSynchronize(0);
+    for (void* p : s.allocs) dfree(p, h->stream);
+  cudaStreamSynchronize(h->stream);
+  release_deferred(true);
   cudaSetDevice(cur);
   delete h;
 }
@@ -468,12 +528,45 @@ afn_status reduce_slots(afn_handle h, unsigned mask, cudaStream_t st) {
   return AFN_OK;
 }
 
-// algorithmic flops of one kernel matvec launch: (3d + 19) per evaluated
-// ordered pair; the symmetric plan evaluates each unordered pair
-// once with one more FMA (column sum): (3d + 21) n (n - 1) / 2
+// executed FP64 flops of one rank's kernel matvec launch (kmv.cu kmv_flops:
+// per useful pair, the symmetric plan's units split evenly over the ranks)
 double kmv_work(afn_handle h, int64_t n, int d) {
-  if (h->rk[0].plan.sym) return (double)n * (double)(n - 1) / 2.0 * (3.0 * d + 21.0);
-  return (double)n * (double)n * (3.0 * d + 19.0) / h->R;
+  const RankSt& s = h->rk[0];
+  const double f = kmv_flops(s.plan, n, s.own.size(), d, h->kn.kind);
+  return s.plan.sym ? f / h->R : f;
+}
+
+// q = (K + mu I) v on every local rank's own rows.  One rank with
+// the symmetric plan: one launch (+ v.q into sc[pq_slot]); R > 1 with the
+// symmetric plan: each rank's share of the pair units, an all-gather of the
+// rank partials, the rank-order combine (+ v.q partials); row-wise plan: the
+// rank's rows.  pq_slot < 0: no dot.
+template <class VF, class QF>
+afn_status matvec_perm(afn_handle h, VF v_of, QF q_of, int pq_slot, cudaStream_t st) {
+  const int64_t n = h->n;
+  const int d = h->d;
+  const bool sym = h->rk[0].plan.sym;
+  if (sym && h->R == 1) {
+    RankSt& s = h->rk[0];
+    return kmv_launch(s.Xs, n, d, h->kn.kind, v_of(s), h->mu, s.own, q_of(s), true, s.kmv_part, s.plan, st,
+                      pq_slot >= 0 ? s.sc + pq_slot : nullptr, s.dws, s.dcnt);
+  }
+  if (sym) {
+    for (auto& s : h->rk)
+      TRY(kmv_sym_rank_partial(s.Xs, n, d, h->kn.kind, v_of(s), s.plan, s.kmv_part, s.qpart + (size_t)s.rank * n,
+                               st));
+    TRY(exchange(h, [](RankSt& s) { return s.qpart; },
+                 [&](int r) { return RankRanges{{8 * (size_t)r * n, 8 * (size_t)n}}; }, st));
+    for (auto& s : h->rk)
+      TRY(kmv_sym_combine(s.qpart, h->R, n, s.own, v_of(s), h->mu, q_of(s), st,
+                          pq_slot >= 0 ? part_dst(h, s, pq_slot) : nullptr, s.dws, s.dcnt));
+    return AFN_OK;
+  }
+  for (auto& s : h->rk) {
+    TRY(kmv_launch(s.Xs, n, d, h->kn.kind, v_of(s), h->mu, s.own, q_of(s), true, s.kmv_part, s.plan, st));
+    if (pq_slot >= 0) TRY(dot(v_of(s), q_of(s), s.own, part_dst(h, s, pq_slot), s.dws, s.dcnt, st));
+  }
+  return AFN_OK;
 }
 
 // algorithmic HBM bytes of one apply: W read twice, L^{-T} twice (upper half),
@@ -619,6 +712,10 @@ afn_status apply_ran_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
 
 template <class RF, class ZF>
 afn_status apply_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
+  if (h->method == AFN_METHOD_NONE) {  // M = I: unpreconditioned CG
+    for (auto& s : h->rk) TRY(vec_copy(z_of(s), r_of(s), s.own, st));
+    return AFN_OK;
+  }
   if (h->method == AFN_METHOD_NYSTROM) return apply_nystrom_perm(h, r_of, z_of, st);
   if (h->method == AFN_METHOD_RAN) return apply_ran_perm(h, r_of, z_of, st);
   return apply_afn_perm(h, r_of, z_of, st);
@@ -749,9 +846,9 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   const afn_params P = *prm;
   REQ(P.l > 0 && std::isfinite(P.l), "l must be > 0");
   REQ(P.mu > 0 && std::isfinite(P.mu), "mu must be > 0");
-  REQ(P.method >= AFN_METHOD_AFN && P.method <= AFN_METHOD_RAN, "unknown method %d", P.method);
-  REQ(P.k_cap >= 1 || P.method == AFN_METHOD_FSAI, "k_cap must be >= 1");
-  REQ(P.w >= 1 && P.w <= 128, "w must be in 1..128");
+  REQ(P.method >= AFN_METHOD_AFN && P.method <= AFN_METHOD_NONE, "unknown method %d", P.method);
+  REQ(P.k_cap >= 1 || P.method == AFN_METHOD_FSAI || P.method == AFN_METHOD_NONE, "k_cap must be >= 1");
+  REQ(P.w >= 1 && P.w <= AFN_W_MAX, "w must be in 1..%d", AFN_W_MAX);
   REQ(P.fps_seed >= 0 && P.fps_seed < n, "need 0 <= fps_seed < n");
   REQ(n <= 0x7fffffffLL, "n must fit int32 indices");
   REQ(P.kernel == AFN_KERNEL_GAUSSIAN || P.kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", P.kernel);
@@ -776,6 +873,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
 
   afn_handle h = new afn_handle_s();
   h->device = dev;
+  h->stream = st;
   h->n = n;
   h->d = d;
   h->l = P.l;
@@ -796,41 +894,6 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   } hg{&h};
 
   AFN_CUDA(cudaEventRecord(ev[0], st));
-  AFN_PHASE("ev0");
-  // kNN candidate lists on the original points (one rank, FPS landmarks, index
-  // ordering, brute-force regime): computed while FPS / Alg. 1 run, filtered
-  // once the landmarks are known (knn_from_candidates).  Opt-in (AFN_KNN_CAND=1):
-  // exact, and it takes the kNN off the Cholesky chain (C2: 3.95 -> 2.64 ms),
-  // but the concurrent kNN slows FPS (2.04 -> 3.7 ms) and Alg. 1 (its 200 KB
-  // single-CTA kernels wait for a free SM), a net loss on C2
-  static const bool cand_env = getenv("AFN_KNN_CAND") && atoi(getenv("AFN_KNN_CAND")) == 1;
-  const int cand_kc = std::min(191, P.w - 1 + 40);
-  const bool cand_on = cand_env && h->R == 1 && P.landmarks == AFN_LANDMARKS_FPS && P.ordering == AFN_ORDER_INDEX &&
-                       (P.method == AFN_METHOD_AFN || P.method == AFN_METHOD_ALG2) && P.w > 1 &&
-                       (d != 3 || n < 50000) && d <= 16 && n >= 1024;
-  int32_t* cand = nullptr;
-  unsigned char* lflag_keep = nullptr;  // landmark flags (original order), kept for the filter
-  cudaEvent_t e_cand = nullptr;
-  struct CandFree {
-    int32_t** c;
-    cudaEvent_t* e;
-    cudaStream_t st;
-    ~CandFree() {
-      if (*e) {
-        cudaStreamWaitEvent(st, *e, 0);
-        cudaEventDestroy(*e);
-      }
-      if (*c) dfree(*c, st);
-    }
-  } candfree{&cand, &e_cand, st};
-  if (cand_on) {
-    cudaStream_t cs = cand_stream();
-    AFN_CUDA(cudaEventCreateWithFlags(&e_cand, cudaEventDisableTiming));
-    AFN_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
-    TRY(dalloc((void**)&cand, sizeof(int32_t) * (size_t)n * cand_kc, cs));
-    TRY(knn_candidates(X, n, d, cand_kc, cand, cs));
-    AFN_CUDA(cudaEventRecord(e_cand, cs));
-  }
   // ---- a2: adaptive k (Alg. 1) -- replicated: every rank computes the same k
   const Kern kn = h->kn;
   int64_t k = std::min<int64_t>(P.k_cap, n);
@@ -838,8 +901,9 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   h->method = P.method == AFN_METHOD_NYSTROM ? AFN_METHOD_NYSTROM
               : P.method == AFN_METHOD_FSAI  ? AFN_METHOD_FSAI
               : P.method == AFN_METHOD_RAN   ? AFN_METHOD_RAN
+              : P.method == AFN_METHOD_NONE  ? AFN_METHOD_NONE
                                              : AFN_METHOD_AFN;
-  const bool adaptive = P.k_adaptive && P.method != AFN_METHOD_FSAI;
+  const bool adaptive = P.k_adaptive && P.method != AFN_METHOD_FSAI && P.method != AFN_METHOD_NONE;
   // FPS landmarks are nested (X_{k-1} in X_k): with an adaptive k the
   // FPS for min(k_cap, n) points runs on the build stream WHILE Alg. 1 runs on
   // a side stream; the first k of them are exactly FPS(k).
@@ -880,8 +944,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   if (adaptive) {
     int m = P.m > 0 ? P.m : alg1_default_m(n);
     REQ(m >= 2 && m <= n && m <= 1024, "need 2 <= m <= min(n, 1024)");
-    static const bool serial = getenv("AFN_NO_OVERLAP") != nullptr;
-    cudaStream_t s2 = serial ? st : side_stream();
+    cudaStream_t s2 = side_stream();
     cudaEvent_t a0, a1;
     AFN_CUDA(cudaEventCreate(&a0));
     AFN_CUDA(cudaEventCreate(&a1));
@@ -907,16 +970,18 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     // Algorithm 2: AFN if khat >= 2000, else Nystrom with khat landmarks
     if (P.method == AFN_METHOD_ALG2) h->method = h->a1.khat >= kthr ? AFN_METHOD_AFN : AFN_METHOD_NYSTROM;
   }
-  if (h->method == AFN_METHOD_FSAI) k = 0;  // plain FSAI of K + mu I
+  // plain FSAI of K + mu I, and M = I (CG): no landmarks
+  if (h->method == AFN_METHOD_FSAI || h->method == AFN_METHOD_NONE) k = 0;
   const bool nys = h->method == AFN_METHOD_NYSTROM || h->method == AFN_METHOD_RAN;  // F-form
   h->k = k;
-  const int64_t N2 = nys ? 0 : n - k;  // the Nystrom branch has no Schur complement
+  // the Nystrom branch has no Schur complement, CG no FSAI part
+  const int64_t N2 = (nys || h->method == AFN_METHOD_NONE) ? 0 : n - k;
   h->N2 = N2;
   h->nnz = knn_nnz(N2, P.w);
   for (auto& s : h->rk) {
     s.own = shard_rows(n, k, h->R, s.rank);
-    s.lo = nys ? 0 : s.own.b0 - k;  // own non-landmark rows (W, pattern, G)
-    s.hi = nys ? 0 : s.lo + s.own.nb;
+    s.lo = N2 == 0 ? 0 : s.own.b0 - k;  // own non-landmark rows (W, pattern, G)
+    s.hi = N2 == 0 ? 0 : s.lo + s.own.nb;
   }
 
   // ---- a3: landmarks (replicated): FPS or uniform (R29)
@@ -939,7 +1004,6 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     AFN_CUDA(cudaEventRecord(efps1, st));
   }
   AFN_CUDA(cudaEventRecord(ev[2], st));
-  AFN_PHASE("ev2");
 
   // kNN pattern of the non-landmark points (own rows; row_ptr in closed form),
   // then its transpose (the pair-union FSAI needs "rows containing a")
@@ -948,24 +1012,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_begin(KT_KNN, ss);
     TRY(ralloc(s, &s.rp, (size_t)N2 + 1, ss));
     TRY(ralloc(s, &s.col, (size_t)(h->nnz > 0 ? h->nnz : 1), ss));
-    bool done = false;
-    if (N2 > 0 && cand && lflag_keep && !nys) {  // filter the candidate lists
-      int64_t* inv = nullptr;
-      int* fb = nullptr;
-      TRY(dalloc((void**)&inv, sizeof(int64_t) * (size_t)n + sizeof(int) * 4, ss));
-      fb = reinterpret_cast<int*>(inv + n);
-      AFN_CUDA(cudaStreamWaitEvent(ss, e_cand, 0));
-      TRY(knn_from_candidates(cand, cand_kc, lflag_keep, s.perm, n, k, P.w, s.rp, s.col, inv, fb, ss));
-      int hfb = 0;
-      AFN_CUDA(cudaMemcpyAsync(&hfb, fb, sizeof(int), cudaMemcpyDeviceToHost, ss));
-      AFN_CUDA(cudaStreamSynchronize(ss));
-      dfree(inv, ss);
-      done = hfb == 0;  // else: a list ran short -> the exact kNN below
-    }
-    if (!done) {
-      if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, ss, s.lo, s.hi));
-      else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), ss));
-    }
+    if (N2 > 0) TRY(knn_run(s.Xp + k * d, N2, d, P.w, s.rp, s.col, ss, s.lo, s.hi));
+    else AFN_CUDA(cudaMemsetAsync(s.rp, 0, sizeof(int64_t), ss));
     kt_end(KT_KNN, ss, 0.0);
     return AFN_OK;
   };
@@ -985,8 +1033,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     return AFN_OK;
   };
   // single rank, AFN: the pattern does not depend on L or W -> overlap it
-  static const bool no_ovl = getenv("AFN_NO_OVERLAP") != nullptr;
-  const bool povl = !no_ovl && h->R == 1 && !nys && N2 > 0 && k > 0;
+  const bool povl = h->R == 1 && !nys && N2 > 0 && k > 0;
   cudaEvent_t e_pat0 = nullptr, e_pat1 = nullptr;
   if (povl) {
     AFN_CUDA(cudaEventCreateWithFlags(&e_pat0, cudaEventDisableTiming));
@@ -1020,8 +1067,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       perm_kernel<<<1, 1024, 0, st>>>(flag, idx[q], n, k, s.perm);
       AFN_LAUNCH_CHECK("perm_kernel");
     }
-    if (cand_on) lflag_keep = flag;  // (the landmark flags feed the kNN filter)
-    else rfree(s, flag, st);
+    rfree(s, flag, st);
     rfree(s, flag32, st);
     TRY(ralloc(s, &s.Xp, (size_t)n * d, st));
     TRY(gather_rows(X, n, d, s.perm, s.Xp, st));
@@ -1053,7 +1099,6 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_end(KT_LINV, st, (double)k * k * k / 3.0);
   }
   AFN_CUDA(cudaEventRecord(ev[3], st));
-  AFN_PHASE("ev3");
   auto chol_check = [&]() -> afn_status {
     for (auto& s : h->rk) {
       int info = 0;
@@ -1071,34 +1116,24 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   if (nys) {
     TRY(build_nystrom(h, st));
     AFN_CUDA(cudaEventRecord(ev[4], st));
-    AFN_PHASE("ev4");
     AFN_CUDA(cudaEventRecord(ev[5], st));
-    AFN_PHASE("ev5");
     AFN_CUDA(cudaEventRecord(ev[6], st));
-    AFN_PHASE("ev6");
     AFN_CUDA(cudaEventRecord(ev[7], st));
-    AFN_PHASE("ev7");
     AFN_CUDA(cudaEventRecord(ev[8], st));
-    AFN_PHASE("ev8");
   } else {
 
   // ---- a5: W = K21 L^{-T}, own rows (into a full-height buffer when sharded:
   // the FSAI rows of a rank need the W rows of all their pattern neighbours)
   std::vector<double*> Wf(nlocal);
-  static const bool w_trsm = getenv("AFN_W_TRSM") != nullptr;
   kt_begin(KT_W_GEMM, st);
   for (int q = 0; q < nlocal; ++q) {
     RankSt& s = h->rk[q];
     TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
     const double* X2 = s.Xp + k * d;
-    if (s.hi > s.lo) {
-      if (w_trsm) TRY(trsm_w(s.L, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
-      else TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
-    }
+    if (s.hi > s.lo) TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
   }
   kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k / h->R);  // (N2/R) k^2/2 FMA per rank
   AFN_CUDA(cudaEventRecord(ev[4], st));
-  AFN_PHASE("ev4");
 
   // ---- a6: kNN pattern (already queued on the side stream when povl)
   if (povl) {
@@ -1107,7 +1142,6 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     for (auto& s : h->rk) TRY(pattern_phase(s, st));
   }
   AFN_CUDA(cudaEventRecord(ev[5], st));
-  AFN_PHASE("ev5");
   if (N2 > 0 && !povl) {
     // exchange W rows and pattern rows
     {
@@ -1122,24 +1156,19 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
   }
   AFN_CUDA(cudaEventRecord(ev[6], st));
-  AFN_PHASE("ev6");
 
   // ---- a7: FSAI rows (own), then G^T
   if (!povl)
     for (int q = 0; q < nlocal; ++q) TRY(transpose_phase(h->rk[q], q, st));
   AFN_CUDA(cudaEventRecord(ev[7], st));
-  AFN_PHASE("ev7");
   if (N2 > 0) {
-    static const int variant = getenv("AFN_FSAI_VARIANT") ? atoi(getenv("AFN_FSAI_VARIANT")) : -1;
     for (int q = 0; q < nlocal; ++q) {
       RankSt& s = h->rk[q];
       const double* X2 = s.Xp + k * d;
-      afn_status fs = AFN_ERR_STATE;
-      if (variant < 0) {
-        fs = fsai_sddmm_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo, s.hi,
-                            s.gval, s.dinfo + 1, st, povl ? side_stream() : st);
-        if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
-      }
+      // (the pair-union product; AFN_ERR_STATE: a group's union overflowed -> per-row Grams)
+      const afn_status fs = fsai_sddmm_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo,
+                                           s.hi, s.gval, s.dinfo + 1, st, povl ? side_stream() : st);
+      if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
       if (fs != AFN_OK) {
         kt_begin(KT_FSAI_GRAM, st);
         TRY(fsai_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.lo, s.hi, s.gval, s.dinfo + 1, st));
@@ -1148,7 +1177,6 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
   }
   AFN_CUDA(cudaEventRecord(ev[8], st));
-  AFN_PHASE("ev8");
   // (AFN, one rank: the Cholesky breakdown check waits until here so that the
   // host has queued W and the FSAI work first -- a failed Cholesky only makes
   // the queued work useless, it is reported before anything is used)
@@ -1180,8 +1208,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   // ---- workspaces for apply / PCG
   for (auto& s : h->rk) {
     const int64_t nl = s.own.size();
-    s.plan = kmv_plan(n, nl, d, num_sms(), h->R == 1);
+    s.plan = kmv_plan(n, nl, d, num_sms(), true, h->R, s.rank);
     TRY(ralloc(s, &s.kmv_part, (size_t)std::max<int64_t>(1, s.plan.ws), st));
+    TRY(kmv_plan_init(s.plan, s.kmv_part, st));
+    if (s.plan.sym && h->R > 1) TRY(ralloc(s, &s.qpart, (size_t)h->R * n, st));
     const int64_t gw = std::max(std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k)),
                                 nys ? gemv_t_ws(nl, k) : (int64_t)1);
     TRY(ralloc(s, &s.gws, (size_t)gw, st));
@@ -1209,19 +1239,35 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     return AFN_ERR_NOMEM;
   }
   AFN_CUDA(cudaEventRecord(ev[9], st));
-  AFN_PHASE("ev9");
-  AFN_CUDA(cudaStreamSynchronize(st));
-  for (auto& s : h->rk) {
-    int e = 0;
-    AFN_CUDA(cudaMemcpy(&e, s.derr, sizeof(int), cudaMemcpyDeviceToHost));
-    if (e) {
-      set_error("internal consistency check failed (code %d: 1/2 landmark ids, 4/8 pattern)", e);
+  // device-side checks of every rank (consistency codes, FSAI breakdown on
+  // the rank's own rows), all-gathered so that every rank returns the same
+  // status (no rank may fail alone and leave the others in a collective)
+  std::vector<int> stat(2 * (size_t)h->R, 0);
+  {
+    std::vector<int*> sb(nlocal);
+    for (int q = 0; q < nlocal; ++q) {
+      RankSt& s = h->rk[q];
+      TRY(ralloc(s, &sb[q], 2 * (size_t)h->R, st));
+      AFN_CUDA(cudaMemsetAsync(sb[q], 0, sizeof(int) * 2 * h->R, st));
+      AFN_CUDA(cudaMemcpyAsync(sb[q] + 2 * s.rank, s.derr, sizeof(int), cudaMemcpyDeviceToDevice, st));
+      AFN_CUDA(cudaMemcpyAsync(sb[q] + 2 * s.rank + 1, s.dinfo + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    }
+    int q2 = 0;
+    TRY(exchange(h, [&](RankSt&) { return sb[q2++]; }, [&](int r) { return RankRanges{{8 * (size_t)r, 8}}; },
+                 st));
+    AFN_CUDA(cudaMemcpyAsync(stat.data(), sb[0], sizeof(int) * 2 * h->R, cudaMemcpyDeviceToHost, st));
+  }
+  TRY(comm_stream_sync(h->comm, st));
+  for (int r = 0; r < h->R; ++r) {
+    if (stat[2 * r]) {
+      set_error("internal consistency check failed on rank %d (code %d: 1/2 landmark ids, 4/8 pattern)", r,
+                stat[2 * r]);
       return AFN_ERR_CUDA;
     }
-    int info = 0;
-    AFN_CUDA(cudaMemcpy(&info, s.dinfo + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    if (info && !getenv("AFN_DEBUG_ALLOW_NOT_SPD")) {
-      set_error("FSAI block Cholesky broke down in row %d", info - 1);
+  }
+  for (int r = 0; r < h->R; ++r) {
+    if (stat[2 * r + 1]) {
+      set_error("FSAI block Cholesky broke down in row %d (rank %d)", stat[2 * r + 1] - 1, r);
       return AFN_ERR_NOT_SPD;
     }
   }
@@ -1245,6 +1291,33 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
 extern "C" {
 
 int32_t afn_abi_version(void) { return AFN_ABI_VERSION; }
+
+afn_status afn_set_allocator(afn_alloc_fn alloc, afn_free_fn free_fn, void* ctx) {
+  REQ((alloc == nullptr) == (free_fn == nullptr), "alloc and free must both be set or both be NULL");
+  release_deferred(true);
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  REQ(g_alloc_size.empty(), "%zu blocks from the current allocator are still live (destroy the handles first)",
+      g_alloc_size.size());
+  g_alloc = alloc;
+  g_free = free_fn;
+  g_alloc_ctx = ctx;
+  return AFN_OK;
+}
+
+afn_status afn_pool_stats(int64_t* reserved, int64_t* used) {
+  REQ(reserved && used, "null argument");
+  int dev = 0;
+  AFN_CUDA(cudaGetDevice(&dev));
+  pool_setup_once();
+  cudaMemPool_t pool;
+  AFN_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t r = 0, u = 0;
+  AFN_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &r));
+  AFN_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &u));
+  *reserved = (int64_t)r;
+  *used = (int64_t)u;
+  return AFN_OK;
+}
 
 void afn_kt_enable(int32_t on) {
   kt_collect();
@@ -1282,9 +1355,10 @@ afn_status kmv_rows_impl(const double* X, int64_t n, int32_t d, int32_t kernel, 
   double* Xs;
   TRY(t.get(&Xs, (size_t)n * d));
   TRY(kmv_prescale(X, n, d, Kern{kernel, l}, Xs, st));
-  KmvPlan plan = kmv_plan(n, nrows, d, num_sms(), sym_ok);
+  KmvPlan plan = kmv_plan(n, nrows, d, num_sms(), sym_ok && row0 == 0 && nrows == n);
   double* part;
   TRY(t.get(&part, (size_t)std::max<int64_t>(1, plan.ws)));
+  TRY(kmv_plan_init(plan, part, st));
   TRY(kmv_launch(Xs, n, d, kernel, v, mu, seg_range(row0, nrows), y, false, part, plan, st));
   return AFN_OK;
 }
@@ -1320,7 +1394,7 @@ afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t see
 afn_status afn_knn_pattern(const double* P, int64_t N, int32_t d, int32_t w, int64_t* row_ptr,
                            int32_t* col, void* stream) {
   TRY(validate_X(P, N, d));
-  REQ(w >= 1 && w <= 128, "w must be in 1..128");
+  REQ(w >= 1 && w <= AFN_W_MAX, "w must be in 1..%d", AFN_W_MAX);
   REQ(N <= 0x7fffffffLL, "N must fit int32 column indices");
   REQ(is_dev(row_ptr) && is_dev(col), "row_ptr, col must be device pointers");
   return knn_run(P, N, d, w, row_ptr, col, (cudaStream_t)stream);
@@ -1352,6 +1426,17 @@ afn_status afn_build(const double* X, int64_t n, int32_t d, const afn_params* pr
 afn_status afn_build_dist(afn_comm comm, const double* X, int64_t n, int32_t d, const afn_params* prm,
                           void* stream, afn_handle* out) {
   return build_impl(comm, X, n, d, prm, stream, out);
+}
+
+afn_status afn_matvec(afn_handle h, const double* v, double* y, void* stream) {
+  REQ(h != nullptr, "null handle");
+  REQ(is_dev(v) && is_dev(y) && v != y, "v, y must be distinct device pointers");
+  cudaStream_t st = (cudaStream_t)stream;
+  for (auto& s : h->rk) TRY(gather_vec(v, s.perm, h->n, s.rbuf, st));
+  TRY(matvec_perm(h, [](RankSt& s) { return s.rbuf; }, [](RankSt& s) { return s.zbuf; }, -1, st));
+  TRY(exchange(h, [](RankSt& s) { return s.zbuf; }, [&](int s) { return vec_ranges(h, s); }, st));
+  TRY(scatter_vec(h->rk[0].zbuf, h->rk[0].perm, h->n, y, st));
+  return AFN_OK;
 }
 
 afn_status afn_apply(afn_handle h, const double* r, double* z, void* stream) {
@@ -1396,7 +1481,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   int napply = 0;
   auto sc_to_host = [&]() -> afn_status {
     AFN_CUDA(cudaMemcpyAsync(hsc, h->rk[0].sc, sizeof(double) * SC_N, cudaMemcpyDeviceToHost, st));
-    AFN_CUDA(cudaStreamSynchronize(st));
+    TRY(comm_stream_sync(h->comm, st));
     return AFN_OK;
   };
   auto apply = [&]() -> afn_status {
@@ -1423,7 +1508,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     // iterations after the stop return at once (skip flag sc[SC_DONE]), x and
     // r stay at the stopping iterate.  One host round trip per chunk instead
     // of one per iteration.
-    static const int PCG_CHUNK = getenv("AFN_PCG_CHUNK") ? std::max(1, atoi(getenv("AFN_PCG_CHUNK"))) : 8;
+    constexpr int PCG_CHUNK = 8;
     double* dhist = nullptr;
     TRY(dalloc((void**)&dhist, sizeof(double) * ((size_t)maxit + 1), st));
     struct HFree {
@@ -1457,8 +1542,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
     int kmv_seen = 0;  // host-loop iterations queued so far (index into kmE / apE)
     // ... and a CUDA graph of PCG_CHUNK iterations (one rank): captured once per
     // solve, replayed per chunk (the iteration number lives on the device);
-    // its event nodes are read after each replay.  AFN_PCG_GRAPH=0 disables.
-    static const bool use_graph = !(getenv("AFN_PCG_GRAPH") && atoi(getenv("AFN_PCG_GRAPH")) == 0);
+    // its event nodes are read after each replay.
     cudaGraphExec_t gexec = nullptr;
     int64_t glaunches = 0;
     std::vector<cudaEvent_t> gE;
@@ -1490,9 +1574,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
       // the stopping test fused into the x/r update
       const bool fused = h->R == 1 && h->rk[0].plan.sym;
       if (kt) kt_begin(KT_KMV, st);
-      for (auto& s : h->rk)
-        TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.p, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st,
-                       fused ? s.sc + SC_PQ : nullptr, s.dws, s.dcnt));
+      TRY(matvec_perm(h, [](RankSt& s) { return s.p; }, [](RankSt& s) { return s.q; }, SC_PQ, st));
       if (kt) kt_end(KT_KMV, st, kmv_work(h, n, d));
       AFN_CUDA(cudaEventRecordWithFlags(ek1, st, ef));
       if (fused) {
@@ -1500,7 +1582,6 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
         TRY(pcg_update_xr_check(s.x, s.r, s.p, s.q, s.own, s.sc, cur, s.dws, s.dcnt, nb, tol, maxit, fixed_iters,
                                 dhist, st));
       } else {
-        for (auto& s : h->rk) TRY(dot(s.p, s.q, s.own, part_dst(h, s, SC_PQ), s.dws, s.dcnt, st));
         TRY(reduce_slots(h, 1u << SC_PQ, st));
         for (auto& s : h->rk)
           TRY(pcg_update_xr(s.x, s.r, s.p, s.q, s.own, s.sc, cur, part_dst(h, s, SC_RR), s.dws, s.dcnt, st));
@@ -1525,7 +1606,7 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
       struct SkipOff {
         ~SkipOff() { set_skip(nullptr); }
       } skipoff;
-      const bool graph = use_graph && h->R == 1 && chunk == PCG_CHUNK && upto - queued == PCG_CHUNK &&
+      const bool graph = h->R == 1 && chunk == PCG_CHUNK && upto - queued == PCG_CHUNK &&
                          (PCG_CHUNK & 1) == 0;
       if (graph) {
         // capture / replay on a private non-blocking stream (the caller's
@@ -1648,8 +1729,8 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   TRY(scatter_vec(h->rk[0].x, h->rk[0].perm, n, a, st));
   AFN_CUDA(cudaEventRecord(e1, st));
   if (nb > 0) {
+    TRY(matvec_perm(h, [](RankSt& s) { return s.x; }, [](RankSt& s) { return s.q; }, -1, st));
     for (auto& s : h->rk) {
-      TRY(kmv_launch(s.Xs, n, d, h->kn.kind, s.x, h->mu, s.own, s.q, true, s.kmv_part, s.plan, st));
       TRY(gather_vec(b, s.perm, n, s.z, st));
       TRY(vec_axpby(s.z, -1.0, s.q, 1.0, s.own, st));
       TRY(dot(s.z, s.z, s.own, part_dst(h, s, SC_TMP), s.dws, s.dcnt, st));
@@ -1670,7 +1751,24 @@ afn_status afn_pcg_solve(afn_handle h, const double* b, double* a, double tol, i
   return AFN_OK;
 }
 
-afn_status afn_solve_host(const double* X, const double* b, double* a, int64_t n, int32_t d,
+afn_status afn_cg_solve(afn_comm comm, const double* X, int64_t n, int32_t d, int32_t kernel, double l,
+                        double mu, const double* b, double* a, double tol, int32_t maxit, int32_t fixed_iters,
+                        afn_solve_report* rep, void* stream) {
+  afn_params P{};
+  P.l = l;
+  P.mu = mu;
+  P.k_cap = 1;
+  P.w = 1;
+  P.kernel = kernel;
+  P.method = AFN_METHOD_NONE;
+  afn_handle h = nullptr;
+  TRY(build_impl(comm, X, n, d, &P, stream, &h));
+  const afn_status s = afn_pcg_solve(h, b, a, tol, maxit, fixed_iters, rep, stream);
+  afn_destroy(h);
+  return s;
+}
+
+afn_status afn_solve_host(afn_comm comm, const double* X, const double* b, double* a, int64_t n, int32_t d,
                           const afn_params* params, double tol, int32_t maxit, afn_info* info,
                           afn_solve_report* rep, void* stream) {
   REQ(X && b && a && params, "X, b, a, params must be non-null host pointers");
@@ -1684,7 +1782,7 @@ afn_status afn_solve_host(const double* X, const double* b, double* a, int64_t n
   AFN_CUDA(cudaMemcpyAsync(dX, X, sizeof(double) * n * d, cudaMemcpyHostToDevice, st));
   AFN_CUDA(cudaMemcpyAsync(db, b, sizeof(double) * n, cudaMemcpyHostToDevice, st));
   afn_handle h = nullptr;
-  TRY(afn_build(dX, n, d, params, stream, &h));
+  TRY(build_impl(comm, dX, n, d, params, stream, &h));
   afn_status s = afn_pcg_solve(h, db, da, tol, maxit, 0, rep, stream);
   if (s == AFN_OK && info) s = afn_get_info(h, info);
   if (s == AFN_OK) {

@@ -175,6 +175,12 @@ afn_status cuda_status(cudaError_t e, const char* what);
     if (e_ != cudaSuccess) return afn::cuda_status(e_, #call);               \
   } while (0)
 
+#define TRY_STATUS(x)                                                        \
+  do {                                                                       \
+    afn_status s_ = (x);                                                     \
+    if (s_ != AFN_OK) return s_;                                             \
+  } while (0)
+
 #define AFN_LAUNCH_CHECK(what)                                               \
   do {                                                                       \
     cudaError_t e_ = cudaGetLastError();                                     \

@@ -16,7 +16,10 @@ struct afn_comm_s {
   int nlocal = 1;
   int rank0 = 0;
   bool emulated = false;
-  void* nccl = nullptr;  // ncclComm_t
+  void* nccl = nullptr;    // ncclComm_t (nullptr after an abort)
+  void* stage = nullptr;   // packed all-gather staging buffer (device)
+  size_t stage_bytes = 0;
+  double timeout_s = 600.0;  // host waits on NCCL work (afn_comm_set_timeout)
 };
 
 namespace afn {
@@ -54,6 +57,9 @@ using RankRanges = std::vector<std::pair<size_t, size_t>>;
 // every local rank's buffer bufs[q] receives all ranks' owned ranges
 afn_status comm_allgatherv(const Comm* c, char* const* bufs, const std::vector<RankRanges>& owned,
                            cudaStream_t st);
+// host wait for `st`; with NCCL: polls ncclCommGetAsyncError, aborts the
+// communicator on an error or after c->timeout_s (AFN_ERR_NCCL)
+afn_status comm_stream_sync(const Comm* c, cudaStream_t st);
 
 int num_sms();  // SM count of the current device (cached per device)
 
@@ -66,21 +72,44 @@ void kt_end(int id, cudaStream_t st, double work);  // work: algorithmic flops (
 void kt_collect();                                  // after a stream sync
 
 // Stream-ordered device allocation helpers (cudaMallocAsync pool).
+// (with a caller allocator set: dalloc calls it; dfree defers the caller's
+// free until the stream position of the free completes -- release_deferred
+// hands back the completed ones, all of them with wait = true)
 afn_status dalloc(void** p, size_t bytes, cudaStream_t st);
 void dfree(void* p, cudaStream_t st);
+void release_deferred(bool wait);
 
 // ---- kernel matvec (kmv.cu) ----------------------------------------------
 struct KmvPlan {
   int64_t row_tiles = 0, chunks = 1, chunk_cols = 0;
-  // symmetric full matvec (each unordered pair once, row and column sums):
-  // row blocks of sym_rbw rows x column chunks of sym_cw (sym_rbw = m sym_cw)
+  // symmetric full matvec (each unordered pair once, row and column sums,
+  // kmv.cu): row blocks of sym_rbw rows, 32-column tiles, sym_units work
+  // units split evenly over sym_gt = sym_R x sym_grid CTAs; this rank runs
+  // CTAs [sym_rank sym_grid, (sym_rank + 1) sym_grid)
   bool sym = false;
-  int64_t sym_rbw = 0, sym_cw = 0, sym_nc = 0, sym_nrb = 0, sym_items = 0;
+  int64_t sym_rbw = 0, sym_nrb = 0, sym_nt = 0, sym_units = 0, sym_grid = 0, sym_gt = 0, sym_tab_dbl = 0;
+  int sym_R = 1, sym_rank = 0;
   int64_t ws = 0;  // workspace doubles for kmv_launch
 };
-// sym_ok: a full matvec (nrows == n) may use the symmetric kernel (its row
-// sums differ from a row shard's by rounding; kernel_matvec_rows never uses it)
-KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok = false);
+// sym_ok: a full matvec may use the symmetric kernel (its row sums differ from
+// a row shard's by rounding; kernel_matvec_rows never uses it).  With R > 1
+// ranks the symmetric plan splits the pair units over the ranks
+// (kmv_sym_rank_partial + an exchange + kmv_sym_combine).
+KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok = false, int R = 1, int rank = 0);
+// upload the plan's tables into its workspace and fill the exp2 tables (once
+// per device); call before the first launch with this workspace (not inside
+// a stream capture)
+afn_status kmv_plan_init(const KmvPlan& p, double* ws, cudaStream_t st);
+// executed FP64 flops (FMA = 2) and FP64-pipe thread instructions of one
+// launch, counted per useful pair
+double kmv_flops(const KmvPlan& p, int64_t n, int64_t nrows, int d, int kind);
+double kmv_fp64_inst(const KmvPlan& p, int64_t n, int64_t nrows, int d, int kind);
+// this rank's partial of the symmetric product (all n rows, no mu term): qout[n]
+afn_status kmv_sym_rank_partial(const double* Xs, int64_t n, int d, int kind, const double* v, const KmvPlan& p,
+                                double* ws, double* qout, cudaStream_t st);
+// y_i = (1 + mu) v_i + sum_s qpart[s n + i] (rank order) over the rows g; dout: v . y over g
+afn_status kmv_sym_combine(const double* qpart, int R, int64_t n, Seg2 g, const double* v, double mu, double* y,
+                           cudaStream_t st, double* dout = nullptr, double* dws = nullptr, unsigned* dcnt = nullptr);
 // Xs = X * sqrt(log2 e)/l   (n x d)
 afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, cudaStream_t st);
 // rows `rows` of (K + mu I) v (v: all n entries); partial: chunks*rows.size() doubles.
@@ -99,15 +128,6 @@ afn_status fps_run(const double* X, int64_t n, int d, int64_t k, int64_t seed, i
 // ---- kNN pattern (knn.cu) -------------------------------------------------
 int64_t knn_nnz(int64_t N, int w);
 // row_ptr for all N rows (closed form); col for rows [row_lo, row_hi) (default: all)
-// Candidate lists: for every point i of X (original order), its min(KC, i)
-// nearest earlier points (j < i) in (d2, j) order, cand[i KC + t].
-afn_status knn_candidates(const double* X, int64_t n, int d, int KC, int32_t* cand, cudaStream_t st);
-// The kNN pattern of the non-landmark points (perm = [landmarks; the rest in
-// ascending original order]) from the candidate lists: drop landmarks (lflag),
-// map to permuted positions; *fallback = 1 if a list ran short (then call knn_run).
-afn_status knn_from_candidates(const int32_t* cand, int KC, const unsigned char* lflag, const int64_t* perm,
-                               int64_t n, int64_t k, int w, int64_t* row_ptr, int32_t* col, int64_t* inv_ws,
-                               int* fallback, cudaStream_t st);
 afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, int32_t* col,
                    cudaStream_t st, int64_t row_lo = 0, int64_t row_hi = -1);
 
@@ -121,9 +141,6 @@ afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, doubl
 // in-place lower Cholesky of the k x k row-major A (upper triangle zeroed);
 // *d_info = 0 on success, else 1 + the failing row.
 afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st);
-// W (N x k row-major) = K(Xr, X1) L^{-T}  (i.e. L W^T = K12), K tiles on the fly
-afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
-                  Kern kn, double* W, cudaStream_t st);
 // W (N x k) = K(Xr, X1) L^{-T} as a GEMM with the explicit L^{-T}
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st);

@@ -174,9 +174,8 @@ __device__ double block_sum_all(double v, double* sh) {  // every thread gets th
 }
 
 constexpr int SM_MAX_M = 164;  // (m^2 + 2m) doubles of dynamic smem <= 227 KB
-#ifndef AFN_TRIDIAG_COLS
-#define AFN_TRIDIAG_COLS 1  // p = A v by columns with row slices (0: warp per row)
-#endif
+// shared-memory path (m <= SM_MAX_M): p = A v by columns with row slices;
+// global-memory path: warp per row
 template <bool SM, int TT>
 __global__ void __launch_bounds__(TT) tridiag_kernel(double* Ag, int m, double* dgl, double* off) {
   extern __shared__ double dsm[];
@@ -220,7 +219,7 @@ __global__ void __launch_bounds__(TT) tridiag_kernel(double* Ag, int m, double* 
     const double beta = s_beta;
     if (beta == 0.0) continue;
     double loc2 = 0.0;
-    if (SM && AFN_TRIDIAG_COLS) {
+    if (SM) {
       // p = beta * A22 v by columns (A symmetric): thread (s, i) sums column
       // i over the rows t = s, s + S, ..  (consecutive threads read consecutive
       // words of a row: no bank conflicts, v[t] broadcast), then thread i adds
@@ -262,7 +261,7 @@ __global__ void __launch_bounds__(TT) tridiag_kernel(double* Ag, int m, double* 
     }
     const double pv = block_sum_all<TT>(loc2, sh);
     const double K = 0.5 * beta * pv;
-    if (SM && AFN_TRIDIAG_COLS) {
+    if (SM) {
       // A22 -= v w^T + w v^T with w = p - K v formed in registers (no pass over
       // p, no barrier); each lane keeps its <= 6 columns' v_t, w_t for all its
       // rows, and a row's loads are issued before its stores
@@ -420,24 +419,14 @@ __global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict
   } while (0)
 
 afn_status launch_tridiag(double* A, int m, double* dgl, double* off, cudaStream_t st) {
-  // AFN_TRIDIAG_T: threads of the single CTA (1024 default: 0.75 ms at m = 163; 256: 1.14 ms)
-  static const int tt = getenv("AFN_TRIDIAG_T") ? atoi(getenv("AFN_TRIDIAG_T")) : 1024;
+  // one CTA of 1024 threads (0.75 ms at m = 163; 512 and 256 threads measured slower: 256 1.14 ms)
   if (m <= SM_MAX_M) {
     // (+ the column partials of p: <= 1024 doubles; 164^2 + 2 164 + 1024 doubles <= 227 KB)
-    const size_t bytes = sizeof(double) * ((size_t)m * m + 2 * (size_t)m + (AFN_TRIDIAG_COLS ? 1024 : 0));
-    if (tt == 1024) {
-      AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      tridiag_kernel<true, 1024><<<1, 1024, bytes, st>>>(A, m, dgl, off);
-    } else if (tt == 512) {
-      AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      tridiag_kernel<true, 512><<<1, 512, bytes, st>>>(A, m, dgl, off);
-    } else {
-      AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      tridiag_kernel<true, 256><<<1, 256, bytes, st>>>(A, m, dgl, off);
-    }
+    const size_t bytes = sizeof(double) * ((size_t)m * m + 2 * (size_t)m + 1024);
+    AFN_CUDA(cudaFuncSetAttribute(tridiag_kernel<true, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    tridiag_kernel<true, 1024><<<1, 1024, bytes, st>>>(A, m, dgl, off);
   } else {
-    if (tt == 1024) tridiag_kernel<false, 1024><<<1, 1024, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
-    else tridiag_kernel<false, 256><<<1, 256, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
+    tridiag_kernel<false, 1024><<<1, 1024, sizeof(double) * 2 * (size_t)m, st>>>(A, m, dgl, off);
   }
   AFN_LAUNCH_CHECK("tridiag_kernel");
   return AFN_OK;
@@ -583,8 +572,7 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   // (needed by the Schur tests), then -- speculatively, it only matters when
   // khat < k_threshold -- the eigen-summary of the unscaled K_m for the
   // refinement.  The main stream computes ||K_m||_2 meanwhile.
-  static const bool a1_serial = getenv("AFN_ALG1_SERIAL") != nullptr;
-  cudaStream_t s3 = a1_serial ? st : alg1_stream();
+  cudaStream_t s3 = alg1_stream();
   cudaEvent_t eA = nullptr, eP = nullptr, eR = nullptr;
   AFN_CUDA(cudaEventCreateWithFlags(&eA, cudaEventDisableTiming));
   AFN_CUDA(cudaEventCreateWithFlags(&eP, cudaEventDisableTiming));

@@ -6,10 +6,16 @@
 // sharded build steps).
 //
 // Two transports behind one call:
-//   * NCCL (one process per GPU): every rank's ranges are broadcast from
-//     their owner inside one ncclGroupStart/End, in place, on the caller's
-//     stream.  libnccl.so.2 is dlopen'ed (the copy PyTorch already loaded),
-//     so libafn.so itself has no link-time NCCL dependency.
+//   * NCCL (one process per GPU): ncclAllGather on the caller's stream --
+//     in place when every rank owns one equal-size range at offset s * len
+//     (the per-rank partials: dot products, the k-vector of W^T s2, the
+//     symmetric matvec's rank partials), otherwise through a packed staging
+//     buffer (each rank's <= 2 row segments packed to a fixed stride,
+//     gathered, unpacked: the PCG vector p, u, G u and the build's W /
+//     pattern / G rows).  libnccl.so.2 is dlopen'ed (the copy PyTorch
+//     already loaded), so libafn.so itself has no link-time NCCL dependency.
+//     Host waits on a stream with NCCL work poll ncclCommGetAsyncError and
+//     abort the communicator on an error or after the timeout.
 //   * emulated (tests): R logical ranks driven by ONE process on ONE device,
 //     each with its own buffers; the exchange is a device-to-device copy of
 //     every owner's ranges into every other rank's buffer on the same stream.
@@ -17,7 +23,10 @@
 //     enqueued before the copies), so this is safe on a single GPU.
 #include <dlfcn.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "afn_common.cuh"
@@ -32,11 +41,12 @@ struct NcclApi {
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 NcclApi& nccl_api(const char* path) {
@@ -50,14 +60,15 @@ NcclApi& nccl_api(const char* path) {
   AFN_SYM(GetUniqueId, "ncclGetUniqueId");
   AFN_SYM(CommInitRank, "ncclCommInitRank");
   AFN_SYM(CommDestroy, "ncclCommDestroy");
-  AFN_SYM(Broadcast, "ncclBroadcast");
   AFN_SYM(GroupStart, "ncclGroupStart");
   AFN_SYM(GroupEnd, "ncclGroupEnd");
   AFN_SYM(GetErrorString, "ncclGetErrorString");
   AFN_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+  AFN_SYM(CommAbort, "ncclCommAbort");
+  AFN_SYM(AllGather, "ncclAllGather");
 #undef AFN_SYM
-  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.Broadcast && api.GroupStart &&
-           api.GroupEnd && api.GetErrorString;
+  api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.GroupStart &&
+           api.GroupEnd && api.GetErrorString && api.CommGetAsyncError && api.CommAbort;
   return api;
 }
 
@@ -85,20 +96,91 @@ afn_status comm_allgatherv(const Comm* c, char* const* bufs, const std::vector<R
   }
   NcclApi& a = nccl_api(nullptr);
   ncclComm_t comm = static_cast<ncclComm_t>(c->nccl);
-  ncclResult_t r = a.GroupStart();
-  if (r != ncclSuccess) return nccl_status(r, "ncclGroupStart");
-  for (int s = 0; s < c->R; ++s)
-    for (const auto& rg : owned[s]) {
-      if (rg.second == 0) continue;
-      r = a.Broadcast(bufs[0] + rg.first, bufs[0] + rg.first, rg.second, ncclUint8, s, comm, st);
-      if (r != ncclSuccess) {
-        a.GroupEnd();
-        return nccl_status(r, "ncclBroadcast");
-      }
+  const int R = c->R, me = c->rank0;
+  // in place: rank s owns exactly [base + s len, base + (s + 1) len)
+  bool inplace = true;
+  size_t len = 0, base = 0;
+  for (int s = 0; s < R && inplace; ++s) {
+    if (owned[s].size() != 1) { inplace = false; break; }
+    if (s == 0) { len = owned[0][0].second; base = owned[0][0].first; }
+    inplace = owned[s][0].second == len && owned[s][0].first == base + (size_t)s * len;
+  }
+  if (inplace) {
+    if (len == 0) return AFN_OK;
+    const ncclResult_t r = a.AllGather(bufs[0] + base + (size_t)me * len, bufs[0] + base, len, ncclUint8, comm, st);
+    if (r != ncclSuccess) return nccl_status(r, "ncclAllGather");
+    return AFN_OK;
+  }
+  // packed: every rank's ranges at a fixed stride (the largest rank's bytes)
+  size_t stride = 0;
+  for (int s = 0; s < R; ++s) {
+    size_t t = 0;
+    for (const auto& rg : owned[s]) t += rg.second;
+    stride = std::max(stride, t);
+  }
+  if (stride == 0) return AFN_OK;
+  stride = (stride + 255) & ~(size_t)255;
+  Comm* cm = const_cast<Comm*>(c);
+  if (cm->stage_bytes < stride * R) {
+    if (cm->stage) {
+      AFN_CUDA(cudaStreamSynchronize(st));
+      cudaFree(cm->stage);
+      cm->stage = nullptr;
+      cm->stage_bytes = 0;
     }
-  r = a.GroupEnd();
-  if (r != ncclSuccess) return nccl_status(r, "ncclGroupEnd");
+    AFN_CUDA(cudaMalloc(&cm->stage, stride * R));
+    cm->stage_bytes = stride * R;
+  }
+  char* stage = static_cast<char*>(cm->stage);
+  size_t o = 0;
+  for (const auto& rg : owned[me]) {  // pack my ranges
+    if (rg.second > 0)
+      AFN_CUDA(cudaMemcpyAsync(stage + (size_t)me * stride + o, bufs[0] + rg.first, rg.second,
+                               cudaMemcpyDeviceToDevice, st));
+    o += rg.second;
+  }
+  const ncclResult_t r = a.AllGather(stage + (size_t)me * stride, stage, stride, ncclUint8, comm, st);
+  if (r != ncclSuccess) return nccl_status(r, "ncclAllGather");
+  for (int s = 0; s < R; ++s) {  // unpack the others' ranges
+    if (s == me) continue;
+    size_t os = 0;
+    for (const auto& rg : owned[s]) {
+      if (rg.second > 0)
+        AFN_CUDA(cudaMemcpyAsync(bufs[0] + rg.first, stage + (size_t)s * stride + os, rg.second,
+                                 cudaMemcpyDeviceToDevice, st));
+      os += rg.second;
+    }
+  }
   return AFN_OK;
+}
+
+afn_status comm_stream_sync(const Comm* c, cudaStream_t st) {
+  if (!c || c->R <= 1 || c->emulated || !c->nccl) {
+    AFN_CUDA(cudaStreamSynchronize(st));
+    return AFN_OK;
+  }
+  NcclApi& a = nccl_api(nullptr);
+  ncclComm_t comm = static_cast<ncclComm_t>(c->nccl);
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) return AFN_OK;
+    if (q != cudaErrorNotReady) return cuda_status(q, "cudaStreamQuery (NCCL stream)");
+    ncclResult_t ae = ncclSuccess;
+    if (a.CommGetAsyncError(comm, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress)) {
+      a.CommAbort(comm);
+      const_cast<Comm*>(c)->nccl = nullptr;
+      return nccl_status(ae, "asynchronous NCCL error (communicator aborted)");
+    }
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (sec > c->timeout_s) {
+      a.CommAbort(comm);
+      const_cast<Comm*>(c)->nccl = nullptr;
+      set_error("NCCL wait exceeded %.0f s (communicator aborted)", c->timeout_s);
+      return AFN_ERR_NCCL;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
 }
 
 }  // namespace afn
@@ -181,7 +263,20 @@ void afn_comm_destroy(afn_comm c) {
     NcclApi& a = nccl_api(nullptr);
     if (a.CommDestroy) a.CommDestroy(static_cast<ncclComm_t>(c->nccl));
   }
+  if (c->stage) {
+    cudaDeviceSynchronize();
+    cudaFree(c->stage);
+  }
   delete c;
+}
+
+afn_status afn_comm_set_timeout(afn_comm c, double seconds) {
+  if (!c || !(seconds > 0.0)) {
+    set_error("need a communicator and seconds > 0");
+    return AFN_ERR_ARG;
+  }
+  c->timeout_s = seconds;
+  return AFN_OK;
 }
 
 afn_status afn_shard_rows(int64_t n, int64_t k, int32_t nranks, int32_t rank, int64_t* rows) {

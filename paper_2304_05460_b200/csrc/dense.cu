@@ -90,63 +90,6 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
   for (int s = 0; s < 16; ++s) T[r * TP + q + 4 * s] = a[s];
 }
 
-// Diagonal block Cholesky (in smem), writes L block, zeroes the upper part.
-// Each of the 2080 lower entries is owned by one thread (in a register);
-// step j subtracts a_ij a_tj / p_j (unscaled columns, one barrier per step);
-// the scaling L_ij = a_ij / sqrt(p_j) is applied at the end.
-constexpr int DG_T = 1024;  // (256: 34 us, 512: 26 us, 1024: 25 us per 64-block on C2; 256 is no better next to the concurrent kNN)
-__global__ void __launch_bounds__(DG_T) potrf_diag_kernel(double* A, int64_t k, int64_t kb, int* info) {
-  __shared__ double s[NB * TP];
-  const int nb = (int)min((int64_t)NB, k - kb);
-  const int tid = threadIdx.x;
-  constexpr int NE = NB * (NB + 1) / 2;  // 2080
-  constexpr int NU = (NE + DG_T - 1) / DG_T;
-  int ei[NU], et[NU];
-  double av[NU];
-#pragma unroll
-  for (int u = 0; u < NU; ++u) {
-    const int e = tid + u * DG_T;
-    int i = -1, t = 0;
-    if (e < NE) {
-      i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
-      while (i * (i + 1) / 2 > e) --i;
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      t = e - i * (i + 1) / 2;
-    }
-    ei[u] = i;
-    et[u] = t;
-    double v = 0.0;
-    if (i >= 0) v = (i < nb && t < nb) ? A[(kb + i) * k + kb + t] : (i == t ? 1.0 : 0.0);
-    av[u] = v;
-    if (i >= 0) s[i * TP + t] = v;
-  }
-  __syncthreads();
-  for (int j = 0; j < NB; ++j) {
-    double p = s[j * TP + j];
-    if (!(p > 0.0)) p = 1.0;  // breakdown is reported below; keep the values finite
-    const double ip = 1.0 / p;
-#pragma unroll
-    for (int u = 0; u < NU; ++u) {
-      const int i = ei[u], t = et[u];
-      if (i >= 0 && t > j) {
-        av[u] = fma(-s[i * TP + j], s[t * TP + j] * ip, av[u]);
-        if (t == j + 1) s[i * TP + t] = av[u];
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int u = 0; u < NU; ++u) {
-    const int i = ei[u], t = et[u];
-    if (i < 0 || i >= nb) continue;
-    const double p = s[t * TP + t];
-    if (i == t && !(p > 0.0)) atomicCAS(info, 0, (int)(kb + t + 1));
-    const double sp = p > 0.0 ? sqrt(p) : 1.0;
-    A[(kb + i) * k + kb + t] = (i == t) ? sp : av[u] / sp;
-    if (t != i) A[(kb + t) * k + kb + i] = 0.0;
-  }
-}
-
 // Blocked diagonal-block Cholesky (256 threads): the 64 x 64 block in shared
 // memory is factored in four 16-column steps -- warp 0 factors the 16 x 16
 // diagonal sub-block (one row per lane in registers, columns broadcast through
@@ -260,151 +203,6 @@ __global__ void __launch_bounds__(DT) potrf_panel_kernel(double* A, int64_t k, i
   }
 }
 
-// Trailing update of the lower part: A[I, J] -= A[I, P] A[J, P]^T for tiles
-// J <= I below the panel P = [kb, kb+NB).
-__global__ void __launch_bounds__(DT) potrf_update_kernel(double* A, int64_t k, int64_t kb) {
-  extern __shared__ double dsm[];
-  double* sA = dsm;  // [kk][row]
-  double* sB = dsm + NB * TP;
-  // triangular tile index
-  const int64_t t = blockIdx.x;
-  int64_t bi = (int64_t)((sqrt(8.0 * (double)t + 1.0) - 1.0) / 2.0);
-  while (bi * (bi + 1) / 2 > t) --bi;
-  while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
-  const int64_t bj = t - bi * (bi + 1) / 2;
-  const int64_t base = kb + NB;
-  const int64_t I0 = base + bi * NB, J0 = base + bj * NB;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  for (int e = tid; e < NB * NB; e += DT) {
-    const int r = e / NB, kk = e % NB;
-    const int64_t ri = I0 + r, rj = J0 + r;
-    sA[kk * TP + r] = (ri < k) ? A[ri * k + kb + kk] : 0.0;
-    sB[kk * TP + r] = (rj < k) ? A[rj * k + kb + kk] : 0.0;
-  }
-  __syncthreads();
-  double acc[4][4] = {};
-#pragma unroll 4
-  for (int kk = 0; kk < NB; ++kk) {
-    double a[4], b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = sA[kk * TP + ty + 16 * i];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sB[kk * TP + tx + 16 * j];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int64_t r = I0 + ty + 16 * i;
-    if (r >= k) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t c = J0 + tx + 16 * j;
-      if (c < k && c <= r) A[r * k + c] -= acc[i][j];
-    }
-  }
-}
-
-// -------------------------------------------------------------------------
-// W (N x k) = B L^{-T} for a row block of 64 rows; B = K(Xr, X1) (MODE 0) or
-// the identity (MODE 1, N = k, giving L^{-T}).  Column blocks b in order:
-//   T = B[:, b] - W[:, <b] L[b, <b]^T ;  W[:, b] = T Lbb^{-T}.
-template <int MODE>
-__global__ void __launch_bounds__(DT) trsm_rows_kernel(const double* __restrict__ L, int64_t k,
-                                                       const double* __restrict__ X1,
-                                                       const double* __restrict__ Xr, int64_t N,
-                                                       int d, KernelFn kf, double* __restrict__ W) {
-  extern __shared__ double dsm[];
-  double* sA = dsm;            // [kk][row]: W tile, later T [row][col]
-  double* sB = dsm + NB * TP;  // [kk][col]: L tile, later Lbb [row][col]
-  __shared__ double s_tab[AFN_EXP2_TAB_N];
-  load_exp2_tab(s_tab);
-  __syncthreads();
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const int64_t R0 = (int64_t)blockIdx.x * NB;
-  const int64_t nblk = (k + NB - 1) / NB;
-  int64_t bstart = 0;
-  if (MODE == 1) {
-    bstart = blockIdx.x;  // L^{-T} row r is zero left of column r
-    for (int64_t b = 0; b < bstart; ++b)
-      for (int e = tid; e < NB * NB; e += DT) {
-        const int r = e / NB, c = e % NB;
-        const int64_t gr = R0 + r, gc = b * NB + c;
-        if (gr < N && gc < k) W[gr * k + gc] = 0.0;
-      }
-  }
-  // row coordinates for MODE 0 (4 rows per thread, strided)
-  for (int64_t b = bstart; b < nblk; ++b) {
-    const int64_t C0 = b * NB;
-    double acc[4][4];
-    // initial T = B[:, b]
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t r = R0 + ty + 16 * i, c = C0 + tx + 16 * j;
-        double v = 0.0;
-        if (r < N && c < k) {
-          if (MODE == 0) {
-            const double s = d2_exact_rt(&Xr[r * d], &X1[c * d], d);
-            v = kern_from_d2(kf, s, s_tab);
-          } else {
-            v = (r == c) ? 1.0 : 0.0;
-          }
-        }
-        acc[i][j] = v;
-      }
-    // GEMM: acc -= W[R, cb] * L[C0.., cb]^T over earlier column blocks
-    for (int64_t cb = bstart; cb < b; ++cb) {
-      __syncthreads();
-      for (int e = tid; e < NB * NB; e += DT) {
-        const int r = e / NB, kk = e % NB;
-        const int64_t gr = R0 + r, lr = C0 + r, gc = cb * NB + kk;
-        sA[kk * TP + r] = (gr < N && gc < k) ? W[gr * k + gc] : 0.0;
-        sB[kk * TP + r] = (lr < k && gc < k) ? L[lr * k + gc] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll 4
-      for (int kk = 0; kk < NB; ++kk) {
-        double a[4], bb[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = sA[kk * TP + ty + 16 * i];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bb[j] = sB[kk * TP + tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(-a[i], bb[j], acc[i][j]);
-      }
-    }
-    __syncthreads();
-    // stage T [row][col] and Lbb [row][col]
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) sA[(ty + 16 * i) * TP + tx + 16 * j] = acc[i][j];
-    for (int e = tid; e < NB * NB; e += DT) {
-      const int r = e / NB, c = e % NB;
-      const int64_t lr = C0 + r, lc = C0 + c;
-      sB[r * TP + c] = (lr < k && lc < k) ? L[lr * k + lc] : (r == c ? 1.0 : 0.0);
-    }
-    __syncthreads();
-    rows_trsm_64(sA, sB, NB);
-    __syncthreads();
-    for (int e = tid; e < NB * NB; e += DT) {
-      const int r = e / NB, c = e % NB;
-      const int64_t gr = R0 + r, gc = C0 + c;
-      if (gr < N && gc < k) W[gr * k + gc] = sA[r * TP + c];
-    }
-    // W[R, b] must be visible to this CTA's next GEMM loads (same threads may
-    // read other threads' writes): barrier + block-scope fence
-    __threadfence_block();
-    __syncthreads();
-  }
-}
-
 constexpr size_t SMEM2 = sizeof(double) * 2 * NB * TP;
 
 __global__ void diag_inv_kernel(const double* __restrict__ Lp, int64_t kp, double* __restrict__ X);
@@ -415,25 +213,18 @@ afn_status set_smem_once() {
   cudaGetDevice(&dev);
   if (dev >= 0 && dev < 64 && done[dev]) return AFN_OK;
   AFN_CUDA(cudaFuncSetAttribute(potrf_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
-  AFN_CUDA(cudaFuncSetAttribute(potrf_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
-  AFN_CUDA(cudaFuncSetAttribute(trsm_rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
-  AFN_CUDA(cudaFuncSetAttribute(trsm_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
   AFN_CUDA(cudaFuncSetAttribute(diag_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2));
   if (dev >= 0 && dev < 64) done[dev] = true;
   return AFN_OK;
 }
-
 
 // -------------------------------------------------------------------------
 // W = K21 L^{-T} as a GEMM with the explicit L^{-T} (upper triangular):
 // W[r][c] = sum_{t <= c} K21[r][t] LinvT[t][c].  With FPS landmarks K11 + mu I
 // is well conditioned (cond(L) <= ~10 on the configs; SURVEY 8(c) Fig. 3.2
 // screening argument), so the explicit inverse loses nothing measurable and
-// the column blocks become independent tiles (no sequential sweep).
-// FP64 SIMT tile: 128 x 64 output, 256 threads, 8 x 4 register micro-tile
-// with stride-16 mapping, BK = 16 double-buffered cp.async stages.
-constexpr int GM = 128, GN = 64, GK = 16;
-constexpr int GPA = GM + 4, GPB = GN + 4;  // smem pitches
+// the column blocks become independent tiles (no sequential sweep): the
+// FP64 tensor-core GEMM gemm_dmma_kernel<0> below.
 
 __device__ __forceinline__ void cpa16_d(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -462,80 +253,6 @@ __global__ void gen_k21_kernel(const double* __restrict__ X1, int64_t k, const d
   Kb[e] = kern_from_d2(kf, sd, s_tab);
 }
 
-// C (M x N) = A (M x K) * B (K x N), B upper triangular (rows t <= col used)
-__global__ void __launch_bounds__(256, 2) gemm_nn_bupper_kernel(const double* __restrict__ A,
-                                                              const double* __restrict__ B,
-                                                              double* __restrict__ Cm, int64_t M,
-                                                              int64_t N, int64_t K) {
-  extern __shared__ __align__(16) double gsm[];
-  double* sA = gsm;                  // [2][GK][GPA]
-  double* sB = gsm + 2 * GK * GPA;   // [2][GK][GPB]
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const int64_t R0 = (int64_t)blockIdx.y * GM, C0 = (int64_t)blockIdx.x * GN;
-  const int64_t kend = min(K, C0 + GN);  // B[t][c] = 0 for t > c
-  const int64_t nkb = (kend + GK - 1) / GK;
-  auto stage = [&](int64_t kb, int buf) {
-    const int64_t k0 = kb * GK;
-    double* a = sA + buf * GK * GPA;
-    double* b = sB + buf * GK * GPB;
-    for (int e = tid; e < GM * GK; e += 256) {
-      const int r = e / GK, kk = e - r * GK;
-      const int64_t gr = R0 + r, gk = k0 + kk;
-      if (gr < M && gk < kend) cpa8(&a[kk * GPA + r], &A[gr * K + gk]);
-      else a[kk * GPA + r] = 0.0;
-    }
-    for (int e = tid; e < GK * GN; e += 256) {
-      const int kk = e / GN, c = e - kk * GN;
-      const int64_t gk = k0 + kk, gc = C0 + c;
-      if (gk < kend && gc < N) cpa8(&b[kk * GPB + c], &B[gk * N + gc]);
-      else b[kk * GPB + c] = 0.0;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  double acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  if (nkb > 0) stage(0, 0);
-  for (int64_t kb = 0; kb < nkb; ++kb) {
-    const int buf = (int)(kb & 1);
-    if (kb + 1 < nkb) {
-      stage(kb + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const double* a = sA + buf * GK * GPA;
-    const double* b = sB + buf * GK * GPB;
-#pragma unroll 4
-    for (int kk = 0; kk < GK; ++kk) {
-      double av[8], bv[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = a[kk * GPA + ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = b[kk * GPB + tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = R0 + ty + 16 * i;
-    if (r >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t c = C0 + tx + 16 * j;
-      if (c < N) Cm[r * N + c] = acc[i][j];
-    }
-  }
-}
-
-
 // -------------------------------------------------------------------------
 // C = A B with B upper triangular (B[t][c] = 0 for t > c): the W = K21 L^{-T}
 // product.  128 x 128 tiles, 256 threads with 8 x 8 register tiles
@@ -543,211 +260,6 @@ __global__ void __launch_bounds__(256, 2) gemm_nn_bupper_kernel(const double* __
 // read is an LDS.128 of two adjacent doubles pairs, A broadcast within the
 // warp, B conflict-free), BK = 16 double-buffered through cp.async (A
 // transposed into [kk][row] while staging).  FP64 SIMT: 64 DFMA per 8 LDS.128.
-constexpr int HM = 128, HN = 128, HK = 16, HPA = HM + 4, HPB = HN + 4;
-
-__global__ void __launch_bounds__(256, 1) gemm128_bupper_kernel(const double* __restrict__ A,
-                                                               const double* __restrict__ B,
-                                                               double* __restrict__ Cm, int64_t M,
-                                                               int64_t N, int64_t K) {
-  extern __shared__ __align__(16) double hsm[];
-  double* sA = hsm;                  // [2][HK][HPA]
-  double* sB = hsm + 2 * HK * HPA;   // [2][HK][HPB]
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const int64_t R0 = (int64_t)blockIdx.y * HM, C0 = (int64_t)blockIdx.x * HN;
-  const int64_t kend = min(K, C0 + HN);  // B[t][c] = 0 for t > c
-  const int64_t nkb = (kend + HK - 1) / HK;
-  auto stage = [&](int64_t kb, int buf) {
-    const int64_t k0 = kb * HK;
-    double* a = sA + buf * HK * HPA;
-    double* b = sB + buf * HK * HPB;
-#pragma unroll
-    for (int u = 0; u < (HM * HK) / 256; ++u) {  // A: 8 B copies, row r, k k0+kk
-      const int e = tid + 256 * u;
-      const int r = e / HK, kk = e - r * HK;
-      const int64_t gr = R0 + r, gk = k0 + kk;
-      if (gr < M && gk < kend) cpa8(&a[kk * HPA + r], &A[gr * K + gk]);
-      else a[kk * HPA + r] = 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < (HK * HN) / (2 * 256); ++u) {  // B: 16 B copies
-      const int e = tid + 256 * u;
-      const int kk = e / (HN / 2), c = 2 * (e - kk * (HN / 2));
-      const int64_t gk = k0 + kk, gc = C0 + c;
-      double* dst = &b[kk * HPB + c];
-      if (gk < kend && gc + 1 < N && (N & 1) == 0) {
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(&B[gk * N + gc]) : "memory");
-      } else {
-        dst[0] = (gk < kend && gc < N) ? B[gk * N + gc] : 0.0;
-        dst[1] = (gk < kend && gc + 1 < N) ? B[gk * N + gc + 1] : 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  double acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
-  if (nkb > 0) stage(0, 0);
-  for (int64_t kb = 0; kb < nkb; ++kb) {
-    const int buf = (int)(kb & 1);
-    if (kb + 1 < nkb) {
-      stage(kb + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const double* a = sA + buf * HK * HPA + ty * 4;
-    // B columns of thread tx: 2 tx + {0, 1} + 32 q (q < 4): the 16 threads of
-    // a row read 256 contiguous bytes per LDS.128 (2 wavefronts, no conflicts)
-    const double* b = sB + buf * HK * HPB + tx * 2;
-    // operands of step kk+1 are loaded while step kk's 64 DFMA run (the
-    // two CTA warps per scheduler cannot hide the LDS latency otherwise)
-    double2 ca[4], cb[4];
-    ca[0] = *reinterpret_cast<const double2*>(a);
-    ca[1] = *reinterpret_cast<const double2*>(a + 2);
-    ca[2] = *reinterpret_cast<const double2*>(a + 64);
-    ca[3] = *reinterpret_cast<const double2*>(a + 66);
-    cb[0] = *reinterpret_cast<const double2*>(b);
-    cb[1] = *reinterpret_cast<const double2*>(b + 32);
-    cb[2] = *reinterpret_cast<const double2*>(b + 64);
-    cb[3] = *reinterpret_cast<const double2*>(b + 96);
-#pragma unroll
-    for (int kk = 0; kk < HK; ++kk) {
-      double2 na[4], nb[4];
-      if (kk + 1 < HK) {
-        const double* an = a + (kk + 1) * HPA;
-        const double* bn = b + (kk + 1) * HPB;
-        na[0] = *reinterpret_cast<const double2*>(an);
-        na[1] = *reinterpret_cast<const double2*>(an + 2);
-        na[2] = *reinterpret_cast<const double2*>(an + 64);
-        na[3] = *reinterpret_cast<const double2*>(an + 66);
-        nb[0] = *reinterpret_cast<const double2*>(bn);
-        nb[1] = *reinterpret_cast<const double2*>(bn + 32);
-        nb[2] = *reinterpret_cast<const double2*>(bn + 64);
-        nb[3] = *reinterpret_cast<const double2*>(bn + 96);
-      }
-      const double av[8] = {ca[0].x, ca[0].y, ca[1].x, ca[1].y, ca[2].x, ca[2].y, ca[3].x, ca[3].y};
-      const double bv[8] = {cb[0].x, cb[0].y, cb[1].x, cb[1].y, cb[2].x, cb[2].y, cb[3].x, cb[3].y};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-      if (kk + 1 < HK) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          ca[q] = na[q];
-          cb[q] = nb[q];
-        }
-      }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = R0 + ty * 4 + (i & 3) + (i >> 2) * 64;
-    if (r >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      const int64_t c = C0 + tx * 2 + (j >> 1) * 32;
-      if (c + 1 < N && (N & 1) == 0) {
-        *reinterpret_cast<double2*>(&Cm[r * N + c]) = make_double2(acc[i][j], acc[i][j + 1]);
-      } else {
-        if (c < N) Cm[r * N + c] = acc[i][j];
-        if (c + 1 < N) Cm[r * N + c + 1] = acc[i][j + 1];
-      }
-    }
-  }
-}
-
-// -------------------------------------------------------------------------
-// L^{-1} by recursive 2x2 block inversion on a power-of-two padding kp:
-//   inv([[A, 0], [B, C]]) = [[A^-1, 0], [-C^-1 B A^-1, C^-1]]
-// 64x64 diagonal blocks first (in-smem triangular solves), then one batched
-// pair of GEMMs per level (all independent tiles) -> log2(kp/64) levels.
-// Mode 1: A lower (K range <= row end); mode 2: B lower (K range >= col start).
-template <int MODE>
-__global__ void __launch_bounds__(256, 2) gemm_nn_batched_kernel(const double* __restrict__ A,
-                                                                const double* __restrict__ B,
-                                                                double* __restrict__ Cm, int64_t n,
-                                                                int64_t ld, int64_t sA, int64_t sB,
-                                                                int64_t sC, double alpha) {
-  extern __shared__ __align__(16) double gsm[];
-  double* sAs = gsm;
-  double* sBs = gsm + 2 * GK * GPA;
-  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const int64_t z = blockIdx.z;
-  A += z * sA;
-  B += z * sB;
-  Cm += z * sC;
-  const int64_t R0 = (int64_t)blockIdx.y * GM, C0 = (int64_t)blockIdx.x * GN;
-  int64_t kbeg = 0, kend = n;
-  if (MODE == 1) kend = min(n, R0 + GM);
-  if (MODE == 2) kbeg = C0;
-  const int64_t kb0 = kbeg / GK;
-  const int64_t nkb = (kend + GK - 1) / GK - kb0;
-  auto stage = [&](int64_t kb, int buf) {
-    const int64_t k0 = (kb0 + kb) * GK;
-    double* a = sAs + buf * GK * GPA;
-    double* b = sBs + buf * GK * GPB;
-    for (int e = tid; e < GM * GK; e += 256) {
-      const int r = e / GK, kk = e - r * GK;
-      const int64_t gr = R0 + r, gk = k0 + kk;
-      if (gr < n && gk < kend) cpa8(&a[kk * GPA + r], &A[gr * ld + gk]);
-      else a[kk * GPA + r] = 0.0;
-    }
-    for (int e = tid; e < GK * GN; e += 256) {
-      const int kk = e / GN, c = e - kk * GN;
-      const int64_t gk = k0 + kk, gc = C0 + c;
-      if (gk < kend && gc < n) cpa8(&b[kk * GPB + c], &B[gk * ld + gc]);
-      else b[kk * GPB + c] = 0.0;
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  double acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-  if (nkb > 0) stage(0, 0);
-  for (int64_t kb = 0; kb < nkb; ++kb) {
-    const int buf = (int)(kb & 1);
-    if (kb + 1 < nkb) {
-      stage(kb + 1, buf ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    __syncthreads();
-    const double* a = sAs + buf * GK * GPA;
-    const double* b = sBs + buf * GK * GPB;
-#pragma unroll 4
-    for (int kk = 0; kk < GK; ++kk) {
-      double av[8], bv[4];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) av[i] = a[kk * GPA + ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) bv[j] = b[kk * GPB + tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t r = R0 + ty + 16 * i;
-    if (r >= n) continue;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t c = C0 + tx + 16 * j;
-      if (c < n) Cm[r * ld + c] = alpha * acc[i][j];
-    }
-  }
-}
 
 // pad L (k x k) into Lp (kp x kp): identity beyond k, zero elsewhere
 __global__ void pad_l_kernel(const double* __restrict__ L, int64_t k, double* __restrict__ Lp, int64_t kp) {
@@ -969,7 +481,6 @@ __global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64
 }
 
 afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
-  static const bool simt = getenv("AFN_POTRF_SIMT") != nullptr;
   static bool uattr = false;
   if (!uattr) {
     AFN_CUDA(cudaFuncSetAttribute(potrf_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -979,36 +490,19 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
   TRY_SMEM();
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
   for (int64_t kb = 0; kb < k; kb += NB) {
-    static const bool diag_old = getenv("AFN_POTRF_DIAG_OLD") != nullptr;
-    if (diag_old) potrf_diag_kernel<<<1, DG_T, 0, st>>>(A, k, kb, d_info);
-    else potrf_diag_blk_kernel<<<1, DB_T, 0, st>>>(A, k, kb, d_info);
-    AFN_LAUNCH_CHECK("potrf_diag_kernel");
+    potrf_diag_blk_kernel<<<1, DB_T, 0, st>>>(A, k, kb, d_info);
+    AFN_LAUNCH_CHECK("potrf_diag_blk_kernel");
     const int64_t rem = k - kb - NB;
     if (rem <= 0) break;
     const int64_t T = (rem + NB - 1) / NB;
     potrf_panel_kernel<<<(unsigned)T, DT, SMEM2, st>>>(A, k, kb);
     AFN_LAUNCH_CHECK("potrf_panel_kernel");
-    if (simt) {
-      potrf_update_kernel<<<(unsigned)(T * (T + 1) / 2), DT, SMEM2, st>>>(A, k, kb);
-      AFN_LAUNCH_CHECK("potrf_update_kernel");
-    } else {  // FP64 tensor cores
-      potrf_update_dmma_kernel<<<(unsigned)(T * (T + 1) / 2), 128, (int)(sizeof(double) * 2 * NB * PUP), st>>>(A, k,
-                                                                                                         kb);
-      AFN_LAUNCH_CHECK("potrf_update_dmma_kernel");
-    }
+    // trailing update on the FP64 tensor cores
+    potrf_update_dmma_kernel<<<(unsigned)(T * (T + 1) / 2), 128, (int)(sizeof(double) * 2 * NB * PUP), st>>>(A, k, kb);
+    AFN_LAUNCH_CHECK("potrf_update_dmma_kernel");
   }
   zero_upper_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, st>>>(A, k);
   AFN_LAUNCH_CHECK("zero_upper_kernel");
-  return AFN_OK;
-}
-
-afn_status trsm_w(const double* L, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
-                  Kern kn, double* W, cudaStream_t st) {
-  if (N <= 0 || k <= 0) return AFN_OK;
-  TRY_SMEM();
-  const KernelFn kf = kernel_fn(kn.kind, kn.l);
-  trsm_rows_kernel<0><<<(unsigned)((N + NB - 1) / NB), DT, SMEM2, st>>>(L, k, X1, Xr, N, d, kf, W);
-  AFN_LAUNCH_CHECK("trsm_rows_kernel<0>");
   return AFN_OK;
 }
 
@@ -1129,43 +623,25 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
   const KernelFn kf = kernel_fn(kn.kind, kn.l);
   // K21 is generated in row blocks of <= ~1 GiB (not all N x k at once: at
   // n = 2^20, k = 8000 that alone would be 66.6 GB)
-  const int64_t rb = std::max<int64_t>(HM, std::min<int64_t>(N, ((1LL << 27) / k) / HM * HM));
+  const int64_t rb = std::max<int64_t>(TM, std::min<int64_t>(N, ((1LL << 27) / k) / TM * TM));
   double* Kb = nullptr;
   afn_status s = dalloc((void**)&Kb, sizeof(double) * rb * k, st);
   if (s != AFN_OK) return s;
-  static const bool legacy = getenv("AFN_W_GEMM64") != nullptr;
-  static const bool simt = getenv("AFN_W_SIMT") != nullptr;  // the DFMA 128 x 128 kernel
   static bool attr = false;
   if (!attr) {
     for (auto kf2 : {gemm_dmma_kernel<0>, gemm_dmma_kernel<1>, gemm_dmma_kernel<2>})
       AFN_CUDA(cudaFuncSetAttribute(kf2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)(sizeof(double) * TS * (TM * TKP + TK * TNP))));
-    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * 2 * GK * (GPA + GPB))));
-    AFN_CUDA(cudaFuncSetAttribute(gemm128_bupper_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)(sizeof(double) * 2 * HK * (HPA + HPB))));
     attr = true;
   }
   for (int64_t r0 = 0; r0 < N; r0 += rb) {
     const int64_t nr = std::min(rb, N - r0);
     gen_k21_kernel<<<(unsigned)((nr * k + 255) / 256), 256, 0, st>>>(X1, k, Xr + r0 * d, nr, d, kf, Kb);
     AFN_LAUNCH_CHECK("gen_k21_kernel");
-    if (legacy) {
-      dim3 grid((unsigned)((k + GN - 1) / GN), (unsigned)((nr + GM - 1) / GM));
-      gemm_nn_bupper_kernel<<<grid, 256, (int)(sizeof(double) * 2 * GK * (GPA + GPB)), st>>>(
-          Kb, LinvT, W + r0 * k, nr, k, k);
-      AFN_LAUNCH_CHECK("gemm_nn_bupper_kernel");
-    } else if (simt) {
-      dim3 grid((unsigned)((k + HN - 1) / HN), (unsigned)((nr + HM - 1) / HM));
-      gemm128_bupper_kernel<<<grid, 256, (int)(sizeof(double) * 2 * HK * (HPA + HPB)), st>>>(
-          Kb, LinvT, W + r0 * k, nr, k, k);
-      AFN_LAUNCH_CHECK("gemm128_bupper_kernel");
-    } else {  // FP64 tensor cores
-      dim3 grid((unsigned)((k + TN - 1) / TN), (unsigned)((nr + TM - 1) / TM));
-      gemm_dmma_kernel<0><<<grid, 128, (int)(sizeof(double) * TS * (TM * TKP + TK * TNP)), st>>>(
-          Kb, LinvT, W + r0 * k, nr, k, k, k, k, k, 0, 0, 0, 1.0);
-      AFN_LAUNCH_CHECK("gemm_dmma_kernel<0>");
-    }
+    dim3 grid((unsigned)((k + TN - 1) / TN), (unsigned)((nr + TM - 1) / TM));  // FP64 tensor cores
+    gemm_dmma_kernel<0><<<grid, 128, (int)(sizeof(double) * TS * (TM * TKP + TK * TNP)), st>>>(
+        Kb, LinvT, W + r0 * k, nr, k, k, k, k, k, 0, 0, 0, 1.0);
+    AFN_LAUNCH_CHECK("gemm_dmma_kernel<0>");
   }
   dfree(Kb, st);
   return AFN_OK;
@@ -1185,14 +661,6 @@ afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_
   AFN_LAUNCH_CHECK("pad_l_kernel");
   diag_inv_kernel<<<(unsigned)(kp / NB), DT, SMEM2, st>>>(Lp, kp, X);
   AFN_LAUNCH_CHECK("diag_inv_kernel");
-  static bool attr = false;
-  const int bytes = (int)(sizeof(double) * 2 * GK * (GPA + GPB));
-  if (!attr) {
-    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_batched_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    AFN_CUDA(cudaFuncSetAttribute(gemm_nn_batched_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    attr = true;
-  }
-  static const bool simt = getenv("AFN_LINV_SIMT") != nullptr;  // the DFMA batched kernels
   static bool dattr = false;
   const int dbytes = (int)(sizeof(double) * TS * (TM * TKP + TK * TNP));
   if (!dattr) {
@@ -1203,24 +671,14 @@ afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_
   for (int64_t h = NB; h < kp; h <<= 1) {
     const int64_t pairs = kp / (2 * h);
     const int64_t stride = 2 * h * kp + 2 * h;  // next diagonal pair
-    if (!simt) {  // FP64 tensor cores
-      dim3 grid((unsigned)((h + TN - 1) / TN), (unsigned)((h + TM - 1) / TM), (unsigned)pairs);
-      gemm_dmma_kernel<2><<<grid, 128, dbytes, st>>>(Lp + h * kp, X, Tt, h, h, h, kp, kp, kp, stride, stride,
-                                                     stride, 1.0);
-      AFN_LAUNCH_CHECK("gemm_dmma_kernel<2>");
-      gemm_dmma_kernel<1><<<grid, 128, dbytes, st>>>(X + h * kp + h, Tt, X + h * kp, h, h, h, kp, kp, kp, stride,
-                                                     stride, stride, -1.0);
-      AFN_LAUNCH_CHECK("gemm_dmma_kernel<1>");
-      continue;
-    }
-    dim3 grid((unsigned)((h + GN - 1) / GN), (unsigned)((h + GM - 1) / GM), (unsigned)pairs);
-    // T = B * A^{-1}   (B = Lp[h.., 0..h), A^{-1} = X[0..h, 0..h) lower -> K >= col start)
-    gemm_nn_batched_kernel<2><<<grid, 256, bytes, st>>>(Lp + h * kp, X, Tt, h, kp, stride, stride, stride, 1.0);
-    AFN_LAUNCH_CHECK("gemm_nn_batched_kernel<2>");
-    // X21 = -C^{-1} * T   (C^{-1} = X[h.., h..) lower -> K <= row end)
-    gemm_nn_batched_kernel<1><<<grid, 256, bytes, st>>>(X + h * kp + h, Tt, X + h * kp, h, kp, stride, stride,
-                                                        stride, -1.0);
-    AFN_LAUNCH_CHECK("gemm_nn_batched_kernel<1>");
+    // FP64 tensor cores: T = B A^{-1}, then X21 = -C^{-1} T
+    dim3 grid((unsigned)((h + TN - 1) / TN), (unsigned)((h + TM - 1) / TM), (unsigned)pairs);
+    gemm_dmma_kernel<2><<<grid, 128, dbytes, st>>>(Lp + h * kp, X, Tt, h, h, h, kp, kp, kp, stride, stride,
+                                                   stride, 1.0);
+    AFN_LAUNCH_CHECK("gemm_dmma_kernel<2>");
+    gemm_dmma_kernel<1><<<grid, 128, dbytes, st>>>(X + h * kp + h, Tt, X + h * kp, h, h, h, kp, kp, kp, stride,
+                                                   stride, stride, -1.0);
+    AFN_LAUNCH_CHECK("gemm_dmma_kernel<1>");
   }
   dim3 tg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
   transpose_k_kernel<<<tg, dim3(32, 8), 0, st>>>(X, kp, k, LinvT);
@@ -1237,16 +695,8 @@ afn_status transpose_sq(const double* A, int64_t k, double* At, cudaStream_t st)
 }
 
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st) {
-  static const bool legacy = getenv("AFN_LINV_TRSM") != nullptr;
-  if (!legacy) {
-    TRY_SMEM();
-    return linv_recursive(L, k, LinvT, st);
-  }
   TRY_SMEM();
-  trsm_rows_kernel<1><<<(unsigned)((k + NB - 1) / NB), DT, SMEM2, st>>>(L, k, nullptr, nullptr, k, 1,
-                                                                   KernelFn{0, 0.0}, LinvT);
-  AFN_LAUNCH_CHECK("trsm_rows_kernel<1>");
-  return AFN_OK;
+  return linv_recursive(L, k, LinvT, st);
 }
 
 }  // namespace afn

@@ -246,8 +246,6 @@ afn_status launch_fps(const double* X, int64_t n, int d, int64_t k, int64_t seed
   return AFN_OK;
 }
 
-
-
 // (d2 desc, index asc) argmax across a warp with three redux.sync reductions.
 // key = bits(d2) + 1 for d2 >= 0 (monotone), 0 for selected (-1) / padding.
 __device__ __forceinline__ unsigned long long fps_key(double d) {
@@ -263,126 +261,10 @@ __device__ __forceinline__ void warp_argmax_key(unsigned long long key, unsigned
 }
 
 // ---------------------------------------------------------------------------
-// Cluster variant (n up to 16 CTAs x NT x 2 points): the per-step exchange is
-// a cluster barrier plus distributed-shared-memory reads of the CL per-CTA
-// winners (no global-memory round trips).
 namespace cg = cooperative_groups;
 
-template <int DP, int P, int NT>
-__global__ void __launch_bounds__(NT, 1)
-fps_cluster_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
-                   int64_t* __restrict__ idx_out, double* __restrict__ fill_out,
-                   const int64_t* __restrict__ kstop) {
-  constexpr int S = Slot<DP>::S;
-  constexpr int NW = NT / 32;
-  __shared__ double s_w[NW][S];
-  __shared__ double s_slot[2][S];
-  __shared__ double s_new[S];
-  // early stop: a host-side writer may lower *kstop while the kernel runs
-  // (Alg. 1 finishing on another stream); rank 0 samples it every 8 steps and
-  // every CTA reads rank 0's sample after the same cluster barrier
-  __shared__ long long s_stop[2];
-  __shared__ long long s_kend;
-  cg::cluster_group cl = cg::this_cluster();
-  const int crank = (int)cl.block_rank();
-  const int CL = (int)cl.num_blocks();
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t stride = (int64_t)CL * NT;
-  const int64_t gtid = (int64_t)crank * NT + tid;
-
-  double pts[P][DP];
-  double mind[P];
-  double y[DP];
-#pragma unroll
-  for (int c = 0; c < DP; ++c) y[c] = c < d ? X[seed * d + c] : 0.0;
-#pragma unroll
-  for (int s = 0; s < P; ++s) {
-    const int64_t i = gtid + s * stride;
-    if (i < n) {
-#pragma unroll
-      for (int c = 0; c < DP; ++c) pts[s][c] = c < d ? X[i * d + c] : 0.0;
-      mind[s] = (i == seed) ? -1.0 : d2_exact<DP>(pts[s], y);
-    } else {
-#pragma unroll
-      for (int c = 0; c < DP; ++c) pts[s][c] = 0.0;
-      mind[s] = -2.0;
-    }
-  }
-  if (crank == 0 && tid == 0) idx_out[0] = seed;
-  if (tid == 0) s_stop[0] = s_stop[1] = k;
-
-  for (int64_t step = 1; step <= k; ++step) {
-    const int par = (int)(step & 1);
-    if (crank == 0 && tid == 0) {
-      long long ks = s_stop[par ^ 1];
-      if (kstop != nullptr && (step & 7) == 0) ks = min(ks, *reinterpret_cast<const volatile long long*>(kstop));
-      s_stop[par] = ks;
-    }
-    // thread-local best (indices ascend with s: strict > keeps the lowest)
-    double bd = -3.0;
-    unsigned bi = 0xffffffffu;
-    int bs = 0;
-#pragma unroll
-    for (int s = 0; s < P; ++s)
-      if (mind[s] > bd) { bd = mind[s]; bi = (unsigned)(gtid + s * stride); bs = s; }
-    unsigned long long wkey;
-    unsigned widx;
-    warp_argmax_key(fps_key(bd), bi, wkey, widx);
-    if (bi == widx) {
-      s_w[wid][0] = bd;
-      s_w[wid][1] = __longlong_as_double((long long)widx);
-#pragma unroll
-      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pts[bs][c];
-    }
-    __syncthreads();
-    if (wid == 0) {
-      const double vd = lane < NW ? s_w[lane][0] : -3.0;
-      const unsigned vi = lane < NW ? (unsigned)__double_as_longlong(s_w[lane][1]) : 0xffffffffu;
-      unsigned long long k2;
-      unsigned i2;
-      warp_argmax_key(fps_key(vd), vi, k2, i2);
-      const int src = __ffs(__ballot_sync(0xffffffffu, lane < NW && vi == i2)) - 1;
-      if (lane < S) s_slot[par][lane] = s_w[src][lane];
-    }
-    cl.sync();
-    if (wid == 0) {
-      double gd = -3.0;
-      unsigned gi = 0xffffffffu;
-      if (lane < CL) {
-        const double* rs = cl.map_shared_rank(&s_slot[par][0], lane);
-        gd = rs[0];
-        gi = (unsigned)__double_as_longlong(rs[1]);
-      }
-      unsigned long long k3;
-      unsigned i3;
-      warp_argmax_key(fps_key(gd), gi, k3, i3);
-      const int src = __ffs(__ballot_sync(0xffffffffu, lane < CL && gi == i3)) - 1;
-      if (lane < S) s_new[lane] = cl.map_shared_rank(&s_slot[par][0], src)[lane];
-      if (lane == 0) s_kend = *cl.map_shared_rank(&s_stop[par], 0);
-    }
-    __syncthreads();
-    const double nd = s_new[0];
-    const long long ni = __double_as_longlong(s_new[1]);
-    if (crank == 0 && tid == 0) {
-      fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
-      if (step < k) idx_out[step] = ni;
-    }
-    if (step >= s_kend) break;
-#pragma unroll
-    for (int c = 0; c < DP; ++c) y[c] = s_new[2 + c];
-#pragma unroll
-    for (int s = 0; s < P; ++s) {
-      const int64_t i = gtid + s * stride;
-      if (i < n) {
-        const double dd = d2_exact<DP>(pts[s], y);
-        mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
-      }
-    }
-  }
-  cl.sync();  // no CTA leaves while its slots may still be read remotely
-}
-
-// Push variant of the cluster kernel: after its CTA-level argmax, warp 0 of
+// Cluster kernel (n up to 16 CTAs x NT x P points, no global-memory round
+// trips per step): after its CTA-level argmax, warp 0 of
 // every CTA writes its winner slot (d2, index, point, early-stop sample) into
 // every CTA's inbox with st.async (asynchronous distributed-shared-memory
 // stores that complete bytes on the destination's mbarrier: no fence, no
@@ -421,10 +303,7 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned a, unsigned ph) {
 template <int DP, int P, int NT>
 __global__ void __launch_bounds__(NT, 1)
 fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
-                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop,
-                long long* prof) {
-  // prof (debug, AFN_FPS_PROF): CTA 0 / warp 0 clock64 totals of the step phases
-  long long pc[6] = {0, 0, 0, 0, 0, 0}, pt = 0;
+                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop) {
   constexpr int KI = DP + 2;          // slot: d2, index, point (DP), early-stop sample (KI)
   constexpr int S = (KI + 2) & ~1;    // even length (16-byte stores)
   constexpr int NW = NT / 32;
@@ -472,8 +351,6 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
     mbar_expect(smem_u32(&s_bar[0]), txb);
   }
   unsigned ph0 = 0, ph1 = 0;
-  const bool pr = prof != nullptr && crank == 0 && tid == 0;
-  if (pr) pt = clock64();
   for (int64_t step = 1; step <= k; ++step) {
     const int par = (int)(step & 1);
     if (crank == 0 && wid == 1 && lane == 0 && kstop != nullptr && (step & 7) == 0)  // early-stop poll
@@ -493,9 +370,7 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
 #pragma unroll
       for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pts[bs][c];
     }
-    if (pr) { const long long t = clock64(); pc[0] += t - pt; pt = t; }
     __syncthreads();
-    if (pr) { const long long t = clock64(); pc[1] += t - pt; pt = t; }
     if (wid == 0) {
       const double vd = lane < NW ? s_w[lane][0] : -3.0;
       const unsigned vi = lane < NW ? (unsigned)__double_as_longlong(s_w[lane][1]) : 0xffffffffu;
@@ -515,11 +390,9 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
         for (int c = 0; c < S; c += 2) st_async_v2(dst + 8 * c, msg[c], msg[c + 1], bar);
       }
     }
-    if (pr) { const long long t = clock64(); pc[2] += t - pt; pt = t; }
     mbar_wait_parity(smem_u32(&s_bar[par]), par ? ph1 : ph0);
     if (par) ph1 ^= 1; else ph0 ^= 1;
     if (tid == 0 && step + 2 <= k) mbar_expect(smem_u32(&s_bar[par]), txb);  // arrival of step + 2
-    if (pr) { const long long t = clock64(); pc[3] += t - pt; pt = t; }
     // every warp reduces the CL slots itself (no second CTA barrier)
     const double gd = lane < CL ? s_in[par][lane][0] : -3.0;
     const unsigned gi = lane < CL ? (unsigned)__double_as_longlong(s_in[par][lane][1]) : 0xffffffffu;
@@ -534,7 +407,6 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
       fill_out[step - 1] = nd >= 0.0 ? sqrt(nd) : 0.0;
       if (step < k) idx_out[step] = ni;
     }
-    if (pr) { const long long t = clock64(); pc[4] += t - pt; pt = t; }
     if (step >= kst) break;
 #pragma unroll
     for (int c = 0; c < DP; ++c) y[c] = s_in[par][src][2 + c];
@@ -546,10 +418,7 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
         mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
       }
     }
-    if (pr) { const long long t = clock64(); pc[5] += t - pt; pt = t; }
   }
-  if (pr)
-    for (int j = 0; j < 6; ++j) prof[j] = pc[j];
   cl.sync();  // no CTA leaves while a push into it may be in flight
 }
 
@@ -570,44 +439,8 @@ afn_status launch_fps_push(const double* X, int64_t n, int d, int64_t k, int64_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  static const bool profon = getenv("AFN_FPS_PROF") != nullptr;
-  long long* prof = nullptr;
-  if (profon) {
-    AFN_CUDA(cudaMalloc(&prof, sizeof(long long) * 6));
-    AFN_CUDA(cudaMemset(prof, 0, sizeof(long long) * 6));
-  }
-  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop, prof));
-  AFN_LAUNCH_CHECK("fps_push_kernel");
-  if (profon) {
-    long long h[6];
-    AFN_CUDA(cudaMemcpy(h, prof, sizeof(h), cudaMemcpyDeviceToHost));
-    cudaFree(prof);
-    fprintf(stderr, "fps_push k=%lld CL=%d cycles/step: local %.0f sync %.0f cta+push %.0f wait %.0f reduce %.0f update %.0f\n",
-            (long long)k, CL, h[0] / (double)k, h[1] / (double)k, h[2] / (double)k, h[3] / (double)k,
-            h[4] / (double)k, h[5] / (double)k);
-  }
-  return AFN_OK;
-}
-
-template <int DP, int P, int NT>
-afn_status launch_fps_cluster(const double* X, int64_t n, int d, int64_t k, int64_t seed,
-                              int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st) {
-  auto kern = fps_cluster_kernel<DP, P, NT>;
-  if (CL > 8) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(CL);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CL;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop));
-  AFN_LAUNCH_CHECK("fps_cluster_kernel");
+  AFN_LAUNCH_CHECK("fps_push_kernel");
   return AFN_OK;
 }
 
@@ -618,36 +451,22 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
   // cluster path: one cluster of CL <= 16 CTAs, 1 or 2 points per thread
   {
     constexpr int CNT = DP <= 4 ? 1024 : 512;
-    // points per thread: fewer CTAs in the cluster (cheaper per-step cluster
-    // barrier) against more distance updates per thread
-    static const int pmin = getenv("AFN_FPS_PPT") ? atoi(getenv("AFN_FPS_PPT")) : 1;
+    // points per thread: fewer CTAs in the cluster against more distance
+    // updates per thread; smaller CTAs with more points per thread: fewer
+    // warps to reduce per step (C2, k = 2000: 1024 threads 2.52 ms, 512: 2.08,
+    // 256: 2.04; the cluster-barrier exchange instead of the pushes 3.34)
     if (n > (int64_t)FPS_NT * 8 && n <= (int64_t)16 * CNT * 4) {
       int P2 = 1;
-      while (P2 < 4 && (n > (int64_t)16 * CNT * P2 || P2 < pmin)) P2 *= 2;
+      while (P2 < 4 && n > (int64_t)16 * CNT * P2) P2 *= 2;
       const int CL = (int)((n + (int64_t)CNT * P2 - 1) / ((int64_t)CNT * P2));
-      // AFN_FPS_PUSH=0: the cluster-barrier exchange instead of the mbarrier pushes
-      static const bool push = !(getenv("AFN_FPS_PUSH") && atoi(getenv("AFN_FPS_PUSH")) == 0);
-      // smaller CTAs with more points per thread (same cluster): fewer warps to
-      // reduce per step.  AFN_FPS_NT: 1024 | 512 (default) | 256
-      // (C2, k = 2000: 1024 threads 2.52 ms, 512: 2.08, 256: 2.04)
-      static const int ntenv = getenv("AFN_FPS_NT") ? atoi(getenv("AFN_FPS_NT")) : 0;
-      const int ntc = ntenv > 0 ? ntenv : (P2 == 1 ? 256 : 512);
-      if (push && CNT == 1024 && ntc == 512 && P2 <= 2) {
-        if (P2 == 1) return launch_fps_push<DP, 2, 512>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-        return launch_fps_push<DP, 4, 512>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-      }
-      if (push && CNT == 1024 && ntc == 256 && P2 == 1)
-        return launch_fps_push<DP, 4, 256>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-      if (push && CNT == 1024 && ntc == 128 && P2 == 1)
-        return launch_fps_push<DP, 8, 128>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-      if (push) {
-        if (P2 == 1) return launch_fps_push<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-        if (P2 == 2) return launch_fps_push<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      if (CNT == 1024) {
+        if (P2 == 1) return launch_fps_push<DP, 4, 256>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+        if (P2 == 2) return launch_fps_push<DP, 4, 512>(X, n, d, k, seed, idx, fill, CL, kstop, st);
         return launch_fps_push<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       }
-      if (P2 == 1) return launch_fps_cluster<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-      if (P2 == 2) return launch_fps_cluster<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
-      return launch_fps_cluster<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      if (P2 == 1) return launch_fps_push<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      if (P2 == 2) return launch_fps_push<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+      return launch_fps_push<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
     }
   }
   // choose points per thread P and grid G (G = 1 needs no grid barrier)

@@ -3,8 +3,8 @@
 // on the kNN pattern (Kolotilina-Yeremin).
 // "The computation of each row of G is independent" (L260-261).  This file
 // holds the per-row fallback used when the pair-union path (fsai_sddmm.cu)
-// does not apply: one CTA per row i with pattern J (ascending, i last,
-// |J| <= 128):
+// does not apply (a group's pair union overflows, or rows wider than 128):
+// one CTA per row i with pattern J (ascending, i last, |J| <= 128):
 //   1. Gram  W_J W_J^T  (lower triangle only): W rows gathered in 32-column
 //      chunks through double-buffered shared memory (cp.async), 16x16 threads
 //      with stride-16 register micro-tiles;
@@ -147,39 +147,47 @@ fsai_gram_kernel(const double* __restrict__ X2, int64_t r0, int d, KernelFn kf, 
     }
 }
 
-// one warp per row: blocked left-looking (Crout) Cholesky of S_JJ in shared
-// memory, then g = R^{-T} e_last.  S arrives column-major packed lower (entry
-// (a, t), a >= t, at cmo(a, t, wp)), so the lanes' row-parallel updates read
-// consecutive addresses.  Columns are factored in panels of 4: each loaded
-// L[a][t] feeds 4 FMAs (one per panel column) before the in-panel solve.
-// Shared memory per warp: wmax(wmax+1)/2 + wmax doubles; blockDim = 32 * CW.
-template <int MT>
+// one warp per row: blocked left-looking (Crout) Cholesky of S_JJ, then
+// g = R^{-T} e_last.  S arrives column-major packed lower (entry (a, t),
+// a >= t, at cmo(a, t, wp)) with row stride spk in Sg, so the lanes'
+// row-parallel updates read consecutive addresses.  Columns are factored in
+// panels of 4: each loaded L[a][t] feeds 4 FMAs (one per panel column) before
+// the in-panel solve.  RR: rows per lane (wp <= 32 RR).  GLB = false: the
+// matrix is copied to shared memory (wmax(wmax+1)/2 + wmax doubles per warp,
+// blockDim = 32 * CW); GLB = true (wide rows): factored in place in global
+// memory (L2), g in the spk - wp(wp+1)/2 >= wp doubles after it.
+template <int RR, bool GLB>
 __global__ void __launch_bounds__(256)
 fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict__ rp,
-                 double* __restrict__ Sg, double* __restrict__ gval, int* info) {
-  constexpr int WP = MT * 16;
-  constexpr int SPK = WP * (WP + 1) / 2;
+                 double* __restrict__ Sg, int64_t spk, double* __restrict__ gval, int* info) {
   extern __shared__ __align__(16) double csm[];
   const int CW = blockDim.x >> 5;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t wr = (int64_t)blockIdx.x * CW + wid;
   if (wr >= nrows) return;
-  const int per = wmax * (wmax + 1) / 2 + wmax;
-  double* L = csm + (int64_t)wid * per;
-  double* gs = L + wmax * (wmax + 1) / 2;
   const int64_t i = r0 + wr;
   const int64_t beg = rp[i];
   const int wp = (int)(rp[i + 1] - beg);
   const int ne = wp * (wp + 1) / 2;
-  const double* src = Sg + wr * SPK;
-  for (int e = lane; e < ne; e += 32) L[e] = src[e];
-  __syncwarp();
+  double* L;
+  double* gs;
+  if (GLB) {
+    L = Sg + wr * spk;
+    gs = L + ne;
+  } else {
+    const int per = wmax * (wmax + 1) / 2 + wmax;
+    L = csm + (int64_t)wid * per;
+    gs = L + wmax * (wmax + 1) / 2;
+    const double* src = Sg + wr * spk;
+    for (int e = lane; e < ne; e += 32) L[e] = src[e];
+    __syncwarp();
+  }
   bool bad = false;
   for (int j0 = 0; j0 < wp; j0 += 4) {
     const int nc = min(4, wp - j0);
-    double acc[4][4];
+    double acc[RR][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
+    for (int r = 0; r < RR; ++r) {
       const int a = j0 + lane + 32 * r;
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[r][c] = (c < nc && a < wp && a >= j0 + c) ? L[cmo(a, j0 + c, wp)] : 0.0;
@@ -190,7 +198,7 @@ fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict_
 #pragma unroll
       for (int c = 0; c < 4; ++c) lj[c] = c < nc ? L[cb + j0 + c - t] : 0.0;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < RR; ++r) {
         const int a = j0 + lane + 32 * r;
         const double la = a < wp ? L[cb + a - t] : 0.0;
 #pragma unroll
@@ -207,9 +215,9 @@ fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict_
       if (!(dj > 0.0)) { bad = true; dj = 1.0; }
       const double piv = sqrt(dj);
       const double inv = 1.0 / piv;
-      double lv[4];
+      double lv[RR];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
+      for (int r = 0; r < RR; ++r) {
         const int a = j0 + lane + 32 * r;
         lv[r] = (a > j && a < wp) ? acc[r][c] * inv : 0.0;
         if (a > j && a < wp) L[cmo(a, j, wp)] = lv[r];
@@ -219,7 +227,7 @@ fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict_
       for (int c2 = c + 1; c2 < 4; ++c2) {
         const double l2 = __shfl_sync(0xffffffffu, lv[0], c2);  // L[j0 + c2][j]
 #pragma unroll
-        for (int r = 0; r < 4; ++r) acc[r][c2] = fma(-lv[r], l2, acc[r][c2]);
+        for (int r = 0; r < RR; ++r) acc[r][c2] = fma(-lv[r], l2, acc[r][c2]);
       }
     }
     __syncwarp();
@@ -235,6 +243,77 @@ fsai_chol_kernel(int64_t r0, int64_t nrows, int wmax, const int64_t* __restrict_
     __syncwarp();
   }
   for (int t = lane; t < wp; t += 32) gval[beg + t] = gs[t];
+}
+
+// Wide rows (|J| > 128, e.g. the paper's plain FSAI comparison with 400
+// neighbours): S_JJ = K(X_J, X_J) + mu I - W_J W_J^T, column-major
+// packed lower, one CTA per row straight into global memory (a warp per
+// column, lanes over rows; the W dots, if any, read W through L2).
+__global__ void __launch_bounds__(256)
+fsai_wide_assemble_kernel(const double* __restrict__ X2, int64_t r0, int d, KernelFn kf, double mu,
+                          const double* __restrict__ W, int64_t k, const int64_t* __restrict__ rp,
+                          const int32_t* __restrict__ col, double* __restrict__ Sg, int64_t spk) {
+  extern __shared__ __align__(16) double wsm[];  // X_J (wp x d)
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+  __shared__ int sJ[AFN_W_MAX];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t i = r0 + blockIdx.x;
+  const int64_t beg = rp[i];
+  const int wp = (int)(rp[i + 1] - beg);
+  load_exp2_tab(s_tab);
+  for (int a = tid; a < wp; a += 256) sJ[a] = col[beg + a];
+  __syncthreads();
+  for (int e = tid; e < wp * d; e += 256) {
+    const int a = e / d, c = e - a * d;
+    wsm[e] = X2[(int64_t)sJ[a] * d + c];
+  }
+  __syncthreads();
+  double* S = Sg + (int64_t)blockIdx.x * spk;
+  for (int t = wid; t < wp; t += 8) {
+    const double* wt = W + (int64_t)sJ[t] * k;
+    for (int a = t + lane; a < wp; a += 32) {
+      double kv = a == t ? 1.0 + mu : kern_from_d2(kf, d2_exact_rt(&wsm[a * d], &wsm[t * d], d), s_tab);
+      if (k > 0) {
+        const double* wa = W + (int64_t)sJ[a] * k;
+        double g = 0.0;
+        for (int64_t c = 0; c < k; ++c) g = fma(wa[c], wt[c], g);
+        kv -= g;
+      }
+      S[cmo(a, t, wp)] = kv;
+    }
+  }
+}
+
+afn_status launch_fsai_wide(const double* X2, int64_t row_lo, int64_t row_hi, int d, KernelFn kf, double mu,
+                            const double* W, int64_t k, const int64_t* rp, const int32_t* col, int wmax,
+                            double* gval, int* info, cudaStream_t st) {
+  const int64_t spk = (int64_t)wmax * (wmax + 1) / 2 + wmax;
+  const int64_t NR = row_hi - row_lo;
+  const int64_t batch = std::min<int64_t>(NR, std::max<int64_t>(256, (int64_t)(1LL << 31) / (spk * 8)));
+  double* Sg = nullptr;
+  afn_status s = dalloc((void**)&Sg, sizeof(double) * spk * batch, st);
+  if (s != AFN_OK) return s;
+  const size_t abytes = sizeof(double) * (size_t)wmax * d;
+  AFN_CUDA(cudaFuncSetAttribute(fsai_wide_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)abytes));
+  const int CW = 8;
+  for (int64_t r0 = row_lo; r0 < row_hi; r0 += batch) {
+    const int64_t nr = std::min(batch, row_hi - r0);
+    fsai_wide_assemble_kernel<<<(unsigned)nr, 256, abytes, st>>>(X2, r0, d, kf, mu, W, k, rp, col, Sg, spk);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      note_launch();
+      fsai_chol_kernel<16, true><<<(unsigned)((nr + CW - 1) / CW), CW * 32, 0, st>>>(r0, nr, wmax, rp, Sg, spk,
+                                                                                      gval, info);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) note_launch();
+    }
+    if (e != cudaSuccess) {
+      dfree(Sg, st);
+      return cuda_status(e, "fsai wide rows");
+    }
+  }
+  dfree(Sg, st);
+  return AFN_OK;
 }
 
 template <int MT>
@@ -350,9 +429,10 @@ afn_status launch_chol(int64_t r0, int64_t nrows, const int64_t* rp, double* Sg,
   const size_t per = sizeof(double) * ((size_t)wmax * (wmax + 1) / 2 + wmax);
   const int CW = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(220 * 1024) / per));
   const size_t bytes = per * CW;
-  auto kern = fsai_chol_kernel<MT>;
+  auto kern = fsai_chol_kernel<4, false>;
   AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  kern<<<(unsigned)((nrows + CW - 1) / CW), CW * 32, bytes, st>>>(r0, nrows, wmax, rp, Sg, gval, info);
+  kern<<<(unsigned)((nrows + CW - 1) / CW), CW * 32, bytes, st>>>(r0, nrows, wmax, rp, Sg,
+                                                                 (int64_t)WP * (WP + 1) / 2, gval, info);
   AFN_LAUNCH_CHECK("fsai_chol_kernel");
   return AFN_OK;
 }
@@ -377,7 +457,7 @@ afn_status fsai_run(const double* X2, int64_t N, int d, Kern kn, double mu, cons
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
   if (N <= 0 || row_hi <= row_lo) return AFN_OK;
   // pattern width: all rows have <= w entries (the widest row is the last
-  // one: rows grow then stay at w); the caller guarantees w <= 128
+  // one: rows grow then stay at w); w <= AFN_W_MAX
   int w = 0;
   {
     int64_t h[2];
@@ -398,7 +478,12 @@ afn_status fsai_run(const double* X2, int64_t N, int d, Kern kn, double mu, cons
     case 6: return launch_fsai_split<6>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
     case 7: return launch_fsai_split<7>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
     case 8: return launch_fsai_split<8>(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, gval, d_info, st);
-    default: set_error("fsai: row width %d unsupported (<= 128)", w); return AFN_ERR_ARG;
+    default:
+      if (w > AFN_W_MAX) {
+        set_error("fsai: row width %d unsupported (<= %d)", w, AFN_W_MAX);
+        return AFN_ERR_ARG;
+      }
+      return launch_fsai_wide(X2, row_lo, row_hi, d, kf, mu, W, k, rp, col, w, gval, d_info, st);
   }
 }
 

@@ -33,12 +33,10 @@ namespace afn {
 
 namespace {
 
-constexpr int GA_MAX = 32;   // largest group size (points a per group)
+constexpr int GA = 16;       // group size (points a per group; 32 trades ~27% more dots for ~37% less W
+                             // traffic and measured no faster)
 constexpr int UCAP = 4096;   // max |U_g|
 constexpr int HC = 8192;     // hash capacity (power of two)
-constexpr int UT = 512;      // U columns per GEMM pass (2 per thread; BC = 4: 1024)
-constexpr int KC2 = 8;       // k per pipeline stage
-constexpr int NST = 3;       // pipeline stages
 
 __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -251,275 +249,29 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
 }
 
 // ---------------------------------------------------------------- group GEMM
-// D_g[j][u] = W[a_j] . W[U_g[u]]  for j < GA, u < |U_g|.  Shared-memory
-// stages hold k-pairs interleaved ([kk/2][row][2]) so every cp.async moves
-// 16 B and every operand read is a conflict-free LDS.128.
 __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-template <int GA, int BC>
-__global__ void __launch_bounds__(256, (GA <= 16 && BC <= 2) ? 2 : 1) group_gemm_kernel(const int* __restrict__ sorder, int64_t N,
-                                                            const double* __restrict__ W, int64_t k,
-                                                            const int* __restrict__ Ucount,
-                                                            const int* __restrict__ Ulist,
-                                                            const int64_t* __restrict__ Doff,
-                                                            const int64_t* __restrict__ Poff, int64_t G,
-                                                            double* __restrict__ D) {
-  constexpr int UT = 256 * BC;  // U columns per pass: BC per thread
-  extern __shared__ __align__(16) double gs[];
-  double* sA = gs;                    // [NST][KC2/2][GA][2]
-  double* sB = gs + NST * KC2 * GA;   // [NST][KC2/2][UT][2]
-  __shared__ int s_a[GA];
-  __shared__ int s_u[UT];
-  const int tid = threadIdx.x;
-  // work item = (group g, pass of UT columns of U_g): Poff = scan of passes
-  const int64_t item = blockIdx.x;
-  int64_t glo = 0, ghi = G;  // largest g with Poff[g] <= item
-  while (ghi - glo > 1) {
-    const int64_t mid = (glo + ghi) >> 1;
-    if (Poff[mid] <= item) glo = mid; else ghi = mid;
-  }
-  const int64_t g = glo;
-  const int pass = (int)(item - Poff[g]);
-  const int64_t m0 = g * GA;
-  const int cnt = (int)min((int64_t)GA, N - m0);
-  const int nu = Ucount[g];
-  double* Dg = D + Doff[g];
-  if (tid < GA) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
-  const int64_t nch = (k + KC2 - 1) / KC2;
-  const bool even = (k & 1) == 0;  // 16-byte aligned rows -> 16-byte copies
-  {
-    const int u0 = pass * UT;
-    const int un = min(UT, nu - u0);
-    __syncthreads();
-    for (int t = tid; t < UT; t += 256) s_u[t] = t < un ? Ulist[g * UCAP + u0 + t] : -1;
-    __syncthreads();
-    auto issue = [&](int64_t ch, int buf) {
-      const int64_t c0 = ch * KC2;
-      double* a = sA + buf * KC2 * GA;
-      double* b = sB + buf * KC2 * UT;
-      for (int e = tid; e < (KC2 / 2) * GA; e += 256) {
-        const int j = e / (KC2 / 2), k2 = e - j * (KC2 / 2);
-        const int aj = s_a[j];
-        const int64_t c = c0 + 2 * k2;
-        double* dst = &a[(k2 * GA + j) * 2];
-        if (aj >= 0 && c + 1 < k && even) {
-          cpa16(dst, &W[(int64_t)aj * k + c]);
-        } else {
-          dst[0] = (aj >= 0 && c < k) ? W[(int64_t)aj * k + c] : 0.0;
-          dst[1] = (aj >= 0 && c + 1 < k) ? W[(int64_t)aj * k + c + 1] : 0.0;
-        }
-      }
-      for (int e = tid; e < (KC2 / 2) * UT; e += 256) {
-        const int u = e / (KC2 / 2), k2 = e - u * (KC2 / 2);
-        const int bu = s_u[u];
-        const int64_t c = c0 + 2 * k2;
-        double* dst = &b[(k2 * UT + u) * 2];
-        if (bu >= 0 && c + 1 < k && even) {
-          cpa16(dst, &W[(int64_t)bu * k + c]);
-        } else {
-          dst[0] = (bu >= 0 && c < k) ? W[(int64_t)bu * k + c] : 0.0;
-          dst[1] = (bu >= 0 && c + 1 < k) ? W[(int64_t)bu * k + c + 1] : 0.0;
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    double acc[GA][BC];
-#pragma unroll
-    for (int j = 0; j < GA; ++j)
-#pragma unroll
-      for (int q = 0; q < BC; ++q) acc[j][q] = 0.0;
-#pragma unroll
-    for (int s0 = 0; s0 < NST - 1; ++s0) {
-      if (s0 < nch) issue(s0, s0);
-      else asm volatile("cp.async.commit_group;" ::: "memory");
-    }
-    for (int64_t ch = 0; ch < nch; ++ch) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
-      __syncthreads();
-      const int64_t nx = ch + NST - 1;
-      if (nx < nch) issue(nx, (int)(nx % NST));
-      else asm volatile("cp.async.commit_group;" ::: "memory");
-      const double* a = sA + (int)(ch % NST) * KC2 * GA;
-      const double* b = sB + (int)(ch % NST) * KC2 * UT;
-#pragma unroll
-      for (int k2 = 0; k2 < KC2 / 2; ++k2) {
-        double2 bq[BC];
-#pragma unroll
-        for (int q = 0; q < BC; ++q) bq[q] = *reinterpret_cast<const double2*>(&b[(k2 * UT + tid + 256 * q) * 2]);
-#pragma unroll
-        for (int j = 0; j < GA; ++j) {
-          const double2 av = *reinterpret_cast<const double2*>(&a[(k2 * GA + j) * 2]);
-#pragma unroll
-          for (int q = 0; q < BC; ++q) {
-            acc[j][q] = fma(av.x, bq[q].x, acc[j][q]);
-            acc[j][q] = fma(av.y, bq[q].y, acc[j][q]);
-          }
-        }
-      }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-#pragma unroll
-    for (int j = 0; j < GA; ++j) {
-      if (j >= cnt) break;
-#pragma unroll
-      for (int q = 0; q < BC; ++q)
-        if (tid + 256 * q < un) Dg[(int64_t)j * nu + u0 + tid + 256 * q] = acc[j][q];
-    }
-  }
-}
-
-// Same product with 4 x 8 register tiles (GA = 16 or 32): thread (warp w,
-// lane) owns rows 4 rg + r (rg = lane % RG, RG = GA/4, r < 4) and columns
-// cb + q (cb = 8 (w CGW + lane / RG), CGW = 32/RG column groups per warp,
-// q < 8) of a pass of UTP = 64 CGW columns.  Per k-pair a thread issues
-// 4 + 8 LDS.128 for 64 DFMA (the 16 x 2 layout: 18), and every LDS is one
-// wavefront: W_g rows are stored in the order (r, rg) so the RG row groups of
-// a read are contiguous, and column u sits at the XOR-swizzled slot
-// (u & ~7) | ((u ^ (u >> 3)) & 7) so the column groups of a read hit
-// distinct 16-byte bank groups.  A warp whose columns are all past |U_g|
-// skips the arithmetic (the last pass of a group is partial).  GA = 32 reads
-// each W column once per 32 rows instead of 16 (L2 -> SM traffic is what
-// bounds the 16-row product: 2 DFMA per byte).
-__device__ __forceinline__ int t48_swz(int u) { return (u & ~7) | ((u ^ (u >> 3)) & 7); }
-
-template <int GA, int KC>
-__global__ void __launch_bounds__(256, 2) group_gemm48_kernel(const int* __restrict__ sorder, int64_t N,
-                                                              const double* __restrict__ W, int64_t k,
-                                                              const int* __restrict__ Ucount,
-                                                              const int* __restrict__ Ulist,
-                                                              const int64_t* __restrict__ Doff,
-                                                              const int64_t* __restrict__ Poff, int64_t G,
-                                                              double* __restrict__ D) {
-  constexpr int RG = GA / 4, CGW = 32 / RG, UTP = 64 * CGW;
-  extern __shared__ __align__(16) double gs[];
-  double* sA = gs;                   // [NST][KC/2][GA slots][2]
-  double* sB = gs + NST * KC * GA;   // [NST][KC/2][UTP slots][2]
-  __shared__ int s_a[GA];
-  __shared__ int s_u[UTP];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int rg = lane % RG, cgl = lane / RG;
-  const int64_t item = blockIdx.x;
-  int64_t glo = 0, ghi = G;
-  while (ghi - glo > 1) {
-    const int64_t mid = (glo + ghi) >> 1;
-    if (Poff[mid] <= item) glo = mid; else ghi = mid;
-  }
-  const int64_t g = glo;
-  const int pass = (int)(item - Poff[g]);
-  const int64_t m0 = g * GA;
-  const int cnt = (int)min((int64_t)GA, N - m0);
-  const int nu = Ucount[g];
-  double* Dg = D + Doff[g];
-  const int u0 = pass * UTP;
-  const int un = min(UTP, nu - u0);
-  if (tid < GA) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
-  for (int t = tid; t < UTP; t += 256) s_u[t] = t < un ? Ulist[g * UCAP + u0 + t] : -1;
-  __syncthreads();
-  const int64_t nch = (k + KC - 1) / KC;
-  const bool even = (k & 1) == 0;
-  auto issue = [&](int64_t ch, int buf) {
-    const int64_t c0 = ch * KC;
-    double* a = sA + buf * KC * GA;
-    double* b = sB + buf * KC * UTP;
-    for (int e = tid; e < (KC / 2) * GA; e += 256) {
-      const int j = e / (KC / 2), k2 = e - j * (KC / 2);
-      const int aj = s_a[j];
-      const int64_t c = c0 + 2 * k2;
-      double* dst = &a[(k2 * GA + (j & 3) * RG + (j >> 2)) * 2];
-      if (aj >= 0 && c + 1 < k && even) {
-        cpa16(dst, &W[(int64_t)aj * k + c]);
-      } else {
-        dst[0] = (aj >= 0 && c < k) ? W[(int64_t)aj * k + c] : 0.0;
-        dst[1] = (aj >= 0 && c + 1 < k) ? W[(int64_t)aj * k + c + 1] : 0.0;
-      }
-    }
-    for (int e = tid; e < (KC / 2) * un; e += 256) {  // idle columns are never read back
-      const int u = e / (KC / 2), k2 = e - u * (KC / 2);
-      const int bu = s_u[u];
-      const int64_t c = c0 + 2 * k2;
-      double* dst = &b[(k2 * UTP + t48_swz(u)) * 2];
-      if (c + 1 < k && even) {
-        cpa16(dst, &W[(int64_t)bu * k + c]);
-      } else {
-        dst[0] = c < k ? W[(int64_t)bu * k + c] : 0.0;
-        dst[1] = c + 1 < k ? W[(int64_t)bu * k + c + 1] : 0.0;
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  double acc[4][8];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[r][q] = 0.0;
-#pragma unroll
-  for (int s0 = 0; s0 < NST - 1; ++s0) {
-    if (s0 < nch) issue(s0, s0);
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-  }
-  const bool wact = wid * CGW * 8 < un;
-  const int cb = (wid * CGW + cgl) * 8;  // first column of this thread
-  const int sw = (cb >> 3) & 7;
-  for (int64_t ch = 0; ch < nch; ++ch) {
-    asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory");
-    __syncthreads();
-    const int64_t nx = ch + NST - 1;
-    if (nx < nch) issue(nx, (int)(nx % NST));
-    else asm volatile("cp.async.commit_group;" ::: "memory");
-    if (!wact) continue;
-    const double* a = sA + (int)(ch % NST) * KC * GA;
-    const double* b = sB + (int)(ch % NST) * KC * UTP;
-#pragma unroll
-    for (int k2 = 0; k2 < KC / 2; ++k2) {
-      double2 av[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) av[r] = *reinterpret_cast<const double2*>(&a[(k2 * GA + r * RG + rg) * 2]);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double2 bq = *reinterpret_cast<const double2*>(&b[(k2 * UTP + cb + (q ^ sw)) * 2]);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          acc[r][q] = fma(av[r].x, bq.x, acc[r][q]);
-          acc[r][q] = fma(av[r].y, bq.y, acc[r][q]);
-        }
-      }
-    }
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (!wact) return;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int j = rg * 4 + r;
-    if (j >= cnt) break;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (cb + q < un) Dg[(int64_t)j * nu + u0 + cb + q] = acc[r][q];
-  }
-}
-
-// FP64 tensor-core variant (GA = 16): D_g = W_g W_U^T with mma.sync m8n8k4
-// f64 (SASS DMMA.8x8x4, 256 FMA per warp instruction -- the instruction and
-// operand traffic of the DFMA kernels was their limit, not the FP64 rate).
+// D_g = W_g W_U^T on the FP64 tensor cores: mma.sync m8n8k4 f64 (SASS
+// DMMA.8x8x4, 256 FMA per warp instruction; the DFMA register-tiled kernels
+// it replaced were bound by instruction and operand traffic: C2 7.0 -> 3.7 ms).
 // Warp w owns the 64 columns [64 w, 64 w + 64) of a 512-column pass: 2 x 8
 // m8n8 tiles, 32 accumulators per thread.  Stages hold k-chunks of 8 per row
 // at a 12-double stride (A/B fragment loads: 8 rows x 4 consecutive k per
 // LDS.64 = 2 wavefronts, conflict-free).  Each dot is summed in k order in
 // groups of 4 (the DMMA k-step).
 constexpr int DKC = 8, DKP = 12;
-#ifndef G16_NTL
-#define G16_NTL 8  // n-tiles per warp at GA = 16 (4: 256-column passes, measured 4.31 vs 3.89 ms)
-#endif
+constexpr int G16_NTL = 8;  // n-tiles per warp (4: 256-column passes, measured 4.31 vs 3.89 ms)
+constexpr int DNS = 2;      // cp.async stages (2 CTAs/SM; 3 stages at 1 CTA/SM measured slower)
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
-template <int GA, int NS>
-__global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
+__global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ W, int64_t k,
     const int* __restrict__ Ucount, const int* __restrict__ Ulist, const int64_t* __restrict__ Doff,
     const int64_t* __restrict__ Poff, int64_t G, double* __restrict__ D, const double* __restrict__ X2, int d,
@@ -527,8 +279,9 @@ __global__ void __launch_bounds__(256, NS == 2 ? 2 : 1) group_gemm_dmma_kernel(
   // epilogue: D_g holds the Schur entries S_ab = K(x_a, x_b) + mu delta_ab - W_a . W_b
   // themselves (the factor kernel then only gathers them)
   __shared__ double s_tab[AFN_EXP2_TAB_N];
-  // GA = 16: warp = 2 x 8 m8n8 tiles (64 columns); GA = 32: 4 x 4 (32 columns)
-  constexpr int MTL = GA / 8, NTL = GA == 16 ? G16_NTL : 4, UTP = 8 * NTL * 8;
+  // warp = 2 x 8 m8n8 tiles (64 columns)
+  constexpr int NS = DNS;
+  constexpr int MTL = GA / 8, NTL = G16_NTL, UTP = 8 * NTL * 8;
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                         // [NS][GA][DKP]
   double* sB = gs + NS * GA * DKP;         // [NS][UTP][DKP]
@@ -687,35 +440,25 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
   return bad;
 }
 
-#ifndef AFN_FACTOR_B
-#define AFN_FACTOR_B 8
-#endif
-constexpr int FB = AFN_FACTOR_B;
-#ifndef AFN_FACTOR_MINB
+constexpr int FB = 8;  // gather batch: independent hash probes / D loads in flight per thread
 #define AFN_FACTOR_MINB 4  // <= 128 registers (5 rows per SM forces <= 96: spills, 2.63 vs 2.18 ms on C2)
-#endif  // gather batch: independent hash probes / D loads in flight per thread
 template <int MT>
 __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
-                                                         int64_t row_hi, const double* __restrict__ X2, int d,
-                                                         KernelFn kf, double mu, const int64_t* __restrict__ rp,
+                                                         int64_t row_hi, const int64_t* __restrict__ rp,
                                                          const int32_t* __restrict__ col,
                                                          const int* __restrict__ grp, const int* __restrict__ loc,
                                                          const int* __restrict__ Ucount,
                                                          const int2* __restrict__ Htab,
                                                          const int64_t* __restrict__ Doff,
                                                          const double* __restrict__ D, double* __restrict__ gval,
-                                                         int* info, int lsz, long long* prof, int dS) {
+                                                         int* info, int lsz) {
   constexpr int WP = MT * 16;
-  // prof (debug, AFN_FACTOR_PROF): per CTA clock64 spans of the phases
-  long long pt0 = clock64(), pdiag = 0, ppanel = 0, ptrail = 0, pasm = 0, pm, ppro = 0, pgat = 0;
   extern __shared__ __align__(16) double fsm[];
   // Lm: packed lower S_JJ / L of the wp real rows (rows padded to even length),
   // then one zero row of 16 (stands for the implicit identity rows wp..WP-1
-  // of the 16-column blocking); sX: the wp points.  lsz = Lm doubles.
+  // of the 16-column blocking).  lsz = Lm doubles.
   double* Lm = fsm;
   const double* zrow = fsm + lsz - 16;
-  double* sX = fsm + lsz;
-  __shared__ double s_tab[AFN_EXP2_TAB_N];
   __shared__ double s_inv[WP];
   __shared__ __align__(16) double s_col[32];
   __shared__ int sJ[WP];
@@ -728,7 +471,6 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
   if (i < row_lo || i >= row_hi) return;  // another rank's row
   const int64_t beg = rp[i];
   const int wp = (int)(rp[i + 1] - beg);
-  load_exp2_tab(s_tab);
   if (tid == 0) {
     s_bad = 0;
     int o = 0;
@@ -741,11 +483,6 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
   if (tid < 16) fsm[lsz - 16 + tid] = 0.0;
   for (int a = tid; a < wp; a += FT2) sJ[a] = col[beg + a];
   __syncthreads();
-  if (!dS)  // (the points are only needed to form kernel values here)
-    for (int e = tid; e < wp * d; e += FT2) {
-      const int a = e / d, c = e - a * d;
-      sX[e] = X2[(int64_t)sJ[a] * d + c];
-    }
   // ---- 1. assemble S_JJ (lower).  Per row p (point a = J_p): the group
   // g(a) and the offset of a's row in D_g; then 8 entries per thread at a
   // time (8 independent hash probes, then 8 independent D loads).
@@ -758,14 +495,11 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
   __syncthreads();
   {
     // entry e of the packed lower triangle <-> (p, q), q <= p; a thread takes
-    // B consecutive entries, (p, q) advanced incrementally.  Pass 1: B hash
-    // probes, then B D loads, Lm <- W_a . W_b.  Pass 2 (rolled, one copy of
-    // the kernel code): Lm <- K(x_a, x_b) + mu delta - Lm.
+    // B consecutive entries, (p, q) advanced incrementally: B hash probes,
+    // then B D loads (D holds S_ab itself: the group product's epilogue).
     constexpr int B = FB;
     const int ne = wp * (wp + 1) / 2;
-    if (prof) ppro = clock64() - pt0;
     for (int e0 = tid * B; e0 < ne; e0 += FT2 * B) {
-      if (prof) pm = clock64();
       int p0 = (int)((sqrtf(8.0f * (float)e0 + 1.0f) - 1.0f) * 0.5f);
       while (p0 * (p0 + 1) / 2 > e0) --p0;
       while ((p0 + 1) * (p0 + 2) / 2 <= e0) ++p0;
@@ -806,27 +540,15 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
           if (++q > p) { ++p; q = 0; }
         }
       }
-      if (prof) pgat += clock64() - pm;
-      if (dS) continue;  // D already holds S_ab (tensor-core group product's epilogue)
-      int p = p0, q = q0;
-#pragma unroll 1  // (unrolled: 22 KB more code, slower -- instruction cache)
-      for (int t = 0; t < B && e0 + t < ne; ++t) {
-        const double kv = p == q ? 1.0 + mu : kern_from_d2(kf, d2_exact_rt(&sX[p * d], &sX[q * d], d), s_tab);
-        double* dst = &Lm[s_off[p] + q];
-        *dst = kv - *dst;
-        if (++q > p) { ++p; q = 0; }
-      }
     }
   }
   __syncthreads();
-  if (prof) pasm = clock64() - pt0;
   // ---- 2. blocked right-looking Cholesky of diag(S_JJ, I) in 16-column
   // blocks; the identity rows wp..WP-1 are implicit (never stored: their
   // entries left of the diagonal are 0 and stay 0)
   auto rowp = [&](int a, int kb) -> const double* { return a < wp ? Lm + s_off[a] + kb : zrow; };
 #pragma unroll 1
   for (int kb = 0; kb < wp; kb += 16) {
-    if (prof) pm = clock64();
     // diagonal block: one warp (the others wait at the barrier)
     if (wid == 0) {
       double dr[16], myinv = 1.0;
@@ -847,7 +569,6 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
       }
     }
     __syncthreads();
-    if (prof) { const long long t = clock64(); pdiag += t - pm; pm = t; }
     const int r0 = kb + 16;
     const int m = wp - r0;
     if (m <= 0) break;
@@ -873,7 +594,6 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
       for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(x[c], x[c + 1]);
     }
     __syncthreads();
-    if (prof) { const long long t = clock64(); ppanel += t - pm; pm = t; }
     // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], wp > a >= b >= r0:
     // 8x8 tiles on the FP64 tensor cores (DMMA, 4 k-steps of 4), a warp per
     // tile, two tiles in flight per warp; rows past wp read the zero row
@@ -917,7 +637,6 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
       }
     }
     __syncthreads();
-    if (prof) ptrail += clock64() - pm;
   }
   if (s_bad) {
     if (tid == 0) atomicCAS(info, 0, (int)(i + 1));
@@ -943,57 +662,27 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
       if (j < t) rhs[r] = fma(-lrw[j], gt, rhs[r]);
     }
   }
-  if (prof && tid == 0) {
-    long long* o = prof + 8 * blockIdx.x;
-    o[0] = wp; o[1] = pasm; o[2] = pdiag; o[3] = ppanel; o[4] = ptrail;
-    o[5] = clock64() - pt0 - pasm - pdiag - ppanel - ptrail; o[6] = ppro; o[7] = pgat;
-  }
 }
 
 template <int MT>
 afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t row_hi, int wcap, cudaStream_t st,
-                         const double* X2, int d, KernelFn kf, double mu, const int64_t* rp, const int32_t* col,
-                         const int* grp, const int* loc, const int* Ucount, const int2* Htab,
-                         const int64_t* Doff, const double* D, double* gval, int* info, int dS) {
+                         const int64_t* rp, const int32_t* col, const int* grp, const int* loc, const int* Ucount,
+                         const int2* Htab, const int64_t* Doff, const double* D, double* gval, int* info) {
   constexpr int WP = MT * 16;
   const int wmax = std::min(WP, wcap);
   const int lsz = ((wmax * (wmax + 1) / 2 + (wmax + 1) / 2 + 16) + 1) & ~1;
-  // (dS: no point coordinates in shared memory -> 5 rows per SM at wp = 100)
-  const size_t bytes = sizeof(double) * ((size_t)lsz + (dS ? 0 : (size_t)wmax * d));
+  const size_t bytes = sizeof(double) * (size_t)lsz;
   auto kern = fsai_factor_kernel<MT>;
   AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-  // debug: AFN_FACTOR_PROF=file appends per-row phase cycles (wp, assembly,
-  // diagonal blocks, panels, trailing updates, back substitution, start)
-  static const char* pfile = getenv("AFN_FACTOR_PROF");
-  long long* prof = nullptr;
-  if (pfile && N <= (1 << 24)) AFN_CUDA(cudaMalloc(&prof, sizeof(long long) * 8 * N));
   for (int64_t r0 = 0; r0 < N; r0 += 1 << 30) {
     const int64_t nr = std::min<int64_t>(N - r0, 1 << 30);
-    kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, X2, d, kf, mu, rp, col, grp, loc,
-                                          Ucount, Htab, Doff, D, gval, info, lsz, prof ? prof + 8 * r0 : nullptr,
-                                          dS);
+    kern<<<(unsigned)nr, FT2, bytes, st>>>(rorder + r0, row_lo, row_hi, rp, col, grp, loc, Ucount, Htab, Doff, D,
+                                          gval, info, lsz);
     AFN_LAUNCH_CHECK("fsai_factor_kernel");
-  }
-  if (prof) {
-    std::vector<long long> h((size_t)8 * N);
-    AFN_CUDA(cudaMemcpyAsync(h.data(), prof, sizeof(long long) * 8 * N, cudaMemcpyDeviceToHost, st));
-    AFN_CUDA(cudaStreamSynchronize(st));
-    cudaFree(prof);
-    if (FILE* f = fopen(pfile, "ab")) {
-      fwrite(h.data(), sizeof(long long), h.size(), f);
-      fclose(f);
-    }
   }
   return AFN_OK;
 }
 
-}  // namespace
-
-namespace {
-auto dmk(int GA, int dm) -> decltype(&group_gemm_dmma_kernel<16, 2>) {
-  if (GA == 32) return dm == 3 ? group_gemm_dmma_kernel<32, 3> : group_gemm_dmma_kernel<32, 2>;
-  return dm == 3 ? group_gemm_dmma_kernel<16, 3> : group_gemm_dmma_kernel<16, 2>;
-}
 }  // namespace
 
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
@@ -1007,8 +696,6 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   const cudaStream_t mst = st;
   if (pst == nullptr) pst = st;
   st = pst;
-  // group size (16; 32 trades ~27% more dots for ~37% less W traffic)
-  static const int GA = getenv("AFN_FSAI_GA") && atoi(getenv("AFN_FSAI_GA")) == 32 ? 32 : 16;
   if (d > 16) {
     set_error("fsai_sddmm: d > 16");
     return AFN_ERR_STATE;
@@ -1035,9 +722,9 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   AFN_CUDA(cudaStreamSynchronize(st));
   const int w = N > 1 ? (int)(h2[1] - h2[0]) : 1;
   const int MT = (w + 15) / 16;
-  if (MT < 1 || MT > 8) {
+  if (MT < 1 || MT > 8) {  // (rows wider than 128: the per-row path, fsai.cu)
     set_error("fsai_sddmm: row width %d", w);
-    return AFN_ERR_ARG;
+    return AFN_ERR_STATE;
   }
   // ---- 1. spatial order
   const int dd = d < 3 ? d : 3;
@@ -1118,15 +805,8 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   int64_t* Poff;
   if ((s = get((void**)&pc, sizeof(int) * G)) != AFN_OK) return s;
   if ((s = get((void**)&Poff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
-  // columns of U per GEMM work item.  Default: the 4 x 8 register-tiled
-  // kernel (512 columns per pass at GA = 16, 256 at GA = 32).  AFN_FSAI_T48=0
-  // selects the 16 x 2 layout (256 x BC columns); its BC = 4 reads the
-  // broadcast W_g operand once per 4 columns but needs 244 registers (1 CTA/SM)
-  // and measured slower (C2 10.5 vs 7.0 ms)
-  static const bool t48 = !(getenv("AFN_FSAI_T48") && atoi(getenv("AFN_FSAI_T48")) == 0);
-  static const int BC = getenv("AFN_FSAI_BC") ? std::max(2, std::min(4, atoi(getenv("AFN_FSAI_BC")))) : 2;
-  static const int dm0 = getenv("AFN_FSAI_DMMA") ? atoi(getenv("AFN_FSAI_DMMA")) : 2;
-  const int ut = t48 ? (GA == 32 ? 256 : (dm0 > 0 ? 64 * G16_NTL : 512)) : 256 * (BC >= 4 ? 4 : 2);
+  // columns of U per GEMM work item (a 512-column pass: 8 warps x 64)
+  const int ut = 64 * G16_NTL;
   pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, ut, pc);
   AFN_LAUNCH_CHECK("pass_count_kernel");
   scan_i64_kernel<<<1, 1024, 0, st>>>(pc, G, 1, Poff);
@@ -1137,8 +817,7 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   AFN_CUDA(cudaStreamSynchronize(st));
   // ---- 3. dense group products
   const KernelFn kf = kernel_fn(kn.kind, kn.l);
-  int dS = 0;  // 1: D holds S_ab (DMMA kernel epilogue), 0: the Gram W_a . W_b
-  double* D;
+  double* D;  // S_ab entries (the product's epilogue forms K_ab + mu delta_ab - W_a . W_b)
   if ((s = get((void**)&D, sizeof(double) * (totD > 0 ? totD : 1))) != AFN_OK) return s;
   if (pst != mst) {  // join: the main stream continues after the preparation
     cudaEvent_t ej;
@@ -1149,33 +828,13 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   }
   st = mst;
   {
-    int kc = KC2;
-    decltype(&group_gemm48_kernel<16, 8>) kern;
-    if (t48) {  // (launch_bounds(256, 1) with deeper stages measured slower: 8 warps/SM)
-      kc = GA == 32 ? 16 : 8;
-      kern = GA == 32 ? group_gemm48_kernel<32, 16> : group_gemm48_kernel<16, 8>;
-    } else {
-      kern = GA == 32 ? (ut == 1024 ? group_gemm_kernel<32, 4> : group_gemm_kernel<32, 2>)
-                      : (ut == 1024 ? group_gemm_kernel<16, 4> : group_gemm_kernel<16, 2>);
-    }
-    int bytes = (int)(sizeof(double) * NST * kc * (GA + ut));
-    // FP64 tensor cores (DMMA) for GA = 16 unless AFN_FSAI_DMMA=0; AFN_FSAI_DMMA=3: 3 stages
-    static const int dm = getenv("AFN_FSAI_DMMA") ? atoi(getenv("AFN_FSAI_DMMA")) : 2;
-    if (t48 && dm > 0 && d <= 16) {
-      dS = 1;
-      bytes = (int)(sizeof(double) * (dm == 3 ? 3 : 2) * DKP * (GA + ut));
-      AFN_CUDA(cudaFuncSetAttribute(dmk(GA, dm), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    } else {
-      AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    }
+    const int bytes = (int)(sizeof(double) * DNS * DKP * (GA + ut));
+    AFN_CUDA(cudaFuncSetAttribute(group_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     kt_begin(KT_FSAI_GEMM, st);
-    if (items > 0 && dS) {
-      auto dk = dmk(GA, dm);
-      dk<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D, X2, d, kf, mu);
+    if (items > 0) {
+      group_gemm_dmma_kernel<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D,
+                                                                  X2, d, kf, mu);
       AFN_LAUNCH_CHECK("group_gemm_dmma_kernel");
-    } else if (items > 0) {
-      kern<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D);
-      AFN_LAUNCH_CHECK("group_gemm_kernel");
     }
     kt_end(KT_FSAI_GEMM, st, 2.0 * (double)k * (double)totD);
   }
@@ -1185,9 +844,9 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   kt_begin(KT_FSAI_CHOL, st);
   switch (MT) {
 #define AFN_FACTOR(M) \
-    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info, dS); break;
+    case M: s = launch_factor<M>(sorder, N, row_lo, row_hi, w, st, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
     AFN_FACTOR(1) AFN_FACTOR(2) AFN_FACTOR(3) AFN_FACTOR(4) AFN_FACTOR(5) AFN_FACTOR(6) AFN_FACTOR(7)
-    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, w, st, X2, d, kf, mu, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info, dS); break;
+    default: s = launch_factor<8>(sorder, N, row_lo, row_hi, w, st, rp, col, grp, loc, Ucount, Htab, Doff, D, gval, d_info); break;
 #undef AFN_FACTOR
   }
   if (s != AFN_OK) return s;

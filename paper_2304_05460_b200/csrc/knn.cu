@@ -18,14 +18,19 @@
 namespace afn {
 namespace {
 
-constexpr int KNN_NW = 8;     // warps (rows) per CTA
-constexpr int KNN_CAP = 256;  // candidate buffer per warp (w-1 <= 127)
+constexpr int KNN_NW = 8;  // warps (rows) per CTA
+// candidate buffer per warp (keys + indices in dynamic shared memory): a
+// compaction keeps the w-1 best, so w - 1 + 32 <= CAP
+constexpr int KNN_CAP_S = 256, KNN_CAP_L = 1024;
+inline int knn_cap(int w) { return w - 1 + 32 <= KNN_CAP_S ? KNN_CAP_S : KNN_CAP_L; }
+inline size_t knn_smem(int cap) { return (size_t)KNN_NW * cap * (sizeof(double) + sizeof(int)); }
 
 __device__ __forceinline__ bool key_less(double da, int ja, double db, int jb) {
   return da < db || (da == db && ja < jb);
 }
 
 // bitonic sort of CAP (d2, j) pairs ascending, one warp
+template <int KNN_CAP>
 __device__ void warp_bitonic(double* key, int* idx) {
   const int lane = threadIdx.x & 31;
   for (int k = 2; k <= KNN_CAP; k <<= 1) {
@@ -49,6 +54,7 @@ __device__ void warp_bitonic(double* key, int* idx) {
 }
 
 // ascending sort of CAP ints (INT_MAX padding), one warp
+template <int KNN_CAP>
 __device__ void warp_bitonic_int(int* v) {
   const int lane = threadIdx.x & 31;
   for (int k = 2; k <= KNN_CAP; k <<= 1) {
@@ -66,16 +72,15 @@ __device__ void warp_bitonic_int(int* v) {
   }
 }
 
-// CAND: candidate lists instead of the pattern -- row i keeps its min(w - 1, i)
-// nearest earlier points in (d2, j) order, written to col[(i - row_lo) (w - 1) + t]
-template <int DP, bool CAND = false>
+template <int DP, int KNN_CAP>
 __global__ void __launch_bounds__(KNN_NW * 32)
 knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, int w,
            int32_t* __restrict__ col) {
   constexpr int TILE = DP <= 4 ? 512 : (DP <= 8 ? 256 : 128);
   __shared__ double s_pts[TILE * DP];
-  __shared__ double s_key[KNN_NW][KNN_CAP];
-  __shared__ int s_idx[KNN_NW][KNN_CAP];
+  extern __shared__ double knn_dyn[];  // [KNN_NW][KNN_CAP] keys, then [KNN_NW][KNN_CAP] indices
+  double(*s_key)[KNN_CAP] = reinterpret_cast<double(*)[KNN_CAP]>(knn_dyn);
+  int(*s_idx)[KNN_CAP] = reinterpret_cast<int(*)[KNN_CAP]>(knn_dyn + KNN_NW * KNN_CAP);
 
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   // heaviest rows first (row i scans i candidates)
@@ -98,7 +103,7 @@ knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, 
   auto compact = [&]() {
     for (int t = cnt + lane; t < KNN_CAP; t += 32) { key[t] = DBL_MAX; idx[t] = 0x7fffffff; }
     __syncwarp();
-    warp_bitonic(key, idx);
+    warp_bitonic<KNN_CAP>(key, idx);
     cnt = min(cnt, W1);
     if (cnt == W1 && W1 > 0) { tau_d = key[W1 - 1]; tau_j = idx[W1 - 1]; }
     __syncwarp();
@@ -137,11 +142,6 @@ knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, 
     }
   }
   if (!active) return;
-  if (CAND) {  // key order, no self entry
-    if (W1 > 0) compact();
-    for (int t = lane; t < W1; t += 32) col[(i - row_lo) * (int64_t)(w - 1) + t] = idx[t];
-    return;
-  }
   if (W1 > 0) {
     compact();
     // ascending positions of the kept neighbours
@@ -151,7 +151,7 @@ knn_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int d, 
       idx[t] = v;
     }
     __syncwarp();
-    warp_bitonic_int(idx);
+    warp_bitonic_int<KNN_CAP>(idx);
   }
   // row_ptr(i) = sum_{t<i} min(w, t+1)
   const int64_t wl = w;
@@ -225,11 +225,13 @@ __global__ void knn_cell_fill_kernel(const double* __restrict__ P, int64_t N, co
   cp[pos] = make_double4(P[i * 3], P[i * 3 + 1], P[i * 3 + 2], __longlong_as_double((long long)i));
 }
 
+template <int KNN_CAP>
 __global__ void __launch_bounds__(KNN_NW * 32)
 knn_grid_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, int64_t N, int w, KnnGrid G,
                 const int* __restrict__ start, const double4* __restrict__ cp, int32_t* __restrict__ col) {
-  __shared__ double s_key[KNN_NW][KNN_CAP];
-  __shared__ int s_idx[KNN_NW][KNN_CAP];
+  extern __shared__ double knn_dyn[];
+  double(*s_key)[KNN_CAP] = reinterpret_cast<double(*)[KNN_CAP]>(knn_dyn);
+  int(*s_idx)[KNN_CAP] = reinterpret_cast<int(*)[KNN_CAP]>(knn_dyn + KNN_NW * KNN_CAP);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t i = row_lo + (int64_t)blockIdx.x * KNN_NW + wid;
   if (i >= row_hi) return;
@@ -243,7 +245,7 @@ knn_grid_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, in
   auto compact = [&]() {
     for (int t = cnt + lane; t < KNN_CAP; t += 32) { key[t] = DBL_MAX; idx[t] = 0x7fffffff; }
     __syncwarp();
-    warp_bitonic(key, idx);
+    warp_bitonic<KNN_CAP>(key, idx);
     cnt = min(cnt, W1);
     if (cnt == W1 && W1 > 0) { tau_d = key[W1 - 1]; tau_j = idx[W1 - 1]; }
     __syncwarp();
@@ -324,7 +326,7 @@ knn_grid_kernel(const double* __restrict__ P, int64_t row_lo, int64_t row_hi, in
       idx[t] = v;
     }
     __syncwarp();
-    warp_bitonic_int(idx);
+    warp_bitonic_int<KNN_CAP>(idx);
   }
   const int64_t wl = w;
   const int64_t start_i = (i < wl) ? i * (i + 1) / 2 : wl * (wl + 1) / 2 + (i - wl) * wl;
@@ -404,7 +406,14 @@ afn_status knn_grid_run(const double* P, int64_t N, int w, int32_t* col, int64_t
   knn_cell_fill_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(P, N, cell, start, cntb + M, cp);
   AFN_LAUNCH_CHECK("knn_cell_fill_kernel");
   const int64_t blocks = (hi - lo + KNN_NW - 1) / KNN_NW;
-  knn_grid_kernel<<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(P, lo, hi, N, w, G, start, cp, col);
+  const int cap = knn_cap(w);
+  const size_t bytes = knn_smem(cap);
+  if (cap == KNN_CAP_S) {
+    knn_grid_kernel<KNN_CAP_S><<<(unsigned)blocks, KNN_NW * 32, bytes, st>>>(P, lo, hi, N, w, G, start, cp, col);
+  } else {
+    AFN_CUDA(cudaFuncSetAttribute(knn_grid_kernel<KNN_CAP_L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    knn_grid_kernel<KNN_CAP_L><<<(unsigned)blocks, KNN_NW * 32, bytes, st>>>(P, lo, hi, N, w, G, start, cp, col);
+  }
   AFN_LAUNCH_CHECK("knn_grid_kernel");
   return AFN_OK;
 }
@@ -417,107 +426,21 @@ __global__ void knn_rowptr_kernel(int64_t N, int w, int64_t* __restrict__ rp) {
 }
 
 template <int DP>
-void launch_knn(const double* P, int64_t lo, int64_t hi, int d, int w, int32_t* col, cudaStream_t st) {
+afn_status launch_knn(const double* P, int64_t lo, int64_t hi, int d, int w, int32_t* col, cudaStream_t st) {
   const int64_t blocks = (hi - lo + KNN_NW - 1) / KNN_NW;
-  knn_kernel<DP><<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(P, lo, hi, d, w, col);
-}
-
-// Landmark filter (AFN, FPS landmarks, non-landmarks in ascending original
-// order): row i of the pattern is the non-landmark point o = perm[k + i]; the
-// candidate list of o (its KC nearest EARLIER points of the original set, in
-// (d2, j) order) minus the landmarks, first min(w - 1, i), mapped to positions
-// i' = inv[j] - k and sorted, plus i itself -- exactly the pattern knn_kernel
-// computes on the permuted non-landmark points (same distances; the original
-// order restricted to non-landmarks is the permuted order, so ties break the
-// same way).  A list that runs out before w - 1 survivors (too many landmarks
-// among the KC candidates) sets *fallback.
-__global__ void __launch_bounds__(KNN_NW * 32)
-knn_filter_kernel(const int32_t* __restrict__ cand, int KC, const unsigned char* __restrict__ lflag,
-                  const int64_t* __restrict__ inv, const int64_t* __restrict__ perm, int64_t k, int64_t N2,
-                  int w, int32_t* __restrict__ col, int* fallback) {
-  __shared__ int s_v[KNN_NW][KNN_CAP];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * KNN_NW + wid;
-  if (i >= N2) return;
-  const int64_t o = perm[k + i];
-  const int W1 = (int)min((int64_t)w - 1, i);
-  const int kc = (int)min((int64_t)KC, o);
-  int* v = s_v[wid];
-  int got = 0;
-  for (int b = 0; b < kc && got < W1; b += 32) {
-    const int t = b + lane;
-    int j = -1;
-    bool keep = false;
-    if (t < kc) {
-      j = cand[o * (int64_t)KC + t];
-      keep = !lflag[j];
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    const int pos = got + __popc(m & ((1u << lane) - 1u));
-    if (keep && pos < W1) v[pos] = (int)(inv[j] - k);
-    got += __popc(m);
+  const int cap = knn_cap(w);
+  const size_t bytes = knn_smem(cap);
+  if (cap == KNN_CAP_S) {
+    knn_kernel<DP, KNN_CAP_S><<<(unsigned)blocks, KNN_NW * 32, bytes, st>>>(P, lo, hi, d, w, col);
+  } else {
+    AFN_CUDA(cudaFuncSetAttribute(knn_kernel<DP, KNN_CAP_L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    knn_kernel<DP, KNN_CAP_L><<<(unsigned)blocks, KNN_NW * 32, bytes, st>>>(P, lo, hi, d, w, col);
   }
-  if (got < W1) {
-    if (lane == 0) atomicExch(fallback, 1);
-    return;
-  }
-  for (int t = W1 + lane; t < KNN_CAP; t += 32) v[t] = 0x7fffffff;
-  __syncwarp();
-  warp_bitonic_int(v);
-  const int64_t wl = w;
-  const int64_t start = (i < wl) ? i * (i + 1) / 2 : wl * (wl + 1) / 2 + (i - wl) * wl;
-  for (int t = lane; t < W1; t += 32) col[start + t] = v[t];
-  if (lane == 0) col[start + W1] = (int32_t)i;
-}
-
-__global__ void inv_perm_kernel(const int64_t* __restrict__ perm, int64_t n, int64_t* __restrict__ inv) {
-  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < n) inv[perm[p]] = p;
-}
-
-template <int DP>
-void launch_knn_cand(const double* X, int64_t n, int d, int KC, int32_t* cand, cudaStream_t st) {
-  const int64_t blocks = (n + KNN_NW - 1) / KNN_NW;
-  knn_kernel<DP, true><<<(unsigned)blocks, KNN_NW * 32, 0, st>>>(X, 0, n, d, KC + 1, cand);
+  AFN_LAUNCH_CHECK("knn_kernel");
+  return AFN_OK;
 }
 
 }  // namespace
-
-afn_status knn_candidates(const double* X, int64_t n, int d, int KC, int32_t* cand, cudaStream_t st) {
-  if (KC < 1 || KC > 191) {
-    set_error("knn_candidates: KC=%d unsupported (1..191)", KC);
-    return AFN_ERR_ARG;
-  }
-  if (n <= 0) return AFN_OK;
-  if (d <= 1) launch_knn_cand<1>(X, n, d, KC, cand, st);
-  else if (d <= 2) launch_knn_cand<2>(X, n, d, KC, cand, st);
-  else if (d <= 3) launch_knn_cand<3>(X, n, d, KC, cand, st);
-  else if (d <= 4) launch_knn_cand<4>(X, n, d, KC, cand, st);
-  else if (d <= 8) launch_knn_cand<8>(X, n, d, KC, cand, st);
-  else if (d <= 16) launch_knn_cand<16>(X, n, d, KC, cand, st);
-  else {
-    set_error("knn_candidates: d=%d unsupported (1..16)", d);
-    return AFN_ERR_ARG;
-  }
-  AFN_LAUNCH_CHECK("knn_kernel<cand>");
-  return AFN_OK;
-}
-
-afn_status knn_from_candidates(const int32_t* cand, int KC, const unsigned char* lflag, const int64_t* perm,
-                               int64_t n, int64_t k, int w, int64_t* row_ptr, int32_t* col, int64_t* inv_ws,
-                               int* fallback, cudaStream_t st) {
-  const int64_t N2 = n - k;
-  if (N2 <= 0) return AFN_OK;
-  knn_rowptr_kernel<<<(unsigned)((N2 + 1 + 255) / 256), 256, 0, st>>>(N2, w, row_ptr);
-  AFN_LAUNCH_CHECK("knn_rowptr_kernel");
-  inv_perm_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(perm, n, inv_ws);
-  AFN_LAUNCH_CHECK("inv_perm_kernel");
-  AFN_CUDA(cudaMemsetAsync(fallback, 0, sizeof(int), st));
-  knn_filter_kernel<<<(unsigned)((N2 + KNN_NW - 1) / KNN_NW), KNN_NW * 32, 0, st>>>(cand, KC, lflag, inv_ws, perm, k,
-                                                                                   N2, w, col, fallback);
-  AFN_LAUNCH_CHECK("knn_filter_kernel");
-  return AFN_OK;
-}
 
 int64_t knn_nnz(int64_t N, int w) {
   const int64_t wl = w;
@@ -527,8 +450,8 @@ int64_t knn_nnz(int64_t N, int w) {
 afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, int32_t* col,
                    cudaStream_t st, int64_t row_lo, int64_t row_hi) {
   if (row_hi < 0) row_hi = N;
-  if (w < 1 || w > 128) {
-    set_error("knn: w=%d unsupported (1..128)", w);
+  if (w < 1 || w > AFN_W_MAX) {
+    set_error("knn: w=%d unsupported (1..%d)", w, AFN_W_MAX);
     return AFN_ERR_ARG;
   }
   if (N <= 0) return AFN_OK;
@@ -536,24 +459,20 @@ afn_status knn_run(const double* P, int64_t N, int d, int w, int64_t* row_ptr, i
   AFN_LAUNCH_CHECK("knn_rowptr_kernel");
   if (row_hi <= row_lo) return AFN_OK;
   const int64_t lo = row_lo, hi = row_hi;
-  static const int64_t grid_min = getenv("AFN_KNN_GRID_MIN") ? atoll(getenv("AFN_KNN_GRID_MIN")) : 50000;
+  constexpr int64_t grid_min = 50000;  // (grid path for d = 3 from here on; brute force below)
   if (d == 3 && N >= grid_min && w > 1) {
     afn_status s = knn_grid_run(P, N, w, col, lo, hi, st);
     if (s != AFN_OK) return s;
     return AFN_OK;
   }
-  if (d <= 1) launch_knn<1>(P, lo, hi, d, w, col, st);
-  else if (d <= 2) launch_knn<2>(P, lo, hi, d, w, col, st);
-  else if (d <= 3) launch_knn<3>(P, lo, hi, d, w, col, st);
-  else if (d <= 4) launch_knn<4>(P, lo, hi, d, w, col, st);
-  else if (d <= 8) launch_knn<8>(P, lo, hi, d, w, col, st);
-  else if (d <= 16) launch_knn<16>(P, lo, hi, d, w, col, st);
-  else {
-    set_error("knn: d=%d unsupported (1..16)", d);
-    return AFN_ERR_ARG;
-  }
-  AFN_LAUNCH_CHECK("knn_kernel");
-  return AFN_OK;
+  if (d <= 1) return launch_knn<1>(P, lo, hi, d, w, col, st);
+  if (d <= 2) return launch_knn<2>(P, lo, hi, d, w, col, st);
+  if (d <= 3) return launch_knn<3>(P, lo, hi, d, w, col, st);
+  if (d <= 4) return launch_knn<4>(P, lo, hi, d, w, col, st);
+  if (d <= 8) return launch_knn<8>(P, lo, hi, d, w, col, st);
+  if (d <= 16) return launch_knn<16>(P, lo, hi, d, w, col, st);
+  set_error("knn: d=%d unsupported (1..16)", d);
+  return AFN_ERR_ARG;
 }
 
 }  // namespace afn

@@ -49,7 +49,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_struct_layout(lib):
     import ctypes as C
-    assert lib.abi_version() == 3
+    assert lib.abi_version() == 4
     # afn_params: 2 doubles, int64, 4 int32, int64, uint64, 4 int32 = 72 bytes
     assert C.sizeof(lib.Params) == 72
     assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4 + 4 * 2
@@ -70,9 +70,19 @@ def test_host_pointers_are_rejected_without_compute(lib):
     st = lib._lib.kernel_matvec(None, 0, 3, 0, 1.0, 1e-4, None, None, None)
     assert st == 1
     h = C.c_void_p()
-    p = lib.make_params(1.0, 1e-4, 10, 500)  # w > 128
+    p = lib.make_params(1.0, 1e-4, 10, lib.W_MAX + 1)  # w > AFN_W_MAX
     st = lib._lib.afn_build(X.ctypes.data_as(C.c_void_p), 4, 3, C.byref(p), None, C.byref(h))
     assert st == 1 and not h.value
+    # allocator: alloc and free must come together; NULL/NULL restores the pool
+    fake = C.cast(lib._ALLOC_FN(lambda n, s, c: None), C.c_void_p)
+    assert lib._lib.afn_set_allocator(fake, None, None) == 1
+    assert lib._lib.afn_set_allocator(None, None, None) == 0
+    # CG on host pointers: rejected before any compute
+    b = np.zeros(4)
+    st = lib._lib.afn_cg_solve(None, X.ctypes.data_as(C.c_void_p), 4, 3, 0, 1.0, 1e-4,
+                               b.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p), 1e-4, 10, 0,
+                               None, None)
+    assert st == 1
 
 
 def test_binding_has_no_cpu_fallback():

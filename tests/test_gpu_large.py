@@ -13,8 +13,15 @@ component:
   * PCG: converged with the GPU's true relative residual <= tol, the GPU
     matvec that computes it being checked on sampled rows of the solution.
 
-The C5 case needs ~70 GB of device memory (W is 66.6 GB) and a few minutes of
-oracle time; it is marked slow as well as gpu."""
+C5 (~70 GB of device memory, W is 66.6 GB) runs in the default suite with a
+bounded oracle: the first 1000 FPS landmarks and their fill trace bit-exact
+(FPS is nested, so they are the first 1000 of the device's 8000), the
+landmark set's remaining structure checked directly, and the factor checks
+on the device's landmark set with the oracle's own L, W and FSAI rows.
+
+C3 also has a full oracle PCG (tests/oracle_data/c3_l1.npz, written by
+tools/make_oracle_fixtures.py from oracle/ only): same iteration count +-2,
+solution <= 1e-6 at the oracle's iteration count."""
 import math
 
 import numpy as np
@@ -50,16 +57,18 @@ def sample_rows(N, count, seed):
     return np.array(sorted(s), dtype=np.int64)
 
 
+import json
 import os
 
-# C5 needs ~70 GB of device memory and ~3 min (the plain oracle's FPS over 2^20
-# points for k = 8000 is most of it): opt-in with AFN_TEST_C5=1 (its run is
-# logged in profiles/r01_large_C3_C5.log)
+DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_data")
+
 CASES = [pytest.param("C3", 1.0, id="C3-l1"),
          pytest.param("C4", 1.0, id="C4-l1"),
          pytest.param("C4", 3.0, id="C4-l3"),
-         pytest.param("C5", 1.0, id="C5-l1", marks=[pytest.mark.slow, pytest.mark.skipif(
-             os.environ.get("AFN_TEST_C5") != "1", reason="set AFN_TEST_C5=1 (3 min, 70 GB)")])]
+         pytest.param("C5", 1.0, id="C5-l1")]
+# oracle FPS prefix checked at C5 (the full k = 8000 oracle FPS over 2^20 points
+# takes minutes; the prefix is exact because FPS is nested)
+C5_FPS_PREFIX = 1000
 
 
 @pytest.mark.parametrize("name,l", CASES)
@@ -78,11 +87,21 @@ def test_full_size_component_parity(name, l):
     k = min(cfg.k_cap, max(1, ro["khat"]), n)
     assert inf["k"] == k
 
-    # ---- FPS, all k landmarks and the fill trace: bit-exact
-    idx, fill = O.fps(X, k, 0)
+    # ---- FPS: the landmarks and the fill trace bit-exact (all k,
+    # or the first C5_FPS_PREFIX at C5: nested)
+    kc = k if name != "C5" else C5_FPS_PREFIX
+    idx, fill = O.fps(X, kc, 0)
     perm = h.copy_out(afn.OUT_PERM)
-    assert np.array_equal(perm[:k], idx)
-    assert np.array_equal(h.copy_out(afn.OUT_FILL), fill)
+    assert np.array_equal(perm[:kc], idx)
+    assert np.array_equal(h.copy_out(afn.OUT_FILL)[:kc], fill)
+    idx = perm[:k]  # (== the oracle's when kc == k)
+    assert len(np.unique(idx)) == k and idx.min() >= 0 and idx.max() < n
+    if kc < k:  # the remaining landmarks: each is the farthest point when picked
+        fl = h.copy_out(afn.OUT_FILL)
+        assert np.all(np.diff(fl) <= 0.0)
+        for t in (kc, k // 2, k - 1):
+            d2 = O.sqdist_block(X[idx[t]][None, :], X[idx[:t]]).min()
+            assert d2 == fl[t - 1] ** 2 or math.isclose(math.sqrt(d2), fl[t - 1], rel_tol=1e-15)
     rest = perm[k:]
     mask = np.ones(n, bool)
     mask[idx] = False
@@ -101,7 +120,7 @@ def test_full_size_component_parity(name, l):
     def V_cols(J):  # V = L^{-1} K12 on the columns J
         return sla.solve_triangular(L, O.kernel_block(X1, X2[J], l), lower=True)
 
-    rows = sample_rows(N2, 40, 7)
+    rows = sample_rows(N2, 32 if name == "C5" else 40, 7)
     Wg = h.copy_out_rows(afn.OUT_W, rows)
     Vo = V_cols(rows)
     assert np.abs(Wg - Vo.T).max() <= 1e-11 * max(1.0, np.abs(Vo).max())
@@ -155,4 +174,33 @@ def test_full_size_component_parity(name, l):
     print(f"{name} l={l}: k={k} khat={inf['khat']} iters={rep['iterations']} "
           f"relres_true={rep['relres_true']:.3e} setup_ms={inf['ms_total']:.1f} "
           f"solve_ms={rep['solve_ms']:.1f}")
+    fx = os.path.join(DATA, f"{name.lower()}_l{l:g}.npz")
+    if name == "C3" and os.path.exists(fx):
+        # full oracle PCG (tools/make_oracle_fixtures.py): +-2 iterations,
+        # <= 1e-6 at the oracle's own count
+        o = np.load(fx)
+        assert int(o["k"]) == k
+        assert abs(rep["iterations"] - int(o["iters"])) <= 2, (rep["iterations"], int(o["iters"]))
+        a2, _ = h.pcg_solve(bd, fixed_iters=int(o["iters"]))
+        assert rel(a2.cpu().numpy(), o["a"]) <= 1e-6
     h.close()
+
+
+def test_c4_shape_iteration_trend():
+    """C4's shape (d = 8 N(0,1), mu = 1e-2, l = 1, w = 64) at n = 2^13..2^15 with
+    k = 1000: the device's PCG iteration counts match the oracle's committed
+    ones (tests/oracle_data/c4_shape_iters.json, tools/make_oracle_fixtures.py)
+    within +-2 -- the growth with n behind C4's non-convergence at 2^18 is the
+    method's, not the implementation's (P:L828's "-")."""
+    from synth import gen_points
+    fx = os.path.join(DATA, "c4_shape_iters.json")
+    ref = json.load(open(fx))["results"]
+    for n_s, r in ref.items():
+        n = int(n_s)
+        X, rng = gen_points(n, 8, "normal", 0)
+        b = rng.standard_normal(n)
+        h = afn.afn_build(T(X), afn.make_params(1.0, 1e-2, 1000, 64))
+        _, rep = h.pcg_solve(T(b), tol=1e-4, maxit=500)
+        h.close()
+        assert rep["converged"] == r["converged"]
+        assert abs(rep["iterations"] - r["iters"]) <= 2, (n, rep["iterations"], r["iters"])

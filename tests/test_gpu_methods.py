@@ -156,9 +156,19 @@ def test_emulated_ranks_new_methods(R, method):
     a1, rep1 = h1.pcg_solve(T(b))
     aR, repR = hR.pcg_solve(T(b))
     assert repR["iterations"] == rep1["iterations"] and repR["converged"]
-    # rank-ordered partial sums round differently from one GPU's; the gap is
-    # amplified by the iteration, so the north star's solution bound applies
-    assert rel(aR.cpu().numpy(), a1.cpu().numpy()) <= 1e-6
+    # The rank split sums partials (matvec pair units, F^T r, the Gram) in rank
+    # order: a rounding-level perturbation of every product, which PCG on a
+    # system with cond(K + mu I) ~ 1e5 (mu = 1e-2) amplifies like any other.
+    # Measured, not assumed: the one-GPU solve's own sensitivity to a one-ulp
+    # perturbation of b at the same iteration count bounds the gap (x 100:
+    # the split perturbs every iteration, b only the start), under the north
+    # star's 1e-6.
+    its = rep1["iterations"]
+    sgn = np.random.default_rng(8).choice([-1.0, 1.0], len(b))
+    ap, _ = h1.pcg_solve(T(b * (1.0 + np.finfo(float).eps * sgn)), fixed_iters=its)
+    sens = rel(ap.cpu().numpy(), a1.cpu().numpy())
+    gap = rel(aR.cpu().numpy(), a1.cpu().numpy())
+    assert gap <= max(1e-12, 100.0 * sens) and gap <= 1e-6, (gap, sens)
     hR.close()
     comm.close()
 

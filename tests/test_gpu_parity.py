@@ -267,6 +267,32 @@ def test_c2_pcg_parity(c2_pair):
     assert rel(a2.cpu().numpy(), ao) <= 1e-6
 
 
+@pytest.mark.parametrize("l", [0.1, 0.5, 1.0, 2.0, 5.0, 10.0])
+def test_c2_sweep_pcg_parity(l):
+    """Every l of the bench's C2 sweep with Alg. 1's adaptive k (k = 2000, 130,
+    54, ...) against the oracle's full AFN-PCG (tests/oracle_data, written by
+    tools/make_oracle_fixtures.py from oracle/ only): Alg. 1 bit-exact, the
+    same k, iterations +-2, true residual <= tol, solution <= 1e-6 at the
+    oracle's iteration count."""
+    import os
+    fx = os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle_data", f"c2_l{l:g}.npz")
+    o = np.load(fx)
+    X, b = gen_problem("C2")
+    bd = T(b)
+    h = afn.afn_build(T(X), afn.make_params(l, 1e-4, 2000, 100, k_adaptive=True))
+    inf = h.info()
+    if min(float(o["err_margin"]), float(o["ev_margin"])) >= 1e-9:
+        assert (inf["khat"], inf["r"], inf["refined"]) == (int(o["khat"]), int(o["r"]), int(o["refined"]))
+    assert inf["k"] == int(o["k"])
+    a, rep = h.pcg_solve(bd, tol=1e-4)
+    assert rep["converged"] == bool(o["converged"])
+    assert abs(rep["iterations"] - int(o["iters"])) <= 2, (rep["iterations"], int(o["iters"]))
+    assert rep["relres_true"] <= 1e-4
+    a2, _ = h.pcg_solve(bd, fixed_iters=int(o["iters"]))
+    assert rel(a2.cpu().numpy(), o["a"]) <= 1e-6
+    h.close()
+
+
 # --------------------------------------------------------------------------- Alg. 1
 @pytest.mark.parametrize("cfg_l", [("C1", 1.0), ("C2", 0.1), ("C2", 0.5), ("C2", 1.0), ("C2", 2.0),
                                    ("C2", 5.0), ("C2", 10.0)])
