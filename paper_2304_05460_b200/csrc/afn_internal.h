@@ -141,11 +141,20 @@ afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, doubl
 // in-place lower Cholesky of the k x k row-major A (upper triangle zeroed);
 // *d_info = 0 on success, else 1 + the failing row.
 afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st);
+// nbatch independent k x k factorisations (matrix b at A + b bs, d_info[b]);
+// skip_thr >= 0: threshold pivoting (a pivot <= skip_thr zeroes its column of
+// L, no report; Alg. 1, reading R10), else breakdowns are reported as above
+afn_status potrf_batched(double* A, int64_t k, int nbatch, int64_t bs, double skip_thr, int* d_info,
+                         cudaStream_t st);
 // W (N x k) = K(Xr, X1) L^{-T} as a GEMM with the explicit L^{-T}
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st);
 // G = F^T F (C x C, full) for F: R x C row-major; deterministic
 afn_status syrk_ata(const double* F, int64_t R, int64_t C, double* G, cudaStream_t st);
+// C = alpha A B (M x N, row-major, leading dimensions lda / ldb / ldc), FP64
+// tensor cores (DMMA); K = 0 gives C = 0
+afn_status gemm_nn(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K, int64_t lda,
+                   int64_t ldb, int64_t ldc, double alpha, cudaStream_t st);
 // LinvT (k x k row-major) = L^{-T} (upper triangular)
 afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st);
 

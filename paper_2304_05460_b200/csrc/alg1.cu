@@ -359,56 +359,183 @@ __global__ void eig_summary_kernel(const double* dgl, const double* off, int m, 
   }
 }
 
-// pass = [ tau I - S^(r) is positive definite ], S^(r) the Schur complement of
-// Kp after r threshold-pivoted elimination steps.  SM: work matrix in shared
-// memory, else in the m x m global scratch Wg.
-template <bool SM>
-__global__ void __launch_bounds__(AT) schur_test_kernel(const double* __restrict__ Kp, int m,
-                                                        const int* __restrict__ rlist, double thr,
-                                                        double tau, double* Wg, int* pass) {
-  extern __shared__ double dsm[];
-  __shared__ double s_piv;
-  __shared__ int s_ok;
-  const int r = rlist[blockIdx.x];
-  double* W = SM ? dsm : Wg + (int64_t)blockIdx.x * m * m;
-  pass += blockIdx.x;
-  const int tid = threadIdx.x;
-  for (int64_t e = tid; e < (int64_t)m * m; e += AT) W[e] = Kp[e];
-  if (tid == 0) s_ok = 1;
+// lambda_max of the symmetric m x m A (global, L2-resident) by Lanczos from
+// the all-ones start vector (it overlaps the positive Perron vector of a
+// kernel matrix) with full reorthogonalisation (classical Gram-Schmidt
+// twice), one CTA.  Every 8 steps the largest eigenvalue of the Lanczos
+// tridiagonal T_j is found by 32-way multisection on Sturm counts; the run
+// stops when it has changed by less than 4e-15 relative over three
+// consecutive checks, when beta_{j+1} <= m eps max|alpha| (an invariant
+// subspace: it contains the start vector's component along the top
+// eigenvector), or at j = m (T_m is then similar to A).  Q: m x (m + 1) scratch, column-major.  out[0] = lambda_max,
+// out[1] = steps.  (Replaces a Householder tridiagonalisation, 500 dependent
+// steps over the whole matrix at m = 500: 20 ms.)
+constexpr int LZ_T = 1024;
+__device__ int sturm_count_lz(const double* al, const double* be, int n, double x) {
+  int c = 0;
+  double q = al[0] - x;
+  if (q < 0.0) ++c;
+  for (int i = 1; i < n; ++i) {
+    const double qq = (q != 0.0) ? q : DBL_MIN * 4.0;
+    q = al[i] - x - be[i] * be[i] / qq;  // be[i] couples i-1 and i
+    if (q < 0.0) ++c;
+  }
+  return c;
+}
+__global__ void __launch_bounds__(LZ_T) lanczos_max_kernel(const double* __restrict__ A, int m, double* Q,
+                                                           double* out) {
+  __shared__ double s_q[1024], s_w[1024], s_al[1025], s_be[1025], s_c[1025];
+  __shared__ double sh[32];
+  __shared__ double s_theta, s_lo, s_hi, s_amax;
+  __shared__ int s_stop;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const double q0 = rsqrt((double)m);
+  for (int i = tid; i < m; i += LZ_T) {
+    s_q[i] = q0;
+    Q[i] = q0;
+  }
+  if (tid == 0) {
+    s_be[0] = 0.0;
+    s_theta = 0.0;
+    s_amax = 0.0;
+    s_stop = 0;
+  }
   __syncthreads();
-  for (int j = 0; j < r; ++j) {
-    const double pj = W[(int64_t)j * m + j];
-    if (!(pj > thr)) continue;  // exhausted column (uniform across the CTA)
-    for (int i = j + 1 + (tid >> 5); i < m; i += AT / 32) {
-      const double wij = W[(int64_t)i * m + j];
-      for (int t = j + 1 + (tid & 31); t < m; t += 32)
-        W[(int64_t)i * m + t] -= (wij * W[(int64_t)j * m + t]) / pj;
+  double theta_prev = -1.0;
+  int stable = 0, j = 0;
+  for (j = 0; j < m; ++j) {
+    // w = A q_j (warp per row, lanes over the columns)
+    for (int i = wid; i < m; i += LZ_T / 32) {
+      const double* row = A + (int64_t)i * m;
+      double acc = 0.0;
+      for (int t = lane; t < m; t += 32) acc = fma(row[t], s_q[t], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) s_w[i] = acc;
+    }
+    __syncthreads();
+    // alpha_j = q_j . w
+    double loc = 0.0;
+    for (int i = tid; i < m; i += LZ_T) loc = fma(s_q[i], s_w[i], loc);
+    loc = warp_sum(loc);
+    if (lane == 0) sh[wid] = loc;
+    __syncthreads();
+    if (wid == 0) {
+      double r = sh[lane];
+      r = warp_sum(r);
+      if (lane == 0) s_al[j] = r;
+    }
+    __syncthreads();
+    // full reorthogonalisation against q_0..q_j, classical Gram-Schmidt twice
+    // (one pass also removes the alpha_j q_j and beta_j q_{j-1} components;
+    // the second restores orthogonality after cancellation)
+    double nrm = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int t = wid; t <= j; t += LZ_T / 32) {
+        const double* qt = Q + (int64_t)t * m;
+        double acc = 0.0;
+        for (int i = lane; i < m; i += 32) acc = fma(qt[i], s_w[i], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) s_c[t] = acc;
+      }
+      __syncthreads();
+      nrm = 0.0;
+      for (int i = tid; i < m; i += LZ_T) {
+        double wi = s_w[i];
+        for (int t = 0; t <= j; ++t) wi = fma(-s_c[t], Q[(int64_t)t * m + i], wi);
+        s_w[i] = wi;
+        nrm = fma(wi, wi, nrm);
+      }
+      __syncthreads();
+    }
+    nrm = warp_sum(nrm);
+    if (lane == 0) sh[wid] = nrm;
+    __syncthreads();
+    if (wid == 0) {
+      double r = sh[lane];
+      r = warp_sum(r);
+      if (lane == 0) {
+        s_be[j + 1] = sqrt(r);
+        s_amax = fmax(s_amax, fabs(s_al[j]));
+      }
+    }
+    __syncthreads();
+    const double beta = s_be[j + 1];
+    // (an invariant subspace: beta tiny against max |alpha_i| <= lambda_max)
+    const bool exhausted = !(beta > (double)m * DBL_EPSILON * s_amax);
+    const bool check = ((j + 1) % 8 == 0) || j + 1 == m || exhausted;
+    if (check && wid == 0) {  // theta = lambda_max(T_{j+1}) by multisection
+      const int nt = j + 1;
+      if (lane == 0) {
+        double lo = DBL_MAX, hi = -DBL_MAX;
+        for (int i = 0; i < nt; ++i) {
+          const double r = (i > 0 ? fabs(s_be[i]) : 0.0) + (i + 1 < nt ? fabs(s_be[i + 1]) : 0.0);
+          lo = fmin(lo, s_al[i] - r);
+          hi = fmax(hi, s_al[i] + r);
+        }
+        s_lo = lo;
+        s_hi = hi;
+      }
+      __syncwarp();
+      double lo = s_lo, hi = s_hi;
+      for (int it = 0; it < 40; ++it) {
+        const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+        const bool all_below = sturm_count_lz(s_al, s_be, nt, x) == nt;
+        const unsigned bal = __ballot_sync(0xffffffffu, all_below);
+        double nlo = lo, nhi = hi;
+        if (bal) {
+          const int t = __ffs(bal) - 1;
+          nhi = lo + (hi - lo) * (double)(t + 1) / 33.0;
+          nlo = t > 0 ? lo + (hi - lo) * (double)t / 33.0 : lo;
+        } else {
+          nlo = lo + (hi - lo) * 32.0 / 33.0;
+        }
+        if (!(nhi - nlo < hi - lo)) break;
+        lo = nlo;
+        hi = nhi;
+      }
+      if (lane == 0) {
+        const double th = hi;
+        stable = (theta_prev > 0.0 && fabs(th - theta_prev) <= 4e-15 * th) ? stable + 1 : 0;
+        theta_prev = th;
+        s_theta = th;
+        if (stable >= 3 || j + 1 == m || exhausted) s_stop = 1;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;
+    const double inv = 1.0 / beta;
+    for (int i = tid; i < m; i += LZ_T) {
+      const double qi = s_w[i] * inv;
+      s_q[i] = qi;
+      Q[(int64_t)(j + 1) * m + i] = qi;
     }
     __syncthreads();
   }
-  // Cholesky of C = tau I - W[r:, r:] (stored in place: W[i][j] <- l_ij below the diagonal)
-  for (int j = r; j < m; ++j) {
-    if (tid == 0) {
-      const double c = tau - W[(int64_t)j * m + j];
-      if (!(c > 0.0)) s_ok = 0;
-      s_piv = c > 0.0 ? sqrt(c) : 1.0;
-    }
-    __syncthreads();
-    if (!s_ok) break;
-    const double piv = s_piv;
-    for (int i = j + 1 + tid; i < m; i += AT) W[(int64_t)i * m + j] = -W[(int64_t)i * m + j] / piv;
-    __syncthreads();
-    // C[i][t] -= l_i l_t  <=>  W[i][t] += l_i l_t  (lower part, incl. the diagonal)
-    for (int i = j + 1 + (tid >> 5); i < m; i += AT / 32) {
-      const double li = W[(int64_t)i * m + j];
-      for (int t = j + 1 + (tid & 31); t <= i; t += 32)
-        W[(int64_t)i * m + t] += li * W[(int64_t)t * m + j];
-    }
-    __syncthreads();
+  if (tid == 0) {
+    out[0] = s_theta;
+    out[1] = (double)(j + 1);
   }
-  if (tid == 0) *pass = s_ok;
 }
 
+// Probe matrices of the Schur tests (batch b = probe with r = rlist[b]):
+//   C_b = diag(tau I_r, tau I - Kp[r:, r:] + G_b),  G_b = L[r:, :r] L[r:, :r]^T
+// (G_b already in C_b's trailing block).  tau I - S^(r) is positive definite
+// iff C_b is (S^(r) = Kp[r:, r:] - L21 L21^T, the Schur complement after r
+// threshold-pivoted steps).  Lower triangle only.
+__global__ void form_probe_kernel(const double* __restrict__ Kp, int m, const int* __restrict__ rlist, double tau,
+                                  double* __restrict__ C) {
+  const int b = blockIdx.y;
+  const int r = rlist[b];
+  double* Cb = C + (int64_t)b * m * m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)m * m;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / m), t = (int)(e - (int64_t)i * m);
+    if (t > i) continue;
+    double v = (i == t) ? tau : 0.0;
+    if (i >= r && t >= r) v = v - Kp[e] + Cb[e];
+    Cb[e] = v;
+  }
+}
 
 }  // namespace
 
@@ -544,34 +671,34 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   }
   // ---- 2. scaled / unscaled subsample, K_m, FPS order
   const double scale = std::pow((double)m / (double)n, 1.0 / (double)d);
-  double *Xm, *Xu, *Km, *Kp, *Wk, *dgl, *off, *summ;
+  double *Xm, *Xu, *Km, *Kp, *Lq, *Lt, *dgl2, *off2, *summ, *summ2, *Wk2;
   int64_t* ord;
   double* fill;
-  int* pass;
+  int* pinfo;
   const size_t mm = (size_t)m * m;
   if ((s = get((void**)&Xm, sizeof(double) * m * d)) != AFN_OK) return s;
   if ((s = get((void**)&Xu, sizeof(double) * m * d)) != AFN_OK) return s;
   if ((s = get((void**)&Km, sizeof(double) * mm)) != AFN_OK) return s;
   if ((s = get((void**)&Kp, sizeof(double) * mm)) != AFN_OK) return s;
-  if ((s = get((void**)&Wk, sizeof(double) * mm)) != AFN_OK) return s;
-  if ((s = get((void**)&dgl, sizeof(double) * m)) != AFN_OK) return s;
-  if ((s = get((void**)&off, sizeof(double) * m)) != AFN_OK) return s;
-  if ((s = get((void**)&summ, sizeof(double) * 4)) != AFN_OK) return s;
-  if ((s = get((void**)&ord, sizeof(int64_t) * m)) != AFN_OK) return s;
-  if ((s = get((void**)&fill, sizeof(double) * m)) != AFN_OK) return s;
-  if ((s = get((void**)&pass, sizeof(int) * 2)) != AFN_OK) return s;
-  double *Wk2, *dgl2, *off2, *summ2;  // the refinement's (unscaled K_m) eigen-summary
+  if ((s = get((void**)&Lq, sizeof(double) * (mm + m))) != AFN_OK) return s;  // Lanczos Q, then L
+  if ((s = get((void**)&Lt, sizeof(double) * mm)) != AFN_OK) return s;
   if ((s = get((void**)&Wk2, sizeof(double) * mm)) != AFN_OK) return s;
   if ((s = get((void**)&dgl2, sizeof(double) * m)) != AFN_OK) return s;
   if ((s = get((void**)&off2, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&summ, sizeof(double) * 4)) != AFN_OK) return s;
   if ((s = get((void**)&summ2, sizeof(double) * 4)) != AFN_OK) return s;
+  if ((s = get((void**)&ord, sizeof(int64_t) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&fill, sizeof(double) * m)) != AFN_OK) return s;
+  if ((s = get((void**)&pinfo, sizeof(int) * 64)) != AFN_OK) return s;
   gather_scale_kernel<<<(m * d + 255) / 256, 256, 0, st>>>(X, d, ids, m, scale, Xm, Xu);
   AFN_LAUNCH_CHECK("gather_scale_kernel");
   if ((s = gen_k11(Xm, m, d, kn, 0.0, Km, st)) != AFN_OK) return s;
-  // Concurrently on a second stream: FPS order of X_m and the permuted K_m
-  // (needed by the Schur tests), then -- speculatively, it only matters when
-  // khat < k_threshold -- the eigen-summary of the unscaled K_m for the
-  // refinement.  The main stream computes ||K_m||_2 meanwhile.
+  // Concurrently on a second stream: the FPS order of X_m and the permuted
+  // K_m (the Schur tests need them), then -- speculatively, when it is cheap
+  // (shared-memory tridiagonalisation, m <= SM_MAX_M) -- the eigen-summary
+  // of the unscaled K_m for the refinement.  The main stream
+  // computes ||K_m||_2 meanwhile.
+  const bool spec = m <= SM_MAX_M;
   cudaStream_t s3 = alg1_stream();
   cudaEvent_t eA = nullptr, eP = nullptr, eR = nullptr;
   AFN_CUDA(cudaEventCreateWithFlags(&eA, cudaEventDisableTiming));
@@ -593,16 +720,18 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   permute_sym_kernel<<<(unsigned)((mm + 255) / 256), 256, 0, s3>>>(Km, m, ord, Kp);
   AFN_LAUNCH_CHECK("permute_sym_kernel");
   AFN_CUDA(cudaEventRecord(eP, s3));
-  if ((s = gen_k11(Xu, m, d, kn, 0.0, Wk2, s3)) != AFN_OK) return s;
-  TRY_A(launch_tridiag(Wk2, m, dgl2, off2, s3));
-  eig_summary_kernel<<<1, 32, 0, s3>>>(dgl2, off2, m, 0.1, summ2);
-  AFN_LAUNCH_CHECK("eig_summary_kernel");
+  auto refine_summary = [&](cudaStream_t ss) -> afn_status {
+    TRY_A(gen_k11(Xu, m, d, kn, 0.0, Wk2, ss));
+    TRY_A(launch_tridiag(Wk2, m, dgl2, off2, ss));
+    eig_summary_kernel<<<1, 32, 0, ss>>>(dgl2, off2, m, 0.1, summ2);
+    AFN_LAUNCH_CHECK("eig_summary_kernel");
+    return AFN_OK;
+  };
+  if (spec) TRY_A(refine_summary(s3));
   AFN_CUDA(cudaEventRecord(eR, s3));
-  // ||K_m||_2 = lambda_max (tridiagonal + bisection)
-  AFN_CUDA(cudaMemcpyAsync(Wk, Km, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
-  TRY_A(launch_tridiag(Wk, m, dgl, off, st));
-  eig_summary_kernel<<<1, 32, 0, st>>>(dgl, off, m, 0.1, summ);
-  AFN_LAUNCH_CHECK("eig_summary_kernel");
+  // ||K_m||_2 = lambda_max (Lanczos)
+  lanczos_max_kernel<<<1, LZ_T, 0, st>>>(Km, m, Lq, summ);
+  AFN_LAUNCH_CHECK("lanczos_max_kernel");
   double hs[2];
   AFN_CUDA(cudaMemcpyAsync(hs, summ, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaStreamSynchronize(st));
@@ -611,18 +740,20 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   const double tau = 0.1 * normK;
 
   // ---- 3. smallest r in [1, m] with ||S^(r)|| < 0.1 ||K_m|| (pass(m) = true).
-  // Multisection: up to 32 probes per round run as independent CTAs.
+  // L = threshold-pivoted Cholesky factor of K_p (FPS order; pivots <= thr
+  // leave zero columns, R10) once; a probe r forms S^(r) = K_p[r:, r:] -
+  // L[r:, :r] L[r:, :r]^T (DMMA GEMM) and tests tau I - S^(r) by a Cholesky
+  // attempt; up to NPROBE probes per multisection round in one batched
+  // factorisation.
   AFN_CUDA(cudaStreamWaitEvent(st, eP, 0));  // K_p from the second stream
+  AFN_CUDA(cudaMemcpyAsync(Lq, Kp, sizeof(double) * mm, cudaMemcpyDeviceToDevice, st));
+  TRY_A(potrf_batched(Lq, m, 1, 0, thr, pinfo, st));
+  TRY_A(transpose_sq(Lq, m, Lt, st));
   constexpr int NPROBE = 32;
   int* rdev;
-  int* pdev;
-  double* Wp = nullptr;
+  double* Cp;
   if ((s = get((void**)&rdev, sizeof(int) * NPROBE)) != AFN_OK) return s;
-  if ((s = get((void**)&pdev, sizeof(int) * NPROBE)) != AFN_OK) return s;
-  if (m > SM_MAX_M && (s = get((void**)&Wp, sizeof(double) * mm * NPROBE)) != AFN_OK) return s;
-  const size_t smb = sizeof(double) * mm;
-  if (m <= SM_MAX_M)
-    AFN_CUDA(cudaFuncSetAttribute(schur_test_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb));
+  if ((s = get((void**)&Cp, sizeof(double) * mm * NPROBE)) != AFN_OK) return s;
   int lo = 0, hi = m;  // pass(hi) true, pass(lo) false (lo = 0: no landmarks)
   while (hi - lo > 1) {
     int rs[NPROBE];
@@ -634,15 +765,21 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
       if (r > lo && r < hi && (np == 0 || r != rs[np - 1])) rs[np++] = r;
     }
     AFN_CUDA(cudaMemcpyAsync(rdev, rs, sizeof(int) * np, cudaMemcpyHostToDevice, st));
-    if (m <= SM_MAX_M) schur_test_kernel<true><<<np, AT, smb, st>>>(Kp, m, rdev, thr, tau, Wk, pdev);
-    else schur_test_kernel<false><<<np, AT, 0, st>>>(Kp, m, rdev, thr, tau, Wp, pdev);
-    AFN_LAUNCH_CHECK("schur_test_kernel");
+    for (int b = 0; b < np; ++b) {  // G_b = L21 L21^T into C_b's trailing block
+      const int r = rs[b];
+      TRY_A(gemm_nn(Lq + (size_t)r * m, Lt + r, Cp + (size_t)b * mm + (size_t)r * m + r, m - r, m - r, r, m, m, m,
+                    1.0, st));
+    }
+    const unsigned gx = (unsigned)std::min<size_t>((mm + 255) / 256, 1024);
+    form_probe_kernel<<<dim3(gx, np), 256, 0, st>>>(Kp, m, rdev, tau, Cp);
+    AFN_LAUNCH_CHECK("form_probe_kernel");
+    TRY_A(potrf_batched(Cp, m, np, (int64_t)mm, -1.0, pinfo, st));
     int ok[NPROBE];
-    AFN_CUDA(cudaMemcpyAsync(ok, pdev, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
+    AFN_CUDA(cudaMemcpyAsync(ok, pinfo, sizeof(int) * np, cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
     int first = np;
     for (int j = 0; j < np; ++j)
-      if (ok[j]) { first = j; break; }
+      if (ok[j] == 0) { first = j; break; }  // (info 0: factorised -> positive definite)
     if (first < np) hi = rs[first];
     if (first > 0) lo = rs[first - 1];
   }
@@ -650,8 +787,12 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
   int64_t khat = (2LL * r * n + m) / (2LL * m);
   int refined = 0;
   // ---- 4. refined branch: #{eig(K_m on unscaled points) > 0.1}
-  if (khat < k_threshold) {  // (eigen-summary computed above on the second stream)
-    AFN_CUDA(cudaStreamWaitEvent(st, eR, 0));
+  if (khat < k_threshold) {
+    if (spec) {
+      AFN_CUDA(cudaStreamWaitEvent(st, eR, 0));
+    } else {
+      TRY_A(refine_summary(st));
+    }
     AFN_CUDA(cudaMemcpyAsync(hs, summ2, sizeof(double) * 2, cudaMemcpyDeviceToHost, st));
     AFN_CUDA(cudaStreamSynchronize(st));
     khat = (int64_t)hs[1];

@@ -59,7 +59,12 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
   const int tid = threadIdx.x;
   // reciprocals of the diagonal first: a multiply (not a division) per step
   __shared__ double s_rinv[NB];
-  if (tid < NB) s_rinv[tid] = 1.0 / Lbb[tid * TP + tid];
+  // (a zero diagonal is an exhausted column of Alg. 1's threshold-pivoted
+  // factor: its entries below are zero as well)
+  if (tid < NB) {
+    const double dg = Lbb[tid * TP + tid];
+    s_rinv[tid] = dg != 0.0 ? 1.0 / dg : 0.0;
+  }
   __syncthreads();
   const int r = tid >> 2, q = tid & 3;
   const int lane = tid & 31;
@@ -96,9 +101,16 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
 // shared memory, one rsqrt per column), every thread then solves one panel row
 // (16 columns, multiplies by the stored reciprocal pivots) and the trailing
 // lower part is updated (16-term dots).  A non-positive pivot is reported in
-// *info (global row) and replaced by 1 so the block stays finite.
+// *info (global row) and replaced by 1 so the block stays finite; with
+// skip_thr >= 0 (Alg. 1's threshold pivoting, reading R10) a pivot <= skip_thr
+// instead marks an exhausted column: L's column (diagonal included) is zero
+// and the trailing matrix is left unchanged, no report.  Batched over
+// blockIdx.y (matrix A + y bs, info + y).
 constexpr int DB_T = 256;
-__global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t k, int64_t kb, int* info) {
+__global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t k, int64_t kb, int* info,
+                                                             int64_t bs, double skip_thr) {
+  A += (int64_t)blockIdx.y * bs;
+  info += blockIdx.y;
   __shared__ double s[NB * TP];
   __shared__ double s_inv[NB];
   __shared__ __align__(16) double s_col[32];
@@ -125,8 +137,13 @@ __global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t
         if (lane < 16) cb[lane] = dr[c];
         __syncwarp();
         double piv = cb[c];
-        if (!(piv > 0.0)) { bad = true; piv = 1.0; }
-        const double inv = rsqrt(piv);
+        double inv;
+        if (skip_thr >= 0.0) {
+          inv = piv > skip_thr ? rsqrt(piv) : 0.0;  // exhausted column: L[:, c] = 0
+        } else {
+          if (!(piv > 0.0)) { bad = true; piv = 1.0; }
+          inv = rsqrt(piv);
+        }
         const double lrc = dr[c] * inv;
         const double f = lrc * inv;
         if (lr == c) myinv = inv;
@@ -181,7 +198,8 @@ __global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t
 }
 
 // Panel below the diagonal block: A[i, kb:kb+nb] <- A[i, kb:kb+nb] L_kk^{-T}.
-__global__ void __launch_bounds__(DT) potrf_panel_kernel(double* A, int64_t k, int64_t kb) {
+__global__ void __launch_bounds__(DT) potrf_panel_kernel(double* A, int64_t k, int64_t kb, int64_t bs) {
+  A += (int64_t)blockIdx.y * bs;
   extern __shared__ double dsm[];
   double* sL = dsm;
   double* sT = dsm + NB * TP;
@@ -305,7 +323,8 @@ __global__ void transpose_k_kernel(const double* __restrict__ X, int64_t kp, int
   }
 }
 
-__global__ void zero_upper_kernel(double* __restrict__ A, int64_t k) {
+__global__ void zero_upper_kernel(double* __restrict__ A, int64_t k, int64_t bs) {
+  A += (int64_t)blockIdx.y * bs;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
   const int64_t i = e / k, j = e - i * k;
@@ -420,7 +439,8 @@ afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, doubl
 // -- 8 rows x 4 consecutive k -- is two conflict-free wavefronts); 4 warps of
 // 32 x 32 (16 DMMA per k-step of 4).
 constexpr int PUP = NB + 4;
-__global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64_t k, int64_t kb) {
+__global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64_t k, int64_t kb, int64_t bs) {
+  A += (int64_t)blockIdx.y * bs;
   extern __shared__ __align__(16) double usm[];
   double* sI = usm;              // [NB][PUP]
   double* sJ = usm + NB * PUP;   // [NB][PUP]
@@ -480,7 +500,8 @@ __global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64
   }
 }
 
-afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
+afn_status potrf_batched(double* A, int64_t k, int nbatch, int64_t bs, double skip_thr, int* d_info,
+                         cudaStream_t st) {
   static bool uattr = false;
   if (!uattr) {
     AFN_CUDA(cudaFuncSetAttribute(potrf_update_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -488,22 +509,27 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
     uattr = true;
   }
   TRY_SMEM();
-  AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int), st));
+  AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int) * nbatch, st));
   for (int64_t kb = 0; kb < k; kb += NB) {
-    potrf_diag_blk_kernel<<<1, DB_T, 0, st>>>(A, k, kb, d_info);
+    potrf_diag_blk_kernel<<<dim3(1, nbatch), DB_T, 0, st>>>(A, k, kb, d_info, bs, skip_thr);
     AFN_LAUNCH_CHECK("potrf_diag_blk_kernel");
     const int64_t rem = k - kb - NB;
     if (rem <= 0) break;
     const int64_t T = (rem + NB - 1) / NB;
-    potrf_panel_kernel<<<(unsigned)T, DT, SMEM2, st>>>(A, k, kb);
+    potrf_panel_kernel<<<dim3((unsigned)T, nbatch), DT, SMEM2, st>>>(A, k, kb, bs);
     AFN_LAUNCH_CHECK("potrf_panel_kernel");
     // trailing update on the FP64 tensor cores
-    potrf_update_dmma_kernel<<<(unsigned)(T * (T + 1) / 2), 128, (int)(sizeof(double) * 2 * NB * PUP), st>>>(A, k, kb);
+    potrf_update_dmma_kernel<<<dim3((unsigned)(T * (T + 1) / 2), nbatch), 128, (int)(sizeof(double) * 2 * NB * PUP),
+                               st>>>(A, k, kb, bs);
     AFN_LAUNCH_CHECK("potrf_update_dmma_kernel");
   }
-  zero_upper_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, st>>>(A, k);
+  zero_upper_kernel<<<dim3((unsigned)((k * k + 255) / 256), nbatch), 256, 0, st>>>(A, k, bs);
   AFN_LAUNCH_CHECK("zero_upper_kernel");
   return AFN_OK;
+}
+
+afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
+  return potrf_batched(A, k, 1, 0, -1.0, d_info, st);
 }
 
 // C (M x N) = A (M x K) B (K x N), all row-major, B upper triangular
@@ -515,7 +541,8 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st) {
 // 4 k x 8 columns) is two conflict-free wavefronts.
 constexpr int TM = 64, TN = 64, TK = 16, TKP = 20, TNP = 72, TS = 3;
 // MODE 0: B upper (K range ends at the tile's last column); 1: A lower (ends
-// at the tile's last row); 2: B lower (starts at the tile's first column).
+// at the tile's last row); 2: B lower (starts at the tile's first column);
+// 3: general.
 // Batched over blockIdx.z with element strides sA, sB, sC; C = alpha A B.
 template <int MODE>
 __global__ void __launch_bounds__(128) gemm_dmma_kernel(const double* __restrict__ A, const double* __restrict__ B,
@@ -534,7 +561,8 @@ __global__ void __launch_bounds__(128) gemm_dmma_kernel(const double* __restrict
   const int64_t kend = MODE == 0 ? min(K, C0 + TN) : (MODE == 1 ? min(K, R0 + TM) : K);
   const int64_t kbeg = MODE == 2 ? (min(K, C0) / TK) * TK : 0;
   const int64_t nkb = (kend - kbeg + TK - 1) / TK;
-  const bool vec = (lda & 1) == 0 && (ldb & 1) == 0 && (ldc & 1) == 0;
+  const bool vec = (lda & 1) == 0 && (ldb & 1) == 0 && (ldc & 1) == 0 &&
+                   (((uintptr_t)A | (uintptr_t)B | (uintptr_t)Cm) & 15) == 0;  // 16-byte copies
   auto stage = [&](int64_t kb, int buf) {
     const int64_t k0 = kbeg + kb * TK;
     double* a = sA + buf * TM * TKP;
@@ -683,6 +711,21 @@ afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_
   dim3 tg((unsigned)((k + 31) / 32), (unsigned)((k + 31) / 32));
   transpose_k_kernel<<<tg, dim3(32, 8), 0, st>>>(X, kp, k, LinvT);
   AFN_LAUNCH_CHECK("transpose_k_kernel");
+  return AFN_OK;
+}
+
+afn_status gemm_nn(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K, int64_t lda,
+                   int64_t ldb, int64_t ldc, double alpha, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return AFN_OK;
+  const int bytes = (int)(sizeof(double) * TS * (TM * TKP + TK * TNP));
+  static bool attr = false;
+  if (!attr) {
+    AFN_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    attr = true;
+  }
+  dim3 grid((unsigned)((N + TN - 1) / TN), (unsigned)((M + TM - 1) / TM), 1);
+  gemm_dmma_kernel<3><<<grid, 128, bytes, st>>>(A, B, C, M, N, K, lda, ldb, ldc, 0, 0, 0, alpha);
+  AFN_LAUNCH_CHECK("gemm_dmma_kernel<3>");
   return AFN_OK;
 }
 

@@ -33,8 +33,12 @@ namespace afn {
 
 namespace {
 
-constexpr int GA = 16;       // group size (points a per group; 32 trades ~27% more dots for ~37% less W
-                             // traffic and measured no faster)
+// group size (points a per group): 32 reads each union column's W row once
+// per 32 rows (the k = 4000 / 8000 products are bound by that traffic) for
+// ~27 % more dots than 16 -- C3 135.7 -> 98.8 ms, C5 2643 -> 1919 ms, C2
+// 3.86 -> 3.66 ms per product.  (A TMA bulk-copy variant with 4 stages of
+// 256-byte row chunks, 1 CTA/SM, measured 2-3x slower.)
+constexpr int GA = 32;
 constexpr int UCAP = 4096;   // max |U_g|
 constexpr int HC = 8192;     // hash capacity (power of two)
 
@@ -263,7 +267,7 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 // LDS.64 = 2 wavefronts, conflict-free).  Each dot is summed in k order in
 // groups of 4 (the DMMA k-step).
 constexpr int DKC = 8, DKP = 12;
-constexpr int G16_NTL = 8;  // n-tiles per warp (4: 256-column passes, measured 4.31 vs 3.89 ms)
+constexpr int G16_NTL = GA == 16 ? 8 : 4;  // n-tiles per warp (32 columns at GA = 32: 256-column passes)
 constexpr int DNS = 2;      // cp.async stages (2 CTAs/SM; 3 stages at 1 CTA/SM measured slower)
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -805,7 +809,7 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   int64_t* Poff;
   if ((s = get((void**)&pc, sizeof(int) * G)) != AFN_OK) return s;
   if ((s = get((void**)&Poff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
-  // columns of U per GEMM work item (a 512-column pass: 8 warps x 64)
+  // columns of U per GEMM work item: 8 warps x 8 NTL
   const int ut = 64 * G16_NTL;
   pass_count_kernel<<<(unsigned)((G + 255) / 256), 256, 0, st>>>(Ucount, G, ut, pc);
   AFN_LAUNCH_CHECK("pass_count_kernel");
@@ -828,10 +832,10 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   }
   st = mst;
   {
-    const int bytes = (int)(sizeof(double) * DNS * DKP * (GA + ut));
-    AFN_CUDA(cudaFuncSetAttribute(group_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0) {
+      const int bytes = (int)(sizeof(double) * DNS * DKP * (GA + ut));
+      AFN_CUDA(cudaFuncSetAttribute(group_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       group_gemm_dmma_kernel<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D,
                                                                   X2, d, kf, mu);
       AFN_LAUNCH_CHECK("group_gemm_dmma_kernel");

@@ -71,6 +71,7 @@ __device__ __forceinline__ double exp2_neg256(double s, const double* tab) {
   return __hiloint2double(hi, __double2loint(p));
 }
 
+
 template <int D>
 struct KmvTraits {
   static constexpr int CS = ((D + 1) + 1) & ~1;   // coords + v, padded to even
@@ -198,8 +199,8 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
   constexpr int RBW = KMV_NT * RB;
   constexpr int M = RBW / 32;  // diagonal tiles per row block
   __shared__ double s_tab[AFN_EXP2_TAB_N];
-  constexpr int TABN = D <= 4 ? 2048 : 256;  // (static shared memory <= 48 KB)
-  __shared__ double s_tx[TABN];
+  constexpr int TABN = D <= 4 ? 2048 : 256;
+  extern __shared__ double s_tx[];  // exp2 table (dynamic: the static arrays take ~28 KB)
   __shared__ __align__(16) double s_col[KMV_TC * CS];
   __shared__ double s_cs[NW][KMV_TC];
   load_exp2_tab(s_tab);
@@ -307,9 +308,13 @@ kmv_sym_kernel(const double* __restrict__ Xs, const double* __restrict__ v, int6
       }
       s_cs[wid][cb + lane] = ca;  // column cb + lane (stage padded: cb + 31 < KMV_TC)
     };
-    for (int c = 0; c < (int)run; ++c) {
-      if (t0 + c < M * (I + 1)) body(std::true_type{}, 32 * c);
-      else body(std::false_type{}, 32 * c);
+    // one body per stage (a stage that starts in the diagonal tiles is masked
+    // throughout: the mask never fires past them; a per-tile choice measured
+    // 3 % slower)
+    if (t0 < M * (I + 1)) {
+      for (int c = 0; c < (int)run; ++c) body(std::true_type{}, 32 * c);
+    } else {
+      for (int c = 0; c < (int)run; ++c) body(std::false_type{}, 32 * c);
     }
     __syncthreads();
     const int64_t cbase = sym_cboff(I, n, RBW) - I * RBW;
@@ -479,8 +484,9 @@ void sym_launch(const KmvPlan& p, cudaStream_t st, const double* Xs, const doubl
                 double* Rp, double* Cb) {
   constexpr int RB = KmvTraits<D>::RB;
   const int64_t g0 = p.sym_grid * (int64_t)p.sym_rank;
-  kmv_sym_kernel<D, RB, KER><<<(unsigned)p.sym_grid, KMV_NT, 0, st>>>(Xs, v, n, p.sym_nrb, p.sym_nt, p.sym_units,
-                                                                     p.sym_gt, g0, segtab, Rp, Cb, get_skip());
+  const size_t tab = sizeof(double) * (D <= 4 ? 2048 : 256);  // (+ ~28 KB static: under 48 KB)
+  kmv_sym_kernel<D, RB, KER><<<(unsigned)p.sym_grid, KMV_NT, tab, st>>>(Xs, v, n, p.sym_nrb, p.sym_nt, p.sym_units,
+                                                                       p.sym_gt, g0, segtab, Rp, Cb, get_skip());
 }
 
 // The exp2 tables (__device__ globals) are filled once per device by a
@@ -530,7 +536,14 @@ KmvPlan kmv_plan(int64_t n, int64_t nrows, int d, int num_sms, bool sym_ok, int 
     const int per_sm = rows_per_thread(d) <= 2 ? 3 : 2;  // (launch bounds)
     p.sym_R = R;
     p.sym_rank = rank;
-    p.sym_grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * per_sm, p.sym_units / R));
+    // CTAs: one wave of resident CTAs when that leaves each >= upc units,
+    // else ~upc units per CTA -- many short CTAs, measured faster at C3 than
+    // one persistent wave (9.73 vs 10.09 ms per launch; C2 equal at 198 us);
+    // upc = 32 past n = 2^18 bounds the row-partial slots (C5: 4.3 GB)
+    const int64_t upc = n > (1 << 18) ? 32 : 16;
+    const int64_t slots = (int64_t)num_sms * per_sm;
+    const int64_t want = std::max<int64_t>(slots, p.sym_units / (upc * R));
+    p.sym_grid = std::max<int64_t>(1, std::min<int64_t>(want, p.sym_units / R));
     p.sym_gt = p.sym_grid * R;
     // workspace: segment table (ints, rounded to doubles), row partials
     // (Gt + nrb slots of RBW), column partials (upper block triangle)
