@@ -9,6 +9,8 @@
   * memory: handles built and destroyed on a non-default stream keep the pool
     flat; the optional caller allocator (PyTorch's caching allocator) gives
     bit-identical results."""
+import os
+
 import numpy as np
 import pytest
 
@@ -193,3 +195,58 @@ def test_torch_allocator_bit_identical():
             assert torch.equal(a1, a0)
     finally:
         afn.use_torch_allocator(False)
+
+
+# ------------------------------------------------------------------ races by repetition
+def test_repetition_bit_identical():
+    """compute-sanitizer is closed on this pool, so the synchronisation of the
+    cluster FPS (st.async + mbarrier inboxes), the persistent-grid FPS
+    (software grid barrier), the last-block-done reductions (dots, the
+    matvec's fused p.q) and the balanced matvec's slot writes are checked by
+    repetition: a race would show up as run-to-run differences.  Every result
+    must be bit-identical across repeated runs on the same inputs."""
+    X, b = gen_problem("C2")
+    Xd, bd = T(X), T(b)
+    ref = [t.clone() for t in afn.afn_fps(Xd, 2000, 0)]          # cluster path (n <= 64K)
+    Xg, _ = gen_points(70000, 3, "cube", 2)
+    Xgd = T(Xg)
+    refg = [t.clone() for t in afn.afn_fps(Xgd, 300, 0)]         # persistent-grid path
+    y0 = afn.kernel_matvec(Xd, 1.0, 1e-4, bd).clone()
+    h = afn.afn_build(Xd, afn.make_params(2.0, 1e-4, 2000, 100, k_adaptive=True))
+    a0, r0 = h.pcg_solve(bd)
+    a0 = a0.clone()
+    k0 = afn.afn_estimate_rank(Xd, 1.0)
+    for _ in range(20):
+        assert all(torch.equal(x, y) for x, y in zip(afn.afn_fps(Xd, 2000, 0), ref))
+        assert all(torch.equal(x, y) for x, y in zip(afn.afn_fps(Xgd, 300, 0), refg))
+        assert torch.equal(afn.kernel_matvec(Xd, 1.0, 1e-4, bd), y0)
+        assert afn.afn_estimate_rank(Xd, 1.0) == k0
+    for _ in range(5):
+        a1, r1 = h.pcg_solve(bd)
+        assert torch.equal(a1, a0) and r1["iterations"] == r0["iterations"]
+    h2 = afn.afn_build(Xd, afn.make_params(2.0, 1e-4, 2000, 100, k_adaptive=True))
+    assert np.array_equal(h2.copy_out(afn.OUT_GVAL), h.copy_out(afn.OUT_GVAL))
+    h.close()
+    h2.close()
+
+
+# ------------------------------------------------------------------ NCCL code path
+@pytest.mark.parametrize("R", [2, 3])
+def test_nccl_path_with_thread_ranks(R, tmp_path):
+    """The communicator's NCCL code path (comm.cu: in-place and packed
+    all-gathers, the build-status exchange, asynchronous-error polling), run
+    with R ranks as host threads of one process on one GPU through a fake
+    libnccl (tests/fake_nccl/fake_nccl.cpp: stream-event dependencies only,
+    no kernel waits on another rank).  Only one GPU is available, so this
+    is what exercises that path beyond nranks = 1."""
+    import subprocess
+    import sys as _sys
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fake_nccl")
+    lib = str(tmp_path / "libfakenccl.so")
+    import nvidia.nccl
+    inc = os.path.join(nvidia.nccl.__path__[0], "include")
+    subprocess.run(["/usr/local/cuda/bin/nvcc", "-shared", "-Xcompiler", "-fPIC", "-O2", "-std=c++17", "-I", inc,
+                    os.path.join(here, "fake_nccl.cpp"), "-o", lib], check=True, capture_output=True)
+    r = subprocess.run([_sys.executable, os.path.join(here, "run_case.py"), lib, str(R)], capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "fake-nccl ok" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
