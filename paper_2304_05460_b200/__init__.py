@@ -277,9 +277,9 @@ def shard_rows(n, k, nranks, rank):
     return tuple(out)
 
 
-def nccl_unique_id() -> bytes:
+def nccl_unique_id(nccl_path=None) -> bytes:
     buf = C.create_string_buffer(COMM_ID_BYTES)
-    path = nccl_library_path()
+    path = nccl_path or nccl_library_path()
     _check(_lib.afn_comm_unique_id(buf, path.encode() if path else None), "afn_comm_unique_id")
     return buf.raw
 
@@ -303,10 +303,10 @@ class Comm:
         self.nranks, self.rank, self.nlocal = nranks, rank, nlocal
 
     @classmethod
-    def nccl(cls, unique_id: bytes, nranks: int, rank: int):
+    def nccl(cls, unique_id: bytes, nranks: int, rank: int, nccl_path=None):
         """One process per GPU; every rank passes rank 0's nccl_unique_id()."""
         c = C.c_void_p()
-        path = nccl_library_path()
+        path = nccl_path or nccl_library_path()
         _check(_lib.afn_comm_init(C.c_char_p(unique_id), int(nranks), int(rank),
                                   path.encode() if path else None, C.byref(c)), "afn_comm_init")
         return cls(c, nranks, rank, 1)

@@ -300,10 +300,15 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned a, unsigned ph) {
       : "memory");
 }
 
-template <int DP, int P, int NT>
+// SP: the points live in dynamic shared memory ([s][c][thread], conflict-free)
+// instead of registers -- 8 points per thread at 1024 threads, so one cluster
+// of 16 CTAs covers n = 131072 (C3) instead of 65536; the running minima stay
+// in registers.
+template <int DP, int P, int NT, bool SP = false>
 __global__ void __launch_bounds__(NT, 1)
 fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
                 int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop) {
+  extern __shared__ __align__(16) double s_pts[];
   constexpr int KI = DP + 2;          // slot: d2, index, point (DP), early-stop sample (KI)
   constexpr int S = (KI + 2) & ~1;    // even length (16-byte stores)
   constexpr int NW = NT / 32;
@@ -326,23 +331,24 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_kend = k;
   }
-  double pts[P][DP];
+  double pts[SP ? 1 : P][DP];
   double mind[P];
   double y[DP];
+  auto pt = [&](int sidx, int c) -> double& {
+    return SP ? s_pts[(sidx * DP + c) * NT + tid] : pts[SP ? 0 : sidx][c];
+  };
 #pragma unroll
   for (int c = 0; c < DP; ++c) y[c] = c < d ? X[seed * d + c] : 0.0;
 #pragma unroll
   for (int s = 0; s < P; ++s) {
     const int64_t i = gtid + s * stride;
-    if (i < n) {
+    double q[DP];
 #pragma unroll
-      for (int c = 0; c < DP; ++c) pts[s][c] = c < d ? X[i * d + c] : 0.0;
-      mind[s] = (i == seed) ? -1.0 : d2_exact<DP>(pts[s], y);
-    } else {
-#pragma unroll
-      for (int c = 0; c < DP; ++c) pts[s][c] = 0.0;
-      mind[s] = -2.0;
+    for (int c = 0; c < DP; ++c) {
+      q[c] = (i < n && c < d) ? X[i * d + c] : 0.0;
+      pt(s, c) = q[c];
     }
+    mind[s] = i < n ? ((i == seed) ? -1.0 : d2_exact<DP>(q, y)) : -2.0;
   }
   if (crank == 0 && tid == 0) idx_out[0] = seed;
   cl.sync();  // every CTA's mbarriers are initialised before the first push
@@ -368,7 +374,7 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
       s_w[wid][0] = bd;
       s_w[wid][1] = __longlong_as_double((long long)widx);
 #pragma unroll
-      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pts[bs][c];
+      for (int c = 0; c < DP; ++c) s_w[wid][2 + c] = pt(bs, c);
     }
     __syncthreads();
     if (wid == 0) {
@@ -414,7 +420,10 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
     for (int s = 0; s < P; ++s) {
       const int64_t i = gtid + s * stride;
       if (i < n) {
-        const double dd = d2_exact<DP>(pts[s], y);
+        double q[DP];
+#pragma unroll
+        for (int c = 0; c < DP; ++c) q[c] = pt(s, c);
+        const double dd = d2_exact<DP>(q, y);
         mind[s] = (i == ni) ? -1.0 : fmin(mind[s], dd);
       }
     }
@@ -422,15 +431,17 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
   cl.sync();  // no CTA leaves while a push into it may be in flight
 }
 
-template <int DP, int P, int NT>
+template <int DP, int P, int NT, bool SP = false>
 afn_status launch_fps_push(const double* X, int64_t n, int d, int64_t k, int64_t seed,
                            int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st) {
-  auto kern = fps_push_kernel<DP, P, NT>;
+  auto kern = fps_push_kernel<DP, P, NT, SP>;
   if (CL > 8) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  const size_t dyn = SP ? sizeof(double) * (size_t)P * DP * NT : 0;
+  if (SP) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CL);
   cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = dyn;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -467,6 +478,11 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
       if (P2 == 1) return launch_fps_push<DP, 1, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       if (P2 == 2) return launch_fps_push<DP, 2, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
       return launch_fps_push<DP, 4, CNT>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+    }
+    // up to 2^17 points (d <= 3): 8 points per thread held in shared memory
+    if (DP <= 3 && n > (int64_t)16 * CNT * 4 && n <= (int64_t)16 * 1024 * 8) {
+      const int CL = (int)((n + 1024 * 8 - 1) / (1024 * 8));
+      return launch_fps_push<DP, 8, 1024, true>(X, n, d, k, seed, idx, fill, CL, kstop, st);
     }
   }
   // choose points per thread P and grid G (G = 1 needs no grid barrier)

@@ -266,15 +266,18 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 // at a 12-double stride (A/B fragment loads: 8 rows x 4 consecutive k per
 // LDS.64 = 2 wavefronts, conflict-free).  Each dot is summed in k order in
 // groups of 4 (the DMMA k-step).
-constexpr int DKC = 8, DKP = 12;
 constexpr int G16_NTL = GA == 16 ? 8 : 4;  // n-tiles per warp (32 columns at GA = 32: 256-column passes)
-constexpr int DNS = 2;      // cp.async stages (2 CTAs/SM; 3 stages at 1 CTA/SM measured slower)
+constexpr int DNS = 2;  // cp.async stages (3 and 4 measured equal at C3 / C2: not latency-bound)
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
 
+// DKC = 16 (128-byte row chunks) when W is several times the L2: C3 (W 4.2
+// GB) 98 -> 85 ms, its gathers of scattered rows being DRAM-bound; DKC = 8
+// below (C2, W 0.23 GB: 3.7 vs 4.1 ms).
+template <int DKC>
 __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ W, int64_t k,
     const int* __restrict__ Ucount, const int* __restrict__ Ulist, const int64_t* __restrict__ Doff,
@@ -284,7 +287,7 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
   // themselves (the factor kernel then only gathers them)
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   // warp = 2 x 8 m8n8 tiles (64 columns)
-  constexpr int NS = DNS;
+  constexpr int NS = DNS, DKP = DKC + 4;  // DKP = 4 or 12 mod 16: conflict-free fragment loads
   constexpr int MTL = GA / 8, NTL = G16_NTL, UTP = 8 * NTL * 8;
   extern __shared__ __align__(16) double gs[];
   double* sA = gs;                         // [NS][GA][DKP]
@@ -834,10 +837,12 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   {
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0) {
-      const int bytes = (int)(sizeof(double) * DNS * DKP * (GA + ut));
-      AFN_CUDA(cudaFuncSetAttribute(group_gemm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      group_gemm_dmma_kernel<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D,
-                                                                  X2, d, kf, mu);
+      const bool wide = (double)N * (double)k * sizeof(double) > 512e6;  // W a few L2s or more
+      const int dkc = wide ? 16 : 8;
+      const int bytes = (int)(sizeof(double) * DNS * (dkc + 4) * (GA + ut));
+      auto kern = wide ? group_gemm_dmma_kernel<16> : group_gemm_dmma_kernel<8>;
+      AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      kern<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D, X2, d, kf, mu);
       AFN_LAUNCH_CHECK("group_gemm_dmma_kernel");
     }
     kt_end(KT_FSAI_GEMM, st, 2.0 * (double)k * (double)totD);

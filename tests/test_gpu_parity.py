@@ -81,7 +81,8 @@ def test_kmv_row_shards():
 
 # --------------------------------------------------------------------------- FPS
 @pytest.mark.parametrize("n,d,k,seed", [(1000, 3, 100, 0), (1, 2, 1, 0), (5000, 2, 300, 17),
-                                        (16384, 3, 2000, 0), (9000, 8, 257, 5), (4097, 1, 4097, 0)])
+                                        (16384, 3, 2000, 0), (9000, 8, 257, 5), (4097, 1, 4097, 0),
+                                        (100000, 3, 200, 7), (70001, 2, 150, 3), (140000, 3, 100, 0)])
 def test_fps_bit_exact(n, d, k, seed):
     X, _ = gen_points(n, d, "cube", 4)
     idx, fill = afn.afn_fps(T(X), k, seed)

@@ -208,7 +208,10 @@ def test_repetition_bit_identical():
     X, b = gen_problem("C2")
     Xd, bd = T(X), T(b)
     ref = [t.clone() for t in afn.afn_fps(Xd, 2000, 0)]          # cluster path (n <= 64K)
-    Xg, _ = gen_points(70000, 3, "cube", 2)
+    Xs, _ = gen_points(100000, 3, "cube", 2)
+    Xsd = T(Xs)
+    refs = [t.clone() for t in afn.afn_fps(Xsd, 300, 0)]         # cluster, points in shared memory
+    Xg, _ = gen_points(140000, 3, "cube", 2)
     Xgd = T(Xg)
     refg = [t.clone() for t in afn.afn_fps(Xgd, 300, 0)]         # persistent-grid path
     y0 = afn.kernel_matvec(Xd, 1.0, 1e-4, bd).clone()
@@ -218,6 +221,7 @@ def test_repetition_bit_identical():
     k0 = afn.afn_estimate_rank(Xd, 1.0)
     for _ in range(20):
         assert all(torch.equal(x, y) for x, y in zip(afn.afn_fps(Xd, 2000, 0), ref))
+        assert all(torch.equal(x, y) for x, y in zip(afn.afn_fps(Xsd, 300, 0), refs))
         assert all(torch.equal(x, y) for x, y in zip(afn.afn_fps(Xgd, 300, 0), refg))
         assert torch.equal(afn.kernel_matvec(Xd, 1.0, 1e-4, bd), y0)
         assert afn.afn_estimate_rank(Xd, 1.0) == k0

@@ -29,7 +29,7 @@ X, b = gen_small(3000, 3, seed=1)
 Xd, bd = T(X), T(b)
 # FPS: cluster path (n <= 64K) and the persistent-grid path (n > 64K), few steps
 idx, _ = afn.afn_fps(Xd, 64, 0)
-Xg, _ = gen_points(70000, 3, "cube", 2)
+Xg, _ = gen_points(140000, 3, "cube", 2)
 afn.afn_fps(T(Xg), 16, 0)
 # kNN grid path (d = 3, N >= 50000)
 afn.afn_knn_pattern(T(Xg[:52000]), 20)
