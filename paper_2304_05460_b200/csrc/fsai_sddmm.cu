@@ -7,17 +7,25 @@
 // many rows' patterns).  Here each needed dot product W_a . W_b (b <= a) is
 // evaluated once, in dense blocks:
 //   1. spatial order: non-landmark points sorted by grid cell (tiled cell
-//      order), consecutive GA = 16 points form a group g;
-//   2. U_g = union over a in g of B_a = { b <= a : a, b in J_i for some row i }
-//      (rows containing a come from the transposed pattern), numbered in the
-//      slot order of a hash set whose global copy maps b -> position in U_g;
+//      order), consecutive GA = 32 points form a group g;
+//   2. U_g = union over a in g of B_a = { b : pos(b) <= pos(a), a, b in J_i
+//      for some row i } (pos = place in the spatial order; rows containing a
+//      come from the transposed pattern), numbered in the slot order of a
+//      hash set whose global copy maps b -> position in U_g.  Each unordered
+//      pair is kept by the spatially later point, so a group's union holds
+//      only the half of its neighbourhood that precedes it in the spatial
+//      order (index order b <= a kept nearly all of it: a group's 32 indices
+//      are scattered; C3 2.0x fewer dots);
 //   3. D_g = W_g W_{U_g}^T (GA x |U_g|, k-long FP64 dots; register-tiled,
 //      cp.async-staged through shared memory) -- ~4x fewer flops than the
 //      per-row Gram on the C2 pattern;
-//   4. per row (one CTA): S_JJ assembled by hash look-up of b in U_{g(a)},
+//   4. per row (one CTA): S_JJ assembled by hash look-up of the earlier point
+//      in the union of the later one's group,
 //      blocked Cholesky in shared memory, g = L^{-T} e_last.
-// Values are independent of the grouping (each dot has a fixed summation
-// order), so the result is deterministic even though the cell sort uses atomics.
+// Values are independent of the grouping and of which point of a pair keeps
+// it (each dot has a fixed summation order, and W_a . W_b and W_b . W_a round
+// the same products), so the result is deterministic even though the cell
+// sort uses atomics.
 #include <math_constants.h>
 
 #include <algorithm>
@@ -181,6 +189,7 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
                                                           const int64_t* __restrict__ trp,
                                                           const int32_t* __restrict__ tcol,
                                                           int64_t row_lo, int64_t row_hi, int ga,
+                                                          const int* __restrict__ grp, const int* __restrict__ loc,
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
                                                           int2* __restrict__ Htab, int* overflow) {
   extern __shared__ int hs[];  // HC keys
@@ -198,12 +207,13 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
   // rows) and the caller falls back to the per-row Gram
   for (int j = 0; j < cnt && !*(volatile int*)&s_ovf; ++j) {
     const int a = sorder[m0 + j];
+    const int pa = (int)(m0 + j);
     for (int64_t e = trp[a] + wid; e < trp[a + 1] && !*(volatile int*)&s_ovf; e += 8) {
       const int i = tcol[e];
       if (i < row_lo || i >= row_hi) continue;  // rows this rank factors
       for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
         const int b = col[q];
-        if (b > a) break;  // columns ascending
+        if (grp[b] * ga + loc[b] > pa) continue;  // kept by the spatially later point
         unsigned h = ((unsigned)b * 2654435761u) & (HC - 1);
         for (int probe = 0; probe < HC; ++probe) {
           const int old = atomicCAS(&hs[h], -1, b);
@@ -282,7 +292,7 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ W, int64_t k,
     const int* __restrict__ Ucount, const int* __restrict__ Ulist, const int64_t* __restrict__ Doff,
     const int64_t* __restrict__ Poff, int64_t G, double* __restrict__ D, const double* __restrict__ X2, int d,
-    KernelFn kf, double mu) {
+    KernelFn kf, double mu, int64_t items) {
   // epilogue: D_g holds the Schur entries S_ab = K(x_a, x_b) + mu delta_ab - W_a . W_b
   // themselves (the factor kernel then only gathers them)
   __shared__ double s_tab[AFN_EXP2_TAB_N];
@@ -295,7 +305,17 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
   __shared__ int s_a[GA];
   __shared__ int s_u[UTP];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t item = blockIdx.x;
+  load_exp2_tab(s_tab);
+  // persistent CTAs: round r takes items [r P, r P + P), P = gridDim.x (the
+  // P items of a round are consecutive: spatially adjacent groups sharing
+  // most union rows).  (A grid barrier between rounds, so that a round's CTAs
+  // stream the same k-chunks together, measured slower -- C3 69.8 vs 56.4
+  // ms: the product is tensor-pipe bound, 77 %, not DRAM-bound.)
+  const int64_t rounds = (items + gridDim.x - 1) / gridDim.x;
+  for (int64_t rd = 0; rd < rounds; ++rd) {
+  const int64_t item = rd * gridDim.x + blockIdx.x;
+  if (rd > 0) __syncthreads();  // (s_a / s_u / the stage buffers of the previous item)
+  if (item >= items) continue;
   int64_t glo = 0, ghi = G;
   while (ghi - glo > 1) {
     const int64_t mid = (glo + ghi) >> 1;
@@ -369,14 +389,13 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
   __syncthreads();  // the stage buffers now hold the points of the rows and columns
   double* sxa = gs;             // [GA][d]
   double* sxb = gs + GA * d;    // [UTP][d]
-  load_exp2_tab(s_tab);
   for (int e = tid; e < (GA + un) * d; e += 256) {
     const int row = e / d, c = e - row * d;
     const int id = row < GA ? s_a[row] : s_u[row - GA];
     (row < GA ? sxa : sxb - GA * d)[e] = id >= 0 ? X2[(int64_t)id * d + c] : 0.0;
   }
   __syncthreads();
-  if (!wact) return;
+  if (!wact) continue;
 #pragma unroll
   for (int mt = 0; mt < MTL; ++mt) {
     const int j = mt * 8 + fr;
@@ -395,6 +414,7 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
       }
     }
   }
+  }  // rounds
 }
 
 // ---------------------------------------------------------------- factor
@@ -405,12 +425,12 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
 //      hash tables), lower triangle into shared memory, rows padded to even
 //      length (16-byte aligned panel reads), padded to WP rows with identity;
 //   2. right-looking blocked Cholesky diag(S_JJ, I) = L L^T with 16-column
-//      panels: every warp factors the 16x16 diagonal block redundantly with
-//      shuffles (warp-uniform code: no divergence fallback, no spills; warp 0
-//      stores it), one row per thread for the panel solve, 4x4 register tiles
-//      (LDS.128 operand pairs) for the trailing update;
+//      panels: one warp factors the 16x16 diagonal block with shuffles
+//      (rows in lanes), one row per thread for the panel solve, 8x8 DMMA
+//      tiles for the trailing update -- with look-ahead: warp 0 updates and
+//      factors the next diagonal block while warps 1..3 update the rest;
 //   3. g = L^{-T} e_last by column-oriented back substitution over the
-//      contiguous rows of L (every warp, warp 0 stores) -- the
+//      contiguous rows of L (warp 0; the other warps exit) -- the
 //      Kolotilina-Yeremin row with diag(G S G^T) = 1 (reading R16).
 constexpr int FT2 = 128;
 __device__ __forceinline__ void dmma884f(double& c0, double& c1, double a, double b) {
@@ -447,8 +467,14 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
   return bad;
 }
 
-constexpr int FB = 8;  // gather batch: independent hash probes / D loads in flight per thread
-#define AFN_FACTOR_MINB 4  // <= 128 registers (5 rows per SM forces <= 96: spills, 2.63 vs 2.18 ms on C2)
+#ifndef AFN_FB
+#define AFN_FB 8
+#endif
+constexpr int FB = AFN_FB;  // gather batch: independent hash probes / D loads in flight per thread
+#ifndef AFN_FACTOR_MINB
+#define AFN_FACTOR_MINB 4
+#endif
+// (MINB 4: // <= 128 registers (5 rows per SM forces <= 96: spills, 2.63 vs 2.18 ms on C2)
 template <int MT>
 __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
                                                          int64_t row_hi, const int64_t* __restrict__ rp,
@@ -467,13 +493,19 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
   double* Lm = fsm;
   const double* zrow = fsm + lsz - 16;
   __shared__ double s_inv[WP];
+  __shared__ __align__(16) double s_dg[16 * 16];  // the current diagonal block of L, dense
   __shared__ __align__(16) double s_col[32];
   __shared__ int sJ[WP];
   __shared__ int s_off[WP + 1];
   __shared__ int s_g[WP];
+  __shared__ int s_pos[WP];
   __shared__ int64_t s_db[WP];
   __shared__ int s_bad;
+  constexpr int NT8 = (WP / 8) * (WP / 8 + 1) / 2;
+  __shared__ short2 s_tile[NT8];  // trailing-update tile t -> (I, J), J <= I (row-wise lower order)
   const int tid = threadIdx.x, lane = tid & 31, lr = lane & 15, wid = tid >> 5;
+  for (int I = wid; I < WP / 8; I += FT2 / 32)
+    for (int J = lane; J <= I; J += 32) s_tile[I * (I + 1) / 2 + J] = make_short2((short)I, (short)J);
   const int64_t i = rorder[blockIdx.x];
   if (i < row_lo || i >= row_hi) return;  // another rank's row
   const int64_t beg = rp[i];
@@ -495,9 +527,10 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
   // time (8 independent hash probes, then 8 independent D loads).
   for (int p = tid; p < wp; p += FT2) {
     const int a = sJ[p];
-    const int g = grp[a];
+    const int g = grp[a], la = loc[a];
     s_g[p] = g;
-    s_db[p] = Doff[g] + (int64_t)loc[a] * Ucount[g];
+    s_pos[p] = g * GA + la;
+    s_db[p] = Doff[g] + (int64_t)la * Ucount[g];
   }
   __syncthreads();
   {
@@ -519,8 +552,10 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
 #pragma unroll
         for (int t = 0; t < B; ++t) {
           const bool ok = e0 + t < ne;
-          pp[t] = ok ? p : 0;
-          bb[t] = sJ[ok ? q : 0];
+          // the pair (J_p, J_q) lives in the group of its spatially later point
+          const int ph = !ok ? 0 : (s_pos[p] >= s_pos[q] ? p : q);
+          pp[t] = ph;
+          bb[t] = sJ[!ok ? 0 : (ph == p ? q : p)];
           hh[t] = ((unsigned)bb[t] * 2654435761u) & (HC - 1);
           hv[t] = __ldg(&Htab[(int64_t)s_g[pp[t]] * HC + hh[t]]);
           if (++q > p) { ++p; q = 0; }
@@ -554,33 +589,77 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
   // blocks; the identity rows wp..WP-1 are implicit (never stored: their
   // entries left of the diagonal are 0 and stay 0)
   auto rowp = [&](int a, int kb) -> const double* { return a < wp ? Lm + s_off[a] + kb : zrow; };
+  // diagonal block at kb (one warp): unblocked, rows in lanes
+  auto diag = [&](int kb) {
+    double dr[16], myinv = 1.0;
+    const bool real = kb + lr < wp;
+    const double* row = rowp(kb + lr, kb);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) dr[c] = (c <= lr) ? (real ? row[c] : (c == lr ? 1.0 : 0.0)) : 0.0;
+    const bool bad = factor_diag16(dr, myinv, lane, s_col);
+    if (lane < 16) {
+      if (kb + lane < wp) {
+        double* wrow = Lm + s_off[kb + lane] + kb;
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c <= lane) wrow[c] = dr[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 16; c += 2)
+        *reinterpret_cast<double2*>(&s_dg[lane * 16 + c]) = make_double2(c <= lane ? dr[c] : 0.0,
+                                                                         c + 1 <= lane ? dr[c + 1] : 0.0);
+      s_inv[kb + lane] = myinv;
+      if (bad) s_bad = 1;
+    }
+  };
+  const int fr = lane >> 2, fk = lane & 3;
+  // trailing-update tiles t0 and t1 (t1 < 0: none) of step kb:
+  // A[a][b] -= sum_c L[a][kb+c] L[b][kb+c] over an 8x8 tile on the FP64
+  // tensor cores (DMMA, 4 k-steps of 4); rows past wp read the zero row
+  auto upd2 = [&](int kb, int r0, int t0, int t1) {
+    const short2 v0 = s_tile[t0], v1 = s_tile[t1 >= 0 ? t1 : t0];
+    const int I0 = v0.x, J0 = v0.y, I1 = v1.x, J1 = v1.y;
+    const double* pa0 = rowp(r0 + 8 * I0 + fr, kb) + fk;
+    const double* pb0 = rowp(r0 + 8 * J0 + fr, kb) + fk;
+    const double* pa1 = rowp(r0 + 8 * I1 + fr, kb) + fk;
+    const double* pb1 = rowp(r0 + 8 * J1 + fr, kb) + fk;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+#pragma unroll
+    for (int k4 = 0; k4 < 16; k4 += 4) {
+      dmma884f(c00, c01, pa0[k4], pb0[k4]);
+      dmma884f(c10, c11, pa1[k4], pb1[k4]);
+    }
+    // (col even, rows start 16-byte aligned: the pair is one 16-byte access)
+    auto sub = [&](int row, int col, double v0, double v1) {
+      if (row >= wp) return;
+      double* q = Lm + s_off[row] + col;
+      if (col + 1 <= row) {
+        double2 o = *reinterpret_cast<double2*>(q);
+        o.x -= v0;
+        o.y -= v1;
+        *reinterpret_cast<double2*>(q) = o;
+      } else if (col <= row) {
+        q[0] -= v0;
+      }
+    };
+    sub(r0 + 8 * I0 + fr, r0 + 8 * J0 + 2 * fk, c00, c01);
+    if (t1 >= 0) sub(r0 + 8 * I1 + fr, r0 + 8 * J1 + 2 * fk, c10, c11);
+  };
+  // look-ahead: warp 0 updates the NEXT diagonal block first (tiles 0..2 of
+  // the step: I, J < 2) and factors it while warps 1..3 update the rest of
+  // the trailing matrix, so the diagonal factor leaves the critical path
+  if (wid == 0) diag(0);
+  __syncthreads();
 #pragma unroll 1
   for (int kb = 0; kb < wp; kb += 16) {
-    // diagonal block: one warp (the others wait at the barrier)
-    if (wid == 0) {
-      double dr[16], myinv = 1.0;
-      const bool real = kb + lr < wp;
-      const double* row = rowp(kb + lr, kb);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) dr[c] = (c <= lr) ? (real ? row[c] : (c == lr ? 1.0 : 0.0)) : 0.0;
-      const bool bad = factor_diag16(dr, myinv, lane, s_col);
-      if (lane < 16) {
-        if (kb + lane < wp) {
-          double* wrow = Lm + s_off[kb + lane] + kb;
-#pragma unroll
-          for (int c = 0; c < 16; ++c)
-            if (c <= lane) wrow[c] = dr[c];
-        }
-        s_inv[kb + lane] = myinv;
-        if (bad) s_bad = 1;
-      }
-    }
-    __syncthreads();
     const int r0 = kb + 16;
     const int m = wp - r0;
     if (m <= 0) break;
-    // panel: rows a >= r0, columns kb..kb+15: x L_diag^T = A
-    for (int a = r0 + tid; a < wp; a += FT2) {
+    // panel: rows a >= r0, columns kb..kb+15: x L_diag^T = A (one row per
+    // thread: wp - 16 < FT2; no loop, so the diagonal block's loads are not
+    // hoisted into registers)
+    static_assert(WP - 16 <= FT2, "panel rows per thread");
+    if (const int a = r0 + tid; a < wp) {
       double x[16];
       double* row = Lm + s_off[a] + kb;
 #pragma unroll
@@ -592,56 +671,25 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
         double sacc = x[c];
-        const double* lrow = rowp(kb + c, kb);
 #pragma unroll
-        for (int c2 = 0; c2 < c; ++c2) sacc = fma(-x[c2], lrow[c2], sacc);
+        for (int c2 = 0; c2 < c; ++c2) sacc = fma(-x[c2], s_dg[c * 16 + c2], sacc);
         x[c] = sacc * s_inv[kb + c];
       }
 #pragma unroll
       for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(x[c], x[c + 1]);
     }
     __syncthreads();
-    // trailing update A[a][b] -= sum_c L[a][kb+c] L[b][kb+c], wp > a >= b >= r0:
-    // 8x8 tiles on the FP64 tensor cores (DMMA, 4 k-steps of 4), a warp per
-    // tile, two tiles in flight per warp; rows past wp read the zero row
     const int mt8 = (m + 7) >> 3;
     const int nt8 = mt8 * (mt8 + 1) / 2;
-    const int fr = lane >> 2, fk = lane & 3;
-    auto tile_ij = [&](int t, int& I, int& J) {
-      I = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-      while (I * (I + 1) / 2 > t) --I;
-      while ((I + 1) * (I + 2) / 2 <= t) ++I;
-      J = t - I * (I + 1) / 2;
-    };
-    for (int t0 = wid; t0 < nt8; t0 += 2 * (FT2 / 32)) {
-      const int t1 = t0 + FT2 / 32;
-      int I0, J0, I1, J1;
-      tile_ij(t0, I0, J0);
-      tile_ij(t1 < nt8 ? t1 : t0, I1, J1);
-      const double* pa0 = rowp(r0 + 8 * I0 + fr, kb) + fk;
-      const double* pb0 = rowp(r0 + 8 * J0 + fr, kb) + fk;
-      const double* pa1 = rowp(r0 + 8 * I1 + fr, kb) + fk;
-      const double* pb1 = rowp(r0 + 8 * J1 + fr, kb) + fk;
-      double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
-#pragma unroll
-      for (int k4 = 0; k4 < 16; k4 += 4) {
-        dmma884f(c00, c01, pa0[k4], pb0[k4]);
-        dmma884f(c10, c11, pa1[k4], pb1[k4]);
-      }
-      {
-        const int row = r0 + 8 * I0 + fr, col = r0 + 8 * J0 + 2 * fk;
-        if (row < wp) {
-          if (col <= row) Lm[s_off[row] + col] -= c00;
-          if (col + 1 <= row) Lm[s_off[row] + col + 1] -= c01;
-        }
-      }
-      if (t1 < nt8) {
-        const int row = r0 + 8 * I1 + fr, col = r0 + 8 * J1 + 2 * fk;
-        if (row < wp) {
-          if (col <= row) Lm[s_off[row] + col] -= c10;
-          if (col + 1 <= row) Lm[s_off[row] + col + 1] -= c11;
-        }
-      }
+    const int nd = nt8 < 3 ? nt8 : 3;  // the next diagonal block's tiles
+    if (wid == 0) {
+      upd2(kb, r0, 0, nd > 1 ? 1 : -1);
+      if (nd > 2) upd2(kb, r0, 2, -1);
+      __syncwarp();
+      diag(r0);
+    } else {
+      constexpr int NW = FT2 / 32 - 1;
+      for (int t0 = 3 + (wid - 1); t0 < nt8; t0 += 2 * NW) upd2(kb, r0, t0, t0 + NW < nt8 ? t0 + NW : -1);
     }
     __syncthreads();
   }
@@ -649,8 +697,10 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
     if (tid == 0) atomicCAS(info, 0, (int)(i + 1));
     return;
   }
-  // ---- 3. g = L^{-T} e_last: rhs_j -= L[t][j] g_t over the rows t, every
-  // warp redundantly (shuffles in warp-uniform code), warp 0 stores
+  // ---- 3. g = L^{-T} e_last: rhs_j -= L[t][j] g_t over the rows t, one
+  // warp (shuffles in warp-uniform code); the others leave, freeing their
+  // issue slots for the SM's other rows
+  if (wid != 0) return;
   double rhs[WP / 32 + 1];
 #pragma unroll
   for (int r = 0; r <= WP / 32; ++r) rhs[r] = (lane + 32 * r == wp - 1) ? 1.0 : 0.0;
@@ -795,8 +845,8 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
       AFN_CUDA(cudaFuncSetAttribute(group_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       uattr = true;
     }
-    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, col, trp, tcol, row_lo, row_hi, GA,
-                                                         Ucount, Ulist, Htab, ovf);
+    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, col, trp, tcol, row_lo, row_hi, GA, grp,
+                                                         loc, Ucount, Ulist, Htab, ovf);
     AFN_LAUNCH_CHECK("group_union_kernel");
   }
   int hov = 0;
@@ -842,7 +892,12 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
       const int bytes = (int)(sizeof(double) * DNS * (dkc + 4) * (GA + ut));
       auto kern = wide ? group_gemm_dmma_kernel<16> : group_gemm_dmma_kernel<8>;
       AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      kern<<<(unsigned)items, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D, X2, d, kf, mu);
+      int occ = 0;
+      AFN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, bytes));
+      // persistent rounds of P consecutive items when W is several L2s (C3:
+      // 59.8 -> 56.4 ms), one item per CTA below (C2: 2.61 vs 2.82 ms)
+      const int64_t P = wide ? std::min<int64_t>(items, (int64_t)std::max(1, occ) * num_sms()) : items;
+      kern<<<(unsigned)P, 256, bytes, st>>>(sorder, N, W, k, Ucount, Ulist, Doff, Poff, G, D, X2, d, kf, mu, items);
       AFN_LAUNCH_CHECK("group_gemm_dmma_kernel");
     }
     kt_end(KT_FSAI_GEMM, st, 2.0 * (double)k * (double)totD);

@@ -25,6 +25,7 @@ for path in paths:
         kt = afn.kernel_timers(enable=False)
         print(os.path.basename(path), cfg.name, "iters", r["iterations"], "setup_ms %.1f" % inf["ms_total"],
               "fsai_ms %.1f" % inf["ms_fsai"], json.dumps({k: round(v["ms"], 2) for k, v in kt.items() if v["count"]}),
+              "group_gflop %.0f" % (kt["group_gemm_kernel"]["work"] / 1e9),
               flush=True)
     finally:
         afn._lib = afn_lib_saved
