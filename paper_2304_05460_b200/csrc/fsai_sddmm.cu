@@ -433,6 +433,16 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
 //      contiguous rows of L (warp 0; the other warps exit) -- the
 //      Kolotilina-Yeremin row with diag(G S G^T) = 1 (reading R16).
 constexpr int FT2 = 128;
+// 1/sqrt(x): MUFU.RSQ64H seed + two Newton steps (8 instructions instead of
+// the ~20 of the library rsqrt, <= 2 ulp; C2 factor 1.76 -> 1.66 ms)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
 __device__ __forceinline__ void dmma884f(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -455,7 +465,7 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
     __syncwarp();
     double piv = cb[c];
     if (!(piv > 0.0)) { bad = true; piv = 1.0; }
-    const double inv = rsqrt(piv);
+    const double inv = rsqrt_nr(piv);
     const double lrc = dr[c] * inv;  // L[lr][c]
     const double f = lrc * inv;      // L[lr][c] L[c2][c] = f A[c2][c]
     if (lr == c) myinv = inv;
@@ -467,16 +477,10 @@ __device__ __forceinline__ bool factor_diag16(double (&dr)[16], double& myinv, i
   return bad;
 }
 
-#ifndef AFN_FB
-#define AFN_FB 8
-#endif
-constexpr int FB = AFN_FB;  // gather batch: independent hash probes / D loads in flight per thread
-#ifndef AFN_FACTOR_MINB
-#define AFN_FACTOR_MINB 4
-#endif
-// (MINB 4: // <= 128 registers (5 rows per SM forces <= 96: spills, 2.63 vs 2.18 ms on C2)
+constexpr int FB = 8;  // gather batch: hash probes / D loads in flight per thread (12: C2 1.81 vs 1.76 ms)
+// 4 rows per SM: <= 128 registers (5 forces <= 96 -- spills: C2 1.86 vs 1.77 ms)
 template <int MT>
-__global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
+__global__ void __launch_bounds__(FT2, 4) fsai_factor_kernel(const int* __restrict__ rorder, int64_t row_lo,
                                                          int64_t row_hi, const int64_t* __restrict__ rp,
                                                          const int32_t* __restrict__ col,
                                                          const int* __restrict__ grp, const int* __restrict__ loc,
@@ -658,8 +662,9 @@ __global__ void __launch_bounds__(FT2, AFN_FACTOR_MINB) fsai_factor_kernel(const
     // panel: rows a >= r0, columns kb..kb+15: x L_diag^T = A (one row per
     // thread: wp - 16 < FT2; no loop, so the diagonal block's loads are not
     // hoisted into registers)
-    static_assert(WP - 16 <= FT2, "panel rows per thread");
-    if (const int a = r0 + tid; a < wp) {
+#pragma unroll 1
+    for (int a = r0 + tid; a < wp; a += FT2) {
+      asm volatile("" ::: "memory");  // (keeps the diagonal block's loads inside the loop: no hoisting)
       double x[16];
       double* row = Lm + s_off[a] + kb;
 #pragma unroll
