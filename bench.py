@@ -352,7 +352,6 @@ def main():
     inf0, rep0 = records[0]
     n, d = cfg.n, cfg.d
     step_ms = job_ms / args.steps
-    kt_step_ms = kt_job_ms / args.steps
     traffic = {}
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
@@ -367,7 +366,9 @@ def main():
             return None
         per_ms = v["ms"] / v["count"]
         out = {"kernel": name, "launches": v["count"], "ms_per_launch": per_ms,
-               "share_of_step": v["ms"] / args.steps / kt_step_ms if kt_step_ms > 0 else None,
+               # (device ms per step over the un-instrumented step: the timers'
+               # event records slow the instrumented pass itself)
+               "share_of_step": v["ms"] / args.steps / step_ms if step_ms > 0 else None,
                "traffic": (traffic.get(args.config, {}) or {}).get(name)}
         if name == "apply":
             ach = v["work"] / (v["ms"] * 1e-3) / 1e9

@@ -10,8 +10,9 @@
 //      order), consecutive GA = 32 points form a group g;
 //   2. U_g = union over a in g of B_a = { b : pos(b) <= pos(a), a, b in J_i
 //      for some row i } (pos = place in the spatial order; rows containing a
-//      come from the transposed pattern), numbered in the slot order of a
-//      hash set whose global copy maps b -> position in U_g.  Each unordered
+//      come from the transposed pattern, scanned as ascending positions up to
+//      pos(a)), numbered in the slot order of a hash set whose global copy
+//      maps pos(b) -> the column of b in U_g.  Each unordered
 //      pair is kept by the spatially later point, so a group's union holds
 //      only the half of its neighbourhood that precedes it in the spatial
 //      order (index order b <= a kept nearly all of it: a group's 32 indices
@@ -167,6 +168,56 @@ __global__ void pass_count_kernel(const int* __restrict__ Ucount, int64_t G, int
   if (g < G) pc[g] = (Ucount[g] + ut - 1) / ut;
 }
 
+// colp: each pattern row's columns as spatial positions, ascending (one warp
+// per row, bitonic sort of <= 128 keys in registers, 4 per lane)
+__global__ void pattern_positions_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                         const int* __restrict__ grp, const int* __restrict__ loc, int ga,
+                                         int64_t N, int32_t* __restrict__ colp) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= N) return;
+  const int64_t b0 = rp[i];
+  const int len = (int)(rp[i + 1] - b0);  // <= 128
+  int k[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = r * 32 + lane;
+    k[r] = e < len ? grp[col[b0 + e]] * ga + loc[col[b0 + e]] : 0x7fffffff;
+  }
+  // element e = r * 32 + lane; bitonic network over the 128 elements
+#pragma unroll
+  for (int sz = 2; sz <= 128; sz <<= 1) {
+#pragma unroll
+    for (int st = sz >> 1; st > 0; st >>= 1) {
+      if (st >= 32) {  // partners in another register of the same lane
+        const int m = st >> 5;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          if (r & m) continue;
+          const int r2 = r | m;
+          const bool up = ((r * 32 + lane) & sz) == 0;
+          const int lo = min(k[r], k[r2]), hi = max(k[r], k[r2]);
+          k[r] = up ? lo : hi;
+          k[r2] = up ? hi : lo;
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int other = __shfl_xor_sync(0xffffffffu, k[r], st);
+          const bool up = ((r * 32 + lane) & sz) == 0;
+          const bool lower = (lane & st) == 0;
+          k[r] = (lower == up) ? min(k[r], other) : max(k[r], other);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = r * 32 + lane;
+    if (e < len) colp[b0 + e] = k[r];
+  }
+}
+
 __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int ga, int* __restrict__ grp,
                                   int* __restrict__ loc) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -185,14 +236,13 @@ __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int
 // one pattern row at a time, lanes over its entries.
 __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict__ sorder, int64_t N,
                                                           const int64_t* __restrict__ rp,
-                                                          const int32_t* __restrict__ col,
+                                                          const int32_t* __restrict__ colp,
                                                           const int64_t* __restrict__ trp,
                                                           const int32_t* __restrict__ tcol,
                                                           int64_t row_lo, int64_t row_hi, int ga,
-                                                          const int* __restrict__ grp, const int* __restrict__ loc,
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
                                                           int2* __restrict__ Htab, int* overflow) {
-  extern __shared__ int hs[];  // HC keys
+  extern __shared__ int hs[];  // HC keys (positions)
   __shared__ int s_n, s_ovf;
   __shared__ int s_scan[256];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -212,16 +262,16 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
       const int i = tcol[e];
       if (i < row_lo || i >= row_hi) continue;  // rows this rank factors
       for (int64_t q = rp[i] + lane; q < rp[i + 1]; q += 32) {
-        const int b = col[q];
-        if (grp[b] * ga + loc[b] > pa) continue;  // kept by the spatially later point
-        unsigned h = ((unsigned)b * 2654435761u) & (HC - 1);
+        const int pb = colp[q];
+        if (pb > pa) break;  // positions ascending: kept by the spatially later point
+        unsigned h = ((unsigned)pb * 2654435761u) & (HC - 1);
         for (int probe = 0; probe < HC; ++probe) {
-          const int old = atomicCAS(&hs[h], -1, b);
+          const int old = atomicCAS(&hs[h], -1, pb);
           if (old == -1) {
             if (atomicAdd(&s_n, 1) >= UCAP) s_ovf = 1;
             break;
           }
-          if (old == b) break;
+          if (old == pb) break;
           h = (h + 1) & (HC - 1);
         }
         if (*(volatile int*)&s_ovf) break;
@@ -250,10 +300,10 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
   int2* H = Htab + g * HC;
   for (int t = 0; t < PER; ++t) {
     const int slot = tid * PER + t;
-    const int b = hs[slot];
-    if (b >= 0) {
-      Ulist[g * UCAP + u] = b;
-      H[slot] = make_int2(b, u);
+    const int pb = hs[slot];
+    if (pb >= 0) {
+      Ulist[g * UCAP + u] = sorder[pb];  // (the product gathers W rows by point)
+      H[slot] = make_int2(pb, u);
       ++u;
     } else {
       H[slot] = make_int2(-1, -1);
@@ -559,7 +609,7 @@ __global__ void __launch_bounds__(FT2, 4) fsai_factor_kernel(const int* __restri
           // the pair (J_p, J_q) lives in the group of its spatially later point
           const int ph = !ok ? 0 : (s_pos[p] >= s_pos[q] ? p : q);
           pp[t] = ph;
-          bb[t] = sJ[!ok ? 0 : (ph == p ? q : p)];
+          bb[t] = s_pos[!ok ? 0 : (ph == p ? q : p)];  // the hash key: the earlier point's position
           hh[t] = ((unsigned)bb[t] * 2654435761u) & (HC - 1);
           hv[t] = __ldg(&Htab[(int64_t)s_g[pp[t]] * HC + hh[t]]);
           if (++q > p) { ++p; q = 0; }
@@ -832,6 +882,13 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   AFN_LAUNCH_CHECK("cell_scatter_kernel");
   group_maps_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(sorder, N, GA, grp, loc);
   AFN_LAUNCH_CHECK("group_maps_kernel");
+  // the pattern rows as ascending spatial positions (the unions' scan stops at
+  // the first position past the point's own)
+  int32_t* colp;
+  const int64_t nnz = N > 1 ? h2[1] : 1;
+  if ((s = get((void**)&colp, sizeof(int32_t) * (size_t)std::max<int64_t>(1, nnz))) != AFN_OK) return s;
+  pattern_positions_kernel<<<(unsigned)((N * 32 + 255) / 256), 256, 0, st>>>(rp, col, grp, loc, GA, N, colp);
+  AFN_LAUNCH_CHECK("pattern_positions_kernel");
   // ---- 2. unions
   const int64_t G = (N + GA - 1) / GA;
   int *Ucount, *Ulist, *ovf;
@@ -850,8 +907,8 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
       AFN_CUDA(cudaFuncSetAttribute(group_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       uattr = true;
     }
-    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, col, trp, tcol, row_lo, row_hi, GA, grp,
-                                                         loc, Ucount, Ulist, Htab, ovf);
+    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi, GA,
+                                                         Ucount, Ulist, Htab, ovf);
     AFN_LAUNCH_CHECK("group_union_kernel");
   }
   int hov = 0;
