@@ -319,7 +319,10 @@ def main():
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
-        mine = sum(e0.elapsed_time(e1) for e0, e1 in evs)
+        per = [e0.elapsed_time(e1) for e0, e1 in evs]
+        if os.environ.get("AFN_BENCH_STEPS"):
+            print("step ms: " + " ".join(f"{x:.1f}" for x in per), file=sys.stderr, flush=True)
+        mine = sum(per)
         t = torch.tensor([mine], dtype=torch.float64, device=dev)
         if dist:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
