@@ -47,6 +47,8 @@ namespace {
 // ~27 % more dots than 16 -- C3 135.7 -> 98.8 ms, C5 2643 -> 1919 ms, C2
 // 3.86 -> 3.66 ms per product.  (A TMA bulk-copy variant with 4 stages of
 // 256-byte row chunks, 1 CTA/SM, measured 2-3x slower.)
+// (with the spatial-order unions: GA = 16 C3 100.9 ms / C2 3.08, GA = 64
+// 71.0 / 3.15, GA = 32 56.0 / 2.72 ms)
 constexpr int GA = 32;
 constexpr int UCAP = 4096;   // max |U_g|
 constexpr int HC = 8192;     // hash capacity (power of two)
@@ -326,7 +328,7 @@ __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
 // at a 12-double stride (A/B fragment loads: 8 rows x 4 consecutive k per
 // LDS.64 = 2 wavefronts, conflict-free).  Each dot is summed in k order in
 // groups of 4 (the DMMA k-step).
-constexpr int G16_NTL = GA == 16 ? 8 : 4;  // n-tiles per warp (32 columns at GA = 32: 256-column passes)
+constexpr int G16_NTL = GA == 16 ? 8 : (GA == 32 ? 4 : 2);  // n-tiles per warp: 32 x 4 tiles (passes of 256 columns) at GA = 32
 constexpr int DNS = 2;  // cp.async stages (3 and 4 measured equal at C3 / C2: not latency-bound)
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
