@@ -404,6 +404,21 @@ cudaStream_t side_stream() {
   return ss[dev];
 }
 
+// high-priority non-blocking stream per device and host thread (the K11
+// factorization beside the kNN pattern)
+cudaStream_t hp_stream() {
+  static thread_local cudaStream_t hs[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!hs[dev]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&hs[dev], cudaStreamNonBlocking, hi);
+  }
+  return hs[dev];
+}
+
 // non-blocking stream per device and host thread for PCG graph capture / replay
 cudaStream_t graph_stream() {
   static thread_local cudaStream_t gs[64] = {nullptr};
@@ -1043,6 +1058,12 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     cudaEvent_t a, b;
     ~EvPat() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
   } evpat{e_pat0, e_pat1};
+  cudaEvent_t e_hp0 = nullptr, e_hp1 = nullptr;
+  if (povl) {
+    AFN_CUDA(cudaEventCreateWithFlags(&e_hp0, cudaEventDisableTiming));
+    AFN_CUDA(cudaEventCreateWithFlags(&e_hp1, cudaEventDisableTiming));
+  }
+  EvPat evhp{e_hp0, e_hp1};
 
   // ---- a1: permutation, permuted + prescaled points; a4: L L^T = K11 + mu I, L^{-T}
   for (int q = 0; q < nlocal; ++q) {
@@ -1085,18 +1106,29 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(ralloc(s, &s.L, (size_t)k * k, st));
     TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
     if (k == 0) continue;
-    // AFN: K11 + mu I (P:L210-211).  Nystrom: K11 + nu I, nu = 1e-10 (reading R30)
-    TRY(gen_k11(s.Xp, k, d, kn, nys ? AFN_NYS_NU : P.mu, s.L, st));
-    kt_begin(KT_POTRF, st);
-    TRY(potrf_lower(s.L, k, s.dinfo, st));
-    kt_end(KT_POTRF, st, (double)k * k * k / 3.0);
-    kt_begin(KT_LINV, st);
-    TRY(trsm_linvt(s.L, k, s.LinvT, st));
-    if (!nys) {
-      TRY(ralloc(s, &s.Linv, (size_t)k * k, st));
-      TRY(transpose_sq(s.LinvT, k, s.Linv, st));
+    if (!nys) TRY(ralloc(s, &s.Linv, (size_t)k * k, st));
+    // K11, its Cholesky and L^{-1}: with the pattern overlapped, on a
+    // high-priority stream -- their ~200 short launches then take SMs ahead
+    // of the kNN grid's pending CTAs instead of queueing behind them
+    cudaStream_t fs = st;
+    if (povl) {
+      fs = hp_stream();
+      AFN_CUDA(cudaEventRecord(e_hp0, st));
+      AFN_CUDA(cudaStreamWaitEvent(fs, e_hp0, 0));
     }
-    kt_end(KT_LINV, st, (double)k * k * k / 3.0);
+    // AFN: K11 + mu I (P:L210-211).  Nystrom: K11 + nu I, nu = 1e-10 (reading R30)
+    TRY(gen_k11(s.Xp, k, d, kn, nys ? AFN_NYS_NU : P.mu, s.L, fs));
+    kt_begin(KT_POTRF, fs);
+    TRY(potrf_lower(s.L, k, s.dinfo, fs));
+    kt_end(KT_POTRF, fs, (double)k * k * k / 3.0);
+    kt_begin(KT_LINV, fs);
+    TRY(trsm_linvt(s.L, k, s.LinvT, fs));
+    if (!nys) TRY(transpose_sq(s.LinvT, k, s.Linv, fs));
+    kt_end(KT_LINV, fs, (double)k * k * k / 3.0);
+    if (fs != st) {
+      AFN_CUDA(cudaEventRecord(e_hp1, fs));
+      AFN_CUDA(cudaStreamWaitEvent(st, e_hp1, 0));
+    }
   }
   AFN_CUDA(cudaEventRecord(ev[3], st));
   auto chol_check = [&]() -> afn_status {
