@@ -106,17 +106,14 @@ __device__ void rows_trsm_64(double* T, const double* Lbb, int rows_valid) {
 // instead marks an exhausted column: L's column (diagonal included) is zero
 // and the trailing matrix is left unchanged, no report.  Batched over
 // blockIdx.y (matrix A + y bs, info + y).
-constexpr int DB_T = 256;
-__global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t k, int64_t kb, int* info,
-                                                             int64_t bs, double skip_thr) {
-  A += (int64_t)blockIdx.y * bs;
-  info += blockIdx.y;
-  __shared__ double s[NB * TP];
-  __shared__ double s_inv[NB];
-  __shared__ __align__(16) double s_col[32];
+// (a device function of NTH threads: the stand-alone kernel for the first
+// block, and the trailing-update kernel's first CTA for the next block)
+template <int NTH>
+__device__ void diag_factor64(double* A, int64_t k, int64_t kb, int* info, double skip_thr, double* s,
+                              double* s_inv, double* s_col) {
   const int nb = (int)min((int64_t)NB, k - kb);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  for (int e = tid; e < NB * NB; e += DB_T) {
+  for (int e = tid; e < NB * NB; e += NTH) {
     const int i = e / NB, t = e - i * NB;
     double v = 0.0;
     if (t <= i) v = (i < nb && t < nb) ? A[(kb + i) * k + kb + t] : (i == t ? 1.0 : 0.0);
@@ -164,7 +161,7 @@ __global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t
     const int r0 = b0 + 16;
     if (r0 >= NB) break;
     // panel: rows r >= r0, columns b0..b0+15: x L_d^T = a (one row per thread)
-    for (int r = r0 + tid; r < NB; r += DB_T) {
+    for (int r = r0 + tid; r < NB; r += NTH) {
       double x[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) x[c] = s[r * TP + b0 + c];
@@ -181,7 +178,7 @@ __global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t
     __syncthreads();
     // trailing lower part: s[r][c] -= sum_t L[r][b0+t] L[c][b0+t], r0 <= c <= r < NB
     const int m = NB - r0;
-    for (int e = tid; e < m * m; e += DB_T) {
+    for (int e = tid; e < m * m; e += NTH) {
       const int r = r0 + e / m, c = r0 + e % m;
       if (c > r) continue;
       double a = 0.0;
@@ -191,10 +188,19 @@ __global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t
     }
     __syncthreads();
   }
-  for (int e = tid; e < NB * NB; e += DB_T) {
+  for (int e = tid; e < NB * NB; e += NTH) {
     const int i = e / NB, t = e - i * NB;
     if (i < nb && t < nb) A[(kb + i) * k + kb + t] = t <= i ? s[i * TP + t] : 0.0;
   }
+}
+
+constexpr int DB_T = 256;
+__global__ void __launch_bounds__(DB_T) potrf_diag_blk_kernel(double* A, int64_t k, int64_t kb, int* info,
+                                                             int64_t bs, double skip_thr) {
+  __shared__ double s[NB * TP];
+  __shared__ double s_inv[NB];
+  __shared__ __align__(16) double s_col[32];
+  diag_factor64<DB_T>(A + (int64_t)blockIdx.y * bs, k, kb, info + blockIdx.y, skip_thr, s, s_inv, s_col);
 }
 
 // Panel below the diagonal block: A[i, kb:kb+nb] <- A[i, kb:kb+nb] L_kk^{-T}.
@@ -439,8 +445,13 @@ afn_status gen_k11(const double* X1, int64_t k, int d, Kern kn, double mu, doubl
 // -- 8 rows x 4 consecutive k -- is two conflict-free wavefronts); 4 warps of
 // 32 x 32 (16 DMMA per k-step of 4).
 constexpr int PUP = NB + 4;
-__global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64_t k, int64_t kb, int64_t bs) {
+// With fuse, the CTA of tile 0 -- the next diagonal block -- factors that
+// block right after updating it (diag_factor64), while the other CTAs still
+// update: the stand-alone diagonal launch leaves the step's critical path.
+__global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64_t k, int64_t kb, int64_t bs,
+                                                                int* info, double skip_thr, int fuse) {
   A += (int64_t)blockIdx.y * bs;
+  info += blockIdx.y;
   extern __shared__ __align__(16) double usm[];
   double* sI = usm;              // [NB][PUP]
   double* sJ = usm + NB * PUP;   // [NB][PUP]
@@ -466,7 +477,7 @@ __global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  if (bi == bj && wm < wn) return;  // strictly upper 32 x 32 block of a diagonal tile
+  if (!(bi == bj && wm < wn)) {  // (not the strictly upper 32 x 32 block of a diagonal tile)
   const int fr = lane >> 2, fk = lane & 3;
   double acc[4][4][2];
 #pragma unroll
@@ -498,6 +509,11 @@ __global__ void __launch_bounds__(128) potrf_update_dmma_kernel(double* A, int64
       if (c + 1 < k && c + 1 <= r) A[r * k + c + 1] -= acc[i][j][1];
     }
   }
+  }
+  if (fuse && t == 0) {
+    __syncthreads();  // (this CTA's updates of the block are visible to the whole CTA)
+    diag_factor64<128>(A, k, base, info, skip_thr, usm, usm + NB * TP, usm + NB * TP + NB);
+  }
 }
 
 afn_status potrf_batched(double* A, int64_t k, int nbatch, int64_t bs, double skip_thr, int* d_info,
@@ -510,17 +526,17 @@ afn_status potrf_batched(double* A, int64_t k, int nbatch, int64_t bs, double sk
   }
   TRY_SMEM();
   AFN_CUDA(cudaMemsetAsync(d_info, 0, sizeof(int) * nbatch, st));
+  potrf_diag_blk_kernel<<<dim3(1, nbatch), DB_T, 0, st>>>(A, k, 0, d_info, bs, skip_thr);
+  AFN_LAUNCH_CHECK("potrf_diag_blk_kernel");
   for (int64_t kb = 0; kb < k; kb += NB) {
-    potrf_diag_blk_kernel<<<dim3(1, nbatch), DB_T, 0, st>>>(A, k, kb, d_info, bs, skip_thr);
-    AFN_LAUNCH_CHECK("potrf_diag_blk_kernel");
     const int64_t rem = k - kb - NB;
     if (rem <= 0) break;
     const int64_t T = (rem + NB - 1) / NB;
     potrf_panel_kernel<<<dim3((unsigned)T, nbatch), DT, SMEM2, st>>>(A, k, kb, bs);
     AFN_LAUNCH_CHECK("potrf_panel_kernel");
-    // trailing update on the FP64 tensor cores
+    // trailing update on the FP64 tensor cores + the next diagonal block
     potrf_update_dmma_kernel<<<dim3((unsigned)(T * (T + 1) / 2), nbatch), 128, (int)(sizeof(double) * 2 * NB * PUP),
-                               st>>>(A, k, kb, bs);
+                               st>>>(A, k, kb, bs, d_info, skip_thr, 1);
     AFN_LAUNCH_CHECK("potrf_update_dmma_kernel");
   }
   zero_upper_kernel<<<dim3((unsigned)((k * k + 255) / 256), nbatch), 256, 0, st>>>(A, k, bs);
