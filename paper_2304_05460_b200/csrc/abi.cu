@@ -1121,6 +1121,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     kt_begin(KT_POTRF, fs);
     TRY(potrf_lower(s.L, k, s.dinfo, fs));
     kt_end(KT_POTRF, fs, (double)k * k * k / 3.0);
+    // L^{-1} (and so W) after the kNN pattern and its transpose: W then runs
+    // with the SMs to itself (measured: W beside the kNN is slower overall --
+    // C2 setup 12.1 vs 11.8 ms)
+    if (fs != st) AFN_CUDA(cudaStreamWaitEvent(fs, e_pat1, 0));
     kt_begin(KT_LINV, fs);
     TRY(trsm_linvt(s.L, k, s.LinvT, fs));
     if (!nys) TRY(transpose_sq(s.LinvT, k, s.Linv, fs));
