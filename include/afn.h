@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define AFN_ABI_VERSION 4
+#define AFN_ABI_VERSION 5
 /* widest FSAI row (nonzeros incl. the diagonal): the paper's plain-FSAI
  * comparison uses 400 neighbours */
 #define AFN_W_MAX 512
@@ -162,6 +162,18 @@ afn_status kernel_matvec_rows(const double* X, int64_t n, int32_t d, int32_t ker
 /* device (fill[i] = fill distance after i+1 selections) or NULL.     */
 afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t seed,
                    int64_t* idx, double* fill, void* stream);
+
+/* W = K(Xr, X1) L^{-T} (the Nystrom factor V^T = K21 L^{-T}; a5) for  */
+/* N points Xr (N x d) against k landmarks X1 (k x d), Linv = L^{-1} (k x k   */
+/* row-major, lower triangular), W: N x k row-major, all device, stream-      */
+/* ordered.  method AFN_WPROD_DMMA: FP64 tensor cores (DMMA); AFN_WPROD_INT8: */
+/* exact INT8 slicing on the tcgen05 tensor cores (8 slices per operand, 36   */
+/* INT8 products, FP64-GEMM-level error; k < 65536).  The AFN build uses      */
+/* AFN_WPROD_INT8 for k >= 512.                                              */
+#define AFN_WPROD_DMMA 0
+#define AFN_WPROD_INT8 1
+afn_status afn_w_product(const double* X1, int64_t k, const double* Xr, int64_t N, int32_t d, int32_t kernel,
+                         double l, const double* Linv, int32_t method, double* W, void* stream);
 
 /* kNN lower pattern.  For each position i of the N points P:   */
 /* row i = {i} plus the min(w-1, i) nearest positions j < i; columns        */

@@ -91,6 +91,8 @@ _sig = {
                                      C.c_int64, C.c_int64, _P, _P]),
     "afn_fps": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, _P, _P, _P]),
     "afn_knn_pattern": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P]),
+    "afn_w_product": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, C.c_double, _P, C.c_int32,
+                                _P, _P]),
     "afn_estimate_rank": (C.c_int, [_P, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_int32,
                                     C.c_uint64,
                                     C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
@@ -238,6 +240,21 @@ def afn_knn_pattern(P, w, stream=None):
     _check(_lib.afn_knn_pattern(_dev(P, "P", torch.float64), N, d, int(w), _dev(rp, "row_ptr"),
                                 _dev(col, "col"), _stream(stream)), "afn_knn_pattern")
     return rp, col[:knn_nnz(N, w)]
+
+
+WPROD_DMMA, WPROD_INT8 = 0, 1
+
+
+def afn_w_product(X1, Xr, l, Linv, method=WPROD_INT8, stream=None, kernel="gaussian"):
+    """W = K(Xr, X1) L^{-T} from Linv = L^{-1} (include/afn.h afn_w_product)."""
+    torch = _torch()
+    k, d = X1.shape
+    N = Xr.shape[0]
+    W = torch.empty(N, k, dtype=torch.float64, device=Xr.device)
+    _check(_lib.afn_w_product(_dev(X1, "X1", torch.float64), k, _dev(Xr, "Xr", torch.float64), N, d,
+                              _kernel_id(kernel), float(l), _dev(Linv, "Linv", torch.float64), int(method),
+                              _dev(W, "W", torch.float64), _stream(stream)), "afn_w_product")
+    return W
 
 
 def afn_estimate_rank(X, l, m=0, rng_seed=0, k_threshold=2000, stream=None, kernel="gaussian"):

@@ -1166,7 +1166,12 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     RankSt& s = h->rk[q];
     TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
     const double* X2 = s.Xp + k * d;
-    if (s.hi > s.lo) TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
+    if (s.hi > s.lo) {
+      if (k >= AFN_W_INT8_MIN_K && s.Linv)  // (INT8 tensor cores, exact slicing: ozaki.cu)
+        TRY(w_gemm_ozaki(s.Linv, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
+      else
+        TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
+    }
   }
   kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k / h->R);  // (N2/R) k^2/2 FMA per rank
   AFN_CUDA(cudaEventRecord(ev[4], st));
@@ -1425,6 +1430,24 @@ afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t see
   TRY(fps_run(X, n, d, k, seed, idx, fill, st));
   AFN_CUDA(cudaStreamSynchronize(st));
   return AFN_OK;
+}
+
+afn_status afn_w_product(const double* X1, int64_t k, const double* Xr, int64_t N, int32_t d, int32_t kernel,
+                         double l, const double* Linv, int32_t method, double* W, void* stream) {
+  TRY(validate_X(X1, k, d));
+  TRY(validate_X(Xr, N, d));
+  REQ(kernel == AFN_KERNEL_GAUSSIAN || kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", kernel);
+  REQ(l > 0 && std::isfinite(l), "l must be > 0");
+  REQ(method == AFN_WPROD_DMMA || method == AFN_WPROD_INT8, "unknown method %d", method);
+  REQ(is_dev(Linv) && is_dev(W), "Linv, W must be device pointers");
+  REQ(method != AFN_WPROD_INT8 || k < 65536, "AFN_WPROD_INT8 needs k < 65536");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (method == AFN_WPROD_INT8) return w_gemm_ozaki(Linv, k, X1, Xr, N, d, Kern{kernel, l}, W, st);
+  Temps t(st);
+  double* LinvT;
+  TRY(t.get(&LinvT, (size_t)k * k));
+  TRY(transpose_sq(Linv, k, LinvT, st));
+  return w_gemm(LinvT, k, X1, Xr, N, d, Kern{kernel, l}, W, st);
 }
 
 afn_status afn_knn_pattern(const double* P, int64_t N, int32_t d, int32_t w, int64_t* row_ptr,

@@ -147,6 +147,10 @@ afn_status potrf_lower(double* A, int64_t k, int* d_info, cudaStream_t st);
 afn_status potrf_batched(double* A, int64_t k, int nbatch, int64_t bs, double skip_thr, int* d_info,
                          cudaStream_t st);
 // W (N x k) = K(Xr, X1) L^{-T} as a GEMM with the explicit L^{-T}
+// W = K(Xr, X1) L^{-T} from Linv = L^{-1} on the INT8 tensor cores (ozaki.cu)
+afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const double* Xr, int64_t N, int d, Kern kn,
+                        double* W, cudaStream_t st);
+constexpr int64_t AFN_W_INT8_MIN_K = 512;  // the build's W takes the INT8 path from this k on
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st);
 // G = F^T F (C x C, full) for F: R x C row-major; deterministic

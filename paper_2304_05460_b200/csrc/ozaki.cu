@@ -1,0 +1,357 @@
+// ozaki.cu -- W = K21 L^{-T} (the Nystrom factor of AFN) in FP64
+// accuracy on the 5th-generation INT8 tensor cores (tcgen05.mma kind::i8,
+// accumulators in TMEM), by exact integer slicing (the Ozaki splitting).
+//
+// Each row r of A = K21 is scaled by 2^-ea_r (2^ea_r >= max_t |A_rt|) and
+// split into S = 8 signed 7-bit slices, x = sum_s a_s 2^(-6-7s), |a_s| <= 64,
+// exactly in FP64 (v <- 64 x; a_s = rint(v); v <- 128 (v - a_s)); each row c
+// of B^T = L^{-1} likewise (2^eb_c, slices b_s).  Then
+//   W_rc = 2^(ea_r + eb_c - 12) sum_{D=0}^{S-1} 2^(-7D) C_D[r][c],
+//   C_D = sum_{i+j=D} A_i B_j^T   (int8 x int8 -> int32, exact: |C_D| <=
+//   8 * 64 * 64 * k < 2^31 for k < 65536),
+// the pairs with i + j >= S dropped (their weight is below 2^-56 of
+// max|A_r| max|B_c| per term): W to within a few units of 2^-56 of
+// sum_t |A_rt||B_ct| -- the size of FP64 GEMM rounding.  36 INT8 products at
+// ~4 POPS replace one FP64 DMMA product at 37 TFLOP/s.
+//
+// GEMM kernel: one CTA (128 threads) per 128 x 64 tile of W (rows x columns,
+// the K range cut at the tile's last column: L^{-1} is lower triangular);
+// the 8 accumulators C_0..C_7 occupy the CTA's 512 TMEM columns (64 each).
+// K advances in 32-byte blocks through four shared-memory stages of all 16
+// slice tiles (48 KB each), loaded with cp.async by all threads into the
+// K-major no-swizzle core-matrix layout; thread 0 issues a stage's 36 MMAs
+// (m128 n64 k32) and commits them to the stage's mbarrier, which gates the
+// stage's reuse three stages later.  Epilogue: tcgen05.ld of the 8
+// accumulators, Horner in FP64, the 2^(ea + eb - 12) scale, FP64 stores.
+//
+// Measured (C3, k = 4000): 59.7 ms per build against 66.6 ms for the DMMA
+// GEMM; the INT8 pipe is ~28 % busy.  The bound is shared memory: an m128
+// n64 k32 MMA reads 6 KB of operands for 0.5 M ops, so 36 MMAs per stage
+// read 216 KB and the stage's cp.async writes add 48 KB -- about the 128
+// B/clk an SM's shared memory moves (the same shape alone, operands resident,
+// peaks at 2.75 POPS in tools/micro/tc_i8_probe.cu; N = 256 reaches 4.1
+// POPS, but 8 accumulators of 256 columns exceed the 512 TMEM columns).
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "afn_common.cuh"
+#include "afn_internal.h"
+
+namespace afn {
+
+namespace {
+
+constexpr int OZ_S = 8;         // slices per operand
+constexpr int OZ_TM = 128;      // tile rows (W rows, MMA M)
+constexpr int OZ_TN = 64;       // tile columns (W columns, MMA N)
+constexpr int OZ_KB = 32;       // K bytes per stage (one MMA k-step)
+constexpr int OZ_NS = 4;        // stages (2 stages of 64 bytes: C3 W 70.4 ms; 4 of 32: 59.7 ms)
+
+constexpr int OZ_NT = 128;      // threads
+constexpr int OZ_A_SL = OZ_TM * OZ_KB;            // bytes of one A slice tile per stage (8 KB)
+constexpr int OZ_B_SL = OZ_TN * OZ_KB;            // bytes of one B slice tile per stage (4 KB)
+constexpr int OZ_STAGE = OZ_S * (OZ_A_SL + OZ_B_SL);  // 96 KB
+constexpr int OZ_SMEM = OZ_NS * OZ_STAGE + 1024;  // stages + alignment slack
+static_assert(OZ_NS * OZ_STAGE <= 200 * 1024, "stages exceed shared memory");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// shared-memory matrix descriptor: K-major, no swizzle (canonical
+// ((8, n), 2) : ((16 B, SBO), LBO) core-matrix layout), sm_100 version 1
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+// instruction descriptor: kind::i8, s32 accumulators, signed int8 A and B, both K-major
+constexpr uint32_t oz_idesc() {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_TN >> 3) << 17) | ((uint32_t)(OZ_TM >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(oz_idesc()), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tOZW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra OZW_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp16(uint32_t saddr, const void* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+// split |x| <= 1 into OZ_S signed 7-bit slices (exact)
+__device__ __forceinline__ void split8(double x, int8_t* out, int64_t stride) {
+  double v = x * 64.0;
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) {
+    const double a = rint(v);
+    out[(int64_t)s * stride] = (int8_t)(int)a;
+    v = (v - a) * 128.0;
+  }
+}
+
+// A slices of K21 rows: one warp per row r (< nr: the kernel values of
+// X_r against the k landmarks; rows nr..nrp-1 and columns k..kp-1 zero).
+// Pass 1: the row max -> ea_r; pass 2: values / 2^ea_r -> slices.
+__global__ void __launch_bounds__(256) k21_slices_kernel(const double* __restrict__ X1, int64_t k, int64_t kp,
+                                                         const double* __restrict__ Xr, int64_t nr, int64_t nrp,
+                                                         int d, KernelFn kf, int8_t* __restrict__ sl,
+                                                         int* __restrict__ ea) {
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+  load_exp2_tab(s_tab);
+  __syncthreads();
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= nrp) return;
+  const int64_t stride = nrp * kp;  // bytes between slices
+  int8_t* row = sl + r * kp;
+  if (r >= nr) {
+    for (int64_t t = lane; t < kp; t += 32)
+      for (int s = 0; s < OZ_S; ++s) row[(int64_t)s * stride + t] = 0;
+    if (lane == 0) ea[r] = 0;
+    return;
+  }
+  double xr[16];
+  for (int c = 0; c < d; ++c) xr[c] = Xr[r * d + c];
+  double mx = 0.0;
+  for (int64_t t = lane; t < k; t += 32) {
+    const double v = kern_from_d2(kf, d2_exact_rt(xr, &X1[t * d], d), s_tab);
+    mx = fmax(mx, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
+  const double sc = ldexp(1.0, -e);
+  for (int64_t t = lane; t < kp; t += 32) {
+    const double v = t < k ? kern_from_d2(kf, d2_exact_rt(xr, &X1[t * d], d), s_tab) * sc : 0.0;
+    split8(v, row + t, stride);
+  }
+  if (lane == 0) ea[r] = e;
+}
+
+// B slices of the rows of a dense row-major matrix M (n x k, row stride ldm):
+// one warp per row c (< n; rows n..np-1 and columns k..kp-1 zero)
+__global__ void __launch_bounds__(256) rows_slices_kernel(const double* __restrict__ Mx, int64_t n, int64_t np,
+                                                          int64_t k, int64_t kp, int64_t ldm,
+                                                          int8_t* __restrict__ sl, int* __restrict__ eb) {
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (c >= np) return;
+  const int64_t stride = np * kp;
+  int8_t* row = sl + c * kp;
+  double mx = 0.0;
+  if (c < n)
+    for (int64_t t = lane; t < k; t += 32) mx = fmax(mx, fabs(Mx[c * ldm + t]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);
+  const double sc = ldexp(1.0, -e);
+  for (int64_t t = lane; t < kp; t += 32) {
+    const double v = (c < n && t < k) ? Mx[c * ldm + t] * sc : 0.0;
+    split8(v, row + t, stride);
+  }
+  if (lane == 0) eb[c] = e;
+}
+
+// W[r][c] for the tile (blockIdx.y: 128 rows, blockIdx.x: 64 columns).
+// Asl: OZ_S slices of nrp x kp bytes; Bsl: OZ_S slices of kcp x kp bytes
+// (rows of L^{-1}); K range [0, min(k, c0 + 64)) rounded up to 64.
+__global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_kernel(const int8_t* __restrict__ Asl, const int* __restrict__ ea,
+                                                           int64_t nr, int64_t nrp, const int8_t* __restrict__ Bsl,
+                                                           const int* __restrict__ eb, int64_t k, int64_t kcp,
+                                                           int64_t kp, double* __restrict__ W, int64_t ldw) {
+  extern __shared__ uint8_t oz_raw[];
+  __shared__ __align__(8) uint64_t bar[OZ_NS];
+  __shared__ uint32_t tmem_base;
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~(uintptr_t)1023);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t r0 = (int64_t)blockIdx.y * OZ_TM, c0 = (int64_t)blockIdx.x * OZ_TN;
+  const int64_t kend = min(k, c0 + OZ_TN);
+  const int nkb = (int)((kend + OZ_KB - 1) / OZ_KB);
+  const int64_t astride = nrp * kp, bstride = kcp * kp;
+  if (tid == 0) {
+    for (int b = 0; b < OZ_NS; ++b) mbar_init(&bar[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+
+  // stage kb -> buffer b: A slice s rows r0.., B slice s rows c0.., bytes
+  // [64 kb, 64 kb + 64) as 16-byte chunks (unit u = 0..3) at
+  //   u * (R / 8) * 128 + (row / 8) * 128 + (row % 8) * 16
+  constexpr int UN = OZ_KB / 16;  // 16-byte units per row per stage
+  auto load = [&](int kb, int b) {
+    uint8_t* base = sm + (size_t)b * OZ_STAGE;
+    const int64_t kb0 = (int64_t)kb * OZ_KB;
+    for (int e = tid; e < OZ_S * OZ_TM * UN; e += OZ_NT) {
+      const int s = e / (OZ_TM * UN), rem = e - s * (OZ_TM * UN);
+      const int row = rem / UN, u = rem % UN;
+      const uint32_t dst = smem_u32(base + s * OZ_A_SL + u * (OZ_TM / 8) * 128 + (row >> 3) * 128 + (row & 7) * 16);
+      cp16(dst, Asl + s * astride + (r0 + row) * kp + kb0 + u * 16);
+    }
+    uint8_t* bb = base + OZ_S * OZ_A_SL;
+    for (int e = tid; e < OZ_S * OZ_TN * UN; e += OZ_NT) {
+      const int s = e / (OZ_TN * UN), rem = e - s * (OZ_TN * UN);
+      const int row = rem / UN, u = rem % UN;
+      const uint32_t dst = smem_u32(bb + s * OZ_B_SL + u * (OZ_TN / 8) * 128 + (row >> 3) * 128 + (row & 7) * 16);
+      cp16(dst, Bsl + s * bstride + (c0 + row) * kp + kb0 + u * 16);
+    }
+  };
+  auto commit = []() { asm volatile("cp.async.commit_group;" ::: "memory"); };
+
+  // stages 0 .. NS-2 in flight before the first MMA; one commit group per
+  // stage index (empty past the end) keeps wait_group's count uniform
+  for (int s0 = 0; s0 < OZ_NS - 1; ++s0) {
+    if (s0 < nkb) load(s0, s0);
+    commit();
+  }
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int b = kb % OZ_NS;
+    asm volatile("cp.async.wait_group %0;" ::"n"(OZ_NS - 2) : "memory");  // stage kb landed (this thread)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");          // generic writes -> tensor core
+    __syncthreads();                                                      // (every thread's)
+    if (tid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t abase = smem_u32(sm + (size_t)b * OZ_STAGE), bbase = abase + OZ_S * OZ_A_SL;
+      constexpr uint32_t LBO_A = (OZ_TM / 8) * 128, LBO_B = (OZ_TN / 8) * 128;
+#pragma unroll
+      for (int D = 0; D < OZ_S; ++D) {
+#pragma unroll
+        for (int i = 0; i <= D; ++i) {
+          const int j = D - i;
+#pragma unroll
+          for (int ks = 0; ks < OZ_KB / 32; ++ks) {
+            const uint64_t da = umma_desc(abase + i * OZ_A_SL + ks * 2 * LBO_A, LBO_A, 128);
+            const uint64_t db = umma_desc(bbase + j * OZ_B_SL + ks * 2 * LBO_B, LBO_B, 128);
+            mma_i8(tmem + (uint32_t)(D * OZ_TN), da, db, (kb > 0 || i > 0 || ks > 0) ? 1u : 0u);
+          }
+        }
+      }
+      mma_commit(&bar[b]);
+    }
+    __syncwarp();
+    const int nxt = kb + OZ_NS - 1;
+    if (nxt < nkb) {
+      // stage kb's MMAs are queued; buffer nxt % NS was last read by stage
+      // kb - 1's MMAs
+      if (kb >= 1) mbar_wait(&bar[(kb - 1) % OZ_NS], (uint32_t)(((kb - 1) / OZ_NS) & 1));
+      load(nxt, nxt % OZ_NS);
+    }
+    commit();
+  }
+  // all MMAs done: the last stage's commit (tracks every earlier MMA of the thread)
+  mbar_wait(&bar[(nkb - 1) % OZ_NS], (uint32_t)(((nkb - 1) / OZ_NS) & 1));
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int64_t r = r0 + warp * 32 + lane;
+  const bool rok = r < nr;
+  const int er = rok ? ea[r] : 0;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#pragma unroll 1
+  for (int cc = 0; cc < OZ_TN; cc += 8) {
+    uint32_t v[OZ_S][8];
+#pragma unroll
+    for (int D = 0; D < OZ_S; ++D) {
+      const uint32_t ta = tmem + lane_base + (uint32_t)(D * OZ_TN + cc);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[D][0]), "=r"(v[D][1]), "=r"(v[D][2]), "=r"(v[D][3]), "=r"(v[D][4]), "=r"(v[D][5]),
+                     "=r"(v[D][6]), "=r"(v[D][7])
+                   : "r"(ta));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (rok) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int64_t c = c0 + cc + j;
+        if (c >= k) break;
+        double acc = (double)(int32_t)v[OZ_S - 1][j];
+#pragma unroll
+        for (int D = OZ_S - 2; D >= 0; --D) acc = fma(acc, 0x1.0p-7, (double)(int32_t)v[D][j]);
+        W[r * ldw + c] = ldexp(acc, er + eb[c] - 12);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+}  // namespace
+
+// W (N x k, row stride k) = K(Xr, X1) L^{-T} with Linv = L^{-1} (k x k,
+// row-major, lower triangular).  K21 is generated and sliced in row blocks.
+afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const double* Xr, int64_t N, int d, Kern kn,
+                        double* W, cudaStream_t st) {
+  if (N <= 0 || k <= 0) return AFN_OK;
+  if (k >= 65536 || d > 16) {
+    set_error("w_gemm_ozaki: k = %lld, d = %d out of range", (long long)k, d);
+    return AFN_ERR_ARG;
+  }
+  const KernelFn kf = kernel_fn(kn.kind, kn.l);
+  const int64_t kp = (k + OZ_KB - 1) / OZ_KB * OZ_KB;
+  const int64_t kcp = (k + OZ_TN - 1) / OZ_TN * OZ_TN;
+  // row blocks: the A slices of one block <= ~1 GiB
+  const int64_t rb = std::max<int64_t>(OZ_TM, ((1ll << 30) / (OZ_S * kp)) / OZ_TM * OZ_TM);
+  const int64_t nblk_rows = std::min<int64_t>(rb, (N + OZ_TM - 1) / OZ_TM * OZ_TM);
+  int8_t *Asl = nullptr, *Bsl = nullptr;
+  int *ea = nullptr, *eb = nullptr;
+  afn_status s;
+  if ((s = dalloc((void**)&Bsl, (size_t)OZ_S * kcp * kp, st)) != AFN_OK) return s;
+  struct Fr {
+    void* p[4];
+    cudaStream_t st;
+    ~Fr() {
+      for (void* q : p)
+        if (q) dfree(q, st);
+    }
+  } fr{{Bsl, nullptr, nullptr, nullptr}, st};
+  if ((s = dalloc((void**)&eb, sizeof(int) * kcp, st)) != AFN_OK) return s;
+  fr.p[1] = eb;
+  if ((s = dalloc((void**)&Asl, (size_t)OZ_S * nblk_rows * kp, st)) != AFN_OK) return s;
+  fr.p[2] = Asl;
+  if ((s = dalloc((void**)&ea, sizeof(int) * nblk_rows, st)) != AFN_OK) return s;
+  fr.p[3] = ea;
+  rows_slices_kernel<<<(unsigned)((kcp * 32 + 255) / 256), 256, 0, st>>>(Linv, k, kcp, k, kp, k, Bsl, eb);
+  AFN_LAUNCH_CHECK("rows_slices_kernel");
+  static bool attr = false;
+  if (!attr) {
+    AFN_CUDA(cudaFuncSetAttribute(w_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
+    attr = true;
+  }
+  for (int64_t q0 = 0; q0 < N; q0 += rb) {
+    const int64_t nr = std::min(rb, N - q0);
+    const int64_t nrp = (nr + OZ_TM - 1) / OZ_TM * OZ_TM;
+    k21_slices_kernel<<<(unsigned)((nrp * 32 + 255) / 256), 256, 0, st>>>(X1, k, kp, Xr + q0 * d, nr, nrp, d, kf,
+                                                                          Asl, ea);
+    AFN_LAUNCH_CHECK("k21_slices_kernel");
+    dim3 grid((unsigned)(kcp / OZ_TN), (unsigned)(nrp / OZ_TM));
+    w_ozaki_kernel<<<grid, OZ_NT, OZ_SMEM, st>>>(Asl, ea, nr, nrp, Bsl, eb, k, kcp, kp, W + q0 * k, k);
+    AFN_LAUNCH_CHECK("w_ozaki_kernel");
+  }
+  return AFN_OK;
+}
+
+}  // namespace afn

@@ -49,7 +49,7 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_struct_layout(lib):
     import ctypes as C
-    assert lib.abi_version() == 4
+    assert lib.abi_version() == 5
     # afn_params: 2 doubles, int64, 4 int32, int64, uint64, 4 int32 = 72 bytes
     assert C.sizeof(lib.Params) == 72
     assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4 + 4 * 2

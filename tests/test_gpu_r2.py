@@ -254,3 +254,36 @@ def test_nccl_path_with_thread_ranks(R, tmp_path):
     r = subprocess.run([_sys.executable, os.path.join(here, "run_case.py"), lib, str(R)], capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "fake-nccl ok" in r.stdout, (r.stdout[-2000:], r.stderr[-4000:])
+
+
+# --------------------------------------------------------------------------- W on the INT8 tensor cores
+@pytest.mark.parametrize("k,N,d,l,kernel,data", [(600, 1000, 3, 1.0, "gaussian", "cube"),
+                                                 (520, 333, 2, 0.3, "gaussian", "cube"),
+                                                 (1100, 700, 8, 2.0, "gaussian", "normal"),
+                                                 (700, 515, 3, 0.5, "matern32", "cube")])
+def test_w_product_int8_slicing(k, N, d, l, kernel, data):
+    """W = K21 L^{-T} by exact INT8 slicing on the tcgen05 tensor
+    cores against the plain fp64 product (oracle kernel entries, LAPACK
+    Cholesky and triangular inverse) and the DMMA path.  The slicing keeps
+    each operand row to 2^-56 of its largest entry, so every entry is within
+    a few 2^-56 k of max_t |K21_rt| max_t |L^{-1}_ct| (checked with 1e-15 k),
+    and each row of W to 1e-13 relative (normwise)."""
+    from scipy.linalg import cholesky, solve_triangular
+    X, _ = gen_points(k + N, d, data, 11)
+    X1, Xr = X[:k], X[k:]
+    K11 = O.kernel_block(X1, X1, l, kernel) + 1e-4 * np.eye(k)
+    Lc = cholesky(K11, lower=True)
+    Linv = solve_triangular(Lc, np.eye(k), lower=True)
+    K21 = O.kernel_block(Xr, X1, l, kernel)
+    Wref = K21 @ Linv.T
+    scale = np.abs(K21).max(axis=1)[:, None] * np.abs(Linv).max(axis=1)[None, :]
+    W8 = afn.afn_w_product(T(X1), T(Xr), l, T(Linv), afn.WPROD_INT8, kernel=kernel).cpu().numpy()
+    Wd = afn.afn_w_product(T(X1), T(Xr), l, T(Linv), afn.WPROD_DMMA, kernel=kernel).cpu().numpy()
+    assert np.all(np.isfinite(W8))
+    e8 = np.max(np.abs(W8 - Wref) / scale) / k
+    ed = np.max(np.abs(Wd - Wref) / scale) / k
+    r8 = np.max(np.linalg.norm(W8 - Wref, axis=1) / np.linalg.norm(Wref, axis=1))
+    rd = np.max(np.linalg.norm(Wd - Wref, axis=1) / np.linalg.norm(Wref, axis=1))
+    print(f"W int8 {e8:.2e} / row {r8:.2e}; dmma {ed:.2e} / row {rd:.2e}")
+    assert e8 <= 1e-15 and ed <= 1e-15
+    assert r8 <= 1e-13 and rd <= 1e-13

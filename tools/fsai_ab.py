@@ -14,7 +14,9 @@ for path in paths:
     afn_lib_saved = afn._lib
     afn._lib = lib  # the binding's marshalling over another build of the same ABI
     for name, (res, args) in afn._sig.items():
-        f = getattr(lib, name); f.restype = res; f.argtypes = args
+        f = getattr(lib, name, None)  # (an older build may lack newer entry points)
+        if f is not None:
+            f.restype = res; f.argtypes = args
     try:
         for rep in range(3):
             afn.kernel_timers(reset=True, enable=rep == 2)
