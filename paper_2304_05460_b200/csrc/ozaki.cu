@@ -18,23 +18,27 @@
 // the K range cut at the tile's last column: L^{-1} is lower triangular);
 // the 8 accumulators C_0..C_7 occupy the CTA's 512 TMEM columns (64 each).
 // K advances in 32-byte blocks through four shared-memory stages of all 16
-// slice tiles (48 KB each), loaded with cp.async by all threads into the
-// K-major no-swizzle core-matrix layout; thread 0 issues a stage's 36 MMAs
-// (m128 n64 k32) and commits them to the stage's mbarrier, which gates the
-// stage's reuse three stages later.  Epilogue: tcgen05.ld of the 8
-// accumulators, Horner in FP64, the 2^(ea + eb - 12) scale, FP64 stores.
+// slice tiles (48 KB each), filled by the TMA (3-D tensor maps over the
+// slice arrays, boxes of 16 bytes x 128 / 64 rows = one column of core
+// matrices of the K-major no-swizzle layout) onto "full" mbarriers; one
+// thread issues a stage's 36 MMAs (m128 n64 k32) and commits them to the
+// stage's "empty" mbarrier; epilogue: tcgen05.ld of the 8 accumulators,
+// Horner in FP64, the 2^(ea + eb - 12) scale, FP64 stores.
 //
-// Measured (C3, k = 4000): 59.7 ms per build against 66.6 ms for the DMMA
-// GEMM; the INT8 pipe is ~28 % busy.  The bound is shared memory: an m128
-// n64 k32 MMA reads 6 KB of operands for 0.5 M ops, so 36 MMAs per stage
-// read 216 KB and the stage's cp.async writes add 48 KB -- about the 128
-// B/clk an SM's shared memory moves (the same shape alone, operands resident,
-// peaks at 2.75 POPS in tools/micro/tc_i8_probe.cu; N = 256 reaches 4.1
-// POPS, but 8 accumulators of 256 columns exceed the 512 TMEM columns).
+// Measured (C3, k = 4000, whole W step incl. the slicing): 54.7 ms per build
+// against 66.6 ms for the DMMA GEMM (cp.async-fed: 59.7; 2 stages of 64
+// bytes: 70.4; a two-pass 128 x 128 variant with 4 accumulators: 69.5).
+// An m128 n64 k32 MMA reads 6 KB of operands for 0.5 M ops, so the shape is
+// bound by shared-memory bandwidth (alone, operands resident, it peaks at
+// 2.75 POPS in tools/micro/tc_i8_probe.cu; N = 256 reaches 4.1 POPS, but 8
+// accumulators of 256 columns exceed the 512 TMEM columns).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <math_constants.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <mutex>
 
 #include "afn_common.cuh"
 #include "afn_internal.h"
@@ -90,9 +94,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void cp16(uint32_t saddr, const void* g) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
 
 // split |x| <= 1 into OZ_S signed 7-bit slices (exact)
 __device__ __forceinline__ void split8(double x, int8_t* out, int64_t stride) {
@@ -128,13 +129,13 @@ __global__ void __launch_bounds__(256) k21_slices_kernel(const double* __restric
   }
   double xr[16];
   for (int c = 0; c < d; ++c) xr[c] = Xr[r * d + c];
-  double mx = 0.0;
-  for (int64_t t = lane; t < k; t += 32) {
-    const double v = kern_from_d2(kf, d2_exact_rt(xr, &X1[t * d], d), s_tab);
-    mx = fmax(mx, fabs(v));
-  }
+  // the row max: both kernels decrease with the distance, so it is the
+  // value at the nearest landmark (a distance pass, one kernel evaluation)
+  double md2 = CUDART_INF;
+  for (int64_t t = lane; t < k; t += 32) md2 = fmin(md2, d2_exact_rt(xr, &X1[t * d], d));
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  for (int o = 16; o > 0; o >>= 1) md2 = fmin(md2, __shfl_xor_sync(0xffffffffu, md2, o));
+  const double mx = kern_from_d2(kf, md2, s_tab);
   int e = 0;
   if (mx > 0.0) frexp(mx, &e);  // mx < 2^e
   const double sc = ldexp(1.0, -e);
@@ -170,24 +171,45 @@ __global__ void __launch_bounds__(256) rows_slices_kernel(const double* __restri
   if (lane == 0) eb[c] = e;
 }
 
-// W[r][c] for the tile (blockIdx.y: 128 rows, blockIdx.x: 64 columns).
-// Asl: OZ_S slices of nrp x kp bytes; Bsl: OZ_S slices of kcp x kp bytes
-// (rows of L^{-1}); K range [0, min(k, c0 + 64)) rounded up to 64.
-__global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_kernel(const int8_t* __restrict__ Asl, const int* __restrict__ ea,
-                                                           int64_t nr, int64_t nrp, const int8_t* __restrict__ Bsl,
-                                                           const int* __restrict__ eb, int64_t k, int64_t kcp,
-                                                           int64_t kp, double* __restrict__ W, int64_t ldw) {
+// W[r][c] for the tile (blockIdx.y: 128 rows, blockIdx.x: 64 columns); the
+// K range [0, min(k, c0 + 64)) in 32-byte blocks.  TMA-fed and
+// warp-specialised: warp 0 (one lane) streams each stage's
+// 32 slice boxes (16 bytes x 128 / 64 rows each: one core-matrix column of
+// the no-swizzle layout) with cp.async.bulk.tensor onto the stage's "full"
+// mbarrier (expect_tx 48 KB); warp 1 (one lane) waits on it, issues the 36
+// MMAs and commits them to the stage's "empty" mbarrier, which the producer
+// waits on before refilling the buffer; the last commit releases the
+// epilogue (all four warps).
+__device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                               const __grid_constant__ CUtensorMap tmB,
+                                                               const int* __restrict__ ea, int64_t nr,
+                                                               const int* __restrict__ eb, int64_t k,
+                                                               double* __restrict__ W, int64_t ldw) {
   extern __shared__ uint8_t oz_raw[];
-  __shared__ __align__(8) uint64_t bar[OZ_NS];
+  __shared__ __align__(8) uint64_t full[OZ_NS], empty[OZ_NS], done;
   __shared__ uint32_t tmem_base;
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~(uintptr_t)1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t r0 = (int64_t)blockIdx.y * OZ_TM, c0 = (int64_t)blockIdx.x * OZ_TN;
-  const int64_t kend = min(k, c0 + OZ_TN);
+  const int r0 = (int)(blockIdx.y * OZ_TM), c0 = (int)(blockIdx.x * OZ_TN);
+  const int64_t kend = min(k, (int64_t)c0 + OZ_TN);
   const int nkb = (int)((kend + OZ_KB - 1) / OZ_KB);
-  const int64_t astride = nrp * kp, bstride = kcp * kp;
   if (tid == 0) {
-    for (int b = 0; b < OZ_NS; ++b) mbar_init(&bar[b], 1);
+    for (int b = 0; b < OZ_NS; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], 1);
+    }
+    mbar_init(&done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -199,45 +221,29 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_kernel(const int8_t* __restr
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-
-  // stage kb -> buffer b: A slice s rows r0.., B slice s rows c0.., bytes
-  // [64 kb, 64 kb + 64) as 16-byte chunks (unit u = 0..3) at
-  //   u * (R / 8) * 128 + (row / 8) * 128 + (row % 8) * 16
-  constexpr int UN = OZ_KB / 16;  // 16-byte units per row per stage
-  auto load = [&](int kb, int b) {
-    uint8_t* base = sm + (size_t)b * OZ_STAGE;
-    const int64_t kb0 = (int64_t)kb * OZ_KB;
-    for (int e = tid; e < OZ_S * OZ_TM * UN; e += OZ_NT) {
-      const int s = e / (OZ_TM * UN), rem = e - s * (OZ_TM * UN);
-      const int row = rem / UN, u = rem % UN;
-      const uint32_t dst = smem_u32(base + s * OZ_A_SL + u * (OZ_TM / 8) * 128 + (row >> 3) * 128 + (row & 7) * 16);
-      cp16(dst, Asl + s * astride + (r0 + row) * kp + kb0 + u * 16);
+  constexpr int UN = OZ_KB / 16;
+  if (warp == 0 && lane == 0) {  // producer
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int b = kb % OZ_NS;
+      if (kb >= OZ_NS) mbar_wait(&empty[b], (uint32_t)(((kb / OZ_NS) - 1) & 1));
+      mbar_expect(&full[b], (uint32_t)OZ_STAGE);
+      const uint32_t base = smem_u32(sm + (size_t)b * OZ_STAGE), fb = smem_u32(&full[b]);
+      const int kx = kb * OZ_KB;
+#pragma unroll
+      for (int sl = 0; sl < OZ_S; ++sl)
+#pragma unroll
+        for (int u = 0; u < UN; ++u) {
+          tma3(base + sl * OZ_A_SL + u * (OZ_TM / 8) * 128, &tmA, kx + u * 16, r0, sl, fb);
+          tma3(base + OZ_S * OZ_A_SL + sl * OZ_B_SL + u * (OZ_TN / 8) * 128, &tmB, kx + u * 16, c0, sl, fb);
+        }
     }
-    uint8_t* bb = base + OZ_S * OZ_A_SL;
-    for (int e = tid; e < OZ_S * OZ_TN * UN; e += OZ_NT) {
-      const int s = e / (OZ_TN * UN), rem = e - s * (OZ_TN * UN);
-      const int row = rem / UN, u = rem % UN;
-      const uint32_t dst = smem_u32(bb + s * OZ_B_SL + u * (OZ_TN / 8) * 128 + (row >> 3) * 128 + (row & 7) * 16);
-      cp16(dst, Bsl + s * bstride + (c0 + row) * kp + kb0 + u * 16);
-    }
-  };
-  auto commit = []() { asm volatile("cp.async.commit_group;" ::: "memory"); };
-
-  // stages 0 .. NS-2 in flight before the first MMA; one commit group per
-  // stage index (empty past the end) keeps wait_group's count uniform
-  for (int s0 = 0; s0 < OZ_NS - 1; ++s0) {
-    if (s0 < nkb) load(s0, s0);
-    commit();
-  }
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int b = kb % OZ_NS;
-    asm volatile("cp.async.wait_group %0;" ::"n"(OZ_NS - 2) : "memory");  // stage kb landed (this thread)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");          // generic writes -> tensor core
-    __syncthreads();                                                      // (every thread's)
-    if (tid == 0) {
+  } else if (warp == 1 && lane == 0) {  // MMA issuer
+    constexpr uint32_t LBO_A = (OZ_TM / 8) * 128, LBO_B = (OZ_TN / 8) * 128;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int b = kb % OZ_NS;
+      mbar_wait(&full[b], (uint32_t)((kb / OZ_NS) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t abase = smem_u32(sm + (size_t)b * OZ_STAGE), bbase = abase + OZ_S * OZ_A_SL;
-      constexpr uint32_t LBO_A = (OZ_TM / 8) * 128, LBO_B = (OZ_TN / 8) * 128;
 #pragma unroll
       for (int D = 0; D < OZ_S; ++D) {
 #pragma unroll
@@ -251,20 +257,12 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_kernel(const int8_t* __restr
           }
         }
       }
-      mma_commit(&bar[b]);
+      mma_commit(&empty[b]);
     }
-    __syncwarp();
-    const int nxt = kb + OZ_NS - 1;
-    if (nxt < nkb) {
-      // stage kb's MMAs are queued; buffer nxt % NS was last read by stage
-      // kb - 1's MMAs
-      if (kb >= 1) mbar_wait(&bar[(kb - 1) % OZ_NS], (uint32_t)(((kb - 1) / OZ_NS) & 1));
-      load(nxt, nxt % OZ_NS);
-    }
-    commit();
+    mma_commit(&done);
   }
-  // all MMAs done: the last stage's commit (tracks every earlier MMA of the thread)
-  mbar_wait(&bar[(nkb - 1) % OZ_NS], (uint32_t)(((nkb - 1) / OZ_NS) & 1));
+  __syncwarp();
+  mbar_wait(&done, 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const int64_t r = r0 + warp * 32 + lane;
   const bool rok = r < nr;
@@ -297,6 +295,40 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_kernel(const int8_t* __restr
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// 3-D tensor map over OZ_S slices of rows x cols int8 (row-major), box
+// 16 bytes x box_rows x 1 (no swizzle, no interleave)
+PFN_cuTensorMapEncodeTiled encode_fn() {
+  static PFN_cuTensorMapEncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  });
+  return fn;
+}
+afn_status slice_map(CUtensorMap* m, const int8_t* base, int64_t rows, int64_t cols, int box_rows) {
+  PFN_cuTensorMapEncodeTiled fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return AFN_ERR_CUDA;
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)OZ_S};
+  const cuuint64_t strides[2] = {(cuuint64_t)cols, (cuuint64_t)(rows * cols)};
+  const cuuint32_t box[3] = {16, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return AFN_ERR_CUDA;
+  }
+  return AFN_OK;
 }
 
 }  // namespace
@@ -338,9 +370,11 @@ afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const d
   AFN_LAUNCH_CHECK("rows_slices_kernel");
   static bool attr = false;
   if (!attr) {
-    AFN_CUDA(cudaFuncSetAttribute(w_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
+    AFN_CUDA(cudaFuncSetAttribute(w_ozaki_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
     attr = true;
   }
+  CUtensorMap tmB;
+  if ((s = slice_map(&tmB, Bsl, kcp, kp, OZ_TN)) != AFN_OK) return s;
   for (int64_t q0 = 0; q0 < N; q0 += rb) {
     const int64_t nr = std::min(rb, N - q0);
     const int64_t nrp = (nr + OZ_TM - 1) / OZ_TM * OZ_TM;
@@ -348,8 +382,10 @@ afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const d
                                                                           Asl, ea);
     AFN_LAUNCH_CHECK("k21_slices_kernel");
     dim3 grid((unsigned)(kcp / OZ_TN), (unsigned)(nrp / OZ_TM));
-    w_ozaki_kernel<<<grid, OZ_NT, OZ_SMEM, st>>>(Asl, ea, nr, nrp, Bsl, eb, k, kcp, kp, W + q0 * k, k);
-    AFN_LAUNCH_CHECK("w_ozaki_kernel");
+    CUtensorMap tmA;
+    if ((s = slice_map(&tmA, Asl, nrp, kp, OZ_TM)) != AFN_OK) return s;
+    w_ozaki_tma_kernel<<<grid, OZ_NT, OZ_SMEM, st>>>(tmA, tmB, ea, nr, eb, k, W + q0 * k, k);
+    AFN_LAUNCH_CHECK("w_ozaki_tma_kernel");
   }
   return AFN_OK;
 }
