@@ -1107,6 +1107,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
     if (k == 0) continue;
     if (!nys) TRY(ralloc(s, &s.Linv, (size_t)k * k, st));
+    // L^{-1}'s workspace from the build stream before the switch (a pool
+    // block taken on fs could carry a wait on another stream's work)
+    double* lws = nullptr;
+    TRY(ralloc(s, &lws, (size_t)linv_ws_doubles(k), st));
     // K11, its Cholesky and L^{-1}: with the pattern overlapped, on a
     // high-priority stream -- their ~200 short launches then take SMs ahead
     // of the kNN grid's pending CTAs instead of queueing behind them
@@ -1126,13 +1130,14 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     // C2 setup 12.1 vs 11.8 ms)
     if (fs != st) AFN_CUDA(cudaStreamWaitEvent(fs, e_pat1, 0));
     kt_begin(KT_LINV, fs);
-    TRY(trsm_linvt(s.L, k, s.LinvT, fs));
+    TRY(trsm_linvt(s.L, k, s.LinvT, fs, lws));
     if (!nys) TRY(transpose_sq(s.LinvT, k, s.Linv, fs));
     kt_end(KT_LINV, fs, (double)k * k * k / 3.0);
     if (fs != st) {
       AFN_CUDA(cudaEventRecord(e_hp1, fs));
       AFN_CUDA(cudaStreamWaitEvent(st, e_hp1, 0));
     }
+    rfree(s, lws, st);
   }
   AFN_CUDA(cudaEventRecord(ev[3], st));
   auto chol_check = [&]() -> afn_status {

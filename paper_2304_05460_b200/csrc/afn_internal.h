@@ -160,7 +160,9 @@ afn_status syrk_ata(const double* F, int64_t R, int64_t C, double* G, cudaStream
 afn_status gemm_nn(const double* A, const double* B, double* C, int64_t M, int64_t N, int64_t K, int64_t lda,
                    int64_t ldb, int64_t ldc, double alpha, cudaStream_t st);
 // LinvT (k x k row-major) = L^{-T} (upper triangular)
-afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st);
+// ws: nullptr (allocated on st) or linv_ws_doubles(k) doubles already ordered before st's work
+afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st, double* ws = nullptr);
+int64_t linv_ws_doubles(int64_t k);
 
 // ---- FSAI (fsai.cu) -------------------------------------------------------
 // G values of rows [row_lo, row_hi) on the pattern of the Schur complement

@@ -691,15 +691,16 @@ afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double
   return AFN_OK;
 }
 
-afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_t st) {
+afn_status linv_recursive(const double* L, int64_t k, double* LinvT, cudaStream_t st, double* ws) {
   int64_t kp = NB;
   while (kp < k) kp <<= 1;
-  double *Lp = nullptr, *X = nullptr, *Tt = nullptr;
   afn_status s;
-  if ((s = dalloc((void**)&Lp, sizeof(double) * kp * kp, st)) != AFN_OK) return s;
-  if ((s = dalloc((void**)&X, sizeof(double) * kp * kp, st)) != AFN_OK) { dfree(Lp, st); return s; }
-  if ((s = dalloc((void**)&Tt, sizeof(double) * kp * kp, st)) != AFN_OK) { dfree(Lp, st); dfree(X, st); return s; }
-  struct F { double *a, *b, *c; cudaStream_t st; ~F() { dfree(a, st); dfree(b, st); dfree(c, st); } } fr{Lp, X, Tt, st};
+  const bool own = ws == nullptr;
+  if (own && (s = dalloc((void**)&ws, sizeof(double) * 3 * kp * kp, st)) != AFN_OK) return s;
+  double* Lp = ws;
+  double* X = ws + kp * kp;
+  double* Tt = ws + 2 * kp * kp;
+  struct F { double* a; bool own; cudaStream_t st; ~F() { if (own) dfree(a, st); } } fr{ws, own, st};
   AFN_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * kp * kp, st));
   pad_l_kernel<<<(unsigned)((kp * kp + 255) / 256), 256, 0, st>>>(L, k, Lp, kp);
   AFN_LAUNCH_CHECK("pad_l_kernel");
@@ -753,9 +754,15 @@ afn_status transpose_sq(const double* A, int64_t k, double* At, cudaStream_t st)
   return AFN_OK;
 }
 
-afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st) {
+int64_t linv_ws_doubles(int64_t k) {
+  int64_t kp = NB;
+  while (kp < k) kp <<= 1;
+  return 3 * kp * kp;
+}
+
+afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st, double* ws) {
   TRY_SMEM();
-  return linv_recursive(L, k, LinvT, st);
+  return linv_recursive(L, k, LinvT, st, ws);
 }
 
 }  // namespace afn
