@@ -42,6 +42,7 @@
 
 #include "afn_common.cuh"
 #include "afn_internal.h"
+#include "tc05.cuh"
 
 namespace afn {
 
@@ -60,40 +61,7 @@ constexpr int OZ_STAGE = OZ_S * (OZ_A_SL + OZ_B_SL);  // 96 KB
 constexpr int OZ_SMEM = OZ_NS * OZ_STAGE + 1024;  // stages + alignment slack
 static_assert(OZ_NS * OZ_STAGE <= 200 * 1024, "stages exceed shared memory");
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-// shared-memory matrix descriptor: K-major, no swizzle (canonical
-// ((8, n), 2) : ((16 B, SBO), LBO) core-matrix layout), sm_100 version 1
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
-}
-// instruction descriptor: kind::i8, s32 accumulators, signed int8 A and B, both K-major
-constexpr uint32_t oz_idesc() {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(OZ_TN >> 3) << 17) | ((uint32_t)(OZ_TM >> 4) << 24);
-}
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(oz_idesc()), "r"(acc), "r"(0), "r"(0), "r"(0), "r"(0));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\tOZW_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra OZW_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
+using namespace tc;
 
 // split |x| <= 1 into OZ_S signed 7-bit slices (exact)
 __device__ __forceinline__ void split8(double x, int8_t* out, int64_t stride) {
@@ -180,17 +148,6 @@ __global__ void __launch_bounds__(256) rows_slices_kernel(const double* __restri
 // MMAs and commits them to the stage's "empty" mbarrier, which the producer
 // waits on before refilling the buffer; the last commit releases the
 // epilogue (all four warps).
-__device__ __forceinline__ void tma3(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(dst),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
 __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB,
                                                                const int* __restrict__ ea, int64_t nr,
@@ -210,17 +167,9 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_cons
       mbar_init(&empty[b], 1);
     }
     mbar_init(&done, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_init_fence();
   }
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_base;
+  const uint32_t tmem = tmem_alloc(&tmem_base, 512);
   constexpr int UN = OZ_KB / 16;
   if (warp == 0 && lane == 0) {  // producer
     for (int kb = 0; kb < nkb; ++kb) {
@@ -253,7 +202,7 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_cons
           for (int ks = 0; ks < OZ_KB / 32; ++ks) {
             const uint64_t da = umma_desc(abase + i * OZ_A_SL + ks * 2 * LBO_A, LBO_A, 128);
             const uint64_t db = umma_desc(bbase + j * OZ_B_SL + ks * 2 * LBO_B, LBO_B, 128);
-            mma_i8(tmem + (uint32_t)(D * OZ_TN), da, db, (kb > 0 || i > 0 || ks > 0) ? 1u : 0u);
+            mma_i8(tmem + (uint32_t)(D * OZ_TN), da, db, idesc_i8(OZ_TM, OZ_TN), (kb > 0 || i > 0 || ks > 0) ? 1u : 0u);
           }
         }
       }
@@ -272,14 +221,8 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_cons
   for (int cc = 0; cc < OZ_TN; cc += 8) {
     uint32_t v[OZ_S][8];
 #pragma unroll
-    for (int D = 0; D < OZ_S; ++D) {
-      const uint32_t ta = tmem + lane_base + (uint32_t)(D * OZ_TN + cc);
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(v[D][0]), "=r"(v[D][1]), "=r"(v[D][2]), "=r"(v[D][3]), "=r"(v[D][4]), "=r"(v[D][5]),
-                     "=r"(v[D][6]), "=r"(v[D][7])
-                   : "r"(ta));
-    }
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    for (int D = 0; D < OZ_S; ++D) tmem_ld8(tmem + lane_base + (uint32_t)(D * OZ_TN + cc), v[D]);
+    tmem_ld_wait();
     if (rok) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -292,9 +235,7 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_cons
       }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  tmem_free(tmem, 512);
 }
 
 // 3-D tensor map over OZ_S slices of rows x cols int8 (row-major), box
