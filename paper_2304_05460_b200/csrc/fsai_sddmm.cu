@@ -108,8 +108,15 @@ struct CellGrid {
   int g[3];   // cells per axis (padded to the tile)
   int t[3];   // tile size per axis
   int nb[3];  // tiles per axis
-  int64_t ncell;
+  int morton; // tiles in Z (Morton) order over a power-of-two tile grid, else raster
+  int64_t ncell;  // key space (cells, with the Morton padding)
 };
+
+__device__ __forceinline__ int64_t spread3(int64_t v) {  // bit i -> bit 3 i (v < 2^20)
+  int64_t r = 0;
+  for (int b = 0; b < 20; ++b) r |= ((v >> b) & 1) << (3 * b);
+  return r;
+}
 
 __global__ void cell_key_kernel(const double* __restrict__ X, int64_t N, int d, const double* __restrict__ box,
                                 CellGrid cg, int* __restrict__ key, int* __restrict__ cnt) {
@@ -125,7 +132,8 @@ __global__ void cell_key_kernel(const double* __restrict__ X, int64_t N, int d, 
   }
   const int b0 = cc[0] / cg.t[0], b1 = cc[1] / cg.t[1], b2 = cc[2] / cg.t[2];
   const int l0 = cc[0] % cg.t[0], l1 = cc[1] % cg.t[1], l2 = cc[2] % cg.t[2];
-  const int64_t tile = ((int64_t)b2 * cg.nb[1] + b1) * cg.nb[0] + b0;
+  const int64_t tile = cg.morton ? (spread3(b0) | (spread3(b1) << 1) | (spread3(b2) << 2))
+                                 : ((int64_t)b2 * cg.nb[1] + b1) * cg.nb[0] + b0;
   const int64_t k = tile * (cg.t[0] * cg.t[1] * cg.t[2]) + ((int64_t)l2 * cg.t[1] + l1) * cg.t[0] + l0;
   key[i] = (int)k;
   atomicAdd(&cnt[k], 1);
@@ -857,6 +865,21 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
       cg.nb[c] = cg.g[c] / cg.t[c];
     }
     cg.ncell = (int64_t)cg.g[0] * cg.g[1] * cg.g[2];
+    // Z-ordered tiles (raster: C3 factor 15.3 vs 14.9 ms, group product DRAM
+    // 155 vs 143 GB; the product's time is unchanged)
+    cg.morton = 1;
+    if (cg.morton) {  // key space: (next power of two of the largest tile count)^dd tiles
+      int nbm = 1;
+      for (int c = 0; c < dd; ++c) nbm = std::max(nbm, cg.nb[c]);
+      int64_t p2 = 1;
+      while (p2 < nbm) p2 <<= 1;
+      int64_t tiles = 1;
+      for (int c = 0; c < dd; ++c) tiles *= p2;
+      // (Morton interleaves 3 axes: with dd < 3 the unused axes are 0 and the
+      // codes of the used ones still fit below p2^dd only for dd = 3)
+      if (dd < 3) tiles = (int64_t)1 << (3 * (int64_t)std::ceil(std::log2((double)p2)));
+      cg.ncell = tiles * cg.t[0] * cg.t[1] * cg.t[2];
+    }
   }
   double *bws, *box;
   int *key, *cnt, *cur, *sorder, *grp, *loc;
