@@ -14,24 +14,27 @@
 // sum_t |A_rt||B_ct| -- the size of FP64 GEMM rounding.  36 INT8 products at
 // ~4 POPS replace one FP64 DMMA product at 37 TFLOP/s.
 //
-// GEMM kernel: one CTA (128 threads) per 128 x 64 tile of W (rows x columns,
-// the K range cut at the tile's last column: L^{-1} is lower triangular);
-// the 8 accumulators C_0..C_7 occupy the CTA's 512 TMEM columns (64 each).
-// K advances in 32-byte blocks through four shared-memory stages of all 16
-// slice tiles (48 KB each), filled by the TMA (3-D tensor maps over the
-// slice arrays, boxes of 16 bytes x 128 / 64 rows = one column of core
-// matrices of the K-major no-swizzle layout) onto "full" mbarriers; one
-// thread issues a stage's 36 MMAs (m128 n64 k32) and commits them to the
-// stage's "empty" mbarrier; epilogue: tcgen05.ld of the 8 accumulators,
-// Horner in FP64, the 2^(ea + eb - 12) scale, FP64 stores.
+// GEMM kernel: a cluster of two CTAs (tcgen05 cta_group::2) per 256 x 64 tile
+// of W (rows x columns, the K range cut at the tile's last column: L^{-1} is
+// lower triangular); each CTA holds its 128 rows' 8 accumulators C_0..C_7 in
+// its 512 TMEM columns (64 each).  K advances in 32-byte blocks through five
+// shared-memory stages: per CTA its 128 rows of the 8 A slices and half (32
+// rows) of the 8 B slices, 40 KB, filled by the TMA (3-D tensor maps over the
+// slice arrays, boxes of 16 bytes x 128 / 32 rows = one column of core
+// matrices of the K-major no-swizzle layout), both CTAs' loads completing on
+// CTA 0's "full" mbarrier; one thread of CTA 0 issues a stage's 36 m256 n64
+// k32 MMAs and commits them to both CTAs' "empty" mbarriers; epilogue:
+// tcgen05.ld of the 8 accumulators, Horner in FP64, the 2^(ea + eb - 12)
+// scale, FP64 stores.
 //
-// Measured (C3, k = 4000, whole W step incl. the slicing): 54.7 ms per build
-// against 66.6 ms for the DMMA GEMM (cp.async-fed: 59.7; 2 stages of 64
-// bytes: 70.4; a two-pass 128 x 128 variant with 4 accumulators: 69.5).
-// An m128 n64 k32 MMA reads 6 KB of operands for 0.5 M ops, so the shape is
-// bound by shared-memory bandwidth (alone, operands resident, it peaks at
-// 2.75 POPS in tools/micro/tc_i8_probe.cu; N = 256 reaches 4.1 POPS, but 8
-// accumulators of 256 columns exceed the 512 TMEM columns).
+// Measured (C3, k = 4000, whole W step incl. the slicing): 48.7 ms per build
+// against 66.6 ms for the DMMA GEMM (one-CTA 128 x 64 tiles, TMA: 55.8;
+// cp.async-fed: 59.7; 2 stages of 64 bytes: 70.4; a two-pass 128 x 128
+// variant with 4 accumulators: 69.5).  Operand traffic bounds it: an m128 n64
+// k32 MMA reads 6 KB for 0.5 M ops (alone, operands resident, the shape peaks
+// at 2.75 POPS in tools/micro/tc_i8_probe.cu; N = 256 reaches 4.1 POPS, but 8
+// accumulators of 256 columns exceed the 512 TMEM columns); the pair halves
+// the B traffic per CTA.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math_constants.h>
@@ -49,17 +52,12 @@ namespace afn {
 namespace {
 
 constexpr int OZ_S = 8;         // slices per operand
-constexpr int OZ_TM = 128;      // tile rows (W rows, MMA M)
+constexpr int OZ_TM = 128;      // tile rows per CTA (W rows; the pair MMA has M = 256)
 constexpr int OZ_TN = 64;       // tile columns (W columns, MMA N)
 constexpr int OZ_KB = 32;       // K bytes per stage (one MMA k-step)
-constexpr int OZ_NS = 4;        // stages (2 stages of 64 bytes: C3 W 70.4 ms; 4 of 32: 59.7 ms)
 
 constexpr int OZ_NT = 128;      // threads
-constexpr int OZ_A_SL = OZ_TM * OZ_KB;            // bytes of one A slice tile per stage (8 KB)
-constexpr int OZ_B_SL = OZ_TN * OZ_KB;            // bytes of one B slice tile per stage (4 KB)
-constexpr int OZ_STAGE = OZ_S * (OZ_A_SL + OZ_B_SL);  // 96 KB
-constexpr int OZ_SMEM = OZ_NS * OZ_STAGE + 1024;  // stages + alignment slack
-static_assert(OZ_NS * OZ_STAGE <= 200 * 1024, "stages exceed shared memory");
+constexpr int OZ_A_SL = OZ_TM * OZ_KB;            // bytes of one A slice tile per stage (4 KB)
 
 using namespace tc;
 
@@ -139,76 +137,114 @@ __global__ void __launch_bounds__(256) rows_slices_kernel(const double* __restri
   if (lane == 0) eb[c] = e;
 }
 
-// W[r][c] for the tile (blockIdx.y: 128 rows, blockIdx.x: 64 columns); the
-// K range [0, min(k, c0 + 64)) in 32-byte blocks.  TMA-fed and
-// warp-specialised: warp 0 (one lane) streams each stage's
-// 32 slice boxes (16 bytes x 128 / 64 rows each: one core-matrix column of
-// the no-swizzle layout) with cp.async.bulk.tensor onto the stage's "full"
-// mbarrier (expect_tx 48 KB); warp 1 (one lane) waits on it, issues the 36
-// MMAs and commits them to the stage's "empty" mbarrier, which the producer
-// waits on before refilling the buffer; the last commit releases the
-// epilogue (all four warps).
-__global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_constant__ CUtensorMap tmA,
+// Pair variant (cta_group::2): a cluster of two CTAs (vertically adjacent
+// row tiles) computes a 256 x 64 tile with m256 MMAs issued by CTA 0: each
+// CTA loads its own 128 A rows and half of the 64 B rows (the pair's tensor
+// cores read both halves), so a CTA stages 40 KB instead of 48 KB per 32-byte
+// K block.  Both CTAs' TMA loads complete on CTA 0's "full" mbarrier (peer
+// bit cleared in the address); CTA 0's commits arrive on both CTAs' "empty"
+// and "done" mbarriers (multicast); each CTA reads its own 128 TMEM lanes in
+// the epilogue.
+constexpr int OZ2_BH = OZ_TN / 2;                       // B rows per CTA
+constexpr int OZ2_B_SL = OZ2_BH * OZ_KB;                // 1 KB
+constexpr int OZ2_STAGE = OZ_S * (OZ_A_SL + OZ2_B_SL);  // 40 KB
+constexpr int OZ2_NS = 5;
+constexpr int OZ2_SMEM = OZ2_NS * OZ2_STAGE + 1024;
+__global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_2sm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                                const __grid_constant__ CUtensorMap tmB,
                                                                const int* __restrict__ ea, int64_t nr,
                                                                const int* __restrict__ eb, int64_t k,
                                                                double* __restrict__ W, int64_t ldw) {
   extern __shared__ uint8_t oz_raw[];
-  __shared__ __align__(8) uint64_t full[OZ_NS], empty[OZ_NS], done;
+  __shared__ __align__(8) uint64_t full[OZ2_NS], empty[OZ2_NS], done;
   __shared__ uint32_t tmem_base;
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(oz_raw) + 1023) & ~(uintptr_t)1023);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int r0 = (int)(blockIdx.y * OZ_TM), c0 = (int)(blockIdx.x * OZ_TN);
+  uint32_t crank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int r0 = (int)(blockIdx.x * OZ_TM), c0 = (int)(blockIdx.y * OZ_TN);  // (pairs along x)
   const int64_t kend = min(k, (int64_t)c0 + OZ_TN);
   const int nkb = (int)((kend + OZ_KB - 1) / OZ_KB);
   if (tid == 0) {
-    for (int b = 0; b < OZ_NS; ++b) {
+    for (int b = 0; b < OZ2_NS; ++b) {
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], 1);
     }
     mbar_init(&done, 1);
     mbar_init_fence();
   }
-  const uint32_t tmem = tmem_alloc(&tmem_base, 512);
+  // TMEM: both CTAs' warp 0 allocate the pair's columns (same slot offset)
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  // both CTAs' barriers initialised and TMEM allocated before any cross-CTA use
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
   constexpr int UN = OZ_KB / 16;
-  if (warp == 0 && lane == 0) {  // producer
+  if (warp == 0 && lane == 0) {  // producer (each CTA: its A rows, its half of B)
     for (int kb = 0; kb < nkb; ++kb) {
-      const int b = kb % OZ_NS;
-      if (kb >= OZ_NS) mbar_wait(&empty[b], (uint32_t)(((kb / OZ_NS) - 1) & 1));
-      mbar_expect(&full[b], (uint32_t)OZ_STAGE);
-      const uint32_t base = smem_u32(sm + (size_t)b * OZ_STAGE), fb = smem_u32(&full[b]);
+      const int b = kb % OZ2_NS;
+      if (kb >= OZ2_NS) mbar_wait(&empty[b], (uint32_t)(((kb / OZ2_NS) - 1) & 1));
+      if (crank == 0) mbar_expect(&full[b], 2u * (uint32_t)OZ2_STAGE);
+      const uint32_t base = smem_u32(sm + (size_t)b * OZ2_STAGE);
+      const uint32_t fb = smem_u32(&full[b]) & 0xFEFFFFFFu;  // CTA 0's barrier
       const int kx = kb * OZ_KB;
 #pragma unroll
       for (int sl = 0; sl < OZ_S; ++sl)
 #pragma unroll
         for (int u = 0; u < UN; ++u) {
-          tma3(base + sl * OZ_A_SL + u * (OZ_TM / 8) * 128, &tmA, kx + u * 16, r0, sl, fb);
-          tma3(base + OZ_S * OZ_A_SL + sl * OZ_B_SL + u * (OZ_TN / 8) * 128, &tmB, kx + u * 16, c0, sl, fb);
+          asm volatile(
+              "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(base + sl * OZ_A_SL + u * (OZ_TM / 8) * 128),
+              "l"(reinterpret_cast<uint64_t>(&tmA)), "r"(kx + u * 16), "r"(r0), "r"(sl), "r"(fb)
+              : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(base + OZ_S * OZ_A_SL + sl * OZ2_B_SL +
+                                                         u * (OZ2_BH / 8) * 128),
+              "l"(reinterpret_cast<uint64_t>(&tmB)), "r"(kx + u * 16), "r"(c0 + OZ2_BH * (int)crank), "r"(sl),
+              "r"(fb)
+              : "memory");
         }
     }
-  } else if (warp == 1 && lane == 0) {  // MMA issuer
-    constexpr uint32_t LBO_A = (OZ_TM / 8) * 128, LBO_B = (OZ_TN / 8) * 128;
+  } else if (warp == 1 && lane == 0 && crank == 0) {  // MMA issuer (CTA 0)
+    constexpr uint32_t LBO_A = (OZ_TM / 8) * 128, LBO_B = (OZ2_BH / 8) * 128;
+    constexpr uint32_t idesc = idesc_i8(2 * OZ_TM, OZ_TN);
     for (int kb = 0; kb < nkb; ++kb) {
-      const int b = kb % OZ_NS;
-      mbar_wait(&full[b], (uint32_t)((kb / OZ_NS) & 1));
+      const int b = kb % OZ2_NS;
+      mbar_wait(&full[b], (uint32_t)((kb / OZ2_NS) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t abase = smem_u32(sm + (size_t)b * OZ_STAGE), bbase = abase + OZ_S * OZ_A_SL;
+      const uint32_t abase = smem_u32(sm + (size_t)b * OZ2_STAGE), bbase = abase + OZ_S * OZ_A_SL;
 #pragma unroll
       for (int D = 0; D < OZ_S; ++D) {
 #pragma unroll
         for (int i = 0; i <= D; ++i) {
-          const int j = D - i;
-#pragma unroll
-          for (int ks = 0; ks < OZ_KB / 32; ++ks) {
-            const uint64_t da = umma_desc(abase + i * OZ_A_SL + ks * 2 * LBO_A, LBO_A, 128);
-            const uint64_t db = umma_desc(bbase + j * OZ_B_SL + ks * 2 * LBO_B, LBO_B, 128);
-            mma_i8(tmem + (uint32_t)(D * OZ_TN), da, db, idesc_i8(OZ_TM, OZ_TN), (kb > 0 || i > 0 || ks > 0) ? 1u : 0u);
-          }
+          const uint64_t da = umma_desc(abase + i * OZ_A_SL, LBO_A, 128);
+          const uint64_t db = umma_desc(bbase + (D - i) * OZ2_B_SL, LBO_B, 128);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8, %9, %10, %11, %12}, p;\n\t}\n" ::
+                  "r"(tmem + (uint32_t)(D * OZ_TN)),
+              "l"(da), "l"(db), "r"(idesc), "r"((kb > 0 || i > 0) ? 1u : 0u), "r"(0), "r"(0), "r"(0), "r"(0),
+              "r"(0), "r"(0), "r"(0), "r"(0));
         }
       }
-      mma_commit(&empty[b]);
+      asm volatile(
+          "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+              smem_u32(&empty[b])),
+          "h"((uint16_t)3)
+          : "memory");
     }
-    mma_commit(&done);
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(&done)),
+        "h"((uint16_t)3)
+        : "memory");
   }
   __syncwarp();
   mbar_wait(&done, 0);
@@ -235,7 +271,10 @@ __global__ void __launch_bounds__(OZ_NT, 1) w_ozaki_tma_kernel(const __grid_cons
       }
     }
   }
-  tmem_free(tmem, 512);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  // neither CTA frees the pair's TMEM before both finished reading
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // 3-D tensor map over OZ_S slices of rows x cols int8 (row-major), box
@@ -287,8 +326,9 @@ afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const d
   const int64_t kp = (k + OZ_KB - 1) / OZ_KB * OZ_KB;
   const int64_t kcp = (k + OZ_TN - 1) / OZ_TN * OZ_TN;
   // row blocks: the A slices of one block <= ~1 GiB
-  const int64_t rb = std::max<int64_t>(OZ_TM, ((1ll << 30) / (OZ_S * kp)) / OZ_TM * OZ_TM);
-  const int64_t nblk_rows = std::min<int64_t>(rb, (N + OZ_TM - 1) / OZ_TM * OZ_TM);
+  // (row tiles in pairs: blocks and padding in multiples of 256 rows)
+  const int64_t rb = std::max<int64_t>(2 * OZ_TM, ((1ll << 30) / (OZ_S * kp)) / (2 * OZ_TM) * (2 * OZ_TM));
+  const int64_t nblk_rows = std::min<int64_t>(rb, (N + 2 * OZ_TM - 1) / (2 * OZ_TM) * (2 * OZ_TM));
   int8_t *Asl = nullptr, *Bsl = nullptr;
   int *ea = nullptr, *eb = nullptr;
   afn_status s;
@@ -311,22 +351,34 @@ afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const d
   AFN_LAUNCH_CHECK("rows_slices_kernel");
   static bool attr = false;
   if (!attr) {
-    AFN_CUDA(cudaFuncSetAttribute(w_ozaki_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ_SMEM));
+    AFN_CUDA(cudaFuncSetAttribute(w_ozaki_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, OZ2_SMEM));
     attr = true;
   }
   CUtensorMap tmB;
-  if ((s = slice_map(&tmB, Bsl, kcp, kp, OZ_TN)) != AFN_OK) return s;
+  if ((s = slice_map(&tmB, Bsl, kcp, kp, OZ2_BH)) != AFN_OK) return s;
   for (int64_t q0 = 0; q0 < N; q0 += rb) {
     const int64_t nr = std::min(rb, N - q0);
-    const int64_t nrp = (nr + OZ_TM - 1) / OZ_TM * OZ_TM;
+    const int64_t nrp = (nr + 2 * OZ_TM - 1) / (2 * OZ_TM) * (2 * OZ_TM);
     k21_slices_kernel<<<(unsigned)((nrp * 32 + 255) / 256), 256, 0, st>>>(X1, k, kp, Xr + q0 * d, nr, nrp, d, kf,
                                                                           Asl, ea);
     AFN_LAUNCH_CHECK("k21_slices_kernel");
-    dim3 grid((unsigned)(kcp / OZ_TN), (unsigned)(nrp / OZ_TM));
     CUtensorMap tmA;
     if ((s = slice_map(&tmA, Asl, nrp, kp, OZ_TM)) != AFN_OK) return s;
-    w_ozaki_tma_kernel<<<grid, OZ_NT, OZ_SMEM, st>>>(tmA, tmB, ea, nr, eb, k, W + q0 * k, k);
-    AFN_LAUNCH_CHECK("w_ozaki_tma_kernel");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nrp / OZ_TM), (unsigned)(kcp / OZ_TN));  // row tiles along x: pairs (2i, 2i + 1)
+    cfg.blockDim = dim3(OZ_NT);
+    cfg.dynamicSmemBytes = OZ2_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    AFN_CUDA(cudaLaunchKernelEx(&cfg, w_ozaki_2sm_kernel, tmA, tmB, (const int*)ea, nr, (const int*)eb, k, W + q0 * k,
+                                (int64_t)k));
+    AFN_LAUNCH_CHECK("w_ozaki_2sm_kernel");
   }
   return AFN_OK;
 }
