@@ -865,9 +865,12 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
       cg.nb[c] = cg.g[c] / cg.t[c];
     }
     cg.ncell = (int64_t)cg.g[0] * cg.g[1] * cg.g[2];
-    // Z-ordered tiles (raster: C3 factor 15.3 vs 14.9 ms, group product DRAM
-    // 155 vs 143 GB; the product's time is unchanged)
-    cg.morton = 1;
+    // raster-ordered tiles.  (Z-ordered tiles measured C3 factor 14.9 vs 15.3
+    // ms and group-product DRAM 143 vs 155 GB, but at C5 some groups' unions
+    // -- the Z-order predecessors of hub points of the early, wide pattern rows
+    // -- exceed UCAP and the build falls back to the per-row Grams: 12.0 vs
+    // 6.8 s per solve)
+    cg.morton = 0;
     if (cg.morton) {  // key space: (next power of two of the largest tile count)^dd tiles
       int nbm = 1;
       for (int c = 0; c < dd; ++c) nbm = std::max(nbm, cg.nb[c]);

@@ -77,8 +77,14 @@ def test_full_size_component_parity(name, l):
     X, b = gen_problem(cfg)
     n = cfg.n
     Xd, bd = T(X), T(b)
+    afn.kernel_timers(reset=True, enable=True)
     h = afn.afn_build(Xd, afn.make_params(l, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True))
+    kt = afn.kernel_timers(enable=False)
     inf = h.info()
+    # the FSAI rows come from the pair-union product (no union overflowed into
+    # the per-row Gram fallback), W from the INT8 path when k >= 512 (d = 3)
+    if cfg.d == 3:
+        assert kt["fsai_gram_kernel"]["count"] == 0 and kt["group_gemm_kernel"]["count"] > 0
 
     # ---- Alg. 1: bit-exact decisions
     ro = O.alg1(X, l)
