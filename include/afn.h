@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define AFN_ABI_VERSION 5
+#define AFN_ABI_VERSION 6
 /* widest FSAI row (nonzeros incl. the diagonal): the paper's plain-FSAI
  * comparison uses 400 neighbours */
 #define AFN_W_MAX 512
@@ -119,6 +119,13 @@ typedef struct {
   int64_t row_a0, row_na, row_b0, row_nb; /* rows of the permuted order it owns   */
   int32_t kernel, method;       /* kernel, preconditioner built (AFN_METHOD_AFN,   */
                                 /* _NYSTROM or _FSAI)                              */
+  /* the handle's kernel-matvec plan (afn_set_matvec_mode):      */
+  /* 0 row-wise, 1 dense symmetric, 2 cutoff; work units of the FP64 and FP32   */
+  /* bodies and the unordered pairs they evaluate per product (one rank's plan  */
+  /* covers all ranks' units)                                                    */
+  int32_t kmv_plan, kmv_reserved;
+  int64_t kmv_units64, kmv_units32;
+  double kmv_pairs64, kmv_pairs32;
 } afn_info;
 
 /* PCG report (host struct).  history: optional host array of >= maxit+1
@@ -308,6 +315,22 @@ afn_status afn_build_dist(afn_comm comm, const double* X, int64_t n, int32_t d,
 afn_status afn_probe_dfma(int64_t iters, double* tflops /*host*/, void* stream);
 /* Same for FP64 tensor-core DMMA (mma.sync m8n8k4 f64).                      */
 afn_status afn_probe_dmma(int64_t iters, double* tflops /*host*/, void* stream);
+/* MUFU.EX2 throughput (ex2.approx.ftz.f32 chains on every SM), in G ops/s: */
+/* the bound of the cutoff matvec's FP32 body (one EX2 per pair).  [sync]    */
+afn_status afn_probe_ex2(int64_t iters, double* gops /*host*/, void* stream);
+
+/* Kernel-matvec plan for the products planned after the call (process-wide; */
+/* DESIGN.md 6.2).  Gaussian kernel, d <= 3, full product:                   */
+/*   0 (default) the cutoff plan -- points in a spatial order, (row block,   */
+/*     column tile) units whose boxes are farther apart than s = 128         */
+/*     (log2 units: every entry < 2^-128) skipped, units farther than s = 48 */
+/*     (entries < 2^-48) in FP32 -- when it keeps at most half of the pairs, */
+/*     else the dense symmetric plan;                                        */
+/*   1 always the dense symmetric plan (every pair in FP64);                 */
+/*   2 the cutoff plan whenever it applies.                                  */
+/* Other kernels / d > 3 / row ranges: the dense plans.  AFN_ERR_ARG for     */
+/* any other mode.                                                           */
+afn_status afn_set_matvec_mode(int32_t mode);
 
 /* Per-kernel CUDA-event timers (off by default).  When enabled the library
  * records an event pair around each timed kernel class on the launching

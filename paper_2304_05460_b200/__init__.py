@@ -63,7 +63,10 @@ class Info(C.Structure):
                 ("ms_fsai", C.c_double), ("ms_total", C.c_double), ("ms_fsai_rows", C.c_double),
                 ("nranks", C.c_int32), ("rank", C.c_int32), ("row_a0", C.c_int64),
                 ("row_na", C.c_int64), ("row_b0", C.c_int64), ("row_nb", C.c_int64),
-                ("kernel", C.c_int32), ("method", C.c_int32)]
+                ("kernel", C.c_int32), ("method", C.c_int32),
+                ("kmv_plan", C.c_int32), ("kmv_reserved", C.c_int32),
+                ("kmv_units64", C.c_int64), ("kmv_units32", C.c_int64),
+                ("kmv_pairs64", C.c_double), ("kmv_pairs32", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -121,6 +124,8 @@ _sig = {
     "afn_destroy": (None, [_P]),
     "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_probe_dmma": (C.c_int, [C.c_int64, _D, _P]),
+    "afn_probe_ex2": (C.c_int, [C.c_int64, _D, _P]),
+    "afn_set_matvec_mode": (C.c_int, [C.c_int32]),
     "afn_launch_count": (C.c_int64, []),
     "afn_kt_enable": (None, [C.c_int32]),
     "afn_kt_reset": (None, []),
@@ -539,6 +544,18 @@ def probe_dmma(iters=1 << 14, stream=None) -> float:
     out = C.c_double()
     _check(_lib.afn_probe_dmma(int(iters), C.byref(out), _stream(stream)), "afn_probe_dmma")
     return out.value
+
+
+def probe_ex2(iters=1 << 16, stream=None) -> float:
+    """MUFU.EX2 G ops/s (afn_probe_ex2)."""
+    out = C.c_double()
+    _check(_lib.afn_probe_ex2(int(iters), C.byref(out), _stream(stream)), "afn_probe_ex2")
+    return out.value
+
+
+def set_matvec_mode(mode: int) -> None:
+    """0 auto (cutoff plan when it pays), 1 dense symmetric, 2 cutoff (afn_set_matvec_mode)."""
+    _check(_lib.afn_set_matvec_mode(int(mode)), "afn_set_matvec_mode")
 
 
 def probe_dfma(iters=1 << 16, stream=None) -> float:

@@ -1254,9 +1254,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   // ---- workspaces for apply / PCG
   for (auto& s : h->rk) {
     const int64_t nl = s.own.size();
-    s.plan = kmv_plan(n, nl, d, num_sms(), true, h->R, s.rank);
-    TRY(ralloc(s, &s.kmv_part, (size_t)std::max<int64_t>(1, s.plan.ws), st));
-    TRY(kmv_plan_init(s.plan, s.kmv_part, st));
+    TRY(kmv_plan_make(s.Xs, n, nl, d, h->kn.kind, true, h->R, s.rank, st,
+                      [&](double** q, size_t c) { return ralloc(s, q, c, st); }, &s.plan, &s.kmv_part));
     if (s.plan.sym && h->R > 1) TRY(ralloc(s, &s.qpart, (size_t)h->R * n, st));
     const int64_t gw = std::max(std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k)),
                                 nys ? gemv_t_ws(nl, k) : (int64_t)1);
@@ -1401,10 +1400,10 @@ afn_status kmv_rows_impl(const double* X, int64_t n, int32_t d, int32_t kernel, 
   double* Xs;
   TRY(t.get(&Xs, (size_t)n * d));
   TRY(kmv_prescale(X, n, d, Kern{kernel, l}, Xs, st));
-  KmvPlan plan = kmv_plan(n, nrows, d, num_sms(), sym_ok && row0 == 0 && nrows == n);
-  double* part;
-  TRY(t.get(&part, (size_t)std::max<int64_t>(1, plan.ws)));
-  TRY(kmv_plan_init(plan, part, st));
+  KmvPlan plan;
+  double* part = nullptr;
+  TRY(kmv_plan_make(Xs, n, nrows, d, kernel, sym_ok && row0 == 0 && nrows == n, 1, 0, st,
+                    [&](double** q, size_t c) { return t.get(q, c); }, &plan, &part));
   TRY(kmv_launch(Xs, n, d, kernel, v, mu, seg_range(row0, nrows), y, false, part, plan, st));
   return AFN_OK;
 }
@@ -1886,6 +1885,12 @@ afn_status afn_get_info(afn_handle h, afn_info* info) {
   I.row_nb = h->rk[0].own.nb;
   I.kernel = h->kn.kind;
   I.method = h->method;
+  const KmvPlan& kp = h->rk[0].plan;
+  I.kmv_plan = kp.cut ? 2 : (kp.sym ? 1 : 0);
+  I.kmv_units64 = kp.cut ? kp.cut_u64 : kp.sym_units;
+  I.kmv_units32 = 0;  // (cutoff plan: classes are per warp; see the pairs)
+  I.kmv_pairs64 = kp.cut ? kp.cut_pairs64 : (kp.sym ? (double)h->n * (double)(h->n - 1) / 2.0 : 0.0);
+  I.kmv_pairs32 = kp.cut_pairs32;
   *info = I;
   return AFN_OK;
 }
@@ -1947,6 +1952,17 @@ afn_status afn_probe_dmma(int64_t iters, double* tflops, void* stream) {
 afn_status afn_probe_dfma(int64_t iters, double* tflops, void* stream) {
   REQ(iters >= 8 && tflops, "bad arguments");
   return probe_dfma(iters, tflops, (cudaStream_t)stream);
+}
+
+afn_status afn_probe_ex2(int64_t iters, double* gops, void* stream) {
+  REQ(iters >= 8 && gops, "bad arguments");
+  return probe_ex2(iters, gops, (cudaStream_t)stream);
+}
+
+afn_status afn_set_matvec_mode(int32_t mode) {
+  REQ(mode >= 0 && mode <= 2, "matvec mode %d (0 auto, 1 dense, 2 cutoff)", mode);
+  kmv_set_mode(mode);
+  return AFN_OK;
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <utility>
 #include <vector>
 
@@ -89,8 +90,32 @@ struct KmvPlan {
   bool sym = false;
   int64_t sym_rbw = 0, sym_nrb = 0, sym_nt = 0, sym_units = 0, sym_grid = 0, sym_gt = 0, sym_tab_dbl = 0;
   int sym_R = 1, sym_rank = 0;
+  // cutoff plan (Gaussian, d <= 3; kmv.cu): the symmetric
+  // split over a spatial order of the points, keeping only the (row block,
+  // 32-column tile) units whose bounding boxes are closer than the skip bound
+  // (every entry of a skipped unit is below 2^-128); units whose boxes are
+  // closer than the FP64 bound run the FP64 body, the rest (entries below
+  // 2^-48) an FP32 body.  The unit list, its transpose and the spatial order
+  // live in the workspace at the offsets below (in doubles).
+  bool cut = false;
+  int64_t cut_u64 = 0, cut_u32 = 0, cut_ntiles = 0;
+  double cut_pairs64 = 0, cut_pairs32 = 0;  // useful unordered pairs per class
+  int64_t o_rp = 0, o_cb = 0, o_xc = 0, o_ctr = 0, o_sidx = 0, o_ut = 0, o_ustart = 0, o_wst = 0, o_seg = 0,
+          o_rbase = 0, o_tptr = 0, o_tu = 0;
   int64_t ws = 0;  // workspace doubles for kmv_launch
 };
+// matvec plan selection (afn_set_matvec_mode): 0 auto (cutoff plan when it
+// keeps at most half of the pairs), 1 never the cutoff plan, 2 the cutoff
+// plan whenever it applies (Gaussian, d <= 3, full symmetric product)
+void kmv_set_mode(int mode);
+int kmv_get_mode();
+using WsGet = std::function<afn_status(double**, size_t)>;
+// The plan of a full (sym_ok) or row-range product for the prescaled points
+// Xs and its workspace *ws (allocated through get, tables uploaded): the
+// cutoff plan when it applies, else kmv_plan + kmv_plan_init.  Synchronises
+// `st` (the unit counts come back to the host).
+afn_status kmv_plan_make(const double* Xs, int64_t n, int64_t nrows, int d, int kind, bool sym_ok, int R, int rank,
+                         cudaStream_t st, const WsGet& get, KmvPlan* out, double** ws);
 // sym_ok: a full matvec may use the symmetric kernel (its row sums differ from
 // a row shard's by rounding; kernel_matvec_rows never uses it).  With R > 1
 // ranks the symmetric plan splits the pair units over the ranks
@@ -254,5 +279,6 @@ afn_status alg1_run(const double* X, int64_t n, int d, Kern kn, int m, uint64_t 
 // ---- probes (probe.cu) -----------------------------------------------------
 afn_status probe_dfma(int64_t iters, double* tflops, cudaStream_t st);
 afn_status probe_dmma(int64_t iters, double* tflops, cudaStream_t st);
+afn_status probe_ex2(int64_t iters, double* gops, cudaStream_t st);
 
 }  // namespace afn

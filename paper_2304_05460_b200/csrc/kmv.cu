@@ -406,6 +406,601 @@ __global__ void __launch_bounds__(SRT) kmv_sym_combine_kernel(const double* __re
   finish_sum(dsum, dws, dcnt, dout);
 }
 
+// ============================================================================
+// Cutoff plan (Gaussian, d <= 3).  K_ij = 2^(-s_ij) with s_ij =
+// ||xs_i - xs_j||^2 (prescaled points).  The points are put in a spatial
+// (Morton cell) order; the symmetric split's units (row block I of 1024
+// positions, 32-position column tile t >= 32 I) are kept only if the boxes of
+// block I and tile t are closer than s = 128 (a skipped unit's entries are all
+// below 2^-128, under FP32's normal range: the FP32 body flushes them too).
+// Units whose boxes are closer than s = 48 run the FP64 body of the dense
+// symmetric kernel; the others (every entry below 2^-48) an FP32 body: the
+// coordinates relative to the row block's box centre, the exponential by
+// MUFU.EX2, per-unit FP32 sums added into the FP64 row and column sums.
+// ============================================================================
+constexpr double KC_S64 = 48.0;
+constexpr double KC_SKIP = 128.0;
+
+__device__ __forceinline__ float kc_ex2_neg(float s) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(-s));
+  return r;
+}
+
+__global__ void kc_bbox_kernel(const double* __restrict__ X, int64_t n, int d, double* __restrict__ ws) {
+  __shared__ double sm[6][256];
+  const int dd = d < 3 ? d : 3;
+  double v6[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    for (int c = 0; c < dd; ++c) {
+      const double x = X[i * d + c];
+      v6[c] = fmin(v6[c], x);
+      v6[3 + c] = fmax(v6[3 + c], x);
+    }
+  for (int c = 0; c < 6; ++c) sm[c][threadIdx.x] = v6[c];
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o)
+      for (int c = 0; c < 6; ++c)
+        sm[c][threadIdx.x] = c < 3 ? fmin(sm[c][threadIdx.x], sm[c][threadIdx.x + o])
+                                   : fmax(sm[c][threadIdx.x], sm[c][threadIdx.x + o]);
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) ws[blockIdx.x * 6 + threadIdx.x] = sm[threadIdx.x][0];
+}
+
+struct KcGrid {
+  int dd, bits, g;
+  double lo[3], inv[3];
+};
+
+__global__ void kc_key_kernel(const double* __restrict__ X, int64_t n, int d, KcGrid gd, unsigned* __restrict__ key,
+                              int* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  unsigned c[3] = {0u, 0u, 0u};
+  for (int q = 0; q < gd.dd; ++q) {
+    int v = (int)((X[i * d + q] - gd.lo[q]) * gd.inv[q]);
+    c[q] = (unsigned)(v < 0 ? 0 : (v >= gd.g ? gd.g - 1 : v));
+  }
+  unsigned k = 0u;
+  for (int b = 0; b < gd.bits; ++b)
+    for (int q = 0; q < gd.dd; ++q) k |= ((c[q] >> b) & 1u) << (b * gd.dd + q);
+  key[i] = k;
+  atomicAdd(&cnt[k], 1);
+}
+
+// exclusive scan of M ints into off[0..M] (int64), one block of 1024
+__global__ void kc_scan_kernel(const int* __restrict__ cnt, int64_t M, int64_t* __restrict__ off) {
+  __shared__ int64_t part[1024];
+  const int tid = threadIdx.x;
+  const int64_t per = (M + 1023) / 1024;
+  const int64_t b = tid * per, e = min(M, b + per);
+  int64_t s = 0;
+  for (int64_t t = b; t < e; ++t) s += cnt[t];
+  part[tid] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    const int64_t v = tid >= o ? part[tid - o] : 0;
+    __syncthreads();
+    part[tid] += v;
+    __syncthreads();
+  }
+  int64_t run = tid > 0 ? part[tid - 1] : 0;
+  for (int64_t t = b; t < e; ++t) {
+    off[t] = run;
+    run += cnt[t];
+  }
+  if (tid == 1023) off[M] = part[1023];
+}
+
+__global__ void kc_scatter_kernel(const unsigned* __restrict__ key, int64_t n, const int64_t* __restrict__ off,
+                                  int* __restrict__ cur, int* __restrict__ sidx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned k = key[i];
+  sidx[off[k] + atomicAdd(&cur[k], 1)] = (int)i;
+}
+
+// within a cell: ascending original index (the atomics' order is not fixed)
+__global__ void kc_cell_sort_kernel(const int64_t* __restrict__ off, int64_t M, int* __restrict__ sidx) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= M) return;
+  const int64_t b = off[c], e = off[c + 1];
+  for (int64_t i = b + 1; i < e; ++i) {
+    const int v = sidx[i];
+    int64_t j = i - 1;
+    while (j >= b && sidx[j] > v) {
+      sidx[j + 1] = sidx[j];
+      --j;
+    }
+    sidx[j + 1] = v;
+  }
+}
+
+__global__ void kc_gather_kernel(const double* __restrict__ X, int64_t n, int d, const int* __restrict__ sidx,
+                                 double* __restrict__ Xc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * d) return;
+  const int64_t p = e / d;
+  Xc[e] = X[(int64_t)sidx[p] * d + (e - p * d)];
+}
+
+// boxes of the 32-position tiles (one warp per tile) -> tbox[t][lo 3, hi 3]
+__global__ void kc_tile_box_kernel(const double* __restrict__ Xc, int64_t n, int d, int64_t ntiles,
+                                   double* __restrict__ tbox) {
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= ntiles) return;
+  const int64_t i = t * 32 + lane;
+  for (int q = 0; q < 3; ++q) {
+    double lo = 1e300, hi = -1e300;
+    if (q < d && i < n) lo = hi = Xc[i * d + q];
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      tbox[t * 6 + q] = q < d ? lo : 0.0;
+      tbox[t * 6 + 3 + q] = q < d ? hi : 0.0;
+    }
+  }
+}
+
+// groups of 128 consecutive positions (4 tiles) own the rows of an item; the
+// coarse blocks of 1024 positions prefilter the box tests
+constexpr int KC_GR = 128;
+constexpr int KC_GT = KC_GR / 32;
+constexpr int KC_CB = 1024;
+constexpr int KC_W64 = 16, KC_W32 = 5;  // split weights of an FP64 / FP32 item
+constexpr unsigned KC_F32 = 0x80000000u;
+
+// boxes of blocks of `per` tiles (one warp per block; per <= 32) and their
+// centres (optional)
+__global__ void kc_block_box_kernel(const double* __restrict__ tbox, int64_t ntiles, int64_t nb, int per,
+                                    double* __restrict__ bbox, double* __restrict__ ctr) {
+  const int64_t I = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (I >= nb) return;
+  const int64_t t = I * per + lane;
+  for (int q = 0; q < 3; ++q) {
+    double lo = 1e300, hi = -1e300;
+    if (lane < per && t < ntiles) {
+      lo = tbox[t * 6 + q];
+      hi = tbox[t * 6 + 3 + q];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if (lane == 0) {
+      bbox[I * 6 + q] = lo;
+      bbox[I * 6 + 3 + q] = hi;
+      if (ctr) ctr[I * 4 + q] = 0.5 * (lo + hi);
+    }
+  }
+}
+
+// minimum s between two boxes (lo[0..2], hi[3..5]); explicitly rounded ops so
+// that every pass of the plan builder sees the same value
+__device__ __forceinline__ double kc_smin(const double* __restrict__ a, const double* __restrict__ b, int dd) {
+  double s = 0.0;
+  for (int q = 0; q < dd; ++q) {
+    const double gap = fmax(0.0, fmax(__dsub_rn(b[q], a[3 + q]), __dsub_rn(a[q], b[3 + q])));
+    s = __dadd_rn(s, __dmul_rn(gap, gap));
+  }
+  return s;
+}
+
+// item (group g, tile t >= 4 g): 0 not kept, 1 FP64, 2 FP32 -- the class of
+// the group's nearest row tile to tile t; *np = its useful pairs (i < j)
+__device__ __forceinline__ int kc_item(int64_t g, int64_t t, const double* __restrict__ cbox,
+                                       const double* __restrict__ tbox, int64_t n, int dd, int64_t* np) {
+  const double* tb = tbox + t * 6;
+  if (kc_smin(cbox + (g * KC_GR / KC_CB) * 6, cbox + (t * 32 / KC_CB) * 6, dd) >= KC_SKIP) return 0;
+  const int64_t r0 = g * KC_GR, r1 = min(n, r0 + KC_GR);
+  double s = 1e300;
+  for (int64_t rt = r0 / 32; rt * 32 < r1; ++rt) s = fmin(s, kc_smin(tbox + rt * 6, tb, dd));
+  if (s >= KC_SKIP) return 0;
+  const int64_t c0 = t * 32, c1 = min(n, c0 + 32);
+  if (r1 <= c0) {
+    *np = (r1 - r0) * (c1 - c0);
+  } else {  // the group's own tiles: pairs i < j only
+    int64_t m = 0;
+    for (int64_t j = c0; j < c1; ++j) m += max((int64_t)0, min(r1, j) - r0);
+    *np = m;
+  }
+  return s >= KC_S64 ? 2 : 1;
+}
+
+// per group: kept items, their split weight and useful pairs per class
+__global__ void __launch_bounds__(256) kc_count_kernel(const double* __restrict__ cbox,
+                                                       const double* __restrict__ tbox, int64_t n, int64_t ntiles,
+                                                       int dd, int* __restrict__ cnt, int64_t* __restrict__ wsum,
+                                                       unsigned long long* __restrict__ pairs) {
+  __shared__ int c_all;
+  __shared__ unsigned long long s64, s32, sw;
+  const int64_t g = blockIdx.x;
+  if (threadIdx.x == 0) {
+    c_all = 0;
+    s64 = s32 = sw = 0ull;
+  }
+  __syncthreads();
+  int ca = 0;
+  unsigned long long q64 = 0ull, q32 = 0ull, qw = 0ull;
+  for (int64_t t = g * KC_GT + threadIdx.x; t < ntiles; t += blockDim.x) {
+    int64_t np = 0;
+    const int c = kc_item(g, t, cbox, tbox, n, dd, &np);
+    if (c == 0) continue;
+    ++ca;
+    if (c == 2) {
+      q32 += (unsigned long long)np;
+      qw += KC_W32;
+    } else {
+      q64 += (unsigned long long)np;
+      qw += KC_W64;
+    }
+  }
+  atomicAdd(&c_all, ca);
+  atomicAdd(&s64, q64);
+  atomicAdd(&s32, q32);
+  atomicAdd(&sw, qw);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    cnt[g] = c_all;
+    wsum[g] = (int64_t)sw;
+    atomicAdd(&pairs[0], s64);
+    atomicAdd(&pairs[1], s32);
+  }
+}
+
+// the kept items of group g in tile order: it[e] = tile | F32 flag,
+// wpre[e] = exclusive prefix of the split weights (from wbase[g])
+__global__ void __launch_bounds__(256) kc_fill_kernel(const double* __restrict__ cbox,
+                                                      const double* __restrict__ tbox, int64_t n, int64_t ntiles,
+                                                      int dd, const int64_t* __restrict__ gstart,
+                                                      const int64_t* __restrict__ wbase, unsigned* __restrict__ it,
+                                                      int64_t* __restrict__ wpre) {
+  __shared__ int wtot[8], wwt[8];
+  __shared__ int64_t base, wb;
+  const int64_t g = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    base = gstart[g];
+    wb = wbase[g];
+  }
+  __syncthreads();
+  for (int64_t t0 = g * KC_GT; t0 < ntiles; t0 += 256) {
+    const int64_t t = t0 + threadIdx.x;
+    int64_t np = 0;
+    const int c = t < ntiles ? kc_item(g, t, cbox, tbox, n, dd, &np) : 0;
+    const int wgt = c == 0 ? 0 : (c == 2 ? KC_W32 : KC_W64);
+    const unsigned m = __ballot_sync(0xffffffffu, c != 0);
+    int wincl = wgt;  // inclusive warp scan of the weights
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, wincl, o);
+      if (lane >= o) wincl += y;
+    }
+    if (lane == 31) {
+      wtot[wid] = __popc(m);
+      wwt[wid] = wincl;
+    }
+    __syncthreads();
+    int64_t off = base, woff = wb;
+    for (int w = 0; w < wid; ++w) {
+      off += wtot[w];
+      woff += wwt[w];
+    }
+    if (c != 0) {
+      const int64_t e = off + __popc(m & ((1u << lane) - 1u));
+      it[e] = (unsigned)t | (c == 2 ? KC_F32 : 0u);
+      wpre[e] = woff + wincl - wgt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < 8; ++w) {
+        base += wtot[w];
+        wb += wwt[w];
+      }
+    __syncthreads();
+  }
+}
+
+// warp w starts at the first item whose weight prefix reaches w TW / Wtot
+__global__ void kc_wsplit_kernel(const int64_t* __restrict__ wpre, int64_t E, int64_t TW, int64_t Wtot,
+                                 int64_t* __restrict__ wst) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > Wtot) return;
+  if (w == Wtot) {
+    wst[w] = E;
+    return;
+  }
+  const int64_t target = (int64_t)((__int128)w * TW / Wtot);
+  int64_t lo = 0, hi = E;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (wpre[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  wst[w] = lo;
+}
+
+__device__ __forceinline__ int64_t kc_owner(const int64_t* __restrict__ wst, int64_t Wtot, int64_t e) {
+  int64_t lo = 0, hi = Wtot - 1;  // last w with wst[w] <= e
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (wst[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+__device__ __forceinline__ int64_t kc_group_of(const int64_t* __restrict__ gstart, int64_t ng, int64_t e) {
+  int64_t lo = 0, hi = ng - 1;  // last g with gstart[g] <= e
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (gstart[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// per group: {first warp, warps} touching it (empty warps in between
+// included: they write zero rows), counts for the slot scan
+__global__ void kc_segs_kernel(const int64_t* __restrict__ gstart, int64_t ng, const int64_t* __restrict__ wst,
+                               int64_t Wtot, int* __restrict__ seg, int* __restrict__ nseg) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  const int64_t f = kc_owner(wst, Wtot, gstart[g]), l = kc_owner(wst, Wtot, gstart[g + 1] - 1);
+  seg[2 * g] = (int)f;
+  seg[2 * g + 1] = (int)(l - f + 1);
+  nseg[g] = (int)(l - f + 1);
+}
+
+// transpose: items per tile (counted, placed, then sorted by item id)
+__global__ void kc_tcount_kernel(const unsigned* __restrict__ it, int64_t E, int* __restrict__ tcnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < E) atomicAdd(&tcnt[it[e] & ~KC_F32], 1);
+}
+__global__ void kc_tplace_kernel(const unsigned* __restrict__ it, int64_t E, const int64_t* __restrict__ tptr,
+                                 int* __restrict__ cur, int* __restrict__ tu) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const unsigned t = it[e] & ~KC_F32;
+  tu[tptr[t] + atomicAdd(&cur[t], 1)] = (int)e;
+}
+__global__ void kc_tsort_kernel(const int64_t* __restrict__ tptr, int64_t ntiles, int* __restrict__ tu) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntiles) return;
+  const int64_t b = tptr[t], e = tptr[t + 1];
+  for (int64_t i = b + 1; i < e; ++i) {
+    const int v = tu[i];
+    int64_t j = i - 1;
+    while (j >= b && tu[j] > v) {
+      tu[j + 1] = tu[j];
+      --j;
+    }
+    tu[j + 1] = v;
+  }
+}
+
+// One warp per item range [wst[w], wst[w+1]) of the (group, tile) items in
+// (group, tile) order: the group's 128 rows in registers (row t of lane l is
+// position 128 g + 32 t + l), the item's 32 columns staged by the warp in its
+// own shared-memory slice (no block barrier), the column sums (lane l =
+// column l, the rotation of kmv_sym_kernel) written to Cb[e], the row sums to
+// the warp's slot of the group when the warp leaves it.
+template <int D>
+__global__ void __launch_bounds__(KMV_NT, 2)
+kmv_cut_kernel(const double* __restrict__ Xc, const int* __restrict__ sidx, const double* __restrict__ v,
+               const double* __restrict__ ctr, int64_t n, int64_t ng, const int64_t* __restrict__ gstart,
+               const unsigned* __restrict__ it, const int64_t* __restrict__ wst, int64_t Wtot, int64_t w0,
+               const int* __restrict__ seg, const int64_t* __restrict__ rbase, double* __restrict__ Rp,
+               double* __restrict__ Cb, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  constexpr int RB = 4;
+  constexpr int CS0 = KmvTraits<D>::CS;
+  constexpr int CS = ((CS0 / 2) % 2 == 0) ? CS0 + 2 : CS0;
+  constexpr int NW = KMV_NT / 32;
+  extern __shared__ double s_tx[];  // 2048-entry exp2 table
+  __shared__ __align__(16) double s_col[NW][32 * CS];
+  __shared__ __align__(16) float4 s_colf[NW][32];
+  for (int t = threadIdx.x; t < 2048; t += KMV_NT) s_tx[t] = g_exp2_2048[t];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t w = w0 + (int64_t)blockIdx.x * NW + wid;
+  if (w >= Wtot) return;
+  const int64_t e0 = wst[w], e1 = wst[w + 1];
+  if (e0 >= e1) {  // empty range: zero rows if a group counts this warp
+    if (e0 < wst[Wtot]) {
+      const int64_t g = kc_group_of(gstart, ng, e0);
+      const int64_t f = seg[2 * g], ns = seg[2 * g + 1];
+      if (w >= f && w < f + ns)
+        for (int t = 0; t < RB; ++t) Rp[(rbase[g] + (w - f)) * KC_GR + 32 * t + lane] = 0.0;
+    }
+    return;
+  }
+  int64_t g = kc_group_of(gstart, ng, e0);
+  double xi[RB][D], vi[RB], acc[RB], cg[D];
+  int64_t ri[RB];
+  auto load_rows = [&]() {
+#pragma unroll
+    for (int q = 0; q < D; ++q) cg[q] = ctr[g * 4 + q];
+#pragma unroll
+    for (int t = 0; t < RB; ++t) {
+      ri[t] = g * KC_GR + 32 * t + lane;
+      const bool ok = ri[t] < n;
+#pragma unroll
+      for (int q = 0; q < D; ++q) xi[t][q] = ok ? Xc[ri[t] * D + q] : 0.0;
+      vi[t] = ok ? v[sidx[ri[t]]] : 0.0;
+      acc[t] = 0.0;
+    }
+  };
+  auto flush_rows = [&]() {
+    double* dst = Rp + (rbase[g] + (w - seg[2 * g])) * KC_GR;
+#pragma unroll
+    for (int t = 0; t < RB; ++t) dst[32 * t + lane] = acc[t];
+  };
+  load_rows();
+  int64_t gend = gstart[g + 1];
+  double* const col = s_col[wid];
+  float4* const colf = s_colf[wid];
+  for (int64_t e = e0; e < e1; ++e) {
+    if (e >= gend) {
+      flush_rows();
+      do {
+        ++g;
+      } while (gstart[g + 1] <= e);
+      gend = gstart[g + 1];
+      load_rows();
+    }
+    const unsigned item = it[e];
+    const int64_t tb = (int64_t)(item & ~KC_F32) * 32;
+    const bool f32 = (item & KC_F32) != 0u;
+    {  // stage the item's columns (lane = column)
+      const int64_t gc = tb + lane;
+      const bool ok = gc < n;
+      const double vj = ok ? v[sidx[gc]] : 0.0;
+      double xj[D];
+#pragma unroll
+      for (int q = 0; q < D; ++q) xj[q] = ok ? Xc[gc * D + q] : 0.0;
+      __syncwarp();
+      if (f32) {
+        float f[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < D; ++q) f[q] = (float)(xj[q] - cg[q]);
+        colf[lane] = make_float4(f[0], f[1], f[2], (float)vj);
+      } else {
+#pragma unroll
+        for (int q = 0; q < D; ++q) col[lane * CS + q] = xj[q];
+        col[lane * CS + D] = vj;
+      }
+      __syncwarp();
+    }
+    if (f32) {
+      float xf[RB][3], vf[RB], a32[RB];
+#pragma unroll
+      for (int t = 0; t < RB; ++t) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) xf[t][q] = q < D ? (float)(xi[t][q < D ? q : 0] - cg[q < D ? q : 0]) : 0.f;
+        vf[t] = (float)vi[t];
+        a32[t] = 0.f;
+      }
+      float ca = 0.f;
+#pragma unroll 4
+      for (int st = 0; st < 32; ++st) {
+        const float4 c4 = colf[(lane + st) & 31];
+#pragma unroll
+        for (int t = 0; t < RB; ++t) {
+          const float dx = xf[t][0] - c4.x;
+          float s2 = dx * dx;
+          if (D > 1) {
+            const float dy = xf[t][1] - c4.y;
+            s2 = fmaf(dy, dy, s2);
+          }
+          if (D > 2) {
+            const float dz = xf[t][2] - c4.z;
+            s2 = fmaf(dz, dz, s2);
+          }
+          const float kv = kc_ex2_neg(s2);
+          a32[t] = fmaf(kv, c4.w, a32[t]);
+          ca = fmaf(kv, vf[t], ca);
+        }
+        ca = __shfl_sync(0xffffffffu, ca, (lane + 1) & 31);
+      }
+      Cb[e * 32 + lane] = (double)ca;
+#pragma unroll
+      for (int t = 0; t < RB; ++t) acc[t] += (double)a32[t];
+    } else {
+      auto body64 = [&](auto masked) {
+        double ca = 0.0;
+#pragma unroll 2
+        for (int st = 0; st < 32; ++st) {
+          const int jl = (lane + st) & 31;
+          double xj[CS];
+#pragma unroll
+          for (int q = 0; q < CS0; q += 2) {
+            const double2 w2 = *reinterpret_cast<const double2*>(&col[jl * CS + q]);
+            xj[q] = w2.x;
+            xj[q + 1] = w2.y;
+          }
+          const double vj = xj[D];
+          const int64_t gj = tb + jl;
+#pragma unroll
+          for (int t = 0; t < RB; ++t) {
+            double dd = xi[t][0] - xj[0];
+            double s2 = dd * dd;
+#pragma unroll
+            for (int q = 1; q < D; ++q) {
+              dd = xi[t][q] - xj[q];
+              s2 = fma(dd, dd, s2);
+            }
+            double kv = exp2_neg2048(s2, s_tx);
+            if (decltype(masked)::value && gj <= ri[t]) kv = 0.0;
+            acc[t] = fma(kv, vj, acc[t]);
+            ca = fma(kv, vi[t], ca);
+          }
+          ca = __shfl_sync(0xffffffffu, ca, (lane + 1) & 31);
+        }
+        Cb[e * 32 + lane] = ca;
+      };
+      if (tb < (g + 1) * KC_GR) body64(std::true_type{});
+      else body64(std::false_type{});
+    }
+  }
+  flush_rows();
+}
+
+// q at spatial position i = the row slots of its group (warp order) + the
+// column partials of the items holding its tile (item order); written to
+// y[sidx[i]].  FINAL as in kmv_sym_reduce_kernel.  This rank: warps
+// [w_lo, w_hi), items [wst[w_lo], wst[w_hi]).
+template <bool FINAL>
+__global__ void __launch_bounds__(SRT) kmv_cut_reduce_kernel(
+    const double* __restrict__ Rp, const double* __restrict__ Cb, const int* __restrict__ seg,
+    const int64_t* __restrict__ rbase, const int* __restrict__ sidx, const int64_t* __restrict__ tptr,
+    const int* __restrict__ tu, const int64_t* __restrict__ wst, int64_t n, int64_t Wtot, int64_t w_lo,
+    int64_t w_hi, const double* __restrict__ v, double mu, double* __restrict__ y, const double* skip, double* dout,
+    double* dws, unsigned* dcnt) {
+  __shared__ double sh[SRT / 32];
+  if (skip != nullptr && *skip != 0.0) return;
+  const bool all = w_lo == 0 && w_hi == Wtot;
+  const int64_t e_lo = wst[w_lo], e_hi = wst[w_hi];
+  const int sub = threadIdx.x % SRL;
+  double dsum = 0.0;
+  const int64_t rows_per_pass = (int64_t)gridDim.x * (SRT / SRL);
+  for (int64_t i0 = (int64_t)blockIdx.x * (SRT / SRL); i0 < n; i0 += rows_per_pass) {
+    const int64_t i = i0 + threadIdx.x / SRL;
+    double s = 0.0;
+    if (i < n) {
+      const int64_t gi = i / KC_GR, li = i - gi * KC_GR;
+      const int64_t f = seg[2 * gi], ns = seg[2 * gi + 1], rb = rbase[gi];
+      for (int64_t t = sub; t < ns; t += SRL)
+        if (all || (f + t >= w_lo && f + t < w_hi)) s += Rp[(rb + t) * KC_GR + li];
+      const int64_t ti = i / 32, tl = i - ti * 32;
+      const int64_t t1 = tptr[ti + 1];
+      for (int64_t q = tptr[ti] + sub; q < t1; q += SRL) {
+        const int64_t e = tu[q];
+        if (all || (e >= e_lo && e < e_hi)) s += Cb[e * 32 + tl];
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < SRL; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (sub == 0 && i < n) {
+      const int64_t o = sidx[i];
+      if (FINAL) {
+        const double yi = fma(1.0 + mu, v[o], s);
+        y[o] = yi;
+        dsum = fma(v[o], yi, dsum);
+      } else {
+        y[o] = s;
+      }
+    }
+  }
+  if (!FINAL || dout == nullptr) return;
+  dsum = block_sum<SRT>(dsum, sh);
+  finish_sum(dsum, dws, dcnt, dout);
+}
+
 __global__ void kmv_reduce_kernel(const double* __restrict__ partial, int nchunks, Seg2 rows,
                                   const double* __restrict__ v, double mu, bool y_phys,
                                   double* __restrict__ y, const double* skip) {
@@ -581,6 +1176,12 @@ double kmv_flops(const KmvPlan& p, int64_t n, int64_t nrows, int d, int kind) {
   //   Matern: sqrt 1 + scale 1 + 2x16-table exp2 15 + (1 + t) 1 + product 1;
   //   row FMA 2 (+ column FMA 2 in the symmetric kernel)
   const double dist = 3.0 * d - 1.0;
+  if (p.cut) {
+    // FP64-equivalent: an FP32-body pair costs one MUFU.EX2 (16 per SM per
+    // clock) against 2d + 9 FP64-pipe instructions (64 lanes per SM per clock)
+    // of an FP64-body pair
+    return (dist + 16.0) * (p.cut_pairs64 + p.cut_pairs32 * 4.0 / (2.0 * d + 9.0));
+  }
   if (p.sym) {
     const double e = kind == 1 ? 19.0 : (d <= 4 ? 12.0 : 14.0);
     return (double)n * (double)(n - 1) / 2.0 * (dist + e + 4.0);
@@ -593,6 +1194,7 @@ double kmv_fp64_inst(const KmvPlan& p, int64_t n, int64_t nrows, int d, int kind
   // FP64-pipe thread instructions per useful pair: distance 2d, exp2 7 (2048
   // table) / 8 (256) / 11 + sqrt (Matern, sqrt counted as 1), row FMA 1, column FMA 1
   const double dist = 2.0 * d;
+  if (p.cut) return p.cut_pairs64 * (dist + 9.0);
   if (p.sym) {
     const double e = kind == 1 ? 14.0 : (d <= 4 ? 7.0 : 8.0);
     return (double)n * (double)(n - 1) / 2.0 * (dist + e + 2.0);
@@ -608,6 +1210,305 @@ afn_status kmv_prescale(const double* X, int64_t n, int d, Kern kn, double* Xs, 
   prescale_kernel<<<(unsigned)((total + nt - 1) / nt), nt, 0, st>>>(X, n, d, f, Xs);
   AFN_LAUNCH_CHECK("prescale_kernel");
   return AFN_OK;
+}
+
+
+// ---------------------------------------------------------------- cutoff plan
+namespace {
+int g_kmv_mode = 0;
+
+template <int D>
+void cut_launch(const KmvPlan& p, cudaStream_t st, const double* ws, const double* v, int64_t n) {
+  const int64_t w0 = p.sym_grid * 8 * (int64_t)p.sym_rank;
+  kmv_cut_kernel<D><<<(unsigned)p.sym_grid, KMV_NT, sizeof(double) * 2048, st>>>(
+      ws + p.o_xc, reinterpret_cast<const int*>(ws + p.o_sidx), v, ws + p.o_ctr, n, p.sym_nrb,
+      reinterpret_cast<const int64_t*>(ws + p.o_ustart), reinterpret_cast<const unsigned*>(ws + p.o_ut),
+      reinterpret_cast<const int64_t*>(ws + p.o_wst), p.sym_gt, w0, reinterpret_cast<const int*>(ws + p.o_seg),
+      reinterpret_cast<const int64_t*>(ws + p.o_rbase), const_cast<double*>(ws) + p.o_rp,
+      const_cast<double*>(ws) + p.o_cb, get_skip());
+}
+
+afn_status cut_partials(const KmvPlan& p, int64_t n, int d, const double* v, double* ws, cudaStream_t st) {
+  switch (d) {
+    case 1: cut_launch<1>(p, st, ws, v, n); break;
+    case 2: cut_launch<2>(p, st, ws, v, n); break;
+    case 3: cut_launch<3>(p, st, ws, v, n); break;
+    default: set_error("kernel_matvec: cutoff plan for d=%d unsupported (1..3)", d); return AFN_ERR_ARG;
+  }
+  AFN_LAUNCH_CHECK("kmv_cut_kernel");
+  return AFN_OK;
+}
+
+// rank partial (final_ = false: y = q at this rank's items and warps) or the
+// one-rank product (+ (1 + mu) v, v . y)
+afn_status cut_reduce(const KmvPlan& p, int64_t n, const double* v, double mu, double* y, const double* ws,
+                      bool final_, cudaStream_t st, double* dout, double* dws, unsigned* dcnt) {
+  const int64_t rows_per_block = SRT / SRL;
+  const int64_t nbk = std::min<int64_t>((n + rows_per_block - 1) / rows_per_block,
+                                        final_ ? dot_ws() : 4 * (int64_t)num_sms());
+  const int64_t wr = p.sym_grid * 8, w_lo = wr * p.sym_rank, w_hi = final_ ? p.sym_gt : w_lo + wr;
+  const int* seg = reinterpret_cast<const int*>(ws + p.o_seg);
+  const int64_t* rbase = reinterpret_cast<const int64_t*>(ws + p.o_rbase);
+  const int* sidx = reinterpret_cast<const int*>(ws + p.o_sidx);
+  const int64_t* tptr = reinterpret_cast<const int64_t*>(ws + p.o_tptr);
+  const int* tu = reinterpret_cast<const int*>(ws + p.o_tu);
+  const int64_t* wst = reinterpret_cast<const int64_t*>(ws + p.o_wst);
+  if (final_)
+    kmv_cut_reduce_kernel<true><<<(unsigned)nbk, SRT, 0, st>>>(ws + p.o_rp, ws + p.o_cb, seg, rbase, sidx, tptr, tu,
+                                                               wst, n, p.sym_gt, 0, p.sym_gt, v, mu, y, get_skip(),
+                                                               dout, dws, dcnt);
+  else
+    kmv_cut_reduce_kernel<false><<<(unsigned)nbk, SRT, 0, st>>>(ws + p.o_rp, ws + p.o_cb, seg, rbase, sidx, tptr,
+                                                                tu, wst, n, p.sym_gt, w_lo, w_hi, v, 0.0, y,
+                                                                get_skip(), nullptr, nullptr, nullptr);
+  AFN_LAUNCH_CHECK("kmv_cut_reduce_kernel");
+  return AFN_OK;
+}
+
+// stream-ordered temporaries of the plan builder
+struct KcTmp {
+  cudaStream_t st;
+  std::vector<void*> ps;
+  explicit KcTmp(cudaStream_t s) : st(s) {}
+  ~KcTmp() {
+    for (void* q : ps) dfree(q, st);
+  }
+  template <class T>
+  afn_status get(T** out, size_t count) {
+    void* q = nullptr;
+    afn_status s = dalloc(&q, sizeof(T) * (count > 0 ? count : 1), st);
+    if (s != AFN_OK) return s;
+    ps.push_back(q);
+    *out = static_cast<T*>(q);
+    return AFN_OK;
+  }
+};
+
+// Builds the cutoff plan; *used = false (nothing allocated through get) when
+// it does not pay (mode 0: it would keep more than half of the pairs).
+afn_status cut_plan_make(const double* Xs, int64_t n, int d, int R, int rank, cudaStream_t st, const WsGet& get,
+                         KmvPlan* out, double** wsp, bool* used) {
+  *used = false;
+  const int nsm = num_sms();
+  KcTmp tmp(st);
+  // ---- spatial order: Morton order of a grid of ~2 points per cell, points
+  // of a cell by ascending index
+  const int nbb = nsm;
+  double *bws, *hbox;
+  TRY_STATUS(tmp.get(&bws, (size_t)6 * nbb));
+  kc_bbox_kernel<<<nbb, 256, 0, st>>>(Xs, n, d, bws);
+  AFN_LAUNCH_CHECK("kc_bbox_kernel");
+  std::vector<double> hb((size_t)6 * nbb);
+  AFN_CUDA(cudaMemcpyAsync(hb.data(), bws, sizeof(double) * hb.size(), cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaStreamSynchronize(st));
+  (void)hbox;
+  KcGrid gd{};
+  gd.dd = d;
+  {
+    const int cap_bits = d == 3 ? 8 : (d == 2 ? 12 : 24);
+    const double target = std::max(1.0, (double)n / 2.0);
+    int g = std::max(1, (int)std::ceil(std::pow(target, 1.0 / d)));
+    int bits = 0;
+    while ((1 << bits) < g) ++bits;
+    if (bits > cap_bits) {
+      bits = cap_bits;
+      g = 1 << bits;
+    }
+    gd.bits = bits;
+    gd.g = g;
+    for (int q = 0; q < 3; ++q) {
+      double lo = 1e300, hi = -1e300;
+      for (int b = 0; b < nbb; ++b) {
+        lo = std::min(lo, hb[(size_t)b * 6 + q]);
+        hi = std::max(hi, hb[(size_t)b * 6 + 3 + q]);
+      }
+      gd.lo[q] = q < d ? lo : 0.0;
+      gd.inv[q] = (q < d && hi > lo) ? (double)g / (hi - lo) : 0.0;
+    }
+  }
+  const int64_t ncell = (int64_t)1 << (gd.bits * d);
+  unsigned* key;
+  int *cnt, *sidx;
+  int64_t* off;
+  TRY_STATUS(tmp.get(&key, (size_t)n));
+  TRY_STATUS(tmp.get(&cnt, (size_t)2 * ncell));
+  TRY_STATUS(tmp.get(&off, (size_t)ncell + 1));
+  TRY_STATUS(tmp.get(&sidx, (size_t)n));
+  AFN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * ncell, st));
+  const unsigned nbn = (unsigned)((n + 255) / 256);
+  kc_key_kernel<<<nbn, 256, 0, st>>>(Xs, n, d, gd, key, cnt);
+  AFN_LAUNCH_CHECK("kc_key_kernel");
+  kc_scan_kernel<<<1, 1024, 0, st>>>(cnt, ncell, off);
+  AFN_LAUNCH_CHECK("kc_scan_kernel");
+  kc_scatter_kernel<<<nbn, 256, 0, st>>>(key, n, off, cnt + ncell, sidx);
+  AFN_LAUNCH_CHECK("kc_scatter_kernel");
+  kc_cell_sort_kernel<<<(unsigned)((ncell + 255) / 256), 256, 0, st>>>(off, ncell, sidx);
+  AFN_LAUNCH_CHECK("kc_cell_sort_kernel");
+  double *Xc, *tbox, *cbox, *ctr;
+  const int64_t ntiles = (n + 31) / 32;
+  const int64_t ng = (n + KC_GR - 1) / KC_GR;
+  const int64_t ncb = (n + KC_CB - 1) / KC_CB;
+  TRY_STATUS(tmp.get(&Xc, (size_t)n * d));
+  TRY_STATUS(tmp.get(&tbox, (size_t)6 * ntiles));
+  TRY_STATUS(tmp.get(&cbox, (size_t)6 * ncb));
+  TRY_STATUS(tmp.get(&ctr, (size_t)4 * ng));
+  kc_gather_kernel<<<(unsigned)((n * d + 255) / 256), 256, 0, st>>>(Xs, n, d, sidx, Xc);
+  AFN_LAUNCH_CHECK("kc_gather_kernel");
+  kc_tile_box_kernel<<<(unsigned)((ntiles * 32 + 255) / 256), 256, 0, st>>>(Xc, n, d, ntiles, tbox);
+  AFN_LAUNCH_CHECK("kc_tile_box_kernel");
+  kc_block_box_kernel<<<(unsigned)((ncb * 32 + 255) / 256), 256, 0, st>>>(tbox, ntiles, ncb, KC_CB / 32, cbox,
+                                                                          nullptr);
+  AFN_LAUNCH_CHECK("kc_block_box_kernel");
+  double* gbox;
+  TRY_STATUS(tmp.get(&gbox, (size_t)6 * ng));
+  kc_block_box_kernel<<<(unsigned)((ng * 32 + 255) / 256), 256, 0, st>>>(tbox, ntiles, ng, KC_GT, gbox, ctr);
+  AFN_LAUNCH_CHECK("kc_block_box_kernel");
+  // ---- kept items per group
+  int* gcnt;
+  int64_t* gw;
+  unsigned long long* pairs;
+  TRY_STATUS(tmp.get(&gcnt, (size_t)ng));
+  TRY_STATUS(tmp.get(&gw, (size_t)ng));
+  TRY_STATUS(tmp.get(&pairs, 2));
+  AFN_CUDA(cudaMemsetAsync(pairs, 0, 2 * sizeof(unsigned long long), st));
+  kc_count_kernel<<<(unsigned)ng, 256, 0, st>>>(cbox, tbox, n, ntiles, d, gcnt, gw, pairs);
+  AFN_LAUNCH_CHECK("kc_count_kernel");
+  std::vector<int> hc((size_t)ng);
+  std::vector<int64_t> hw((size_t)ng);
+  unsigned long long hp[2];
+  AFN_CUDA(cudaMemcpyAsync(hc.data(), gcnt, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaMemcpyAsync(hw.data(), gw, sizeof(int64_t) * ng, cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaMemcpyAsync(hp, pairs, sizeof(hp), cudaMemcpyDeviceToHost, st));
+  AFN_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> gstart((size_t)ng + 1, 0), wbase((size_t)ng + 1, 0);
+  for (int64_t g = 0; g < ng; ++g) {
+    gstart[g + 1] = gstart[g] + hc[g];
+    wbase[g + 1] = wbase[g] + hw[g];
+  }
+  const int64_t E = gstart[ng], TW = wbase[ng];
+  const double all_pairs = (double)n * (double)(n - 1) / 2.0;
+  if (g_kmv_mode == 0 && (double)(hp[0] + hp[1]) > 0.5 * all_pairs) return AFN_OK;
+  if (E >= ((int64_t)1 << 31) || E < 1) return AFN_OK;
+
+  KmvPlan p;
+  p.sym = true;
+  p.cut = true;
+  p.sym_rbw = KC_GR;
+  p.sym_nrb = ng;
+  p.sym_nt = ntiles;
+  p.sym_units = E;
+  p.sym_R = R;
+  p.sym_rank = rank;
+  p.cut_u64 = E;
+  p.cut_ntiles = ntiles;
+  p.cut_pairs64 = (double)hp[0];
+  p.cut_pairs32 = (double)hp[1];
+  {
+    // warps per rank: two waves of 2 CTAs x 8 warps per SM, at least ~4 items
+    // per warp (the split is by weight, FP64 : FP32 items = 16 : 5)
+    const int64_t want = (int64_t)nsm * 2 * 8 * 2;
+    int64_t wr = std::max<int64_t>(8, std::min<int64_t>(want, E / (4 * (int64_t)R)));
+    wr = (wr + 7) / 8 * 8;
+    p.sym_grid = wr / 8;
+    p.sym_gt = wr * R;
+  }
+  const int64_t Wtot = p.sym_gt;
+  auto dbl = [](int64_t bytes) { return (bytes + 7) / 8; };
+  int64_t o = 0;
+  p.sym_tab_dbl = 0;
+  p.o_rp = o;
+  o += (Wtot + ng) * KC_GR;
+  p.o_cb = o;
+  o += E * 32;
+  p.o_xc = o;
+  o += n * d;
+  p.o_ctr = o;
+  o += 4 * ng;
+  p.o_sidx = o;
+  o += dbl(sizeof(int) * n);
+  p.o_ut = o;
+  o += dbl(sizeof(unsigned) * E);
+  p.o_ustart = o;
+  o += ng + 1;
+  p.o_wst = o;
+  o += Wtot + 1;
+  p.o_seg = o;
+  o += dbl(sizeof(int) * 2 * ng);
+  p.o_rbase = o;
+  o += ng + 1;
+  p.o_tptr = o;
+  o += ntiles + 1;
+  p.o_tu = o;
+  o += dbl(sizeof(int) * E);
+  p.ws = o;
+  double* ws = nullptr;
+  TRY_STATUS(get(&ws, (size_t)p.ws));
+  *used = true;
+  *wsp = ws;
+  TRY_STATUS(ensure_exp2_tables());
+  {  // the 2048-entry table is dynamic shared memory on top of the static ~20 KB
+    const int dyn = (int)sizeof(double) * 2048;
+    if (d == 1) AFN_CUDA(cudaFuncSetAttribute(kmv_cut_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    if (d == 2) AFN_CUDA(cudaFuncSetAttribute(kmv_cut_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    if (d == 3) AFN_CUDA(cudaFuncSetAttribute(kmv_cut_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+  }
+  int64_t* dgs = reinterpret_cast<int64_t*>(ws + p.o_ustart);
+  int64_t* dwb;
+  TRY_STATUS(tmp.get(&dwb, (size_t)ng + 1));
+  AFN_CUDA(cudaMemcpyAsync(dgs, gstart.data(), sizeof(int64_t) * gstart.size(), cudaMemcpyHostToDevice, st));
+  AFN_CUDA(cudaMemcpyAsync(dwb, wbase.data(), sizeof(int64_t) * wbase.size(), cudaMemcpyHostToDevice, st));
+  AFN_CUDA(cudaMemcpyAsync(ws + p.o_xc, Xc, sizeof(double) * n * d, cudaMemcpyDeviceToDevice, st));
+  AFN_CUDA(cudaMemcpyAsync(ws + p.o_ctr, ctr, sizeof(double) * 4 * ng, cudaMemcpyDeviceToDevice, st));
+  AFN_CUDA(cudaMemcpyAsync(ws + p.o_sidx, sidx, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+  unsigned* dit = reinterpret_cast<unsigned*>(ws + p.o_ut);
+  int64_t* wpre;
+  TRY_STATUS(tmp.get(&wpre, (size_t)E));
+  kc_fill_kernel<<<(unsigned)ng, 256, 0, st>>>(cbox, tbox, n, ntiles, d, dgs, dwb, dit, wpre);
+  AFN_LAUNCH_CHECK("kc_fill_kernel");
+  int64_t* wst = reinterpret_cast<int64_t*>(ws + p.o_wst);
+  kc_wsplit_kernel<<<(unsigned)((Wtot + 1 + 255) / 256), 256, 0, st>>>(wpre, E, TW, Wtot, wst);
+  AFN_LAUNCH_CHECK("kc_wsplit_kernel");
+  int* nseg;
+  TRY_STATUS(tmp.get(&nseg, (size_t)ng));
+  kc_segs_kernel<<<(unsigned)((ng + 255) / 256), 256, 0, st>>>(dgs, ng, wst, Wtot,
+                                                               reinterpret_cast<int*>(ws + p.o_seg), nseg);
+  AFN_LAUNCH_CHECK("kc_segs_kernel");
+  kc_scan_kernel<<<1, 1024, 0, st>>>(nseg, ng, reinterpret_cast<int64_t*>(ws + p.o_rbase));
+  AFN_LAUNCH_CHECK("kc_scan_kernel");
+  int *tcnt, *tcur;
+  TRY_STATUS(tmp.get(&tcnt, (size_t)2 * ntiles));
+  tcur = tcnt + ntiles;
+  AFN_CUDA(cudaMemsetAsync(tcnt, 0, sizeof(int) * 2 * ntiles, st));
+  const unsigned nbe = (unsigned)((E + 255) / 256);
+  kc_tcount_kernel<<<nbe, 256, 0, st>>>(dit, E, tcnt);
+  AFN_LAUNCH_CHECK("kc_tcount_kernel");
+  int64_t* tptr = reinterpret_cast<int64_t*>(ws + p.o_tptr);
+  kc_scan_kernel<<<1, 1024, 0, st>>>(tcnt, ntiles, tptr);
+  AFN_LAUNCH_CHECK("kc_scan_kernel");
+  int* tu = reinterpret_cast<int*>(ws + p.o_tu);
+  kc_tplace_kernel<<<nbe, 256, 0, st>>>(dit, E, tptr, tcur, tu);
+  AFN_LAUNCH_CHECK("kc_tplace_kernel");
+  kc_tsort_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(tptr, ntiles, tu);
+  AFN_LAUNCH_CHECK("kc_tsort_kernel");
+  AFN_CUDA(cudaStreamSynchronize(st));  // (pageable sources; temporaries freed on return)
+  *out = p;
+  return AFN_OK;
+}
+}  // namespace
+
+void kmv_set_mode(int mode) { g_kmv_mode = mode; }
+int kmv_get_mode() { return g_kmv_mode; }
+
+afn_status kmv_plan_make(const double* Xs, int64_t n, int64_t nrows, int d, int kind, bool sym_ok, int R, int rank,
+                         cudaStream_t st, const WsGet& get, KmvPlan* out, double** ws) {
+  if (sym_ok && kind == 0 && d <= 3 && n >= 4096 && g_kmv_mode != 1) {
+    bool used = false;
+    TRY_STATUS(cut_plan_make(Xs, n, d, R, rank, st, get, out, ws, &used));
+    if (used) return AFN_OK;
+  }
+  *out = kmv_plan(n, nrows, d, num_sms(), sym_ok, R, rank);
+  TRY_STATUS(get(ws, (size_t)std::max<int64_t>(1, out->ws)));
+  return kmv_plan_init(*out, *ws, st);
 }
 
 namespace {
@@ -639,13 +1540,17 @@ afn_status kmv_sym_rank_partial(const double* Xs, int64_t n, int d, int kind, co
     set_error("kmv_sym_rank_partial: plan is not symmetric");
     return AFN_ERR_STATE;
   }
+  const int64_t glo = p.sym_grid * (int64_t)p.sym_rank;
+  if (p.cut) {
+    TRY_STATUS(cut_partials(p, n, d, v, ws, st));
+    return cut_reduce(p, n, v, 0.0, qout, ws, false, st, nullptr, nullptr, nullptr);
+  }
   TRY_STATUS(sym_partials(Xs, n, d, kind, v, p, ws, st));
   const int* segtab = reinterpret_cast<const int*>(ws);
   const double* Rp = ws + p.sym_tab_dbl;
   const double* Cb = Rp + (p.sym_gt + p.sym_nrb) * p.sym_rbw;
   const int64_t rows_per_block = SRT / SRL;
   const int64_t nbk = std::min<int64_t>((n + rows_per_block - 1) / rows_per_block, 4 * (int64_t)num_sms());
-  const int64_t glo = p.sym_grid * (int64_t)p.sym_rank;
   kmv_sym_reduce_kernel<false><<<(unsigned)nbk, SRT, 0, st>>>(Rp, Cb, segtab, n, p.sym_rbw, p.sym_nt, p.sym_units,
                                                               p.sym_gt, glo, glo + p.sym_grid, v, 0.0, qout,
                                                               get_skip(), nullptr, nullptr, nullptr);
@@ -670,6 +1575,10 @@ afn_status kmv_launch(const double* Xs, int64_t n, int d, int kind, const double
     if (p.sym_R != 1 || !(rows.na + rows.nb == n && rows.a0 == 0 && (rows.nb == 0 || rows.b0 == rows.na))) {
       set_error("kernel_matvec: the one-rank symmetric plan needs all rows");
       return AFN_ERR_ARG;
+    }
+    if (p.cut) {
+      TRY_STATUS(cut_partials(p, n, d, v, partial, st));
+      return cut_reduce(p, n, v, mu, y, partial, true, st, dout, dws, dcnt);
     }
     TRY_STATUS(sym_partials(Xs, n, d, kind, v, p, partial, st));
     const int* segtab = reinterpret_cast<const int*>(partial);

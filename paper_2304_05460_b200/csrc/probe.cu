@@ -97,3 +97,47 @@ afn_status probe_dmma(int64_t iters, double* tflops, cudaStream_t st) {
   return AFN_OK;
 }
 }  // namespace afn
+
+// MUFU.EX2 (ex2.approx.ftz.f32) throughput probe: the bound of the cutoff
+// matvec's FP32 body (one EX2 per pair, kmv.cu)
+namespace afn {
+namespace {
+__global__ void __launch_bounds__(256) ex2_probe_kernel(int64_t iters, float seed, float* out) {
+  float a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = seed + 1e-3f * (threadIdx.x + u);
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[u]));
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) s += a[u];
+  if (s == 12345.678f) out[0] = s;
+}
+}  // namespace
+
+afn_status probe_ex2(int64_t iters, double* gops, cudaStream_t st) {
+  const int blocks = num_sms() * 8;
+  float* out = nullptr;
+  afn_status s = dalloc((void**)&out, sizeof(float), st);
+  if (s != AFN_OK) return s;
+  cudaEvent_t e0, e1;
+  AFN_CUDA(cudaEventCreate(&e0));
+  AFN_CUDA(cudaEventCreate(&e1));
+  ex2_probe_kernel<<<blocks, 256, 0, st>>>(iters / 8, -0.5f, out);
+  AFN_LAUNCH_CHECK("ex2_probe_kernel");
+  AFN_CUDA(cudaEventRecord(e0, st));
+  ex2_probe_kernel<<<blocks, 256, 0, st>>>(iters, -0.5f, out);
+  AFN_LAUNCH_CHECK("ex2_probe_kernel");
+  AFN_CUDA(cudaEventRecord(e1, st));
+  AFN_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  AFN_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  dfree(out, st);
+  *gops = 8.0 * (double)iters * (double)blocks * 256.0 / (ms * 1e-3) / 1e9;
+  return AFN_OK;
+}
+}  // namespace afn

@@ -49,10 +49,11 @@ def test_every_declared_symbol_is_exported(lib):
 
 def test_abi_version_and_struct_layout(lib):
     import ctypes as C
-    assert lib.abi_version() == 5
+    assert lib.abi_version() == 6
     # afn_params: 2 doubles, int64, 4 int32, int64, uint64, 4 int32 = 72 bytes
     assert C.sizeof(lib.Params) == 72
-    assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4 + 4 * 2
+    assert C.sizeof(lib.Info) == 8 * 4 + 4 * 4 + 8 * 9 + 4 * 2 + 8 * 4 + 4 * 2 + 4 * 2 + 8 * 4
+    # (kmv_plan, kmv_reserved; kmv_units64/32, kmv_pairs64/32)
     assert C.sizeof(lib.Report) == 4 * 4 + 8 * 6 + 8
 
 
