@@ -397,17 +397,33 @@ def main():
     if r_kmv:
         # executed FP64-pipe instructions per useful pair / flops per pair
         # (kmv.cu kmv_fp64_inst / kmv_flops; Gaussian, symmetric, d <= 4):
-        # (2d + 9) / (3d + 15)
+        # (2d + 9) / (3d + 15).  Cutoff plan: the work is
+        # FP64-equivalent -- an FP32-body pair (one MUFU.EX2 at 16 / SM / clk)
+        # is credited the (3d + 15) * 4 / (2d + 9) flops whose FP64 pipe time
+        # it takes -- so `frac` and `fp64_pipe_frac` are fractions of the
+        # product's issue-bound lower time.
         inst_per_flop = (2 * d + 9) / (3 * d + 15)
         r_kmv["fp64_pipe_frac"] = r_kmv["achieved"] * 1e12 * inst_per_flop / FP64_PIPE_INST_PER_S
         kmv = kt["kmv_kernel"]
-        r_kmv["gpairs_per_s"] = float(n) * n * kmv["count"] / (kmv["ms"] * 1e-3) / 1e9 / max(1, world)
+        per_s = kmv["count"] / (kmv["ms"] * 1e-3) / max(1, world)  # products per second per rank
+        p64, p32 = float(inf0["kmv_pairs64"]), float(inf0["kmv_pairs32"])
+        r_kmv["plan"] = {0: "row-wise", 1: "dense symmetric", 2: "cutoff"}.get(inf0["kmv_plan"], "?")
+        r_kmv["pairs_fp64"], r_kmv["pairs_fp32"] = p64, p32
+        r_kmv["pairs_fraction"] = (p64 + p32) / (n * (n - 1) / 2.0)
+        if inf0["kmv_plan"] == 2:
+            r_kmv["peak_source"] = ("FP64 from the guide's unit counts (148 SM x 64 FP64 lanes x 2 x 1.965 GHz); "
+                                    "FP32-body pairs credited at the MUFU.EX2 rate (afn_probe_ex2)")
+        # unordered pairs evaluated x 2 (ordered) per second, and n^2 per
+        # product per second (what the dense product would have to reach)
+        r_kmv["gpairs_per_s"] = 2.0 * (p64 + p32) * per_s / 1e9
+        r_kmv["gpairs_per_s_dense_equiv"] = float(n) * n * per_s / 1e9
     r_apply = roof("apply")
     kernel_ms = {k: round(v["ms"] / args.steps, 3) for k, v in kt.items() if v["count"] > 0}
     try:
         probe = afn.probe_dfma()
+        probe_ex2 = afn.probe_ex2()
     except Exception:
-        probe = None
+        probe, probe_ex2 = None, None
 
     # ---- C2 sweep (BASELINE.json configs[1]) as an extra key
     sweep = None
@@ -468,7 +484,7 @@ def main():
                 "kmv_gpairs_per_s": r_kmv["gpairs_per_s"] if r_kmv else None,
                 "gpu_launches": launches,
                 "roofline": roofline, "roofline_kmv": r_kmv, "roofline_apply": r_apply,
-                "fp64_probe_tflops": probe, "kernel_ms_per_step": kernel_ms,
+                "fp64_probe_tflops": probe, "ex2_probe_gops": probe_ex2, "kernel_ms_per_step": kernel_ms,
                 "clocks": sampler.summary(), "c2_sweep": sweep,
                 "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)

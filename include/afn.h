@@ -119,7 +119,7 @@ typedef struct {
   int64_t row_a0, row_na, row_b0, row_nb; /* rows of the permuted order it owns   */
   int32_t kernel, method;       /* kernel, preconditioner built (AFN_METHOD_AFN,   */
                                 /* _NYSTROM or _FSAI)                              */
-  /* the handle's kernel-matvec plan (afn_set_matvec_mode):      */
+  /* the handle's kernel-matvec plan (afn_set_cutoff_mode):      */
   /* 0 row-wise, 1 dense symmetric, 2 cutoff; work units of the FP64 and FP32   */
   /* bodies and the unordered pairs they evaluate per product (one rank's plan  */
   /* covers all ranks' units)                                                    */
@@ -175,10 +175,14 @@ afn_status afn_fps(const double* X, int64_t n, int32_t d, int64_t k, int64_t see
 /* row-major, lower triangular), W: N x k row-major, all device, stream-      */
 /* ordered.  method AFN_WPROD_DMMA: FP64 tensor cores (DMMA); AFN_WPROD_INT8: */
 /* exact INT8 slicing on the tcgen05 tensor cores (8 slices per operand, 36   */
-/* INT8 products, FP64-GEMM-level error; k < 65536).  The AFN build uses      */
-/* AFN_WPROD_INT8 for k >= 512.                                              */
+/* INT8 products, FP64-GEMM-level error; k < 65536); AFN_WPROD_CUT (Gaussian, */
+/* d <= 3): the terms with K21 entries < 2^-128 dropped (wcut.cu, DESIGN.md  */
+/* 6.3).  The AFN build uses the cutoff product when it keeps at most half   */
+/* of the landmarks per tile (afn_set_cutoff_mode), else AFN_WPROD_INT8 for  */
+/* k >= 512.                                                                 */
 #define AFN_WPROD_DMMA 0
 #define AFN_WPROD_INT8 1
+#define AFN_WPROD_CUT 2
 afn_status afn_w_product(const double* X1, int64_t k, const double* Xr, int64_t N, int32_t d, int32_t kernel,
                          double l, const double* Linv, int32_t method, double* W, void* stream);
 
@@ -319,18 +323,20 @@ afn_status afn_probe_dmma(int64_t iters, double* tflops /*host*/, void* stream);
 /* the bound of the cutoff matvec's FP32 body (one EX2 per pair).  [sync]    */
 afn_status afn_probe_ex2(int64_t iters, double* gops /*host*/, void* stream);
 
-/* Kernel-matvec plan for the products planned after the call (process-wide; */
-/* DESIGN.md 6.2).  Gaussian kernel, d <= 3, full product:                   */
-/*   0 (default) the cutoff plan -- points in a spatial order, (row block,   */
-/*     column tile) units whose boxes are farther apart than s = 128         */
-/*     (log2 units: every entry < 2^-128) skipped, units farther than s = 48 */
-/*     (entries < 2^-48) in FP32 -- when it keeps at most half of the pairs, */
-/*     else the dense symmetric plan;                                        */
-/*   1 always the dense symmetric plan (every pair in FP64);                 */
-/*   2 the cutoff plan whenever it applies.                                  */
-/* Other kernels / d > 3 / row ranges: the dense plans.  AFN_ERR_ARG for     */
-/* any other mode.                                                           */
-afn_status afn_set_matvec_mode(int32_t mode);
+/* Use of the Gaussian kernel's decay for the handles  */
+/* built and products planned after the call (process-wide).  Gaussian       */
+/* kernel, d <= 3:                                                           */
+/*   kernel matvec (full product): the cutoff plan -- points in a spatial    */
+/*     order, (128-row group, 32-column tile) items whose boxes are at least */
+/*     s = 128 apart (s = ||x - y||^2 log2(e) / l^2: every entry < 2^-128)   */
+/*     skipped, items at least s = 48 apart (entries < 2^-48) in FP32;       */
+/*   W = K21 L^{-T} in afn_build: terms with K21 entries < 2^-128 dropped,  */
+/*     per 64-row tile of a spatial order a dense product over the kept     */
+/*     landmarks.                                                            */
+/* mode 0 (default): each when it keeps at most half of the work, else the  */
+/* dense path; 1: never; 2: whenever it applies.  Other kernels / d > 3 /    */
+/* row ranges: the dense paths.  AFN_ERR_ARG for any other mode.             */
+afn_status afn_set_cutoff_mode(int32_t mode);
 
 /* Per-kernel CUDA-event timers (off by default).  When enabled the library
  * records an event pair around each timed kernel class on the launching

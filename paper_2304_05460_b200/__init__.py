@@ -125,7 +125,7 @@ _sig = {
     "afn_probe_dfma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_probe_dmma": (C.c_int, [C.c_int64, _D, _P]),
     "afn_probe_ex2": (C.c_int, [C.c_int64, _D, _P]),
-    "afn_set_matvec_mode": (C.c_int, [C.c_int32]),
+    "afn_set_cutoff_mode": (C.c_int, [C.c_int32]),
     "afn_launch_count": (C.c_int64, []),
     "afn_kt_enable": (None, [C.c_int32]),
     "afn_kt_reset": (None, []),
@@ -247,7 +247,7 @@ def afn_knn_pattern(P, w, stream=None):
     return rp, col[:knn_nnz(N, w)]
 
 
-WPROD_DMMA, WPROD_INT8 = 0, 1
+WPROD_DMMA, WPROD_INT8, WPROD_CUT = 0, 1, 2
 
 
 def afn_w_product(X1, Xr, l, Linv, method=WPROD_INT8, stream=None, kernel="gaussian"):
@@ -553,9 +553,10 @@ def probe_ex2(iters=1 << 16, stream=None) -> float:
     return out.value
 
 
-def set_matvec_mode(mode: int) -> None:
-    """0 auto (cutoff plan when it pays), 1 dense symmetric, 2 cutoff (afn_set_matvec_mode)."""
-    _check(_lib.afn_set_matvec_mode(int(mode)), "afn_set_matvec_mode")
+def set_cutoff_mode(mode: int) -> None:
+    """Cutoff matvec plan and W product: 0 auto (when they pay), 1 never,
+    2 whenever they apply (afn_set_cutoff_mode)."""
+    _check(_lib.afn_set_cutoff_mode(int(mode)), "afn_set_cutoff_mode")
 
 
 def probe_dfma(iters=1 << 16, stream=None) -> float:

@@ -1065,6 +1065,23 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   }
   EvPat evhp{e_hp0, e_hp1};
 
+  // cutoff plans (kmv.cu matvec plan, wcut.cu W product), per local rank
+  std::vector<WCutPlan> wplan(nlocal);
+  struct WPlanFree {
+    std::vector<WCutPlan>& p;
+    ~WPlanFree() {
+      for (auto& x : p) w_cut_free(&x);
+    }
+  } wpf{wplan};
+  auto early_plans = [&](RankSt& s) -> afn_status {
+    const int q = (int)(&s - &h->rk[0]);
+    TRY(kmv_plan_make(s.Xs, n, s.own.size(), d, h->kn.kind, true, h->R, s.rank, st,
+                      [&](double** qq, size_t c) { return ralloc(s, qq, c, st); }, &s.plan, &s.kmv_part));
+    if (!nys && k > 0 && N2 > 0 && s.hi > s.lo && kmv_get_mode() != 1)
+      TRY(w_cut_plan(s.Xp, k, s.Xp + (k + s.lo) * d, s.hi - s.lo, d, kn, kmv_get_mode() == 2, st, &wplan[q]));
+    return AFN_OK;
+  };
+
   // ---- a1: permutation, permuted + prescaled points; a4: L L^T = K11 + mu I, L^{-T}
   for (int q = 0; q < nlocal; ++q) {
     RankSt& s = h->rk[q];
@@ -1105,7 +1122,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
     TRY(ralloc(s, &s.L, (size_t)k * k, st));
     TRY(ralloc(s, &s.LinvT, (size_t)k * k, st));
-    if (k == 0) continue;
+    if (k == 0) {
+      TRY(early_plans(s));
+      continue;
+    }
     if (!nys) TRY(ralloc(s, &s.Linv, (size_t)k * k, st));
     // L^{-1}'s workspace from the build stream before the switch (a pool
     // block taken on fs could carry a wait on another stream's work)
@@ -1133,6 +1153,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(trsm_linvt(s.L, k, s.LinvT, fs, lws));
     if (!nys) TRY(transpose_sq(s.LinvT, k, s.Linv, fs));
     kt_end(KT_LINV, fs, (double)k * k * k / 3.0);
+    // the cutoff plans need only the points: made here on st while the
+    // Cholesky (fs) and the kNN pattern (side stream) run -- their host waits
+    // then hide behind that work instead of serialising the build
+    TRY(early_plans(s));
     if (fs != st) {
       AFN_CUDA(cudaEventRecord(e_hp1, fs));
       AFN_CUDA(cudaStreamWaitEvent(st, e_hp1, 0));
@@ -1167,18 +1191,25 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   // the FSAI rows of a rank need the W rows of all their pattern neighbours)
   std::vector<double*> Wf(nlocal);
   kt_begin(KT_W_GEMM, st);
+  double w_work = 0.0;  // executed flops (dense: (N2/R) k^2 / 2 FMA per rank)
   for (int q = 0; q < nlocal; ++q) {
     RankSt& s = h->rk[q];
     TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
     const double* X2 = s.Xp + k * d;
     if (s.hi > s.lo) {
-      if (k >= AFN_W_INT8_MIN_K && s.Linv)  // (INT8 tensor cores, exact slicing: ozaki.cu)
+      const bool cut = wplan[q].used;  // (the decay of K21: wcut.cu)
+      if (cut) {
+        w_work += wplan[q].flops;
+        TRY(w_cut_run(&wplan[q], s.LinvT, Wf[q] + s.lo * k, st));
+      }
+      else if (k >= AFN_W_INT8_MIN_K && s.Linv)  // (INT8 tensor cores, exact slicing: ozaki.cu)
         TRY(w_gemm_ozaki(s.Linv, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
       else
         TRY(w_gemm(s.LinvT, k, s.Xp, X2 + s.lo * d, s.hi - s.lo, d, kn, Wf[q] + s.lo * k, st));
+      if (!cut) w_work += (double)(s.hi - s.lo) * (double)k * (double)k;
     }
   }
-  kt_end(KT_W_GEMM, st, (double)N2 * (double)k * (double)k / h->R);  // (N2/R) k^2/2 FMA per rank
+  kt_end(KT_W_GEMM, st, w_work / nlocal);
   AFN_CUDA(cudaEventRecord(ev[4], st));
 
   // ---- a6: kNN pattern (already queued on the side stream when povl)
@@ -1254,8 +1285,9 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   // ---- workspaces for apply / PCG
   for (auto& s : h->rk) {
     const int64_t nl = s.own.size();
-    TRY(kmv_plan_make(s.Xs, n, nl, d, h->kn.kind, true, h->R, s.rank, st,
-                      [&](double** q, size_t c) { return ralloc(s, q, c, st); }, &s.plan, &s.kmv_part));
+    if (!s.kmv_part)  // (normally made early, beside the Cholesky)
+      TRY(kmv_plan_make(s.Xs, n, nl, d, h->kn.kind, true, h->R, s.rank, st,
+                        [&](double** q, size_t c) { return ralloc(s, q, c, st); }, &s.plan, &s.kmv_part));
     if (s.plan.sym && h->R > 1) TRY(ralloc(s, &s.qpart, (size_t)h->R * n, st));
     const int64_t gw = std::max(std::max(gemv_t_ws(k, k), gemv_t_ws(h->R == 1 ? N2 : s.hi - s.lo, k)),
                                 nys ? gemv_t_ws(nl, k) : (int64_t)1);
@@ -1442,7 +1474,9 @@ afn_status afn_w_product(const double* X1, int64_t k, const double* Xr, int64_t 
   TRY(validate_X(Xr, N, d));
   REQ(kernel == AFN_KERNEL_GAUSSIAN || kernel == AFN_KERNEL_MATERN32, "unknown kernel %d", kernel);
   REQ(l > 0 && std::isfinite(l), "l must be > 0");
-  REQ(method == AFN_WPROD_DMMA || method == AFN_WPROD_INT8, "unknown method %d", method);
+  REQ(method == AFN_WPROD_DMMA || method == AFN_WPROD_INT8 || method == AFN_WPROD_CUT, "unknown method %d", method);
+  REQ(method != AFN_WPROD_CUT || (kernel == AFN_KERNEL_GAUSSIAN && d <= 3),
+      "AFN_WPROD_CUT needs the Gaussian kernel and d <= 3");
   REQ(is_dev(Linv) && is_dev(W), "Linv, W must be device pointers");
   REQ(method != AFN_WPROD_INT8 || k < 65536, "AFN_WPROD_INT8 needs k < 65536");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1451,6 +1485,12 @@ afn_status afn_w_product(const double* X1, int64_t k, const double* Xr, int64_t 
   double* LinvT;
   TRY(t.get(&LinvT, (size_t)k * k));
   TRY(transpose_sq(Linv, k, LinvT, st));
+  if (method == AFN_WPROD_CUT) {
+    bool used = false;
+    TRY(w_gemm_cut(LinvT, k, X1, Xr, N, d, Kern{kernel, l}, W, st, true, &used, nullptr));
+    REQ(used, "AFN_WPROD_CUT: too many row tiles");
+    return AFN_OK;
+  }
   return w_gemm(LinvT, k, X1, Xr, N, d, Kern{kernel, l}, W, st);
 }
 
@@ -1959,8 +1999,8 @@ afn_status afn_probe_ex2(int64_t iters, double* gops, void* stream) {
   return probe_ex2(iters, gops, (cudaStream_t)stream);
 }
 
-afn_status afn_set_matvec_mode(int32_t mode) {
-  REQ(mode >= 0 && mode <= 2, "matvec mode %d (0 auto, 1 dense, 2 cutoff)", mode);
+afn_status afn_set_cutoff_mode(int32_t mode) {
+  REQ(mode >= 0 && mode <= 2, "cutoff mode %d (0 auto, 1 never, 2 whenever it applies)", mode);
   kmv_set_mode(mode);
   return AFN_OK;
 }

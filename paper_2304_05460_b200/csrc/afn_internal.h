@@ -104,9 +104,16 @@ struct KmvPlan {
           o_rbase = 0, o_tptr = 0, o_tu = 0;
   int64_t ws = 0;  // workspace doubles for kmv_launch
 };
-// matvec plan selection (afn_set_matvec_mode): 0 auto (cutoff plan when it
-// keeps at most half of the pairs), 1 never the cutoff plan, 2 the cutoff
-// plan whenever it applies (Gaussian, d <= 3, full symmetric product)
+// ---- spatial order (spatial.cu) ----------------------------------------------
+// sidx[pos] = point: Morton order of a grid of ~2 points per cell over the
+// first min(d, 3) coordinates, a cell's points by ascending index (deterministic)
+afn_status morton_order(const double* X, int64_t n, int d, int* sidx, cudaStream_t st);
+// off[0..M] = exclusive scan of cnt[0..M) (one block; M up to a few million)
+afn_status scan_i32_i64(const int* cnt, int64_t M, int64_t* off, cudaStream_t st);
+
+// cutoff selection (afn_set_cutoff_mode) for the kernel matvec and W: 0 auto
+// (the cutoff plan / product when it keeps at most half of the pairs), 1
+// never, 2 whenever it applies (Gaussian, d <= 3, full symmetric product)
 void kmv_set_mode(int mode);
 int kmv_get_mode();
 using WsGet = std::function<afn_status(double**, size_t)>;
@@ -176,6 +183,29 @@ afn_status potrf_batched(double* A, int64_t k, int nbatch, int64_t bs, double sk
 afn_status w_gemm_ozaki(const double* Linv, int64_t k, const double* X1, const double* Xr, int64_t N, int d, Kern kn,
                         double* W, cudaStream_t st);
 constexpr int64_t AFN_W_INT8_MIN_K = 512;  // the build's W takes the INT8 path from this k on
+// W = K(Xr, X1) L^{-T} keeping only the entries >= 2^-128 (Gaussian, d <= 3;
+// wcut.cu).  *used = false (nothing written) when it does not
+// apply or (unless force) keeps more than half of the landmarks per tile;
+// *flops = executed FP64 flops
+afn_status w_gemm_cut(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d, Kern kn,
+                      double* W, cudaStream_t st, bool force, bool* used, double* flops);
+// The same in two calls: the plan (spatial order, kept landmarks, the K21
+// tiles; needs only the points, synchronises st) and the product with L^{-T}
+// (stream-ordered; releases the plan).  used = false: the dense path applies.
+struct WCutPlan {
+  bool used = false;
+  int64_t k = 0, N = 0, nt = 0;
+  int *sidx = nullptr, *ulist = nullptr;
+  int64_t *uoff = nullptr, *aoff = nullptr;
+  double* A = nullptr;
+  double flops = 0.0;
+  std::vector<void*> mem;
+  cudaStream_t st = nullptr;
+};
+afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, int d, Kern kn, bool force,
+                      cudaStream_t st, WCutPlan* p);
+afn_status w_cut_run(WCutPlan* p, const double* LinvT, double* W, cudaStream_t st);
+void w_cut_free(WCutPlan* p);
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st);
 // G = F^T F (C x C, full) for F: R x C row-major; deterministic

@@ -41,8 +41,8 @@ def elementwise(y, X, l, mu, v, rows):
 
 @pytest.fixture
 def mode():
-    yield afn.set_matvec_mode
-    afn.set_matvec_mode(0)
+    yield afn.set_cutoff_mode
+    afn.set_cutoff_mode(0)
 
 
 def _plan_of(Xd, l):
@@ -156,7 +156,7 @@ def test_cut_afn_pcg_c2(mode, l):
 def test_cut_c3_auto_sampled_rows():
     """C3 (n = 2^17, l = 1): auto mode picks the cutoff plan; sampled rows
     element-wise against the oracle."""
-    afn.set_matvec_mode(0)
+    afn.set_cutoff_mode(0)
     X, b = gen_problem("C3")
     Xd, bd = T(X), T(b)
     info = _plan_of(Xd, 1.0)
@@ -166,3 +166,62 @@ def test_cut_c3_auto_sampled_rows():
     y = afn.kernel_matvec(Xd, 1.0, 1e-4, bd).cpu().numpy()
     rows = np.random.default_rng(5).choice(n, 200, replace=False)
     assert elementwise(y, X, 1.0, 1e-4, b, rows) <= 1e-12
+
+
+@pytest.mark.parametrize("k,N,d,l,edge", [(1000, 20000, 3, 1.0, 28.0), (700, 5000, 3, 0.5, None),
+                                          (333, 4097, 3, 1.0, 40.0), (64, 200, 3, 1.0, 30.0),
+                                          (500, 6000, 2, 1.0, None), (300, 3000, 1, 2.0, None),
+                                          (1, 1000, 3, 1.0, None)])
+def test_w_product_cutoff(k, N, d, l, edge):
+    """W = K21 L^{-T} with the terms whose K21 entry is below 2^-128
+    dropped (wcut.cu).  Against the DMMA path (the same kernel
+    entries): every entry within 1e-15 k max_t |K21_rt| max_t |L^{-1}_ct| plus
+    the dropped terms' bound k 2^-128 max |L^{-1}|.  Against the plain fp64
+    product (oracle entries, LAPACK Cholesky and triangular inverse): every
+    row above the dropped-term floor within 1e-12 (normwise), as the dense
+    paths (a far entry's own rounding, ~s eps relative, is the same on both)."""
+    from scipy.linalg import cholesky, solve_triangular
+    X, _ = gen_points(k + N, d, "cube", 13, edge)
+    X1, Xr = X[:k], X[k:]
+    K11 = O.kernel_block(X1, X1, l) + 1e-4 * np.eye(k)
+    Lc = cholesky(K11, lower=True)
+    Linv = solve_triangular(Lc, np.eye(k), lower=True)
+    K21 = O.kernel_block(Xr, X1, l)
+    Wref = K21 @ Linv.T
+    scale = np.abs(K21).max(axis=1)[:, None] * np.abs(Linv).max(axis=1)[None, :]
+    Wc = afn.afn_w_product(T(X1), T(Xr), l, T(Linv), afn.WPROD_CUT).cpu().numpy()
+    Wd = afn.afn_w_product(T(X1), T(Xr), l, T(Linv), afn.WPROD_DMMA).cpu().numpy()
+    assert np.all(np.isfinite(Wc))
+    drop = k * 2.0 ** -128 * np.max(np.abs(Linv))
+    assert np.all(np.abs(Wc - Wd) <= 1e-15 * k * scale + drop)
+    nr = np.linalg.norm(Wref, axis=1)
+    ok = nr > 1e20 * drop
+    assert ok.any()
+    rc = np.max(np.linalg.norm(Wc - Wref, axis=1)[ok] / nr[ok])
+    assert rc <= 1e-12, rc
+
+
+def test_build_uses_w_cutoff_and_matches_dense(mode):
+    """C2 (l = 1) handles built with and without the cutoff paths (mode 1:
+    dense matvec and INT8 W): the same landmarks and pattern, W rows and G
+    rows within the build's parity bounds, the same PCG iteration count."""
+    X, b = gen_problem("C2")
+    Xd, bd = T(X), T(b)
+    prm = afn.make_params(1.0, 1e-4, 2000, 100, k_adaptive=True)
+    mode(2)
+    hc = afn.afn_build(Xd, prm)
+    mode(1)
+    hd = afn.afn_build(Xd, prm)
+    assert hc.info()["kmv_plan"] == 2 and hd.info()["kmv_plan"] == 1
+    k = hc.info()["k"]
+    rows = np.arange(0, len(X) - k, 97)
+    Wc = hc.copy_out_rows(afn.OUT_W, rows)
+    Wdd = hd.copy_out_rows(afn.OUT_W, rows)
+    assert np.max(np.linalg.norm(Wc - Wdd, axis=1) / np.linalg.norm(Wdd, axis=1)) <= 1e-12
+    gc, gd = hc.copy_out(afn.OUT_GVAL), hd.copy_out(afn.OUT_GVAL)
+    assert np.max(np.abs(gc - gd)) <= 1e-10 * np.max(np.abs(gd))
+    _, rc = hc.pcg_solve(bd, tol=1e-4)
+    _, rd = hd.pcg_solve(bd, tol=1e-4)
+    assert rc["iterations"] == rd["iterations"]
+    hc.close()
+    hd.close()

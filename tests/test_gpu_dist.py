@@ -5,8 +5,11 @@ PCG code that runs with NCCL across GPUs.  No kernel waits
 on another rank.  Checks against the single-GPU handle (itself checked
 against the oracle in test_gpu_parity.py) and against the oracle:
 
-  * replicated pieces (permutation, L, pattern, G) bit-identical on every rank;
-  * each rank's W rows bit-identical to the same rows of the single-GPU W;
+  * replicated pieces (permutation, fill, L, pattern) bit-identical on every rank;
+  * each rank's W rows within 1e-14 (row norm) of the same rows of the
+    single-GPU W and G within 1e-12: the cutoff W product (wcut.cu) tiles a
+    rank's own rows, so its tensor-core k-chunks group the same terms
+    differently (DESIGN.md 6.3);
   * apply and PCG: same iteration count, solution and apply within rounding
     of the single-GPU path, true residual <= tol; oracle iteration count +-2."""
 import numpy as np
@@ -54,11 +57,18 @@ def test_emulated_ranks_match_single_gpu(R, n, l, mu, k, w, adaptive):
     assert iR["nranks"] == R and iR["k"] == i1["k"] and iR["nnz"] == i1["nnz"]
     kk = i1["k"]
     W1 = h1.copy_out(afn.OUT_W)
+    G1 = h1.copy_out(afn.OUT_GVAL)
     for q in range(R):
-        for what in (afn.OUT_PERM, afn.OUT_FILL, afn.OUT_L, afn.OUT_ROWPTR, afn.OUT_COL, afn.OUT_GVAL):
+        for what in (afn.OUT_PERM, afn.OUT_FILL, afn.OUT_L, afn.OUT_ROWPTR, afn.OUT_COL):
             assert np.array_equal(hR.copy_out(what, q), h1.copy_out(what)), (q, what)
         a0, na, b0, nb = afn.shard_rows(n, kk, R, q)
-        assert np.array_equal(hR.copy_out(afn.OUT_W, q), W1[b0 - kk:b0 - kk + nb])
+        # W rows: the cutoff product (wcut.cu) tiles a rank's own rows, so its
+        # DMMA k-chunks group the kept terms differently -- rounding only
+        Wq, Wr = hR.copy_out(afn.OUT_W, q), W1[b0 - kk:b0 - kk + nb]
+        nr = np.linalg.norm(Wr, axis=1)
+        assert np.all(np.linalg.norm(Wq - Wr, axis=1) <= 1e-14 * nr + 1e-300)
+        if G1.size:
+            assert np.max(np.abs(hR.copy_out(afn.OUT_GVAL, q) - G1)) <= 1e-12 * np.max(np.abs(G1))
     # apply
     r = T(np.random.default_rng(3).standard_normal(n))
     z1 = h1.apply(r).cpu().numpy()

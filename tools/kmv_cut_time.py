@@ -20,7 +20,7 @@ for cfg in cfgs:
         for mode in (1, 2):
             if cfg == "C5" and mode == 1:
                 continue
-            afn.set_matvec_mode(mode)
+            afn.set_cutoff_mode(mode)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             h = afn.afn_build(Xd, afn.make_params(l, 1e-4, 1, 1, method=afn.METHOD_NONE))
@@ -51,4 +51,4 @@ for cfg in cfgs:
         if 1 in res and 2 in res:
             d = (res[1] - res[2]).norm() / res[1].norm()
             print(f"   rel(cut, dense) = {float(d):.3e}", flush=True)
-afn.set_matvec_mode(0)
+afn.set_cutoff_mode(0)
