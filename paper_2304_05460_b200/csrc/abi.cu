@@ -1077,8 +1077,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     const int q = (int)(&s - &h->rk[0]);
     TRY(kmv_plan_make(s.Xs, n, s.own.size(), d, h->kn.kind, true, h->R, s.rank, st,
                       [&](double** qq, size_t c) { return ralloc(s, qq, c, st); }, &s.plan, &s.kmv_part));
+    // (Z mode: one rank, AFN -- the FSAI products through Z = K21 M)
     if (!nys && k > 0 && N2 > 0 && s.hi > s.lo && kmv_get_mode() != 1)
-      TRY(w_cut_plan(s.Xp, k, s.Xp + (k + s.lo) * d, s.hi - s.lo, d, kn, kmv_get_mode() == 2, st, &wplan[q]));
+      TRY(w_cut_plan(s.Xp, k, s.Xp + (k + s.lo) * d, s.hi - s.lo, d, kn, kmv_get_mode() == 2,
+                     h->R == 1 && povl && k <= 8192, st, &wplan[q]));
     return AFN_OK;
   };
 
@@ -1209,6 +1211,37 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       if (!cut) w_work += (double)(s.hi - s.lo) * (double)k * (double)k;
     }
   }
+  // Z mode: M = (K11 + mu I)^{-1} and Z = K21 M over the landmarks' Morton
+  // order for the FSAI products (freed after them); no memory -> W products
+  std::vector<double*> zbuf(3 * nlocal, nullptr);
+  std::vector<FsaiZ> fz(nlocal);
+  for (int q = 0; q < nlocal; ++q) {
+    RankSt& s = h->rk[q];
+    WCutPlan& wp = wplan[q];
+    if (!wp.used || !wp.lp) continue;
+    const afn_status a1 = dalloc((void**)&zbuf[3 * q], sizeof(double) * (size_t)k * k, st);
+    const afn_status a2 = a1 == AFN_OK ? dalloc((void**)&zbuf[3 * q + 1], sizeof(double) * (size_t)k * k, st) : a1;
+    const afn_status a3 =
+        a2 == AFN_OK ? dalloc((void**)&zbuf[3 * q + 2], sizeof(double) * (size_t)(s.hi - s.lo) * k, st) : a2;
+    if (a3 != AFN_OK) {  // (not enough memory for Z: the W products)
+      for (int e = 0; e < 3; ++e)
+        if (zbuf[3 * q + e]) dfree(zbuf[3 * q + e], st), zbuf[3 * q + e] = nullptr;
+      w_cut_free(&wp);
+      continue;
+    }
+    TRY(w_cut_z(&wp, s.LinvT, s.Linv, zbuf[3 * q], zbuf[3 * q + 1], zbuf[3 * q + 2], st));
+    w_work += wp.zflops + (double)k * k * k;
+    fz[q] = FsaiZ{zbuf[3 * q + 2], wp.tilerow, wp.uoff, wp.ulistp, wp.aoff, wp.Ap,
+                  (double)k / (double)std::max<int64_t>(1, N2) <= 0.015};  // (C5 0.0077 staged; C3 0.031 not)
+  }
+  struct ZFree {
+    std::vector<double*>& b;
+    cudaStream_t st;
+    ~ZFree() {
+      for (double* x : b)
+        if (x) dfree(x, st);
+    }
+  } zfree{zbuf, st};
   kt_end(KT_W_GEMM, st, w_work / nlocal);
   AFN_CUDA(cudaEventRecord(ev[4], st));
 
@@ -1244,7 +1277,8 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       const double* X2 = s.Xp + k * d;
       // (the pair-union product; AFN_ERR_STATE: a group's union overflowed -> per-row Grams)
       const afn_status fs = fsai_sddmm_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.trp, s.tcol, s.lo,
-                                           s.hi, s.gval, s.dinfo + 1, st, povl ? side_stream() : st);
+                                           s.hi, s.gval, s.dinfo + 1, st, povl ? side_stream() : st,
+                                           fz[q].Zp ? &fz[q] : nullptr);
       if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
       if (fs != AFN_OK) {
         kt_begin(KT_FSAI_GRAM, st);

@@ -192,20 +192,31 @@ afn_status w_gemm_cut(const double* LinvT, int64_t k, const double* X1, const do
 // The same in two calls: the plan (spatial order, kept landmarks, the K21
 // tiles; needs only the points, synchronises st) and the product with L^{-T}
 // (stream-ordered; releases the plan).  used = false: the dense path applies.
+// zmode (one rank): also the landmarks' Morton order lp, the same lists over
+// it (ulistp, positions ascending) with their K21 tiles Ap, and tilerow[b] =
+// (tile << 6) | row of point b -- what the FSAI product through Z = K21 M
+// needs (fsai_sddmm.cu); w_cut_run then keeps the plan, w_cut_z forms
+// M = L^{-T} L^{-1}, Mp = M[lp][:, lp] and Zp = K21 M[:, lp] (N x k, rows by point).
 struct WCutPlan {
   bool used = false;
   int64_t k = 0, N = 0, nt = 0;
   int *sidx = nullptr, *ulist = nullptr;
   int64_t *uoff = nullptr, *aoff = nullptr;
   double* A = nullptr;
-  double flops = 0.0;
+  int *lp = nullptr, *ulistp = nullptr, *tilerow = nullptr;
+  double* Ap = nullptr;
+  double flops = 0.0, zflops = 0.0;  // executed flops of the W and Z products
   std::vector<void*> mem;
   cudaStream_t st = nullptr;
 };
 afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, int d, Kern kn, bool force,
-                      cudaStream_t st, WCutPlan* p);
+                      bool zmode, cudaStream_t st, WCutPlan* p);
 afn_status w_cut_run(WCutPlan* p, const double* LinvT, double* W, cudaStream_t st);
+afn_status w_cut_z(WCutPlan* p, const double* LinvT, const double* Linv, double* M, double* Mp, double* Zp,
+                   cudaStream_t st);
 void w_cut_free(WCutPlan* p);
+// C = A B (k x k, row-major) for A upper and B lower triangular (dense.cu)
+afn_status gemm_upper_lower(const double* A, const double* B, int64_t k, double* C, cudaStream_t st);
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st);
 // G = F^T F (C x C, full) for F: R x C row-major; deterministic
@@ -231,12 +242,25 @@ afn_status csr_transpose(const int64_t* rp, const int32_t* col, const double* va
                          int64_t nnz, int64_t* trp, int32_t* tcol, double* tval, cudaStream_t st,
                          int64_t* tmap = nullptr);
 afn_status gather_map(const double* v, const int64_t* map, int64_t nnz, double* out, cudaStream_t st);
+// The products W_a . W_b through Z = K21 M (one rank, the cutoff W plan's
+// Z mode): Zp (N x k, rows by point, columns in the
+// landmarks' Morton order) and the plan's per-tile K21 blocks over that order.
+struct FsaiZ {
+  const double* Zp = nullptr;
+  const int* tilerow = nullptr;
+  const int64_t* uoff = nullptr;
+  const int* ulistp = nullptr;
+  const int64_t* aoff = nullptr;
+  const double* Ap = nullptr;
+  bool staged = false;  // stage each half group's Z columns in shared memory
+};
 // FSAI through the union of needed Schur-complement pairs (fsai_sddmm.cu).
 // Returns AFN_ERR_STATE (nothing written) if a group's pair union overflows.
+// z: the products through Z (else D_g = W_g W_U^T).
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval,
-                          int* d_info, cudaStream_t st, cudaStream_t pst = nullptr);
+                          int* d_info, cudaStream_t st, cudaStream_t pst = nullptr, const FsaiZ* z = nullptr);
 
 // ---- BLAS-2 / SpMV / vectors (blas.cu) ------------------------------------
 // y = ybase + alpha * A x, A: R x C row-major (lda = C).  ybase may be null (0)

@@ -766,3 +766,17 @@ afn_status trsm_linvt(const double* L, int64_t k, double* LinvT, cudaStream_t st
 }
 
 }  // namespace afn
+
+namespace afn {
+// C = A B for A upper and B lower triangular (k x k, row-major): the
+// K range of a column block starts at its first column (MODE 2), k^3 / 2 FMA
+afn_status gemm_upper_lower(const double* A, const double* B, int64_t k, double* C, cudaStream_t st) {
+  if (k <= 0) return AFN_OK;
+  const int bytes = (int)(sizeof(double) * TS * (TM * TKP + TK * TNP));
+  AFN_CUDA(cudaFuncSetAttribute(gemm_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  dim3 grid((unsigned)((k + TN - 1) / TN), (unsigned)((k + TM - 1) / TM), 1);
+  gemm_dmma_kernel<2><<<grid, 128, bytes, st>>>(A, B, C, k, k, k, k, k, k, 0, 0, 0, 1.0);
+  AFN_LAUNCH_CHECK("gemm_dmma_kernel<2>");
+  return AFN_OK;
+}
+}  // namespace afn

@@ -244,6 +244,13 @@ __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int
 // list) and the global copy of the table H_g[slot] = (b, u) that the factor
 // kernel uses to find W_a . W_b in D_g (one or two probes).  A warp walks
 // one pattern row at a time, lanes over its entries.
+// TILE (the product through Z = K21 M, group_zk_kernel): the keys are
+// numbered grouped by the 64-point tile of the cutoff W plan that holds them
+// (tilerow[b] >> 6; any order inside a tile -- a value never depends on its
+// column), and the group's pieces (a tile's columns, <= 32 at a time) are
+// listed in Pc / Pcount; *zwork += the product's MACs (GA per column and
+// kept landmark of its tile).
+template <bool TILE>
 __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict__ sorder, int64_t N,
                                                           const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ colp,
@@ -251,8 +258,12 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
                                                           const int32_t* __restrict__ tcol,
                                                           int64_t row_lo, int64_t row_hi, int ga,
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
-                                                          int2* __restrict__ Htab, int* overflow) {
-  extern __shared__ int hs[];  // HC keys (positions)
+                                                          int2* __restrict__ Htab, int* overflow,
+                                                          const int* __restrict__ tilerow,
+                                                          const int64_t* __restrict__ uoff, int2* __restrict__ Pc,
+                                                          int* __restrict__ Pcount,
+                                                          unsigned long long* __restrict__ zwork) {
+  extern __shared__ int hs[];  // HC keys (positions); TILE: + tile keys, counts, offsets (HC each)
   __shared__ int s_n, s_ovf;
   __shared__ int s_scan[256];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -294,8 +305,89 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     if (tid == 0) atomicExch(overflow, 1);
     return;
   }
-  // number the occupied slots in slot order (block scan over 32-slot strips)
   constexpr int PER = HC / 256;
+  if (TILE) {
+    int* tk = hs + HC;      // tile keys
+    int* tc = hs + 2 * HC;  // counts, then running cursors
+    int* to = hs + 3 * HC;  // offsets
+    for (int t = tid; t < HC; t += 256) {
+      tk[t] = -1;
+      tc[t] = 0;
+    }
+    __syncthreads();
+    auto tslot = [&](int tile, bool ins) {
+      unsigned h = ((unsigned)tile * 2654435761u) & (HC - 1);
+      for (;;) {
+        const int old = ins ? atomicCAS(&tk[h], -1, tile) : tk[h];
+        if (old == -1 || old == tile) return (int)h;
+        h = (h + 1) & (HC - 1);
+      }
+    };
+    for (int slot = tid; slot < HC; slot += 256) {
+      const int pb = hs[slot];
+      if (pb >= 0) atomicAdd(&tc[tslot(tilerow[sorder[pb]] >> 6, true)], 1);
+    }
+    __syncthreads();
+    // offsets (columns) and piece offsets in slot order
+    int cc = 0, pp = 0;
+    for (int t = 0; t < PER; ++t) {
+      const int c1 = tc[tid * PER + t];
+      cc += c1;
+      pp += (c1 + 31) / 32;
+    }
+    s_scan[tid] = cc;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+      const int v = tid >= o ? s_scan[tid - o] : 0;
+      __syncthreads();
+      s_scan[tid] += v;
+      __syncthreads();
+    }
+    int run = s_scan[tid] - cc;
+    __syncthreads();
+    s_scan[tid] = pp;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+      const int v = tid >= o ? s_scan[tid - o] : 0;
+      __syncthreads();
+      s_scan[tid] += v;
+      __syncthreads();
+    }
+    int prun = s_scan[tid] - pp;
+    unsigned long long wk = 0ull;
+    for (int t = 0; t < PER; ++t) {
+      const int slot = tid * PER + t;
+      const int c1 = tc[slot];
+      to[slot] = run;
+      if (c1 > 0) {
+        const int tile = tk[slot];
+        wk += (unsigned long long)c1 * (unsigned long long)(uoff[tile + 1] - uoff[tile]);
+        for (int q = 0; q < c1; q += 32) Pc[g * UCAP + prun++] = make_int2(run + q, min(32, c1 - q));
+      }
+      run += c1;
+    }
+    if (tid == 255) Pcount[g] = prun;
+    for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
+    if (lane == 0) atomicAdd(zwork, wk * (unsigned long long)GA);
+    __syncthreads();
+    for (int t = tid; t < HC; t += 256) tc[t] = 0;
+    __syncthreads();
+    int2* H = Htab + g * HC;
+    for (int slot = tid; slot < HC; slot += 256) {
+      const int pb = hs[slot];
+      if (pb >= 0) {
+        const int ts = tslot(tilerow[sorder[pb]] >> 6, false);
+        const int u = to[ts] + atomicAdd(&tc[ts], 1);
+        Ulist[g * UCAP + u] = sorder[pb];
+        H[slot] = make_int2(pb, u);
+      } else {
+        H[slot] = make_int2(-1, -1);
+      }
+    }
+    if (tid == 0) Ucount[g] = nu;
+    return;
+  }
+  // number the occupied slots in slot order (block scan over 32-slot strips)
   int c = 0;
   for (int t = 0; t < PER; ++t) c += hs[tid * PER + t] >= 0;
   s_scan[tid] = c;
@@ -475,6 +567,179 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
     }
   }
   }  // rounds
+}
+
+// ---------------------------------------------------------------- group product through Z
+// D_g[a][u] = S_ab = K(x_a, x_b) + mu delta_ab - Z_a . k_b with Z = K21 M,
+// M = (K11 + mu I)^{-1} (Z_a . k_b = k_a^T M k_b = W_a . W_b), k_b the row
+// of K21 kept by the cutoff W plan (wcut.cu: its tile's landmark list U_t,
+// over the landmarks' Morton order, and its row of the tile's K21 block).
+// One CTA per half group (ZH = 16 rows a): the landmark columns the group's
+// tiles keep, U' = union of their U_t, are marked in a shared bitmap over the
+// k positions and the 16 Z rows are staged at those columns in shared memory
+// once (k_b's columns are then looked up by the bitmap's prefix counts);
+// warps take the pieces (<= 32 union columns of one tile): a 16 x 32 x |U_t|
+// product on the FP64 tensor cores (DMMA m8n8k4), A fragments from the staged
+// Z, B fragments from the tile's K21 rows in global memory.
+//
+// !STAGED (dense landmarks, U' too wide to stage): ZS consecutive CTAs share a
+// group (all 32 rows), each taking every ZS-th piece; fragments straight from
+// Z in global memory -- the CTAs in flight then cover few groups, whose Z
+// rows stay in L2 (one CTA per whole group: C3 28.5 ms, DRAM 46 GB).
+constexpr int ZH = 16;
+constexpr int ZCAP = 1664;  // staged columns (16 x 1664 x 8 B = 208 KB); wider U' -> global loads
+constexpr int ZS = 4;
+template <bool STAGED>
+__global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
+    const int* __restrict__ sorder, int64_t N, const double* __restrict__ Zp, int64_t k,
+    const int* __restrict__ tilerow, const int64_t* __restrict__ uoff, const int* __restrict__ ulistp,
+    const int64_t* __restrict__ aoff, const double* __restrict__ Ap, const int* __restrict__ Ucount,
+    const int* __restrict__ Ulist, const int64_t* __restrict__ Doff, const int2* __restrict__ Pc,
+    const int* __restrict__ Pcount, double* __restrict__ D, const double* __restrict__ X2, int d, KernelFn kf,
+    double mu) {
+  extern __shared__ __align__(16) double zs[];  // [ZH][ncol] staged Z (ld = ncol)
+  __shared__ double s_tab[AFN_EXP2_TAB_N];
+  __shared__ int s_a[GA];
+  __shared__ unsigned s_bits[256];   // k <= 8192 positions
+  __shared__ int s_pre[257];         // prefix counts of s_bits
+  __shared__ int s_u[8][256];        // per warp: the piece's U_t as staged columns
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  load_exp2_tab(s_tab);
+  constexpr int RH = STAGED ? ZH : GA;  // rows per CTA
+  const int64_t g = STAGED ? (int64_t)(blockIdx.x >> 1) : (int64_t)(blockIdx.x / ZS);
+  const int half = STAGED ? (int)(blockIdx.x & 1) : 0;
+  const int pq = STAGED ? 0 : (int)(blockIdx.x % ZS);  // this CTA's share of the pieces
+  const int pstep = STAGED ? 8 : 8 * ZS;
+  const int64_t m0 = g * GA + half * ZH;
+  const int cnt = (int)max((int64_t)0, min((int64_t)RH, N - m0));
+  if (tid < RH) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
+  const int nwords = (int)((k + 31) / 32);
+  for (int w = tid; w < 256; w += 256) s_bits[w] = 0u;
+  __syncthreads();
+  if (cnt == 0) return;
+  const int nu = Ucount[g], np = Pcount[g];
+  // mark U' (every piece's tile list)
+  for (int p = wid; STAGED && p < np; p += 8) {
+    const int tile = tilerow[Ulist[g * UCAP + Pc[g * UCAP + p].x]] >> 6;
+    const int64_t us = uoff[tile], ue = uoff[tile + 1];
+    for (int64_t m = us + lane; m < ue; m += 32) {
+      const int pos = ulistp[m];
+      atomicOr(&s_bits[pos >> 5], 1u << (pos & 31));
+    }
+  }
+  __syncthreads();
+  auto prefix = [&]() {
+    if (tid == 0) {
+      int run = 0;
+      for (int w = 0; w < nwords; ++w) {
+        s_pre[w] = run;
+        run += __popc(s_bits[w]);
+      }
+      s_pre[nwords] = run;
+    }
+    __syncthreads();
+  };
+  if (STAGED) prefix();
+  const int ncol = STAGED ? s_pre[nwords] : 0;
+  const bool staged = STAGED && ncol <= ZCAP;
+  if (staged) {  // Z rows at the marked columns (a warp per row, lanes over bitmap words)
+    for (int r = wid; r < ZH; r += 8) {
+      const int a = s_a[r];
+      for (int w = lane; w < nwords; w += 32) {
+        unsigned bits = s_bits[w];
+        int c = s_pre[w];
+        while (bits) {
+          const int bpos = __ffs(bits) - 1;
+          bits &= bits - 1;
+          zs[r * ncol + c++] = a >= 0 ? Zp[(int64_t)a * k + w * 32 + bpos] : 0.0;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* Dg = D + Doff[g];
+  const int fr = lane >> 2, fk = lane & 3;
+  constexpr int MTL = RH / 8;
+  int arow[MTL];
+#pragma unroll
+  for (int mt = 0; mt < MTL; ++mt) arow[mt] = s_a[mt * 8 + fr];
+  for (int p = pq * 8 + wid; p < np; p += pstep) {
+    const int2 pc = Pc[g * UCAP + p];
+    const int u0 = pc.x, nb = pc.y;
+    int bid[4], brow[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      const int col = n * 8 + fr;
+      bid[n] = col < nb ? Ulist[g * UCAP + u0 + col] : -1;
+      brow[n] = bid[n] >= 0 ? (tilerow[bid[n]] & 63) : 0;
+    }
+    const int tile = tilerow[Ulist[g * UCAP + u0]] >> 6;
+    const int64_t us = uoff[tile];
+    const int nuT = (int)(uoff[tile + 1] - us);
+    const int ld = (nuT + 1) & ~1;
+    const int* U = ulistp + us;
+    const double* At = Ap + aoff[tile];
+    double acc[MTL][4][2];
+#pragma unroll
+    for (int mt = 0; mt < MTL; ++mt)
+#pragma unroll
+      for (int n = 0; n < 4; ++n) acc[mt][n][0] = acc[mt][n][1] = 0.0;
+    const int nn = (nb + 7) / 8;
+    for (int c0 = 0; c0 < nuT; c0 += 256) {  // (U_t in chunks of 256 staged columns)
+      const int cn = min(256, nuT - c0);
+      __syncwarp();
+      for (int m = lane; m < cn; m += 32) {
+        const int pos = U[c0 + m];
+        const unsigned wb = s_bits[pos >> 5];
+        s_u[wid][m] = !staged ? pos
+                              : ((wb >> (pos & 31)) & 1u) ? s_pre[pos >> 5] + __popc(wb & ((1u << (pos & 31)) - 1u))
+                                                          : -1;  // (a zero column for this group)
+      }
+      __syncwarp();
+      for (int k4 = 0; k4 < cn; k4 += 4) {
+        const int m = k4 + fk;
+        const bool ok = m < cn;
+        const int col = ok ? s_u[wid][m] : -1;
+        double av[MTL], bv[4];
+#pragma unroll
+        for (int mt = 0; mt < MTL; ++mt)
+          av[mt] = (col >= 0 && arow[mt] >= 0)
+                       ? (staged ? zs[(mt * 8 + fr) * ncol + col] : __ldg(&Zp[(int64_t)arow[mt] * k + col]))
+                       : 0.0;
+#pragma unroll
+        for (int n = 0; n < 4; ++n) bv[n] = (ok && bid[n] >= 0) ? __ldg(&At[(int64_t)brow[n] * ld + c0 + m]) : 0.0;
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+          if (n >= nn) break;
+#pragma unroll
+          for (int mt = 0; mt < MTL; ++mt) dmma884(acc[mt][n][0], acc[mt][n][1], av[mt], bv[n]);
+        }
+      }
+    }
+    // epilogue: lane holds rows mt*8 + fr, columns n*8 + 2fk + h
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      int bh[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) bh[h] = __shfl_sync(0xffffffffu, bid[n], (2 * fk + h) * 4);
+      if (n >= nn) continue;
+#pragma unroll
+      for (int mt = 0; mt < MTL; ++mt) {
+        const int j = mt * 8 + fr;
+        const int a = arow[mt];
+        if (j >= cnt) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cu = n * 8 + 2 * fk + h;
+          const int b = bh[h];
+          if (cu < nb && b >= 0) {
+            const double kv = a == b ? 1.0 + mu : kern_from_d2(kf, d2_exact_rt(&X2[(int64_t)a * d], &X2[(int64_t)b * d], d), s_tab);
+            Dg[(int64_t)(half * ZH + j) * nu + u0 + cu] = kv - acc[mt][n][h];
+          }
+        }
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------- factor
@@ -810,7 +1075,7 @@ afn_status launch_factor(const int* rorder, int64_t N, int64_t row_lo, int64_t r
 afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu, const double* W,
                           int64_t k, const int64_t* rp, const int32_t* col, const int64_t* trp,
                           const int32_t* tcol, int64_t row_lo, int64_t row_hi, double* gval, int* d_info,
-                          cudaStream_t st, cudaStream_t pst) {
+                          cudaStream_t st, cudaStream_t pst, const FsaiZ* z) {
   if (N <= 0 || row_hi <= row_lo) return AFN_OK;
   // steps 1-2 (spatial order, unions, pass offsets; they need only the
   // pattern) run on pst -- concurrently with W on st when pst != st; the
@@ -928,19 +1193,35 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   if ((s = get((void**)&ovf, sizeof(int) * 2)) != AFN_OK) return s;
   if ((s = get((void**)&Doff, sizeof(int64_t) * (G + 1))) != AFN_OK) return s;
   AFN_CUDA(cudaMemsetAsync(ovf, 0, sizeof(int) * 2, st));
+  int2* Pc = nullptr;
+  int* Pcount = nullptr;
+  unsigned long long* zwork = nullptr;
+  if (z) {
+    if ((s = get((void**)&Pc, sizeof(int2) * G * UCAP)) != AFN_OK) return s;
+    if ((s = get((void**)&Pcount, sizeof(int) * G)) != AFN_OK) return s;
+    if ((s = get((void**)&zwork, sizeof(unsigned long long))) != AFN_OK) return s;
+    AFN_CUDA(cudaMemsetAsync(zwork, 0, sizeof(unsigned long long), st));
+  }
   {
-    const int bytes = (int)(sizeof(int) * HC);
-    static bool uattr = false;
-    if (!uattr) {
-      AFN_CUDA(cudaFuncSetAttribute(group_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      uattr = true;
+    if (z) {
+      const int bytes = (int)(sizeof(int) * 4 * HC);
+      AFN_CUDA(cudaFuncSetAttribute(group_union_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      group_union_kernel<true><<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi, GA,
+                                                                 Ucount, Ulist, Htab, ovf, z->tilerow, z->uoff, Pc,
+                                                                 Pcount, zwork);
+    } else {
+      const int bytes = (int)(sizeof(int) * HC);
+      AFN_CUDA(cudaFuncSetAttribute(group_union_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+      group_union_kernel<false><<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi,
+                                                                  GA, Ucount, Ulist, Htab, ovf, nullptr, nullptr,
+                                                                  nullptr, nullptr, nullptr);
     }
-    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi, GA,
-                                                         Ucount, Ulist, Htab, ovf);
     AFN_LAUNCH_CHECK("group_union_kernel");
   }
   int hov = 0;
+  unsigned long long hzw = 0ull;
   AFN_CUDA(cudaMemcpyAsync(&hov, ovf, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (z) AFN_CUDA(cudaMemcpyAsync(&hzw, zwork, sizeof(hzw), cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaStreamSynchronize(st));
   if (hov) {
     set_error("fsai_sddmm: pair union exceeds %d in a group", UCAP);
@@ -974,7 +1255,25 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
     cudaEventDestroy(ej);
   }
   st = mst;
-  {
+  if (z) {
+    kt_begin(KT_FSAI_GEMM, st);
+    // staged when the group's landmark columns fit: sparse landmarks (k / N,
+    // landmarks per unit volume, small: C5 8000 / 2^20); C3 (4000 / 2^17)
+    // unions of ~1300-2500 columns mostly do not
+    if (z->staged) {
+      const int zb = (int)(sizeof(double) * ZH * ZCAP);
+      AFN_CUDA(cudaFuncSetAttribute(group_zk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, zb));
+      group_zk_kernel<true><<<(unsigned)(2 * G), 256, zb, st>>>(sorder, N, z->Zp, k, z->tilerow, z->uoff, z->ulistp,
+                                                                z->aoff, z->Ap, Ucount, Ulist, Doff, Pc, Pcount, D, X2,
+                                                                d, kf, mu);
+    } else {
+      group_zk_kernel<false><<<(unsigned)(ZS * G), 256, 0, st>>>(sorder, N, z->Zp, k, z->tilerow, z->uoff, z->ulistp,
+                                                                 z->aoff, z->Ap, Ucount, Ulist, Doff, Pc, Pcount, D,
+                                                                 X2, d, kf, mu);
+    }
+    AFN_LAUNCH_CHECK("group_zk_kernel");
+    kt_end(KT_FSAI_GEMM, st, 2.0 * (double)hzw);
+  } else {
     kt_begin(KT_FSAI_GEMM, st);
     if (items > 0) {
       const bool wide = (double)N * (double)k * sizeof(double) > 512e6;  // W a few L2s or more

@@ -88,9 +88,12 @@ __global__ void __launch_bounds__(256) wc_count_kernel(const double* __restrict_
 
 // U_t ascending into ulist[uoff[t] ..]; *work += the tile's executed MACs
 // (64 rows x 64 columns x the K range of every column block)
+// (lmap: the landmarks in the order lmap[0..k) -- the list then holds those
+// positions, ascending; null: landmark ids ascending)
 __global__ void __launch_bounds__(256) wc_fill_kernel(const double* __restrict__ box, const double* __restrict__ X1,
                                                       int64_t k, int d, double thr, const int64_t* __restrict__ uoff,
-                                                      int* __restrict__ ulist, unsigned long long* __restrict__ work) {
+                                                      const int* __restrict__ lmap, int* __restrict__ ulist,
+                                                      unsigned long long* __restrict__ work) {
   __shared__ int wtot[8];
   __shared__ int64_t base;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(256) wc_fill_kernel(const double* __restrict__
   unsigned long long wk = 0ull;
   for (int64_t j0 = 0; j0 < k; j0 += 256) {
     const int64_t j = j0 + threadIdx.x;
-    const bool kp = j < k && wc_keep(b, X1 + j * d, d, thr);
+    const bool kp = j < k && wc_keep(b, X1 + (lmap ? (int64_t)lmap[j] : j) * d, d, thr);
     const unsigned m = __ballot_sync(0xffffffffu, kp);
     if (lane == 0) wtot[wid] = __popc(m);
     __syncthreads();
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(256) wc_fill_kernel(const double* __restrict__
     for (int w = 0; w < wid; ++w) off += wtot[w];
     if (kp) {
       ulist[off + __popc(m & ((1u << lane) - 1u))] = (int)j;
-      wk += (unsigned long long)(ncb - j / WN) * WM * WN;
+      wk += lmap ? (unsigned long long)ncb * WM * WN : (unsigned long long)(ncb - j / WN) * WM * WN;
     }
     __syncthreads();
     if (threadIdx.x == 0)
@@ -118,15 +121,15 @@ __global__ void __launch_bounds__(256) wc_fill_kernel(const double* __restrict__
     __syncthreads();
   }
   for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
-  if (lane == 0) atomicAdd(work, wk);
+  if (lane == 0 && work) atomicAdd(work, wk);
 }
 
 // A_t[r][m] = K(x_{sidx[64 t + r]}, x1_{U_t[m]}), ld = |U_t| rounded up to 2
 __global__ void __launch_bounds__(256) wc_gen_a_kernel(const double* __restrict__ Xr, int64_t N, int d,
                                                        const int* __restrict__ sidx, const double* __restrict__ X1,
                                                        const int64_t* __restrict__ uoff, const int* __restrict__ ulist,
-                                                       const int64_t* __restrict__ aoff, KernelFn kf, double thr,
-                                                       double* __restrict__ A) {
+                                                       const int* __restrict__ lmap, const int64_t* __restrict__ aoff,
+                                                       KernelFn kf, double thr, double* __restrict__ A) {
   __shared__ double s_tab[AFN_EXP2_TAB_N];
   load_exp2_tab(s_tab);
   __syncthreads();
@@ -141,17 +144,36 @@ __global__ void __launch_bounds__(256) wc_gen_a_kernel(const double* __restrict_
     if (p < N && m < nu) {
       // a pair beyond the bound contributes nothing on any tiling: a row's
       // terms are exactly {j : ||x_r - x_j||^2 < thr}
-      const double d2 = d2_exact_rt(&Xr[(int64_t)sidx[p] * d], &X1[(int64_t)ulist[u0 + m] * d], d);
+      const int j = lmap ? lmap[ulist[u0 + m]] : ulist[u0 + m];
+      const double d2 = d2_exact_rt(&Xr[(int64_t)sidx[p] * d], &X1[(int64_t)j * d], d);
       if (d2 < thr) v = kern_from_d2(kf, d2, s_tab);
     }
     At[e] = v;
   }
 }
 
+// point -> (its tile << 6) | its row in the tile
+__global__ void wc_tilerow_kernel(const int* __restrict__ sidx, int64_t N, int* __restrict__ tilerow) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < N) tilerow[sidx[p]] = (int)p;  // (64-row tiles: p = 64 t + r)
+}
+
+// Mp[p][q] = M[lp[p]][lp[q]]
+__global__ void wc_perm_sq_kernel(const double* __restrict__ M, int64_t k, const int* __restrict__ lp,
+                                  double* __restrict__ Mp) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= k * k) return;
+  const int64_t p = e / k, q = e - p * k;
+  Mp[e] = M[(int64_t)lp[p] * k + lp[q]];
+}
+
 // W rows of tile t, columns [64 c, 64 c + 64): A_t (64 x kc) times the rows
 // U_t[0..kc) of L^{-T}, kc = #{m : U_t[m] < 64 c + 64}.  CTA tile 64 x 64,
 // 4 warps of 32 x 32 (4 x 4 DMMA m8n8 tiles), k-chunks of 16 through 3
 // cp.async stages (A at a 20-double, B at a 72-double row stride).
+// TRI = false (Z = K21 M over the landmark order of the lists): every kept
+// landmark contributes to every column block
+template <bool TRI>
 __global__ void __launch_bounds__(128) wc_gemm_kernel(const double* __restrict__ A, const int64_t* __restrict__ aoff,
                                                       const int64_t* __restrict__ uoff, const int* __restrict__ ulist,
                                                       const double* __restrict__ LinvT, int64_t k,
@@ -166,8 +188,8 @@ __global__ void __launch_bounds__(128) wc_gemm_kernel(const double* __restrict__
   const int64_t lda = (nu + 1) & ~(int64_t)1;
   const double* At = A + aoff[t];
   const int* U = ulist + u0;
-  int64_t kc;
-  {  // first m with U[m] >= C0 + WN
+  int64_t kc = nu;
+  if (TRI) {  // first m with U[m] >= C0 + WN
     int64_t lo = 0, hi = nu;
     while (lo < hi) {
       const int64_t mid = (lo + hi) / 2;
@@ -270,7 +292,7 @@ void w_cut_free(WCutPlan* p) {
 }
 
 afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, int d, Kern kn, bool force,
-                      cudaStream_t st, WCutPlan* p) {
+                      bool zmode, cudaStream_t st, WCutPlan* p) {
   w_cut_free(p);
   p->used = false;
   p->st = st;
@@ -324,15 +346,30 @@ afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, 
   AFN_CUDA(cudaMemcpyAsync(p->uoff, ho.data(), sizeof(int64_t) * ho.size(), cudaMemcpyHostToDevice, st));
   AFN_CUDA(cudaMemcpyAsync(p->aoff, ha.data(), sizeof(int64_t) * ha.size(), cudaMemcpyHostToDevice, st));
   AFN_CUDA(cudaMemsetAsync(work, 0, sizeof(unsigned long long), st));
-  wc_fill_kernel<<<(unsigned)nt, 256, 0, st>>>(box, X1, k, d, thr, p->uoff, p->ulist, work);
+  wc_fill_kernel<<<(unsigned)nt, 256, 0, st>>>(box, X1, k, d, thr, p->uoff, nullptr, p->ulist, work);
   AFN_LAUNCH_CHECK("wc_fill_kernel");
-  wc_gen_a_kernel<<<(unsigned)nt, 256, 0, st>>>(Xr, N, d, p->sidx, X1, p->uoff, p->ulist, p->aoff,
+  wc_gen_a_kernel<<<(unsigned)nt, 256, 0, st>>>(Xr, N, d, p->sidx, X1, p->uoff, p->ulist, nullptr, p->aoff,
                                                 kernel_fn(kn.kind, kn.l), thr, p->A);
+  if (zmode) {  // the same lists and tiles over the landmarks' Morton order (Z = K21 M, fsai_sddmm.cu)
+    TRY_STATUS(get((void**)&p->lp, sizeof(int) * k, true));
+    TRY_STATUS(get((void**)&p->ulistp, sizeof(int) * std::max<int64_t>(1, ho[nt]), true));
+    TRY_STATUS(get((void**)&p->Ap, sizeof(double) * std::max<int64_t>(1, ha[nt]), true));
+    TRY_STATUS(get((void**)&p->tilerow, sizeof(int) * N, true));
+    TRY_STATUS(morton_order(X1, k, d, p->lp, st));
+    wc_fill_kernel<<<(unsigned)nt, 256, 0, st>>>(box, X1, k, d, thr, p->uoff, p->lp, p->ulistp, nullptr);
+    AFN_LAUNCH_CHECK("wc_fill_kernel");
+    wc_gen_a_kernel<<<(unsigned)nt, 256, 0, st>>>(Xr, N, d, p->sidx, X1, p->uoff, p->ulistp, p->lp, p->aoff,
+                                                  kernel_fn(kn.kind, kn.l), thr, p->Ap);
+    AFN_LAUNCH_CHECK("wc_gen_a_kernel");
+    wc_tilerow_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(p->sidx, N, p->tilerow);
+    AFN_LAUNCH_CHECK("wc_tilerow_kernel");
+  }
   AFN_LAUNCH_CHECK("wc_gen_a_kernel");
   unsigned long long hw = 0ull;
   AFN_CUDA(cudaMemcpyAsync(&hw, work, sizeof(hw), cudaMemcpyDeviceToHost, st));
   AFN_CUDA(cudaStreamSynchronize(st));  // (pageable copies; temporaries freed on return)
   p->flops = 2.0 * (double)hw;
+  p->zflops = 2.0 * WM * (double)((k + WN - 1) / WN * WN) * (double)ho[nt];
   p->k = k;
   p->N = N;
   p->nt = nt;
@@ -346,19 +383,38 @@ afn_status w_cut_run(WCutPlan* p, const double* LinvT, double* W, cudaStream_t s
     return AFN_ERR_STATE;
   }
   const int smem = (int)(sizeof(double) * WS * (WM * WKP + WK * WNP));
-  AFN_CUDA(cudaFuncSetAttribute(wc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  AFN_CUDA(cudaFuncSetAttribute(wc_gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid((unsigned)((p->k + WN - 1) / WN), (unsigned)p->nt);
-  wc_gemm_kernel<<<grid, 128, smem, st>>>(p->A, p->aoff, p->uoff, p->ulist, LinvT, p->k, p->sidx, p->N, W);
+  wc_gemm_kernel<true><<<grid, 128, smem, st>>>(p->A, p->aoff, p->uoff, p->ulist, LinvT, p->k, p->sidx, p->N, W);
   AFN_LAUNCH_CHECK("wc_gemm_kernel");
   p->st = st;  // (the plan's memory is released in this stream's order)
-  w_cut_free(p);
+  if (!p->lp) w_cut_free(p);  // (Z mode: kept for w_cut_z and the FSAI products)
+  return AFN_OK;
+}
+
+afn_status w_cut_z(WCutPlan* p, const double* LinvT, const double* Linv, double* M, double* Mp, double* Zp,
+                   cudaStream_t st) {
+  if (!p->used || !p->lp) {
+    set_error("w_cut_z: no Z-mode plan");
+    return AFN_ERR_STATE;
+  }
+  const int64_t k = p->k;
+  TRY_STATUS(gemm_upper_lower(LinvT, Linv, k, M, st));  // M = L^{-T} L^{-1} = (K11 + mu I)^{-1}
+  wc_perm_sq_kernel<<<(unsigned)((k * k + 255) / 256), 256, 0, st>>>(M, k, p->lp, Mp);
+  AFN_LAUNCH_CHECK("wc_perm_sq_kernel");
+  const int smem = (int)(sizeof(double) * WS * (WM * WKP + WK * WNP));
+  AFN_CUDA(cudaFuncSetAttribute(wc_gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid((unsigned)((k + WN - 1) / WN), (unsigned)p->nt);
+  wc_gemm_kernel<false><<<grid, 128, smem, st>>>(p->Ap, p->aoff, p->uoff, p->ulistp, Mp, k, p->sidx, p->N, Zp);
+  AFN_LAUNCH_CHECK("wc_gemm_kernel<false>");
+  p->st = st;
   return AFN_OK;
 }
 
 afn_status w_gemm_cut(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d, Kern kn,
                       double* W, cudaStream_t st, bool force, bool* used, double* flops) {
   WCutPlan p;
-  afn_status s = w_cut_plan(X1, k, Xr, N, d, kn, force, st, &p);
+  afn_status s = w_cut_plan(X1, k, Xr, N, d, kn, force, false, st, &p);
   if (s != AFN_OK) {
     w_cut_free(&p);
     return s;
