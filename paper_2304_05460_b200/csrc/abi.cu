@@ -86,6 +86,21 @@ struct Deferred {
   cudaEvent_t ev;
 };
 std::vector<Deferred> g_deferred;
+// Large blocks (>= 32 MB: W, Z, the FSAI products, the K21 tiles...) are kept
+// by the library after their free and handed out again once the free has
+// completed on the GPU: a stream-ordered pool allocation that finds no block
+// it may reuse (frees still pending on another stream) can block the host
+// while the driver reclaims memory -- measured up to 200 ms inside a 100 ms
+// C3 build, at random.  Reuse needs no wait and no cross-stream dependency.
+constexpr size_t BIG_BLOCK = (size_t)32 << 20;
+struct BigBlk {
+  void* p;
+  size_t bytes;
+  cudaEvent_t ev;
+  int dev;
+};
+std::vector<BigBlk> g_big;                          // freed, awaiting reuse
+std::unordered_map<void*, std::pair<size_t, int>> g_big_live;  // handed out: size, device
 }  // namespace
 
 void release_deferred(bool wait) {
@@ -107,7 +122,7 @@ void release_deferred(bool wait) {
 
 afn_status dalloc(void** p, size_t bytes, cudaStream_t st) {
   *p = nullptr;
-  const size_t nb = bytes > 0 ? bytes : 8;
+  size_t nb = bytes > 0 ? bytes : 8;
   {
     std::unique_lock<std::mutex> lk(g_alloc_mu);
     if (g_alloc) {
@@ -124,13 +139,67 @@ afn_status dalloc(void** p, size_t bytes, cudaStream_t st) {
     }
   }
   pool_setup_once();
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (nb >= BIG_BLOCK) {  // size classes 2^m (1 + j/8): a build's sizes vary a little run to run
+    int m = 0;
+    while (((size_t)1 << (m + 1)) <= nb) ++m;
+    const size_t step = (size_t)1 << (m - 3);
+    nb = (nb + step - 1) / step * step;
+  }
+  if (nb >= BIG_BLOCK) {  // a completed large block of 1 - 1.5x the size
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    int best = -1;
+    for (int i = 0; i < (int)g_big.size(); ++i) {
+      const BigBlk& b = g_big[i];
+      if (b.dev != dev || b.bytes < nb || b.bytes > nb + nb / 2) continue;
+      if (best >= 0 && b.bytes >= g_big[best].bytes) continue;
+      if (cudaEventQuery(b.ev) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      best = i;
+    }
+    if (best >= 0) {
+      BigBlk b = g_big[best];
+      g_big.erase(g_big.begin() + best);
+      cudaEventDestroy(b.ev);
+      g_big_live[b.p] = {b.bytes, dev};
+      *p = b.p;
+      return AFN_OK;
+    }
+  }
   cudaError_t e = cudaMallocAsync(p, nb, st);
+  if (e != cudaSuccess && nb >= BIG_BLOCK) {  // cached blocks back to the pool, then retry
+    cudaGetLastError();
+    trim_big_blocks();
+    e = cudaMallocAsync(p, nb, st);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     set_error("device allocation of %zu bytes failed (%s)", bytes, cudaGetErrorString(e));
     return AFN_ERR_NOMEM;
   }
+  if (nb >= BIG_BLOCK) {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    g_big_live[*p] = {nb, dev};
+  }
   return AFN_OK;
+}
+
+void trim_big_blocks() {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (BigBlk& b : g_big) {
+    cudaSetDevice(b.dev);
+    cudaEventSynchronize(b.ev);
+    cudaEventDestroy(b.ev);
+    cudaFree(b.p);  // (pool memory: returns it to the pool)
+  }
+  g_big.clear();
+  cudaSetDevice(cur);
+  cudaGetLastError();
 }
 
 void dfree(void* p, cudaStream_t st) {
@@ -151,6 +220,17 @@ void dfree(void* p, cudaStream_t st) {
         if (g_free) g_free(p, f.bytes, (void*)st, g_alloc_ctx);
       }
       return;
+    }
+    auto bl = g_big_live.find(p);
+    if (bl != g_big_live.end()) {  // kept for reuse once this free completes
+      BigBlk b{p, bl->second.first, nullptr, bl->second.second};
+      g_big_live.erase(bl);
+      if (cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) == cudaSuccess && cudaEventRecord(b.ev, st) == cudaSuccess) {
+        g_big.push_back(b);
+        return;
+      }
+      cudaGetLastError();
+      if (b.ev) cudaEventDestroy(b.ev);
     }
   }
   cudaFreeAsync(p, st);
@@ -1080,7 +1160,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     // (Z mode: one rank, AFN -- the FSAI products through Z = K21 M)
     if (!nys && k > 0 && N2 > 0 && s.hi > s.lo && kmv_get_mode() != 1)
       TRY(w_cut_plan(s.Xp, k, s.Xp + (k + s.lo) * d, s.hi - s.lo, d, kn, kmv_get_mode() == 2,
-                     h->R == 1 && povl && k <= 8192, st, &wplan[q]));
+                     h->R == 1 && povl && k <= 8192 && kmv_get_mode() != 3, st, &wplan[q]));
     return AFN_OK;
   };
 
@@ -2034,7 +2114,7 @@ afn_status afn_probe_ex2(int64_t iters, double* gops, void* stream) {
 }
 
 afn_status afn_set_cutoff_mode(int32_t mode) {
-  REQ(mode >= 0 && mode <= 2, "cutoff mode %d (0 auto, 1 never, 2 whenever it applies)", mode);
+  REQ(mode >= 0 && mode <= 3, "cutoff mode %d (0 auto, 1 never, 2 whenever it applies, 3 auto without Z)", mode);
   kmv_set_mode(mode);
   return AFN_OK;
 }

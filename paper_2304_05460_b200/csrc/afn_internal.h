@@ -79,6 +79,9 @@ void kt_collect();                                  // after a stream sync
 afn_status dalloc(void** p, size_t bytes, cudaStream_t st);
 void dfree(void* p, cudaStream_t st);
 void release_deferred(bool wait);
+// return the library's cached large blocks to the pool (afn_pool_stats and
+// allocation failures call it)
+void trim_big_blocks();
 
 // ---- kernel matvec (kmv.cu) ----------------------------------------------
 struct KmvPlan {

@@ -52,6 +52,7 @@ namespace {
 constexpr int GA = 32;
 constexpr int UCAP = 4096;   // max |U_g|
 constexpr int HC = 8192;     // hash capacity (power of two)
+constexpr int TH = HC;       // tile-table capacity of the Z-mode unions (>= 2 |U_g|: never full)
 
 __device__ __forceinline__ void cpa8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -307,31 +308,45 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
   }
   constexpr int PER = HC / 256;
   if (TILE) {
-    int* tk = hs + HC;      // tile keys
-    int* tc = hs + 2 * HC;  // counts, then running cursors
-    int* to = hs + 3 * HC;  // offsets
-    for (int t = tid; t < HC; t += 256) {
+    // a union's points lie in at most a few hundred tiles: a TH-slot table
+    // (an overfull one flags the group: the per-row Gram fallback)
+    int* tk = hs + HC;       // tile keys
+    int* tc = hs + HC + TH;  // counts, then offsets + running cursors
+    __shared__ int s_tn;
+    for (int t = tid; t < TH; t += 256) {
       tk[t] = -1;
       tc[t] = 0;
     }
+    if (tid == 0) s_tn = 0;
     __syncthreads();
     auto tslot = [&](int tile, bool ins) {
-      unsigned h = ((unsigned)tile * 2654435761u) & (HC - 1);
-      for (;;) {
+      unsigned h = ((unsigned)tile * 2654435761u) & (TH - 1);
+      for (int probe = 0; probe < TH; ++probe) {
         const int old = ins ? atomicCAS(&tk[h], -1, tile) : tk[h];
-        if (old == -1 || old == tile) return (int)h;
-        h = (h + 1) & (HC - 1);
+        if (old == tile) return (int)h;
+        if (old == -1) {
+          if (ins && atomicAdd(&s_tn, 1) >= TH / 2) s_ovf = 1;
+          return (int)h;
+        }
+        h = (h + 1) & (TH - 1);
       }
+      s_ovf = 1;
+      return 0;
     };
     for (int slot = tid; slot < HC; slot += 256) {
       const int pb = hs[slot];
       if (pb >= 0) atomicAdd(&tc[tslot(tilerow[sorder[pb]] >> 6, true)], 1);
     }
     __syncthreads();
+    if (s_ovf) {
+      if (tid == 0) atomicExch(overflow, 1);
+      return;
+    }
     // offsets (columns) and piece offsets in slot order
+    constexpr int TPER = TH / 256;
     int cc = 0, pp = 0;
-    for (int t = 0; t < PER; ++t) {
-      const int c1 = tc[tid * PER + t];
+    for (int t = 0; t < TPER; ++t) {
+      const int c1 = tc[tid * TPER + t];
       cc += c1;
       pp += (c1 + 31) / 32;
     }
@@ -355,10 +370,10 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     }
     int prun = s_scan[tid] - pp;
     unsigned long long wk = 0ull;
-    for (int t = 0; t < PER; ++t) {
-      const int slot = tid * PER + t;
+    for (int t = 0; t < TPER; ++t) {
+      const int slot = tid * TPER + t;
       const int c1 = tc[slot];
-      to[slot] = run;
+      tc[slot] = run;
       if (c1 > 0) {
         const int tile = tk[slot];
         wk += (unsigned long long)c1 * (unsigned long long)(uoff[tile + 1] - uoff[tile]);
@@ -370,14 +385,12 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
     if (lane == 0) atomicAdd(zwork, wk * (unsigned long long)GA);
     __syncthreads();
-    for (int t = tid; t < HC; t += 256) tc[t] = 0;
-    __syncthreads();
     int2* H = Htab + g * HC;
     for (int slot = tid; slot < HC; slot += 256) {
       const int pb = hs[slot];
       if (pb >= 0) {
         const int ts = tslot(tilerow[sorder[pb]] >> 6, false);
-        const int u = to[ts] + atomicAdd(&tc[ts], 1);
+        const int u = atomicAdd(&tc[ts], 1);
         Ulist[g * UCAP + u] = sorder[pb];
         H[slot] = make_int2(pb, u);
       } else {
@@ -696,11 +709,12 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
                                                           : -1;  // (a zero column for this group)
       }
       __syncwarp();
-      for (int k4 = 0; k4 < cn; k4 += 4) {
+      // fragments of step k4 + 4 are loaded while step k4's DMMAs run
+      double av[MTL], bv[4];
+      auto fetch = [&](int k4) {
         const int m = k4 + fk;
         const bool ok = m < cn;
         const int col = ok ? s_u[wid][m] : -1;
-        double av[MTL], bv[4];
 #pragma unroll
         for (int mt = 0; mt < MTL; ++mt)
           av[mt] = (col >= 0 && arow[mt] >= 0)
@@ -708,11 +722,20 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
                        : 0.0;
 #pragma unroll
         for (int n = 0; n < 4; ++n) bv[n] = (ok && bid[n] >= 0) ? __ldg(&At[(int64_t)brow[n] * ld + c0 + m]) : 0.0;
+      };
+      fetch(0);
+      for (int k4 = 0; k4 < cn; k4 += 4) {
+        double ac[MTL], bc[4];
+#pragma unroll
+        for (int mt = 0; mt < MTL; ++mt) ac[mt] = av[mt];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) bc[n] = bv[n];
+        if (k4 + 4 < cn) fetch(k4 + 4);
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
           if (n >= nn) break;
 #pragma unroll
-          for (int mt = 0; mt < MTL; ++mt) dmma884(acc[mt][n][0], acc[mt][n][1], av[mt], bv[n]);
+          for (int mt = 0; mt < MTL; ++mt) dmma884(acc[mt][n][0], acc[mt][n][1], ac[mt], bc[n]);
         }
       }
     }
@@ -1204,7 +1227,7 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
   }
   {
     if (z) {
-      const int bytes = (int)(sizeof(int) * 4 * HC);
+      const int bytes = (int)(sizeof(int) * (HC + 2 * TH));
       AFN_CUDA(cudaFuncSetAttribute(group_union_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
       group_union_kernel<true><<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi, GA,
                                                                  Ucount, Ulist, Htab, ovf, z->tilerow, z->uoff, Pc,

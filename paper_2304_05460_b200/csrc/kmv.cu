@@ -677,10 +677,39 @@ __global__ void kc_tplace_kernel(const unsigned* __restrict__ it, int64_t E, con
   const unsigned t = it[e] & ~KC_F32;
   tu[tptr[t] + atomicAdd(&cur[t], 1)] = (int)e;
 }
-__global__ void kc_tsort_kernel(const int64_t* __restrict__ tptr, int64_t ntiles, int* __restrict__ tu) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= ntiles) return;
+// one block per tile: bitonic sort in shared memory (lists up to 1024; the
+// rare longer one by thread 0's insertion sort)
+__global__ void __launch_bounds__(256) kc_tsort_kernel(const int64_t* __restrict__ tptr, int64_t ntiles,
+                                                       int* __restrict__ tu) {
+  __shared__ int sv[1024];
+  const int64_t t = blockIdx.x;
   const int64_t b = tptr[t], e = tptr[t + 1];
+  const int len = (int)(e - b);
+  if (len <= 1) return;
+  if (len <= 1024) {
+    int p2 = 1;
+    while (p2 < len) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) sv[i] = i < len ? tu[b + i] : 0x7fffffff;
+    __syncthreads();
+    for (int kk = 2; kk <= p2; kk <<= 1)
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+          const int l = i ^ j;
+          if (l > i) {
+            const bool up = (i & kk) == 0;
+            const int x = sv[i], y = sv[l];
+            if ((x > y) == up) {
+              sv[i] = y;
+              sv[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) tu[b + i] = sv[i];
+    return;
+  }
+  if (threadIdx.x != 0) return;
   for (int64_t i = b + 1; i < e; ++i) {
     const int v = tu[i];
     int64_t j = i - 1;
@@ -1346,7 +1375,7 @@ afn_status cut_plan_make(const double* Xs, int64_t n, int d, int R, int rank, cu
   int* tu = reinterpret_cast<int*>(ws + p.o_tu);
   kc_tplace_kernel<<<nbe, 256, 0, st>>>(dit, E, tptr, tcur, tu);
   AFN_LAUNCH_CHECK("kc_tplace_kernel");
-  kc_tsort_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(tptr, ntiles, tu);
+  kc_tsort_kernel<<<(unsigned)ntiles, 256, 0, st>>>(tptr, ntiles, tu);
   AFN_LAUNCH_CHECK("kc_tsort_kernel");
   AFN_CUDA(cudaStreamSynchronize(st));  // (pageable sources; temporaries freed on return)
   *out = p;

@@ -22,7 +22,7 @@
 namespace afn {
 namespace {
 
-constexpr int WM = 64, WN = 64, WK = 16, WKP = 20, WNP = 72, WS = 3;
+constexpr int WM = 64, WN = 64, WK = 16, WKP = 20, WNP = 72, WS = 2;
 
 __device__ __forceinline__ void wc_cpa16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
