@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256, 2) group_gemm_dmma_kernel(
 // rows stay in L2 (one CTA per whole group: C3 28.5 ms, DRAM 46 GB).
 constexpr int ZH = 16;
 constexpr int ZCAP = 1664;  // staged columns (16 x 1664 x 8 B = 208 KB); wider U' -> global loads
-constexpr int ZS = 4;
+constexpr int ZS = 8;
 template <bool STAGED>
 __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ Zp, int64_t k,
