@@ -8,7 +8,8 @@ cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C3"]
 X, b = gen_problem(cfg)
 Xd, bd = torch.from_numpy(X).cuda(), torch.from_numpy(b).cuda()
 afn.set_cutoff_mode(int(sys.argv[3]) if len(sys.argv) > 3 else 0)
-prm = afn.make_params(cfg.ls[0], cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True)
+L = float(sys.argv[4]) if len(sys.argv) > 4 else cfg.ls[0]
+prm = afn.make_params(L, cfg.mu, cfg.k_cap, cfg.w, k_adaptive=True)
 for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 12):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
