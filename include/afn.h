@@ -333,8 +333,9 @@ afn_status afn_probe_ex2(int64_t iters, double* gops /*host*/, void* stream);
 /*   W = K21 L^{-T} in afn_build: terms with K21 entries < 2^-128 dropped,  */
 /*     per 64-row tile of a spatial order a dense product over the kept     */
 /*     landmarks.                                                            */
-/* mode 0 (default): each when it keeps at most half of the work, else the  */
-/* dense path; 1: never; 2: whenever it applies; 3: as 0 but the FSAI pair   */
+/* mode 0 (default): the cutoff matvec whenever it applies, the cutoff W    */
+/* when it keeps at most half of the landmarks per tile, else the dense     */
+/* paths; 1: never; 2: both whenever they apply; 3: as 0 but the FSAI pair  */
 /* products through W instead of Z = K21 (K11 + mu I)^{-1} (DESIGN.md 6.4;  */
 /* Z takes another (n - k) x k buffer during the build).  Other kernels /    */
 /* d > 3 / row ranges: the dense paths.  AFN_ERR_ARG for any other mode.     */

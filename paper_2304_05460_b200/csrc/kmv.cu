@@ -1276,7 +1276,9 @@ afn_status cut_plan_make(const double* Xs, int64_t n, int d, int R, int rank, cu
   }
   const int64_t E = gstart[ng], TW = wbase[ng];
   const double all_pairs = (double)n * (double)(n - 1) / 2.0;
-  if (g_kmv_mode == 0 && (double)(hp[0] + hp[1]) > 0.5 * all_pairs) return AFN_OK;
+  // (auto: always -- measured on C2 it is at least as fast as the dense
+  // symmetric plan for every l, 0.197 vs 0.199 ms even when no pair is skipped)
+  (void)all_pairs;
   if (E >= ((int64_t)1 << 31) || E < 1) return AFN_OK;
 
   KmvPlan p;

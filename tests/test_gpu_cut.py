@@ -95,7 +95,9 @@ def test_cut_matvec_classes_and_skips(mode):
     assert i1["kmv_pairs64"] > 0 and i1["kmv_pairs32"] > 0
     assert i1["kmv_pairs64"] + i1["kmv_pairs32"] < allp
     assert i01["kmv_pairs64"] + i01["kmv_pairs32"] < 0.5 * (i1["kmv_pairs64"] + i1["kmv_pairs32"])
-    mode(0)  # auto keeps the dense plan when the cut keeps more than half
+    mode(0)  # auto: the cutoff plan whenever it applies (C2: never slower)
+    assert _plan_of(Xd, 10.0)["kmv_plan"] == 2
+    mode(1)
     assert _plan_of(Xd, 10.0)["kmv_plan"] == 1
 
 

@@ -15,7 +15,7 @@ for cfg in cfgs:
     X, b = gen_problem(cfg)
     Xd, bd = torch.from_numpy(X).cuda(), torch.from_numpy(b).cuda()
     n = len(X)
-    for l in ((1.0, 2.0) if cfg == "C2" else (1.0,)):
+    for l in ((0.5, 1.0, 2.0, 5.0, 10.0) if cfg == "C2" else (1.0,)):
         res = {}
         for mode in (1, 2):
             if cfg == "C5" and mode == 1:
