@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
   __shared__ unsigned s_bits[256];   // k <= 8192 positions
   __shared__ int s_pre[257];         // prefix counts of s_bits
   __shared__ int s_u[8][256];        // per warp: the piece's U_t as staged columns
+  __shared__ long long s_pk[STAGED ? 1 : UCAP];  // !STAGED: (tile, piece) keys, sorted
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   load_exp2_tab(s_tab);
   constexpr int RH = STAGED ? ZH : GA;  // rows per CTA
@@ -676,7 +677,41 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
   int arow[MTL];
 #pragma unroll
   for (int mt = 0; mt < MTL; ++mt) arow[mt] = s_a[mt * 8 + fr];
-  for (int p = pq * 8 + wid; p < np; p += pstep) {
+  // !STAGED: the group's pieces sorted by tile (Morton: adjacent tiles,
+  // overlapping landmark lists), this CTA takes a contiguous 1/ZS of them and
+  // its warps consecutive ones -- warps running together read the same Z
+  // columns (L1)
+  int p_lo = 0, p_hi = np, p_st = pstep, p_first = pq * 8 + wid;
+  if (!STAGED) {
+    int p2 = 1;
+    while (p2 < np) p2 <<= 1;
+    for (int e = tid; e < p2; e += 256) {
+      s_pk[e] = e < np ? ((long long)(tilerow[Ulist[g * UCAP + Pc[g * UCAP + e].x]] >> 6) << 32) | e
+                       : 0x7fffffffffffffffll;
+    }
+    __syncthreads();
+    for (int kk = 2; kk <= p2; kk <<= 1)
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int e = tid; e < p2; e += 256) {
+          const int l = e ^ jj;
+          if (l > e) {
+            const bool up = (e & kk) == 0;
+            const long long x = s_pk[e], y = s_pk[l];
+            if ((x > y) == up) {
+              s_pk[e] = y;
+              s_pk[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    p_lo = (int)((int64_t)np * pq / ZS);
+    p_hi = (int)((int64_t)np * (pq + 1) / ZS);
+    p_st = 8;
+    p_first = p_lo + wid;
+  }
+  for (int pi = p_first; pi < p_hi; pi += p_st) {
+    const int p = STAGED ? pi : (int)(s_pk[pi] & 0xffffffff);
     const int2 pc = Pc[g * UCAP + p];
     const int u0 = pc.x, nb = pc.y;
     int bid[4], brow[4];
