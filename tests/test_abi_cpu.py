@@ -86,6 +86,26 @@ def test_host_pointers_are_rejected_without_compute(lib):
     assert st == 1
 
 
+def test_cutoff_mode_and_w_product_arguments(lib):
+    """afn_set_cutoff_mode takes 0..3 only; afn_w_product
+    returns AFN_ERR_ARG, without computing, for bad arguments (here host
+    pointers, an unknown method, the cutoff method with d > 3)."""
+    import ctypes as C
+    for m in (0, 1, 2, 3):
+        assert lib._lib.afn_set_cutoff_mode(m) == 0
+    for m in (-1, 4, 99):
+        assert lib._lib.afn_set_cutoff_mode(m) == 1  # AFN_ERR_ARG
+    assert lib._lib.afn_set_cutoff_mode(0) == 0
+    assert lib.WPROD_CUT == 2
+    # (host pointers: argument checks come first, no compute without a GPU)
+    import numpy as np
+    X1, Xr, Li, W = np.zeros((4, 3)), np.zeros((8, 3)), np.eye(4), np.zeros((8, 4))
+    P = lambda a: a.ctypes.data_as(C.c_void_p)
+    assert lib._lib.afn_w_product(P(X1), 4, P(Xr), 8, 3, 0, 1.0, P(Li), 7, P(W), None) == 1
+    X1b, Xrb = np.zeros((4, 5)), np.zeros((8, 5))
+    assert lib._lib.afn_w_product(P(X1b), 4, P(Xrb), 8, 5, 0, 1.0, P(Li), 2, P(W), None) == 1
+
+
 def test_binding_has_no_cpu_fallback():
     """The product package never imports the oracle and never computes on the host."""
     pkg = os.path.join(ROOT, "paper_2304_05460_b200")
