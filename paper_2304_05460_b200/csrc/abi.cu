@@ -449,6 +449,9 @@ struct RankSt {
   // local order), RinvT = R^{-T} with R R^T = mu I + F^T F
   double* F = nullptr;
   double* RinvT = nullptr;
+  // one rank, cutoff W: the K21 tiles of the W plan, kept for the apply
+  // (W t = K21 (L^{-T} t), W^T s = L^{-1} (K21^T s): DESIGN.md 6.6)
+  WCutPlan kt;
   // RAN (AFN_METHOD_RAN): R1invT = R1^{-T}, R1 R1^T = F^T F + nu I
   double* R1invT = nullptr;
   std::vector<void*> allocs;
@@ -561,8 +564,11 @@ void handle_free(afn_handle h) {
   // go back to the pool on the build stream (cudaFree would unmap them and
   // force the next build to map fresh pages) and are reusable from any stream
   cudaDeviceSynchronize();
-  for (auto& s : h->rk)
+  for (auto& s : h->rk) {
+    s.kt.st = h->stream;
+    w_cut_free(&s.kt);
     for (void* p : s.allocs) dfree(p, h->stream);
+  }
   cudaStreamSynchronize(h->stream);
   release_deferred(true);
   cudaSetDevice(cur);
@@ -668,6 +674,9 @@ afn_status matvec_perm(afn_handle h, VF v_of, QF q_of, int pq_slot, cudaStream_t
 // G and G^T (values + 4-byte columns) once each, plus the vectors
 double apply_bytes(afn_handle h) {
   const double k = (double)h->k, N2 = (double)h->N2, nnz = (double)h->nnz;
+  if (h->R == 1 && h->rk[0].kt.used)  // the K21 tiles twice, four triangles (L^{-1}, L^{-T} twice each)
+    return 8.0 * (2.0 * (double)h->rk[0].kt.Adbl + 2.0 * k * (k + 1.0)) + 2.0 * 12.0 * nnz +
+           8.0 * (6.0 * N2 + 10.0 * k);
   return 8.0 * (2.0 * N2 * k + k * (k + 1.0)) + 2.0 * 12.0 * nnz + 8.0 * (6.0 * N2 + 6.0 * k);
 }
 
@@ -684,8 +693,13 @@ afn_status apply_afn_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
   for (auto& s : h->rk) {
     const double* r = r_of(s);
     TRY(gemv_n(s.Linv, k, k, r, nullptr, 1.0, s.tvec, st, 2));
-    // u = r2 - W t (own rows)
-    if (s.hi > s.lo) TRY(gemv_n(s.W, s.hi - s.lo, k, s.tvec, r + k + s.lo, -1.0, s.uvec + s.lo, st));
+    // u = r2 - W t (own rows); one rank with the K21 tiles: r2 - K21 (L^{-T} t)
+    if (s.kt.used) {
+      TRY(gemv_n(s.LinvT, k, k, s.tvec, nullptr, 1.0, s.kpart, st, 1));
+      TRY(w_cut_apply_n(&s.kt, s.kpart, r + k, s.uvec, st));
+    } else if (s.hi > s.lo) {
+      TRY(gemv_n(s.W, s.hi - s.lo, k, s.tvec, r + k + s.lo, -1.0, s.uvec + s.lo, st));
+    }
   }
   if (N2 > 0) {
     TRY(exchange(h, [](RankSt& s) { return s.uvec; }, [&](int s) { return rows2_ranges(h, s, 8); }, st));
@@ -696,7 +710,10 @@ afn_status apply_afn_perm(afn_handle h, RF r_of, ZF z_of, cudaStream_t st) {
       double* z = z_of(s);
       // s2 = G^T y (own rows of G^T)
       TRY(spmv_csr(s.trp + s.lo, s.tcol, s.tval, s.hi - s.lo, s.yvec, z + k + s.lo, st));
-      if (R == 1) {  // v = t - W^T s2
+      if (R == 1 && s.kt.used) {  // v = t - L^{-1} (K21^T s2)
+        TRY(w_cut_apply_t(&s.kt, z + k, s.kpart, st));
+        TRY(gemv_n(s.Linv, k, k, s.kpart, s.tvec, -1.0, s.vvec, st, 2));
+      } else if (R == 1) {  // v = t - W^T s2
         TRY(gemv_t(s.W, N2, k, z + k, s.tvec, -1.0, s.vvec, s.gws, st));
       } else {       // rank partial of W^T s2
         double* kp = s.kpart + (size_t)s.rank * k;
@@ -1158,6 +1175,7 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     TRY(kmv_plan_make(s.Xs, n, s.own.size(), d, h->kn.kind, true, h->R, s.rank, st,
                       [&](double** qq, size_t c) { return ralloc(s, qq, c, st); }, &s.plan, &s.kmv_part));
     // (Z mode: one rank, AFN -- the FSAI products through Z = K21 M)
+    wplan[q].keep = h->R == 1 && povl;  // (the apply through the tiles)
     if (!nys && k > 0 && N2 > 0 && s.hi > s.lo && kmv_get_mode() != 1)
       TRY(w_cut_plan(s.Xp, k, s.Xp + (k + s.lo) * d, s.hi - s.lo, d, kn, kmv_get_mode() == 2,
                      h->R == 1 && povl && k <= 8192 && kmv_get_mode() != 3, st, &wplan[q]));
@@ -1397,8 +1415,14 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   }  // AFN / FSAI
 
   // ---- workspaces for apply / PCG
+  auto q_of = [&](RankSt& s) { return (int)(&s - &h->rk[0]); };
   for (auto& s : h->rk) {
     const int64_t nl = s.own.size();
+    if (wplan[q_of(s)].used && wplan[q_of(s)].keep) {  // the K21 tiles stay for the apply
+      s.kt = std::move(wplan[q_of(s)]);
+      wplan[q_of(s)] = WCutPlan{};
+      TRY(w_cut_apply_prep(&s.kt, st));
+    }
     if (!s.kmv_part)  // (normally made early, beside the Cholesky)
       TRY(kmv_plan_make(s.Xs, n, nl, d, h->kn.kind, true, h->R, s.rank, st,
                         [&](double** q, size_t c) { return ralloc(s, q, c, st); }, &s.plan, &s.kmv_part));

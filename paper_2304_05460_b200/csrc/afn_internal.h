@@ -209,9 +209,21 @@ struct WCutPlan {
   int *lp = nullptr, *ulistp = nullptr, *tilerow = nullptr;
   double* Ap = nullptr;
   double flops = 0.0, zflops = 0.0;  // executed flops of the W and Z products
+  int64_t E = 0;          // list entries over all tiles
+  int64_t Adbl = 0;       // doubles of the K21 tiles (A)
+  bool keep = false;      // keep the plan after W (the apply through the tiles)
+  int64_t* jptr = nullptr;  // apply: per landmark its list entries (jidx), and
+  int* jidx = nullptr;      // the per-entry column sums CT
+  double* CT = nullptr;
   std::vector<void*> mem;
   cudaStream_t st = nullptr;
 };
+// The AFN apply's two W products through the tiles (one rank): u = r2 - K21 y1
+// (rows by point) and w = K21^T s2 (fixed summation order); w_cut_apply_prep
+// builds the transposed lists once after the build.
+afn_status w_cut_apply_prep(WCutPlan* p, cudaStream_t st);
+afn_status w_cut_apply_n(const WCutPlan* p, const double* y1, const double* r2, double* u, cudaStream_t st);
+afn_status w_cut_apply_t(const WCutPlan* p, const double* s2, double* w, cudaStream_t st);
 afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, int d, Kern kn, bool force,
                       bool zmode, cudaStream_t st, WCutPlan* p);
 afn_status w_cut_run(WCutPlan* p, const double* LinvT, double* W, cudaStream_t st);

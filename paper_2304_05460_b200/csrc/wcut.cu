@@ -283,12 +283,179 @@ __global__ void __launch_bounds__(128) wc_gemm_kernel(const double* __restrict__
   }
 }
 
+// ---- the AFN apply through the tiles (W t = K21 (L^{-T} t), W^T s = L^{-1} (K21^T s))
+// u[i] = r2[i] - K21[i, :] y1: a warp per row (Morton position p), lanes over the tile's list
+__global__ void __launch_bounds__(256) wc_apply_n_kernel(const double* __restrict__ A, const int64_t* __restrict__ aoff,
+                                                         const int64_t* __restrict__ uoff, const int* __restrict__ ulist,
+                                                         const int* __restrict__ sidx, int64_t N,
+                                                         const double* __restrict__ y1, const double* __restrict__ r2,
+                                                         double* __restrict__ u, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= N) return;
+  const int64_t t = p >> 6;
+  const int r = (int)(p & 63);
+  const int64_t us = uoff[t];
+  const int nu = (int)(uoff[t + 1] - us);
+  const int ld = (nu + 1) & ~1;
+  const double* Ar = A + aoff[t] + (int64_t)r * ld;
+  const int* U = ulist + us;
+  double acc = 0.0;
+  for (int m = lane; m < nu; m += 32) acc = fma(Ar[m], __ldg(&y1[U[m]]), acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    const int i = sidx[p];
+    u[i] = r2[i] - acc;
+  }
+}
+// CT[uoff[t] + m] = sum_r K21[row r of t, U_t[m]] s2[row r] (a block per tile)
+__global__ void __launch_bounds__(256) wc_apply_t1_kernel(const double* __restrict__ A, const int64_t* __restrict__ aoff,
+                                                          const int64_t* __restrict__ uoff, const int* __restrict__ sidx,
+                                                          int64_t N, const double* __restrict__ s2,
+                                                          double* __restrict__ CT, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  __shared__ double ss[WM];
+  const int64_t t = blockIdx.x;
+  const int64_t us = uoff[t];
+  const int nu = (int)(uoff[t + 1] - us);
+  const int ld = (nu + 1) & ~1;
+  const double* At = A + aoff[t];
+  if (threadIdx.x < WM) {
+    const int64_t p = t * WM + threadIdx.x;
+    ss[threadIdx.x] = p < N ? s2[sidx[p]] : 0.0;
+  }
+  __syncthreads();
+  for (int m = threadIdx.x; m < nu; m += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < WM; ++r) acc = fma(At[(int64_t)r * ld + m], ss[r], acc);
+    CT[us + m] = acc;
+  }
+}
+// w[j] = sum of CT over the entries of landmark j (ascending): a warp per landmark
+__global__ void __launch_bounds__(256) wc_apply_t2_kernel(const int64_t* __restrict__ jptr, const int* __restrict__ jidx,
+                                                          int64_t k, const double* __restrict__ CT,
+                                                          double* __restrict__ w, const double* skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= k) return;
+  double acc = 0.0;
+  for (int64_t q = jptr[j] + lane; q < jptr[j + 1]; q += 32) acc += CT[jidx[q]];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) w[j] = acc;
+}
+// the transpose of the lists: per landmark its flat entries, ascending
+__global__ void wc_jcount_kernel(const int* __restrict__ ulist, int64_t E, int* __restrict__ cnt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < E) atomicAdd(&cnt[ulist[e]], 1);
+}
+__global__ void wc_jplace_kernel(const int* __restrict__ ulist, int64_t E, const int64_t* __restrict__ jptr,
+                                 int* __restrict__ cur, int* __restrict__ jidx) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < E) jidx[jptr[ulist[e]] + atomicAdd(&cur[ulist[e]], 1)] = (int)e;
+}
+__global__ void __launch_bounds__(256) wc_jsort_kernel(const int64_t* __restrict__ jptr, int* __restrict__ jidx) {
+  __shared__ int sv[2048];
+  const int64_t b = jptr[blockIdx.x], e = jptr[blockIdx.x + 1];
+  const int len = (int)(e - b);
+  if (len <= 1) return;
+  if (len <= 2048) {
+    int p2 = 1;
+    while (p2 < len) p2 <<= 1;
+    for (int i = threadIdx.x; i < p2; i += blockDim.x) sv[i] = i < len ? jidx[b + i] : 0x7fffffff;
+    __syncthreads();
+    for (int kk = 2; kk <= p2; kk <<= 1)
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+          const int l = i ^ jj;
+          if (l > i) {
+            const bool up = (i & kk) == 0;
+            const int x = sv[i], y = sv[l];
+            if ((x > y) == up) {
+              sv[i] = y;
+              sv[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int i = threadIdx.x; i < len; i += blockDim.x) jidx[b + i] = sv[i];
+    return;
+  }
+  if (threadIdx.x != 0) return;
+  for (int64_t i = b + 1; i < e; ++i) {
+    const int v = jidx[i];
+    int64_t q = i - 1;
+    while (q >= b && jidx[q] > v) {
+      jidx[q + 1] = jidx[q];
+      --q;
+    }
+    jidx[q + 1] = v;
+  }
+}
+
 }  // namespace
+
+afn_status w_cut_apply_prep(WCutPlan* p, cudaStream_t st) {
+  if (!p->used) {
+    set_error("w_cut_apply_prep: no plan");
+    return AFN_ERR_STATE;
+  }
+  const int64_t E = p->E, k = p->k;
+  int* cnt = nullptr;
+  TRY_STATUS(dalloc((void**)&p->jptr, sizeof(int64_t) * (k + 1), st));
+  p->mem.push_back(p->jptr);
+  TRY_STATUS(dalloc((void**)&p->jidx, sizeof(int) * std::max<int64_t>(1, E), st));
+  p->mem.push_back(p->jidx);
+  TRY_STATUS(dalloc((void**)&p->CT, sizeof(double) * std::max<int64_t>(1, E), st));
+  p->mem.push_back(p->CT);
+  TRY_STATUS(dalloc((void**)&cnt, sizeof(int) * 2 * k, st));
+  AFN_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * 2 * k, st));
+  const unsigned nbe = (unsigned)((E + 255) / 256);
+  if (E > 0) {
+    wc_jcount_kernel<<<nbe, 256, 0, st>>>(p->ulist, E, cnt);
+    AFN_LAUNCH_CHECK("wc_jcount_kernel");
+  }
+  TRY_STATUS(scan_i32_i64(cnt, k, p->jptr, st));
+  if (E > 0) {
+    wc_jplace_kernel<<<nbe, 256, 0, st>>>(p->ulist, E, p->jptr, cnt + k, p->jidx);
+    AFN_LAUNCH_CHECK("wc_jplace_kernel");
+  }
+  wc_jsort_kernel<<<(unsigned)k, 256, 0, st>>>(p->jptr, p->jidx);
+  AFN_LAUNCH_CHECK("wc_jsort_kernel");
+  dfree(cnt, st);
+  return AFN_OK;
+}
+
+afn_status w_cut_apply_n(const WCutPlan* p, const double* y1, const double* r2, double* u, cudaStream_t st) {
+  if (p->N <= 0) return AFN_OK;
+  wc_apply_n_kernel<<<(unsigned)((p->N + 7) / 8), 256, 0, st>>>(p->A, p->aoff, p->uoff, p->ulist, p->sidx, p->N, y1,
+                                                                  r2, u, get_skip());
+  AFN_LAUNCH_CHECK("wc_apply_n_kernel");
+  return AFN_OK;
+}
+
+afn_status w_cut_apply_t(const WCutPlan* p, const double* s2, double* w, cudaStream_t st) {
+  if (p->N > 0) {
+    wc_apply_t1_kernel<<<(unsigned)p->nt, 256, 0, st>>>(p->A, p->aoff, p->uoff, p->sidx, p->N, s2, p->CT, get_skip());
+    AFN_LAUNCH_CHECK("wc_apply_t1_kernel");
+  }
+  wc_apply_t2_kernel<<<(unsigned)((p->k + 7) / 8), 256, 0, st>>>(p->jptr, p->jidx, p->k, p->CT, w, get_skip());
+  AFN_LAUNCH_CHECK("wc_apply_t2_kernel");
+  return AFN_OK;
+}
 
 void w_cut_free(WCutPlan* p) {
   for (void* q : p->mem) dfree(q, p->st);
   p->mem.clear();
   p->used = false;
+  p->jptr = nullptr;
+  p->jidx = nullptr;
+  p->CT = nullptr;
 }
 
 afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, int d, Kern kn, bool force,
@@ -376,6 +543,8 @@ afn_status w_cut_plan(const double* X1, int64_t k, const double* Xr, int64_t N, 
   p->k = k;
   p->N = N;
   p->nt = nt;
+  p->E = ho[nt];
+  p->Adbl = ha[nt];
   p->used = true;
   return AFN_OK;
 }
@@ -391,7 +560,7 @@ afn_status w_cut_run(WCutPlan* p, const double* LinvT, double* W, cudaStream_t s
   wc_gemm_kernel<true><<<grid, 128, smem, st>>>(p->A, p->aoff, p->uoff, p->ulist, LinvT, p->k, p->sidx, p->N, W);
   AFN_LAUNCH_CHECK("wc_gemm_kernel");
   p->st = st;  // (the plan's memory is released in this stream's order)
-  if (!p->lp) w_cut_free(p);  // (Z mode: kept for w_cut_z and the FSAI products)
+  if (!p->lp && !p->keep) w_cut_free(p);  // (kept for w_cut_z / the FSAI products / the apply)
   return AFN_OK;
 }
 
