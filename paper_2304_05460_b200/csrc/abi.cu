@@ -1294,6 +1294,13 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   double w_work = 0.0;  // executed flops (dense: (N2/R) k^2 / 2 FMA per rank)
   for (int q = 0; q < nlocal; ++q) {
     RankSt& s = h->rk[q];
+    // one rank, Z mode: neither the FSAI products (Z) nor the apply (the K21
+    // tiles, §6.6) read W -- it is formed only on demand (copy-out, the per-row
+    // FSAI fallback) from the kept plan
+    if (wplan[q].used && wplan[q].lp && wplan[q].keep) {
+      Wf[q] = nullptr;
+      continue;
+    }
     TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
     const double* X2 = s.Xp + k * d;
     if (s.hi > s.lo) {
@@ -1380,6 +1387,10 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
       if (fs != AFN_OK && fs != AFN_ERR_STATE) return fs;
       if (fs != AFN_OK) {
         kt_begin(KT_FSAI_GRAM, st);
+        if (!Wf[q]) {  // (Z mode skipped W: form it now from the plan)
+          TRY(ralloc(s, &Wf[q], (size_t)(N2 > 0 ? N2 : 1) * k, st));
+          TRY(w_cut_run(&wplan[q], s.LinvT, Wf[q], st));
+        }
         TRY(fsai_run(X2, N2, d, kn, P.mu, Wf[q], k, s.rp, s.col, s.lo, s.hi, s.gval, s.dinfo + 1, st));
         kt_end(KT_FSAI_GRAM, st, 0.0);
       }
@@ -2073,9 +2084,19 @@ afn_status afn_get_info(afn_handle h, afn_info* info) {
   return AFN_OK;
 }
 
+// W on demand (one rank, Z mode: not formed by the build) from the kept plan
+static afn_status ensure_w(afn_handle h, RankSt& s) {
+  if (s.W || !s.kt.used || h->N2 <= 0) return AFN_OK;
+  TRY(ralloc(s, &s.W, (size_t)h->N2 * h->k, h->stream));
+  TRY(w_cut_run(&s.kt, s.LinvT, s.W, h->stream));
+  AFN_CUDA(cudaStreamSynchronize(h->stream));
+  return AFN_OK;
+}
+
 afn_status afn_copy_out_local(afn_handle h, int32_t local_rank, int32_t what, void* host, size_t bytes) {
   REQ(h && host, "null argument");
   REQ(local_rank >= 0 && local_rank < (int)h->rk.size(), "local rank %d out of range", local_rank);
+  if (what == AFN_OUT_W) TRY(ensure_w(h, h->rk[local_rank]));
   const RankSt& s = h->rk[local_rank];
   const void* src = nullptr;
   size_t need = 0;
@@ -2102,6 +2123,7 @@ afn_status afn_copy_out(afn_handle h, int32_t what, void* host, size_t bytes) {
 afn_status afn_copy_out_rows(afn_handle h, int32_t what, const int64_t* rows, int64_t nrows,
                              void* host, size_t bytes) {
   REQ(h && host && (rows || nrows == 0) && nrows >= 0, "null argument");
+  if (what == AFN_OUT_W) TRY(ensure_w(h, h->rk[0]));
   const RankSt& s = h->rk[0];
   const double* src = nullptr;
   int64_t lo = 0, hi = 0;
