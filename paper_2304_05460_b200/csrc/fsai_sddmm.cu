@@ -245,13 +245,6 @@ __global__ void group_maps_kernel(const int* __restrict__ sorder, int64_t N, int
 // list) and the global copy of the table H_g[slot] = (b, u) that the factor
 // kernel uses to find W_a . W_b in D_g (one or two probes).  A warp walks
 // one pattern row at a time, lanes over its entries.
-// TILE (the product through Z = K21 M, group_zk_kernel): the keys are
-// numbered grouped by the 64-point tile of the cutoff W plan that holds them
-// (tilerow[b] >> 6; any order inside a tile -- a value never depends on its
-// column), and the group's pieces (a tile's columns, <= 32 at a time) are
-// listed in Pc / Pcount; *zwork += the product's MACs (GA per column and
-// kept landmark of its tile).
-template <bool TILE>
 __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict__ sorder, int64_t N,
                                                           const int64_t* __restrict__ rp,
                                                           const int32_t* __restrict__ colp,
@@ -259,12 +252,8 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
                                                           const int32_t* __restrict__ tcol,
                                                           int64_t row_lo, int64_t row_hi, int ga,
                                                           int* __restrict__ Ucount, int* __restrict__ Ulist,
-                                                          int2* __restrict__ Htab, int* overflow,
-                                                          const int* __restrict__ tilerow,
-                                                          const int64_t* __restrict__ uoff, int2* __restrict__ Pc,
-                                                          int* __restrict__ Pcount,
-                                                          unsigned long long* __restrict__ zwork) {
-  extern __shared__ int hs[];  // HC keys (positions); TILE: + tile keys, counts, offsets (HC each)
+                                                          int2* __restrict__ Htab, int* overflow) {
+  extern __shared__ int hs[];  // HC keys (positions)
   __shared__ int s_n, s_ovf;
   __shared__ int s_scan[256];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -307,99 +296,6 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     return;
   }
   constexpr int PER = HC / 256;
-  if (TILE) {
-    // a union's points lie in at most a few hundred tiles: a TH-slot table
-    // (an overfull one flags the group: the per-row Gram fallback)
-    int* tk = hs + HC;       // tile keys
-    int* tc = hs + HC + TH;  // counts, then offsets + running cursors
-    __shared__ int s_tn;
-    for (int t = tid; t < TH; t += 256) {
-      tk[t] = -1;
-      tc[t] = 0;
-    }
-    if (tid == 0) s_tn = 0;
-    __syncthreads();
-    auto tslot = [&](int tile, bool ins) {
-      unsigned h = ((unsigned)tile * 2654435761u) & (TH - 1);
-      for (int probe = 0; probe < TH; ++probe) {
-        const int old = ins ? atomicCAS(&tk[h], -1, tile) : tk[h];
-        if (old == tile) return (int)h;
-        if (old == -1) {
-          if (ins && atomicAdd(&s_tn, 1) >= TH / 2) s_ovf = 1;
-          return (int)h;
-        }
-        h = (h + 1) & (TH - 1);
-      }
-      s_ovf = 1;
-      return 0;
-    };
-    for (int slot = tid; slot < HC; slot += 256) {
-      const int pb = hs[slot];
-      if (pb >= 0) atomicAdd(&tc[tslot(tilerow[sorder[pb]] >> 6, true)], 1);
-    }
-    __syncthreads();
-    if (s_ovf) {
-      if (tid == 0) atomicExch(overflow, 1);
-      return;
-    }
-    // offsets (columns) and piece offsets in slot order
-    constexpr int TPER = TH / 256;
-    int cc = 0, pp = 0;
-    for (int t = 0; t < TPER; ++t) {
-      const int c1 = tc[tid * TPER + t];
-      cc += c1;
-      pp += (c1 + 31) / 32;
-    }
-    s_scan[tid] = cc;
-    __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {
-      const int v = tid >= o ? s_scan[tid - o] : 0;
-      __syncthreads();
-      s_scan[tid] += v;
-      __syncthreads();
-    }
-    int run = s_scan[tid] - cc;
-    __syncthreads();
-    s_scan[tid] = pp;
-    __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {
-      const int v = tid >= o ? s_scan[tid - o] : 0;
-      __syncthreads();
-      s_scan[tid] += v;
-      __syncthreads();
-    }
-    int prun = s_scan[tid] - pp;
-    unsigned long long wk = 0ull;
-    for (int t = 0; t < TPER; ++t) {
-      const int slot = tid * TPER + t;
-      const int c1 = tc[slot];
-      tc[slot] = run;
-      if (c1 > 0) {
-        const int tile = tk[slot];
-        wk += (unsigned long long)c1 * (unsigned long long)(uoff[tile + 1] - uoff[tile]);
-        for (int q = 0; q < c1; q += 32) Pc[g * UCAP + prun++] = make_int2(run + q, min(32, c1 - q));
-      }
-      run += c1;
-    }
-    if (tid == 255) Pcount[g] = prun;
-    for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
-    if (lane == 0) atomicAdd(zwork, wk * (unsigned long long)GA);
-    __syncthreads();
-    int2* H = Htab + g * HC;
-    for (int slot = tid; slot < HC; slot += 256) {
-      const int pb = hs[slot];
-      if (pb >= 0) {
-        const int ts = tslot(tilerow[sorder[pb]] >> 6, false);
-        const int u = atomicAdd(&tc[ts], 1);
-        Ulist[g * UCAP + u] = sorder[pb];
-        H[slot] = make_int2(pb, u);
-      } else {
-        H[slot] = make_int2(-1, -1);
-      }
-    }
-    if (tid == 0) Ucount[g] = nu;
-    return;
-  }
   // number the occupied slots in slot order (block scan over 32-slot strips)
   int c = 0;
   for (int t = 0; t < PER; ++t) c += hs[tid * PER + t] >= 0;
@@ -425,6 +321,102 @@ __global__ void __launch_bounds__(256) group_union_kernel(const int* __restrict_
     }
   }
   if (tid == 0) Ucount[g] = nu;
+}
+
+// Z mode: renumber a group's union (already in its global hash table H_g,
+// slot -> (position, column)) grouped by W-plan tile, list the pieces (<= 32
+// columns of one tile) and count the products' MACs -- a separate pass, so
+// that the union kernel keeps its small shared-memory footprint (the pattern
+// walk is latency-bound: 96 KB per CTA there cost 8.4 vs ~3.4 ms at C3).
+__global__ void __launch_bounds__(256) group_tile_renumber_kernel(
+    const int* __restrict__ sorder, const int* __restrict__ Ucount, int* __restrict__ Ulist,
+    int2* __restrict__ Htab, const int* __restrict__ tilerow, const int64_t* __restrict__ uoff,
+    int2* __restrict__ Pc, int* __restrict__ Pcount, unsigned long long* __restrict__ zwork, int* overflow) {
+  extern __shared__ int ts[];  // tile keys [TH], counts -> offsets + cursors [TH]
+  __shared__ int s_scan[256];
+  __shared__ int s_ovf;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t g = blockIdx.x;
+  int* tk = ts;
+  int* tc = ts + TH;
+  for (int t = tid; t < TH; t += 256) {
+    tk[t] = -1;
+    tc[t] = 0;
+  }
+  if (tid == 0) s_ovf = 0;
+  __syncthreads();
+  int2* H = Htab + g * HC;
+  auto tslot = [&](int tile, bool ins) {
+    unsigned h = ((unsigned)tile * 2654435761u) & (TH - 1);
+    for (int probe = 0; probe < TH; ++probe) {
+      const int old = ins ? atomicCAS(&tk[h], -1, tile) : tk[h];
+      if (old == tile || old == -1) return (int)h;
+      h = (h + 1) & (TH - 1);
+    }
+    s_ovf = 1;
+    return 0;
+  };
+  for (int slot = tid; slot < HC; slot += 256) {
+    const int pb = H[slot].x;
+    if (pb >= 0) atomicAdd(&tc[tslot(tilerow[sorder[pb]] >> 6, true)], 1);
+  }
+  __syncthreads();
+  if (s_ovf) {
+    if (tid == 0) atomicExch(overflow, 1);
+    return;
+  }
+  constexpr int TPER = TH / 256;
+  int cc = 0, pp = 0;
+  for (int t = 0; t < TPER; ++t) {
+    const int c1 = tc[tid * TPER + t];
+    cc += c1;
+    pp += (c1 + 31) / 32;
+  }
+  s_scan[tid] = cc;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const int v = tid >= o ? s_scan[tid - o] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  int run = s_scan[tid] - cc;
+  __syncthreads();
+  s_scan[tid] = pp;
+  __syncthreads();
+  for (int o = 1; o < 256; o <<= 1) {
+    const int v = tid >= o ? s_scan[tid - o] : 0;
+    __syncthreads();
+    s_scan[tid] += v;
+    __syncthreads();
+  }
+  int prun = s_scan[tid] - pp;
+  unsigned long long wk = 0ull;
+  for (int t = 0; t < TPER; ++t) {
+    const int slot = tid * TPER + t;
+    const int c1 = tc[slot];
+    tc[slot] = run;
+    if (c1 > 0) {
+      const int tile = tk[slot];
+      wk += (unsigned long long)c1 * (unsigned long long)(uoff[tile + 1] - uoff[tile]);
+      for (int q = 0; q < c1; q += 32) Pc[g * UCAP + prun++] = make_int2(run + q, min(32, c1 - q));
+    }
+    run += c1;
+  }
+  if (tid == 255) Pcount[g] = prun;
+  for (int o = 16; o > 0; o >>= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
+  if (lane == 0) atomicAdd(zwork, wk * (unsigned long long)GA);
+  __syncthreads();
+  for (int slot = tid; slot < HC; slot += 256) {
+    const int2 e = H[slot];
+    if (e.x >= 0) {
+      const int ts2 = tslot(tilerow[sorder[e.x]] >> 6, false);
+      const int u = atomicAdd(&tc[ts2], 1);
+      Ulist[g * UCAP + u] = sorder[e.x];
+      H[slot] = make_int2(e.x, u);
+    }
+  }
+  (void)Ucount;
 }
 
 // ---------------------------------------------------------------- group GEMM
@@ -1261,20 +1253,18 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
     AFN_CUDA(cudaMemsetAsync(zwork, 0, sizeof(unsigned long long), st));
   }
   {
-    if (z) {
-      const int bytes = (int)(sizeof(int) * (HC + 2 * TH));
-      AFN_CUDA(cudaFuncSetAttribute(group_union_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      group_union_kernel<true><<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi, GA,
-                                                                 Ucount, Ulist, Htab, ovf, z->tilerow, z->uoff, Pc,
-                                                                 Pcount, zwork);
-    } else {
-      const int bytes = (int)(sizeof(int) * HC);
-      AFN_CUDA(cudaFuncSetAttribute(group_union_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-      group_union_kernel<false><<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi,
-                                                                  GA, Ucount, Ulist, Htab, ovf, nullptr, nullptr,
-                                                                  nullptr, nullptr, nullptr);
-    }
+    const int bytes = (int)(sizeof(int) * HC);
+    AFN_CUDA(cudaFuncSetAttribute(group_union_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    group_union_kernel<<<(unsigned)G, 256, bytes, st>>>(sorder, N, rp, colp, trp, tcol, row_lo, row_hi, GA, Ucount,
+                                                         Ulist, Htab, ovf);
     AFN_LAUNCH_CHECK("group_union_kernel");
+    if (z) {  // (Z mode: the unions renumbered by tile, the pieces listed)
+      const int rbytes = (int)(sizeof(int) * 2 * TH);
+      AFN_CUDA(cudaFuncSetAttribute(group_tile_renumber_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, rbytes));
+      group_tile_renumber_kernel<<<(unsigned)G, 256, rbytes, st>>>(sorder, Ucount, Ulist, Htab, z->tilerow, z->uoff, Pc,
+                                                                    Pcount, zwork, ovf);
+      AFN_LAUNCH_CHECK("group_tile_renumber_kernel");
+    }
   }
   int hov = 0;
   unsigned long long hzw = 0ull;
