@@ -230,7 +230,8 @@ afn_status w_cut_run(WCutPlan* p, const double* LinvT, double* W, cudaStream_t s
 afn_status w_cut_z(WCutPlan* p, const double* LinvT, const double* Linv, double* M, double* Mp, double* Zp,
                    cudaStream_t st);
 void w_cut_free(WCutPlan* p);
-// C = A B (k x k, row-major) for A upper and B lower triangular (dense.cu)
+// C = A B (k x k, row-major) for A = B^T upper, B lower triangular: the symmetric C's lower
+// block triangle only (entries above the diagonal tiles unwritten; dense.cu)
 afn_status gemm_upper_lower(const double* A, const double* B, int64_t k, double* C, cudaStream_t st);
 afn_status w_gemm(const double* LinvT, int64_t k, const double* X1, const double* Xr, int64_t N, int d,
                   Kern kn, double* W, cudaStream_t st);

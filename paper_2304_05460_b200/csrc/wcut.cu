@@ -158,13 +158,14 @@ __global__ void wc_tilerow_kernel(const int* __restrict__ sidx, int64_t N, int* 
   if (p < N) tilerow[sidx[p]] = (int)p;  // (64-row tiles: p = 64 t + r)
 }
 
-// Mp[p][q] = M[lp[p]][lp[q]]
+// Mp[p][q] = M[lp[p]][lp[q]] from M's lower triangle
 __global__ void wc_perm_sq_kernel(const double* __restrict__ M, int64_t k, const int* __restrict__ lp,
                                   double* __restrict__ Mp) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= k * k) return;
   const int64_t p = e / k, q = e - p * k;
-  Mp[e] = M[(int64_t)lp[p] * k + lp[q]];
+  const int64_t a = lp[p], b = lp[q];  // (M symmetric, its lower triangle formed)
+  Mp[e] = a >= b ? M[a * k + b] : M[b * k + a];
 }
 
 // W rows of tile t, columns [64 c, 64 c + 64): A_t (64 x kc) times the rows
