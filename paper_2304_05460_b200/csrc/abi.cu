@@ -1075,6 +1075,25 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
     }
     AFN_CUDA(cudaEventRecord(a1, s2));
     AFN_CUDA(cudaStreamWaitEvent(st, a1, 0));
+    // the cutoff matvec plan depends only on the point set: made now from the
+    // original points on the (idle) high-priority stream while FPS runs on a
+    // few SMs, its point indices remapped after the permutation
+    if (kn.kind == 0 && d <= 3 && n >= 4096 && kmv_get_mode() != 1) {
+      cudaStream_t ps = hp_stream();
+      for (auto& s : h->rk) {
+        double* Xs0 = nullptr;
+        TRY(dalloc((void**)&Xs0, sizeof(double) * (size_t)n * d, ps));
+        TRY(kmv_prescale(X, n, d, kn, Xs0, ps));
+        TRY(kmv_plan_make(Xs0, n, n, d, kn.kind, true, h->R, s.rank, ps,
+                          [&](double** qq, size_t c) { return ralloc(s, qq, c, ps); }, &s.plan, &s.kmv_part));
+        dfree(Xs0, ps);
+        if (!s.plan.cut) {  // (the dense plans read the permuted points: made later)
+          rfree(s, s.kmv_part, ps);
+          s.kmv_part = nullptr;
+          s.plan = KmvPlan{};
+        }
+      }
+    }
     AFN_CUDA(cudaEventSynchronize(a1));
     alg1_ms = ev_ms(a0, a1);
     k = std::min<int64_t>(P.k_cap, std::max<int64_t>(1, h->a1.khat));
@@ -1172,8 +1191,11 @@ afn_status build_impl(const Comm* comm, const double* X, int64_t n, int32_t d, c
   } wpf{wplan};
   auto early_plans = [&](RankSt& s) -> afn_status {
     const int q = (int)(&s - &h->rk[0]);
-    TRY(kmv_plan_make(s.Xs, n, s.own.size(), d, h->kn.kind, true, h->R, s.rank, st,
-                      [&](double** qq, size_t c) { return ralloc(s, qq, c, st); }, &s.plan, &s.kmv_part));
+    if (s.kmv_part)  // (made from the original points during FPS: to the handle's positions)
+      TRY(kmv_plan_remap(s.plan, s.kmv_part, s.perm, n, st));
+    else
+      TRY(kmv_plan_make(s.Xs, n, s.own.size(), d, h->kn.kind, true, h->R, s.rank, st,
+                        [&](double** qq, size_t c) { return ralloc(s, qq, c, st); }, &s.plan, &s.kmv_part));
     // (Z mode: one rank, AFN -- the FSAI products through Z = K21 M)
     wplan[q].keep = h->R == 1 && povl;  // (the apply through the tiles)
     if (!nys && k > 0 && N2 > 0 && s.hi > s.lo && kmv_get_mode() != 1)

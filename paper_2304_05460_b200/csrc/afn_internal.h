@@ -126,6 +126,10 @@ using WsGet = std::function<afn_status(double**, size_t)>;
 // `st` (the unit counts come back to the host).
 afn_status kmv_plan_make(const double* Xs, int64_t n, int64_t nrows, int d, int kind, bool sym_ok, int R, int rank,
                          cudaStream_t st, const WsGet& get, KmvPlan* out, double** ws);
+// A cutoff plan built over the points in another order (the build makes it
+// from the original X while FPS runs): its point indices become the handle's
+// positions, sidx <- iperm[sidx] with perm[position] = original index
+afn_status kmv_plan_remap(const KmvPlan& p, double* ws, const int64_t* perm, int64_t n, cudaStream_t st);
 // sym_ok: a full matvec may use the symmetric kernel (its row sums differ from
 // a row shard's by rounding; kernel_matvec_rows never uses it).  With R > 1
 // ranks the symmetric plan splits the pair units over the ranks

@@ -1385,6 +1385,30 @@ afn_status cut_plan_make(const double* Xs, int64_t n, int d, int R, int rank, cu
 }
 }  // namespace
 
+namespace {
+__global__ void kmv_iperm_kernel(const int64_t* __restrict__ perm, int64_t n, int* __restrict__ iperm) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < n) iperm[perm[p]] = (int)p;
+}
+__global__ void kmv_remap_kernel(int* __restrict__ sidx, int64_t n, const int* __restrict__ iperm) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) sidx[q] = iperm[sidx[q]];
+}
+}  // namespace
+
+afn_status kmv_plan_remap(const KmvPlan& p, double* ws, const int64_t* perm, int64_t n, cudaStream_t st) {
+  if (!p.cut) return AFN_OK;
+  int* iperm = nullptr;
+  TRY_STATUS(dalloc((void**)&iperm, sizeof(int) * n, st));
+  const unsigned nb = (unsigned)((n + 255) / 256);
+  kmv_iperm_kernel<<<nb, 256, 0, st>>>(perm, n, iperm);
+  AFN_LAUNCH_CHECK("kmv_iperm_kernel");
+  kmv_remap_kernel<<<nb, 256, 0, st>>>(reinterpret_cast<int*>(ws + p.o_sidx), n, iperm);
+  AFN_LAUNCH_CHECK("kmv_remap_kernel");
+  dfree(iperm, st);
+  return AFN_OK;
+}
+
 void kmv_set_mode(int mode) { g_kmv_mode = mode; }
 int kmv_get_mode() { return g_kmv_mode; }
 
