@@ -876,7 +876,6 @@ __global__ void __launch_bounds__(FT2, 4) fsai_factor_kernel(const int* __restri
   __shared__ __align__(16) double s_col[32];
   __shared__ int sJ[WP];
   __shared__ int s_off[WP + 1];
-  __shared__ int s_g[WP];
   __shared__ int s_pos[WP];
   __shared__ int64_t s_db[WP];
   __shared__ int s_bad;
@@ -907,7 +906,6 @@ __global__ void __launch_bounds__(FT2, 4) fsai_factor_kernel(const int* __restri
   for (int p = tid; p < wp; p += FT2) {
     const int a = sJ[p];
     const int g = grp[a], la = loc[a];
-    s_g[p] = g;
     s_pos[p] = g * GA + la;
     s_db[p] = Doff[g] + (int64_t)la * Ucount[g];
   }
@@ -923,7 +921,7 @@ __global__ void __launch_bounds__(FT2, 4) fsai_factor_kernel(const int* __restri
       while (p0 * (p0 + 1) / 2 > e0) --p0;
       while ((p0 + 1) * (p0 + 2) / 2 <= e0) ++p0;
       const int q0 = e0 - p0 * (p0 + 1) / 2;
-      int pp[B], bb[B];
+      int pp[B], bb[B], gg[B];
       unsigned hh[B];
       int2 hv[B];
       {
@@ -931,19 +929,22 @@ __global__ void __launch_bounds__(FT2, 4) fsai_factor_kernel(const int* __restri
 #pragma unroll
         for (int t = 0; t < B; ++t) {
           const bool ok = e0 + t < ne;
-          // the pair (J_p, J_q) lives in the group of its spatially later point
-          const int ph = !ok ? 0 : (s_pos[p] >= s_pos[q] ? p : q);
-          pp[t] = ph;
-          bb[t] = s_pos[!ok ? 0 : (ph == p ? q : p)];  // the hash key: the earlier point's position
+          // the pair (J_p, J_q) lives in the group of its spatially later
+          // point (position g GA + loc: the group is position / GA); the
+          // hash key is the earlier point's position
+          const int sp = s_pos[ok ? p : 0], sq = s_pos[ok ? q : 0];
+          pp[t] = !ok ? 0 : (sp >= sq ? p : q);
+          bb[t] = min(sp, sq);
+          gg[t] = max(sp, sq) / GA;
           hh[t] = ((unsigned)bb[t] * 2654435761u) & (HC - 1);
-          hv[t] = __ldg(&Htab[(int64_t)s_g[pp[t]] * HC + hh[t]]);
+          hv[t] = __ldg(&Htab[(int64_t)gg[t] * HC + hh[t]]);
           if (++q > p) { ++p; q = 0; }
         }
       }
       double gram[B];
 #pragma unroll
       for (int t = 0; t < B; ++t) {
-        const int2* H = Htab + (int64_t)s_g[pp[t]] * HC;
+        const int2* H = Htab + (int64_t)gg[t] * HC;
         int probe = 0;
         while (hv[t].x != bb[t] && probe < HC) {  // b is in U_g by construction
           hh[t] = (hh[t] + 1) & (HC - 1);
