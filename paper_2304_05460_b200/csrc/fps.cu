@@ -14,6 +14,7 @@
 // and are never re-picked; ties go to the lowest index.
 #include <cstdio>
 #include <cooperative_groups.h>
+#include <math_constants.h>
 
 #include <algorithm>
 #include <cmath>
@@ -262,6 +263,9 @@ __device__ __forceinline__ void warp_argmax_key(unsigned long long key, unsigned
 
 // ---------------------------------------------------------------------------
 namespace cg = cooperative_groups;
+#ifndef AFN_FPS_CULL
+#define AFN_FPS_CULL 1
+#endif
 
 // Cluster kernel (n up to 16 CTAs x NT x P points, no global-memory round
 // trips per step): after its CTA-level argmax, warp 0 of
@@ -304,10 +308,20 @@ __device__ __forceinline__ void mbar_wait_parity(unsigned a, unsigned ph) {
 // instead of registers -- 8 points per thread at 1024 threads, so one cluster
 // of 16 CTAs covers n = 131072 (C3) instead of 65536; the running minima stay
 // in registers.
-template <int DP, int P, int NT, bool SP = false>
+//
+// CULL (with SP): the slots hold the points in a spatial order perm (a warp's
+// 8 x 32 slots are 256 consecutive positions, its bounding box kept in shared
+// memory) and each slot keeps its point's index; a step skips a warp's
+// distance updates when the new landmark's squared distance to the warp's box
+// exceeds the warp's largest running minimum -- computed with the rounded
+// operations of d2_exact on the box gaps, it is a lower bound of every
+// point's d2, so no minimum could change.  Ties take the lowest index as in
+// the unpermuted kernel, so landmarks and fill distances are bit-identical.
+template <int DP, int P, int NT, bool SP = false, bool CULL = false>
 __global__ void __launch_bounds__(NT, 1)
 fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64_t seed,
-                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop) {
+                int64_t* __restrict__ idx_out, double* __restrict__ fill_out, const int64_t* __restrict__ kstop,
+                const int* __restrict__ perm) {
   extern __shared__ __align__(16) double s_pts[];
   constexpr int KI = DP + 2;          // slot: d2, index, point (DP), early-stop sample (KI)
   constexpr int S = (KI + 2) & ~1;    // even length (16-byte stores)
@@ -318,6 +332,7 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
   __shared__ __align__(16) double s_in[2][CLX][S];
   __shared__ __align__(8) unsigned long long s_bar[2];
   __shared__ long long s_kend;
+  __shared__ double s_box[CULL ? NT / 32 : 1][2 * DP];  // CULL: per warp lo[DP], hi[DP]
   cg::cluster_group cl = cg::this_cluster();
   const int crank = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
@@ -334,21 +349,54 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
   double pts[SP ? 1 : P][DP];
   double mind[P];
   double y[DP];
+  int oi[CULL ? P : 1];  // CULL: the slot's point index (-1: none)
   auto pt = [&](int sidx, int c) -> double& {
     return SP ? s_pts[(sidx * DP + c) * NT + tid] : pts[SP ? 0 : sidx][c];
   };
+  // the point index of slot s (CULL: through the spatial order)
+  auto slot_index = [&](int s) -> int64_t {
+    if (!CULL) return gtid + s * stride;
+    const int64_t j = ((int64_t)crank * NT + wid * 32) * P + s * 32 + lane;
+    return j < n ? (int64_t)perm[j] : n;
+  };
 #pragma unroll
   for (int c = 0; c < DP; ++c) y[c] = c < d ? X[seed * d + c] : 0.0;
+  double blo[DP], bhi[DP];
+#pragma unroll
+  for (int c = 0; c < DP; ++c) {
+    blo[c] = CUDART_INF;
+    bhi[c] = -CUDART_INF;
+  }
 #pragma unroll
   for (int s = 0; s < P; ++s) {
-    const int64_t i = gtid + s * stride;
+    const int64_t i = slot_index(s);
+    if (CULL) oi[CULL ? s : 0] = i < n ? (int)i : -1;
     double q[DP];
 #pragma unroll
     for (int c = 0; c < DP; ++c) {
       q[c] = (i < n && c < d) ? X[i * d + c] : 0.0;
       pt(s, c) = q[c];
+      if (CULL && i < n) {
+        blo[c] = fmin(blo[c], q[c]);
+        bhi[c] = fmax(bhi[c], q[c]);
+      }
     }
     mind[s] = i < n ? ((i == seed) ? -1.0 : d2_exact<DP>(q, y)) : -2.0;
+  }
+  if (CULL) {
+#pragma unroll
+    for (int c = 0; c < DP; ++c) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        blo[c] = fmin(blo[c], __shfl_xor_sync(0xffffffffu, blo[c], o));
+        bhi[c] = fmax(bhi[c], __shfl_xor_sync(0xffffffffu, bhi[c], o));
+      }
+      if (lane == 0) {
+        s_box[CULL ? wid : 0][c] = blo[c];
+        s_box[CULL ? wid : 0][DP + c] = bhi[c];
+      }
+    }
+    __syncwarp();
   }
   if (crank == 0 && tid == 0) idx_out[0] = seed;
   cl.sync();  // every CTA's mbarriers are initialised before the first push
@@ -365,8 +413,10 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
     unsigned bi = 0xffffffffu;
     int bs = 0;
 #pragma unroll
-    for (int s = 0; s < P; ++s)
-      if (mind[s] > bd) { bd = mind[s]; bi = (unsigned)(gtid + s * stride); bs = s; }
+    for (int s = 0; s < P; ++s) {
+      const unsigned is = CULL ? (unsigned)oi[CULL ? s : 0] : (unsigned)(gtid + s * stride);
+      if (mind[s] > bd || (CULL && mind[s] == bd && is < bi)) { bd = mind[s]; bi = is; bs = s; }
+    }
     unsigned long long wkey;
     unsigned widx;
     warp_argmax_key(fps_key(bd), bi, wkey, widx);
@@ -416,10 +466,23 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
     if (step >= kst) break;
 #pragma unroll
     for (int c = 0; c < DP; ++c) y[c] = s_in[par][src][2 + c];
+    if (CULL) {  // the new landmark's d2 to the warp's box against the warp's largest minimum
+      double g[DP];
+#pragma unroll
+      for (int c = 0; c < DP; ++c) {
+        const double lo = s_box[CULL ? wid : 0][c], hi = s_box[CULL ? wid : 0][DP + c];
+        g[c] = y[c] < lo ? __dsub_rn(lo, y[c]) : (y[c] > hi ? __dsub_rn(y[c], hi) : 0.0);
+      }
+      double bd2 = __dmul_rn(g[0], g[0]);
+#pragma unroll
+      for (int c = 1; c < DP; ++c) bd2 = __dadd_rn(bd2, __dmul_rn(g[c], g[c]));
+      const double wmax = wkey == 0ull ? -1.0 : __longlong_as_double((long long)(wkey - 1ull));
+      if (bd2 > wmax) continue;
+    }
 #pragma unroll
     for (int s = 0; s < P; ++s) {
-      const int64_t i = gtid + s * stride;
-      if (i < n) {
+      const int64_t i = CULL ? (int64_t)oi[CULL ? s : 0] : gtid + s * stride;
+      if (i >= 0 && i < n) {
         double q[DP];
 #pragma unroll
         for (int c = 0; c < DP; ++c) q[c] = pt(s, c);
@@ -431,10 +494,11 @@ fps_push_kernel(const double* __restrict__ X, int64_t n, int d, int64_t k, int64
   cl.sync();  // no CTA leaves while a push into it may be in flight
 }
 
-template <int DP, int P, int NT, bool SP = false>
+template <int DP, int P, int NT, bool SP = false, bool CULL = false>
 afn_status launch_fps_push(const double* X, int64_t n, int d, int64_t k, int64_t seed,
-                           int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st) {
-  auto kern = fps_push_kernel<DP, P, NT, SP>;
+                           int64_t* idx, double* fill, int CL, const int64_t* kstop, cudaStream_t st,
+                           const int* perm = nullptr) {
+  auto kern = fps_push_kernel<DP, P, NT, SP, CULL>;
   if (CL > 8) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   const size_t dyn = SP ? sizeof(double) * (size_t)P * DP * NT : 0;
   if (SP) AFN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
@@ -450,7 +514,7 @@ afn_status launch_fps_push(const double* X, int64_t n, int d, int64_t k, int64_t
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop));
+  AFN_CUDA(cudaLaunchKernelEx(&cfg, kern, X, n, d, k, seed, idx, fill, kstop, perm));
   AFN_LAUNCH_CHECK("fps_push_kernel");
   return AFN_OK;
 }
@@ -482,7 +546,17 @@ afn_status fps_dispatch_p(const double* X, int64_t n, int d, int64_t k, int64_t 
     // up to 2^17 points (d <= 3): 8 points per thread held in shared memory
     if (DP <= 3 && n > (int64_t)16 * CNT * 4 && n <= (int64_t)16 * 1024 * 8) {
       const int CL = (int)((n + 1024 * 8 - 1) / (1024 * 8));
+#if AFN_FPS_CULL
+      int* perm = nullptr;
+      afn_status s = dalloc((void**)&perm, sizeof(int) * (size_t)n, st);
+      if (s != AFN_OK) return s;
+      s = morton_order(X, n, d, perm, st);
+      if (s == AFN_OK) s = launch_fps_push<DP, 8, 1024, true, true>(X, n, d, k, seed, idx, fill, CL, kstop, st, perm);
+      dfree(perm, st);
+      return s;
+#else
       return launch_fps_push<DP, 8, 1024, true>(X, n, d, k, seed, idx, fill, CL, kstop, st);
+#endif
     }
   }
   // choose points per thread P and grid G (G = 1 needs no grid barrier)

@@ -91,6 +91,30 @@ def test_fps_bit_exact(n, d, k, seed):
     assert np.array_equal(fill.cpu().numpy(), fo)
 
 
+@pytest.mark.parametrize("case", ["lattice3", "dup3", "lattice2"])
+def test_fps_spatial_cull_ties(case):
+    """The shared-memory cluster FPS (65536 < n <= 131072, d <= 3) keeps its
+    points in a spatial order and skips warps whose box is out of reach: on
+    integer lattices (many exactly equal distances) and on duplicated points
+    the lowest-index tie rule of P:L101's argmax must still give the oracle's
+    landmarks and fill distances bit for bit."""
+    if case == "lattice3":
+        g = np.stack(np.meshgrid(np.arange(50), np.arange(50), np.arange(40), indexing="ij"), -1)
+        X = g.reshape(-1, 3).astype(np.float64)
+    elif case == "dup3":
+        Y, _ = gen_points(50000, 3, "cube", 11)
+        X = np.concatenate([Y, Y[::-1]])
+    else:
+        g = np.stack(np.meshgrid(np.arange(300), np.arange(250), indexing="ij"), -1)
+        X = g.reshape(-1, 2).astype(np.float64)
+    rng = np.random.default_rng(5)
+    X = X[rng.permutation(len(X))]
+    idx, fill = afn.afn_fps(T(X), 300, 3)
+    io, fo = O.fps(X, 300, 3)
+    assert np.array_equal(idx.cpu().numpy(), io)
+    assert np.array_equal(fill.cpu().numpy(), fo)
+
+
 def test_fps_duplicates_and_golden():
     X = np.repeat(np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 3.0]]), 3, axis=0)
     idx, fill = afn.afn_fps(T(X), 9, 0)
