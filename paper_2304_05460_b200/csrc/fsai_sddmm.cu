@@ -27,6 +27,7 @@
 // it (each dot has a fixed summation order, and W_a . W_b and W_b . W_a round
 // the same products), so the result is deterministic even though the cell
 // sort uses atomics.
+#include <type_traits>
 #include <math_constants.h>
 
 #include <algorithm>
@@ -595,7 +596,7 @@ constexpr int ZH = 16;
 constexpr int ZCAP = 1664;  // staged columns (16 x 1664 x 8 B = 208 KB); wider U' -> global loads
 constexpr int ZS = 8;
 template <bool STAGED>
-__global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
+__global__ void __launch_bounds__(STAGED ? 512 : 256, STAGED ? 1 : 2) group_zk_kernel(
     const int* __restrict__ sorder, int64_t N, const double* __restrict__ Zp, int64_t k,
     const int* __restrict__ tilerow, const int64_t* __restrict__ uoff, const int* __restrict__ ulistp,
     const int64_t* __restrict__ aoff, const double* __restrict__ Ap, const int* __restrict__ Ucount,
@@ -607,7 +608,11 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
   __shared__ int s_a[GA];
   __shared__ unsigned s_bits[256];   // k <= 8192 positions
   __shared__ int s_pre[257];         // prefix counts of s_bits
-  __shared__ int s_u[8][256];        // per warp: the piece's U_t as staged columns
+  // STAGED: 16 warps (one CTA per SM by its shared memory; with 8 warps the C5 kernel had
+  // 12.5 % occupancy and no eligible warp in 80 % of the cycles)
+  constexpr int NW = STAGED ? 16 : 8;
+  typedef typename std::conditional<STAGED, short, int>::type su_t;  // (k <= 8192)
+  __shared__ su_t s_u[NW][256];      // per warp: the piece's U_t as staged columns
   __shared__ long long s_pk[STAGED ? 1 : UCAP];  // !STAGED: (tile, piece) keys, sorted
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   load_exp2_tab(s_tab);
@@ -615,7 +620,7 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
   const int64_t g = STAGED ? (int64_t)(blockIdx.x >> 1) : (int64_t)(blockIdx.x / ZS);
   const int half = STAGED ? (int)(blockIdx.x & 1) : 0;
   const int pq = STAGED ? 0 : (int)(blockIdx.x % ZS);  // this CTA's share of the pieces
-  const int pstep = STAGED ? 8 : 8 * ZS;
+  const int pstep = STAGED ? NW : 8 * ZS;
   const int64_t m0 = g * GA + half * ZH;
   const int cnt = (int)max((int64_t)0, min((int64_t)RH, N - m0));
   if (tid < RH) s_a[tid] = tid < cnt ? sorder[m0 + tid] : -1;
@@ -625,7 +630,7 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
   if (cnt == 0) return;
   const int nu = Ucount[g], np = Pcount[g];
   // mark U' (every piece's tile list)
-  for (int p = wid; STAGED && p < np; p += 8) {
+  for (int p = wid; STAGED && p < np; p += NW) {
     const int tile = tilerow[Ulist[g * UCAP + Pc[g * UCAP + p].x]] >> 6;
     const int64_t us = uoff[tile], ue = uoff[tile + 1];
     for (int64_t m = us + lane; m < ue; m += 32) {
@@ -649,7 +654,7 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
   const int ncol = STAGED ? s_pre[nwords] : 0;
   const bool staged = STAGED && ncol <= ZCAP;
   if (staged) {  // Z rows at the marked columns (a warp per row, lanes over bitmap words)
-    for (int r = wid; r < ZH; r += 8) {
+    for (int r = wid; r < ZH; r += NW) {
       const int a = s_a[r];
       for (int w = lane; w < nwords; w += 32) {
         unsigned bits = s_bits[w];
@@ -731,9 +736,9 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) group_zk_kernel(
       for (int m = lane; m < cn; m += 32) {
         const int pos = U[c0 + m];
         const unsigned wb = s_bits[pos >> 5];
-        s_u[wid][m] = !staged ? pos
+        s_u[wid][m] = (su_t)(!staged ? pos
                               : ((wb >> (pos & 31)) & 1u) ? s_pre[pos >> 5] + __popc(wb & ((1u << (pos & 31)) - 1u))
-                                                          : -1;  // (a zero column for this group)
+                                                          : -1);  // (a zero column for this group)
       }
       __syncwarp();
       // fragments of step k4 + 4 are loaded while step k4's DMMAs run
@@ -1312,7 +1317,7 @@ afn_status fsai_sddmm_run(const double* X2, int64_t N, int d, Kern kn, double mu
     if (z->staged) {
       const int zb = (int)(sizeof(double) * ZH * ZCAP);
       AFN_CUDA(cudaFuncSetAttribute(group_zk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, zb));
-      group_zk_kernel<true><<<(unsigned)(2 * G), 256, zb, st>>>(sorder, N, z->Zp, k, z->tilerow, z->uoff, z->ulistp,
+      group_zk_kernel<true><<<(unsigned)(2 * G), 512, zb, st>>>(sorder, N, z->Zp, k, z->tilerow, z->uoff, z->ulistp,
                                                                 z->aoff, z->Ap, Ucount, Ulist, Doff, Pc, Pcount, D, X2,
                                                                 d, kf, mu);
     } else {
